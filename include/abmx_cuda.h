@@ -1,0 +1,174 @@
+/*
+ * abmx_cuda.h — C-ABI of the B200-native (sm_100a) engine for the Abmax hot path
+ * (arXiv 2508.16508; reference C++ implementation "abmx" under /root/reference/proj).
+ *
+ * Plain pointers and sizes only. Three layers, each citing the reference interface it
+ * replaces:
+ *
+ *  1. KernelTable drop-in (host pointers, synchronous, bit-identical to the scalar
+ *     table) — replaces abmx::simd::KernelTable, include/abmx/simd/kernels.hpp:15-43.
+ *     abmx_cuda_kernel_table() returns a struct with the SAME layout as KernelTable,
+ *     so the reference's dispatch (src/simd/dispatch.cpp:16-58) can hand it out as a
+ *     third backend; see INTEGRATION.md.
+ *  2. The same entries on device pointers + a cudaStream_t (passed as void*).
+ *  3. Fused model engines: the predation step (PredationModel, include/abmx/models/
+ *     predation.hpp:76-107, src/models/predation.cpp:167-263) for one model or a batch
+ *     of replicas, and the ensemble runner (run_batch, include/abmx/batch.hpp:48-54).
+ *
+ * Errors: int-returning entries give ABMX_OK or one of the codes below, mirroring the
+ * reference exception taxonomy (include/abmx/errors.hpp:8-40); abmx_cuda_last_error()
+ * holds the message (thread-local). The void KernelTable entries cannot report errors
+ * (the reference's never fail); on a CUDA failure they print and abort().
+ */
+#ifndef ABMX_CUDA_H
+#define ABMX_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ABMX_OK 0
+#define ABMX_E_DOMAIN 1   /* DomainError   errors.hpp:26-28 */
+#define ABMX_E_CAPACITY 2 /* CapacityError errors.hpp:21-23 */
+#define ABMX_E_SCHEMA 3   /* SchemaError   errors.hpp:16-18 */
+#define ABMX_E_BATCH 4    /* BatchError    errors.hpp:36-38 */
+#define ABMX_E_CUDA 5     /* device / driver failure (no reference counterpart) */
+#define ABMX_E_ARG 6      /* null handle or pointer */
+
+const char* abmx_cuda_last_error(void);
+const char* abmx_cuda_version(void);
+/* number of kernels this library has launched in this process (all threads) */
+uint64_t abmx_cuda_launch_count(void);
+
+/* ======================================================================= 1. KernelTable
+ * Host pointers. Semantics of src/simd/kernels_scalar.cpp:7-54; any nonzero mask byte
+ * is true; `out` may alias `a` or `b` in the blends (lifecycle.cpp:105-111). */
+void abmx_cuda_rank_scan(const uint8_t* mask, int32_t* ranks, size_t n);
+int64_t abmx_cuda_count_true(const uint8_t* mask, size_t n);
+void abmx_cuda_compact_indices(const uint8_t* mask, int32_t* out, size_t n);
+void abmx_cuda_match_first_equal(const int32_t* ra, size_t n, const int32_t* rb, size_t m,
+                                 int32_t* row_out);
+void abmx_cuda_blend_i64(const uint8_t* mask, const int64_t* a, const int64_t* b, int64_t* out,
+                         size_t n);
+void abmx_cuda_blend_f64(const uint8_t* mask, const double* a, const double* b, double* out,
+                         size_t n);
+void abmx_cuda_blend_u8(const uint8_t* mask, const uint8_t* a, const uint8_t* b, uint8_t* out,
+                        size_t n);
+
+/* Layout-identical to abmx::simd::KernelTable (kernels.hpp:15-43). */
+typedef struct abmx_kernel_table {
+    const char* name; /* "cuda" */
+    void (*rank_scan)(const uint8_t*, int32_t*, size_t);
+    int64_t (*count_true)(const uint8_t*, size_t);
+    void (*compact_indices)(const uint8_t*, int32_t*, size_t);
+    void (*match_first_equal)(const int32_t*, size_t, const int32_t*, size_t, int32_t*);
+    void (*blend_i64)(const uint8_t*, const int64_t*, const int64_t*, int64_t*, size_t);
+    void (*blend_f64)(const uint8_t*, const double*, const double*, double*, size_t);
+    void (*blend_u8)(const uint8_t*, const uint8_t*, const uint8_t*, uint8_t*, size_t);
+} abmx_kernel_table;
+
+const abmx_kernel_table* abmx_cuda_kernel_table(void);
+
+/* ======================================================================= 2. device variants
+ * All pointers are device pointers; `stream` is a cudaStream_t (NULL = legacy default).
+ * Stream-ordered and asynchronous; temporaries come from the stream-ordered pool. */
+int abmx_cuda_rank_scan_async(const uint8_t* d_mask, int32_t* d_ranks, size_t n, void* stream);
+int abmx_cuda_count_true_async(const uint8_t* d_mask, size_t n, int64_t* d_count, void* stream);
+int abmx_cuda_compact_indices_async(const uint8_t* d_mask, int32_t* d_out, size_t n,
+                                    int64_t* d_count, void* stream);
+int abmx_cuda_match_first_equal_async(const int32_t* d_ra, size_t n, const int32_t* d_rb, size_t m,
+                                      int32_t* d_row_out, void* stream);
+int abmx_cuda_blend_i64_async(const uint8_t* d_mask, const int64_t* d_a, const int64_t* d_b,
+                              int64_t* d_out, size_t n, void* stream);
+int abmx_cuda_blend_f64_async(const uint8_t* d_mask, const double* d_a, const double* d_b,
+                              double* d_out, size_t n, void* stream);
+int abmx_cuda_blend_u8_async(const uint8_t* d_mask, const uint8_t* d_a, const uint8_t* d_b,
+                             uint8_t* d_out, size_t n, void* stream);
+
+/* ======================================================================= 3. predation
+ * Field order identical to abmx::models::PredationConfig (predation.hpp:13-27). */
+typedef struct abmx_predation_config {
+    int32_t width, height, n_sheep0, n_wolves0, sheep_capacity, wolf_capacity;
+    double energy_gain_sheep, energy_gain_wolf, metabolism;
+    double reproduce_prob_sheep, reproduce_prob_wolf, reproduce_energy_frac;
+    int64_t regrow_delay;
+} abmx_predation_config;
+
+/* SpeciesEvents / PredationEvents (predation.hpp:41-57) without the birth-pair vector
+ * (see abmx_predation_birth_pairs). */
+typedef struct abmx_species_events {
+    int64_t metabolized, deaths, births, births_dropped;
+    double energy_removed_deaths, energy_dropped_births;
+} abmx_species_events;
+
+typedef struct abmx_predation_events {
+    int64_t grass_eaten, sheep_eaten_by_wolves;
+    abmx_species_events sheep, wolves;
+} abmx_predation_events;
+
+typedef struct abmx_predation abmx_predation; /* opaque: R replicas resident in HBM */
+
+/* init_predation (predation.cpp:154-165) for `replicas` models with the given replica
+ * seeds (RngState keys). Errors: CAPACITY (n0 > capacity), DOMAIN (regrow_delay > 254,
+ * width/height < 1, grid too large). */
+int abmx_predation_create(const abmx_predation_config* cfg, const uint64_t* seeds,
+                          int32_t replicas, abmx_predation** out);
+int abmx_predation_destroy(abmx_predation* h);
+/* PredationModel::step(t) for every replica (predation.cpp:277-279). Asynchronous. */
+int abmx_predation_step(abmx_predation* h, int64_t t);
+/* steps t0 .. t0+steps-1; metrics_out (nullable, host) receives [replicas][steps][4]
+ * rows n_sheep, n_wolves, n_grass, births_dropped (predation.cpp:281-287). Synchronous
+ * iff metrics_out != NULL. */
+int abmx_predation_run(abmx_predation* h, int64_t t0, int64_t steps, double* metrics_out);
+int abmx_predation_sync(abmx_predation* h);
+/* collect_metrics of the last step: [replicas][4] */
+int abmx_predation_metrics(abmx_predation* h, int64_t* out);
+/* events of the last step: [replicas] */
+int abmx_predation_last_events(abmx_predation* h, abmx_predation_events* out);
+/* (parent slot, child slot) pairs of the last step's births, ascending child slot */
+int32_t abmx_predation_birth_pairs(abmx_predation* h, int32_t replica, int32_t species,
+                                   int32_t* parent, int32_t* child, int32_t cap);
+/* AgentSet export/import in the reference layout (agent_set.hpp:15-77). species 0 = sheep,
+ * 1 = wolves. Import requires num_active == popcount(active) and x, y in range. */
+int abmx_predation_export(abmx_predation* h, int32_t replica, int32_t species, uint8_t* active,
+                          int64_t* ids, int64_t* types, int64_t* ages, int64_t* x, int64_t* y,
+                          double* energy, int32_t* num_active, int64_t* next_id);
+int abmx_predation_import(abmx_predation* h, int32_t replica, int32_t species,
+                          const uint8_t* active, const int64_t* ids, const int64_t* ages,
+                          const int64_t* x, const int64_t* y, const double* energy,
+                          int32_t num_active, int64_t next_id);
+int abmx_predation_export_world(abmx_predation* h, int32_t replica, uint8_t* grass_ready,
+                                int64_t* regrow);
+int abmx_predation_import_world(abmx_predation* h, int32_t replica, const uint8_t* grass_ready,
+                                const int64_t* regrow);
+/* the CUDA stream all of h's work is ordered on (cudaStream_t) */
+void* abmx_predation_stream(abmx_predation* h);
+/* Per-kernel timing: when enabled, steps launch kernel-by-kernel (no CUDA graph) with CUDA
+ * events around each kernel; abmx_predation_kernel_times returns the accumulated device
+ * milliseconds and launch counts per kernel (names via abmx_predation_kernel_name). */
+int abmx_predation_set_timing(abmx_predation* h, int enabled);
+int32_t abmx_predation_kernel_count(void);
+const char* abmx_predation_kernel_name(int32_t k);
+int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches);
+/* device-resident bytes of h (state + scratch) */
+int64_t abmx_predation_device_bytes(abmx_predation* h);
+
+/* ======================================================================= ensemble
+ * run_batch (batch.cpp:21-101) for replicas [replica_begin, replica_begin+count) of
+ * master seed `master` (seeds master.split(2).split(r), batch.cpp:12-19), t = 1..steps.
+ * metrics_out: host [count][steps][4] in run_batch row order. `path`: 0 auto, 1 the
+ * SMEM-resident CTA-per-replica kernel, 2 the batched HBM engine. kernel_ms (nullable)
+ * receives the device time of the simulation kernels. */
+int abmx_ensemble_run(const abmx_predation_config* cfg, uint64_t master, int32_t replica_begin,
+                      int32_t count, int64_t steps, int32_t path, double* metrics_out,
+                      double* kernel_ms);
+/* 1 if the SMEM-resident path supports cfg */
+int abmx_ensemble_smem_fits(const abmx_predation_config* cfg);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABMX_CUDA_H */

@@ -1,0 +1,458 @@
+/*
+ * abmx_oracle.c — TEST INFRASTRUCTURE ONLY. Plain-C restatement of the reference's
+ * CPU algorithm for the predation hot path; see abmx_oracle.h for the pinning story.
+ * Every function cites the reference file:line (under /root/reference/proj) it follows.
+ * Build: make -C oracle (gcc, default x86-64 target: no FMA contraction, matching the
+ * reference's g++ build, which is what keeps frac*E bit-identical).
+ */
+#include "abmx_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ------------------------------------------------------------------ RNG */
+/* src/rng.cpp:9-10 */
+#define K_DRAW 0x9E3779B97F4A7C15ULL
+#define K_SPLIT 0xC2B2AE3D27D4EB4FULL
+
+/* splitmix64 finalizer, src/rng.cpp:12-16 */
+uint64_t orc_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+/* src/rng.cpp:18-20 */
+uint64_t orc_split(uint64_t key, uint64_t i) { return orc_mix64(key + K_SPLIT * (i + 1)); }
+/* src/rng.cpp:22-24 */
+uint64_t orc_draw(uint64_t key, uint64_t c) { return orc_mix64(key + K_DRAW * (c + 1)); }
+/* src/rng.cpp:26-28 */
+double orc_uniform_double(uint64_t key, uint64_t c) {
+    return (double)(orc_draw(key, c) >> 11) * 0x1.0p-53;
+}
+/* src/rng.cpp:30-36 (lo < hi is the caller's contract here) */
+int64_t orc_uniform_int(uint64_t key, uint64_t c, int64_t lo, int64_t hi) {
+    const uint64_t span = (uint64_t)(hi - lo);
+    const unsigned __int128 wide = (unsigned __int128)orc_draw(key, c) * span;
+    return lo + (int64_t)(uint64_t)(wide >> 64);
+}
+/* src/rng.cpp:38-40 */
+int orc_bernoulli(uint64_t key, uint64_t c, double p) { return orc_uniform_double(key, c) < p; }
+/* src/batch.cpp:12-19: master.split(BatchReplica=2).split(r) */
+uint64_t orc_replica_seed(uint64_t master, int64_t r) {
+    return orc_split(orc_split(master, 2), (uint64_t)r);
+}
+
+/* ------------------------------------------------------------------ kernel table */
+/* src/simd/kernels_scalar.cpp:7-13 */
+void orc_rank_scan(const uint8_t* mask, int32_t* ranks, size_t n) {
+    int32_t run = 0;
+    for (size_t i = 0; i < n; ++i) {
+        run += mask[i] ? 1 : 0;
+        ranks[i] = mask[i] ? run : 0;
+    }
+}
+/* src/simd/kernels_scalar.cpp:15-20 */
+int64_t orc_count_true(const uint8_t* mask, size_t n) {
+    int64_t c = 0;
+    for (size_t i = 0; i < n; ++i) c += mask[i] ? 1 : 0;
+    return c;
+}
+/* src/simd/kernels_scalar.cpp:22-31 */
+void orc_compact_indices(const uint8_t* mask, int32_t* out, size_t n) {
+    size_t f = 0;
+    for (size_t i = 0; i < n; ++i)
+        if (mask[i]) out[f++] = (int32_t)i;
+    for (size_t i = 0; i < n; ++i)
+        if (!mask[i]) out[f++] = (int32_t)i;
+}
+/* src/simd/kernels_scalar.cpp:33-48 */
+void orc_match_first_equal(const int32_t* ra, size_t n, const int32_t* rb, size_t m,
+                           int32_t* row_out) {
+    for (size_t i = 0; i < n; ++i) {
+        row_out[i] = -1;
+        if (ra[i] == 0) continue;
+        for (size_t j = 0; j < m; ++j)
+            if (rb[j] == ra[i]) {
+                row_out[i] = (int32_t)j;
+                break;
+            }
+    }
+}
+/* src/simd/kernels_scalar.cpp:50-54 (bitwise select) */
+void orc_blend_i64(const uint8_t* mask, const int64_t* a, const int64_t* b, int64_t* out,
+                   size_t n) {
+    for (size_t i = 0; i < n; ++i) out[i] = mask[i] ? a[i] : b[i];
+}
+void orc_blend_f64(const uint8_t* mask, const double* a, const double* b, double* out, size_t n) {
+    for (size_t i = 0; i < n; ++i) memcpy(&out[i], mask[i] ? &a[i] : &b[i], 8);
+}
+void orc_blend_u8(const uint8_t* mask, const uint8_t* a, const uint8_t* b, uint8_t* out,
+                  size_t n) {
+    for (size_t i = 0; i < n; ++i) out[i] = mask[i] ? a[i] : b[i];
+}
+
+/* tests/support/oracle.cpp:11-31 */
+int32_t orc_pair(const uint8_t* target, int32_t n, const uint8_t* valid, int32_t m,
+                 int32_t* slots, int32_t* rows) {
+    int32_t p = 0, q = 0;
+    for (int32_t i = 0; i < n; ++i)
+        if (target[i]) slots[p++] = i;
+    for (int32_t j = 0; j < m; ++j)
+        if (valid[j]) rows[q++] = j;
+    return p < q ? p : q;
+}
+
+/* kernels.cpp:52-73: std::stable_sort of the identity permutation by key; here a
+ * bottom-up merge sort (also stable). */
+int orc_sort_perm(const double* key, const uint8_t* active, int32_t n, int descending,
+                  int32_t* perm) {
+    for (int32_t i = 0; i < n; ++i)
+        if (active[i] && !isfinite(key[i])) return 2;
+    int32_t* tmp = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    for (int32_t i = 0; i < n; ++i) perm[i] = i;
+    int32_t *src = perm, *dst = tmp;
+    for (int32_t w = 1; w < n; w *= 2) {
+        for (int32_t lo = 0; lo < n; lo += 2 * w) {
+            int32_t mid = lo + w < n ? lo + w : n, hi = lo + 2 * w < n ? lo + 2 * w : n;
+            int32_t a = lo, b = mid, k = lo;
+            while (a < mid && b < hi) {
+                const double ka = key[src[a]], kb = key[src[b]];
+                /* take b first only when strictly before a (stability) */
+                const int b_first = descending ? (kb > ka) : (kb < ka);
+                dst[k++] = b_first ? src[b++] : src[a++];
+            }
+            while (a < mid) dst[k++] = src[a++];
+            while (b < hi) dst[k++] = src[b++];
+        }
+        int32_t* t = src;
+        src = dst;
+        dst = t;
+    }
+    if (src != perm) memcpy(perm, src, sizeof(int32_t) * (size_t)n);
+    free(tmp);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ predation */
+/* src/models/predation.cpp:13-15 */
+static const int kNeigh[8][2] = {{-1, -1}, {-1, 0}, {-1, 1}, {0, -1},
+                                 {0, 1},   {1, -1}, {1, 0},  {1, 1}};
+
+static void species_alloc(orc_species* s, int32_t cap) {
+    size_t n = (size_t)(cap > 0 ? cap : 1);
+    s->capacity = cap;
+    s->active = (uint8_t*)calloc(n, 1);
+    s->ids = (int64_t*)calloc(n, 8);
+    s->types = (int64_t*)calloc(n, 8);
+    s->ages = (int64_t*)calloc(n, 8);
+    s->x = (int64_t*)calloc(n, 8);
+    s->y = (int64_t*)calloc(n, 8);
+    s->energy = (double*)calloc(n, 8);
+}
+
+static void species_free(orc_species* s) {
+    free(s->active);
+    free(s->ids);
+    free(s->types);
+    free(s->ages);
+    free(s->x);
+    free(s->y);
+    free(s->energy);
+}
+
+/* agent_set.cpp:45-58: zero state, id, age, active; type kept */
+static void reset_slot(orc_species* s, int32_t i) {
+    s->active[i] = 0;
+    s->ids[i] = 0;
+    s->ages[i] = 0;
+    s->x[i] = 0;
+    s->y[i] = 0;
+    s->energy[i] = 0.0;
+}
+
+/* predation.cpp:22-33 + lifecycle.cpp:11-85 (create_agents; field ordinals x=0,y=1,energy=2,
+ * draws for ALL slots from seed.split(CreateField=1).split(ordinal), then reset slots>=n0) */
+static void create_species(orc_species* s, int32_t cap, int32_t n0, int32_t W, int32_t H,
+                           double gain, uint64_t seed, int64_t type) {
+    species_alloc(s, cap);
+    const uint64_t root = orc_split(seed, 1);
+    const uint64_t sx = orc_split(root, 0), sy = orc_split(root, 1), se = orc_split(root, 2);
+    const int64_t ehi = 2 * (int64_t)gain + 1;
+    for (int32_t i = 0; i < cap; ++i) {
+        s->x[i] = orc_uniform_int(sx, (uint64_t)i, 0, W);
+        s->y[i] = orc_uniform_int(sy, (uint64_t)i, 0, H);
+        s->energy[i] = (double)orc_uniform_int(se, (uint64_t)i, 1, ehi);
+        s->types[i] = type;
+    }
+    for (int32_t i = 0; i < n0; ++i) {
+        s->active[i] = 1;
+        s->ids[i] = i;
+    }
+    for (int32_t i = n0; i < cap; ++i) reset_slot(s, i);
+    s->num_active = n0;
+    s->next_id = n0;
+}
+
+/* predation.cpp:154-165 */
+orc_pred* orc_pred_create(const orc_pred_config* cfg, uint64_t seed) {
+    if (cfg->n_sheep0 > cfg->sheep_capacity || cfg->n_wolves0 > cfg->wolf_capacity) return NULL;
+    orc_pred* p = (orc_pred*)calloc(1, sizeof(orc_pred));
+    p->cfg = *cfg;
+    p->seed = seed;
+    const size_t cells = (size_t)cfg->width * (size_t)cfg->height;
+    p->ready = (uint8_t*)malloc(cells ? cells : 1);
+    memset(p->ready, 1, cells);
+    p->regrow = (int64_t*)calloc(cells ? cells : 1, 8);
+    create_species(&p->sp[0], cfg->sheep_capacity, cfg->n_sheep0, cfg->width, cfg->height,
+                   cfg->energy_gain_sheep, orc_split(seed, 20), 0);
+    create_species(&p->sp[1], cfg->wolf_capacity, cfg->n_wolves0, cfg->width, cfg->height,
+                   cfg->energy_gain_wolf, orc_split(seed, 21), 1);
+    return p;
+}
+
+void orc_pred_free(orc_pred* p) {
+    if (!p) return;
+    species_free(&p->sp[0]);
+    species_free(&p->sp[1]);
+    free(p->ready);
+    free(p->regrow);
+    free(p);
+}
+
+/* predation.cpp:35-49 + lifecycle.cpp:87-122 (step_agents: transition, blend placeholders
+ * to 0, age++ on active) */
+static void move_species(orc_species* s, int32_t W, int32_t H, uint64_t stream) {
+    for (int32_t i = 0; i < s->capacity; ++i) {
+        if (s->active[i]) {
+            const int64_t u = orc_uniform_int(stream, (uint64_t)i, 0, 8);
+            s->x[i] = (s->x[i] + kNeigh[u][0] + W) % W;
+            s->y[i] = (s->y[i] + kNeigh[u][1] + H) % H;
+            s->ages[i] += 1;
+        } else {
+            s->x[i] = 0;
+            s->y[i] = 0;
+            s->energy[i] = 0.0;
+        }
+    }
+}
+
+/* lifecycle.cpp:124-142 */
+static void remove_masked(orc_species* s, const uint8_t* kill) {
+    int32_t killed = 0;
+    for (int32_t i = 0; i < s->capacity; ++i)
+        if (s->active[i] && kill[i]) {
+            reset_slot(s, i);
+            ++killed;
+        }
+    s->num_active -= killed;
+}
+
+/* predation.cpp:76-137 + lifecycle.cpp:144-195 (spawn via rank-match of !active vs valid) */
+static void reproduce(orc_species* s, const orc_pred_config* cfg, double prob, uint64_t stream,
+                      int64_t type, orc_species_events* ev) {
+    const int32_t n = s->capacity;
+    uint8_t* valid = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
+    int64_t* cx = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    int64_t* cy = (int64_t*)malloc(sizeof(int64_t) * (size_t)(n > 0 ? n : 1));
+    double* ce = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    for (int32_t i = 0; i < n; ++i) {
+        if (!s->active[i] || s->energy[i] <= cfg->metabolism) continue;
+        if (!orc_bernoulli(stream, (uint64_t)i, prob)) continue;
+        /* quantize_energy, predation.cpp:141-143 */
+        const double child = floor((cfg->reproduce_energy_frac * s->energy[i]) / 0x1p-20) * 0x1p-20;
+        s->energy[i] -= child;
+        cx[i] = s->x[i];
+        cy[i] = s->y[i];
+        ce[i] = child;
+        valid[i] = 1;
+    }
+    /* k-th free slot (ascending) <- k-th valid row (ascending) */
+    int32_t q = 0;
+    for (int32_t i = 0; i < n; ++i) q += valid[i] ? 1 : 0;
+    int32_t row = 0, spawned = 0;
+    for (int32_t slot = 0; slot < n && spawned < q; ++slot) {
+        if (s->active[slot]) continue;
+        while (!valid[row]) ++row;
+        s->x[slot] = cx[row];
+        s->y[slot] = cy[row];
+        s->energy[slot] = ce[row];
+        s->active[slot] = 1;
+        s->ids[slot] = s->next_id++;
+        s->ages[slot] = 0;
+        s->types[slot] = type;
+        ++row;
+        ++spawned;
+    }
+    s->num_active += spawned;
+    ev->births += spawned;
+    ev->births_dropped += q - spawned;
+    /* predation.cpp:121-135: energy of the dropped (highest-slot) rows */
+    for (; row < n; ++row)
+        if (valid[row]) ev->energy_dropped_births += ce[row];
+    free(valid);
+    free(cx);
+    free(cy);
+    free(ce);
+}
+
+/* predation.cpp:167-263 */
+void orc_pred_step(orc_pred* p, int64_t t, orc_pred_events* ev_out) {
+    const orc_pred_config* cfg = &p->cfg;
+    orc_pred_events ev;
+    memset(&ev, 0, sizeof ev);
+    const int32_t W = cfg->width, H = cfg->height;
+    orc_species* sh = &p->sp[0];
+    orc_species* wo = &p->sp[1];
+    const uint64_t ut = (uint64_t)t;
+
+    /* 1. move (PredMove = 3) */
+    const uint64_t move_root = orc_split(orc_split(p->seed, 3), ut);
+    move_species(sh, W, H, orc_split(move_root, 0));
+    move_species(wo, W, H, orc_split(move_root, 1));
+
+    /* 2a. graze: ascending sheep slots, first on a ready cell eats (predation.cpp:178-195) */
+    for (int32_t i = 0; i < sh->capacity; ++i) {
+        if (!sh->active[i]) continue;
+        const size_t c = (size_t)sh->y[i] * (size_t)W + (size_t)sh->x[i];
+        if (p->ready[c]) {
+            p->ready[c] = 0;
+            p->regrow[c] = cfg->regrow_delay;
+            sh->energy[i] += cfg->energy_gain_sheep;
+            ++ev.grass_eaten;
+        }
+    }
+
+    /* 2b. predation: k-th wolf (slot order) in a cell takes the k-th sheep (predation.cpp:197-239) */
+    {
+        const size_t cells = (size_t)W * (size_t)H;
+        int32_t* head = (int32_t*)malloc(sizeof(int32_t) * (cells ? cells : 1));
+        int32_t* tail = (int32_t*)malloc(sizeof(int32_t) * (cells ? cells : 1));
+        int32_t* next = (int32_t*)malloc(sizeof(int32_t) * (size_t)(sh->capacity > 0 ? sh->capacity : 1));
+        uint8_t* eaten = (uint8_t*)calloc((size_t)(sh->capacity > 0 ? sh->capacity : 1), 1);
+        for (size_t c = 0; c < cells; ++c) head[c] = tail[c] = -1;
+        for (int32_t i = 0; i < sh->capacity; ++i) next[i] = -1;
+        for (int32_t i = 0; i < sh->capacity; ++i) {
+            if (!sh->active[i]) continue;
+            const size_t c = (size_t)sh->y[i] * (size_t)W + (size_t)sh->x[i];
+            if (head[c] < 0)
+                head[c] = i;
+            else
+                next[tail[c]] = i;
+            tail[c] = i;
+        }
+        for (int32_t i = 0; i < wo->capacity; ++i) {
+            if (!wo->active[i]) continue;
+            const size_t c = (size_t)wo->y[i] * (size_t)W + (size_t)wo->x[i];
+            const int32_t v = head[c];
+            if (v < 0) continue;
+            head[c] = next[v];
+            eaten[v] = 1;
+            ev.sheep.energy_removed_deaths += sh->energy[v];
+            ++ev.sheep.deaths;
+            ++ev.sheep_eaten_by_wolves;
+            wo->energy[i] += cfg->energy_gain_wolf;
+        }
+        remove_masked(sh, eaten);
+        free(head);
+        free(tail);
+        free(next);
+        free(eaten);
+    }
+
+    /* 3+4. metabolize, then starve (predation.cpp:51-74, 241-245) */
+    orc_species* sp[2] = {sh, wo};
+    orc_species_events* se[2] = {&ev.sheep, &ev.wolves};
+    for (int k = 0; k < 2; ++k)
+        for (int32_t i = 0; i < sp[k]->capacity; ++i)
+            if (sp[k]->active[i]) {
+                sp[k]->energy[i] -= cfg->metabolism;
+                ++se[k]->metabolized;
+            }
+    for (int k = 0; k < 2; ++k) {
+        uint8_t* kill = (uint8_t*)calloc((size_t)(sp[k]->capacity > 0 ? sp[k]->capacity : 1), 1);
+        for (int32_t i = 0; i < sp[k]->capacity; ++i)
+            if (sp[k]->active[i] && sp[k]->energy[i] <= 0.0) {
+                kill[i] = 1;
+                se[k]->energy_removed_deaths += sp[k]->energy[i];
+                ++se[k]->deaths;
+            }
+        remove_masked(sp[k], kill);
+        free(kill);
+    }
+
+    /* 5. reproduce (PredReproduce = 4) */
+    const uint64_t rep_root = orc_split(orc_split(p->seed, 4), ut);
+    reproduce(sh, cfg, cfg->reproduce_prob_sheep, orc_split(rep_root, 0), 0, &ev.sheep);
+    reproduce(wo, cfg, cfg->reproduce_prob_wolf, orc_split(rep_root, 1), 1, &ev.wolves);
+
+    /* 6. regrow (predation.cpp:252-258) */
+    const size_t cells = (size_t)W * (size_t)H;
+    for (size_t c = 0; c < cells; ++c)
+        if (p->regrow[c] > 0 && --p->regrow[c] == 0) p->ready[c] = 1;
+
+    p->ev = ev;
+    if (ev_out) *ev_out = ev;
+}
+
+/* predation.cpp:265-272, 281-287 */
+void orc_pred_metrics(const orc_pred* p, int64_t* out4) {
+    out4[0] = p->sp[0].num_active;
+    out4[1] = p->sp[1].num_active;
+    out4[2] = orc_count_true(p->ready, (size_t)p->cfg.width * (size_t)p->cfg.height);
+    out4[3] = p->ev.sheep.births_dropped + p->ev.wolves.births_dropped;
+}
+
+static uint64_t fnv(uint64_t h, const void* d, size_t n) {
+    const uint8_t* b = (const uint8_t*)d;
+    for (size_t i = 0; i < n; ++i) {
+        h ^= b[i];
+        h *= 0x100000001b3ULL;
+    }
+    return h;
+}
+
+uint64_t orc_pred_hash(const orc_pred* p, int with_world) {
+    uint64_t h = 0xcbf29ce484222325ULL;
+    for (int k = 0; k < 2; ++k) {
+        const orc_species* s = &p->sp[k];
+        const size_t n = (size_t)s->capacity;
+        h = fnv(h, s->active, n);
+        h = fnv(h, s->ids, n * 8);
+        h = fnv(h, s->ages, n * 8);
+        h = fnv(h, s->x, n * 8);
+        h = fnv(h, s->y, n * 8);
+        h = fnv(h, s->energy, n * 8);
+    }
+    if (with_world) {
+        const size_t cells = (size_t)p->cfg.width * (size_t)p->cfg.height;
+        h = fnv(h, p->ready, cells);
+        h = fnv(h, p->regrow, cells * 8);
+    }
+    return h;
+}
+
+orc_species* orc_pred_species(orc_pred* p, int species) { return &p->sp[species ? 1 : 0]; }
+uint8_t* orc_pred_ready(orc_pred* p) { return p->ready; }
+int64_t* orc_pred_regrow(orc_pred* p) { return p->regrow; }
+
+/* batch.cpp:21-101 with one thread; rows in (replica, step) order, t = 1..steps */
+int orc_run_batch(const orc_pred_config* cfg, uint64_t master, int32_t replicas, int64_t steps,
+                  double* metrics_out) {
+    for (int32_t r = 0; r < replicas; ++r) {
+        orc_pred* p = orc_pred_create(cfg, orc_replica_seed(master, r));
+        if (!p) return 1;
+        for (int64_t t = 1; t <= steps; ++t) {
+            orc_pred_step(p, t, NULL);
+            int64_t m[4];
+            orc_pred_metrics(p, m);
+            double* o = metrics_out + ((size_t)r * (size_t)steps + (size_t)(t - 1)) * 4;
+            for (int j = 0; j < 4; ++j) o[j] = (double)m[j];
+        }
+        orc_pred_free(p);
+    }
+    return 0;
+}
+
+/* FNV-1a-64 helper for state hashes (test bookkeeping, not a reference algorithm) */
+uint64_t orc_fnv1a(uint64_t h, const void* data, size_t n) { return fnv(h, data, n); }

@@ -1,0 +1,435 @@
+"""pyoracle — TEST INFRASTRUCTURE ONLY: ctypes access to the two CPU checkers.
+
+* ``Oracle``    — oracle/liboracle.so, the plain-C restatement (abmx_oracle.c).
+* ``Reference`` — oracle/_ref/libabmx_ref.so, the UNMODIFIED reference library compiled
+                  from /root/reference/proj/src by oracle/Makefile (+ ref_driver.cpp shim).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU legs may import this module.
+Both classes expose the same predation interface so a test can run either as the checker.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libabmx_ref.so")
+
+u8p = C.POINTER(C.c_uint8)
+i32p = C.POINTER(C.c_int32)
+i64p = C.POINTER(C.c_int64)
+f64p = C.POINTER(C.c_double)
+
+
+class Cfg(C.Structure):
+    _fields_ = [(n, C.c_int32) for n in ("width", "height", "n_sheep0", "n_wolves0",
+                                         "sheep_capacity", "wolf_capacity")] + \
+               [(n, C.c_double) for n in ("energy_gain_sheep", "energy_gain_wolf", "metabolism",
+                                          "reproduce_prob_sheep", "reproduce_prob_wolf",
+                                          "reproduce_energy_frac")] + [("regrow_delay", C.c_int64)]
+
+
+class SpEv(C.Structure):
+    _fields_ = [("metabolized", C.c_int64), ("deaths", C.c_int64), ("births", C.c_int64),
+                ("births_dropped", C.c_int64), ("energy_removed_deaths", C.c_double),
+                ("energy_dropped_births", C.c_double)]
+
+
+class Ev(C.Structure):
+    _fields_ = [("grass_eaten", C.c_int64), ("sheep_eaten_by_wolves", C.c_int64),
+                ("sheep", SpEv), ("wolves", SpEv)]
+
+
+class OrcSpecies(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("num_active", C.c_int32), ("next_id", C.c_int64),
+                ("active", u8p), ("ids", i64p), ("types", i64p), ("ages", i64p), ("x", i64p),
+                ("y", i64p), ("energy", f64p)]
+
+
+def to_cfg(cfg) -> Cfg:
+    """Accepts a PredationConfig (product struct, same layout), a Cfg, or a dict."""
+    if isinstance(cfg, dict):
+        return Cfg(**cfg)
+    return Cfg(**{k: getattr(cfg, k) for k, _ in Cfg._fields_})
+
+
+def _p(a, t):
+    return a.ctypes.data_as(t)
+
+
+def events_dict(e: Ev) -> dict:
+    def sp(x):
+        return dict(metabolized=x.metabolized, deaths=x.deaths, births=x.births,
+                    births_dropped=x.births_dropped,
+                    energy_removed_deaths=x.energy_removed_deaths,
+                    energy_dropped_births=x.energy_dropped_births)
+    return dict(grass_eaten=e.grass_eaten, sheep_eaten_by_wolves=e.sheep_eaten_by_wolves,
+                sheep=sp(e.sheep), wolves=sp(e.wolves))
+
+
+_FNV = None
+
+
+def fnv1a(arrays) -> int:
+    """FNV-1a-64 over the concatenated bytes (same definition as ref_pred_hash)."""
+    global _FNV
+    if _FNV is None:
+        _FNV = C.CDLL(ORACLE_SO).orc_fnv1a
+        _FNV.restype = C.c_uint64
+        _FNV.argtypes = [C.c_uint64, C.c_void_p, C.c_size_t]
+    h = 0xcbf29ce484222325
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h = _FNV(h, a.ctypes.data, a.nbytes)
+    return int(h)
+
+
+def state_arrays(sheep: dict, wolves: dict, world=None):
+    out = []
+    for s in (sheep, wolves):
+        out += [s["active"].astype(np.uint8), s["ids"].astype(np.int64), s["ages"].astype(np.int64),
+                s["x"].astype(np.int64), s["y"].astype(np.int64), s["energy"].astype(np.float64)]
+    if world is not None:
+        out += [world[0].astype(np.uint8), world[1].astype(np.int64)]
+    return out
+
+
+class _Base:
+    lib: C.CDLL
+    prefix: str
+
+    def _f(self, name):
+        return getattr(self.lib, self.prefix + name)
+
+
+class Oracle(_Base):
+    """The C restatement (abmx_oracle.c)."""
+
+    prefix = "orc_"
+
+    def __init__(self, path: str = ORACLE_SO):
+        self.lib = L = C.CDLL(path)
+        L.orc_split.restype = C.c_uint64
+        L.orc_split.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_draw.restype = C.c_uint64
+        L.orc_draw.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_uniform_double.restype = C.c_double
+        L.orc_uniform_double.argtypes = [C.c_uint64, C.c_uint64]
+        L.orc_uniform_int.restype = C.c_int64
+        L.orc_uniform_int.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64]
+        L.orc_bernoulli.restype = C.c_int
+        L.orc_bernoulli.argtypes = [C.c_uint64, C.c_uint64, C.c_double]
+        L.orc_replica_seed.restype = C.c_uint64
+        L.orc_replica_seed.argtypes = [C.c_uint64, C.c_int64]
+        L.orc_rank_scan.argtypes = [u8p, i32p, C.c_size_t]
+        L.orc_count_true.restype = C.c_int64
+        L.orc_count_true.argtypes = [u8p, C.c_size_t]
+        L.orc_compact_indices.argtypes = [u8p, i32p, C.c_size_t]
+        L.orc_match_first_equal.argtypes = [i32p, C.c_size_t, i32p, C.c_size_t, i32p]
+        L.orc_blend_i64.argtypes = [u8p, i64p, i64p, i64p, C.c_size_t]
+        L.orc_blend_f64.argtypes = [u8p, f64p, f64p, f64p, C.c_size_t]
+        L.orc_blend_u8.argtypes = [u8p, u8p, u8p, u8p, C.c_size_t]
+        L.orc_pair.restype = C.c_int32
+        L.orc_pair.argtypes = [u8p, C.c_int32, u8p, C.c_int32, i32p, i32p]
+        L.orc_sort_perm.restype = C.c_int
+        L.orc_sort_perm.argtypes = [f64p, u8p, C.c_int32, C.c_int, i32p]
+        L.orc_pred_create.restype = C.c_void_p
+        L.orc_pred_create.argtypes = [C.POINTER(Cfg), C.c_uint64]
+        L.orc_pred_free.argtypes = [C.c_void_p]
+        L.orc_pred_step.argtypes = [C.c_void_p, C.c_int64, C.POINTER(Ev)]
+        L.orc_pred_metrics.argtypes = [C.c_void_p, i64p]
+        L.orc_pred_hash.restype = C.c_uint64
+        L.orc_pred_hash.argtypes = [C.c_void_p, C.c_int]
+        L.orc_pred_species.restype = C.POINTER(OrcSpecies)
+        L.orc_pred_species.argtypes = [C.c_void_p, C.c_int]
+        L.orc_pred_ready.restype = u8p
+        L.orc_pred_ready.argtypes = [C.c_void_p]
+        L.orc_pred_regrow.restype = i64p
+        L.orc_pred_regrow.argtypes = [C.c_void_p]
+        L.orc_run_batch.restype = C.c_int
+        L.orc_run_batch.argtypes = [C.POINTER(Cfg), C.c_uint64, C.c_int32, C.c_int64, f64p]
+
+    # rng
+    def split(self, k, i): return self.lib.orc_split(k, i)
+    def draw(self, k, c): return self.lib.orc_draw(k, c)
+    def uniform_double(self, k, c): return self.lib.orc_uniform_double(k, c)
+    def uniform_int(self, k, c, lo, hi): return self.lib.orc_uniform_int(k, c, lo, hi)
+    def replica_seed(self, m, r): return self.lib.orc_replica_seed(m, r)
+
+    # kernel table
+    def rank_scan(self, m):
+        m = np.ascontiguousarray(m, np.uint8)
+        o = np.empty(m.size, np.int32)
+        self.lib.orc_rank_scan(_p(m, u8p), _p(o, i32p), m.size)
+        return o
+
+    def count_true(self, m):
+        m = np.ascontiguousarray(m, np.uint8)
+        return int(self.lib.orc_count_true(_p(m, u8p), m.size))
+
+    def compact_indices(self, m):
+        m = np.ascontiguousarray(m, np.uint8)
+        o = np.empty(m.size, np.int32)
+        self.lib.orc_compact_indices(_p(m, u8p), _p(o, i32p), m.size)
+        return o
+
+    def match_first_equal(self, ra, rb):
+        a = np.ascontiguousarray(ra, np.int32)
+        b = np.ascontiguousarray(rb, np.int32)
+        o = np.empty(a.size, np.int32)
+        self.lib.orc_match_first_equal(_p(a, i32p), a.size, _p(b, i32p), b.size, _p(o, i32p))
+        return o
+
+    def blend(self, kind, m, a, b):
+        dt, pt = {"i64": (np.int64, i64p), "f64": (np.float64, f64p), "u8": (np.uint8, u8p)}[kind]
+        m = np.ascontiguousarray(m, np.uint8)
+        a = np.ascontiguousarray(a, dt)
+        b = np.ascontiguousarray(b, dt)
+        o = np.empty(m.size, dt)
+        getattr(self.lib, "orc_blend_" + kind)(_p(m, u8p), _p(a, pt), _p(b, pt), _p(o, pt), m.size)
+        return o
+
+    def pair(self, target, valid):
+        t = np.ascontiguousarray(target, np.uint8)
+        v = np.ascontiguousarray(valid, np.uint8)
+        s = np.empty(max(t.size, 1), np.int32)
+        r = np.empty(max(v.size, 1), np.int32)
+        k = self.lib.orc_pair(_p(t, u8p), t.size, _p(v, u8p), v.size, _p(s, i32p), _p(r, i32p))
+        return s[:k].copy(), r[:k].copy()
+
+    def sort_perm(self, key, active, descending=False):
+        k = np.ascontiguousarray(key, np.float64)
+        a = np.ascontiguousarray(active, np.uint8)
+        p = np.empty(max(k.size, 1), np.int32)
+        rc = self.lib.orc_sort_perm(_p(k, f64p), _p(a, u8p), k.size, int(descending), _p(p, i32p))
+        if rc:
+            raise ValueError("non-finite sort key on an active slot")
+        return p[:k.size].copy()
+
+    # predation
+    def pred(self, cfg, seed):
+        return OraclePred(self, to_cfg(cfg), seed)
+
+    def run_batch(self, cfg, master, replicas, steps):
+        out = np.empty((replicas, steps, 4), np.float64)
+        rc = self.lib.orc_run_batch(C.byref(to_cfg(cfg)), master, replicas, steps, _p(out, f64p))
+        assert rc == 0
+        return out
+
+
+class OraclePred:
+    def __init__(self, o: Oracle, cfg: Cfg, seed: int):
+        self.o, self.cfg = o, cfg
+        self.h = o.lib.orc_pred_create(C.byref(cfg), seed)
+        if not self.h:
+            raise ValueError("initial counts exceed capacities")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.lib.orc_pred_free(self.h)
+            self.h = None
+
+    def step(self, t):
+        ev = Ev()
+        self.o.lib.orc_pred_step(self.h, t, C.byref(ev))
+        return events_dict(ev)
+
+    def metrics(self):
+        m = (C.c_int64 * 4)()
+        self.o.lib.orc_pred_metrics(self.h, m)
+        return list(m)
+
+    def hash(self, with_world=True):
+        return int(self.o.lib.orc_pred_hash(self.h, 1 if with_world else 0))
+
+    def export_species(self, s):
+        sp = self.o.lib.orc_pred_species(self.h, s).contents
+        n = sp.capacity
+
+        def arr(ptr, dt):
+            return np.ctypeslib.as_array(ptr, shape=(max(n, 1),))[:n].astype(dt).copy() if n else np.zeros(0, dt)
+        return dict(active=arr(sp.active, np.uint8), ids=arr(sp.ids, np.int64),
+                    types=arr(sp.types, np.int64), ages=arr(sp.ages, np.int64),
+                    x=arr(sp.x, np.int64), y=arr(sp.y, np.int64), energy=arr(sp.energy, np.float64),
+                    num_active=sp.num_active, next_id=sp.next_id)
+
+    def import_species(self, s, d):
+        sp = self.o.lib.orc_pred_species(self.h, s).contents
+        n = sp.capacity
+        for name, dt in (("active", np.uint8), ("ids", np.int64), ("ages", np.int64),
+                         ("x", np.int64), ("y", np.int64), ("energy", np.float64)):
+            dst = np.ctypeslib.as_array(getattr(sp, name), shape=(max(n, 1),))
+            dst[:n] = np.asarray(d[name], dt)[:n]
+        sp.num_active = int(d["num_active"])
+        sp.next_id = int(d["next_id"])
+
+    def export_world(self):
+        c = self.cfg.width * self.cfg.height
+        r = np.ctypeslib.as_array(self.o.lib.orc_pred_ready(self.h), shape=(c,)).copy()
+        g = np.ctypeslib.as_array(self.o.lib.orc_pred_regrow(self.h), shape=(c,)).copy()
+        return r, g
+
+    def import_world(self, ready, regrow):
+        c = self.cfg.width * self.cfg.height
+        np.ctypeslib.as_array(self.o.lib.orc_pred_ready(self.h), shape=(c,))[:] = ready
+        np.ctypeslib.as_array(self.o.lib.orc_pred_regrow(self.h), shape=(c,))[:] = regrow
+
+
+class Reference(_Base):
+    """The unmodified reference library (oracle/_ref/libabmx_ref.so)."""
+
+    prefix = "ref_"
+
+    def __init__(self, path: str = REF_SO):
+        self.lib = L = C.CDLL(path)
+        L.ref_rng_split.restype = C.c_uint64
+        L.ref_rng_split.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_rng_draw.restype = C.c_uint64
+        L.ref_rng_draw.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_rng_uniform_double.restype = C.c_double
+        L.ref_rng_uniform_double.argtypes = [C.c_uint64, C.c_uint64]
+        L.ref_rng_uniform_int.restype = C.c_int64
+        L.ref_rng_uniform_int.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64]
+        L.ref_replica_seed.restype = C.c_uint64
+        L.ref_replica_seed.argtypes = [C.c_uint64, C.c_int32]
+        L.ref_kernel_table.restype = C.c_void_p
+        L.ref_kernel_table.argtypes = [C.c_int]
+        L.ref_pred_create.restype = C.c_void_p
+        L.ref_pred_create.argtypes = [C.POINTER(Cfg), C.c_uint64]
+        L.ref_pred_free.argtypes = [C.c_void_p]
+        L.ref_pred_step.argtypes = [C.c_void_p, C.c_int64, C.POINTER(Ev)]
+        L.ref_pred_run.restype = C.c_double
+        L.ref_pred_run.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.ref_pred_metrics.argtypes = [C.c_void_p, i64p]
+        L.ref_pred_hash.restype = C.c_uint64
+        L.ref_pred_hash.argtypes = [C.c_void_p, C.c_int]
+        L.ref_pred_export.argtypes = [C.c_void_p, C.c_int, u8p, i64p, i64p, i64p, i64p, i64p, f64p,
+                                      i32p, i64p]
+        L.ref_pred_import.argtypes = [C.c_void_p, C.c_int, u8p, i64p, i64p, i64p, i64p, i64p, f64p,
+                                      C.c_int32, C.c_int64]
+        L.ref_pred_export_world.argtypes = [C.c_void_p, u8p, i64p]
+        L.ref_pred_import_world.argtypes = [C.c_void_p, u8p, i64p]
+        L.ref_pred_birth_pairs.restype = C.c_int32
+        L.ref_pred_birth_pairs.argtypes = [C.c_void_p, C.c_int, i32p, i32p, C.c_int32]
+        L.ref_run_batch.restype = C.c_double
+        L.ref_run_batch.argtypes = [C.POINTER(Cfg), C.c_uint64, C.c_int32, C.c_int64, C.c_int, f64p]
+        L.ref_set_agents.restype = C.c_int
+        L.ref_set_agents.argtypes = [C.c_int, C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, u8p,
+                                     C.c_int32, i64p, f64p, u8p, u8p, i64p, f64p, u8p]
+        L.ref_select_mask.restype = C.c_int32
+        L.ref_select_mask.argtypes = [u8p, C.c_int32, i32p]
+        L.ref_sort_agents.restype = C.c_int
+        L.ref_sort_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, f64p, C.c_int,
+                                      u8p, i64p, i64p, i64p, f64p, u8p]
+
+    def split(self, k, i): return self.lib.ref_rng_split(k, i)
+    def draw(self, k, c): return self.lib.ref_rng_draw(k, c)
+    def uniform_double(self, k, c): return self.lib.ref_rng_uniform_double(k, c)
+    def uniform_int(self, k, c, lo, hi): return self.lib.ref_rng_uniform_int(k, c, lo, hi)
+    def replica_seed(self, m, r): return self.lib.ref_replica_seed(m, r)
+
+    def table(self, backend: int):
+        """The reference's own KernelTable (0 scalar, 1 avx2) as a ctypes struct."""
+        from types import SimpleNamespace
+        p = self.lib.ref_kernel_table(backend)
+        if not p:
+            return None
+
+        class KT(C.Structure):
+            _fields_ = [("name", C.c_char_p),
+                        ("rank_scan", C.CFUNCTYPE(None, u8p, i32p, C.c_size_t)),
+                        ("count_true", C.CFUNCTYPE(C.c_int64, u8p, C.c_size_t)),
+                        ("compact_indices", C.CFUNCTYPE(None, u8p, i32p, C.c_size_t)),
+                        ("match_first_equal", C.CFUNCTYPE(None, i32p, C.c_size_t, i32p, C.c_size_t, i32p)),
+                        ("blend_i64", C.CFUNCTYPE(None, u8p, i64p, i64p, i64p, C.c_size_t)),
+                        ("blend_f64", C.CFUNCTYPE(None, u8p, f64p, f64p, f64p, C.c_size_t)),
+                        ("blend_u8", C.CFUNCTYPE(None, u8p, u8p, u8p, u8p, C.c_size_t))]
+        return SimpleNamespace(struct=C.cast(p, C.POINTER(KT)).contents, lib=self.lib)
+
+    def pred(self, cfg, seed):
+        return RefPred(self, to_cfg(cfg), seed)
+
+    def run_batch(self, cfg, master, replicas, steps, threads=0):
+        out = np.empty((replicas, steps, 4), np.float64)
+        wall = self.lib.ref_run_batch(C.byref(to_cfg(cfg)), master, replicas, steps, threads,
+                                      _p(out, f64p))
+        assert wall >= 0
+        return out, wall
+
+
+class RefPred:
+    def __init__(self, r: Reference, cfg: Cfg, seed: int):
+        self.r, self.cfg = r, cfg
+        self.h = r.lib.ref_pred_create(C.byref(cfg), seed)
+        if not self.h:
+            raise ValueError("initial counts exceed capacities")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.r.lib.ref_pred_free(self.h)
+            self.h = None
+
+    def step(self, t):
+        ev = Ev()
+        self.r.lib.ref_pred_step(self.h, t, C.byref(ev))
+        return events_dict(ev)
+
+    def run(self, t0, steps):
+        return self.r.lib.ref_pred_run(self.h, t0, steps)
+
+    def metrics(self):
+        m = (C.c_int64 * 4)()
+        self.r.lib.ref_pred_metrics(self.h, m)
+        return list(m)
+
+    def hash(self, with_world=True):
+        return int(self.r.lib.ref_pred_hash(self.h, 1 if with_world else 0))
+
+    def export_species(self, s):
+        n = self.cfg.sheep_capacity if s == 0 else self.cfg.wolf_capacity
+        d = dict(active=np.empty(n, np.uint8), ids=np.empty(n, np.int64),
+                 types=np.empty(n, np.int64), ages=np.empty(n, np.int64),
+                 x=np.empty(n, np.int64), y=np.empty(n, np.int64), energy=np.empty(n, np.float64))
+        na, nid = C.c_int32(), C.c_int64()
+        self.r.lib.ref_pred_export(self.h, s, _p(d["active"], u8p), _p(d["ids"], i64p),
+                                   _p(d["types"], i64p), _p(d["ages"], i64p), _p(d["x"], i64p),
+                                   _p(d["y"], i64p), _p(d["energy"], f64p), C.byref(na),
+                                   C.byref(nid))
+        d["num_active"], d["next_id"] = na.value, nid.value
+        return d
+
+    def import_species(self, s, d):
+        a = {k: np.ascontiguousarray(d[k], dt) for k, dt in (
+            ("active", np.uint8), ("ids", np.int64), ("types", np.int64), ("ages", np.int64),
+            ("x", np.int64), ("y", np.int64), ("energy", np.float64))} if "types" in d else None
+        if a is None:
+            n = len(d["active"])
+            d = dict(d)
+            d["types"] = np.full(n, s, np.int64)
+            return self.import_species(s, d)
+        self.r.lib.ref_pred_import(self.h, s, _p(a["active"], u8p), _p(a["ids"], i64p),
+                                   _p(a["types"], i64p), _p(a["ages"], i64p), _p(a["x"], i64p),
+                                   _p(a["y"], i64p), _p(a["energy"], f64p), int(d["num_active"]),
+                                   int(d["next_id"]))
+
+    def export_world(self):
+        c = self.cfg.width * self.cfg.height
+        r = np.empty(c, np.uint8)
+        g = np.empty(c, np.int64)
+        self.r.lib.ref_pred_export_world(self.h, _p(r, u8p), _p(g, i64p))
+        return r, g
+
+    def import_world(self, ready, regrow):
+        r = np.ascontiguousarray(ready, np.uint8)
+        g = np.ascontiguousarray(regrow, np.int64)
+        self.r.lib.ref_pred_import_world(self.h, _p(r, u8p), _p(g, i64p))
+
+    def birth_pairs(self, s):
+        n = self.cfg.sheep_capacity if s == 0 else self.cfg.wolf_capacity
+        par = np.empty(max(n, 1), np.int32)
+        ch = np.empty(max(n, 1), np.int32)
+        k = self.r.lib.ref_pred_birth_pairs(self.h, s, _p(par, i32p), _p(ch, i32p), n)
+        return list(zip(par[:k].tolist(), ch[:k].tolist()))

@@ -1,0 +1,158 @@
+// abmx_device.cuh — shared device primitives for the sm_100a engine.
+//
+//  * counter-based RNG, bit-exact with the reference RngState (src/rng.cpp:12-40)
+//  * packed two-counter decoupled-lookback tile scan (single pass, warp-ballot lookback)
+//  * block-level helpers
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace abmx_dev {
+
+// ------------------------------------------------------------------ RNG
+// draw(c)  = mix64(key + 0x9E3779B97F4A7C15 * (c + 1))        src/rng.cpp:22-24
+// split(i) = mix64(key + 0xC2B2AE3D27D4EB4F * (i + 1))        src/rng.cpp:18-20
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t split(uint64_t key, uint64_t i) {
+    return mix64(key + 0xC2B2AE3D27D4EB4FULL * (i + 1));
+}
+__host__ __device__ __forceinline__ uint64_t draw(uint64_t key, uint64_t c) {
+    return mix64(key + 0x9E3779B97F4A7C15ULL * (c + 1));
+}
+// uniform_int(c, 0, span) = high64(draw * span)                src/rng.cpp:30-36
+__device__ __forceinline__ uint64_t uniform_span(uint64_t key, uint64_t c, uint64_t span) {
+    return __umul64hi(draw(key, c), span);
+}
+// (draw >> 11) * 2^-53: the u64->f64 conversion is exact for 53-bit values  src/rng.cpp:26-28
+__device__ __forceinline__ double uniform_double(uint64_t key, uint64_t c) {
+    return __dmul_rn(__ull2double_rn(draw(key, c) >> 11), 0x1.0p-53);
+}
+
+// ------------------------------------------------------------------ memory order
+__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// ------------------------------------------------------------------ packed counters
+// Two non-negative counts (each < 2^31) share one u64 so a tile publishes both of
+// its aggregates (e.g. free-slot and valid-row counts) with one store. Bits 63..62
+// hold the lookback flag.
+constexpr unsigned long long kFlagAgg = 1ULL << 62;
+constexpr unsigned long long kFlagPrefix = 2ULL << 62;
+constexpr unsigned long long kValueMask = (1ULL << 62) - 1;
+
+__host__ __device__ __forceinline__ unsigned long long pack2(uint32_t a, uint32_t b) {
+    return (static_cast<unsigned long long>(a) << 31) | b;
+}
+__host__ __device__ __forceinline__ uint32_t lo31(unsigned long long v) {
+    return static_cast<uint32_t>(v & 0x7FFFFFFFULL);
+}
+__host__ __device__ __forceinline__ uint32_t hi31(unsigned long long v) {
+    return static_cast<uint32_t>((v >> 31) & 0x7FFFFFFFULL);
+}
+
+// Warp-inclusive scan of packed u64 values (fields never overflow by construction).
+__device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned long long n = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += n;
+    }
+    return v;
+}
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// Block exclusive scan of a packed value. `smem` needs (blockDim/32 + 1) entries.
+// Returns the exclusive prefix for this thread; *block_total receives the tile sum.
+template <int kThreads>
+__device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
+                                                              unsigned long long* smem,
+                                                              unsigned long long* block_total) {
+    constexpr int kWarps = kThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned long long incl = warp_incl_scan(v);
+    if (lane == 31) smem[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned long long w = lane < kWarps ? smem[lane] : 0ULL;
+        const unsigned long long wi = warp_incl_scan(w);
+        if (lane < kWarps) smem[lane] = wi - w;  // exclusive warp offsets
+        if (lane == kWarps - 1) smem[kWarps] = wi;
+    }
+    __syncthreads();
+    *block_total = smem[kWarps];
+    return smem[warp] + incl - v;
+}
+
+// Decoupled lookback (single pass). Called by ONE full warp of the tile after the tile
+// aggregate is known. `status` entries start at 0 (invalid). Tiles must be processed in
+// ticket order (tile k obtained its ticket after tiles < k), which guarantees progress.
+// Returns the exclusive prefix of this tile (flag bits stripped), valid in all lanes.
+__device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* status, int tile,
+                                                            unsigned long long aggregate) {
+    const int lane = threadIdx.x & 31;
+    if (tile == 0) {
+        if (lane == 0) st_release(&status[0], kFlagPrefix | aggregate);
+        return 0ULL;
+    }
+    if (lane == 0) st_release(&status[tile], kFlagAgg | aggregate);
+    unsigned long long excl = 0ULL;
+    int end = tile - 1;  // closest predecessor examined by lane 0
+    for (;;) {
+        const int j = end - lane;
+        unsigned long long sv = j >= 0 ? ld_acquire(&status[j]) : kFlagPrefix;
+        // spin (convergently) until every examined predecessor has published something
+        while (__any_sync(0xffffffffu, (sv >> 62) == 0)) {
+            if ((sv >> 62) == 0) {
+                __nanosleep(32);
+                sv = ld_acquire(&status[j]);
+            }
+        }
+        const unsigned pmask = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
+        unsigned long long contrib = sv & kValueMask;
+        if (pmask) {
+            const int first = __ffs(pmask) - 1;  // closest tile with an inclusive prefix
+            if (lane > first) contrib = 0ULL;
+            excl += warp_sum(contrib);
+            break;
+        }
+        excl += warp_sum(contrib);
+        end -= 32;
+    }
+    if (lane == 0) st_release(&status[tile], kFlagPrefix | (excl + aggregate));
+    return excl;
+}
+
+// Warp-aggregated atomic increment: every lane with `pred` receives a unique index.
+__device__ __forceinline__ unsigned warp_append(unsigned* counter, bool pred) {
+    const unsigned mask = __ballot_sync(__activemask(), pred);
+    if (!pred) return 0u;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(mask) - 1;
+    unsigned base = 0;
+    if (lane == leader) base = atomicAdd(counter, static_cast<unsigned>(__popc(mask)));
+    base = __shfl_sync(mask, base, leader);
+    return base + __popc(mask & ((1u << lane) - 1u));
+}
+
+}  // namespace abmx_dev

@@ -1,0 +1,31 @@
+// abmx_internal.h — declarations shared by the .cu translation units (not public).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include <cuda_runtime.h>
+
+namespace abmx_internal {
+
+int num_sms();
+void count_launch(int k = 1);          // launches of our own kernels (gpu_launches)
+unsigned long long launches();
+
+void set_error(const std::string& msg);  // thread-local last error
+const char* last_error();
+
+// KernelTable launchers (device pointers, stream-ordered); table.cu
+cudaError_t launch_rank_scan(const uint8_t* d_mask, int32_t* d_ranks, size_t n, cudaStream_t s);
+cudaError_t launch_count_true(const uint8_t* d_mask, size_t n, unsigned long long* d_out,
+                              cudaStream_t s);
+cudaError_t launch_compact_indices(const uint8_t* d_mask, int32_t* d_out, size_t n,
+                                   unsigned long long* d_count, cudaStream_t s);
+cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_t* d_rb, size_t m,
+                                     int32_t* d_out, cudaStream_t s);
+template <class T>
+cudaError_t launch_blend(const uint8_t* d_mask, const T* d_a, const T* d_b, T* d_out, size_t n,
+                         cudaStream_t s);
+
+}  // namespace abmx_internal

@@ -1,0 +1,577 @@
+// ensemble.cu — batched ensemble of independent predation models (run_batch,
+// src/batch.cpp:21-101; the paper's vmapped ensemble), one CTA per replica.
+//
+// A C1-sized replica (100x100 cells, 2 x 1024 slots) is small enough that its whole state
+// stays ON CHIP for the entire run: agent columns live in REGISTERS (thread t owns slots
+// t*SPT .. t*SPT+SPT-1 of both species for every step), the lattice and the per-cell lists
+// live in shared memory, and HBM is touched only for the initial draw, the id column
+// (written at births/deaths) and one metrics row per step. Each step is four phases
+// separated by __syncthreads:
+//   1 move + push onto packed per-cell lists (u32: sheep head | wolf head)     lifecycle.cpp:87-122
+//   2 graze (lowest sheep slot per ready cell) + predation (slot-sorted pairing per wolf cell)
+//                                                                              predation.cpp:178-239
+//   3 eat/metabolise/starve/reproduce, one block-wide scan of four packed 16-bit counters
+//     (free/valid x sheep/wolves) and compaction of the valid rows              predation.cpp:241-250
+//   4 free slots pull their rank-matched row (spawn_agents), regrow, metrics   lifecycle.cpp:144-195
+#include <climits>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "abmx_device.cuh"
+#include "abmx_internal.h"
+#include "ensemble.h"
+
+using namespace abmx_dev;
+
+namespace abmx_ens {
+
+constexpr int kT = 512;
+constexpr int kMaxSPT = 8;
+constexpr unsigned kEnd = 0xFFFFu;
+
+__constant__ int e_dx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+__constant__ int e_dy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+
+struct EnsParams {
+    int W, H, C, Cpad;
+    int N[2], n0[2], stride;
+    double gain[2], metab, prob[2], frac;
+    unsigned delay_code;
+    long long steps;
+    const unsigned long long* seeds;
+    long long* ids;     // [count][2][stride]
+    double* metrics;    // [count][steps][4]
+    // optional final-state dump
+    uint8_t* d_active;  // [count][2][stride]
+    int* d_cell;
+    int* d_age;
+    double* d_energy;
+    uint8_t* d_g;       // [count][Cpad]
+    long long* d_next;  // [count][2]
+    int* d_num;         // [count][2]
+    // dynamic shared memory carve-up (byte offsets)
+    int o_rowe[2], o_scan, o_cw, o_rowc[2], o_nxt[2], o_pool, o_flag[2], o_g, o_misc, smem;
+};
+
+__device__ __forceinline__ unsigned long long pack4(unsigned a, unsigned b, unsigned c, unsigned d) {
+    return (static_cast<unsigned long long>(a) << 48) | (static_cast<unsigned long long>(b) << 32) |
+           (static_cast<unsigned long long>(c) << 16) | d;
+}
+__device__ __forceinline__ unsigned f16(unsigned long long v, int k) {  // k = 0..3 from the top
+    return static_cast<unsigned>((v >> (48 - 16 * k)) & 0xFFFFu);
+}
+
+__device__ void sort_small(unsigned short* a, int n) {
+    for (int i = 1; i < n; ++i) {
+        const unsigned short v = a[i];
+        int j = i - 1;
+        while (j >= 0 && a[j] > v) {
+            a[j + 1] = a[j];
+            --j;
+        }
+        a[j + 1] = v;
+    }
+}
+__device__ void heap_sort16(unsigned short* a, int n) {
+    auto sift = [&](int root, int end) {
+        for (;;) {
+            int child = 2 * root + 1;
+            if (child >= end) return;
+            if (child + 1 < end && a[child + 1] > a[child]) ++child;
+            if (a[root] >= a[child]) return;
+            const unsigned short t = a[root];
+            a[root] = a[child];
+            a[child] = t;
+            root = child;
+        }
+    };
+    for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
+    for (int end = n - 1; end > 0; --end) {
+        const unsigned short t = a[0];
+        a[0] = a[end];
+        a[end] = t;
+        sift(0, end);
+    }
+}
+
+template <int SPT>
+__global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    double* rowE[2] = {reinterpret_cast<double*>(sm + P.o_rowe[0]), reinterpret_cast<double*>(sm + P.o_rowe[1])};
+    unsigned long long* scan = reinterpret_cast<unsigned long long*>(sm + P.o_scan);
+    unsigned* cw = reinterpret_cast<unsigned*>(sm + P.o_cw);
+    unsigned* rowc[2] = {reinterpret_cast<unsigned*>(sm + P.o_rowc[0]), reinterpret_cast<unsigned*>(sm + P.o_rowc[1])};
+    unsigned short* nxt[2] = {reinterpret_cast<unsigned short*>(sm + P.o_nxt[0]),
+                              reinterpret_cast<unsigned short*>(sm + P.o_nxt[1])};
+    unsigned short* pool = reinterpret_cast<unsigned short*>(sm + P.o_pool);
+    uint8_t* flag[2] = {sm + P.o_flag[0], sm + P.o_flag[1]};
+    uint8_t* g = sm + P.o_g;
+    unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [0] pool top, [1] grass
+    long long* red = reinterpret_cast<long long*>(sm + P.o_misc + 16);
+
+    const int r = blockIdx.x, tid = threadIdx.x;
+    const unsigned long long seed = P.seeds[r];
+    long long* ids = P.ids + static_cast<size_t>(r) * 2 * P.stride;
+
+    // ---- create_species (predation.cpp:22-33, lifecycle.cpp:53-85)
+    bool act[2][SPT];
+    int cell[2][SPT], age[2][SPT], pc[2][SPT], frk[2][SPT];
+    double E[2][SPT];
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+        const unsigned long long root = split(split(seed, s == 0 ? 20 : 21), 1);
+        const unsigned long long kx = split(root, 0), ky = split(root, 1), ke = split(root, 2);
+        const long long ehi = 2 * static_cast<long long>(P.gain[s]) + 1;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int i = tid * SPT + k;
+            act[s][k] = i < P.n0[s];
+            cell[s][k] = 0;
+            age[s][k] = 0;
+            E[s][k] = 0.0;
+            if (act[s][k]) {
+                const long long x = static_cast<long long>(__umul64hi(draw(kx, i), static_cast<unsigned long long>(P.W)));
+                const long long y = static_cast<long long>(__umul64hi(draw(ky, i), static_cast<unsigned long long>(P.H)));
+                const long long en = 1 + static_cast<long long>(__umul64hi(draw(ke, i), static_cast<unsigned long long>(ehi - 1)));
+                cell[s][k] = static_cast<int>(y * P.W + x);
+                E[s][k] = static_cast<double>(en);
+            }
+            if (i < P.N[s]) ids[static_cast<size_t>(s) * P.stride + i] = act[s][k] ? i : 0;
+        }
+    }
+    for (int c = tid; c < P.Cpad; c += kT) g[c] = c < P.C ? 0 : 255;
+    for (int c = tid; c < P.C; c += kT) cw[c] = 0xFFFFFFFFu;
+    for (int i = tid; i < P.N[0]; i += kT) flag[0][i] = 0;
+    for (int i = tid; i < P.N[1]; i += kT) flag[1][i] = 0;
+    if (tid == 0) misc[0] = 0;
+    long long next_id[2] = {P.n0[0], P.n0[1]};
+    const unsigned long long mroot = split(seed, 3), rroot = split(seed, 4);
+    __syncthreads();
+
+    for (long long t = 1; t <= P.steps; ++t) {
+        unsigned long long mk[2], rk[2];
+        {
+            const unsigned long long mt = split(mroot, static_cast<unsigned long long>(t));
+            const unsigned long long rt = split(rroot, static_cast<unsigned long long>(t));
+            mk[0] = split(mt, 0);
+            mk[1] = split(mt, 1);
+            rk[0] = split(rt, 0);
+            rk[1] = split(rt, 1);
+        }
+        // ---- phase 1: move + push onto the per-cell lists
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                pc[s][k] = -1;
+                if (!act[s][k]) continue;
+                const int i = tid * SPT + k;
+                const int u = static_cast<int>(draw(mk[s], static_cast<unsigned long long>(i)) >> 61);
+                const int c = cell[s][k];
+                const int y = c / P.W, x = c - y * P.W;
+                int nx = x + e_dx[u], ny = y + e_dy[u];
+                nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
+                ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
+                const int nc = ny * P.W + nx;
+                cell[s][k] = nc;
+                pc[s][k] = nc;
+                age[s][k] += 1;
+                unsigned old = cw[nc];
+                for (;;) {
+                    const unsigned nv = s == 0 ? ((old & 0xFFFF0000u) | static_cast<unsigned>(i))
+                                               : ((old & 0x0000FFFFu) | (static_cast<unsigned>(i) << 16));
+                    const unsigned prev = atomicCAS(&cw[nc], old, nv);
+                    if (prev == old) break;
+                    old = prev;
+                }
+                nxt[s][i] = static_cast<unsigned short>(s == 0 ? (old & 0xFFFFu) : (old >> 16));
+            }
+        __syncthreads();
+        // ---- phase 2: graze + predation pairing
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            if (!act[0][k]) continue;
+            const int i = tid * SPT + k;
+            const int c = cell[0][k];
+            unsigned m = static_cast<unsigned>(i);
+            for (unsigned v = cw[c] & 0xFFFFu; v != kEnd; v = nxt[0][v]) m = v < m ? v : m;
+            if (m == static_cast<unsigned>(i) && g[c] == 0) {
+                g[c] = static_cast<uint8_t>(P.delay_code);
+                E[0][k] = __dadd_rn(E[0][k], P.gain[0]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            if (!act[1][k]) continue;
+            const int i = tid * SPT + k;
+            const int c = cell[1][k];
+            const unsigned head = cw[c];
+            if ((head >> 16) != static_cast<unsigned>(i)) continue;  // the list head leads its cell
+            const unsigned s0 = head & 0xFFFFu;
+            if (s0 == kEnd) continue;
+            int lw = 0, ls = 0;
+            for (unsigned v = head >> 16; v != kEnd; v = nxt[1][v]) ++lw;
+            for (unsigned v = s0; v != kEnd; v = nxt[0][v]) ++ls;
+            unsigned short wl_r[8], sl_r[8];
+            unsigned short *wl = wl_r, *sl = sl_r;
+            const bool small = lw <= 8 && ls <= 8;
+            if (!small) {
+                const unsigned off = atomicAdd(&misc[0], static_cast<unsigned>(lw + ls));
+                wl = pool + off;
+                sl = wl + lw;
+            }
+            int q = 0;
+            for (unsigned v = head >> 16; v != kEnd; v = nxt[1][v]) wl[q++] = static_cast<unsigned short>(v);
+            q = 0;
+            for (unsigned v = s0; v != kEnd; v = nxt[0][v]) sl[q++] = static_cast<unsigned short>(v);
+            if (small) {
+                sort_small(wl, lw);
+                sort_small(sl, ls);
+            } else {
+                heap_sort16(wl, lw);
+                heap_sort16(sl, ls);
+            }
+            const int pairs = lw < ls ? lw : ls;
+            for (int p = 0; p < pairs; ++p) {
+                flag[0][sl[p]] = 1;
+                flag[1][wl[p]] = 1;
+            }
+        }
+        __syncthreads();
+        // ---- phase 3: eat / metabolise / starve / reproduce, one packed scan
+        unsigned cnt[2][2] = {{0, 0}, {0, 0}};  // [species][free, valid]
+        bool valid[2][SPT];
+        double child[2][SPT];
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                const int i = tid * SPT + k;
+                valid[s][k] = false;
+                child[s][k] = 0.0;
+                if (pc[s][k] >= 0) cw[pc[s][k]] = 0xFFFFFFFFu;  // clear for the next step
+                bool alive = act[s][k];
+                if (alive && flag[s][i]) {
+                    flag[s][i] = 0;
+                    if (s == 0)
+                        alive = false;  // eaten (predation.cpp:224-238)
+                    else
+                        E[s][k] = __dadd_rn(E[s][k], P.gain[1]);
+                }
+                if (alive) {
+                    E[s][k] = __dsub_rn(E[s][k], P.metab);
+                    if (E[s][k] <= 0.0) alive = false;
+                }
+                if (alive && E[s][k] > P.metab &&
+                    uniform_double(rk[s], static_cast<unsigned long long>(i)) < P.prob[s]) {
+                    const double cE = __dmul_rn(floor(__dmul_rn(__dmul_rn(P.frac, E[s][k]), 1048576.0)), 0x1p-20);
+                    E[s][k] = __dsub_rn(E[s][k], cE);
+                    child[s][k] = cE;
+                    valid[s][k] = true;
+                }
+                if (act[s][k] && !alive) {
+                    act[s][k] = false;
+                    cell[s][k] = 0;
+                    age[s][k] = 0;
+                    E[s][k] = 0.0;
+                    ids[static_cast<size_t>(s) * P.stride + i] = 0;
+                }
+                const bool fr = !alive && i < P.N[s];
+                frk[s][k] = fr ? 1 : -1;
+                cnt[s][0] += fr;
+                cnt[s][1] += valid[s][k];
+            }
+        unsigned long long total;
+        const unsigned long long ex =
+            block_excl_scan<kT>(pack4(cnt[0][0], cnt[0][1], cnt[1][0], cnt[1][1]), scan, &total);
+        if (tid == 0) misc[0] = 0;
+        unsigned run[2][2] = {{f16(ex, 0), f16(ex, 1)}, {f16(ex, 2), f16(ex, 3)}};
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                if (frk[s][k] > 0) frk[s][k] = static_cast<int>(run[s][0]++);
+                if (valid[s][k]) {
+                    const unsigned v = run[s][1]++;
+                    rowc[s][v] = static_cast<unsigned>(cell[s][k]);
+                    rowE[s][v] = child[s][k];
+                }
+            }
+        const int F[2] = {static_cast<int>(f16(total, 0)), static_cast<int>(f16(total, 2))};
+        const int Q[2] = {static_cast<int>(f16(total, 1)), static_cast<int>(f16(total, 3))};
+        __syncthreads();
+        // ---- phase 4: rank-matched births, regrow, metrics row
+        int pairs[2];
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            pairs[s] = F[s] < Q[s] ? F[s] : Q[s];
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                const int f = frk[s][k];
+                if (f >= 0 && f < pairs[s]) {
+                    const int i = tid * SPT + k;
+                    act[s][k] = true;
+                    cell[s][k] = static_cast<int>(rowc[s][f]);
+                    E[s][k] = rowE[s][f];
+                    age[s][k] = 0;
+                    ids[static_cast<size_t>(s) * P.stride + i] = next_id[s] + f;
+                }
+            }
+            next_id[s] += pairs[s];
+        }
+        unsigned ready = 0;
+        unsigned* g32 = reinterpret_cast<unsigned*>(g);
+        for (int w = tid; w < P.Cpad / 4; w += kT) {
+            unsigned x = g32[w], o = 0;
+            bool ch = false;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                unsigned v = (x >> (8 * b)) & 0xFFu;
+                if (v >= 1 && v <= 254) {
+                    --v;
+                    ch = true;
+                }
+                ready += v == 0;
+                o |= v << (8 * b);
+            }
+            if (ch) g32[w] = o;
+        }
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) ready += __shfl_xor_sync(0xffffffffu, ready, d);
+        if ((tid & 31) == 0) red[tid >> 5] = ready;
+        __syncthreads();
+        if (tid == 0) {
+            long long grass = 0;
+            for (int w = 0; w < kT / 32; ++w) grass += red[w];
+            double* row = P.metrics + (static_cast<size_t>(r) * P.steps + (t - 1)) * 4;
+            row[0] = static_cast<double>(P.N[0] - F[0] + pairs[0]);
+            row[1] = static_cast<double>(P.N[1] - F[1] + pairs[1]);
+            row[2] = static_cast<double>(grass);
+            row[3] = static_cast<double>((Q[0] - pairs[0]) + (Q[1] - pairs[1]));
+            if (t == P.steps && P.d_num) {
+                P.d_num[2 * r] = P.N[0] - F[0] + pairs[0];
+                P.d_num[2 * r + 1] = P.N[1] - F[1] + pairs[1];
+            }
+        }
+    }
+    if (P.d_active) {
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int k = 0; k < SPT; ++k) {
+                const int i = tid * SPT + k;
+                if (i >= P.N[s]) continue;
+                const size_t q = (static_cast<size_t>(r) * 2 + s) * P.stride + i;
+                P.d_active[q] = act[s][k];
+                P.d_cell[q] = cell[s][k];
+                P.d_age[q] = age[s][k];
+                P.d_energy[q] = E[s][k];
+            }
+        for (int c = tid; c < P.Cpad; c += kT) P.d_g[static_cast<size_t>(r) * P.Cpad + c] = g[c];
+        if (tid == 0) {
+            P.d_next[2 * r] = next_id[0];
+            P.d_next[2 * r + 1] = next_id[1];
+        }
+    }
+}
+
+static int layout(const abmx_predation_config& cfg, EnsParams& P) {
+    const int N[2] = {cfg.sheep_capacity, cfg.wolf_capacity};
+    int off = 0;
+    auto take = [&](int bytes, int align) {
+        off = (off + align - 1) / align * align;
+        const int o = off;
+        off += bytes;
+        return o;
+    };
+    P.o_rowe[0] = take(8 * (N[0] > 0 ? N[0] : 1), 16);
+    P.o_rowe[1] = take(8 * (N[1] > 0 ? N[1] : 1), 16);
+    P.o_scan = take(8 * (kT / 32 + 2), 16);
+    P.o_misc = take(16 + 8 * (kT / 32), 16);
+    P.o_cw = take(4 * P.C, 16);
+    P.o_rowc[0] = take(4 * (N[0] > 0 ? N[0] : 1), 16);
+    P.o_rowc[1] = take(4 * (N[1] > 0 ? N[1] : 1), 16);
+    P.o_nxt[0] = take(2 * (N[0] > 0 ? N[0] : 1), 16);
+    P.o_nxt[1] = take(2 * (N[1] > 0 ? N[1] : 1), 16);
+    P.o_pool = take(2 * (N[0] + N[1] + 2), 16);
+    P.o_flag[0] = take(N[0] > 0 ? N[0] : 1, 16);
+    P.o_flag[1] = take(N[1] > 0 ? N[1] : 1, 16);
+    P.o_g = take(P.Cpad, 16);
+    P.smem = (off + 15) / 16 * 16;
+    return P.smem;
+}
+
+static int spt_for(const abmx_predation_config& cfg) {
+    const int n = cfg.sheep_capacity > cfg.wolf_capacity ? cfg.sheep_capacity : cfg.wolf_capacity;
+    for (int spt = 1; spt <= kMaxSPT; spt *= 2)
+        if (n <= spt * kT) return spt;
+    return 0;
+}
+
+bool smem_fits(const abmx_predation_config& cfg) {
+    if (cfg.width < 1 || cfg.height < 1 || cfg.sheep_capacity < 0 || cfg.wolf_capacity < 0) return false;
+    if (cfg.regrow_delay > 254) return false;
+    const long long C = static_cast<long long>(cfg.width) * cfg.height;
+    if (C > 65536LL * 4) return false;
+    if (spt_for(cfg) == 0) return false;
+    EnsParams P{};
+    P.C = static_cast<int>(C);
+    P.Cpad = static_cast<int>((C + 15) / 16 * 16);
+    return layout(cfg, P) <= 227 * 1024;
+}
+
+#define CKE(x)                                                                        \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            abmx_internal::set_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+            rc = ABMX_E_CUDA;                                                         \
+            goto done;                                                                \
+        }                                                                             \
+    } while (0)
+
+int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count, long long steps,
+             double* metrics_out, double* kernel_ms, Dump* dump) {
+    if (cfg.n_sheep0 > cfg.sheep_capacity || cfg.n_wolves0 > cfg.wolf_capacity || cfg.n_sheep0 < 0 ||
+        cfg.n_wolves0 < 0) {
+        abmx_internal::set_error("initial counts exceed capacities");
+        return ABMX_E_CAPACITY;
+    }
+    if (!smem_fits(cfg)) {
+        abmx_internal::set_error("configuration does not fit the SMEM-resident ensemble kernel");
+        return ABMX_E_DOMAIN;
+    }
+    EnsParams P{};
+    P.W = cfg.width;
+    P.H = cfg.height;
+    P.C = cfg.width * cfg.height;
+    P.Cpad = (P.C + 15) / 16 * 16;
+    P.N[0] = cfg.sheep_capacity;
+    P.N[1] = cfg.wolf_capacity;
+    P.n0[0] = cfg.n_sheep0;
+    P.n0[1] = cfg.n_wolves0;
+    P.stride = ((P.N[0] > P.N[1] ? P.N[0] : P.N[1]) + 15) / 16 * 16;
+    if (P.stride == 0) P.stride = 16;
+    P.gain[0] = cfg.energy_gain_sheep;
+    P.gain[1] = cfg.energy_gain_wolf;
+    P.metab = cfg.metabolism;
+    P.prob[0] = cfg.reproduce_prob_sheep;
+    P.prob[1] = cfg.reproduce_prob_wolf;
+    P.frac = cfg.reproduce_energy_frac;
+    P.delay_code = cfg.regrow_delay >= 1 ? static_cast<unsigned>(cfg.regrow_delay) : 255u;
+    P.steps = steps;
+    layout(cfg, P);
+    const int spt = spt_for(cfg);
+
+    int rc = ABMX_OK;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    void* dseeds = nullptr;
+    void* dids = nullptr;
+    void* dmet = nullptr;
+    void* ddump = nullptr;
+    const size_t mbytes = sizeof(double) * 4 * static_cast<size_t>(count) * static_cast<size_t>(steps);
+    const size_t ids_n = static_cast<size_t>(count) * 2 * P.stride;
+    float ms = 0.f;
+    CKE(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CKE(cudaEventCreate(&ea));
+    CKE(cudaEventCreate(&eb));
+    CKE(cudaMallocAsync(&dseeds, sizeof(unsigned long long) * count, st));
+    CKE(cudaMallocAsync(&dids, ids_n * 8, st));
+    CKE(cudaMallocAsync(&dmet, mbytes, st));
+    CKE(cudaMemcpyAsync(dseeds, seeds, sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, st));
+    P.seeds = static_cast<const unsigned long long*>(dseeds);
+    P.ids = static_cast<long long*>(dids);
+    P.metrics = static_cast<double*>(dmet);
+    if (dump) {
+        const size_t n = ids_n;
+        const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
+        CKE(cudaMallocAsync(&ddump, bytes, st));
+        char* b = static_cast<char*>(ddump);
+        P.d_energy = reinterpret_cast<double*>(b);
+        b += n * 8;
+        P.d_next = reinterpret_cast<long long*>(b);
+        b += static_cast<size_t>(count) * 2 * 8;
+        P.d_cell = reinterpret_cast<int*>(b);
+        b += n * 4;
+        P.d_age = reinterpret_cast<int*>(b);
+        b += n * 4;
+        P.d_num = reinterpret_cast<int*>(b);
+        b += static_cast<size_t>(count) * 2 * 4;
+        P.d_active = reinterpret_cast<uint8_t*>(b);
+        b += n;
+        P.d_g = reinterpret_cast<uint8_t*>(b);
+    }
+    {
+        void (*kern)(EnsParams) = nullptr;
+        switch (spt) {
+            case 1: kern = k_ensemble<1>; break;
+            case 2: kern = k_ensemble<2>; break;
+            case 4: kern = k_ensemble<4>; break;
+            default: kern = k_ensemble<8>; break;
+        }
+        CKE(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem));
+        CKE(cudaEventRecord(ea, st));
+        (void)cudaGetLastError();
+        kern<<<count, kT, P.smem, st>>>(P);
+        abmx_internal::count_launch();
+        CKE(cudaGetLastError());
+        CKE(cudaEventRecord(eb, st));
+    }
+    if (metrics_out) CKE(cudaMemcpyAsync(metrics_out, dmet, mbytes, cudaMemcpyDeviceToHost, st));
+    if (dump) {
+        const int r = dump->replica;
+        std::vector<uint8_t> a(P.stride), gg(P.Cpad);
+        std::vector<int> c(P.stride), ag(P.stride);
+        long long nx[2];
+        int nm[2];
+        for (int s = 0; s < 2; ++s) {
+            const size_t q = (static_cast<size_t>(r) * 2 + s) * P.stride;
+            const size_t n = static_cast<size_t>(P.N[s]);
+            if (n == 0) continue;
+            CKE(cudaMemcpyAsync(a.data(), P.d_active + q, n, cudaMemcpyDeviceToHost, st));
+            CKE(cudaMemcpyAsync(c.data(), P.d_cell + q, n * 4, cudaMemcpyDeviceToHost, st));
+            CKE(cudaMemcpyAsync(ag.data(), P.d_age + q, n * 4, cudaMemcpyDeviceToHost, st));
+            CKE(cudaMemcpyAsync(dump->energy[s], P.d_energy + q, n * 8, cudaMemcpyDeviceToHost, st));
+            CKE(cudaMemcpyAsync(dump->ids[s], P.ids + q, n * 8, cudaMemcpyDeviceToHost, st));
+            CKE(cudaStreamSynchronize(st));
+            for (size_t i = 0; i < n; ++i) {
+                dump->active[s][i] = a[i];
+                dump->ages[s][i] = ag[i];
+                dump->x[s][i] = c[i] % P.W;
+                dump->y[s][i] = c[i] / P.W;
+            }
+        }
+        CKE(cudaMemcpyAsync(nx, P.d_next + 2 * r, 16, cudaMemcpyDeviceToHost, st));
+        CKE(cudaMemcpyAsync(nm, P.d_num + 2 * r, 8, cudaMemcpyDeviceToHost, st));
+        CKE(cudaMemcpyAsync(gg.data(), P.d_g + static_cast<size_t>(r) * P.Cpad, P.Cpad, cudaMemcpyDeviceToHost, st));
+        CKE(cudaStreamSynchronize(st));
+        for (int s = 0; s < 2; ++s) {
+            dump->next_id[s] = nx[s];
+            dump->num_active[s] = nm[s];
+        }
+        for (int cc = 0; cc < P.C; ++cc) {
+            dump->grass_ready[cc] = gg[cc] == 0;
+            dump->regrow[cc] = gg[cc] == 255 ? (cfg.regrow_delay <= 0 ? cfg.regrow_delay : 0) : gg[cc];
+        }
+    }
+    CKE(cudaStreamSynchronize(st));
+    CKE(cudaEventElapsedTime(&ms, ea, eb));
+    if (kernel_ms) *kernel_ms = ms;
+done:
+    if (st) {
+        if (dseeds) cudaFreeAsync(dseeds, st);
+        if (dids) cudaFreeAsync(dids, st);
+        if (dmet) cudaFreeAsync(dmet, st);
+        if (ddump) cudaFreeAsync(ddump, st);
+        cudaStreamSynchronize(st);
+        cudaStreamDestroy(st);
+    }
+    if (ea) cudaEventDestroy(ea);
+    if (eb) cudaEventDestroy(eb);
+    return rc;
+}
+
+}  // namespace abmx_ens

@@ -1,0 +1,131 @@
+// predation_engine.h — device data layout and the host-side engine object for the
+// predation step (internal; the public surface is include/abmx_cuda.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "../../include/abmx_cuda.h"
+
+namespace abmx_pred {
+
+constexpr int kT = 256;         // threads per slot-tile CTA
+constexpr int kS = 8;           // slots per thread
+constexpr int kTile = kT * kS;  // slots per tile
+constexpr int kNumKernels = 4;
+
+// Device control block: step bookkeeping shared by the four kernels of a step.
+struct Ctl {
+    unsigned long long epoch;  // internal step counter (>= 1) stamping the per-cell lists
+    long long t;               // the reference's step index t fed to the RNG streams
+    unsigned k1_ticket, k1_wolves_done, k3_ticket, wcell_count;
+    unsigned pool_top, k4_done, needs_blend, error;
+    unsigned run_step, metrics_stride;
+    long long* metrics;  // [R][metrics_stride][4]
+};
+
+// Per (replica, species) persistent counters + this step's spawn plan.
+struct SpeciesRep {
+    int num_active;
+    int pad;
+    long long next_id;
+    long long base_id;  // first fresh id of this step's births
+    int pairs;          // min(free, valid)
+    int Q;              // valid rows
+};
+
+// Per replica, per parity event accumulators (PredationEvents, predation.hpp:41-57).
+// Energies are exact fixed-point multiples of 2^-20.
+struct Events {
+    unsigned long long grass_eaten, sheep_eaten;
+    unsigned long long metabolized[2], deaths[2], births[2], dropped[2];
+    long long e_removed_fx[2], e_dropped_fx[2];
+};
+
+struct Params {
+    int R, W, H, Cpad;
+    long long C;
+    int N[2], Npad[2], tiles[2];
+    double gain[2], metab, prob[2], frac;
+    unsigned delay_code;
+    int spawn_cps, spawn_ctas, regrow_ctas, k2_ctas, status_stride;
+    const unsigned long long* seeds;
+    uint8_t* active[2];
+    int* cell[2];
+    int* age[2];
+    double* energy[2];
+    long long* id[2];
+    int* next[2];
+    uint8_t* flag[2];
+    int* free_at[2];
+    int* row_at[2];
+    int* rowcell[2];
+    double* rowE[2];
+    unsigned long long* head[2];
+    uint8_t* g;
+    unsigned long long* smin;
+    unsigned long long* status;
+    unsigned long long* wcells;
+    int* pool;
+    long long pool_size;
+    Ctl* ctl;
+    SpeciesRep* rep;
+    Events* ev;
+};
+
+const char* kernel_name(int k);
+
+struct Engine {
+    abmx_predation_config cfg{};
+    int R = 0;
+    Params params{};
+    cudaStream_t stream = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    std::vector<void*> allocs;
+    long long device_bytes = 0;
+    unsigned long long* d_seeds = nullptr;
+    long long* d_metrics_step = nullptr;   // [R][1][4]
+    long long* d_run_metrics = nullptr;    // [R][steps][4]
+    size_t run_metrics_bytes = 0;
+    long long* cur_metrics = nullptr;      // target currently installed in ctl
+    unsigned cur_stride = 0;
+    long long last_run_steps = 0;
+    long long next_t = 1;                  // the t the device will use next
+    unsigned long long host_epoch = 1;     // mirrors ctl->epoch
+    long long staged_t = 0;
+    long long* staged_ptr = nullptr;
+    unsigned staged_u[2] = {0, 0};
+    bool timing = false;
+    cudaEvent_t tev[2 * kNumKernels] = {};
+    double kernel_ms[kNumKernels] = {};
+    long long kernel_launches[kNumKernels] = {};
+
+    ~Engine();
+    int create(const abmx_predation_config& c, const uint64_t* seeds, int replicas);
+    int step(long long t);
+    int run_async(long long t0, long long steps);           // metrics -> d_run_metrics
+    int fetch_run_metrics(double* out);                     // [R][last_run_steps][4]
+    int last_metrics(long long* out);                       // [R][4] of the last step
+    int last_events(abmx_predation_events* out);
+    int export_species(int r, int s, uint8_t* active, int64_t* ids, int64_t* types, int64_t* ages,
+                       int64_t* x, int64_t* y, double* energy, int32_t* num_active, int64_t* next_id);
+    int import_species(int r, int s, const uint8_t* active, const int64_t* ids, const int64_t* ages,
+                       const int64_t* x, const int64_t* y, const double* energy, int32_t num_active,
+                       int64_t next_id);
+    int export_world(int r, uint8_t* ready, int64_t* regrow);
+    int import_world(int r, const uint8_t* ready, const int64_t* regrow);
+    int birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t cap);
+
+    // internals
+    int alloc(void** p, size_t bytes);
+    int set_t(long long t);
+    int set_metrics_target(long long* d_metrics, unsigned stride);
+    void launch_step_kernels(bool timed);
+    int launch_steps(long long steps);
+    int accumulate_times();
+};
+
+}  // namespace abmx_pred

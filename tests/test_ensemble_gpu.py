@@ -1,0 +1,56 @@
+"""Ensemble runner (run_batch) on the B200: SMEM-resident CTA-per-replica kernel and the
+batched HBM engine vs the oracle's run_batch, bitwise on every metrics row."""
+import numpy as np
+import pytest
+
+from helpers import c1, tiny
+
+pytestmark = pytest.mark.gpu
+
+
+def test_smem_path_fits_c1(abmx):
+    assert abmx.smem_fits(abmx.PredationConfig(**c1()))
+
+
+@pytest.mark.parametrize("path", [1, 2])
+def test_c1_ensemble_matches_oracle(abmx, oracle, path):
+    K, T = 24, 100
+    got, ms = abmx.run_batch(abmx.PredationConfig(**c1()), 7, K, T, path=path)
+    want = oracle.run_batch(c1(), 7, K, T)
+    assert np.array_equal(got, want)
+    assert ms > 0
+
+
+def test_c1_ensemble_matches_reference_run_batch(abmx, reference):
+    K, T = 16, 50
+    got, _ = abmx.run_batch(abmx.PredationConfig(**c1()), 99, K, T)
+    want, _ = reference.run_batch(c1(), 99, K, T, threads=4)
+    assert np.array_equal(got, want)
+
+
+def test_replica_offsets_shard_cleanly(abmx, oracle):
+    """Replica r's seed depends only on (master, r): shards [0,8) + [8,16) == [0,16)."""
+    cfg = abmx.PredationConfig(**c1())
+    full, _ = abmx.run_batch(cfg, 5, 16, 30)
+    a, _ = abmx.run_batch(cfg, 5, 8, 30, begin=0)
+    b, _ = abmx.run_batch(cfg, 5, 8, 30, begin=8)
+    assert np.array_equal(np.concatenate([a, b]), full)
+
+
+@pytest.mark.parametrize("cfgd", [
+    tiny(), tiny(width=1, height=1, n_sheep0=2, n_wolves0=3), tiny(regrow_delay=0),
+    tiny(n_sheep0=8, sheep_capacity=8, reproduce_prob_sheep=1.0),
+    c1(sheep_capacity=2000, wolf_capacity=600),
+    c1(width=30, height=7, n_sheep0=200, n_wolves0=150, sheep_capacity=3000, wolf_capacity=4000),
+])
+def test_smem_path_edge_configs(abmx, oracle, cfgd):
+    got, _ = abmx.run_batch(abmx.PredationConfig(**cfgd), 11, 6, 40, path=1)
+    want = oracle.run_batch(cfgd, 11, 6, 40)
+    assert np.array_equal(got, want)
+
+
+def test_run_batch_errors(abmx):
+    with pytest.raises(abmx.BatchError):
+        abmx.run_batch(abmx.PredationConfig(**c1()), 1, 0, 5)
+    with pytest.raises(abmx.DomainError):
+        abmx.run_batch(abmx.PredationConfig(**c1()), 1, 2, 0)

@@ -1,0 +1,219 @@
+"""Predation step on the B200 vs the CPU oracle: bit-exact state after every step.
+
+Mirrors tests/test_predation.cpp and the survey's C1/C2 parity runs."""
+import numpy as np
+import pytest
+
+from helpers import c1, species_equal, state_hash, tiny
+import pyoracle
+
+pytestmark = pytest.mark.gpu
+
+
+def make_pair(abmx, oracle, cfgd, seed):
+    cfg = abmx.PredationConfig(**cfgd)
+    return abmx.PredationModel(cfg, seed), oracle.pred(cfgd, seed)
+
+
+def assert_same_state(gpu, orc, what):
+    for s in (0, 1):
+        species_equal(gpu.export_species(s), orc.export_species(s), f"{what} species {s}")
+    gr, gg = gpu.export_world()
+    orr, org = orc.export_world()
+    assert np.array_equal(gr, orr), what
+    assert np.array_equal(gg, org), what
+
+
+def assert_same_events(ge, oe, what):
+    assert ge.grass_eaten == oe["grass_eaten"], what
+    assert ge.sheep_eaten_by_wolves == oe["sheep_eaten_by_wolves"], what
+    for name in ("sheep", "wolves"):
+        g, o = getattr(ge, name), oe[name]
+        for k in ("metabolized", "deaths", "births", "births_dropped"):
+            assert getattr(g, k) == o[k], (what, name, k, getattr(g, k), o[k])
+        for k in ("energy_removed_deaths", "energy_dropped_births"):
+            assert getattr(g, k) == o[k], (what, name, k, getattr(g, k), o[k])
+
+
+def test_init_matches_oracle(abmx, oracle):
+    seed = abmx.replica_seeds(7, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, c1(), seed)
+    assert_same_state(gpu, orc, "init")
+    assert state_hash(gpu) == orc.hash(True)
+
+
+def test_c1_trajectory_bitexact_every_step(abmx, oracle):
+    seed = abmx.replica_seeds(7, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, c1(), seed)
+    for t in range(1, 101):
+        gpu.step(t)
+        oe = orc.step(t)
+        m = gpu.collect_metrics()[0].tolist()
+        assert m == orc.metrics(), (t, m, orc.metrics())
+        assert_same_events(gpu.last_events(), oe, f"t={t}")
+        if t % 10 == 0 or t < 5:
+            assert_same_state(gpu, orc, f"t={t}")
+    # SURVEY §8c known answers at t=100
+    assert gpu.collect_metrics()[0].tolist()[:3] == [715, 61, 4613]
+
+
+def test_c1_run_metrics_match_survey_known_answers(abmx):
+    seed = abmx.replica_seeds(7, 1)[0]
+    gpu = abmx.PredationModel(abmx.PredationConfig(**c1()), seed)
+    m = gpu.run(1, 100)[0]
+    for t, want in ((1, (589, 408, 9414)), (2, (591, 422, 8884)), (3, (589, 433, 8447)),
+                    (50, (429, 203, 5891)), (100, (715, 61, 4613))):
+        assert tuple(int(v) for v in m[t - 1, :3]) == want, t
+
+
+def test_run_equals_step_loop(abmx):
+    cfg = abmx.PredationConfig(**tiny())
+    a = abmx.PredationModel(cfg, 10)
+    b = abmx.PredationModel(cfg, 10)
+    ma = a.run(1, 40)[0]
+    for t in range(1, 41):
+        b.step(t)
+        assert b.collect_metrics()[0].tolist() == ma[t - 1].astype(np.int64).tolist()
+    assert state_hash(a) == state_hash(b)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 10, 12, 99])
+def test_tiny_configs_bitexact(abmx, oracle, seed):
+    gpu, orc = make_pair(abmx, oracle, tiny(), seed)
+    for t in range(1, 41):
+        gpu.step(t)
+        oe = orc.step(t)
+        assert_same_events(gpu.last_events(), oe, f"seed {seed} t={t}")
+        assert_same_state(gpu, orc, f"seed {seed} t={t}")
+
+
+def test_birth_pairs_match_reference(abmx, reference):
+    cfgd = tiny(reproduce_prob_sheep=0.9, reproduce_prob_wolf=0.9)
+    gpu = abmx.PredationModel(abmx.PredationConfig(**cfgd), 8)
+    ref = reference.pred(cfgd, 8)
+    for t in range(1, 7):
+        gpu.step(t)
+        ref.step(t)
+        for s in (0, 1):
+            assert gpu.birth_pairs(s) == ref.birth_pairs(s), (t, s)
+            st = gpu.export_species(s)
+            for parent, child in gpu.birth_pairs(s):
+                assert st["x"][child] == st["x"][parent] and st["y"][child] == st["y"][parent]
+                assert st["ages"][child] == 0
+
+
+@pytest.mark.parametrize("case", ["one_cell_two_sheep", "wolf_and_sheep", "two_wolves_one_sheep",
+                                  "overflow", "starve", "regrow_zero", "regrow_negative",
+                                  "crowded_cell"])
+def test_unit_cases_vs_reference(abmx, reference, case):
+    """tests/test_predation.cpp:89-224 setups, compared field-by-field with the reference."""
+    cfgd = tiny()
+    seed = 5
+    if case == "one_cell_two_sheep":
+        cfgd = tiny(width=1, height=1, n_sheep0=2, n_wolves0=0, reproduce_prob_sheep=0.0)
+    elif case == "wolf_and_sheep":
+        cfgd = tiny(width=1, height=1, n_sheep0=1, n_wolves0=1, reproduce_prob_sheep=0.0,
+                    reproduce_prob_wolf=0.0)
+    elif case == "two_wolves_one_sheep":
+        cfgd = tiny(width=1, height=1, n_sheep0=1, n_wolves0=2, reproduce_prob_wolf=0.0)
+    elif case == "overflow":
+        cfgd = tiny(n_sheep0=8, sheep_capacity=8, n_wolves0=0, reproduce_prob_sheep=1.0)
+    elif case == "starve":
+        cfgd = tiny(n_sheep0=1, n_wolves0=0, metabolism=2.0)
+    elif case == "regrow_zero":
+        cfgd = tiny(regrow_delay=0)
+    elif case == "regrow_negative":
+        cfgd = tiny(regrow_delay=-3)
+    elif case == "crowded_cell":
+        # long per-cell lists: exercises the pool + heap-sort pairing path
+        cfgd = tiny(width=2, height=1, n_sheep0=300, n_wolves0=40, sheep_capacity=400,
+                    wolf_capacity=400)
+    gpu = abmx.PredationModel(abmx.PredationConfig(**cfgd), seed)
+    ref = reference.pred(cfgd, seed)
+    if case == "overflow":
+        for m in (gpu, ref):
+            d = m.export_species(0)
+            d["energy"] = np.where(d["active"] > 0, 10.0, 0.0)
+            m.import_species(0, d)
+    if case == "starve":
+        for m in (gpu, ref):
+            d = m.export_species(0)
+            d["energy"][0] = 1.0
+            m.import_species(0, d)
+            c = cfgd["width"] * cfgd["height"]
+            m.import_world(np.zeros(c, np.uint8), np.full(c, 5, np.int64))
+    for t in range(1, 16):
+        gpu.step(t)
+        oe = ref.step(t)
+        assert_same_events(gpu.last_events(), oe, f"{case} t={t}")
+        assert_same_state(gpu, ref, f"{case} t={t}")
+
+
+def test_energy_ledger_balances_exactly(abmx):
+    """test_predation.cpp:226-239: delta(E) == eats*gain - metab - removed - dropped."""
+    cfgd = tiny()
+    gpu = abmx.PredationModel(abmx.PredationConfig(**cfgd), 10)
+    before = [gpu.export_species(s)["energy"].sum() for s in (0, 1)]
+    for t in range(1, 41):
+        gpu.step(t)
+        ev = gpu.last_events()
+        after = [gpu.export_species(s)["energy"].sum() for s in (0, 1)]
+        eats = (ev.grass_eaten, ev.sheep_eaten_by_wolves)
+        gains = (cfgd["energy_gain_sheep"], cfgd["energy_gain_wolf"])
+        for s, sp in enumerate((ev.sheep, ev.wolves)):
+            rhs = eats[s] * gains[s] - sp.metabolized * cfgd["metabolism"] - \
+                sp.energy_removed_deaths - sp.energy_dropped_births
+            assert after[s] - before[s] == rhs, (t, s)
+        before = after
+
+
+def test_capacity_invariance(abmx):
+    """C1 with caps 1024 and caps 20000 give identical trajectories."""
+    seed = abmx.replica_seeds(7, 1)[0]
+    a = abmx.PredationModel(abmx.PredationConfig(**c1()), seed).run(1, 100)
+    b = abmx.PredationModel(abmx.PredationConfig(**c1(sheep_capacity=20000, wolf_capacity=20000)),
+                            seed).run(1, 100)
+    assert np.array_equal(a, b)
+
+
+def test_batched_replicas_equal_solo_runs(abmx):
+    """test_batch.cpp:72-90: a batch of R replicas == R solo models, bitwise."""
+    cfg = abmx.PredationConfig(**tiny(width=16, height=16, sheep_capacity=600, wolf_capacity=600))
+    seeds = abmx.replica_seeds(3, 6)
+    batch = abmx.PredationModel(cfg, seeds).run(1, 15)
+    for r, s in enumerate(seeds):
+        solo = abmx.PredationModel(cfg, s).run(1, 15)[0]
+        assert np.array_equal(batch[r], solo), r
+
+
+def test_c2_scale_first_steps_bitexact(abmx, oracle):
+    """C2 (1M-slot capacity, 2048^2 cells): full state bit-exact after 3 steps."""
+    cfgd = c1(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000,
+              sheep_capacity=524288, wolf_capacity=524288)
+    seed = abmx.replica_seeds(7, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, cfgd, seed)
+    for t in range(1, 4):
+        gpu.step(t)
+        oe = orc.step(t)
+        assert gpu.collect_metrics()[0].tolist() == orc.metrics()
+        assert_same_events(gpu.last_events(), oe, f"C2 t={t}")
+    assert_same_state(gpu, orc, "C2 t=3")
+
+
+def test_import_rejects_bad_state(abmx):
+    m = abmx.PredationModel(abmx.PredationConfig(**tiny()), 1)
+    d = m.export_species(0)
+    d["num_active"] += 1
+    with pytest.raises(abmx.CapacityError):
+        m.import_species(0, d)
+    d = m.export_species(0)
+    d["x"][0] = 99
+    with pytest.raises(abmx.DomainError):
+        m.import_species(0, d)
+
+
+def test_create_errors(abmx):
+    with pytest.raises(abmx.CapacityError):
+        abmx.PredationModel(abmx.PredationConfig(**tiny(n_sheep0=500)), 1)
+    with pytest.raises(abmx.DomainError):
+        abmx.PredationModel(abmx.PredationConfig(**tiny(regrow_delay=300)), 1)

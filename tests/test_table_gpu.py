@@ -1,0 +1,137 @@
+"""KernelTable entries on the B200 vs the scalar oracle and the reference's own tables.
+
+Mirrors tests/test_simd.cpp (sizes 0..4096 with ragged tails, NaN/inf bit patterns, nonzero
+bytes as true) plus large sizes where the decoupled-lookback spans many tiles."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+SIZES = [0, 1, 3, 7, 8, 9, 15, 16, 31, 32, 33, 64, 100, 257, 1000, 4096]  # test_simd.cpp:17
+BIG = [4097, 65537, 1 << 20, (1 << 24) + 3]
+
+
+def masks(rng, n, density=0.5):
+    m = (rng.random(n) < density).astype(np.uint8)
+    # any nonzero byte is true (test_simd.cpp:136-150)
+    m[m > 0] = rng.integers(1, 256, int(m.sum()), dtype=np.uint8) if n else m[m > 0]
+    return m
+
+
+@pytest.mark.parametrize("n", SIZES + BIG)
+def test_rank_scan_count_compact(abmx, oracle, n):
+    rng = np.random.default_rng(n)
+    for density in (0.0, 0.3, 0.5, 1.0):
+        m = masks(rng, n, density)
+        assert np.array_equal(abmx.rank_scan(m), oracle.rank_scan(m)), (n, density)
+        assert abmx.count_true(m) == oracle.count_true(m)
+        assert np.array_equal(abmx.compact_indices(m), oracle.compact_indices(m)), (n, density)
+
+
+def test_literal_examples(abmx):
+    """test_kernels.cpp:48-52, 73-92."""
+    assert abmx.compute_ranks([0, 0, 0]).tolist() == [0, 0, 0]
+    assert abmx.compute_ranks([1, 0, 1, 1]).tolist() == [1, 0, 2, 3]
+    assert abmx.compute_ranks([1, 1, 1]).tolist() == [1, 2, 3]
+    r = abmx.compact_mask([0, 1, 0, 1, 1])
+    assert r.count == 3 and r.indices.tolist() == [1, 3, 4, 0, 2]
+
+
+def test_nonzero_bytes_count_as_true(abmx, oracle):
+    m = np.array([0, 1, 2, 0, 255, 128, 0, 7] * 4 + [9], np.uint8)
+    assert abmx.count_true(m) == 21
+    assert np.array_equal(abmx.rank_scan(m), oracle.rank_scan(m))
+
+
+@pytest.mark.parametrize("n,m", [(n, m) for n in (0, 1, 9, 33, 100, 3000) for m in (0, 1, 8, 31, 100, 3000)])
+def test_match_first_equal_ranks(abmx, oracle, n, m):
+    rng = np.random.default_rng(n * 7919 + m)
+    ra = oracle.rank_scan(masks(rng, n))
+    rb = oracle.rank_scan(masks(rng, m))
+    assert np.array_equal(abmx.match_first_equal(ra, rb), oracle.match_first_equal(ra, rb))
+
+
+@pytest.mark.parametrize("spread", [10, 1 << 30])
+def test_match_first_equal_arbitrary_ints(abmx, oracle, spread):
+    """Non-rank inputs with duplicates: FIRST match wins (dense and hash table paths)."""
+    rng = np.random.default_rng(spread)
+    rb = rng.integers(-spread, spread, 777).astype(np.int32)
+    ra = np.concatenate([rb[rng.integers(0, 777, 300)], rng.integers(-spread, spread, 300)]).astype(np.int32)
+    ra[::17] = 0
+    assert np.array_equal(abmx.match_first_equal(ra, rb), oracle.match_first_equal(ra, rb))
+
+
+@pytest.mark.parametrize("n", SIZES + [4097, 100003])
+def test_blends_bit_patterns(abmx, oracle, n):
+    rng = np.random.default_rng(n + 5)
+    m = masks(rng, n)
+    ia = rng.integers(-2**63, 2**63 - 1, n, dtype=np.int64)
+    ib = rng.integers(-2**63, 2**63 - 1, n, dtype=np.int64)
+    fa = rng.uniform(-1, 1, n)
+    fa[rng.integers(0, 4, n) == 0] = np.nan
+    fa[rng.integers(0, 4, n) == 1] = np.inf
+    fb = rng.uniform(-1, 1, n)
+    ba = rng.integers(0, 256, n, dtype=np.uint8)
+    bb = rng.integers(0, 256, n, dtype=np.uint8)
+    assert np.array_equal(abmx.blend_i64(m, ia, ib), oracle.blend("i64", m, ia, ib))
+    assert np.array_equal(abmx.blend_f64(m, fa, fb).view(np.uint64),
+                          oracle.blend("f64", m, fa, fb).view(np.uint64))
+    assert np.array_equal(abmx.blend_u8(m, ba, bb), oracle.blend("u8", m, ba, bb))
+
+
+def test_blend_out_aliases_input(abmx, oracle):
+    """lifecycle.cpp:105-111 passes the same column as `a` and `out`."""
+    rng = np.random.default_rng(3)
+    n = 5000
+    m = masks(rng, n)
+    a = rng.integers(-100, 100, n, dtype=np.int64)
+    want = oracle.blend("i64", m, a, np.zeros(n, np.int64))
+    abmx.blend_i64(m, a, np.zeros(n, np.int64), out=a)
+    assert np.array_equal(a, want)
+
+
+def test_table_struct_matches_reference_tables(abmx, reference):
+    """The "cuda" KernelTable is layout-compatible with the reference's scalar/avx2 tables
+    and agrees with them entry by entry when called through its function pointers."""
+    t = abmx.kernel_table()
+    assert t.name == b"cuda"
+    u8p, i32p = C.POINTER(C.c_uint8), C.POINTER(C.c_int32)
+    rank = C.CFUNCTYPE(None, u8p, i32p, C.c_size_t)(t.rank_scan)
+    count = C.CFUNCTYPE(C.c_int64, u8p, C.c_size_t)(t.count_true)
+    rng = np.random.default_rng(11)
+    for backend in (0, 1):
+        tab = reference.table(backend)
+        if tab is None:
+            continue
+        for n in SIZES + [12345]:
+            m = masks(rng, n)
+            a = np.empty(n, np.int32)
+            b = np.empty(n, np.int32)
+            rank(m.ctypes.data_as(u8p), a.ctypes.data_as(i32p), n)
+            tab.struct.rank_scan(m.ctypes.data_as(u8p), b.ctypes.data_as(i32p), n)
+            assert np.array_equal(a, b)
+            assert count(m.ctypes.data_as(u8p), n) == tab.struct.count_true(m.ctypes.data_as(u8p), n)
+
+
+def test_device_pointer_variants_unaligned(abmx, oracle):
+    """The *_async entries on device pointers, including misaligned (odd-offset) buffers."""
+    import torch
+    rng = np.random.default_rng(9)
+    n = 300001
+    host = masks(rng, n + 1)
+    d = torch.from_numpy(host).cuda()
+    out = torch.empty(n + 1, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+    lib = abmx.lib
+    rc = lib.abmx_cuda_rank_scan_async(C.c_void_p(d.data_ptr() + 1), C.c_void_p(out.data_ptr() + 4),
+                                       C.c_size_t(n), C.c_void_p(s))
+    assert rc == 0
+    rc = lib.abmx_cuda_count_true_async(C.c_void_p(d.data_ptr() + 1), C.c_size_t(n),
+                                        C.c_void_p(cnt.data_ptr()), C.c_void_p(s))
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy()[1:], oracle.rank_scan(host[1:]))
+    assert int(cnt.item()) == oracle.count_true(host[1:])
