@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""bench.py — predation hot path on B200: agent-steps/sec and % of the HBM roofline.
+
+Workload (BASELINE.json configs[1], SURVEY §8d "C2"): ONE predation model at 1M-agent
+capacity per GPU — 2048 x 2048 cells, 300,000 sheep + 30,000 wolves initially, capacities
+524,288 + 524,288 — heavy birth/death churn every step. A "step" is one full
+step_predation (move, graze, predation, metabolise, starve, reproduce + spawn, regrow).
+Under torchrun each rank runs its own replica (seed master.split(2).split(rank)): weak
+scaling, no data-path collective; the per-rank summary rows are gathered with NCCL.
+The line also carries the C3 ensemble (4096 x C1 replicas, sharded over the ranks).
+
+  value      capacity slot-steps/s over all ranks, device-timed (CUDA events per step,
+             L2 flushed by an untimed 256 MiB write before every timed step), max over ranks
+  e2e        the same metric through the C-ABI call a user makes: abmx_predation_step(t)
+             (H2D of t) + abmx_predation_metrics (D2H of the metrics row), host wall clock
+  roofline   dominant kernel: SURVEY §8d algorithmic bytes apportioned to that kernel
+             / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline  the reference's own C++ step_predation (oracle/_ref, -O3) on this host
+
+`--impl reference` times the reference CPU implementation (oracle/_ref) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MASTER_SEED = 7
+C2 = dict(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000, sheep_capacity=524288,
+          wolf_capacity=524288, energy_gain_sheep=4.0, energy_gain_wolf=20.0, metabolism=1.0,
+          reproduce_prob_sheep=0.04, reproduce_prob_wolf=0.05, reproduce_energy_frac=0.5,
+          regrow_delay=30)
+C1 = dict(C2, width=100, height=100, n_sheep0=600, n_wolves0=400, sheep_capacity=1024,
+          wolf_capacity=1024)
+ENSEMBLE_REPLICAS = 4096
+ENSEMBLE_STEPS = 100
+FLUSH_BYTES = 256 << 20  # > 126 MB L2
+METRIC = "agent-steps/sec"
+UNIT = "slot-steps/s"
+WORKLOAD = ("C2 predation: 2048x2048 cells, 300k sheep + 30k wolves, capacity 524288 + 524288 "
+            "(1,048,576 slots) per GPU; one model per rank")
+
+
+def capacity(cfg):
+    return cfg["sheep_capacity"] + cfg["wolf_capacity"]
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = str(gpu_index)
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", self.gpu, f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        time.sleep(0.2)
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower() in ("active", "1"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------- reference arm
+def reference_arm(args, world):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified abmx sources,
+    -O3) on this host, same metric/config; rank 0 only."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle
+    if not os.path.exists(pyoracle.REF_SO):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libabmx_ref.so not built"}))
+        return
+    ref = pyoracle.Reference()
+    cores = os.cpu_count() or 1
+    K, W = args.steps, args.warmup
+    if world == 1:
+        # one model: the reference steps a single model on one thread by design
+        seed = ref.replica_seed(MASTER_SEED, 0)
+        m = ref.pred(C2, seed)
+        m.run(1, W)
+        ms = m.run(W + 1, K)
+        threads = 1
+        sample = f"C2 model, steps {W + 1}..{W + K} after {W} warm-up steps, 1 thread"
+    else:
+        # N replicas (one per rank in our arm) on run_batch threads; warmup-subtraction protocol
+        threads = min(world, cores)
+        _, a = ref.run_batch(C2, MASTER_SEED, world, W + K, threads=threads)
+        _, b = ref.run_batch(C2, MASTER_SEED, world, W, threads=threads)
+        ms = a - b
+        sample = (f"{world} C2 replicas via run_batch on {threads} threads, wall({W + K} steps) - "
+                  f"wall({W} steps)")
+    value = world * capacity(C2) * K / (ms / 1e3)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64+int", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "replicas": world},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------- our arm
+def kernel_bytes(cfg, births_deaths):
+    """SURVEY §8d algorithmic bytes per step, B = 42*N_tot + 2*C + 8*(births+deaths),
+    apportioned to the kernel that owns each column."""
+    n = capacity(cfg)
+    cells = cfg["width"] * cfg["height"]
+    return {"k_move": 25 * n,            # x,y,age read+write (2*(4+4+4)) + active read (1)
+            "k_predation": 0,            # scratch only (per-cell lists), not counted by §8d
+            "k_update": 17 * n,          # energy read+write (2*8) + active write (1)
+            "k_spawn_regrow": 2 * cells + 8 * births_deaths}
+
+
+def our_arm(args, rank, world, local_rank, dist):
+    import numpy as np
+    import torch
+    import paper_2508_16508_b200 as abmx
+
+    torch.cuda.set_device(local_rank)
+    K, W = args.steps, args.warmup
+    cfg = abmx.PredationConfig(**C2)
+    seed = abmx.replica_seeds(MASTER_SEED, world)[rank]
+    model = abmx.PredationModel(cfg, seed)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def allreduce(x, op):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    # warm-up (also builds and instantiates the CUDA graph)
+    model.bench(1, W, FLUSH_BYTES)
+    t_next = W + 1
+    barrier()
+    launches0 = abmx.launch_count()
+    with ClockSampler(local_rank) as clk:
+        step_ms, met = model.bench(t_next, K, FLUSH_BYTES)
+    launches = abmx.launch_count() - launches0
+    t_next += K
+    barrier()
+    total_ms = float(np.sum(step_ms))
+    max_ms = allreduce(total_ms, dist.ReduceOp.MAX if dist else None)
+    live = float(met[0, :, 0].sum() + met[0, :, 1].sum())
+    live_all = allreduce(live, dist.ReduceOp.SUM if dist else None)
+    value = world * capacity(C2) * K / (max_ms / 1e3)
+
+    # per-kernel durations (events around each kernel, graph off) for the roofline
+    model.set_timing(True)
+    model.set_timing(False)
+    kt_steps = max(3, min(K, 10))
+    model.bench(t_next, kt_steps, FLUSH_BYTES, per_kernel=True)
+    t_next += kt_steps
+    times = model.kernel_times()
+    ev = model.last_events()
+    bd = ev.sheep.births + ev.wolves.births + ev.sheep.deaths + ev.wolves.deaths
+    kb = kernel_bytes(C2, bd)
+    avg = {k: ms / max(n, 1) for k, (ms, n) in times.items()}
+    step_sum = sum(avg.values())
+    dom = max(avg, key=avg.get)
+    peak, peak_src = hbm_peak()
+    achieved = kb[dom] / (avg[dom] / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    step_bytes = 42 * capacity(C2) + 2 * C2["width"] * C2["height"] + 8 * bd
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                "algorithmic_bytes": kb[dom], "avg_launch_ms": avg[dom],
+                "kernel_share": avg[dom] / step_sum,
+                "per_kernel_ms": avg,
+                "step_effective_gbs": step_bytes / (total_ms / K / 1e3) / 1e9}
+
+    # e2e through the C-ABI: step(t) [H2D t] + collect_metrics [D2H row], L2 flushed between
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    e2e_s = 0.0
+    for q in range(K):
+        flush.fill_(q)
+        torch.cuda.synchronize()
+        a = time.perf_counter()
+        model.step(t_next)
+        model.collect_metrics()
+        e2e_s += time.perf_counter() - a
+        t_next += 1
+    e2e_max = allreduce(e2e_s, dist.ReduceOp.MAX if dist else None)
+    e2e = {"value": world * capacity(C2) * K / e2e_max, "unit": UNIT, "h2d_bytes_per_step": 8,
+           "d2h_bytes_per_step": 32}
+    del flush
+    model.close()
+
+    # C3 ensemble, sharded by contiguous replica blocks; NCCL gathers the metrics rows
+    ens = None
+    if not args.no_ensemble:
+        per = ENSEMBLE_REPLICAS // world
+        begin = rank * per
+        count = per if rank < world - 1 else ENSEMBLE_REPLICAS - begin
+        c1 = abmx.PredationConfig(**C1)
+        abmx.run_batch(c1, MASTER_SEED, min(count, 296), 5, begin=begin, path=1)  # warm-up
+        barrier()
+        rows, kms = abmx.run_batch(c1, MASTER_SEED, count, ENSEMBLE_STEPS, begin=begin, path=1)
+        kmax = allreduce(kms, dist.ReduceOp.MAX if dist else None)
+        gathered = ENSEMBLE_REPLICAS
+        if dist is not None:
+            t = torch.from_numpy(rows).cuda()
+            sizes = [ENSEMBLE_REPLICAS // world] * (world - 1)
+            sizes.append(ENSEMBLE_REPLICAS - sum(sizes))
+            bufs = [torch.empty((s, ENSEMBLE_STEPS, 4), dtype=torch.float64, device="cuda")
+                    for s in sizes]
+            if t.shape[0] != sizes[rank]:
+                raise RuntimeError("shard size mismatch")
+            # all_gather needs equal sizes: pad to the largest shard
+            mx = max(sizes)
+            pad = torch.zeros((mx, ENSEMBLE_STEPS, 4), dtype=torch.float64, device="cuda")
+            pad[: t.shape[0]] = t
+            outs = [torch.empty_like(pad) for _ in range(world)]
+            dist.all_gather(outs, pad)
+            gathered = sum(o[:s].shape[0] for o, s in zip(outs, sizes))
+            del bufs
+        slots = ENSEMBLE_REPLICAS * capacity(C1) * ENSEMBLE_STEPS
+        c3_bytes = ENSEMBLE_REPLICAS * ENSEMBLE_STEPS * (42 * capacity(C1) + 2 * 100 * 100)
+        ens = {"workload": "C3: 4096 x C1 replicas (100x100, 600+400, caps 1024+1024), 100 steps, "
+                           "SMEM/register-resident CTA per replica",
+               "value": slots / (kmax / 1e3), "unit": UNIT, "kernel_ms": kmax,
+               "replicas_gathered": gathered, "scaling": "strong",
+               "effective_gbs": c3_bytes / (kmax / 1e3) / 1e9,
+               "note": "state stays on chip for all steps; effective GB/s uses SURVEY §8d bytes "
+                       "and may exceed HBM peak"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+        if os.path.exists(pyoracle.REF_SO):
+            ref = pyoracle.Reference()
+            m = ref.pred(C2, abmx.replica_seeds(MASTER_SEED, 1)[0])
+            m.run(1, 2)
+            n_cpu = args.cpu_steps
+            ms = m.run(3, n_cpu)
+            cpu = {"value": capacity(C2) * n_cpu / (ms / 1e3), "unit": UNIT, "cores": 1,
+                   "kind": "reference",
+                   "sample": f"reference step_predation (oracle/_ref, -O3), C2 steps 3..{2 + n_cpu}, "
+                             f"1 thread ({ms / 1e3:.1f} s)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+                "warmup": W, "ms_per_step": max_ms / K, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64+int", "data": "synthetic",
+                "config": {"workload": WORKLOAD, "replicas_per_gpu": 1, "seed": MASTER_SEED,
+                           "l2": "flushed before every timed step (untimed 256 MiB write)",
+                           "timing": "CUDA events per step on the engine stream; max over ranks"},
+                "live_agent_steps_per_s": live_all / (max_ms / 1e3),
+                "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+                "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens}
+        print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-steps", type=int, default=40)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ensemble", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rules: >= 3 warm-up steps
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args, world)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as D
+        torch.cuda.set_device(local_rank)
+        D.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = D
+    try:
+        our_arm(args, rank, world, local_rank, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

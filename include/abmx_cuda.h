@@ -155,6 +155,14 @@ const char* abmx_predation_kernel_name(int32_t k);
 int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches);
 /* device-resident bytes of h (state + scratch) */
 int64_t abmx_predation_device_bytes(abmx_predation* h);
+/* Device-timed steps t0..t0+steps-1 for benchmarking: before each step an (untimed) write
+ * of flush_bytes evicts L2; CUDA events on h's stream bracket each step (per_kernel = 0,
+ * CUDA-graph launch) or each kernel (per_kernel = 1, also accumulates kernel_times).
+ * step_ms[steps] receives the device milliseconds of every step. Metrics of these steps
+ * are then readable with abmx_predation_fetch_metrics ([replicas][steps][4]). */
+int abmx_predation_bench(abmx_predation* h, int64_t t0, int64_t steps, int64_t flush_bytes,
+                         int32_t per_kernel, double* step_ms);
+int abmx_predation_fetch_metrics(abmx_predation* h, double* out);
 
 /* ======================================================================= ensemble
  * run_batch (batch.cpp:21-101) for replicas [replica_begin, replica_begin+count) of

@@ -186,6 +186,9 @@ _sig("abmx_predation_kernel_count", C.c_int32, [])
 _sig("abmx_predation_kernel_name", C.c_char_p, [C.c_int32])
 _sig("abmx_predation_kernel_times", C.c_int, [C.c_void_p, f64p, i64p])
 _sig("abmx_predation_device_bytes", C.c_int64, [C.c_void_p])
+_sig("abmx_predation_bench", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int32,
+                                       f64p])
+_sig("abmx_predation_fetch_metrics", C.c_int, [C.c_void_p, f64p])
 _sig("abmx_ensemble_run", C.c_int, [C.POINTER(PredationConfig), C.c_uint64, C.c_int32, C.c_int32,
                                     C.c_int64, C.c_int32, f64p, f64p])
 _sig("abmx_ensemble_smem_fits", C.c_int, [C.POINTER(PredationConfig)])
@@ -431,6 +434,17 @@ class PredationModel:
         r = _mask(ready)
         g = np.ascontiguousarray(regrow, dtype=np.int64)
         _check(lib.abmx_predation_import_world(self._h, replica, _p(r, u8p), _p(g, i64p)))
+
+    def bench(self, t0: int, steps: int, flush_bytes: int = 256 << 20, per_kernel: bool = False):
+        """Device-timed steps (CUDA events per step, L2 flushed between steps, untimed).
+        Returns (step_ms [steps], metrics [replicas, steps, 4])."""
+        ms = np.empty(steps, np.float64)
+        _check(lib.abmx_predation_bench(self._h, t0, steps, flush_bytes, 1 if per_kernel else 0,
+                                        _p(ms, f64p)))
+        met = np.empty((self.replicas, steps, 4), np.float64)
+        _check(lib.abmx_predation_fetch_metrics(self._h, _p(met, f64p)))
+        self._last_t = t0 + steps - 1
+        return ms, met
 
     # -- per-kernel timing (CUDA events around each launch; disables the CUDA graph)
     def set_timing(self, on: bool):

@@ -322,6 +322,19 @@ int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches
     return ABMX_OK;
 }
 int64_t abmx_predation_device_bytes(abmx_predation* h) { return h ? h->eng.device_bytes : 0; }
+int abmx_predation_bench(abmx_predation* h, int64_t t0, int64_t steps, int64_t flush_bytes, int32_t per_kernel,
+                         double* step_ms) {
+    HANDLE(h);
+    if (!step_ms || flush_bytes < 0) {
+        set_error("step_ms required; flush_bytes >= 0");
+        return ABMX_E_ARG;
+    }
+    return h->eng.bench(t0, steps, static_cast<size_t>(flush_bytes), per_kernel != 0, step_ms);
+}
+int abmx_predation_fetch_metrics(abmx_predation* h, double* out) {
+    HANDLE(h);
+    return h->eng.fetch_run_metrics(out);
+}
 
 // ---------------------------------------------------------------- ensemble
 int abmx_ensemble_smem_fits(const abmx_predation_config* cfg) {

@@ -640,6 +640,7 @@ Engine::~Engine() {
         if (ev) cudaEventDestroy(ev);
     for (void* p : allocs) cudaFree(p);
     if (d_run_metrics) cudaFree(d_run_metrics);
+    if (flush_buf) cudaFree(flush_buf);
     if (stream) cudaStreamDestroy(stream);
 }
 
@@ -876,8 +877,11 @@ int Engine::launch_steps(long long steps) {
 }
 
 int Engine::step(long long t) {
-    int rc = set_t(t);
-    if (rc) return rc;
+    // the step index is this call's only input: always ship it (8 B H2D), then launch
+    staged_t = t;
+    CK(cudaMemcpyAsync(&params.ctl->t, &staged_t, sizeof(long long), cudaMemcpyHostToDevice, stream));
+    next_t = t;
+    int rc = ABMX_OK;
     CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
     rc = set_metrics_target(d_metrics_step, 1);
     if (rc) return rc;
@@ -1088,6 +1092,61 @@ int Engine::birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t c
         CK(cudaStreamSynchronize(stream));
     }
     return sr.pairs;
+}
+
+// L2 flush: overwrite a buffer larger than the 126 MB L2 between timed steps.
+__global__ void k_flush(uint4* p, size_t n) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = make_uint4(static_cast<unsigned>(i), 0u, 0u, 0u);
+}
+
+int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_kernel, double* step_ms) {
+    if (steps <= 0) return ABMX_OK;
+    int rc = set_t(t0);
+    if (rc) return rc;
+    const size_t mbytes = sizeof(long long) * 4 * static_cast<size_t>(R) * static_cast<size_t>(steps);
+    if (mbytes > run_metrics_bytes) {
+        CK(cudaStreamSynchronize(stream));
+        if (d_run_metrics) cudaFree(d_run_metrics);
+        cur_metrics = nullptr;
+        CK(cudaMalloc(&d_run_metrics, mbytes));
+        run_metrics_bytes = mbytes;
+    }
+    CK(cudaMemsetAsync(d_run_metrics, 0, mbytes, stream));
+    rc = set_metrics_target(d_run_metrics, static_cast<unsigned>(steps));
+    if (rc) return rc;
+    if (flush_bytes > flush_cap) {
+        if (flush_buf) cudaFree(flush_buf);
+        CK(cudaMalloc(&flush_buf, flush_bytes));
+        flush_cap = flush_bytes;
+    }
+    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(steps));
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    const bool saved_timing = timing;
+    timing = per_kernel;
+    for (long long q = 0; q < steps; ++q) {
+        if (flush_bytes) {
+            k_flush<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(static_cast<uint4*>(flush_buf), flush_bytes / 16);
+        }
+        CK(cudaEventRecord(ev[2 * q], stream));
+        rc = launch_steps(1);
+        if (rc) {
+            timing = saved_timing;
+            return rc;
+        }
+        CK(cudaEventRecord(ev[2 * q + 1], stream));
+    }
+    timing = saved_timing;
+    CK(cudaStreamSynchronize(stream));
+    for (long long q = 0; q < steps; ++q) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, ev[2 * q], ev[2 * q + 1]));
+        step_ms[q] = ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    last_run_steps = steps;
+    return ABMX_OK;
 }
 
 }  // namespace abmx_pred

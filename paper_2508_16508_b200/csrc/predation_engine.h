@@ -102,6 +102,8 @@ struct Engine {
     cudaEvent_t tev[2 * kNumKernels] = {};
     double kernel_ms[kNumKernels] = {};
     long long kernel_launches[kNumKernels] = {};
+    void* flush_buf = nullptr;
+    size_t flush_cap = 0;
 
     ~Engine();
     int create(const abmx_predation_config& c, const uint64_t* seeds, int replicas);
@@ -118,6 +120,9 @@ struct Engine {
     int export_world(int r, uint8_t* ready, int64_t* regrow);
     int import_world(int r, const uint8_t* ready, const int64_t* regrow);
     int birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t cap);
+    // timed steps: optional L2 flush (untimed) before each step, CUDA events around each
+    // step (graph) or around each kernel (per_kernel); step_ms[steps] receives device ms.
+    int bench(long long t0, long long steps, size_t flush_bytes, bool per_kernel, double* step_ms);
 
     // internals
     int alloc(void** p, size_t bytes);
