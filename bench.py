@@ -155,10 +155,10 @@ def kernel_bytes(cfg, births_deaths):
     apportioned to the kernel that owns each column."""
     n = capacity(cfg)
     cells = cfg["width"] * cfg["height"]
-    return {"k_move": 25 * n,            # x,y,age read+write (2*(4+4+4)) + active read (1)
-            "k_predation": 0,            # scratch only (per-cell lists), not counted by §8d
-            "k_update": 17 * n,          # energy read+write (2*8) + active write (1)
-            "k_spawn_regrow": 2 * cells + 8 * births_deaths}
+    return {"k_move": 25 * n,                  # x,y,age read+write (2*(4+4+4)) + active read (1)
+            "k_cells": 0,                      # per-cell list scratch only, not counted by §8d
+            "k_update": 17 * n + 2 * cells,    # energy r+w (16) + active write (1) + regrow sweep
+            "k_spawn": 8 * births_deaths}      # id writes of births (+ zeroed ids of deaths)
 
 
 def our_arm(args, rank, world, local_rank, dist):

@@ -34,17 +34,20 @@ __device__ __forceinline__ double uniform_double(uint64_t key, uint64_t c) {
 }
 
 // ------------------------------------------------------------------ memory order
-__device__ __forceinline__ void st_release(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+// The lookback words carry their payload in the word itself (flag + counts in one u64), so
+// relaxed GPU-scope accesses are enough: no other data is published through them. (An
+// ld.acquire.gpu would make ptxas emit CCTL.IVALL, an L1 invalidate, on every poll.)
+__device__ __forceinline__ void st_word(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+__device__ __forceinline__ unsigned long long ld_word(const unsigned long long* p) {
     unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+__device__ __forceinline__ unsigned ld_word_u32(const unsigned* p) {
     unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -112,20 +115,20 @@ __device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* 
                                                             unsigned long long aggregate) {
     const int lane = threadIdx.x & 31;
     if (tile == 0) {
-        if (lane == 0) st_release(&status[0], kFlagPrefix | aggregate);
+        if (lane == 0) st_word(&status[0], kFlagPrefix | aggregate);
         return 0ULL;
     }
-    if (lane == 0) st_release(&status[tile], kFlagAgg | aggregate);
+    if (lane == 0) st_word(&status[tile], kFlagAgg | aggregate);
     unsigned long long excl = 0ULL;
     int end = tile - 1;  // closest predecessor examined by lane 0
     for (;;) {
         const int j = end - lane;
-        unsigned long long sv = j >= 0 ? ld_acquire(&status[j]) : kFlagPrefix;
+        unsigned long long sv = j >= 0 ? ld_word(&status[j]) : kFlagPrefix;
         // spin (convergently) until every examined predecessor has published something
         while (__any_sync(0xffffffffu, (sv >> 62) == 0)) {
             if ((sv >> 62) == 0) {
                 __nanosleep(32);
-                sv = ld_acquire(&status[j]);
+                sv = ld_word(&status[j]);
             }
         }
         const unsigned pmask = __ballot_sync(0xffffffffu, (sv >> 62) == 2);
@@ -139,7 +142,66 @@ __device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* 
         excl += warp_sum(contrib);
         end -= 32;
     }
-    if (lane == 0) st_release(&status[tile], kFlagPrefix | (excl + aggregate));
+    if (lane == 0) st_word(&status[tile], kFlagPrefix | (excl + aggregate));
+    return excl;
+}
+
+// Block-wide decoupled lookback: every thread of the CTA inspects one predecessor, so one
+// round trip covers kThreads tiles (the warp-wide version needs tile/32 round trips when the
+// predecessors have only published aggregates, which is the common case for a wide first
+// wave). Called by ALL threads; returns the exclusive prefix (flags stripped) in all threads.
+// `red` needs kThreads/32 + 2 entries.
+template <int kThreads>
+__device__ __forceinline__ unsigned long long block_lookback(unsigned long long* status, int tile,
+                                                             unsigned long long aggregate,
+                                                             unsigned long long* red) {
+    constexpr int kWarps = kThreads / 32;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tile == 0) {
+        if (tid == 0) st_word(&status[0], kFlagPrefix | aggregate);
+        return 0ULL;
+    }
+    if (tid == 0) st_word(&status[tile], kFlagAgg | aggregate);
+    unsigned long long excl = 0ULL;
+    int end = tile - 1;
+    for (;;) {
+        const int j = end - tid;
+        unsigned long long v = kFlagPrefix;  // virtual zero prefix before tile 0
+        if (j >= 0) {
+            v = ld_word(&status[j]);
+            while ((v >> 62) == 0) {
+                __nanosleep(20);
+                v = ld_word(&status[j]);
+            }
+        }
+        // closest predecessor (smallest tid) holding an inclusive prefix
+        const unsigned pm = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+        if (lane == 0) red[warp] = pm ? static_cast<unsigned long long>(warp * 32 + __ffs(pm) - 1) : ~0ULL;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long f = ~0ULL;
+            for (int w = 0; w < kWarps; ++w) f = red[w] < f ? red[w] : f;
+            red[kWarps] = f;
+        }
+        __syncthreads();
+        const unsigned long long first = red[kWarps];
+        unsigned long long c = (static_cast<unsigned long long>(tid) <= first) ? (v & kValueMask) : 0ULL;
+        c = warp_sum(c);
+        __syncthreads();
+        if (lane == 0) red[warp] = c;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kWarps; ++w) t += red[w];
+            red[kWarps + 1] = t;
+        }
+        __syncthreads();
+        excl += red[kWarps + 1];
+        if (first != ~0ULL) break;
+        end -= kThreads;
+        __syncthreads();
+    }
+    if (tid == 0) st_word(&status[tile], kFlagPrefix | (excl + aggregate));
     return excl;
 }
 

@@ -45,44 +45,48 @@ __device__ __forceinline__ size_t sidx(const Params& P, int s, int r, int i) {
 __device__ __forceinline__ size_t cidx(const Params& P, int r, int c) {
     return static_cast<size_t>(r) * P.Cpad + c;
 }
-__device__ __forceinline__ unsigned long long inv_key(unsigned long long epoch, int slot) {
-    return ((0xFFFFFFFFULL - (epoch & 0xFFFFFFFFULL)) << 32) | static_cast<uint32_t>(slot);
-}
 // exact fixed-point image of an energy on the 2^-20 grid (predation.hpp:60-63)
 __device__ __forceinline__ long long to_fx(double e) {
     return __double2ll_rn(__dmul_rn(e, 1048576.0));
 }
 
-__device__ __forceinline__ void load8_u8(const uint8_t* p, uint8_t (&v)[kS]) {
-    const uint2 w = *reinterpret_cast<const uint2*>(p);
+template <int N>
+__device__ __forceinline__ void load8_u8(const uint8_t* p, uint8_t (&v)[N]) {
+    static_assert(N == 4 || N == 8, "4 or 8 slots per thread");
+    if constexpr (N == 4) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
 #pragma unroll
-    for (int k = 0; k < kS; ++k) v[k] = static_cast<uint8_t>((k < 4 ? w.x : w.y) >> (8 * (k & 3)));
-}
-__device__ __forceinline__ void store8_u8(uint8_t* p, const uint8_t (&v)[kS]) {
-    uint2 w;
-    w.x = v[0] | (v[1] << 8) | (v[2] << 16) | (static_cast<uint32_t>(v[3]) << 24);
-    w.y = v[4] | (v[5] << 8) | (v[6] << 16) | (static_cast<uint32_t>(v[7]) << 24);
-    *reinterpret_cast<uint2*>(p) = w;
-}
-__device__ __forceinline__ void load8_i32(const int* p, int (&v)[kS]) {
-    const int4 a = reinterpret_cast<const int4*>(p)[0], b = reinterpret_cast<const int4*>(p)[1];
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-}
-__device__ __forceinline__ void store8_i32(int* p, const int (&v)[kS]) {
-    reinterpret_cast<int4*>(p)[0] = make_int4(v[0], v[1], v[2], v[3]);
-    reinterpret_cast<int4*>(p)[1] = make_int4(v[4], v[5], v[6], v[7]);
-}
-__device__ __forceinline__ void load8_f64(const double* p, double (&v)[kS]) {
+        for (int k = 0; k < 4; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
+    } else {
+        const uint2 w = *reinterpret_cast<const uint2*>(p);
 #pragma unroll
-    for (int q = 0; q < kS / 2; ++q) {
+        for (int k = 0; k < 8; ++k) v[k] = static_cast<uint8_t>((k < 4 ? w.x : w.y) >> (8 * (k & 3)));
+    }
+}
+template <int N>
+__device__ __forceinline__ void store8_u8(uint8_t* p, const uint8_t (&v)[N]) {
+    uint32_t w[N / 4];
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q)
+        w[q] = v[4 * q] | (v[4 * q + 1] << 8) | (v[4 * q + 2] << 16) | (static_cast<uint32_t>(v[4 * q + 3]) << 24);
+    if constexpr (N == 4)
+        *reinterpret_cast<uint32_t*>(p) = w[0];
+    else
+        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+}
+template <int N>
+__device__ __forceinline__ void load8_f64(const double* p, double (&v)[N]) {
+#pragma unroll
+    for (int q = 0; q < N / 2; ++q) {
         const double2 d = reinterpret_cast<const double2*>(p)[q];
         v[2 * q] = d.x;
         v[2 * q + 1] = d.y;
     }
 }
-__device__ __forceinline__ void store8_f64(double* p, const double (&v)[kS]) {
+template <int N>
+__device__ __forceinline__ void store8_f64(double* p, const double (&v)[N]) {
 #pragma unroll
-    for (int q = 0; q < kS / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+    for (int q = 0; q < N / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
 }
 
 template <class T>
@@ -98,120 +102,132 @@ __device__ __forceinline__ T block_sum(T v, T* smem) {
     return t;  // valid in thread 0
 }
 
-// ============================================================== K1: move + bin
-__global__ void __launch_bounds__(kT) k_move(Params P) {
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned long long s_key;
-    Ctl* ctl = P.ctl;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&ctl->k1_ticket, 1u);
-    __syncthreads();
-    const unsigned ticket = s_ticket;
-    const unsigned long long epoch = ctl->epoch;
-    const long long t = ctl->t;
-    const unsigned wolf_ctas = static_cast<unsigned>(P.R * P.tiles[1]);
-    int s, r, tile;
-    if (ticket < wolf_ctas) {
-        s = 1;
-        r = ticket / P.tiles[1];
-        tile = ticket % P.tiles[1];
-    } else {
+// ============================================================== per-cell lists
+// One uint2 per cell: .x = sheep list head, .y = wolf list head, each {epoch8:8 | slot:24}.
+// A head is current iff its epoch byte equals this step's epoch8 (so nothing is cleared
+// per step); the host zeroes the array every kEpochClear steps, before epoch8 can alias.
+__device__ __forceinline__ unsigned epoch8(unsigned long long epoch) {
+    return static_cast<unsigned>(epoch % 255ULL) + 1u;  // 1..255, never the cleared 0
+}
+constexpr unsigned kNil = 0xFFFFFFu;  // end of list
+
+// blockIdx -> (species, replica, tile) for the per-slot kernels: sheep tiles first.
+__device__ __forceinline__ void tile_of(const Params& P, unsigned b, int tiles0, int tiles1, int& s, int& r,
+                                        int& tile) {
+    const unsigned sheep_ctas = static_cast<unsigned>(P.R * tiles0);
+    if (b < sheep_ctas) {
         s = 0;
-        const unsigned u = ticket - wolf_ctas;
-        r = u / P.tiles[0];
-        tile = u % P.tiles[0];
+        r = b / tiles0;
+        tile = b % tiles0;
+    } else {
+        s = 1;
+        const unsigned u = b - sheep_ctas;
+        r = u / tiles1;
+        tile = u % tiles1;
     }
+}
+
+__device__ __forceinline__ void load4_u8(const uint8_t* p, uint8_t (&v)[4]) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
+}
+
+// ============================================================== K1: move + bin
+// step_agents with the move transition (predation.cpp:35-49, lifecycle.cpp:87-122), then each
+// live agent pushes itself onto its new cell's list with one atomicExch. The agent that finds
+// a stale head is the first in its cell this step and records the cell in the occupied-cell
+// list of its species (one block-aggregated atomic per CTA).
+__global__ void __launch_bounds__(kT) k_move(Params P) {
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ unsigned s_base;
+    const unsigned long long epoch = P.epoch;
+    const unsigned e8 = epoch8(epoch);
+    int s, r, tile;
+    tile_of(P, blockIdx.x, P.mtiles[0], P.mtiles[1], s, r, tile);
     // zero this parity's event accumulators (consumed by K2..K4 of this step)
     {
         Events* ev = P.ev + static_cast<size_t>(epoch & 1) * P.R;
-        for (int rr = ticket; rr < P.R; rr += gridDim.x)
-            if (threadIdx.x == 0) memset(&ev[rr], 0, sizeof(Events));
+        for (unsigned rr = blockIdx.x * kT + threadIdx.x; rr < static_cast<unsigned>(P.R); rr += gridDim.x * kT)
+            memset(&ev[rr], 0, sizeof(Events));
     }
-    if (threadIdx.x == 0) {
-        if (s == 0) {  // sheep bin only after every wolf is binned (sheep lists are built
-                       // only for cells that hold a wolf)
-            while (ld_acquire_u32(&ctl->k1_wolves_done) < wolf_ctas) __nanosleep(64);
-        }
-        s_key = split(split(split(P.seeds[r], 3), static_cast<unsigned long long>(t)), s);
-    }
-    __syncthreads();
-    const unsigned long long key = s_key;
-    const int i0 = tile * kTile + threadIdx.x * kS;
+    const unsigned long long key = split(split(split(P.seeds[r], 3), static_cast<unsigned long long>(P.t)), s);
+    const int i0 = tile * kMTile + threadIdx.x * kM;
     const int W = P.W, H = P.H;
+    bool first[kM] = {false, false, false, false};
+    int cell[kM] = {0, 0, 0, 0};
     if (i0 < P.N[s]) {
         const size_t base = sidx(P, s, r, i0);
-        uint8_t act[kS];
-        load8_u8(P.active[s] + base, act);
-        bool any = false;
-#pragma unroll
-        for (int k = 0; k < kS; ++k) any |= act[k] != 0;
-        int cell[kS], age[kS];
-        bool first[kS];
-        if (any) {
-            load8_i32(P.cell[s] + base, cell);
-            load8_i32(P.age[s] + base, age);
+        uint8_t act[kM];
+        int4 cv = make_int4(0, 0, 0, 0), av = make_int4(0, 0, 0, 0);
+        if (s == 0) {  // dense species: issue the column loads together with the mask load
+            cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
+            av = *reinterpret_cast<const int4*>(P.age[s] + base);
         }
-#pragma unroll
-        for (int k = 0; k < kS; ++k) {
-            first[k] = false;
-            if (!act[k]) continue;
-            const int i = i0 + k;
-            const int u = static_cast<int>(draw(key, static_cast<unsigned long long>(i)) >> 61);
-            const int c = cell[k];
-            const int y = c / W, x = c - y * W;
-            int nx = x + c_dx[u], ny = y + c_dy[u];
-            nx = nx < 0 ? nx + W : (nx >= W ? nx - W : nx);
-            ny = ny < 0 ? ny + H : (ny >= H ? ny - H : ny);
-            const int nc = ny * W + nx;
-            cell[k] = nc;
-            age[k] += 1;
-            const unsigned long long stamp = (epoch << 32) | static_cast<uint32_t>(i);
-            const size_t ci = cidx(P, r, nc);
+        load4_u8(P.active[s] + base, act);
+        const bool any = (act[0] | act[1] | act[2] | act[3]) != 0;
+        if (any) {
             if (s == 1) {
-                const unsigned long long old = atomicExch(&P.head[1][ci], stamp);
-                first[k] = (old >> 32) != (epoch & 0xFFFFFFFFULL);
-                P.next[1][base + k] = first[k] ? -1 : static_cast<int>(static_cast<uint32_t>(old));
-            } else {
-                atomicMin(&P.smin[ci], inv_key(epoch, i));
-                const unsigned long long hw = __ldcg(&P.head[1][ci]);
-                if ((hw >> 32) == (epoch & 0xFFFFFFFFULL)) {
-                    const unsigned long long old = atomicExch(&P.head[0][ci], stamp);
-                    P.next[0][base + k] =
-                        (old >> 32) == (epoch & 0xFFFFFFFFULL) ? static_cast<int>(static_cast<uint32_t>(old)) : -1;
-                }
+                cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
+                av = *reinterpret_cast<const int4*>(P.age[s] + base);
             }
-        }
-        if (any) {
-            store8_i32(P.cell[s] + base, cell);
-            store8_i32(P.age[s] + base, age);
-        }
-        if (ctl->needs_blend) {  // step_agents masks placeholder state back to defaults
+            cell[0] = cv.x;
+            cell[1] = cv.y;
+            cell[2] = cv.z;
+            cell[3] = cv.w;
+            int age[kM] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-            for (int k = 0; k < kS; ++k)
+            for (int k = 0; k < kM; ++k) {
+                if (!act[k]) continue;
+                const int u = static_cast<int>(draw(key, static_cast<unsigned long long>(i0 + k)) >> 61);
+                const int c = cell[k];
+                const int y = c / W, x = c - y * W;
+                int nx = x + c_dx[u], ny = y + c_dy[u];
+                nx = nx < 0 ? nx + W : (nx >= W ? nx - W : nx);
+                ny = ny < 0 ? ny + H : (ny >= H ? ny - H : ny);
+                cell[k] = ny * W + nx;
+                age[k] += 1;
+            }
+            // push onto the cell lists: exchanges issued back to back, then consumed
+            unsigned* cw = reinterpret_cast<unsigned*>(P.cw);
+            unsigned old[kM];
+#pragma unroll
+            for (int k = 0; k < kM; ++k)
+                if (act[k]) old[k] = atomicExch(&cw[2 * cidx(P, r, cell[k]) + s], (e8 << 24) | static_cast<unsigned>(i0 + k));
+#pragma unroll
+            for (int k = 0; k < kM; ++k)
+                if (act[k]) {
+                    const bool cur = (old[k] >> 24) == e8;
+                    P.next[s][base + k] = cur ? static_cast<int>(old[k] & kNil) : -1;
+                    first[k] = !cur;
+                }
+            *reinterpret_cast<int4*>(P.cell[s] + base) = make_int4(cell[0], cell[1], cell[2], cell[3]);
+            *reinterpret_cast<int4*>(P.age[s] + base) = make_int4(age[0], age[1], age[2], age[3]);
+        }
+        if (P.needs_blend) {  // step_agents masks placeholder state back to defaults
+#pragma unroll
+            for (int k = 0; k < kM; ++k)
                 if (!act[k] && i0 + k < P.N[s]) {
                     P.cell[s][base + k] = 0;
                     P.energy[s][base + k] = 0.0;
                 }
         }
-        if (s == 1) {
-#pragma unroll
-            for (int k = 0; k < kS; ++k) {
-                const unsigned pos = warp_append(&ctl->wcell_count, first[k]);
-                if (first[k]) P.wcells[pos] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
-            }
-        }
-    } else if (s == 1) {
-        // keep warp_append convergent: nothing to append
     }
-    if (s == 1) {
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            __threadfence();
-            atomicAdd(&ctl->k1_wolves_done, 1u);
-        }
+    // append the cells this thread opened to the occupied-cell list of species s
+    const unsigned nfirst = first[0] + first[1] + first[2] + first[3];
+    unsigned long long total;
+    const unsigned long long off = block_excl_scan<kT>(nfirst, s_scan, &total);
+    if (threadIdx.x == 0 && total) s_base = atomicAdd(&P.ctl->occ[s], static_cast<unsigned>(total));
+    __syncthreads();
+    if (nfirst) {
+        unsigned pos = s_base + static_cast<unsigned>(off);
+#pragma unroll
+        for (int k = 0; k < kM; ++k)
+            if (first[k]) P.occ[s][pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
     }
 }
 
-// ============================================================== K2: predation pairing
+// ============================================================== K2: occupied cells
 __device__ void insertion_sort(int* a, int n) {
     for (int i = 1; i < n; ++i) {
         const int v = a[i];
@@ -247,143 +263,177 @@ __device__ void heap_sort(int* a, int n) {
 
 constexpr int kSmallList = 8;
 
-__global__ void __launch_bounds__(256) k_predation(Params P) {
-    Ctl* ctl = P.ctl;
-    const unsigned count = *reinterpret_cast<volatile unsigned*>(&ctl->wcell_count);
-    const unsigned long long epoch = ctl->epoch & 0xFFFFFFFFULL;
-    Events* ev = P.ev + static_cast<size_t>(ctl->epoch & 1) * P.R;
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
-        const unsigned long long ent = P.wcells[e];
+// One thread per occupied (cell, species):
+//  * sheep cell: graze — the LOWEST sheep slot of the cell eats if the cell is ready
+//    (predation.cpp:178-195); the winner gets a graze flag, the cell its regrow code.
+//  * wolf cell: predation — the k-th wolf (slot order) takes the k-th sheep (slot order)
+//    (predation.cpp:197-239); lists come unordered from the exchanges, so both are sorted
+//    (registers for short lists, heap sort in a global scratch pool otherwise).
+__global__ void __launch_bounds__(kT) k_cells(Params P) {
+    const unsigned e8 = epoch8(P.epoch);
+    const unsigned ns = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[0]);
+    const unsigned nw = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[1]);
+    Events* ev = P.ev + static_cast<size_t>(P.epoch & 1) * P.R;
+    const unsigned stride = gridDim.x * kT;
+    for (unsigned e = blockIdx.x * kT + threadIdx.x; e < ns; e += stride) {
+        const unsigned long long ent = P.occ[0][e];
         const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
         const size_t ci = cidx(P, r, c);
-        const size_t wb = static_cast<size_t>(r) * P.Npad[1], sb = static_cast<size_t>(r) * P.Npad[0];
-        const unsigned long long hw = P.head[1][ci];
-        const unsigned long long hs = P.head[0][ci];
-        const int w0 = static_cast<int>(static_cast<uint32_t>(hw));
-        const int s0 = (hs >> 32) == epoch ? static_cast<int>(static_cast<uint32_t>(hs)) : -1;
+        const size_t sb = static_cast<size_t>(r) * P.Npad[0];
+        const uint8_t gv = P.g[ci];  // independent of the list walk: issue first
+        int m = static_cast<int>(reinterpret_cast<const unsigned*>(P.cw)[2 * ci] & kNil);
+        for (int v = P.next[0][sb + m]; v >= 0; v = P.next[0][sb + v]) m = v < m ? v : m;
+        if (gv == 0) {
+            P.g[ci] = static_cast<uint8_t>(P.delay_code);
+            P.graze[sb + m] = 1;
+        }
+    }
+    for (unsigned e = blockIdx.x * kT + threadIdx.x; e < nw; e += stride) {
+        const unsigned long long ent = P.occ[1][e];
+        const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
+        const uint2 word = P.cw[cidx(P, r, c)];
+        if ((word.x >> 24) != e8) continue;  // no sheep in this cell
+        const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
+        const int w0 = static_cast<int>(word.y & kNil), s0 = static_cast<int>(word.x & kNil);
         int lw = 0, ls = 0;
         for (int w = w0; w >= 0; w = P.next[1][wb + w]) ++lw;
         for (int v = s0; v >= 0; v = P.next[0][sb + v]) ++ls;
-        if (ls == 0) continue;
         const int pairs = lw < ls ? lw : ls;
-        if (lw <= kSmallList && ls <= kSmallList) {
-            int wl[kSmallList], sl[kSmallList];
-            int k = 0;
-            for (int w = w0; w >= 0; w = P.next[1][wb + w]) wl[k++] = w;
-            k = 0;
-            for (int v = s0; v >= 0; v = P.next[0][sb + v]) sl[k++] = v;
-            insertion_sort(wl, lw);
-            insertion_sort(sl, ls);
-            for (int q = 0; q < pairs; ++q) {
-                P.flag[0][sb + sl[q]] = 1;  // eaten
-                P.flag[1][wb + wl[q]] = 1;  // ate
-            }
-        } else {
-            const unsigned off = atomicAdd(&ctl->pool_top, static_cast<unsigned>(lw + ls));
+        int wl_r[kSmallList], sl_r[kSmallList];
+        int *wl = wl_r, *sl = sl_r;
+        const bool small = lw <= kSmallList && ls <= kSmallList;
+        if (!small) {
+            const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
             if (static_cast<long long>(off) + lw + ls > P.pool_size) {
-                atomicExch(&ctl->error, 1u);
+                atomicExch(&P.ctl->error, 1u);
                 continue;
             }
-            int* wl = P.pool + off;
-            int* sl = wl + lw;
-            int k = 0;
-            for (int w = w0; w >= 0; w = P.next[1][wb + w]) wl[k++] = w;
-            k = 0;
-            for (int v = s0; v >= 0; v = P.next[0][sb + v]) sl[k++] = v;
+            wl = P.pool + off;
+            sl = wl + lw;
+        }
+        int q = 0;
+        for (int w = w0; w >= 0; w = P.next[1][wb + w]) wl[q++] = w;
+        q = 0;
+        for (int v = s0; v >= 0; v = P.next[0][sb + v]) sl[q++] = v;
+        if (small) {
+            insertion_sort(wl, lw);
+            insertion_sort(sl, ls);
+        } else {
             heap_sort(wl, lw);
             heap_sort(sl, ls);
-            for (int q = 0; q < pairs; ++q) {
-                P.flag[0][sb + sl[q]] = 1;
-                P.flag[1][wb + wl[q]] = 1;
-            }
+        }
+        for (q = 0; q < pairs; ++q) {
+            P.flag[0][sb + sl[q]] = 1;  // eaten
+            P.flag[1][wb + wl[q]] = 1;  // ate
         }
         atomicAdd(&ev[r].sheep_eaten, static_cast<unsigned long long>(pairs));
     }
 }
 
-// ============================================================== K3: per-slot update + scans
-__global__ void __launch_bounds__(kT) k_update(Params P) {
-    __shared__ unsigned s_ticket;
-    __shared__ unsigned long long s_key;
+// ============================================================== K3: per-slot update
+// Streams every slot once: graze gain, predation kill / gain, metabolise, starve, reproduce
+// (predation.cpp:178-250). Each tile compacts its own free slots and valid rows (tile-local
+// ranks from one block scan of packed (free, valid) counters) and publishes its two counts;
+// no tile waits on another — the global ranks are resolved in k_spawn.
+// CTAs past the slot tiles run the cell regrow sweep (predation.cpp:252-258) and count ready
+// cells for the metrics row.
+__global__ void __launch_bounds__(kT, 4) k_update(Params P) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
-    __shared__ unsigned long long s_prefix;
     __shared__ long long s_red[kT / 32];
-    Ctl* ctl = P.ctl;
-    if (threadIdx.x == 0) s_ticket = atomicAdd(&ctl->k3_ticket, 1u);
-    __syncthreads();
-    const unsigned ticket = s_ticket;
-    const unsigned long long epoch = ctl->epoch;
+    const unsigned slot_ctas = static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
+    if (blockIdx.x >= slot_ctas) {
+        // regrow: 16 cells per thread (Cpad is a multiple of 16: a chunk never straddles replicas)
+        const size_t nchunk = static_cast<size_t>(P.R) * P.Cpad / 16;
+        const size_t stride = static_cast<size_t>(gridDim.x - slot_ctas) * kT;
+        for (size_t q = static_cast<size_t>(blockIdx.x - slot_ctas) * kT + threadIdx.x; q - threadIdx.x < nchunk; q += stride) {
+            unsigned ready = 0;
+            int r = -1;
+            if (q < nchunk) {
+                const size_t c0 = q * 16;
+                r = static_cast<int>(c0 / P.Cpad);
+                uint4 v = *reinterpret_cast<const uint4*>(P.g + c0);
+                uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                bool changed = false;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t o = 0;
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        uint32_t x = (w[j] >> (8 * b)) & 0xFF;
+                        if (x >= 1 && x <= 254) {
+                            --x;
+                            changed = true;
+                        }
+                        ready += x == 0;
+                        o |= x << (8 * b);
+                    }
+                    w[j] = o;
+                }
+                if (changed) *reinterpret_cast<uint4*>(P.g + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+            // per-replica grass count, aggregated over the lanes of a warp sharing a replica
+            const unsigned grp = __match_any_sync(0xffffffffu, r);
+            const unsigned tot = __reduce_add_sync(grp, ready);
+            if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot) {
+                long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
+                atomicAdd(reinterpret_cast<unsigned long long*>(&row[2]), static_cast<unsigned long long>(tot));
+            }
+        }
+        return;
+    }
+    const unsigned long long epoch = P.epoch;
     const int p = static_cast<int>(epoch & 1);
-    const unsigned sheep_ctas = static_cast<unsigned>(P.R * P.tiles[0]);
     int s, r, tile;
-    if (ticket < sheep_ctas) {
-        s = 0;
-        r = ticket / P.tiles[0];
-        tile = ticket % P.tiles[0];
-    } else {
-        s = 1;
-        const unsigned u = ticket - sheep_ctas;
-        r = u / P.tiles[1];
-        tile = u % P.tiles[1];
-    }
-    if (threadIdx.x == 0) {
-        s_key = split(split(split(P.seeds[r], 4), static_cast<unsigned long long>(ctl->t)), s);
-        // clear this tile's lookback word of the other parity for the next step
-        P.status[((static_cast<size_t>(1 - p) * 2 + s) * P.R + r) * P.status_stride + tile] = 0ULL;
-    }
-    __syncthreads();
-    const unsigned long long key = s_key;
-    unsigned long long* status = P.status + ((static_cast<size_t>(p) * 2 + s) * P.R + r) * P.status_stride;
+    tile_of(P, blockIdx.x, P.tiles[0], P.tiles[1], s, r, tile);
+    const unsigned long long key = split(split(split(P.seeds[r], 4), static_cast<unsigned long long>(P.t)), s);
     const int N = P.N[s];
     const int i0 = tile * kTile + threadIdx.x * kS;
     const size_t base = sidx(P, s, r, i0);
     const double gain = P.gain[s], metab = P.metab, prob = P.prob[s], frac = P.frac;
 
-    uint8_t act[kS], flg[kS];
+    uint8_t act[kS];
     double E[kS], child[kS];
-    int cell[kS];
     bool valid[kS], freek[kS];
     unsigned n_graze = 0, n_metab = 0, n_death = 0;
     long long fx_removed = 0;
+#pragma unroll
+    for (int k = 0; k < kS; ++k) {
+        valid[k] = false;
+        freek[k] = false;
+        child[k] = 0.0;
+    }
     if (i0 < N) {
+        uint8_t flg[kS], grz[kS];
         load8_u8(P.active[s] + base, act);
         load8_u8(P.flag[s] + base, flg);
-        bool any = false, anyflag = false;
+        if (s == 0) load8_u8(P.graze + base, grz);
+        bool any = false, anyflag = false, anygrz = false;
+        if (s == 0) load8_f64(P.energy[s] + base, E);  // dense: issue with the masks
 #pragma unroll
         for (int k = 0; k < kS; ++k) {
             any |= act[k] != 0;
             anyflag |= flg[k] != 0;
+            if (s == 0) anygrz |= grz[k] != 0;
         }
-        if (anyflag) {
-            const uint8_t z[kS] = {0, 0, 0, 0, 0, 0, 0, 0};
-            store8_u8(P.flag[s] + base, z);
-        }
-        if (any) {
-            load8_f64(P.energy[s] + base, E);
-            if (s == 0) load8_i32(P.cell[s] + base, cell);
-        }
+        if (s == 1 && any) load8_f64(P.energy[s] + base, E);
+        const uint8_t z[kS] = {};
+        if (anyflag) store8_u8(P.flag[s] + base, z);
+        if (anygrz) store8_u8(P.graze + base, z);
         bool died_any = false;
 #pragma unroll
         for (int k = 0; k < kS; ++k) {
-            valid[k] = false;
-            child[k] = 0.0;
             const int i = i0 + k;
             bool alive = act[k] != 0;
-            if (alive) {
-                if (s == 0) {
-                    // graze: lowest active sheep slot on a ready cell eats (predation.cpp:178-195)
-                    const size_t ci = cidx(P, r, cell[k]);
-                    if (static_cast<int>(static_cast<uint32_t>(P.smin[ci])) == i && P.g[ci] == 0) {
-                        P.g[ci] = static_cast<uint8_t>(P.delay_code);
-                        E[k] = __dadd_rn(E[k], gain);
-                        ++n_graze;
-                    }
-                    if (flg[k]) {  // eaten by a wolf this step (predation.cpp:224-238)
-                        fx_removed += to_fx(E[k]);
-                        ++n_death;
-                        alive = false;
-                    }
-                } else if (flg[k]) {
+            if (alive && s == 0 && grz[k]) {  // grazed (predation.cpp:188-193)
+                E[k] = __dadd_rn(E[k], gain);
+                ++n_graze;
+            }
+            if (alive && flg[k]) {
+                if (s == 0) {  // eaten by a wolf this step (predation.cpp:224-238)
+                    fx_removed += to_fx(E[k]);
+                    ++n_death;
+                    alive = false;
+                } else {
                     E[k] = __dadd_rn(E[k], gain);  // the wolf ate (predation.cpp:236)
                 }
             }
@@ -421,13 +471,6 @@ __global__ void __launch_bounds__(kT) k_update(Params P) {
                     P.id[s][base + k] = 0;
                 }
         }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kS; ++k) {
-            valid[k] = false;
-            freek[k] = false;
-            child[k] = 0.0;
-        }
     }
     unsigned nf = 0, nv = 0;
 #pragma unroll
@@ -437,143 +480,117 @@ __global__ void __launch_bounds__(kT) k_update(Params P) {
     }
     unsigned long long tile_total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(nf, nv), s_scan, &tile_total);
-    if (threadIdx.x < 32) {
-        const unsigned long long pre = tile_lookback(status, tile, tile_total);
-        if (threadIdx.x == 0) s_prefix = pre;
-    }
-    __syncthreads();
-    const unsigned long long pre = s_prefix + excl;
-    int fr = static_cast<int>(hi31(pre)), vr = static_cast<int>(lo31(pre));
-    const size_t rb = static_cast<size_t>(r) * P.Npad[s];
+    // tile-local compaction: slot order within the tile, tiles concatenate in k_spawn
+    int fr = static_cast<int>(hi31(excl)), vr = static_cast<int>(lo31(excl));
+    const size_t tb = static_cast<size_t>(r) * P.Npad[s] + static_cast<size_t>(tile) * kTile;
 #pragma unroll
     for (int k = 0; k < kS; ++k) {
-        if (freek[k]) P.free_at[s][rb + fr++] = i0 + k;
+        if (freek[k]) P.free_at[s][tb + fr++] = i0 + k;
         if (valid[k]) {
-            int c = (s == 0) ? cell[k] : P.cell[s][base + k];
-            P.row_at[s][rb + vr] = i0 + k;
-            P.rowcell[s][rb + vr] = c;
-            P.rowE[s][rb + vr] = child[k];
+            P.row_at[s][tb + vr] = i0 + k;
+            P.rowcell[s][tb + vr] = P.cell[s][base + k];
+            P.rowE[s][tb + vr] = child[k];
             ++vr;
         }
     }
-    // event reductions
+    // event reductions + the tile's (free, valid) counts
     Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
     const long long g_sum = block_sum<long long>(n_graze, s_red);
     const long long m_sum = block_sum<long long>(n_metab, s_red);
     const long long d_sum = block_sum<long long>(n_death, s_red);
     const long long x_sum = block_sum<long long>(fx_removed, s_red);
     if (threadIdx.x == 0) {
+        P.status[(static_cast<size_t>(s) * P.R + r) * P.status_stride + tile] = tile_total;
         if (g_sum) atomicAdd(&ev->grass_eaten, static_cast<unsigned long long>(g_sum));
         if (m_sum) atomicAdd(&ev->metabolized[s], static_cast<unsigned long long>(m_sum));
         if (d_sum) atomicAdd(&ev->deaths[s], static_cast<unsigned long long>(d_sum));
         if (x_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_removed_fx[s]), static_cast<unsigned long long>(x_sum));
-        if (tile == P.tiles[s] - 1) {
-            // last tile: totals known -> spawn plan, counters and the metrics row
-            const unsigned long long tot = s_prefix + tile_total;
-            const int F = static_cast<int>(hi31(tot)), Q = static_cast<int>(lo31(tot));
-            const int pairs = F < Q ? F : Q;
-            SpeciesRep* sr = &P.rep[static_cast<size_t>(r) * 2 + s];
-            sr->base_id = sr->next_id;
-            sr->pairs = pairs;
-            sr->Q = Q;
-            sr->next_id += pairs;
-            sr->num_active = N - F + pairs;
-            atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
-            atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
-            long long* row = ctl->metrics + (static_cast<size_t>(r) * ctl->metrics_stride + ctl->run_step) * 4;
-            row[s] = sr->num_active;
-            if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
-        }
     }
 }
 
-// ============================================================== K4: spawn + regrow
-__global__ void __launch_bounds__(kT) k_spawn_regrow(Params P) {
+// ============================================================== K4: spawn
+// Rank-match (lifecycle.cpp:144-195): the k-th free slot (ascending) receives the k-th valid
+// row (ascending parent slot), k < pairs = min(F, Q); fresh ids next_id + k. Every CTA scans
+// the per-tile counts of its (replica, species) in shared memory and maps each global rank to
+// (tile, local offset) by binary search. CTA 0 of each (replica, species) advances the
+// counters (double-buffered by step parity), writes the metrics row and the ledger totals.
+__device__ __forceinline__ int find_tile(const unsigned long long* pre, int tiles, unsigned k, bool free_rank) {
+    // largest t with prefix(t) <= k, prefix over the chosen counter
+    int lo = 0, hi = tiles - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        const unsigned v = free_rank ? hi31(pre[mid]) : lo31(pre[mid]);
+        if (v <= k)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
+}
+
+__global__ void __launch_bounds__(kT) k_spawn(Params P) {
+    extern __shared__ unsigned long long s_pre[];  // [tiles + 1] exclusive prefix of tile counts
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ long long s_red[kT / 32];
-    __shared__ bool s_last;
-    Ctl* ctl = P.ctl;
-    const unsigned long long epoch = ctl->epoch;
-    if (static_cast<int>(blockIdx.x) < P.spawn_ctas) {
-        const int rs = blockIdx.x / P.spawn_cps, local = blockIdx.x % P.spawn_cps;
-        const int s = rs / P.R, r = rs % P.R;
-        const SpeciesRep sr = P.rep[static_cast<size_t>(r) * 2 + s];
-        const size_t rb = static_cast<size_t>(r) * P.Npad[s];
-        long long fx_dropped = 0;
-        for (int k = local * kT + threadIdx.x; k < sr.Q; k += P.spawn_cps * kT) {
-            if (k < sr.pairs) {
-                const size_t slot = rb + P.free_at[s][rb + k];
-                P.active[s][slot] = 1;
-                P.cell[s][slot] = P.rowcell[s][rb + k];
-                P.energy[s][slot] = P.rowE[s][rb + k];
-                P.age[s][slot] = 0;
-                P.id[s][slot] = sr.base_id + k;
-            } else {
-                fx_dropped += to_fx(P.rowE[s][rb + k]);  // predation.cpp:121-135
-            }
-        }
-        if (sr.Q > sr.pairs) {
-            const long long tot = block_sum<long long>(fx_dropped, s_red);
-            if (threadIdx.x == 0 && tot) {
-                Events* ev = P.ev + static_cast<size_t>(epoch & 1) * P.R + r;
-                atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_dropped_fx[s]), static_cast<unsigned long long>(tot));
-            }
-        }
-    } else {
-        // regrow: 16 cells per thread (Cpad is a multiple of 16, so a chunk never straddles replicas)
-        const size_t q = static_cast<size_t>(blockIdx.x - P.spawn_ctas) * kT + threadIdx.x;
-        const size_t c0 = q * 16;
-        unsigned ready = 0;
-        int r = -1;
-        if (c0 < static_cast<size_t>(P.R) * P.Cpad) {
-            r = static_cast<int>(c0 / P.Cpad);
-            uint4 v = *reinterpret_cast<const uint4*>(P.g + c0);
-            uint32_t w[4] = {v.x, v.y, v.z, v.w};
-            bool changed = false;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t o = 0;
-#pragma unroll
-                for (int b = 0; b < 4; ++b) {
-                    uint32_t x = (w[j] >> (8 * b)) & 0xFF;
-                    if (x >= 1 && x <= 254) {
-                        --x;
-                        changed = true;
-                    }
-                    ready += x == 0;
-                    o |= x << (8 * b);
-                }
-                w[j] = o;
-            }
-            if (changed) *reinterpret_cast<uint4*>(P.g + c0) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        // per-replica grass count, aggregated over the lanes of a warp sharing a replica
-        const unsigned grp = __match_any_sync(0xffffffffu, r);
-        const unsigned tot = __reduce_add_sync(grp, ready);
-        if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot) {
-            long long* row = ctl->metrics + (static_cast<size_t>(r) * ctl->metrics_stride + ctl->run_step) * 4;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&row[2]), static_cast<unsigned long long>(tot));
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // K1/K2 of this step are complete
+        P.ctl->occ[0] = P.ctl->occ[1] = 0;
+        P.ctl->pool_top = 0;
+    }
+    const int rs = blockIdx.x / P.spawn_cps, local = blockIdx.x % P.spawn_cps;
+    const int s = rs / P.R, r = rs % P.R;
+    const int tiles = P.tiles[s];
+    const int p = static_cast<int>(P.epoch & 1);
+    const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
+    // block-wide exclusive scan of the tile counts (chunks of kT)
+    unsigned long long carry = 0;
+    for (int t0 = 0; t0 < tiles; t0 += kT) {
+        const int t = t0 + threadIdx.x;
+        const unsigned long long v = t < tiles ? tc[t] : 0ULL;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan<kT>(v, s_scan, &tot);
+        if (t < tiles) s_pre[t] = carry + ex;
+        carry += tot;
+        __syncthreads();
+    }
+    const int F = static_cast<int>(hi31(carry)), Q = static_cast<int>(lo31(carry));
+    const int pairs = F < Q ? F : Q;
+    SpeciesRep* sr = &P.rep[static_cast<size_t>(r) * 2 + s];
+    const long long base_id = sr->next_id[p];
+    const size_t rb = static_cast<size_t>(r) * P.Npad[s];
+    long long fx_dropped = 0;
+    for (int k = local * kT + threadIdx.x; k < Q; k += P.spawn_cps * kT) {
+        const int vt = find_tile(s_pre, tiles, static_cast<unsigned>(k), false);
+        const size_t vrow = rb + static_cast<size_t>(vt) * kTile + (k - lo31(s_pre[vt]));
+        if (k < pairs) {
+            const int ft = find_tile(s_pre, tiles, static_cast<unsigned>(k), true);
+            const size_t fpos = rb + static_cast<size_t>(ft) * kTile + (k - hi31(s_pre[ft]));
+            const size_t slot = rb + P.free_at[s][fpos];
+            P.active[s][slot] = 1;
+            P.cell[s][slot] = P.rowcell[s][vrow];
+            P.energy[s][slot] = P.rowE[s][vrow];
+            P.age[s][slot] = 0;
+            P.id[s][slot] = base_id + k;
+        } else {
+            fx_dropped += to_fx(P.rowE[s][vrow]);  // predation.cpp:121-135
         }
     }
-    // the last CTA to finish closes the step
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&ctl->k4_done, 1u) == gridDim.x - 1;
+    Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
+    if (Q > pairs) {
+        const long long tot = block_sum<long long>(fx_dropped, s_red);
+        if (threadIdx.x == 0 && tot)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_dropped_fx[s]), static_cast<unsigned long long>(tot));
     }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        __threadfence();
-        ctl->epoch = epoch + 1;
-        ctl->t += 1;
-        ctl->run_step += 1;
-        ctl->k1_ticket = 0;
-        ctl->k1_wolves_done = 0;
-        ctl->k3_ticket = 0;
-        ctl->wcell_count = 0;
-        ctl->pool_top = 0;
-        ctl->needs_blend = 0;
-        ctl->k4_done = 0;
-        __threadfence();
+    if (local == 0 && threadIdx.x == 0) {
+        sr->next_id[p ^ 1] = base_id + pairs;
+        sr->num_active[p ^ 1] = P.N[s] - F + pairs;
+        sr->base_id = base_id;
+        sr->pairs = pairs;
+        sr->Q = Q;
+        atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
+        atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
+        long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
+        row[s] = P.N[s] - F + pairs;
+        if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
     }
 }
 
@@ -621,7 +638,7 @@ __global__ void k_init_cells(Params P) {
 // ====================================================================== host engine
 namespace abmx_pred {
 
-static const char* kKernelNames[kNumKernels] = {"k_move", "k_predation", "k_update", "k_spawn_regrow"};
+static const char* kKernelNames[kNumKernels] = {"k_move", "k_cells", "k_update", "k_spawn"};
 
 const char* kernel_name(int k) { return (k >= 0 && k < kNumKernels) ? kKernelNames[k] : ""; }
 
@@ -639,6 +656,7 @@ Engine::~Engine() {
     for (auto& ev : tev)
         if (ev) cudaEventDestroy(ev);
     for (void* p : allocs) cudaFree(p);
+    if (graph) cudaGraphDestroy(graph);
     if (d_run_metrics) cudaFree(d_run_metrics);
     if (flush_buf) cudaFree(flush_buf);
     if (stream) cudaStreamDestroy(stream);
@@ -674,6 +692,10 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         abmx_internal::set_error("initial counts exceed capacities");  // predation.cpp:155-156
         return ABMX_E_CAPACITY;
     }
+    if (c.sheep_capacity > 0xFFFFFE || c.wolf_capacity > 0xFFFFFE) {
+        abmx_internal::set_error("capacity per species above 16,777,214 (24-bit cell-list slots)");
+        return ABMX_E_CAPACITY;
+    }
     if (c.regrow_delay > 254) {
         abmx_internal::set_error("regrow_delay > 254 is not representable in the u8 cell layout");
         return ABMX_E_DOMAIN;
@@ -698,6 +720,8 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         if (P.Npad[s] == 0) P.Npad[s] = 16;
         P.tiles[s] = (N[s] + kTile - 1) / kTile;
         if (P.tiles[s] == 0) P.tiles[s] = 1;
+        P.mtiles[s] = (N[s] + kMTile - 1) / kMTile;
+        if (P.mtiles[s] == 0) P.mtiles[s] = 1;
     }
     P.gain[0] = c.energy_gain_sheep;
     P.gain[1] = c.energy_gain_wolf;
@@ -713,7 +737,13 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     P.spawn_ctas = 2 * R * P.spawn_cps;
     const long long chunks = (static_cast<long long>(R) * P.Cpad) / 16;
     P.regrow_ctas = static_cast<int>((chunks + kT - 1) / kT);
-    P.k2_ctas = abmx_internal::num_sms() * 4;
+    if (P.regrow_ctas > abmx_internal::num_sms() * 4) P.regrow_ctas = abmx_internal::num_sms() * 4;
+    {
+        const long long agents = static_cast<long long>(R) * (N[0] + N[1]);
+        long long k2 = (agents + kT - 1) / kT;
+        if (k2 > abmx_internal::num_sms() * 8LL) k2 = abmx_internal::num_sms() * 8LL;
+        P.k2_ctas = static_cast<int>(k2 > 0 ? k2 : 1);
+    }
     P.status_stride = P.tiles[0] > P.tiles[1] ? P.tiles[0] : P.tiles[1];
 
     int rc;
@@ -729,16 +759,16 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         AL(P.id[s], n * 8);
         AL(P.next[s], n * 4);
         AL(P.flag[s], n);
+        if (s == 0) AL(P.graze, n);
+        AL(P.occ[s], n * 8);
         AL(P.free_at[s], n * 4);
         AL(P.row_at[s], n * 4);
         AL(P.rowcell[s], n * 4);
         AL(P.rowE[s], n * 8);
-        AL(P.head[s], static_cast<size_t>(R) * P.Cpad * 8);
     }
     AL(P.g, static_cast<size_t>(R) * P.Cpad);
-    AL(P.smin, static_cast<size_t>(R) * P.Cpad * 8);
-    AL(P.status, static_cast<size_t>(2) * 2 * R * P.status_stride * 8);
-    AL(P.wcells, static_cast<size_t>(R) * (P.Npad[1]) * 8);
+    AL(P.cw, static_cast<size_t>(R) * P.Cpad * 8);
+    AL(P.status, static_cast<size_t>(2) * R * P.status_stride * 8);
     P.pool_size = static_cast<long long>(R) * (P.Npad[0] + P.Npad[1]);
     AL(P.pool, static_cast<size_t>(P.pool_size) * 4);
     AL(P.ctl, sizeof(Ctl));
@@ -750,26 +780,25 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     P.seeds = d_seeds;
     CK(cudaMemcpyAsync(d_seeds, seeds, sizeof(unsigned long long) * R, cudaMemcpyHostToDevice, stream));
     for (int s = 0; s < 2; ++s) {
-        CK(cudaMemsetAsync(P.head[s], 0, static_cast<size_t>(R) * P.Cpad * 8, stream));
         CK(cudaMemsetAsync(P.next[s], 0xFF, static_cast<size_t>(R) * P.Npad[s] * 4, stream));
     }
-    CK(cudaMemsetAsync(P.smin, 0xFF, static_cast<size_t>(R) * P.Cpad * 8, stream));
-    CK(cudaMemsetAsync(P.status, 0, static_cast<size_t>(2) * 2 * R * P.status_stride * 8, stream));
+    CK(cudaMemsetAsync(P.cw, 0, static_cast<size_t>(R) * P.Cpad * 8, stream));
+    CK(cudaMemsetAsync(P.status, 0, static_cast<size_t>(2) * R * P.status_stride * 8, stream));
+    spawn_smem = static_cast<size_t>(P.status_stride + 1) * 8;
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_spawn), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(spawn_smem)));
     CK(cudaMemsetAsync(P.ev, 0, sizeof(Events) * 2 * R, stream));
-    Ctl ctl;
-    memset(&ctl, 0, sizeof ctl);
-    ctl.epoch = 1;
-    ctl.t = 1;
-    ctl.metrics = d_metrics_step;
-    ctl.metrics_stride = 1;
-    cur_metrics = d_metrics_step;
-    cur_stride = 1;
-    CK(cudaMemcpyAsync(P.ctl, &ctl, sizeof ctl, cudaMemcpyHostToDevice, stream));
-    next_t = 1;
+    CK(cudaMemsetAsync(P.graze, 0, static_cast<size_t>(R) * P.Npad[0], stream));
+    CK(cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream));
+    P.epoch = 1;
+    P.t = 1;
+    P.metrics = d_metrics_step;
+    P.metrics_stride = 1;
+    P.run_step = 0;
     std::vector<SpeciesRep> rep(static_cast<size_t>(2) * R);
     for (int r = 0; r < R; ++r) {
-        rep[2 * r + 0] = SpeciesRep{c.n_sheep0, 0, c.n_sheep0, 0, 0, 0};
-        rep[2 * r + 1] = SpeciesRep{c.n_wolves0, 0, c.n_wolves0, 0, 0, 0};
+        rep[2 * r + 0] = SpeciesRep{{c.n_sheep0, c.n_sheep0}, {c.n_sheep0, c.n_sheep0}, 0, 0, 0};
+        rep[2 * r + 1] = SpeciesRep{{c.n_wolves0, c.n_wolves0}, {c.n_wolves0, c.n_wolves0}, 0, 0, 0};
     }
     CK(cudaMemcpyAsync(P.rep, rep.data(), sizeof(SpeciesRep) * rep.size(), cudaMemcpyHostToDevice, stream));
     CK(cudaStreamSynchronize(stream));  // rep (a host vector) must be consumed
@@ -788,32 +817,31 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     return ABMX_OK;
 }
 
-void Engine::launch_step_kernels(bool timed) {
+unsigned Engine::grid(int k) const {
     const Params& P = params;
-    const unsigned k1 = static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
-    if (timed) cudaEventRecord(tev[0], stream);
-    k_move<<<k1, kT, 0, stream>>>(P);
-    if (timed) {
-        cudaEventRecord(tev[1], stream);
-        cudaEventRecord(tev[2], stream);
+    switch (k) {
+        case 0: return static_cast<unsigned>(P.R * (P.mtiles[0] + P.mtiles[1]));
+        case 1: return static_cast<unsigned>(P.k2_ctas);
+        case 2: return static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]) + P.regrow_ctas);
+        default: return static_cast<unsigned>(P.spawn_ctas);
     }
-    k_predation<<<P.k2_ctas, 256, 0, stream>>>(P);
-    if (timed) {
-        cudaEventRecord(tev[3], stream);
-        cudaEventRecord(tev[4], stream);
+}
+
+static void* const kKernelFns[kNumKernels] = {reinterpret_cast<void*>(k_move), reinterpret_cast<void*>(k_cells),
+                                              reinterpret_cast<void*>(k_update), reinterpret_cast<void*>(k_spawn)};
+
+void Engine::launch_step_kernels(bool timed) {
+    void* args[1] = {&params};
+    for (int k = 0; k < kNumKernels; ++k) {
+        if (timed) cudaEventRecord(tev[2 * k], stream);
+        cudaLaunchKernel(kKernelFns[k], dim3(grid(k)), dim3(kT), args, k == 3 ? spawn_smem : 0, stream);
+        if (timed) cudaEventRecord(tev[2 * k + 1], stream);
     }
-    k_update<<<k1, kT, 0, stream>>>(P);
-    if (timed) {
-        cudaEventRecord(tev[5], stream);
-        cudaEventRecord(tev[6], stream);
-    }
-    k_spawn_regrow<<<P.spawn_ctas + P.regrow_ctas, kT, 0, stream>>>(P);
-    if (timed) cudaEventRecord(tev[7], stream);
     abmx_internal::count_launch(kNumKernels);
 }
 
 int Engine::accumulate_times() {
-    CK(cudaEventSynchronize(tev[7]));
+    CK(cudaEventSynchronize(tev[2 * kNumKernels - 1]));
     for (int k = 0; k < kNumKernels; ++k) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, tev[2 * k], tev[2 * k + 1]));
@@ -823,53 +851,70 @@ int Engine::accumulate_times() {
     return ABMX_OK;
 }
 
+// The step's varying scalars (epoch, t, metrics row, blend flag) are kernel PARAMETERS kept on
+// the host: nothing on the device has to advance them, and a graph replay only needs its
+// kernel nodes' parameters refreshed.
 int Engine::set_t(long long t) {
-    if (t != next_t) {
-        staged_t = t;
-        CK(cudaMemcpyAsync(&params.ctl->t, &staged_t, sizeof(long long), cudaMemcpyHostToDevice, stream));
-        CK(cudaStreamSynchronize(stream));
-        next_t = t;
-    }
+    params.t = t;
     return ABMX_OK;
 }
 
 int Engine::set_metrics_target(long long* d_metrics, unsigned stride) {
-    if (d_metrics != cur_metrics || stride != cur_stride) {
-        staged_ptr = d_metrics;
-        staged_u[0] = 0;
-        staged_u[1] = stride;
-        CK(cudaMemcpyAsync(&params.ctl->metrics, &staged_ptr, sizeof(long long*), cudaMemcpyHostToDevice, stream));
-        CK(cudaMemcpyAsync(&params.ctl->run_step, staged_u, sizeof(unsigned) * 2, cudaMemcpyHostToDevice, stream));
-        CK(cudaStreamSynchronize(stream));
-        cur_metrics = d_metrics;
-        cur_stride = stride;
-    } else {
-        CK(cudaMemsetAsync(&params.ctl->run_step, 0, sizeof(unsigned), stream));
+    params.metrics = d_metrics;
+    params.metrics_stride = stride;
+    params.run_step = 0;
+    return ABMX_OK;
+}
+
+int Engine::build_graph() {
+    CK(cudaGraphCreate(&graph, 0));
+    void* args[1] = {&params};
+    cudaGraphNode_t prev = nullptr;
+    for (int k = 0; k < kNumKernels; ++k) {
+        cudaKernelNodeParams kp{};
+        kp.func = kKernelFns[k];
+        kp.gridDim = dim3(grid(k));
+        kp.blockDim = dim3(kT);
+        kp.sharedMemBytes = k == 3 ? static_cast<unsigned>(spawn_smem) : 0;
+        kp.kernelParams = args;
+        CK(cudaGraphAddKernelNode(&nodes[k], graph, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+        prev = nodes[k];
     }
+    CK(cudaGraphInstantiate(&graph_exec, graph, 0));
     return ABMX_OK;
 }
 
 int Engine::launch_steps(long long steps) {
     (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated runtime calls
+    if (!timing && !graph_exec) {
+        int rc = build_graph();
+        if (rc) return rc;
+    }
     for (long long q = 0; q < steps; ++q) {
+        params.epoch = host_epoch;
+        if (host_epoch % kEpochClear == 0)  // epoch8 must not alias a stale list head
+            CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 8, stream));
         if (timing) {
             launch_step_kernels(true);
             int rc = accumulate_times();
             if (rc) return rc;
         } else {
-            if (!graph_exec) {
-                cudaGraph_t graph;
-                CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
-                launch_step_kernels(false);
-                CK(cudaStreamEndCapture(stream, &graph));
-                CK(cudaGraphInstantiate(&graph_exec, graph, 0));
-                cudaGraphDestroy(graph);
-                abmx_internal::count_launch(-kNumKernels);  // capture launched nothing
+            void* args[1] = {&params};
+            for (int k = 0; k < kNumKernels; ++k) {
+                cudaKernelNodeParams kp{};
+                kp.func = kKernelFns[k];
+                kp.gridDim = dim3(grid(k));
+                kp.blockDim = dim3(kT);
+                kp.sharedMemBytes = k == 3 ? static_cast<unsigned>(spawn_smem) : 0;
+                kp.kernelParams = args;
+                CK(cudaGraphExecKernelNodeSetParams(graph_exec, nodes[k], &kp));
             }
             CK(cudaGraphLaunch(graph_exec, stream));
             abmx_internal::count_launch(kNumKernels);
         }
-        ++next_t;
+        params.needs_blend = 0;
+        params.t += 1;
+        params.run_step += 1;
         ++host_epoch;
     }
     CK(cudaGetLastError());
@@ -877,11 +922,7 @@ int Engine::launch_steps(long long steps) {
 }
 
 int Engine::step(long long t) {
-    // the step index is this call's only input: always ship it (8 B H2D), then launch
-    staged_t = t;
-    CK(cudaMemcpyAsync(&params.ctl->t, &staged_t, sizeof(long long), cudaMemcpyHostToDevice, stream));
-    next_t = t;
-    int rc = ABMX_OK;
+    int rc = set_t(t);
     CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
     rc = set_metrics_target(d_metrics_step, 1);
     if (rc) return rc;
@@ -902,7 +943,7 @@ int Engine::run_async(long long t0, long long steps) {
     if (mbytes > run_metrics_bytes) {
         CK(cudaStreamSynchronize(stream));
         if (d_run_metrics) cudaFree(d_run_metrics);
-        cur_metrics = nullptr;
+
         CK(cudaMalloc(&d_run_metrics, mbytes));
         run_metrics_bytes = mbytes;
     }
@@ -985,8 +1026,9 @@ int Engine::export_species(int r, int s, uint8_t* active, int64_t* ids, int64_t*
         x[i] = cell[i] % P.W;
         y[i] = cell[i] / P.W;
     }
-    *num_active = sr.num_active;
-    *next_id = sr.next_id;
+    const int q = static_cast<int>(host_epoch & 1);  // slot the next step will read
+    *num_active = sr.num_active[q];
+    *next_id = sr.next_id[q];
     return ABMX_OK;
 }
 
@@ -1034,10 +1076,13 @@ int Engine::import_species(int r, int s, const uint8_t* active, const int64_t* i
         CK(cudaMemcpy(P.cell[s] + off, cell.data(), n * 4, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(P.age[s] + off, age.data(), n * 4, cudaMemcpyHostToDevice));
     }
-    SpeciesRep sr{num_active, 0, next_id, 0, 0, 0};
+    SpeciesRep sr;
+    CK(cudaMemcpy(&sr, P.rep + static_cast<size_t>(r) * 2 + s, sizeof sr, cudaMemcpyDeviceToHost));
+    const int q = static_cast<int>(host_epoch & 1);
+    sr.num_active[q] = num_active;
+    sr.next_id[q] = next_id;
     CK(cudaMemcpy(P.rep + static_cast<size_t>(r) * 2 + s, &sr, sizeof sr, cudaMemcpyHostToDevice));
-    const unsigned one = 1;
-    CK(cudaMemcpy(&P.ctl->needs_blend, &one, sizeof one, cudaMemcpyHostToDevice));
+    params.needs_blend = 1;
     return ABMX_OK;
 }
 
@@ -1080,16 +1125,30 @@ int Engine::import_world(int r, const uint8_t* ready, const int64_t* regrow) {
 }
 
 int Engine::birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t cap) {
+    // pairs are stored tile-locally (k_update) and matched by global rank (k_spawn): rebuild
+    // the k-th valid row and the k-th free slot from the per-tile counts
     const Params& P = params;
     SpeciesRep sr;
+    const int tiles = P.tiles[s];
+    std::vector<unsigned long long> tc(static_cast<size_t>(tiles));
     CK(cudaMemcpyAsync(&sr, P.rep + static_cast<size_t>(r) * 2 + s, sizeof sr, cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    const int n = sr.pairs < cap ? sr.pairs : cap;
+    CK(cudaMemcpyAsync(tc.data(), P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride,
+                       tiles * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
     const size_t off = static_cast<size_t>(r) * P.Npad[s];
-    if (n > 0) {
-        CK(cudaMemcpyAsync(parent, P.row_at[s] + off, n * 4, cudaMemcpyDeviceToHost, stream));
-        CK(cudaMemcpyAsync(child, P.free_at[s] + off, n * 4, cudaMemcpyDeviceToHost, stream));
-        CK(cudaStreamSynchronize(stream));
+    std::vector<int> rows(static_cast<size_t>(P.Npad[s])), frees(static_cast<size_t>(P.Npad[s]));
+    CK(cudaMemcpyAsync(rows.data(), P.row_at[s] + off, rows.size() * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(frees.data(), P.free_at[s] + off, frees.size() * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    int k = 0, kf = 0;
+    for (int t = 0; t < tiles && k < sr.pairs; ++t) {
+        const int nv = static_cast<int>(abmx_dev::lo31(tc[t]));
+        for (int j = 0; j < nv && k < sr.pairs; ++j, ++k)
+            if (k < cap) parent[k] = rows[static_cast<size_t>(t) * kTile + j];
+    }
+    for (int t = 0; t < tiles && kf < sr.pairs; ++t) {
+        const int nf = static_cast<int>(abmx_dev::hi31(tc[t]));
+        for (int j = 0; j < nf && kf < sr.pairs; ++j, ++kf)
+            if (kf < cap) child[kf] = frees[static_cast<size_t>(t) * kTile + j];
     }
     return sr.pairs;
 }
@@ -1109,7 +1168,7 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
     if (mbytes > run_metrics_bytes) {
         CK(cudaStreamSynchronize(stream));
         if (d_run_metrics) cudaFree(d_run_metrics);
-        cur_metrics = nullptr;
+
         CK(cudaMalloc(&d_run_metrics, mbytes));
         run_metrics_bytes = mbytes;
     }

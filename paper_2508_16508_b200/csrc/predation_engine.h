@@ -12,29 +12,31 @@
 
 namespace abmx_pred {
 
-constexpr int kT = 256;         // threads per slot-tile CTA
-constexpr int kS = 8;           // slots per thread
-constexpr int kTile = kT * kS;  // slots per tile
+constexpr int kT = 256;          // threads per slot-tile CTA
+constexpr int kS = 4;            // slots per thread in the scanning kernel (k_update)
+constexpr int kTile = kT * kS;   // slots per lookback tile
+constexpr int kM = 4;            // slots per thread in k_move / k_cells
+constexpr int kMTile = kT * kM;
 constexpr int kNumKernels = 4;
+constexpr int kEpochClear = 128;  // cw is zeroed every kEpochClear steps (epoch8 period 255)
 
 // Device control block: step bookkeeping shared by the four kernels of a step.
 struct Ctl {
-    unsigned long long epoch;  // internal step counter (>= 1) stamping the per-cell lists
-    long long t;               // the reference's step index t fed to the RNG streams
-    unsigned k1_ticket, k1_wolves_done, k3_ticket, wcell_count;
-    unsigned pool_top, k4_done, needs_blend, error;
-    unsigned run_step, metrics_stride;
-    long long* metrics;  // [R][metrics_stride][4]
+    unsigned pad0;
+    unsigned pool_top;   // bump allocator of the long-list sort pool
+    unsigned error;      // set if the sort pool overflowed (cannot happen: sized N_s + N_w)
+    unsigned occ[2];     // entries in the occupied-cell lists (sheep, wolves) this step
 };
 
 // Per (replica, species) persistent counters + this step's spawn plan.
+// Counters are double-buffered by step parity p = epoch & 1: k_spawn of a step reads
+// next_id[p] and writes next_id[p ^ 1] / num_active[p ^ 1] for the next step.
 struct SpeciesRep {
-    int num_active;
-    int pad;
-    long long next_id;
-    long long base_id;  // first fresh id of this step's births
-    int pairs;          // min(free, valid)
-    int Q;              // valid rows
+    long long next_id[2];
+    int num_active[2];
+    long long base_id;  // first fresh id of the last step's births
+    int pairs;          // min(free, valid) of the last step
+    int Q;              // valid rows of the last step
 };
 
 // Per replica, per parity event accumulators (PredationEvents, predation.hpp:41-57).
@@ -46,9 +48,15 @@ struct Events {
 };
 
 struct Params {
+    // per-step scalars (host-advanced kernel parameters)
+    unsigned long long epoch;  // internal step counter (>= 1) stamping the per-cell lists
+    long long t;               // the reference's step index t fed to the RNG streams
+    long long* metrics;        // [R][metrics_stride][4]
+    unsigned run_step, metrics_stride, needs_blend, pad0;
+    // model constants
     int R, W, H, Cpad;
     long long C;
-    int N[2], Npad[2], tiles[2];
+    int N[2], Npad[2], tiles[2], mtiles[2];
     double gain[2], metab, prob[2], frac;
     unsigned delay_code;
     int spawn_cps, spawn_ctas, regrow_ctas, k2_ctas, status_stride;
@@ -59,16 +67,16 @@ struct Params {
     double* energy[2];
     long long* id[2];
     int* next[2];
-    uint8_t* flag[2];
+    uint8_t* flag[2];   // sheep: eaten this step; wolves: ate this step
+    uint8_t* graze;     // sheep: grazed this step
     int* free_at[2];
     int* row_at[2];
     int* rowcell[2];
     double* rowE[2];
-    unsigned long long* head[2];
+    uint2* cw;  // per-cell list heads {sheep, wolf}, each {epoch8:8 | slot:24}
     uint8_t* g;
-    unsigned long long* smin;
-    unsigned long long* status;
-    unsigned long long* wcells;
+    unsigned long long* status;  // [species][R][status_stride] packed (free, valid) per k_update tile
+    unsigned long long* occ[2];  // occupied cells per species: (replica << 32) | cell
     int* pool;
     long long pool_size;
     Ctl* ctl;
@@ -83,25 +91,22 @@ struct Engine {
     int R = 0;
     Params params{};
     cudaStream_t stream = nullptr;
+    cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
+    cudaGraphNode_t nodes[kNumKernels] = {};
     std::vector<void*> allocs;
     long long device_bytes = 0;
     unsigned long long* d_seeds = nullptr;
     long long* d_metrics_step = nullptr;   // [R][1][4]
     long long* d_run_metrics = nullptr;    // [R][steps][4]
     size_t run_metrics_bytes = 0;
-    long long* cur_metrics = nullptr;      // target currently installed in ctl
-    unsigned cur_stride = 0;
     long long last_run_steps = 0;
-    long long next_t = 1;                  // the t the device will use next
-    unsigned long long host_epoch = 1;     // mirrors ctl->epoch
-    long long staged_t = 0;
-    long long* staged_ptr = nullptr;
-    unsigned staged_u[2] = {0, 0};
+    unsigned long long host_epoch = 1;     // epoch of the next step
     bool timing = false;
     cudaEvent_t tev[2 * kNumKernels] = {};
     double kernel_ms[kNumKernels] = {};
     long long kernel_launches[kNumKernels] = {};
+    size_t spawn_smem = 0;
     void* flush_buf = nullptr;
     size_t flush_cap = 0;
 
@@ -129,6 +134,8 @@ struct Engine {
     int set_t(long long t);
     int set_metrics_target(long long* d_metrics, unsigned stride);
     void launch_step_kernels(bool timed);
+    unsigned grid(int k) const;
+    int build_graph();
     int launch_steps(long long steps);
     int accumulate_times();
 };

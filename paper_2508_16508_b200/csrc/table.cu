@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kThreads) rank_scan_kernel(const uint8_t* __re
                                                              ScanWs* ws) {
     __shared__ unsigned long long s_scan[kThreads / 32 + 1];
     __shared__ unsigned s_tile;
-    __shared__ unsigned long long s_prefix;
+    __shared__ unsigned long long s_look[kThreads / 32 + 2];
     if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
@@ -60,12 +60,9 @@ __global__ void __launch_bounds__(kThreads) rank_scan_kernel(const uint8_t* __re
     for (int k = 0; k < kItems; ++k) cnt += b[k] != 0;
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kThreads>(cnt, s_scan, &total);
-    if (threadIdx.x < 32) {
-        const unsigned long long p = tile_lookback(ws->status, static_cast<int>(tile), total);
-        if (threadIdx.x == 0) s_prefix = p;
-    }
     __syncthreads();
-    int32_t run = static_cast<int32_t>(s_prefix + excl);
+    const unsigned long long tile_prefix = block_lookback<kThreads>(ws->status, static_cast<int>(tile), total, s_look);
+    int32_t run = static_cast<int32_t>(tile_prefix + excl);
     int32_t r[kItems];
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
@@ -116,7 +113,7 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const uint8_t* __rest
                                                            ScanWs* ws) {
     __shared__ unsigned long long s_scan[kThreads / 32 + 1];
     __shared__ unsigned s_tile;
-    __shared__ unsigned long long s_prefix;
+    __shared__ unsigned long long s_look[kThreads / 32 + 2];
     if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
@@ -129,13 +126,10 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const uint8_t* __rest
     for (int k = 0; k < kItems; ++k) cnt += b[k] != 0;
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kThreads>(cnt, s_scan, &total);
-    if (threadIdx.x < 32) {
-        const unsigned long long p = tile_lookback(ws->status, static_cast<int>(tile), total);
-        if (threadIdx.x == 0) s_prefix = p;
-    }
     __syncthreads();
+    const unsigned long long tile_prefix = block_lookback<kThreads>(ws->status, static_cast<int>(tile), total, s_look);
     const size_t T = *true_total;
-    size_t t_run = s_prefix + excl;  // trues before this thread's first element
+    size_t t_run = tile_prefix + excl;  // trues before this thread's first element
     size_t f_run = base - t_run;     // falses before it
 #pragma unroll
     for (int k = 0; k < kItems; ++k) {
