@@ -1,0 +1,169 @@
+"""Generate tests/golden/*.json from the UNMODIFIED reference library (oracle/_ref).
+
+TEST INFRASTRUCTURE ONLY. Run here (where /root/reference exists and `make -C oracle`
+built oracle/_ref/libabmx_ref.so):   python oracle/gen_golden.py
+The fixtures are small and committed; the GPU box never needs /root/reference.
+"""
+import base64
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+sys.path.insert(0, HERE)
+import pyoracle  # noqa: E402
+
+OUT = os.path.join(ROOT, "tests", "golden")
+SIMD_SIZES = [0, 1, 3, 7, 8, 9, 15, 16, 31, 32, 33, 64, 100, 257, 1000, 4096]  # test_simd.cpp:17
+
+
+def b64(a):
+    return base64.b64encode(np.ascontiguousarray(a).tobytes()).decode()
+
+
+def c1(**kw):
+    d = dict(width=100, height=100, n_sheep0=600, n_wolves0=400, sheep_capacity=1024,
+             wolf_capacity=1024, energy_gain_sheep=4.0, energy_gain_wolf=20.0, metabolism=1.0,
+             reproduce_prob_sheep=0.04, reproduce_prob_wolf=0.05, reproduce_energy_frac=0.5,
+             regrow_delay=30)
+    d.update(kw)
+    return d
+
+
+def tiny(**kw):
+    return c1(**dict(dict(width=12, height=12, n_sheep0=30, n_wolves0=15, sheep_capacity=400,
+                          wolf_capacity=400, regrow_delay=10), **kw))
+
+
+def main():
+    ref = pyoracle.Reference()
+    os.makedirs(OUT, exist_ok=True)
+
+    # ---- RNG (test_rng.cpp:18-31 formula replay + SURVEY §8c known answers)
+    rng = {"keys": []}
+    for k in (0, 1, 42, 0xDEADBEEFCAFE, 7):
+        rng["keys"].append({
+            "key": k,
+            "split": [ref.split(k, i) for i in range(16)],
+            "draw": [ref.draw(k, c) for c in range(64)],
+            "uniform_double": [ref.uniform_double(k, c) for c in range(64)],
+            "uniform_int_m5_17": [ref.uniform_int(k, c, -5, 17) for c in range(64)],
+            "uniform_int_0_8": [ref.uniform_int(k, c, 0, 8) for c in range(64)],
+        })
+    rng["replica_seeds_master7"] = [ref.replica_seed(7, r) for r in range(8)]
+    json.dump(rng, open(os.path.join(OUT, "rng.json"), "w"), indent=0)
+
+    # ---- KernelTable (reference scalar table) on seeded masks
+    tab = ref.table(0).struct
+    import ctypes as C
+    u8p, i32p = C.POINTER(C.c_uint8), C.POINTER(C.c_int32)
+    cases = []
+    g = np.random.default_rng(2508)
+    for n in SIMD_SIZES + [12345]:
+        for dens in (0.0, 0.3, 0.5, 1.0):
+            m = (g.random(n) < dens).astype(np.uint8)
+            m[m > 0] = g.integers(1, 256, int(m.sum()), dtype=np.uint8)
+            ranks = np.empty(n, np.int32)
+            comp = np.empty(n, np.int32)
+            tab.rank_scan(m.ctypes.data_as(u8p), ranks.ctypes.data_as(i32p), n)
+            tab.compact_indices(m.ctypes.data_as(u8p), comp.ctypes.data_as(i32p), n)
+            cnt = tab.count_true(m.ctypes.data_as(u8p), n)
+            cases.append({"n": n, "mask": b64(m), "ranks": b64(ranks), "compact": b64(comp),
+                          "count": int(cnt)})
+    json.dump({"source": "reference scalar KernelTable (src/simd/kernels_scalar.cpp)",
+               "cases": cases}, open(os.path.join(OUT, "kernel_table.json"), "w"))
+
+    # ---- predation trajectories
+    def traj(cfgd, seed, steps, every):
+        m = ref.pred(cfgd, seed)
+        rows, hashes, events = [], {0: m.hash(True)}, []
+        for t in range(1, steps + 1):
+            ev = m.step(t)
+            rows.append(m.metrics())
+            events.append(ev)
+            if t % every == 0 or t <= 3:
+                hashes[t] = m.hash(True)
+        return {"config": cfgd, "seed": seed, "steps": steps, "metrics": rows,
+                "hashes": {str(k): v for k, v in hashes.items()}, "events": events}
+
+    seed7 = ref.replica_seed(7, 0)
+    pred = {
+        "hash": "FNV-1a-64 over sheep then wolves of (active u8, ids i64, ages i64, x i64, y i64, "
+                "energy f64) bytes, then grass_ready u8 and regrow i64 (oracle/ref_driver.cpp)",
+        "c1": traj(c1(), seed7, 100, 10),
+        "c1_caps20000": traj(c1(sheep_capacity=20000, wolf_capacity=20000), seed7, 30, 10),
+        "tiny": [traj(tiny(), s, 40, 5) for s in (1, 2, 10, 12)],
+        "tiny_regrow0": traj(tiny(regrow_delay=0), 3, 20, 5),
+        "one_cell": traj(tiny(width=1, height=1, n_sheep0=5, n_wolves0=3), 4, 20, 5),
+        "overflow": traj(tiny(n_sheep0=8, sheep_capacity=8, reproduce_prob_sheep=1.0), 9, 10, 5),
+    }
+    json.dump(pred, open(os.path.join(OUT, "predation.json"), "w"))
+
+    c2 = c1(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000, sheep_capacity=524288,
+            wolf_capacity=524288)
+    json.dump({"c2": traj(c2, seed7, 3, 1)}, open(os.path.join(OUT, "predation_c2.json"), "w"))
+
+    # ---- run_batch (batch.cpp:21-101)
+    K, T = 8, 30
+    rows, _ = ref.run_batch(c1(), 99, K, T, threads=4)
+    json.dump({"config": c1(), "master": 99, "replicas": K, "steps": T, "metrics": rows.tolist()},
+              open(os.path.join(OUT, "batch.json"), "w"))
+
+    # ---- subset updates: set_agents_rm / set_agents_sci / select / sort (kernels.cpp)
+    sub = []
+    g = np.random.default_rng(31337)
+    for trial in range(60):
+        cap = int(g.integers(0, 65))
+        m = int(g.integers(0, 65))
+        inst = dict(
+            active=(g.random(cap) < 0.5).astype(np.uint8), ids=np.arange(cap, dtype=np.int64),
+            ages=g.integers(0, 21, cap).astype(np.int64), e=g.integers(-100, 101, cap).astype(np.int64),
+            w=g.uniform(-10, 10, cap), f=(g.random(cap) < 0.5).astype(np.uint8),
+            target=(g.random(cap) < 0.5).astype(np.uint8), re=g.integers(-100, 101, m).astype(np.int64) + 10000,
+            rw=g.uniform(-10, 10, m), rf=(g.random(m) < 0.5).astype(np.uint8),
+            valid=(g.random(m) < 0.5).astype(np.uint8), key=g.uniform(-5, 5, cap))
+        out = {}
+        for mode, name in ((0, "rm"), (1, "sci")):
+            oe = np.empty(cap, np.int64)
+            ow = np.empty(cap, np.float64)
+            of = np.empty(cap, np.uint8)
+            rc = ref.lib.ref_set_agents(
+                mode, cap, *(inst[k].ctypes.data_as(t) for k, t in (
+                    ("active", u8p), ("ids", pyoracle.i64p), ("ages", pyoracle.i64p),
+                    ("e", pyoracle.i64p), ("w", pyoracle.f64p), ("f", u8p), ("target", u8p))),
+                m, inst["re"].ctypes.data_as(pyoracle.i64p), inst["rw"].ctypes.data_as(pyoracle.f64p),
+                inst["rf"].ctypes.data_as(u8p), inst["valid"].ctypes.data_as(u8p),
+                oe.ctypes.data_as(pyoracle.i64p), ow.ctypes.data_as(pyoracle.f64p), of.ctypes.data_as(u8p))
+            assert rc == 0
+            out[name] = {"e": b64(oe), "w": b64(ow), "f": b64(of)}
+        sel = np.empty(cap, np.int32)
+        cnt = ref.lib.ref_select_mask(inst["target"].ctypes.data_as(u8p), cap, sel.ctypes.data_as(i32p))
+        out["select"] = {"indices": b64(sel), "count": int(cnt)}
+        for desc in (0, 1):
+            oa = np.empty(cap, np.uint8)
+            oi = np.empty(cap, np.int64)
+            og = np.empty(cap, np.int64)
+            oe = np.empty(cap, np.int64)
+            ow = np.empty(cap, np.float64)
+            of = np.empty(cap, np.uint8)
+            rc = ref.lib.ref_sort_agents(
+                cap, inst["active"].ctypes.data_as(u8p), inst["ids"].ctypes.data_as(pyoracle.i64p),
+                inst["ages"].ctypes.data_as(pyoracle.i64p), inst["e"].ctypes.data_as(pyoracle.i64p),
+                inst["w"].ctypes.data_as(pyoracle.f64p), inst["f"].ctypes.data_as(u8p),
+                inst["key"].ctypes.data_as(pyoracle.f64p), desc, oa.ctypes.data_as(u8p),
+                oi.ctypes.data_as(pyoracle.i64p), og.ctypes.data_as(pyoracle.i64p),
+                oe.ctypes.data_as(pyoracle.i64p), ow.ctypes.data_as(pyoracle.f64p), of.ctypes.data_as(u8p))
+            assert rc == 0
+            out["sort_desc" if desc else "sort_asc"] = {"ids": b64(oi), "e": b64(oe)}
+        sub.append({"cap": cap, "m": m, "inputs": {k: b64(v) for k, v in inst.items()}, "out": out})
+    json.dump({"source": "reference set_agents_rm/_sci, compact_mask, sort_agents with the e/w/f "
+                         "copy-apply of tests/support/oracle.cpp", "cases": sub},
+              open(os.path.join(OUT, "subset.json"), "w"))
+    print("golden fixtures written to", OUT)
+
+
+if __name__ == "__main__":
+    main()

@@ -34,7 +34,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_HERE, "libabmx_cuda.so")
+library_path = os.environ.get("ABMX_CUDA_LIB") or os.path.join(_HERE, "libabmx_cuda.so")
 
 
 class AbmxError(RuntimeError):

@@ -194,6 +194,11 @@ __global__ void __launch_bounds__(kT) k_move(Params P) {
 #pragma unroll
             for (int k = 0; k < kM; ++k)
                 if (act[k]) old[k] = atomicExch(&cw[2 * cidx(P, r, cell[k]) + s], (e8 << 24) | static_cast<unsigned>(i0 + k));
+            if (s == 0) {  // k_cells will read these grass bytes: start pulling them into L2 now
+#pragma unroll
+                for (int k = 0; k < kM; ++k)
+                    if (act[k]) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.g + cidx(P, r, cell[k])));
+            }
 #pragma unroll
             for (int k = 0; k < kM; ++k)
                 if (act[k]) {
@@ -269,64 +274,96 @@ constexpr int kSmallList = 8;
 //  * wolf cell: predation — the k-th wolf (slot order) takes the k-th sheep (slot order)
 //    (predation.cpp:197-239); lists come unordered from the exchanges, so both are sorted
 //    (registers for short lists, heap sort in a global scratch pool otherwise).
+__device__ __forceinline__ void wolf_cell(const Params& P, unsigned long long ent, unsigned e8,
+                                          unsigned long long& eaten_out, int& r_out) {
+    const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
+    r_out = r;
+    const uint2 word = P.cw[cidx(P, r, c)];
+    if ((word.x >> 24) != e8) return;  // no sheep in this cell
+    const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
+    const int w0 = static_cast<int>(word.y & kNil), s0 = static_cast<int>(word.x & kNil);
+    // one pass over both lists (interleaved), up to kSmallList each in registers
+    int wl[kSmallList], sl[kSmallList];
+    int lw = 0, ls = 0;
+    for (int w = w0, v = s0; w >= 0 || v >= 0;) {
+        const int nw = w >= 0 ? P.next[1][wb + w] : -1;
+        const int nv = v >= 0 ? P.next[0][sb + v] : -1;
+        if (w >= 0) {
+            if (lw < kSmallList) wl[lw] = w;
+            ++lw;
+        }
+        if (v >= 0) {
+            if (ls < kSmallList) sl[ls] = v;
+            ++ls;
+        }
+        w = nw;
+        v = nv;
+    }
+    const int pairs = lw < ls ? lw : ls;
+    if (lw <= kSmallList && ls <= kSmallList) {
+        insertion_sort(wl, lw);
+        insertion_sort(sl, ls);
+        for (int q = 0; q < pairs; ++q) {
+            P.flag[0][sb + sl[q]] = 1;  // eaten
+            P.flag[1][wb + wl[q]] = 1;  // ate
+        }
+    } else {  // long lists (crowded cells): heap sort in the global scratch pool
+        const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
+        if (static_cast<long long>(off) + lw + ls > P.pool_size) {
+            atomicExch(&P.ctl->error, 1u);
+            return;
+        }
+        int* pw = P.pool + off;
+        int* ps = pw + lw;
+        int q = 0;
+        for (int w = w0; w >= 0; w = P.next[1][wb + w]) pw[q++] = w;
+        q = 0;
+        for (int v = s0; v >= 0; v = P.next[0][sb + v]) ps[q++] = v;
+        heap_sort(pw, lw);
+        heap_sort(ps, ls);
+        for (q = 0; q < pairs; ++q) {
+            P.flag[0][sb + ps[q]] = 1;
+            P.flag[1][wb + pw[q]] = 1;
+        }
+    }
+    eaten_out = static_cast<unsigned long long>(pairs);
+}
+
+// One work item per occupied (cell, species) — wolf cells first, so the longer pairing chains
+// start earliest, and no thread runs both kinds:
+//  * wolf cell: predation — the k-th wolf (slot order) takes the k-th sheep (slot order)
+//    (predation.cpp:197-239); lists come unordered from the exchanges, so both are sorted.
+//  * sheep cell: graze — the LOWEST sheep slot of the cell eats if the cell is ready
+//    (predation.cpp:178-195); the winner gets a graze flag, the cell its regrow code.
 __global__ void __launch_bounds__(kT) k_cells(Params P) {
     const unsigned e8 = epoch8(P.epoch);
     const unsigned ns = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[0]);
     const unsigned nw = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[1]);
-    Events* ev = P.ev + static_cast<size_t>(P.epoch & 1) * P.R;
     const unsigned stride = gridDim.x * kT;
-    for (unsigned e = blockIdx.x * kT + threadIdx.x; e < ns; e += stride) {
-        const unsigned long long ent = P.occ[0][e];
-        const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
-        const size_t ci = cidx(P, r, c);
-        const size_t sb = static_cast<size_t>(r) * P.Npad[0];
-        const uint8_t gv = P.g[ci];  // independent of the list walk: issue first
-        int m = static_cast<int>(reinterpret_cast<const unsigned*>(P.cw)[2 * ci] & kNil);
-        for (int v = P.next[0][sb + m]; v >= 0; v = P.next[0][sb + v]) m = v < m ? v : m;
-        if (gv == 0) {
-            P.g[ci] = static_cast<uint8_t>(P.delay_code);
-            P.graze[sb + m] = 1;
-        }
-    }
-    for (unsigned e = blockIdx.x * kT + threadIdx.x; e < nw; e += stride) {
-        const unsigned long long ent = P.occ[1][e];
-        const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
-        const uint2 word = P.cw[cidx(P, r, c)];
-        if ((word.x >> 24) != e8) continue;  // no sheep in this cell
-        const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
-        const int w0 = static_cast<int>(word.y & kNil), s0 = static_cast<int>(word.x & kNil);
-        int lw = 0, ls = 0;
-        for (int w = w0; w >= 0; w = P.next[1][wb + w]) ++lw;
-        for (int v = s0; v >= 0; v = P.next[0][sb + v]) ++ls;
-        const int pairs = lw < ls ? lw : ls;
-        int wl_r[kSmallList], sl_r[kSmallList];
-        int *wl = wl_r, *sl = sl_r;
-        const bool small = lw <= kSmallList && ls <= kSmallList;
-        if (!small) {
-            const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
-            if (static_cast<long long>(off) + lw + ls > P.pool_size) {
-                atomicExch(&P.ctl->error, 1u);
-                continue;
+    const unsigned* cw32 = reinterpret_cast<const unsigned*>(P.cw);
+    for (unsigned q = blockIdx.x * kT + threadIdx.x; q - threadIdx.x < nw + ns; q += stride) {
+        unsigned long long eaten = 0;
+        int rw = -1;
+        if (q < nw) {
+            wolf_cell(P, P.occ[1][q], e8, eaten, rw);
+        } else if (q < nw + ns) {
+            const unsigned long long ent = P.occ[0][q - nw];
+            const int r = static_cast<int>(ent >> 32);
+            const size_t ci = cidx(P, r, static_cast<int>(static_cast<uint32_t>(ent)));
+            const size_t sb = static_cast<size_t>(r) * P.Npad[0];
+            const uint8_t gv = P.g[ci];  // independent of the list walk: issued together
+            int m = static_cast<int>(cw32[2 * ci] & kNil);
+            for (int v = P.next[0][sb + m]; v >= 0; v = P.next[0][sb + v]) m = v < m ? v : m;
+            if (gv == 0) {
+                P.g[ci] = static_cast<uint8_t>(P.delay_code);
+                P.graze[sb + m] = 1;
             }
-            wl = P.pool + off;
-            sl = wl + lw;
         }
-        int q = 0;
-        for (int w = w0; w >= 0; w = P.next[1][wb + w]) wl[q++] = w;
-        q = 0;
-        for (int v = s0; v >= 0; v = P.next[0][sb + v]) sl[q++] = v;
-        if (small) {
-            insertion_sort(wl, lw);
-            insertion_sort(sl, ls);
-        } else {
-            heap_sort(wl, lw);
-            heap_sort(sl, ls);
-        }
-        for (q = 0; q < pairs; ++q) {
-            P.flag[0][sb + sl[q]] = 1;  // eaten
-            P.flag[1][wb + wl[q]] = 1;  // ate
-        }
-        atomicAdd(&ev[r].sheep_eaten, static_cast<unsigned long long>(pairs));
+        // per-replica predation count: lanes sharing a replica combine (one atomic each)
+        const unsigned grp = __match_any_sync(0xffffffffu, rw);
+        const unsigned long long tot = __reduce_add_sync(grp, static_cast<unsigned>(eaten));
+        if (rw >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot)
+            atomicAdd(&P.ev[static_cast<size_t>(P.epoch & 1) * P.R + rw].sheep_eaten, tot);
     }
 }
 
@@ -340,6 +377,7 @@ __global__ void __launch_bounds__(kT) k_cells(Params P) {
 __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ long long s_red[kT / 32];
+    __shared__ long long s_red2[kT / 32];
     const unsigned slot_ctas = static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
     if (blockIdx.x >= slot_ctas) {
         // regrow: 16 cells per thread (Cpad is a multiple of 16: a chunk never straddles replicas)
@@ -495,10 +533,31 @@ __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
     }
     // event reductions + the tile's (free, valid) counts
     Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
-    const long long g_sum = block_sum<long long>(n_graze, s_red);
-    const long long m_sum = block_sum<long long>(n_metab, s_red);
-    const long long d_sum = block_sum<long long>(n_death, s_red);
-    const long long x_sum = block_sum<long long>(fx_removed, s_red);
+    // one reduction for the four counters: (graze, metab, death) packed 21 bits each, + energy
+    unsigned long long cnt = (static_cast<unsigned long long>(n_graze) << 42) |
+                             (static_cast<unsigned long long>(n_metab) << 21) | n_death;
+    long long fx = fx_removed;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+        fx += __shfl_xor_sync(0xffffffffu, fx, d);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_red[threadIdx.x >> 5] = static_cast<long long>(cnt);
+        s_red2[threadIdx.x >> 5] = fx;
+    }
+    __syncthreads();
+    long long g_sum = 0, m_sum = 0, d_sum = 0, x_sum = 0;
+    if (threadIdx.x == 0) {
+        unsigned long long c = 0;
+        for (int w = 0; w < kT / 32; ++w) {
+            c += static_cast<unsigned long long>(s_red[w]);
+            x_sum += s_red2[w];
+        }
+        g_sum = static_cast<long long>(c >> 42);
+        m_sum = static_cast<long long>((c >> 21) & 0x1FFFFF);
+        d_sum = static_cast<long long>(c & 0x1FFFFF);
+    }
     if (threadIdx.x == 0) {
         P.status[(static_cast<size_t>(s) * P.R + r) * P.status_stride + tile] = tile_total;
         if (g_sum) atomicAdd(&ev->grass_eaten, static_cast<unsigned long long>(g_sum));
@@ -1153,11 +1212,22 @@ int Engine::birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t c
     return sr.pairs;
 }
 
-// L2 flush: overwrite a buffer larger than the 126 MB L2 between timed steps.
+// L2 flush between timed steps: overwrite a buffer larger than the 126 MB L2, then read a
+// second one so L2 is left holding CLEAN lines (otherwise the timed step would pay for
+// writing back the flush buffer's dirty lines, traffic that is not part of the workload).
 __global__ void k_flush(uint4* p, size_t n) {
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
         p[i] = make_uint4(static_cast<unsigned>(i), 0u, 0u, 0u);
+}
+__global__ void k_flush_read(const uint4* p, size_t n, unsigned* sink) {
+    unsigned acc = 0;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint4 v = p[i];
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x9E3779B9u) *sink = acc;  // practically never; keeps the loads alive
 }
 
 int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_kernel, double* step_ms) {
@@ -1177,31 +1247,67 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
     if (rc) return rc;
     if (flush_bytes > flush_cap) {
         if (flush_buf) cudaFree(flush_buf);
-        CK(cudaMalloc(&flush_buf, flush_bytes));
+        CK(cudaMalloc(&flush_buf, 2 * flush_bytes + 64));
+        CK(cudaMemset(flush_buf, 0, 2 * flush_bytes + 64));
         flush_cap = flush_bytes;
     }
-    std::vector<cudaEvent_t> ev(2 * static_cast<size_t>(steps));
+    // per-kernel mode records 2 events around every kernel of every step and synchronises
+    // only at the end, so host launch latency never lands inside a kernel's bracket
+    const size_t per_step = per_kernel ? 2 * kNumKernels : 2;
+    std::vector<cudaEvent_t> ev(per_step * static_cast<size_t>(steps));
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    const bool saved_timing = timing;
-    timing = per_kernel;
+    if (!per_kernel && !graph_exec) {
+        rc = build_graph();
+        if (rc) return rc;
+    }
+    (void)cudaGetLastError();
     for (long long q = 0; q < steps; ++q) {
         if (flush_bytes) {
-            k_flush<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(static_cast<uint4*>(flush_buf), flush_bytes / 16);
+            uint4* fb = static_cast<uint4*>(flush_buf);
+            k_flush<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(fb, flush_bytes / 16);
+            k_flush_read<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(
+                fb + flush_bytes / 16, flush_bytes / 16, reinterpret_cast<unsigned*>(fb + flush_bytes / 8));
         }
-        CK(cudaEventRecord(ev[2 * q], stream));
-        rc = launch_steps(1);
-        if (rc) {
-            timing = saved_timing;
-            return rc;
+        cudaEvent_t* e = &ev[per_step * static_cast<size_t>(q)];
+        if (per_kernel) {
+            params.epoch = host_epoch;
+            if (host_epoch % kEpochClear == 0)
+                CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 8, stream));
+            void* args[1] = {&params};
+            for (int k = 0; k < kNumKernels; ++k) {
+                CK(cudaEventRecord(e[2 * k], stream));
+                CK(cudaLaunchKernel(kKernelFns[k], dim3(grid(k)), dim3(kT), args, k == 3 ? spawn_smem : 0, stream));
+                CK(cudaEventRecord(e[2 * k + 1], stream));
+            }
+            abmx_internal::count_launch(kNumKernels);
+            params.needs_blend = 0;
+            params.t += 1;
+            params.run_step += 1;
+            ++host_epoch;
+        } else {
+            CK(cudaEventRecord(e[0], stream));
+            rc = launch_steps(1);
+            if (rc) return rc;
+            CK(cudaEventRecord(e[1], stream));
         }
-        CK(cudaEventRecord(ev[2 * q + 1], stream));
     }
-    timing = saved_timing;
     CK(cudaStreamSynchronize(stream));
     for (long long q = 0; q < steps; ++q) {
+        cudaEvent_t* e = &ev[per_step * static_cast<size_t>(q)];
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, ev[2 * q], ev[2 * q + 1]));
-        step_ms[q] = ms;
+        if (per_kernel) {
+            double tot = 0.0;
+            for (int k = 0; k < kNumKernels; ++k) {
+                CK(cudaEventElapsedTime(&ms, e[2 * k], e[2 * k + 1]));
+                kernel_ms[k] += ms;
+                kernel_launches[k] += 1;
+                tot += ms;
+            }
+            step_ms[q] = tot;
+        } else {
+            CK(cudaEventElapsedTime(&ms, e[0], e[1]));
+            step_ms[q] = ms;
+        }
     }
     for (auto& e : ev) cudaEventDestroy(e);
     last_run_steps = steps;

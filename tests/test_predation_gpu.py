@@ -217,3 +217,47 @@ def test_create_errors(abmx):
         abmx.PredationModel(abmx.PredationConfig(**tiny(n_sheep0=500)), 1)
     with pytest.raises(abmx.DomainError):
         abmx.PredationModel(abmx.PredationConfig(**tiny(regrow_delay=300)), 1)
+
+
+# ---------------------------------------------------------------------- golden fixtures
+def _golden(name):
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", name)) as f:
+        return json.load(f)
+
+
+def _run_golden(abmx, tr):
+    m = abmx.PredationModel(abmx.PredationConfig(**tr["config"]), tr["seed"])
+    assert state_hash(m) == tr["hashes"]["0"]
+    for t in range(1, tr["steps"] + 1):
+        m.step(t)
+        assert m.collect_metrics()[0].tolist() == tr["metrics"][t - 1], t
+        ev = m.last_events()
+        want = tr["events"][t - 1]
+        assert ev.grass_eaten == want["grass_eaten"] and ev.sheep_eaten_by_wolves == want["sheep_eaten_by_wolves"]
+        if str(t) in tr["hashes"]:
+            assert state_hash(m) == tr["hashes"][str(t)], t
+
+
+@pytest.mark.parametrize("name", ["c1", "c1_caps20000", "tiny_regrow0", "one_cell", "overflow"])
+def test_golden_trajectories_from_reference(abmx, name):
+    """Fixtures generated from the unmodified reference (oracle/gen_golden.py)."""
+    _run_golden(abmx, _golden("predation.json")[name])
+
+
+def test_golden_tiny_from_reference(abmx):
+    for tr in _golden("predation.json")["tiny"]:
+        _run_golden(abmx, tr)
+
+
+def test_golden_c2_from_reference(abmx):
+    _run_golden(abmx, _golden("predation_c2.json")["c2"])
+
+
+def test_golden_run_batch_from_reference(abmx):
+    g = _golden("batch.json")
+    for path in (1, 2):
+        got, _ = abmx.run_batch(abmx.PredationConfig(**g["config"]), g["master"], g["replicas"],
+                                g["steps"], path=path)
+        assert np.array_equal(got, np.array(g["metrics"])), path

@@ -135,3 +135,16 @@ def test_device_pointer_variants_unaligned(abmx, oracle):
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy()[1:], oracle.rank_scan(host[1:]))
     assert int(cnt.item()) == oracle.count_true(host[1:])
+
+
+def test_golden_kernel_table_from_reference(abmx):
+    import base64
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "kernel_table.json")) as f:
+        cases = json.load(f)["cases"]
+    for c in cases:
+        m = np.frombuffer(base64.b64decode(c["mask"]), np.uint8)
+        assert np.array_equal(abmx.rank_scan(m), np.frombuffer(base64.b64decode(c["ranks"]), np.int32))
+        assert np.array_equal(abmx.compact_indices(m), np.frombuffer(base64.b64decode(c["compact"]), np.int32))
+        assert abmx.count_true(m) == c["count"]
