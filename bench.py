@@ -157,8 +157,8 @@ def kernel_bytes(cfg, births_deaths):
     cells = cfg["width"] * cfg["height"]
     return {"k_move": 25 * n,                  # x,y,age read+write (2*(4+4+4)) + active read (1)
             "k_cells": 0,                      # per-cell list scratch only, not counted by §8d
-            "k_update": 17 * n + 2 * cells,    # energy r+w (16) + active write (1) + regrow sweep
-            "k_spawn": 8 * births_deaths}      # id writes of births (+ zeroed ids of deaths)
+            "k_update": 17 * n,                # energy read+write (2*8) + active write (1)
+            "k_spawn": 2 * cells + 8 * births_deaths}  # regrow sweep (u8 r+w) + id writes
 
 
 def our_arm(args, rank, world, local_rank, dist):

@@ -151,6 +151,15 @@ void* abmx_predation_stream(abmx_predation* h);
  * milliseconds and launch counts per kernel (names via abmx_predation_kernel_name). */
 int abmx_predation_set_timing(abmx_predation* h, int enabled);
 int32_t abmx_predation_kernel_count(void);
+/* Step launch mode: 1 (default) = four per-phase kernels in a CUDA graph; 0 = the whole step
+ * as ONE persistent cooperative kernel with grid-wide barriers between its phases. Results
+ * are bit-identical; per-kernel timing always uses the per-phase kernels. */
+int abmx_predation_set_mode(abmx_predation* h, int32_t mode);
+/* Fused-mode phase timing from the device clock (%globaltimer, CTA 0 after each grid
+ * barrier). enable = 1 zeroes and turns on the accumulators, -1 only reads, 0 reads and turns
+ * off. ns_out (nullable) receives the accumulated nanoseconds of [move+bin, cells,
+ * update+regrow, spawn]. */
+int abmx_predation_phase_times(abmx_predation* h, int32_t enable, double* ns_out);
 const char* abmx_predation_kernel_name(int32_t k);
 int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches);
 /* device-resident bytes of h (state + scratch) */

@@ -31,6 +31,9 @@
 #include "abmx_internal.h"
 #include "predation_engine.h"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 using namespace abmx_dev;
 
 namespace abmx_pred {
@@ -102,16 +105,23 @@ __device__ __forceinline__ T block_sum(T v, T* smem) {
     return t;  // valid in thread 0
 }
 
-// ============================================================== per-cell lists
-// One uint2 per cell: .x = sheep list head, .y = wolf list head, each {epoch8:8 | slot:24}.
-// A head is current iff its epoch byte equals this step's epoch8 (so nothing is cleared
-// per step); the host zeroes the array every kEpochClear steps, before epoch8 can alias.
+// ============================================================== per-cell words
+// One uint4 per cell:
+//   .x sheep list head {epoch8:8 | slot:24}      (atomicExch; the list links through next[0])
+//   .y wolf  list head {epoch8:8 | slot:24}      (atomicExch; links through next[1])
+//   .z lowest sheep slot {tag:8 | ~slot:24}      (atomicMax, fire-and-forget), tag = epoch%128 + 1
+// A head / minimum is current iff its tag equals this step's; nothing is cleared per step.
+// The host zeroes the array every kEpochClear (= 128) steps, so tags never alias and the
+// .z tag of the current step is the largest one alive (a max-reduction keeps it).
 __device__ __forceinline__ unsigned epoch8(unsigned long long epoch) {
     return static_cast<unsigned>(epoch % 255ULL) + 1u;  // 1..255, never the cleared 0
 }
+__device__ __forceinline__ unsigned min_tag(unsigned long long epoch) {
+    return static_cast<unsigned>(epoch % kEpochClear) + 1u;  // 1..128, grows within a clear window
+}
 constexpr unsigned kNil = 0xFFFFFFu;  // end of list
 
-// blockIdx -> (species, replica, tile) for the per-slot kernels: sheep tiles first.
+// blockIdx -> (species, replica, tile) for the per-slot phases: sheep tiles first.
 __device__ __forceinline__ void tile_of(const Params& P, unsigned b, int tiles0, int tiles1, int& s, int& r,
                                         int& tile) {
     const unsigned sheep_ctas = static_cast<unsigned>(P.R * tiles0);
@@ -133,22 +143,22 @@ __device__ __forceinline__ void load4_u8(const uint8_t* p, uint8_t (&v)[4]) {
     for (int k = 0; k < 4; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
 }
 
-// ============================================================== K1: move + bin
-// step_agents with the move transition (predation.cpp:35-49, lifecycle.cpp:87-122), then each
-// live agent pushes itself onto its new cell's list with one atomicExch. The agent that finds
-// a stale head is the first in its cell this step and records the cell in the occupied-cell
-// list of its species (one block-aggregated atomic per CTA).
-__global__ void __launch_bounds__(kT) k_move(Params P) {
+// ============================================================== phase 1: move + bin
+// step_agents with the move transition (predation.cpp:35-49, lifecycle.cpp:87-122). Every
+// live agent then pushes itself onto its new cell's list (one atomicExch); sheep also post
+// their slot to the cell's lowest-slot word (atomicMax, no return) and prefetch the cell's
+// grass byte for phase 3. The first wolf of a cell records it in the wolf-cell list.
+__device__ void move_phase(const Params& P, unsigned b, unsigned nb) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ unsigned s_base;
     const unsigned long long epoch = P.epoch;
-    const unsigned e8 = epoch8(epoch);
+    const unsigned e8 = epoch8(epoch), tag = min_tag(epoch);
     int s, r, tile;
-    tile_of(P, blockIdx.x, P.mtiles[0], P.mtiles[1], s, r, tile);
-    // zero this parity's event accumulators (consumed by K2..K4 of this step)
+    tile_of(P, b, P.mtiles[0], P.mtiles[1], s, r, tile);
+    // zero this parity's event accumulators (consumed by the later phases of this step)
     {
         Events* ev = P.ev + static_cast<size_t>(epoch & 1) * P.R;
-        for (unsigned rr = blockIdx.x * kT + threadIdx.x; rr < static_cast<unsigned>(P.R); rr += gridDim.x * kT)
+        for (unsigned rr = b * kT + threadIdx.x; rr < static_cast<unsigned>(P.R); rr += nb * kT)
             memset(&ev[rr], 0, sizeof(Events));
     }
     const unsigned long long key = split(split(split(P.seeds[r], 3), static_cast<unsigned long long>(P.t)), s);
@@ -188,23 +198,26 @@ __global__ void __launch_bounds__(kT) k_move(Params P) {
                 cell[k] = ny * W + nx;
                 age[k] += 1;
             }
-            // push onto the cell lists: exchanges issued back to back, then consumed
             unsigned* cw = reinterpret_cast<unsigned*>(P.cw);
             unsigned old[kM];
 #pragma unroll
             for (int k = 0; k < kM; ++k)
-                if (act[k]) old[k] = atomicExch(&cw[2 * cidx(P, r, cell[k]) + s], (e8 << 24) | static_cast<unsigned>(i0 + k));
-            if (s == 0) {  // k_cells will read these grass bytes: start pulling them into L2 now
+                if (act[k]) old[k] = atomicExch(&cw[4 * cidx(P, r, cell[k]) + s], (e8 << 24) | static_cast<unsigned>(i0 + k));
+            if (s == 0) {
 #pragma unroll
                 for (int k = 0; k < kM; ++k)
-                    if (act[k]) asm volatile("prefetch.global.L2 [%0];" ::"l"(P.g + cidx(P, r, cell[k])));
+                    if (act[k]) {
+                        const size_t ci = cidx(P, r, cell[k]);
+                        atomicMax(&cw[4 * ci + 2], (tag << 24) | (kNil - static_cast<unsigned>(i0 + k)));
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.g + ci));
+                    }
             }
 #pragma unroll
             for (int k = 0; k < kM; ++k)
                 if (act[k]) {
                     const bool cur = (old[k] >> 24) == e8;
                     P.next[s][base + k] = cur ? static_cast<int>(old[k] & kNil) : -1;
-                    first[k] = !cur;
+                    first[k] = s == 1 && !cur;
                 }
             *reinterpret_cast<int4*>(P.cell[s] + base) = make_int4(cell[0], cell[1], cell[2], cell[3]);
             *reinterpret_cast<int4*>(P.age[s] + base) = make_int4(age[0], age[1], age[2], age[3]);
@@ -218,21 +231,22 @@ __global__ void __launch_bounds__(kT) k_move(Params P) {
                 }
         }
     }
-    // append the cells this thread opened to the occupied-cell list of species s
-    const unsigned nfirst = first[0] + first[1] + first[2] + first[3];
-    unsigned long long total;
-    const unsigned long long off = block_excl_scan<kT>(nfirst, s_scan, &total);
-    if (threadIdx.x == 0 && total) s_base = atomicAdd(&P.ctl->occ[s], static_cast<unsigned>(total));
-    __syncthreads();
-    if (nfirst) {
-        unsigned pos = s_base + static_cast<unsigned>(off);
+    if (s == 1) {  // block-aggregated append of the cells this thread's wolves opened
+        const unsigned nfirst = first[0] + first[1] + first[2] + first[3];
+        unsigned long long total;
+        const unsigned long long off = block_excl_scan<kT>(nfirst, s_scan, &total);
+        if (threadIdx.x == 0 && total) s_base = atomicAdd(&P.ctl->occ[1], static_cast<unsigned>(total));
+        __syncthreads();
+        if (nfirst) {
+            unsigned pos = s_base + static_cast<unsigned>(off);
 #pragma unroll
-        for (int k = 0; k < kM; ++k)
-            if (first[k]) P.occ[s][pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
+            for (int k = 0; k < kM; ++k)
+                if (first[k]) P.occ[1][pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
+        }
     }
 }
 
-// ============================================================== K2: occupied cells
+// ============================================================== phase 2: predation pairing
 __device__ void insertion_sort(int* a, int n) {
     for (int i = 1; i < n; ++i) {
         const int v = a[i];
@@ -268,18 +282,10 @@ __device__ void heap_sort(int* a, int n) {
 
 constexpr int kSmallList = 8;
 
-// One thread per occupied (cell, species):
-//  * sheep cell: graze — the LOWEST sheep slot of the cell eats if the cell is ready
-//    (predation.cpp:178-195); the winner gets a graze flag, the cell its regrow code.
-//  * wolf cell: predation — the k-th wolf (slot order) takes the k-th sheep (slot order)
-//    (predation.cpp:197-239); lists come unordered from the exchanges, so both are sorted
-//    (registers for short lists, heap sort in a global scratch pool otherwise).
-__device__ __forceinline__ void wolf_cell(const Params& P, unsigned long long ent, unsigned e8,
-                                          unsigned long long& eaten_out, int& r_out) {
+__device__ __forceinline__ unsigned long long wolf_cell(const Params& P, unsigned long long ent, unsigned e8) {
     const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
-    r_out = r;
-    const uint2 word = P.cw[cidx(P, r, c)];
-    if ((word.x >> 24) != e8) return;  // no sheep in this cell
+    const uint2 word = *reinterpret_cast<const uint2*>(&P.cw[cidx(P, r, c)]);
+    if ((word.x >> 24) != e8) return 0;  // no sheep in this cell
     const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
     const int w0 = static_cast<int>(word.y & kNil), s0 = static_cast<int>(word.x & kNil);
     // one pass over both lists (interleaved), up to kSmallList each in registers
@@ -311,7 +317,7 @@ __device__ __forceinline__ void wolf_cell(const Params& P, unsigned long long en
         const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
         if (static_cast<long long>(off) + lw + ls > P.pool_size) {
             atomicExch(&P.ctl->error, 1u);
-            return;
+            return 0;
         }
         int* pw = P.pool + off;
         int* ps = pw + lw;
@@ -326,38 +332,22 @@ __device__ __forceinline__ void wolf_cell(const Params& P, unsigned long long en
             P.flag[1][wb + pw[q]] = 1;
         }
     }
-    eaten_out = static_cast<unsigned long long>(pairs);
+    return static_cast<unsigned long long>(pairs);
 }
 
-// One work item per occupied (cell, species) — wolf cells first, so the longer pairing chains
-// start earliest, and no thread runs both kinds:
-//  * wolf cell: predation — the k-th wolf (slot order) takes the k-th sheep (slot order)
-//    (predation.cpp:197-239); lists come unordered from the exchanges, so both are sorted.
-//  * sheep cell: graze — the LOWEST sheep slot of the cell eats if the cell is ready
-//    (predation.cpp:178-195); the winner gets a graze flag, the cell its regrow code.
-__global__ void __launch_bounds__(kT) k_cells(Params P) {
+// One work item per cell holding >= 1 wolf: the k-th wolf (slot order) takes the k-th sheep
+// (slot order) of the cell (predation.cpp:197-239). Lists come unordered from the exchanges,
+// so both are sorted by slot first.
+__device__ void cells_phase(const Params& P, unsigned q0, unsigned stride) {
     const unsigned e8 = epoch8(P.epoch);
-    const unsigned ns = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[0]);
     const unsigned nw = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[1]);
-    const unsigned stride = gridDim.x * kT;
-    const unsigned* cw32 = reinterpret_cast<const unsigned*>(P.cw);
-    for (unsigned q = blockIdx.x * kT + threadIdx.x; q - threadIdx.x < nw + ns; q += stride) {
+    for (unsigned q = q0; q - threadIdx.x < nw; q += stride) {
         unsigned long long eaten = 0;
         int rw = -1;
         if (q < nw) {
-            wolf_cell(P, P.occ[1][q], e8, eaten, rw);
-        } else if (q < nw + ns) {
-            const unsigned long long ent = P.occ[0][q - nw];
-            const int r = static_cast<int>(ent >> 32);
-            const size_t ci = cidx(P, r, static_cast<int>(static_cast<uint32_t>(ent)));
-            const size_t sb = static_cast<size_t>(r) * P.Npad[0];
-            const uint8_t gv = P.g[ci];  // independent of the list walk: issued together
-            int m = static_cast<int>(cw32[2 * ci] & kNil);
-            for (int v = P.next[0][sb + m]; v >= 0; v = P.next[0][sb + v]) m = v < m ? v : m;
-            if (gv == 0) {
-                P.g[ci] = static_cast<uint8_t>(P.delay_code);
-                P.graze[sb + m] = 1;
-            }
+            const unsigned long long ent = P.occ[1][q];
+            rw = static_cast<int>(ent >> 32);
+            eaten = wolf_cell(P, ent, e8);
         }
         // per-replica predation count: lanes sharing a replica combine (one atomic each)
         const unsigned grp = __match_any_sync(0xffffffffu, rw);
@@ -367,62 +357,21 @@ __global__ void __launch_bounds__(kT) k_cells(Params P) {
     }
 }
 
-// ============================================================== K3: per-slot update
-// Streams every slot once: graze gain, predation kill / gain, metabolise, starve, reproduce
-// (predation.cpp:178-250). Each tile compacts its own free slots and valid rows (tile-local
-// ranks from one block scan of packed (free, valid) counters) and publishes its two counts;
-// no tile waits on another — the global ranks are resolved in k_spawn.
-// CTAs past the slot tiles run the cell regrow sweep (predation.cpp:252-258) and count ready
-// cells for the metrics row.
-__global__ void __launch_bounds__(kT, 4) k_update(Params P) {
+// ============================================================== phase 3: per-slot update
+// Streams every slot once: graze (the lowest sheep slot of a ready cell eats, predation.cpp:
+// 178-195, decided from the cell's lowest-slot word), predation kill / gain, metabolise,
+// starve, reproduce (predation.cpp:197-250). Each tile compacts its own free slots and valid
+// rows (tile-local ranks from one block scan of packed (free, valid) counters) and publishes
+// its two counts; no tile waits on another — global ranks are resolved in phase 4.
+__device__ void update_phase(const Params& P, unsigned b) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ long long s_red[kT / 32];
     __shared__ long long s_red2[kT / 32];
-    const unsigned slot_ctas = static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
-    if (blockIdx.x >= slot_ctas) {
-        // regrow: 16 cells per thread (Cpad is a multiple of 16: a chunk never straddles replicas)
-        const size_t nchunk = static_cast<size_t>(P.R) * P.Cpad / 16;
-        const size_t stride = static_cast<size_t>(gridDim.x - slot_ctas) * kT;
-        for (size_t q = static_cast<size_t>(blockIdx.x - slot_ctas) * kT + threadIdx.x; q - threadIdx.x < nchunk; q += stride) {
-            unsigned ready = 0;
-            int r = -1;
-            if (q < nchunk) {
-                const size_t c0 = q * 16;
-                r = static_cast<int>(c0 / P.Cpad);
-                uint4 v = *reinterpret_cast<const uint4*>(P.g + c0);
-                uint32_t w[4] = {v.x, v.y, v.z, v.w};
-                bool changed = false;
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint32_t o = 0;
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        uint32_t x = (w[j] >> (8 * b)) & 0xFF;
-                        if (x >= 1 && x <= 254) {
-                            --x;
-                            changed = true;
-                        }
-                        ready += x == 0;
-                        o |= x << (8 * b);
-                    }
-                    w[j] = o;
-                }
-                if (changed) *reinterpret_cast<uint4*>(P.g + c0) = make_uint4(w[0], w[1], w[2], w[3]);
-            }
-            // per-replica grass count, aggregated over the lanes of a warp sharing a replica
-            const unsigned grp = __match_any_sync(0xffffffffu, r);
-            const unsigned tot = __reduce_add_sync(grp, ready);
-            if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot) {
-                long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
-                atomicAdd(reinterpret_cast<unsigned long long*>(&row[2]), static_cast<unsigned long long>(tot));
-            }
-        }
-        return;
-    }
     const unsigned long long epoch = P.epoch;
     const int p = static_cast<int>(epoch & 1);
+    const unsigned tag = min_tag(epoch);
     int s, r, tile;
-    tile_of(P, blockIdx.x, P.tiles[0], P.tiles[1], s, r, tile);
+    tile_of(P, b, P.tiles[0], P.tiles[1], s, r, tile);
     const unsigned long long key = split(split(split(P.seeds[r], 4), static_cast<unsigned long long>(P.t)), s);
     const int N = P.N[s];
     const int i0 = tile * kTile + threadIdx.x * kS;
@@ -431,6 +380,7 @@ __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
 
     uint8_t act[kS];
     double E[kS], child[kS];
+    int cell[kS];
     bool valid[kS], freek[kS];
     unsigned n_graze = 0, n_metab = 0, n_death = 0;
     long long fx_removed = 0;
@@ -439,33 +389,61 @@ __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
         valid[k] = false;
         freek[k] = false;
         child[k] = 0.0;
+        cell[k] = 0;
     }
     if (i0 < N) {
-        uint8_t flg[kS], grz[kS];
+        uint8_t flg[kS];
         load8_u8(P.active[s] + base, act);
         load8_u8(P.flag[s] + base, flg);
-        if (s == 0) load8_u8(P.graze + base, grz);
-        bool any = false, anyflag = false, anygrz = false;
-        if (s == 0) load8_f64(P.energy[s] + base, E);  // dense: issue with the masks
+        bool any = false, anyflag = false;
+        if (s == 0) {  // dense species: issue the column loads with the masks
+            load8_f64(P.energy[s] + base, E);
+            const int4 cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
+            cell[0] = cv.x;
+            cell[1] = cv.y;
+            cell[2] = cv.z;
+            cell[3] = cv.w;
+        }
 #pragma unroll
         for (int k = 0; k < kS; ++k) {
             any |= act[k] != 0;
             anyflag |= flg[k] != 0;
-            if (s == 0) anygrz |= grz[k] != 0;
         }
-        if (s == 1 && any) load8_f64(P.energy[s] + base, E);
+        if (s == 1 && any) {
+            load8_f64(P.energy[s] + base, E);
+            const int4 cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
+            cell[0] = cv.x;
+            cell[1] = cv.y;
+            cell[2] = cv.z;
+            cell[3] = cv.w;
+        }
         const uint8_t z[kS] = {};
         if (anyflag) store8_u8(P.flag[s] + base, z);
-        if (anygrz) store8_u8(P.graze + base, z);
+        if (s == 0 && any) {
+            // graze: lowest-slot word and grass byte of every live sheep's cell, in parallel
+            const unsigned* cw = reinterpret_cast<const unsigned*>(P.cw);
+            unsigned mw[kS];
+            uint8_t gv[kS];
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                if (act[k]) {
+                    const size_t ci = cidx(P, r, cell[k]);
+                    mw[k] = cw[4 * ci + 2];
+                    gv[k] = P.g[ci];
+                }
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                if (act[k] && mw[k] == ((tag << 24) | (kNil - static_cast<unsigned>(i0 + k))) && gv[k] == 0) {
+                    P.g[cidx(P, r, cell[k])] = static_cast<uint8_t>(P.delay_code);
+                    E[k] = __dadd_rn(E[k], gain);
+                    ++n_graze;
+                }
+        }
         bool died_any = false;
 #pragma unroll
         for (int k = 0; k < kS; ++k) {
             const int i = i0 + k;
             bool alive = act[k] != 0;
-            if (alive && s == 0 && grz[k]) {  // grazed (predation.cpp:188-193)
-                E[k] = __dadd_rn(E[k], gain);
-                ++n_graze;
-            }
             if (alive && flg[k]) {
                 if (s == 0) {  // eaten by a wolf this step (predation.cpp:224-238)
                     fx_removed += to_fx(E[k]);
@@ -518,7 +496,7 @@ __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
     }
     unsigned long long tile_total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(nf, nv), s_scan, &tile_total);
-    // tile-local compaction: slot order within the tile, tiles concatenate in k_spawn
+    // tile-local compaction: slot order within the tile, tiles concatenate in phase 4
     int fr = static_cast<int>(hi31(excl)), vr = static_cast<int>(lo31(excl));
     const size_t tb = static_cast<size_t>(r) * P.Npad[s] + static_cast<size_t>(tile) * kTile;
 #pragma unroll
@@ -526,14 +504,12 @@ __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
         if (freek[k]) P.free_at[s][tb + fr++] = i0 + k;
         if (valid[k]) {
             P.row_at[s][tb + vr] = i0 + k;
-            P.rowcell[s][tb + vr] = P.cell[s][base + k];
+            P.rowcell[s][tb + vr] = cell[k];
             P.rowE[s][tb + vr] = child[k];
             ++vr;
         }
     }
-    // event reductions + the tile's (free, valid) counts
-    Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
-    // one reduction for the four counters: (graze, metab, death) packed 21 bits each, + energy
+    // one reduction for the counters: (graze, metab, death) packed 21 bits each, + energy
     unsigned long long cnt = (static_cast<unsigned long long>(n_graze) << 42) |
                              (static_cast<unsigned long long>(n_metab) << 21) | n_death;
     long long fx = fx_removed;
@@ -547,35 +523,32 @@ __global__ void __launch_bounds__(kT, 4) k_update(Params P) {
         s_red2[threadIdx.x >> 5] = fx;
     }
     __syncthreads();
-    long long g_sum = 0, m_sum = 0, d_sum = 0, x_sum = 0;
     if (threadIdx.x == 0) {
         unsigned long long c = 0;
+        long long x_sum = 0;
         for (int w = 0; w < kT / 32; ++w) {
             c += static_cast<unsigned long long>(s_red[w]);
             x_sum += s_red2[w];
         }
-        g_sum = static_cast<long long>(c >> 42);
-        m_sum = static_cast<long long>((c >> 21) & 0x1FFFFF);
-        d_sum = static_cast<long long>(c & 0x1FFFFF);
-    }
-    if (threadIdx.x == 0) {
+        const unsigned long long g_sum = c >> 42, m_sum = (c >> 21) & 0x1FFFFF, d_sum = c & 0x1FFFFF;
+        Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
         P.status[(static_cast<size_t>(s) * P.R + r) * P.status_stride + tile] = tile_total;
-        if (g_sum) atomicAdd(&ev->grass_eaten, static_cast<unsigned long long>(g_sum));
-        if (m_sum) atomicAdd(&ev->metabolized[s], static_cast<unsigned long long>(m_sum));
-        if (d_sum) atomicAdd(&ev->deaths[s], static_cast<unsigned long long>(d_sum));
+        if (g_sum) atomicAdd(&ev->grass_eaten, g_sum);
+        if (m_sum) atomicAdd(&ev->metabolized[s], m_sum);
+        if (d_sum) atomicAdd(&ev->deaths[s], d_sum);
         if (x_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_removed_fx[s]), static_cast<unsigned long long>(x_sum));
     }
 }
 
-// ============================================================== K4: spawn
+// ============================================================== phase 4: spawn + regrow
 // Rank-match (lifecycle.cpp:144-195): the k-th free slot (ascending) receives the k-th valid
-// row (ascending parent slot), k < pairs = min(F, Q); fresh ids next_id + k. Every CTA scans
-// the per-tile counts of its (replica, species) in shared memory and maps each global rank to
-// (tile, local offset) by binary search. CTA 0 of each (replica, species) advances the
-// counters (double-buffered by step parity), writes the metrics row and the ledger totals.
+// row (ascending parent slot), k < pairs = min(F, Q); fresh ids next_id + k. Every spawn
+// block scans the per-tile counts of its (replica, species) in shared memory and maps each
+// global rank to (tile, local offset) by binary search. Block 0 of each (replica, species)
+// advances the counters (double-buffered by step parity), writes the metrics row and the
+// ledger totals. Blocks past the spawn blocks run the regrow sweep (predation.cpp:252-258).
 __device__ __forceinline__ int find_tile(const unsigned long long* pre, int tiles, unsigned k, bool free_rank) {
-    // largest t with prefix(t) <= k, prefix over the chosen counter
-    int lo = 0, hi = tiles - 1;
+    int lo = 0, hi = tiles - 1;  // largest t with prefix(t) <= k
     while (lo < hi) {
         const int mid = (lo + hi + 1) >> 1;
         const unsigned v = free_rank ? hi31(pre[mid]) : lo31(pre[mid]);
@@ -587,21 +560,64 @@ __device__ __forceinline__ int find_tile(const unsigned long long* pre, int tile
     return lo;
 }
 
-__global__ void __launch_bounds__(kT) k_spawn(Params P) {
-    extern __shared__ unsigned long long s_pre[];  // [tiles + 1] exclusive prefix of tile counts
+__device__ void regrow_block(const Params& P, unsigned b, unsigned nb) {
+    // 16 cells per thread (Cpad is a multiple of 16: a chunk never straddles replicas)
+    const size_t nchunk = static_cast<size_t>(P.R) * P.Cpad / 16;
+    const size_t stride = static_cast<size_t>(nb) * kT;
+    for (size_t q = static_cast<size_t>(b) * kT + threadIdx.x; q - threadIdx.x < nchunk; q += stride) {
+        unsigned ready = 0;
+        int r = -1;
+        if (q < nchunk) {
+            const size_t c0 = q * 16;
+            r = static_cast<int>(c0 / P.Cpad);
+            uint4 v = *reinterpret_cast<const uint4*>(P.g + c0);
+            uint32_t w[4] = {v.x, v.y, v.z, v.w};
+            bool changed = false;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint32_t o = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t x = (w[j] >> (8 * k)) & 0xFF;
+                    if (x >= 1 && x <= 254) {
+                        --x;
+                        changed = true;
+                    }
+                    ready += x == 0;
+                    o |= x << (8 * k);
+                }
+                w[j] = o;
+            }
+            if (changed) *reinterpret_cast<uint4*>(P.g + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+        // per-replica grass count, aggregated over the lanes of a warp sharing a replica
+        const unsigned grp = __match_any_sync(0xffffffffu, r);
+        const unsigned tot = __reduce_add_sync(grp, ready);
+        if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot) {
+            long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
+            atomicAdd(reinterpret_cast<unsigned long long*>(&row[2]), static_cast<unsigned long long>(tot));
+        }
+    }
+}
+
+__device__ void spawn_phase(const Params& P, unsigned b, unsigned long long* s_pre) {
+    // s_pre: [tiles + 1] exclusive prefix of the tile counts (dynamic shared memory)
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ long long s_red[kT / 32];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // K1/K2 of this step are complete
+    if (b >= static_cast<unsigned>(P.spawn_ctas)) {
+        regrow_block(P, b - P.spawn_ctas, P.regrow_ctas);
+        return;
+    }
+    if (b == 0 && threadIdx.x == 0) {  // phases 1-2 of this step are complete
         P.ctl->occ[0] = P.ctl->occ[1] = 0;
         P.ctl->pool_top = 0;
     }
-    const int rs = blockIdx.x / P.spawn_cps, local = blockIdx.x % P.spawn_cps;
+    const int rs = b / P.spawn_cps, local = b % P.spawn_cps;
     const int s = rs / P.R, r = rs % P.R;
     const int tiles = P.tiles[s];
     const int p = static_cast<int>(P.epoch & 1);
     const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
-    // block-wide exclusive scan of the tile counts (chunks of kT)
-    unsigned long long carry = 0;
+    unsigned long long carry = 0;  // block-wide exclusive scan of the tile counts (chunks of kT)
     for (int t0 = 0; t0 < tiles; t0 += kT) {
         const int t = t0 + threadIdx.x;
         const unsigned long long v = t < tiles ? tc[t] : 0ULL;
@@ -650,6 +666,69 @@ __global__ void __launch_bounds__(kT) k_spawn(Params P) {
         long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
         row[s] = P.N[s] - F + pairs;
         if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
+    }
+}
+
+// ============================================================== step kernels
+// One launch per phase (per-kernel timing / profiling) ...
+__global__ void __launch_bounds__(kT) k_move(Params P) { move_phase(P, blockIdx.x, gridDim.x); }
+__global__ void __launch_bounds__(kT) k_cells(Params P) { cells_phase(P, blockIdx.x * kT + threadIdx.x, gridDim.x * kT); }
+__global__ void __launch_bounds__(kT, 4) k_update(Params P) { update_phase(P, blockIdx.x); }
+__global__ void __launch_bounds__(kT) k_spawn(Params P) {
+    extern __shared__ unsigned long long s_pre[];
+    spawn_phase(P, blockIdx.x, s_pre);
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ... or the whole step as ONE persistent cooperative kernel: every CTA walks each phase's
+// work items and the phases are separated by grid-wide barriers instead of kernel boundaries.
+__global__ void __launch_bounds__(kT, 4) k_step(Params P) {
+    extern __shared__ unsigned long long s_pre[];
+    cg::grid_group grid = cg::this_grid();
+    const bool stamp = P.phase_ns != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
+    unsigned long long t0 = stamp ? globaltimer() : 0, t1;
+    const unsigned n1 = static_cast<unsigned>(P.R * (P.mtiles[0] + P.mtiles[1]));
+    for (unsigned b = blockIdx.x; b < n1; b += gridDim.x) {
+        move_phase(P, b, n1);
+        __syncthreads();
+    }
+    grid.sync();
+    if (stamp) {
+        t1 = globaltimer();
+        P.phase_ns[0] += t1 - t0;
+        t0 = t1;
+    }
+    cells_phase(P, blockIdx.x * kT + threadIdx.x, gridDim.x * kT);
+    grid.sync();
+    if (stamp) {
+        t1 = globaltimer();
+        P.phase_ns[1] += t1 - t0;
+        t0 = t1;
+    }
+    const unsigned n3 = static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
+    for (unsigned b = blockIdx.x; b < n3; b += gridDim.x) {
+        update_phase(P, b);
+        __syncthreads();
+    }
+    grid.sync();
+    if (stamp) {
+        t1 = globaltimer();
+        P.phase_ns[2] += t1 - t0;
+        t0 = t1;
+    }
+    const unsigned n4 = static_cast<unsigned>(P.spawn_ctas + P.regrow_ctas);
+    for (unsigned b = blockIdx.x; b < n4; b += gridDim.x) {
+        spawn_phase(P, b, s_pre);
+        __syncthreads();
+    }
+    if (P.phase_ns != nullptr) {
+        grid.sync();
+        if (stamp) P.phase_ns[3] += globaltimer() - t0;
     }
 }
 
@@ -818,7 +897,6 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         AL(P.id[s], n * 8);
         AL(P.next[s], n * 4);
         AL(P.flag[s], n);
-        if (s == 0) AL(P.graze, n);
         AL(P.occ[s], n * 8);
         AL(P.free_at[s], n * 4);
         AL(P.row_at[s], n * 4);
@@ -826,7 +904,7 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         AL(P.rowE[s], n * 8);
     }
     AL(P.g, static_cast<size_t>(R) * P.Cpad);
-    AL(P.cw, static_cast<size_t>(R) * P.Cpad * 8);
+    AL(P.cw, static_cast<size_t>(R) * P.Cpad * 16);
     AL(P.status, static_cast<size_t>(2) * R * P.status_stride * 8);
     P.pool_size = static_cast<long long>(R) * (P.Npad[0] + P.Npad[1]);
     AL(P.pool, static_cast<size_t>(P.pool_size) * 4);
@@ -841,13 +919,19 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     for (int s = 0; s < 2; ++s) {
         CK(cudaMemsetAsync(P.next[s], 0xFF, static_cast<size_t>(R) * P.Npad[s] * 4, stream));
     }
-    CK(cudaMemsetAsync(P.cw, 0, static_cast<size_t>(R) * P.Cpad * 8, stream));
+    CK(cudaMemsetAsync(P.cw, 0, static_cast<size_t>(R) * P.Cpad * 16, stream));
     CK(cudaMemsetAsync(P.status, 0, static_cast<size_t>(2) * R * P.status_stride * 8, stream));
     spawn_smem = static_cast<size_t>(P.status_stride + 1) * 8;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_spawn), cudaFuncAttributeMaxDynamicSharedMemorySize,
                             static_cast<int>(spawn_smem)));
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_step), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(spawn_smem)));
+    {
+        int per_sm = 0;
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step, kT, spawn_smem));
+        coop_grid = per_sm * abmx_internal::num_sms();  // 0: k_step cannot be co-resident
+    }
     CK(cudaMemsetAsync(P.ev, 0, sizeof(Events) * 2 * R, stream));
-    CK(cudaMemsetAsync(P.graze, 0, static_cast<size_t>(R) * P.Npad[0], stream));
     CK(cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream));
     P.epoch = 1;
     P.t = 1;
@@ -881,8 +965,8 @@ unsigned Engine::grid(int k) const {
     switch (k) {
         case 0: return static_cast<unsigned>(P.R * (P.mtiles[0] + P.mtiles[1]));
         case 1: return static_cast<unsigned>(P.k2_ctas);
-        case 2: return static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]) + P.regrow_ctas);
-        default: return static_cast<unsigned>(P.spawn_ctas);
+        case 2: return static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
+        default: return static_cast<unsigned>(P.spawn_ctas + P.regrow_ctas);
     }
 }
 
@@ -945,18 +1029,23 @@ int Engine::build_graph() {
 
 int Engine::launch_steps(long long steps) {
     (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated runtime calls
-    if (!timing && !graph_exec) {
+    if (!timing && !fused && !graph_exec) {
         int rc = build_graph();
         if (rc) return rc;
     }
     for (long long q = 0; q < steps; ++q) {
         params.epoch = host_epoch;
         if (host_epoch % kEpochClear == 0)  // epoch8 must not alias a stale list head
-            CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 8, stream));
+            CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 16, stream));
         if (timing) {
             launch_step_kernels(true);
             int rc = accumulate_times();
             if (rc) return rc;
+        } else if (fused) {
+            void* args[1] = {&params};
+            CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_step), dim3(coop_grid), dim3(kT), args,
+                                           spawn_smem, stream));
+            abmx_internal::count_launch(1);
         } else {
             void* args[1] = {&params};
             for (int k = 0; k < kNumKernels; ++k) {
@@ -1256,7 +1345,7 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
     const size_t per_step = per_kernel ? 2 * kNumKernels : 2;
     std::vector<cudaEvent_t> ev(per_step * static_cast<size_t>(steps));
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    if (!per_kernel && !graph_exec) {
+    if (!per_kernel && !fused && !graph_exec) {
         rc = build_graph();
         if (rc) return rc;
     }
@@ -1272,7 +1361,7 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
         if (per_kernel) {
             params.epoch = host_epoch;
             if (host_epoch % kEpochClear == 0)
-                CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 8, stream));
+                CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 16, stream));
             void* args[1] = {&params};
             for (int k = 0; k < kNumKernels; ++k) {
                 CK(cudaEventRecord(e[2 * k], stream));

@@ -68,18 +68,18 @@ struct Params {
     long long* id[2];
     int* next[2];
     uint8_t* flag[2];   // sheep: eaten this step; wolves: ate this step
-    uint8_t* graze;     // sheep: grazed this step
     int* free_at[2];
     int* row_at[2];
     int* rowcell[2];
     double* rowE[2];
-    uint2* cw;  // per-cell list heads {sheep, wolf}, each {epoch8:8 | slot:24}
+    uint4* cw;  // per cell: sheep head, wolf head, lowest sheep slot (see predation.cu)
     uint8_t* g;
     unsigned long long* status;  // [species][R][status_stride] packed (free, valid) per k_update tile
     unsigned long long* occ[2];  // occupied cells per species: (replica << 32) | cell
     int* pool;
     long long pool_size;
     Ctl* ctl;
+    unsigned long long* phase_ns;  // optional: k_step accumulates per-phase ns (globaltimer)
     SpeciesRep* rep;
     Events* ev;
 };
@@ -103,6 +103,8 @@ struct Engine {
     long long last_run_steps = 0;
     unsigned long long host_epoch = 1;     // epoch of the next step
     bool timing = false;
+    bool fused = false;  // true: one cooperative k_step launch per step; false: the 4-kernel graph
+    int coop_grid = 0;
     cudaEvent_t tev[2 * kNumKernels] = {};
     double kernel_ms[kNumKernels] = {};
     long long kernel_launches[kNumKernels] = {};

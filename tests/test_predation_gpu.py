@@ -261,3 +261,16 @@ def test_golden_run_batch_from_reference(abmx):
         got, _ = abmx.run_batch(abmx.PredationConfig(**g["config"]), g["master"], g["replicas"],
                                 g["steps"], path=path)
         assert np.array_equal(got, np.array(g["metrics"])), path
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_fused_and_graph_modes_identical(abmx, oracle, mode):
+    """The cooperative single-kernel step and the per-phase graph give the oracle's states."""
+    seed = abmx.replica_seeds(7, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, tiny(width=30, height=30, n_sheep0=200, n_wolves0=60), seed)
+    gpu.set_mode(mode)
+    got = gpu.run(1, 30)[0]
+    for t in range(1, 31):
+        orc.step(t)
+        assert got[t - 1].astype(np.int64).tolist() == orc.metrics(), t
+    assert_same_state(gpu, orc, f"mode {mode}")
