@@ -112,8 +112,8 @@ typedef struct abmx_predation_events {
 typedef struct abmx_predation abmx_predation; /* opaque: R replicas resident in HBM */
 
 /* init_predation (predation.cpp:154-165) for `replicas` models with the given replica
- * seeds (RngState keys). Errors: CAPACITY (n0 > capacity), DOMAIN (regrow_delay > 254,
- * width/height < 1, grid too large). */
+ * seeds (RngState keys). Errors: CAPACITY (n0 > capacity, capacity >= 2^24 per species),
+ * DOMAIN (regrow_delay > 2^24, width/height < 1, grid too large). */
 int abmx_predation_create(const abmx_predation_config* cfg, const uint64_t* seeds,
                           int32_t replicas, abmx_predation** out);
 int abmx_predation_destroy(abmx_predation* h);

@@ -106,20 +106,25 @@ __device__ __forceinline__ T block_sum(T v, T* smem) {
 }
 
 // ============================================================== per-cell words
-// One uint4 per cell:
+// One uint4 per cell, all four words in the same 32-byte sector:
 //   .x sheep list head {epoch8:8 | slot:24}      (atomicExch; the list links through next[0])
 //   .y wolf  list head {epoch8:8 | slot:24}      (atomicExch; links through next[1])
 //   .z lowest sheep slot {tag:8 | ~slot:24}      (atomicMax, fire-and-forget), tag = epoch%128 + 1
-// A head / minimum is current iff its tag equals this step's; nothing is cleared per step.
-// The host zeroes the array every kEpochClear (= 128) steps, so tags never alias and the
-// .z tag of the current step is the largest one alive (a max-reduction keeps it).
+//   .w grass "due" epoch: the cell is ready at the graze of step e iff due < e (lazy regrow:
+//      grazing at epoch e with delay D >= 1 stores due = e + D - 1, reproducing the countdown
+//      regrow[c] = D, -1 per step, ready at 0 of predation.cpp:188-190,252-258 without a
+//      per-step sweep; kFrozen marks a cell grazed with D <= 0, never ready again).
+// x/y/z are current iff their tag equals this step's; the host clears x/y/z (not w) every
+// kEpochClear (= 128) steps, so tags never alias and the .z tag of the current step is the
+// largest alive (a max-reduction keeps it).
 __device__ __forceinline__ unsigned epoch8(unsigned long long epoch) {
     return static_cast<unsigned>(epoch % 255ULL) + 1u;  // 1..255, never the cleared 0
 }
 __device__ __forceinline__ unsigned min_tag(unsigned long long epoch) {
     return static_cast<unsigned>(epoch % kEpochClear) + 1u;  // 1..128, grows within a clear window
 }
-constexpr unsigned kNil = 0xFFFFFFu;  // end of list
+constexpr unsigned kNil = 0xFFFFFFu;        // end of list
+constexpr unsigned kFrozen = 0xFFFFFFFFu;   // grazed with regrow_delay <= 0: never ready
 
 // blockIdx -> (species, replica, tile) for the per-slot phases: sheep tiles first.
 __device__ __forceinline__ void tile_of(const Params& P, unsigned b, int tiles0, int tiles1, int& s, int& r,
@@ -209,7 +214,6 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb) {
                     if (act[k]) {
                         const size_t ci = cidx(P, r, cell[k]);
                         atomicMax(&cw[4 * ci + 2], (tag << 24) | (kNil - static_cast<unsigned>(i0 + k)));
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.g + ci));
                     }
             }
 #pragma unroll
@@ -421,20 +425,16 @@ __device__ void update_phase(const Params& P, unsigned b) {
         if (anyflag) store8_u8(P.flag[s] + base, z);
         if (s == 0 && any) {
             // graze: lowest-slot word and grass byte of every live sheep's cell, in parallel
-            const unsigned* cw = reinterpret_cast<const unsigned*>(P.cw);
-            unsigned mw[kS];
-            uint8_t gv[kS];
+            // (lowest-slot word, due epoch) of every live sheep's cell: one 8-byte L2 load each
+            uint2 zw[kS];
 #pragma unroll
             for (int k = 0; k < kS; ++k)
-                if (act[k]) {
-                    const size_t ci = cidx(P, r, cell[k]);
-                    mw[k] = cw[4 * ci + 2];
-                    gv[k] = P.g[ci];
-                }
+                if (act[k]) zw[k] = *reinterpret_cast<const uint2*>(&P.cw[cidx(P, r, cell[k])].z);
+            const unsigned ep = static_cast<unsigned>(epoch);
 #pragma unroll
             for (int k = 0; k < kS; ++k)
-                if (act[k] && mw[k] == ((tag << 24) | (kNil - static_cast<unsigned>(i0 + k))) && gv[k] == 0) {
-                    P.g[cidx(P, r, cell[k])] = static_cast<uint8_t>(P.delay_code);
+                if (act[k] && zw[k].x == ((tag << 24) | (kNil - static_cast<unsigned>(i0 + k))) && zw[k].y < ep) {
+                    P.cw[cidx(P, r, cell[k])].w = P.delay >= 1 ? ep + static_cast<unsigned>(P.delay) - 1u : kFrozen;
                     E[k] = __dadd_rn(E[k], gain);
                     ++n_graze;
                 }
@@ -533,20 +533,26 @@ __device__ void update_phase(const Params& P, unsigned b) {
         const unsigned long long g_sum = c >> 42, m_sum = (c >> 21) & 0x1FFFFF, d_sum = c & 0x1FFFFF;
         Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
         P.status[(static_cast<size_t>(s) * P.R + r) * P.status_stride + tile] = tile_total;
-        if (g_sum) atomicAdd(&ev->grass_eaten, g_sum);
+        if (g_sum) {
+            atomicAdd(&ev->grass_eaten, g_sum);
+            if (P.delay >= 1)  // every cell grazed this step comes due at the same epoch
+                atomicAdd(&P.due_count[static_cast<size_t>(r) * P.due_ring +
+                                       (epoch + static_cast<unsigned long long>(P.delay) - 1) % P.due_ring],
+                          static_cast<unsigned>(g_sum));
+        }
         if (m_sum) atomicAdd(&ev->metabolized[s], m_sum);
         if (d_sum) atomicAdd(&ev->deaths[s], d_sum);
         if (x_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_removed_fx[s]), static_cast<unsigned long long>(x_sum));
     }
 }
 
-// ============================================================== phase 4: spawn + regrow
+// ============================================================== phase 4: spawn
 // Rank-match (lifecycle.cpp:144-195): the k-th free slot (ascending) receives the k-th valid
 // row (ascending parent slot), k < pairs = min(F, Q); fresh ids next_id + k. Every spawn
 // block scans the per-tile counts of its (replica, species) in shared memory and maps each
 // global rank to (tile, local offset) by binary search. Block 0 of each (replica, species)
 // advances the counters (double-buffered by step parity), writes the metrics row and the
-// ledger totals. Blocks past the spawn blocks run the regrow sweep (predation.cpp:252-258).
+// ledger totals; the sheep block also closes the grass count (lazy regrow, see the cell words).
 __device__ __forceinline__ int find_tile(const unsigned long long* pre, int tiles, unsigned k, bool free_rank) {
     int lo = 0, hi = tiles - 1;  // largest t with prefix(t) <= k
     while (lo < hi) {
@@ -560,54 +566,10 @@ __device__ __forceinline__ int find_tile(const unsigned long long* pre, int tile
     return lo;
 }
 
-__device__ void regrow_block(const Params& P, unsigned b, unsigned nb) {
-    // 16 cells per thread (Cpad is a multiple of 16: a chunk never straddles replicas)
-    const size_t nchunk = static_cast<size_t>(P.R) * P.Cpad / 16;
-    const size_t stride = static_cast<size_t>(nb) * kT;
-    for (size_t q = static_cast<size_t>(b) * kT + threadIdx.x; q - threadIdx.x < nchunk; q += stride) {
-        unsigned ready = 0;
-        int r = -1;
-        if (q < nchunk) {
-            const size_t c0 = q * 16;
-            r = static_cast<int>(c0 / P.Cpad);
-            uint4 v = *reinterpret_cast<const uint4*>(P.g + c0);
-            uint32_t w[4] = {v.x, v.y, v.z, v.w};
-            bool changed = false;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                uint32_t o = 0;
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    uint32_t x = (w[j] >> (8 * k)) & 0xFF;
-                    if (x >= 1 && x <= 254) {
-                        --x;
-                        changed = true;
-                    }
-                    ready += x == 0;
-                    o |= x << (8 * k);
-                }
-                w[j] = o;
-            }
-            if (changed) *reinterpret_cast<uint4*>(P.g + c0) = make_uint4(w[0], w[1], w[2], w[3]);
-        }
-        // per-replica grass count, aggregated over the lanes of a warp sharing a replica
-        const unsigned grp = __match_any_sync(0xffffffffu, r);
-        const unsigned tot = __reduce_add_sync(grp, ready);
-        if (r >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot) {
-            long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
-            atomicAdd(reinterpret_cast<unsigned long long*>(&row[2]), static_cast<unsigned long long>(tot));
-        }
-    }
-}
-
 __device__ void spawn_phase(const Params& P, unsigned b, unsigned long long* s_pre) {
     // s_pre: [tiles + 1] exclusive prefix of the tile counts (dynamic shared memory)
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ long long s_red[kT / 32];
-    if (b >= static_cast<unsigned>(P.spawn_ctas)) {
-        regrow_block(P, b - P.spawn_ctas, P.regrow_ctas);
-        return;
-    }
     if (b == 0 && threadIdx.x == 0) {  // phases 1-2 of this step are complete
         P.ctl->occ[0] = P.ctl->occ[1] = 0;
         P.ctl->pool_top = 0;
@@ -666,6 +628,13 @@ __device__ void spawn_phase(const Params& P, unsigned b, unsigned long long* s_p
         long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
         row[s] = P.N[s] - F + pairs;
         if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
+        if (s == 0) {  // ready cells after this step's (lazy) regrow: - grazed + those due now
+            unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.epoch % P.due_ring];
+            const long long ng = P.n_grass[r] - static_cast<long long>(ev->grass_eaten) + *due;
+            *due = 0;
+            P.n_grass[r] = ng;
+            row[2] = ng;
+        }
     }
 }
 
@@ -721,7 +690,7 @@ __global__ void __launch_bounds__(kT, 4) k_step(Params P) {
         P.phase_ns[2] += t1 - t0;
         t0 = t1;
     }
-    const unsigned n4 = static_cast<unsigned>(P.spawn_ctas + P.regrow_ctas);
+    const unsigned n4 = static_cast<unsigned>(P.spawn_ctas);
     for (unsigned b = blockIdx.x; b < n4; b += gridDim.x) {
         spawn_phase(P, b, s_pre);
         __syncthreads();
@@ -767,7 +736,17 @@ __global__ void k_init_cells(Params P) {
     for (size_t q = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
          q += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const long long c = static_cast<long long>(q % P.Cpad);
-        P.g[q] = c < P.C ? 0 : 255;  // full grass; padding frozen
+        P.cw[q] = make_uint4(0u, 0u, 0u, c < P.C ? 0u : kFrozen);  // full grass; padding frozen
+    }
+}
+
+// Every kEpochClear steps: reset the tagged words (list heads, lowest slot), keep the due word.
+__global__ void k_clear_cells(uint4* cw, size_t n) {
+    for (size_t q = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        cw[q].x = 0u;
+        cw[q].y = 0u;
+        cw[q].z = 0u;
     }
 }
 
@@ -834,8 +813,8 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         abmx_internal::set_error("capacity per species above 16,777,214 (24-bit cell-list slots)");
         return ABMX_E_CAPACITY;
     }
-    if (c.regrow_delay > 254) {
-        abmx_internal::set_error("regrow_delay > 254 is not representable in the u8 cell layout");
+    if (c.regrow_delay > (1 << 24)) {
+        abmx_internal::set_error("regrow_delay > 2^24 is not supported (due-epoch ring size)");
         return ABMX_E_DOMAIN;
     }
     const long long C = static_cast<long long>(c.width) * c.height;
@@ -867,15 +846,14 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     P.prob[0] = c.reproduce_prob_sheep;
     P.prob[1] = c.reproduce_prob_wolf;
     P.frac = c.reproduce_energy_frac;
-    P.delay_code = c.regrow_delay >= 1 ? static_cast<unsigned>(c.regrow_delay) : 255u;
+    P.delay = c.regrow_delay >= 1 ? static_cast<int>(c.regrow_delay) : 0;
+    P.due_ring = 256;  // must exceed the longest pending countdown (regrow_delay)
+    while (P.due_ring <= P.delay) P.due_ring *= 2;
     const int maxN = N[0] > N[1] ? N[0] : N[1];
     P.spawn_cps = maxN / 8192;
     if (P.spawn_cps < 1) P.spawn_cps = 1;
     if (P.spawn_cps > 64) P.spawn_cps = 64;
     P.spawn_ctas = 2 * R * P.spawn_cps;
-    const long long chunks = (static_cast<long long>(R) * P.Cpad) / 16;
-    P.regrow_ctas = static_cast<int>((chunks + kT - 1) / kT);
-    if (P.regrow_ctas > abmx_internal::num_sms() * 4) P.regrow_ctas = abmx_internal::num_sms() * 4;
     {
         const long long agents = static_cast<long long>(R) * (N[0] + N[1]);
         long long k2 = (agents + kT - 1) / kT;
@@ -903,7 +881,8 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         AL(P.rowcell[s], n * 4);
         AL(P.rowE[s], n * 8);
     }
-    AL(P.g, static_cast<size_t>(R) * P.Cpad);
+    AL(P.n_grass, sizeof(long long) * R);
+    AL(P.due_count, sizeof(unsigned) * P.due_ring * R);
     AL(P.cw, static_cast<size_t>(R) * P.Cpad * 16);
     AL(P.status, static_cast<size_t>(2) * R * P.status_stride * 8);
     P.pool_size = static_cast<long long>(R) * (P.Npad[0] + P.Npad[1]);
@@ -919,7 +898,11 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     for (int s = 0; s < 2; ++s) {
         CK(cudaMemsetAsync(P.next[s], 0xFF, static_cast<size_t>(R) * P.Npad[s] * 4, stream));
     }
-    CK(cudaMemsetAsync(P.cw, 0, static_cast<size_t>(R) * P.Cpad * 16, stream));
+    CK(cudaMemsetAsync(P.due_count, 0, sizeof(unsigned) * P.due_ring * R, stream));
+    {
+        std::vector<long long> ng(static_cast<size_t>(R), C);
+        CK(cudaMemcpy(P.n_grass, ng.data(), sizeof(long long) * R, cudaMemcpyHostToDevice));
+    }
     CK(cudaMemsetAsync(P.status, 0, static_cast<size_t>(2) * R * P.status_stride * 8, stream));
     spawn_smem = static_cast<size_t>(P.status_stride + 1) * 8;
     CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_spawn), cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -966,7 +949,7 @@ unsigned Engine::grid(int k) const {
         case 0: return static_cast<unsigned>(P.R * (P.mtiles[0] + P.mtiles[1]));
         case 1: return static_cast<unsigned>(P.k2_ctas);
         case 2: return static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
-        default: return static_cast<unsigned>(P.spawn_ctas + P.regrow_ctas);
+        default: return static_cast<unsigned>(P.spawn_ctas);
     }
 }
 
@@ -1234,41 +1217,62 @@ int Engine::import_species(int r, int s, const uint8_t* active, const int64_t* i
     return ABMX_OK;
 }
 
+// Lazy regrow (see the cell words): at the end of the last completed step E, a cell is ready
+// iff due <= E, and its reference counter is regrow = due - E (predation.cpp:252-258).
 int Engine::export_world(int r, uint8_t* ready, int64_t* regrow) {
     const Params& P = params;
     const size_t C = static_cast<size_t>(P.C);
-    std::vector<uint8_t> g(C);
-    CK(cudaMemcpyAsync(g.data(), P.g + static_cast<size_t>(r) * P.Cpad, C, cudaMemcpyDeviceToHost, stream));
+    std::vector<uint4> w(C);
+    CK(cudaMemcpyAsync(w.data(), P.cw + static_cast<size_t>(r) * P.Cpad, C * sizeof(uint4), cudaMemcpyDeviceToHost,
+                       stream));
     CK(cudaStreamSynchronize(stream));
+    const unsigned long long E = host_epoch - 1;
     for (size_t c = 0; c < C; ++c) {
-        ready[c] = g[c] == 0;
-        regrow[c] = g[c] == 255 ? (cfg.regrow_delay <= 0 ? cfg.regrow_delay : 0) : g[c];
+        const unsigned due = w[c].w;
+        if (due == 0xFFFFFFFFu) {  // grazed with regrow_delay <= 0: regrow holds the delay
+            ready[c] = 0;
+            regrow[c] = cfg.regrow_delay;
+        } else {
+            ready[c] = due <= E;
+            regrow[c] = due <= E ? 0 : static_cast<int64_t>(due - E);
+        }
     }
     return ABMX_OK;
 }
 
 int Engine::import_world(int r, const uint8_t* ready, const int64_t* regrow) {
-    const Params& P = params;
+    Params& P = params;
     const size_t C = static_cast<size_t>(P.C);
-    std::vector<uint8_t> g(C);
+    const unsigned long long E = host_epoch - 1;
+    std::vector<unsigned> due(C);
+    std::vector<unsigned> ring(static_cast<size_t>(P.due_ring), 0u);
+    long long n_ready = 0;
     for (size_t c = 0; c < C; ++c) {
         if (ready[c]) {
             if (regrow[c] != 0) {
                 abmx_internal::set_error("grass_ready cell with a nonzero regrow counter");
                 return ABMX_E_DOMAIN;
             }
-            g[c] = 0;
-        } else if (regrow[c] >= 1 && regrow[c] <= 254) {
-            g[c] = static_cast<uint8_t>(regrow[c]);
+            due[c] = 0;
+            ++n_ready;
         } else if (regrow[c] <= 0) {
-            g[c] = 255;  // not ready and never regrowing (predation.cpp:254 guard)
+            due[c] = 0xFFFFFFFFu;  // not ready and never regrowing (predation.cpp:254 guard)
+        } else if (regrow[c] < P.due_ring) {
+            due[c] = static_cast<unsigned>(E + static_cast<unsigned long long>(regrow[c]));
+            ++ring[due[c] % static_cast<unsigned>(P.due_ring)];
         } else {
-            abmx_internal::set_error("regrow counter > 254 not representable");
+            abmx_internal::set_error("regrow counter exceeds the due-epoch ring of this model");
             return ABMX_E_DOMAIN;
         }
     }
+    std::vector<uint4> w(C);
     CK(cudaStreamSynchronize(stream));
-    CK(cudaMemcpy(P.g + static_cast<size_t>(r) * P.Cpad, g.data(), C, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(w.data(), P.cw + static_cast<size_t>(r) * P.Cpad, C * sizeof(uint4), cudaMemcpyDeviceToHost));
+    for (size_t c = 0; c < C; ++c) w[c].w = due[c];
+    CK(cudaMemcpy(P.cw + static_cast<size_t>(r) * P.Cpad, w.data(), C * sizeof(uint4), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(P.due_count + static_cast<size_t>(r) * P.due_ring, ring.data(), ring.size() * sizeof(unsigned),
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(P.n_grass + r, &n_ready, sizeof(long long), cudaMemcpyHostToDevice));
     return ABMX_OK;
 }
 
@@ -1361,7 +1365,7 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
         if (per_kernel) {
             params.epoch = host_epoch;
             if (host_epoch % kEpochClear == 0)
-                CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 16, stream));
+                k_clear_cells<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(params.cw, static_cast<size_t>(R) * params.Cpad);
             void* args[1] = {&params};
             for (int k = 0; k < kNumKernels; ++k) {
                 CK(cudaEventRecord(e[2 * k], stream));

@@ -18,7 +18,7 @@ constexpr int kTile = kT * kS;   // slots per lookback tile
 constexpr int kM = 4;            // slots per thread in k_move / k_cells
 constexpr int kMTile = kT * kM;
 constexpr int kNumKernels = 4;
-constexpr int kEpochClear = 128;  // cw is zeroed every kEpochClear steps (epoch8 period 255)
+constexpr int kEpochClear = 128;  // cell tags are cleared every kEpochClear steps (epoch8 period 255)
 
 // Device control block: step bookkeeping shared by the four kernels of a step.
 struct Ctl {
@@ -58,8 +58,9 @@ struct Params {
     long long C;
     int N[2], Npad[2], tiles[2], mtiles[2];
     double gain[2], metab, prob[2], frac;
-    unsigned delay_code;
-    int spawn_cps, spawn_ctas, regrow_ctas, k2_ctas, status_stride;
+    int delay;     // regrow_delay if >= 1, else 0 (a grazed cell never regrows)
+    int due_ring;  // due-epoch histogram ring length per replica (power of two > delay)
+    int spawn_cps, spawn_ctas, k2_ctas, status_stride;
     const unsigned long long* seeds;
     uint8_t* active[2];
     int* cell[2];
@@ -72,8 +73,9 @@ struct Params {
     int* row_at[2];
     int* rowcell[2];
     double* rowE[2];
-    uint4* cw;  // per cell: sheep head, wolf head, lowest sheep slot (see predation.cu)
-    uint8_t* g;
+    uint4* cw;             // per cell: sheep head, wolf head, lowest sheep slot, grass due epoch
+    long long* n_grass;    // [R] ready cells after the last step
+    unsigned* due_count;   // [R][due_ring] cells coming due at each epoch (mod ring)
     unsigned long long* status;  // [species][R][status_stride] packed (free, valid) per k_update tile
     unsigned long long* occ[2];  // occupied cells per species: (replica << 32) | cell
     int* pool;

@@ -216,7 +216,7 @@ def test_create_errors(abmx):
     with pytest.raises(abmx.CapacityError):
         abmx.PredationModel(abmx.PredationConfig(**tiny(n_sheep0=500)), 1)
     with pytest.raises(abmx.DomainError):
-        abmx.PredationModel(abmx.PredationConfig(**tiny(regrow_delay=300)), 1)
+        abmx.PredationModel(abmx.PredationConfig(**tiny(regrow_delay=1 << 25)), 1)
 
 
 # ---------------------------------------------------------------------- golden fixtures
@@ -274,3 +274,37 @@ def test_fused_and_graph_modes_identical(abmx, oracle, mode):
         orc.step(t)
         assert got[t - 1].astype(np.int64).tolist() == orc.metrics(), t
     assert_same_state(gpu, orc, f"mode {mode}")
+
+
+@pytest.mark.parametrize("delay", [1, 2, 300])
+def test_regrow_delays_including_long_ones(abmx, reference, delay):
+    """Lazy regrow (due epochs) vs the reference countdown, incl. delays beyond a byte."""
+    cfgd = tiny(regrow_delay=delay, width=6, height=6, n_sheep0=40)
+    gpu = abmx.PredationModel(abmx.PredationConfig(**cfgd), 17)
+    ref = reference.pred(cfgd, 17)
+    for t in range(1, 25):
+        gpu.step(t)
+        ref.step(t)
+        assert gpu.collect_metrics()[0].tolist() == ref.metrics(), t
+        assert_same_state(gpu, ref, f"delay {delay} t={t}")
+
+
+def test_world_import_mid_run(abmx, reference):
+    """Import a hand-made world after some steps (due epochs rebuilt from counters)."""
+    cfgd = tiny()
+    gpu = abmx.PredationModel(abmx.PredationConfig(**cfgd), 21)
+    ref = reference.pred(cfgd, 21)
+    for t in range(1, 6):
+        gpu.step(t)
+        ref.step(t)
+    c = cfgd["width"] * cfgd["height"]
+    rng = np.random.default_rng(1)
+    regrow = rng.integers(0, 8, c).astype(np.int64)
+    ready = (regrow == 0).astype(np.uint8)
+    for m in (gpu, ref):
+        m.import_world(ready, regrow)
+    for t in range(6, 20):
+        gpu.step(t)
+        ref.step(t)
+        assert_same_state(gpu, ref, f"t={t}")
+        assert gpu.collect_metrics()[0].tolist() == ref.metrics(), t
