@@ -150,15 +150,15 @@ def reference_arm(args, world):
 
 
 # ---------------------------------------------------------------------- our arm
-def kernel_bytes(cfg, births_deaths):
+def kernel_bytes(cfg, births, deaths):
     """SURVEY §8d algorithmic bytes per step, B = 42*N_tot + 2*C + 8*(births+deaths),
-    apportioned to the kernel that owns each column."""
+    apportioned to the kernel that owns each column. The 2*C regrow term is
+    not given to any kernel: the lazy regrow never sweeps the cells (it stays in the step
+    total, `step_effective_gbs`)."""
     n = capacity(cfg)
-    cells = cfg["width"] * cfg["height"]
-    return {"k_move": 25 * n,                  # x,y,age read+write (2*(4+4+4)) + active read (1)
-            "k_cells": 0,                      # per-cell list scratch only, not counted by §8d
-            "k_update": 17 * n,                # energy read+write (2*8) + active write (1)
-            "k_spawn": 2 * cells + 8 * births_deaths}  # regrow sweep (u8 r+w) + id writes
+    return {"k_move": 25 * n + 8 * births,   # x,y,age read+write (2*(4+4+4)) + active read; newborn ids
+            "k_cells": 0,                    # crowded grids only (pairing scratch)
+            "k_update": 17 * n + 8 * deaths}  # energy read+write (2*8) + active write; zeroed ids
 
 
 def our_arm(args, rank, world, local_rank, dist):
@@ -208,9 +208,11 @@ def our_arm(args, rank, world, local_rank, dist):
     t_next += kt_steps
     times = model.kernel_times()
     ev = model.last_events()
-    bd = ev.sheep.births + ev.wolves.births + ev.sheep.deaths + ev.wolves.deaths
-    kb = kernel_bytes(C2, bd)
-    avg = {k: ms / max(n, 1) for k, (ms, n) in times.items()}
+    births = ev.sheep.births + ev.wolves.births
+    deaths = ev.sheep.deaths + ev.wolves.deaths
+    bd = births + deaths
+    kb = kernel_bytes(C2, births, deaths)
+    avg = {k: ms / n for k, (ms, n) in times.items() if n}
     step_sum = sum(avg.values())
     dom = max(avg, key=avg.get)
     peak, peak_src = hbm_peak()

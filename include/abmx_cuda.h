@@ -146,20 +146,12 @@ int abmx_predation_import_world(abmx_predation* h, int32_t replica, const uint8_
                                 const int64_t* regrow);
 /* the CUDA stream all of h's work is ordered on (cudaStream_t) */
 void* abmx_predation_stream(abmx_predation* h);
-/* Per-kernel timing: when enabled, steps launch kernel-by-kernel (no CUDA graph) with CUDA
- * events around each kernel; abmx_predation_kernel_times returns the accumulated device
- * milliseconds and launch counts per kernel (names via abmx_predation_kernel_name). */
+/* Per-kernel timing: abmx_predation_bench(..., per_kernel = 1) brackets every kernel with CUDA
+ * events; abmx_predation_kernel_times returns the accumulated device milliseconds and launch
+ * counts per kernel (names via abmx_predation_kernel_name); abmx_predation_set_timing resets
+ * the accumulators. */
 int abmx_predation_set_timing(abmx_predation* h, int enabled);
 int32_t abmx_predation_kernel_count(void);
-/* Step launch mode: 1 (default) = four per-phase kernels in a CUDA graph; 0 = the whole step
- * as ONE persistent cooperative kernel with grid-wide barriers between its phases. Results
- * are bit-identical; per-kernel timing always uses the per-phase kernels. */
-int abmx_predation_set_mode(abmx_predation* h, int32_t mode);
-/* Fused-mode phase timing from the device clock (%globaltimer, CTA 0 after each grid
- * barrier). enable = 1 zeroes and turns on the accumulators, -1 only reads, 0 reads and turns
- * off. ns_out (nullable) receives the accumulated nanoseconds of [move+bin, cells,
- * update+regrow, spawn]. */
-int abmx_predation_phase_times(abmx_predation* h, int32_t enable, double* ns_out);
 const char* abmx_predation_kernel_name(int32_t k);
 int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches);
 /* device-resident bytes of h (state + scratch) */

@@ -183,8 +183,6 @@ _sig("abmx_predation_import_world", C.c_int, [C.c_void_p, C.c_int32, u8p, i64p])
 _sig("abmx_predation_stream", C.c_void_p, [C.c_void_p])
 _sig("abmx_predation_set_timing", C.c_int, [C.c_void_p, C.c_int])
 _sig("abmx_predation_kernel_count", C.c_int32, [])
-_sig("abmx_predation_set_mode", C.c_int, [C.c_void_p, C.c_int32])
-_sig("abmx_predation_phase_times", C.c_int, [C.c_void_p, C.c_int32, f64p])
 _sig("abmx_predation_kernel_name", C.c_char_p, [C.c_int32])
 _sig("abmx_predation_kernel_times", C.c_int, [C.c_void_p, f64p, i64p])
 _sig("abmx_predation_device_bytes", C.c_int64, [C.c_void_p])
@@ -449,19 +447,6 @@ class PredationModel:
         return ms, met
 
     # -- per-kernel timing (CUDA events around each launch; disables the CUDA graph)
-    def set_mode(self, mode: int):
-        """1 = per-phase kernels in a CUDA graph (default), 0 = fused cooperative step kernel."""
-        _check(lib.abmx_predation_set_mode(self._h, mode))
-
-    def phase_times(self, enable=None):
-        """Fused-mode per-phase device nanoseconds (globaltimer): phase_times(True) resets and
-        enables, phase_times() reads [move, cells, update, spawn], phase_times(False) reads
-        and disables."""
-        out = np.zeros(4, np.float64)
-        code = -1 if enable is None else (1 if enable else 0)
-        _check(lib.abmx_predation_phase_times(self._h, code, _p(out, f64p)))
-        return out
-
     def set_timing(self, on: bool):
         _check(lib.abmx_predation_set_timing(self._h, 1 if on else 0))
 

@@ -304,46 +304,11 @@ int abmx_predation_import_world(abmx_predation* h, int32_t replica, const uint8_
 void* abmx_predation_stream(abmx_predation* h) { return h ? h->eng.stream : nullptr; }
 int abmx_predation_set_timing(abmx_predation* h, int enabled) {
     HANDLE(h);
-    h->eng.timing = enabled != 0;
+    (void)enabled;  // per-kernel timing is taken by abmx_predation_bench(per_kernel = 1)
     for (int k = 0; k < abmx_pred::kNumKernels; ++k) {
         h->eng.kernel_ms[k] = 0.0;
         h->eng.kernel_launches[k] = 0;
     }
-    return ABMX_OK;
-}
-int abmx_predation_set_mode(abmx_predation* h, int32_t mode) {
-    HANDLE(h);
-    if (mode != 0 && mode != 1) {
-        set_error("mode must be 0 (fused cooperative step) or 1 (per-phase kernels in a CUDA graph)");
-        return ABMX_E_DOMAIN;
-    }
-    if (mode == 0 && h->eng.coop_grid < 1) {
-        set_error("the fused step kernel cannot be made co-resident on this device");
-        return ABMX_E_DOMAIN;
-    }
-    h->eng.fused = mode == 0;
-    return ABMX_OK;
-}
-int abmx_predation_phase_times(abmx_predation* h, int32_t enable, double* ns_out) {
-    HANDLE(h);
-    auto& P = h->eng.params;
-    if (enable == 1) {
-        if (!P.phase_ns) {
-            if (cudaMalloc(&P.phase_ns, 4 * sizeof(unsigned long long)) != cudaSuccess) {
-                set_error("cudaMalloc failed");
-                return ABMX_E_CUDA;
-            }
-            h->eng.allocs.push_back(P.phase_ns);
-        }
-        cudaMemsetAsync(P.phase_ns, 0, 4 * sizeof(unsigned long long), h->eng.stream);
-    }
-    if (ns_out && P.phase_ns) {
-        unsigned long long v[4];
-        cudaMemcpyAsync(v, P.phase_ns, sizeof v, cudaMemcpyDeviceToHost, h->eng.stream);
-        if (cudaStreamSynchronize(h->eng.stream) != cudaSuccess) return ABMX_E_CUDA;
-        for (int k = 0; k < 4; ++k) ns_out[k] = static_cast<double>(v[k]);
-    }
-    if (enable == 0) P.phase_ns = nullptr;  // buffer stays owned by allocs
     return ABMX_OK;
 }
 int32_t abmx_predation_kernel_count(void) { return abmx_pred::kNumKernels; }

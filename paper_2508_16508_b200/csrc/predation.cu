@@ -1,24 +1,26 @@
-// predation.cu — the predation step (src/models/predation.cpp:167-263) as four fused
-// sm_100a kernels over device-resident SoA state, for R replicas at once.
+// predation.cu — the predation step (src/models/predation.cpp:167-263) on sm_100a for R
+// replicas at once, device-resident SoA state, bit-exact with the reference.
 //
-// Per step (all launches stream-ordered, captured once in a CUDA graph):
-//   K1 k_move       per slot: RNG move + toroidal wrap + age++ (step_agents, lifecycle.cpp:87-122),
-//                   then spatial binning into per-cell epoch-stamped lists (wolves first, then
-//                   sheep; ticket-ordered CTAs) and an atomicMin "lowest sheep slot" per cell.
-//   K2 k_predation  one thread per cell holding >= 1 wolf: stable (slot-sorted) wolf and sheep
-//                   lists, k-th wolf <-> k-th sheep (predation.cpp:197-239).
-//   K3 k_update     per slot: graze (lowest slot on a ready cell), predation kill, metabolise,
-//                   starve, reproduce (Bernoulli + quantised child energy); the free-slot and
-//                   valid-row masks are scanned in ONE single-pass decoupled lookback (two
-//                   counters packed per tile) and compacted (spawn_agents rank-match,
-//                   lifecycle.cpp:144-195).
-//   K4 k_spawn      k-th free slot <- k-th valid row, fresh ids; plus the cell regrow sweep
-//                   (predation.cpp:252-258) and the grass count for the metrics row.
+// A step is TWO kernels (three on crowded grids), captured once in a CUDA graph:
+//   k_move    (a) births of the previous step: the k-th free slot (ascending) receives the
+//                 k-th valid parent row (rank-match, lifecycle.cpp:144-195), ranks from one
+//                 block scan of the active mask + the per-tile counts published by k_update;
+//             (b) step_agents with the move transition (predation.cpp:35-49,
+//                 lifecycle.cpp:87-122), then every live agent pushes itself onto its new
+//                 cell's list (atomicExch) and sheep post their slot to the cell's
+//                 lowest-slot word (atomicMax, fire-and-forget).
+//   [k_cells] crowded grids only (capacity > cells): sort-based k-th wolf <-> k-th sheep
+//             pairing per wolf cell (predation.cpp:197-239) -> flags.
+//   k_update  graze (lowest sheep slot of a ready cell), predation (sparse grids: each agent
+//             of a wolf-and-sheep cell walks the cell's two short lists for its slot rank),
+//             metabolise, starve, reproduce (predation.cpp:178-250); valid parent rows are
+//             compacted tile-locally and every tile publishes its (free, valid) counts.
+// The births of the last step are applied by k_finalize (k_move without the move) whenever
+// the host needs the state (export, metrics, end of a run).
 //
 // HBM layout (per species, per replica, stride Npad): active u8, cell i32 (= y*W + x),
-// age i32, energy f64, id i64. Cells: one u8 code per cell (0 = ready, 1..254 = regrow
-// countdown, 255 = not ready and frozen: grazed with regrow_delay <= 0, and padding).
-// Placeholder slots hold zeros (agent_set.cpp:45-58); the agent type is implied by species.
+// age i32, energy f64, id i64; the agent type is implied by the species. Per cell one uint4
+// (list heads, lowest sheep slot, grass due epoch — see "per-cell words").
 #include <climits>
 #include <cstdint>
 #include <cstdio>
@@ -30,9 +32,6 @@
 #include "abmx_device.cuh"
 #include "abmx_internal.h"
 #include "predation_engine.h"
-
-#include <cooperative_groups.h>
-namespace cg = cooperative_groups;
 
 using namespace abmx_dev;
 
@@ -53,43 +52,35 @@ __device__ __forceinline__ long long to_fx(double e) {
     return __double2ll_rn(__dmul_rn(e, 1048576.0));
 }
 
-template <int N>
-__device__ __forceinline__ void load8_u8(const uint8_t* p, uint8_t (&v)[N]) {
-    static_assert(N == 4 || N == 8, "4 or 8 slots per thread");
-    if constexpr (N == 4) {
-        const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+__device__ __forceinline__ void load4_u8(const uint8_t* p, uint8_t (&v)[kS]) {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
-    } else {
-        const uint2 w = *reinterpret_cast<const uint2*>(p);
-#pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = static_cast<uint8_t>((k < 4 ? w.x : w.y) >> (8 * (k & 3)));
-    }
+    for (int k = 0; k < kS; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
 }
-template <int N>
-__device__ __forceinline__ void store8_u8(uint8_t* p, const uint8_t (&v)[N]) {
-    uint32_t w[N / 4];
-#pragma unroll
-    for (int q = 0; q < N / 4; ++q)
-        w[q] = v[4 * q] | (v[4 * q + 1] << 8) | (v[4 * q + 2] << 16) | (static_cast<uint32_t>(v[4 * q + 3]) << 24);
-    if constexpr (N == 4)
-        *reinterpret_cast<uint32_t*>(p) = w[0];
-    else
-        *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+__device__ __forceinline__ void store4_u8(uint8_t* p, const uint8_t (&v)[kS]) {
+    *reinterpret_cast<uint32_t*>(p) =
+        v[0] | (v[1] << 8) | (v[2] << 16) | (static_cast<uint32_t>(v[3]) << 24);
 }
-template <int N>
-__device__ __forceinline__ void load8_f64(const double* p, double (&v)[N]) {
-#pragma unroll
-    for (int q = 0; q < N / 2; ++q) {
-        const double2 d = reinterpret_cast<const double2*>(p)[q];
-        v[2 * q] = d.x;
-        v[2 * q + 1] = d.y;
-    }
+__device__ __forceinline__ void load4_f64(const double* p, double (&v)[kS]) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = b.x;
+    v[3] = b.y;
 }
-template <int N>
-__device__ __forceinline__ void store8_f64(double* p, const double (&v)[N]) {
-#pragma unroll
-    for (int q = 0; q < N / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+__device__ __forceinline__ void store4_f64(double* p, const double (&v)[kS]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+}
+__device__ __forceinline__ void load4_i32(const int* p, int (&v)[kS]) {
+    const int4 a = *reinterpret_cast<const int4*>(p);
+    v[0] = a.x;
+    v[1] = a.y;
+    v[2] = a.z;
+    v[3] = a.w;
+}
+__device__ __forceinline__ void store4_i32(int* p, const int (&v)[kS]) {
+    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
 }
 
 template <class T>
@@ -126,131 +117,245 @@ __device__ __forceinline__ unsigned min_tag(unsigned long long epoch) {
 constexpr unsigned kNil = 0xFFFFFFu;        // end of list
 constexpr unsigned kFrozen = 0xFFFFFFFFu;   // grazed with regrow_delay <= 0: never ready
 
-// blockIdx -> (species, replica, tile) for the per-slot phases: sheep tiles first.
-__device__ __forceinline__ void tile_of(const Params& P, unsigned b, int tiles0, int tiles1, int& s, int& r,
-                                        int& tile) {
-    const unsigned sheep_ctas = static_cast<unsigned>(P.R * tiles0);
+// blockIdx -> (species, replica, tile): sheep tiles first.
+__device__ __forceinline__ void tile_of(const Params& P, unsigned b, int& s, int& r, int& tile) {
+    const unsigned sheep_ctas = static_cast<unsigned>(P.R * P.tiles[0]);
     if (b < sheep_ctas) {
         s = 0;
-        r = b / tiles0;
-        tile = b % tiles0;
+        r = b / P.tiles[0];
+        tile = b % P.tiles[0];
     } else {
         s = 1;
         const unsigned u = b - sheep_ctas;
-        r = u / tiles1;
-        tile = u % tiles1;
+        r = u / P.tiles[1];
+        tile = u % P.tiles[1];
     }
 }
 
-__device__ __forceinline__ void load4_u8(const uint8_t* p, uint8_t (&v)[4]) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
+// largest t with prefix(t) <= k over the chosen packed counter (hi31 = free, lo31 = valid)
+__device__ __forceinline__ int find_tile(const unsigned long long* pre, int tiles, unsigned k, bool free_rank) {
+    int lo = 0, hi = tiles - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        const unsigned v = free_rank ? hi31(pre[mid]) : lo31(pre[mid]);
+        if (v <= k)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return lo;
 }
 
-// ============================================================== phase 1: move + bin
-// step_agents with the move transition (predation.cpp:35-49, lifecycle.cpp:87-122). Every
-// live agent then pushes itself onto its new cell's list (one atomicExch); sheep also post
-// their slot to the cell's lowest-slot word (atomicMax, no return) and prefetch the cell's
-// grass byte for phase 3. The first wolf of a cell records it in the wolf-cell list.
-__device__ void move_phase(const Params& P, unsigned b, unsigned nb) {
+// ============================================================== k_move / k_finalize
+// kMove = false: k_finalize (births + counters only).
+template <bool kMove>
+__device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned long long* s_pre) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ long long s_red[kT / 32];
     __shared__ unsigned s_base;
     const unsigned long long epoch = P.epoch;
-    const unsigned e8 = epoch8(epoch), tag = min_tag(epoch);
     int s, r, tile;
-    tile_of(P, b, P.mtiles[0], P.mtiles[1], s, r, tile);
-    // zero this parity's event accumulators (consumed by the later phases of this step)
-    {
+    tile_of(P, b, s, r, tile);
+    const int N = P.N[s];
+    const int i0 = tile * kTile + threadIdx.x * kS;
+    const size_t base = sidx(P, s, r, i0);
+    const size_t rb = static_cast<size_t>(r) * P.Npad[s];
+    if (kMove) {  // zero this step's event accumulators (its parity; births use the other)
         Events* ev = P.ev + static_cast<size_t>(epoch & 1) * P.R;
         for (unsigned rr = b * kT + threadIdx.x; rr < static_cast<unsigned>(P.R); rr += nb * kT)
             memset(&ev[rr], 0, sizeof(Events));
     }
-    const unsigned long long key = split(split(split(P.seeds[r], 3), static_cast<unsigned long long>(P.t)), s);
-    const int i0 = tile * kMTile + threadIdx.x * kM;
-    const int W = P.W, H = P.H;
-    bool first[kM] = {false, false, false, false};
-    int cell[kM] = {0, 0, 0, 0};
-    if (i0 < P.N[s]) {
-        const size_t base = sidx(P, s, r, i0);
-        uint8_t act[kM];
-        int4 cv = make_int4(0, 0, 0, 0), av = make_int4(0, 0, 0, 0);
-        if (s == 0) {  // dense species: issue the column loads together with the mask load
-            cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
-            av = *reinterpret_cast<const int4*>(P.age[s] + base);
+    // dense species: issue the column loads together with the mask load
+    uint8_t act[kS] = {0, 0, 0, 0};
+    int cell[kS] = {0, 0, 0, 0}, age[kS] = {0, 0, 0, 0};
+    const bool live = i0 < N;
+    if (live) {
+        if (kMove && s == 0) {
+            load4_i32(P.cell[s] + base, cell);
+            load4_i32(P.age[s] + base, age);
         }
         load4_u8(P.active[s] + base, act);
-        const bool any = (act[0] | act[1] | act[2] | act[3]) != 0;
-        if (any) {
-            if (s == 1) {
-                cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
-                av = *reinterpret_cast<const int4*>(P.age[s] + base);
-            }
-            cell[0] = cv.x;
-            cell[1] = cv.y;
-            cell[2] = cv.z;
-            cell[3] = cv.w;
-            int age[kM] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-            for (int k = 0; k < kM; ++k) {
-                if (!act[k]) continue;
-                const int u = static_cast<int>(draw(key, static_cast<unsigned long long>(i0 + k)) >> 61);
-                const int c = cell[k];
-                const int y = c / W, x = c - y * W;
-                int nx = x + c_dx[u], ny = y + c_dy[u];
-                nx = nx < 0 ? nx + W : (nx >= W ? nx - W : nx);
-                ny = ny < 0 ? ny + H : (ny >= H ? ny - H : ny);
-                cell[k] = ny * W + nx;
-                age[k] += 1;
-            }
-            unsigned* cw = reinterpret_cast<unsigned*>(P.cw);
-            unsigned old[kM];
-#pragma unroll
-            for (int k = 0; k < kM; ++k)
-                if (act[k]) old[k] = atomicExch(&cw[4 * cidx(P, r, cell[k]) + s], (e8 << 24) | static_cast<unsigned>(i0 + k));
-            if (s == 0) {
-#pragma unroll
-                for (int k = 0; k < kM; ++k)
-                    if (act[k]) {
-                        const size_t ci = cidx(P, r, cell[k]);
-                        atomicMax(&cw[4 * ci + 2], (tag << 24) | (kNil - static_cast<unsigned>(i0 + k)));
-                    }
-            }
-#pragma unroll
-            for (int k = 0; k < kM; ++k)
-                if (act[k]) {
-                    const bool cur = (old[k] >> 24) == e8;
-                    P.next[s][base + k] = cur ? static_cast<int>(old[k] & kNil) : -1;
-                    first[k] = s == 1 && !cur;
-                }
-            *reinterpret_cast<int4*>(P.cell[s] + base) = make_int4(cell[0], cell[1], cell[2], cell[3]);
-            *reinterpret_cast<int4*>(P.age[s] + base) = make_int4(age[0], age[1], age[2], age[3]);
+    }
+
+    // ---------------- (a) births of step P.birth_epoch (rank-match, lifecycle.cpp:144-195)
+    bool born[kS] = {false, false, false, false};
+    bool born_any = false;
+    if (P.pending) {
+        const int tiles = P.tiles[s];
+        const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
+        unsigned long long carry = 0;  // exclusive prefix of the tile counts -> s_pre
+        for (int t0 = 0; t0 < tiles; t0 += kT) {
+            const int t = t0 + threadIdx.x;
+            const unsigned long long v = t < tiles ? tc[t] : 0ULL;
+            unsigned long long tot;
+            const unsigned long long ex = block_excl_scan<kT>(v, s_scan, &tot);
+            if (t < tiles) s_pre[t] = carry + ex;
+            carry += tot;
+            __syncthreads();
         }
-        if (P.needs_blend) {  // step_agents masks placeholder state back to defaults
+        const int F = static_cast<int>(hi31(carry)), Q = static_cast<int>(lo31(carry));
+        const int pairs = F < Q ? F : Q;
+        const int pb = static_cast<int>(P.birth_epoch & 1);
+        SpeciesRep* sr = &P.rep[static_cast<size_t>(r) * 2 + s];
+        const long long base_id = sr->next_id[pb];
+        // free slots of this tile in slot order: block scan of the free counts
+        bool fr[kS];
+        unsigned nf = 0;
 #pragma unroll
-            for (int k = 0; k < kM; ++k)
-                if (!act[k] && i0 + k < P.N[s]) {
-                    P.cell[s][base + k] = 0;
-                    P.energy[s][base + k] = 0.0;
+        for (int k = 0; k < kS; ++k) {
+            fr[k] = live && !act[k] && i0 + k < N;
+            nf += fr[k];
+        }
+        unsigned long long tot_f;
+        const unsigned long long off = block_excl_scan<kT>(nf, s_scan, &tot_f);
+        unsigned rank = hi31(s_pre[tile]) + static_cast<unsigned>(off);
+        int vrow[kS];
+        unsigned brank[kS];
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (fr[k]) {
+                if (static_cast<int>(rank) < pairs) {
+                    const int vt = find_tile(s_pre, tiles, rank, false);
+                    vrow[k] = vt * kTile + static_cast<int>(rank - lo31(s_pre[vt]));
+                    brank[k] = rank;
+                    born[k] = true;
+                }
+                ++rank;
+            }
+        int bc[kS];
+        double be[kS];
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (born[k]) {
+                bc[k] = P.rowcell[s][rb + vrow[k]];
+                be[k] = P.rowE[s][rb + vrow[k]];
+            }
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (born[k]) {
+                act[k] = 1;
+                cell[k] = bc[k];
+                age[k] = 0;
+                P.energy[s][base + k] = be[k];
+                P.id[s][base + k] = base_id + brank[k];
+                P.birth_child[s][rb + brank[k]] = i0 + k;
+                born_any = true;
+            }
+        // energy of this tile's valid rows beyond the pairs (dropped births, predation.cpp:121-135)
+        const int qt = static_cast<int>(lo31(tc[tile])), q0 = static_cast<int>(lo31(s_pre[tile]));
+        long long fx = 0;
+        if (q0 + qt > pairs)
+            for (int l = threadIdx.x; l < qt; l += kT)
+                if (q0 + l >= pairs) fx += to_fx(P.rowE[s][rb + static_cast<size_t>(tile) * kTile + l]);
+        const long long fx_tot = block_sum<long long>(fx, s_red);
+        Events* ev = P.ev + static_cast<size_t>(pb) * P.R + r;
+        if (threadIdx.x == 0) {
+            if (fx_tot) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_dropped_fx[s]), static_cast<unsigned long long>(fx_tot));
+            if (tile == 0) {  // counters, ledger and the metrics row of step birth_epoch
+                sr->next_id[pb ^ 1] = base_id + pairs;
+                sr->num_active[pb ^ 1] = N - F + pairs;
+                sr->pairs = pairs;
+                sr->Q = Q;
+                atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
+                atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
+                long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
+                row[s] = N - F + pairs;
+                if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
+                if (s == 0) {  // ready cells after that step's (lazy) regrow: - grazed + those due
+                    unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.birth_epoch % P.due_ring];
+                    const long long ng = P.n_grass[r] - static_cast<long long>(ev->grass_eaten) + *due;
+                    *due = 0;
+                    P.n_grass[r] = ng;
+                    row[2] = ng;
+                }
+            }
+        }
+        if (!kMove && born_any) {
+            store4_u8(P.active[s] + base, act);
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                if (born[k]) {
+                    P.cell[s][base + k] = cell[k];
+                    P.age[s][base + k] = 0;
                 }
         }
     }
-    if (s == 1) {  // block-aggregated append of the cells this thread's wolves opened
+    if (!kMove) return;
+
+    // ---------------- (b) move + bin
+    const unsigned e8 = epoch8(epoch), tag = min_tag(epoch);
+    const unsigned long long key = split(split(split(P.seeds[r], 3), static_cast<unsigned long long>(P.t)), s);
+    const bool any = (act[0] | act[1] | act[2] | act[3]) != 0;
+    bool first[kS] = {false, false, false, false};
+    if (live && any) {
+        if (s == 1) {  // sparse species: columns only where something lives (newborns keep theirs)
+            int c2[kS], a2[kS];
+            load4_i32(P.cell[s] + base, c2);
+            load4_i32(P.age[s] + base, a2);
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                if (!born[k]) {
+                    cell[k] = c2[k];
+                    age[k] = a2[k];
+                }
+        }
+#pragma unroll
+        for (int k = 0; k < kS; ++k) {
+            if (!act[k]) continue;
+            const int u = static_cast<int>(draw(key, static_cast<unsigned long long>(i0 + k)) >> 61);
+            const int c = cell[k];
+            const int y = c / P.W, x = c - y * P.W;
+            int nx = x + c_dx[u], ny = y + c_dy[u];
+            nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
+            ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
+            cell[k] = ny * P.W + nx;
+            age[k] += 1;
+        }
+        unsigned* cw = reinterpret_cast<unsigned*>(P.cw);
+        unsigned old[kS];
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (act[k]) old[k] = atomicExch(&cw[4 * cidx(P, r, cell[k]) + s], (e8 << 24) | static_cast<unsigned>(i0 + k));
+        if (s == 0) {
+#pragma unroll
+            for (int k = 0; k < kS; ++k)
+                if (act[k]) atomicMax(&cw[4 * cidx(P, r, cell[k]) + 2], (tag << 24) | (kNil - static_cast<unsigned>(i0 + k)));
+        }
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (act[k]) {
+                const bool cur = (old[k] >> 24) == e8;
+                P.next[s][base + k] = cur ? static_cast<int>(old[k] & kNil) : -1;
+                first[k] = P.crowded && s == 1 && !cur;
+            }
+        store4_i32(P.cell[s] + base, cell);
+        store4_i32(P.age[s] + base, age);
+        if (born_any) store4_u8(P.active[s] + base, act);
+    }
+    if (live && P.needs_blend) {  // step_agents masks placeholder state back to defaults
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (!act[k] && i0 + k < N) {
+                P.cell[s][base + k] = 0;
+                P.energy[s][base + k] = 0.0;
+            }
+    }
+    if (P.crowded && s == 1) {  // block-aggregated append of the cells this thread's wolves opened
         const unsigned nfirst = first[0] + first[1] + first[2] + first[3];
         unsigned long long total;
         const unsigned long long off = block_excl_scan<kT>(nfirst, s_scan, &total);
-        if (threadIdx.x == 0 && total) s_base = atomicAdd(&P.ctl->occ[1], static_cast<unsigned>(total));
+        if (threadIdx.x == 0 && total) s_base = atomicAdd(&P.ctl->occ, static_cast<unsigned>(total));
         __syncthreads();
         if (nfirst) {
             unsigned pos = s_base + static_cast<unsigned>(off);
 #pragma unroll
-            for (int k = 0; k < kM; ++k)
-                if (first[k]) P.occ[1][pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
+            for (int k = 0; k < kS; ++k)
+                if (first[k]) P.occ[pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
         }
     }
 }
 
-// ============================================================== phase 2: predation pairing
+// ============================================================== k_cells (crowded grids)
 __device__ void insertion_sort(int* a, int n) {
     for (int i = 1; i < n; ++i) {
         const int v = a[i];
@@ -286,13 +391,15 @@ __device__ void heap_sort(int* a, int n) {
 
 constexpr int kSmallList = 8;
 
-__device__ __forceinline__ unsigned long long wolf_cell(const Params& P, unsigned long long ent, unsigned e8) {
+// One thread per cell holding >= 1 wolf: sort both lists by slot (registers, or a heap sort
+// in the scratch pool for long lists) and flag the k-th wolf / k-th sheep pairs
+// (predation.cpp:197-239). On crowded grids the pull pairing of k_update would walk long lists.
+__device__ unsigned long long wolf_cell(const Params& P, unsigned long long ent, unsigned e8) {
     const int r = static_cast<int>(ent >> 32), c = static_cast<int>(static_cast<uint32_t>(ent));
     const uint2 word = *reinterpret_cast<const uint2*>(&P.cw[cidx(P, r, c)]);
     if ((word.x >> 24) != e8) return 0;  // no sheep in this cell
     const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
     const int w0 = static_cast<int>(word.y & kNil), s0 = static_cast<int>(word.x & kNil);
-    // one pass over both lists (interleaved), up to kSmallList each in registers
     int wl[kSmallList], sl[kSmallList];
     int lw = 0, ls = 0;
     for (int w = w0, v = s0; w >= 0 || v >= 0;) {
@@ -317,7 +424,7 @@ __device__ __forceinline__ unsigned long long wolf_cell(const Params& P, unsigne
             P.flag[0][sb + sl[q]] = 1;  // eaten
             P.flag[1][wb + wl[q]] = 1;  // ate
         }
-    } else {  // long lists (crowded cells): heap sort in the global scratch pool
+    } else {
         const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
         if (static_cast<long long>(off) + lw + ls > P.pool_size) {
             atomicExch(&P.ctl->error, 1u);
@@ -339,21 +446,18 @@ __device__ __forceinline__ unsigned long long wolf_cell(const Params& P, unsigne
     return static_cast<unsigned long long>(pairs);
 }
 
-// One work item per cell holding >= 1 wolf: the k-th wolf (slot order) takes the k-th sheep
-// (slot order) of the cell (predation.cpp:197-239). Lists come unordered from the exchanges,
-// so both are sorted by slot first.
-__device__ void cells_phase(const Params& P, unsigned q0, unsigned stride) {
+__global__ void __launch_bounds__(kT) k_cells(Params P) {
     const unsigned e8 = epoch8(P.epoch);
-    const unsigned nw = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ[1]);
-    for (unsigned q = q0; q - threadIdx.x < nw; q += stride) {
+    const unsigned nw = *reinterpret_cast<volatile unsigned*>(&P.ctl->occ);
+    const unsigned stride = gridDim.x * kT;
+    for (unsigned q = blockIdx.x * kT + threadIdx.x; q - threadIdx.x < nw; q += stride) {
         unsigned long long eaten = 0;
         int rw = -1;
         if (q < nw) {
-            const unsigned long long ent = P.occ[1][q];
+            const unsigned long long ent = P.occ[q];
             rw = static_cast<int>(ent >> 32);
             eaten = wolf_cell(P, ent, e8);
         }
-        // per-replica predation count: lanes sharing a replica combine (one atomic each)
         const unsigned grp = __match_any_sync(0xffffffffu, rw);
         const unsigned long long tot = __reduce_add_sync(grp, static_cast<unsigned>(eaten));
         if (rw >= 0 && (threadIdx.x & 31) == __ffs(grp) - 1 && tot)
@@ -361,83 +465,95 @@ __device__ void cells_phase(const Params& P, unsigned q0, unsigned stride) {
     }
 }
 
-// ============================================================== phase 3: per-slot update
-// Streams every slot once: graze (the lowest sheep slot of a ready cell eats, predation.cpp:
-// 178-195, decided from the cell's lowest-slot word), predation kill / gain, metabolise,
-// starve, reproduce (predation.cpp:197-250). Each tile compacts its own free slots and valid
-// rows (tile-local ranks from one block scan of packed (free, valid) counters) and publishes
-// its two counts; no tile waits on another — global ranks are resolved in phase 4.
+// ============================================================== k_update
+// Rank of `me` among a cell list's slots, and the list's length (short lists on sparse grids).
+__device__ __forceinline__ void list_rank(const int* next, int head, int me, int& rank, int& len) {
+    rank = 0;
+    len = 0;
+    for (int v = head; v >= 0; v = next[v]) {
+        rank += v < me;
+        ++len;
+    }
+}
+
 __device__ void update_phase(const Params& P, unsigned b) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
-    __shared__ long long s_red[kT / 32];
-    __shared__ long long s_red2[kT / 32];
+    __shared__ unsigned long long s_cnt[kT / 32];
+    __shared__ long long s_fx[kT / 32];
+    __shared__ unsigned s_eat[kT / 32];
     const unsigned long long epoch = P.epoch;
     const int p = static_cast<int>(epoch & 1);
-    const unsigned tag = min_tag(epoch);
+    const unsigned tag = min_tag(epoch), e8 = epoch8(epoch), ep = static_cast<unsigned>(epoch);
     int s, r, tile;
-    tile_of(P, b, P.tiles[0], P.tiles[1], s, r, tile);
+    tile_of(P, b, s, r, tile);
+    if (b == 0 && threadIdx.x == 0) {  // the move (and pairing) of this step are complete
+        P.ctl->occ = 0;
+        P.ctl->pool_top = 0;
+    }
     const unsigned long long key = split(split(split(P.seeds[r], 4), static_cast<unsigned long long>(P.t)), s);
     const int N = P.N[s];
     const int i0 = tile * kTile + threadIdx.x * kS;
     const size_t base = sidx(P, s, r, i0);
+    const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
     const double gain = P.gain[s], metab = P.metab, prob = P.prob[s], frac = P.frac;
 
-    uint8_t act[kS];
-    double E[kS], child[kS];
-    int cell[kS];
-    bool valid[kS], freek[kS];
-    unsigned n_graze = 0, n_metab = 0, n_death = 0;
+    uint8_t act[kS] = {0, 0, 0, 0};
+    double E[kS] = {0.0, 0.0, 0.0, 0.0}, child[kS] = {0.0, 0.0, 0.0, 0.0};
+    int cell[kS] = {0, 0, 0, 0};
+    bool valid[kS] = {false, false, false, false}, freek[kS] = {false, false, false, false};
+    unsigned n_graze = 0, n_metab = 0, n_death = 0, n_eaten = 0;
     long long fx_removed = 0;
-#pragma unroll
-    for (int k = 0; k < kS; ++k) {
-        valid[k] = false;
-        freek[k] = false;
-        child[k] = 0.0;
-        cell[k] = 0;
-    }
     if (i0 < N) {
-        uint8_t flg[kS];
-        load8_u8(P.active[s] + base, act);
-        load8_u8(P.flag[s] + base, flg);
-        bool any = false, anyflag = false;
-        if (s == 0) {  // dense species: issue the column loads with the masks
-            load8_f64(P.energy[s] + base, E);
-            const int4 cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
-            cell[0] = cv.x;
-            cell[1] = cv.y;
-            cell[2] = cv.z;
-            cell[3] = cv.w;
+        uint8_t flg[kS] = {0, 0, 0, 0};
+        if (s == 0) {  // dense species: issue the column loads with the mask
+            load4_f64(P.energy[s] + base, E);
+            load4_i32(P.cell[s] + base, cell);
         }
-#pragma unroll
-        for (int k = 0; k < kS; ++k) {
-            any |= act[k] != 0;
-            anyflag |= flg[k] != 0;
-        }
+        load4_u8(P.active[s] + base, act);
+        if (P.crowded) load4_u8(P.flag[s] + base, flg);
+        const bool any = (act[0] | act[1] | act[2] | act[3]) != 0;
         if (s == 1 && any) {
-            load8_f64(P.energy[s] + base, E);
-            const int4 cv = *reinterpret_cast<const int4*>(P.cell[s] + base);
-            cell[0] = cv.x;
-            cell[1] = cv.y;
-            cell[2] = cv.z;
-            cell[3] = cv.w;
+            load4_f64(P.energy[s] + base, E);
+            load4_i32(P.cell[s] + base, cell);
         }
-        const uint8_t z[kS] = {};
-        if (anyflag) store8_u8(P.flag[s] + base, z);
-        if (s == 0 && any) {
-            // graze: lowest-slot word and grass byte of every live sheep's cell, in parallel
-            // (lowest-slot word, due epoch) of every live sheep's cell: one 8-byte L2 load each
-            uint2 zw[kS];
+        if (P.crowded && (flg[0] | flg[1] | flg[2] | flg[3])) {
+            const uint8_t z[kS] = {0, 0, 0, 0};
+            store4_u8(P.flag[s] + base, z);
+        }
+        if (any) {
+            // the cell word of every live agent (list heads, lowest sheep slot, grass due)
+            uint4 cw[kS];
 #pragma unroll
             for (int k = 0; k < kS; ++k)
-                if (act[k]) zw[k] = *reinterpret_cast<const uint2*>(&P.cw[cidx(P, r, cell[k])].z);
-            const unsigned ep = static_cast<unsigned>(epoch);
+                if (act[k]) cw[k] = P.cw[cidx(P, r, cell[k])];
+            if (s == 0) {  // graze: lowest sheep slot of a ready cell (predation.cpp:178-195)
 #pragma unroll
-            for (int k = 0; k < kS; ++k)
-                if (act[k] && zw[k].x == ((tag << 24) | (kNil - static_cast<unsigned>(i0 + k))) && zw[k].y < ep) {
-                    P.cw[cidx(P, r, cell[k])].w = P.delay >= 1 ? ep + static_cast<unsigned>(P.delay) - 1u : kFrozen;
-                    E[k] = __dadd_rn(E[k], gain);
-                    ++n_graze;
+                for (int k = 0; k < kS; ++k)
+                    if (act[k] && cw[k].z == ((tag << 24) | (kNil - static_cast<unsigned>(i0 + k))) && cw[k].w < ep) {
+                        P.cw[cidx(P, r, cell[k])].w = P.delay >= 1 ? ep + static_cast<unsigned>(P.delay) - 1u : kFrozen;
+                        E[k] = __dadd_rn(E[k], gain);
+                        ++n_graze;
+                    }
+            }
+            if (!P.crowded) {
+                // predation (predation.cpp:197-239): in a cell holding wolves and sheep the k-th
+                // wolf by slot takes the k-th sheep by slot; each agent finds its own rank with
+                // a walk over the cell's (short) lists
+#pragma unroll
+                for (int k = 0; k < kS; ++k) {
+                    if (!act[k] || (cw[k].x >> 24) != e8 || (cw[k].y >> 24) != e8) continue;
+                    const int hs = static_cast<int>(cw[k].x & kNil), hw = static_cast<int>(cw[k].y & kNil);
+                    int rank, len_mine, rank_o, len_other;
+                    if (s == 0) {
+                        list_rank(P.next[0] + sb, hs, i0 + k, rank, len_mine);
+                        list_rank(P.next[1] + wb, hw, INT_MAX, rank_o, len_other);
+                    } else {
+                        list_rank(P.next[1] + wb, hw, i0 + k, rank, len_mine);
+                        list_rank(P.next[0] + sb, hs, INT_MAX, rank_o, len_other);
+                    }
+                    flg[k] = rank < len_other;
                 }
+            }
         }
         bool died_any = false;
 #pragma unroll
@@ -448,6 +564,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
                 if (s == 0) {  // eaten by a wolf this step (predation.cpp:224-238)
                     fx_removed += to_fx(E[k]);
                     ++n_death;
+                    ++n_eaten;
                     alive = false;
                 } else {
                     E[k] = __dadd_rn(E[k], gain);  // the wolf ate (predation.cpp:236)
@@ -476,9 +593,9 @@ __device__ void update_phase(const Params& P, unsigned b) {
             }
             freek[k] = !alive && i < N;
         }
-        if (any) store8_f64(P.energy[s] + base, E);
+        if (any) store4_f64(P.energy[s] + base, E);
         if (died_any) {
-            store8_u8(P.active[s] + base, act);
+            store4_u8(P.active[s] + base, act);
 #pragma unroll
             for (int k = 0; k < kS; ++k)
                 if (!act[k] && i0 + k < N) {
@@ -496,39 +613,40 @@ __device__ void update_phase(const Params& P, unsigned b) {
     }
     unsigned long long tile_total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(nf, nv), s_scan, &tile_total);
-    // tile-local compaction: slot order within the tile, tiles concatenate in phase 4
-    int fr = static_cast<int>(hi31(excl)), vr = static_cast<int>(lo31(excl));
+    // tile-local compaction of the valid parent rows (slot order); k_move concatenates tiles
+    int vr = static_cast<int>(lo31(excl));
     const size_t tb = static_cast<size_t>(r) * P.Npad[s] + static_cast<size_t>(tile) * kTile;
 #pragma unroll
-    for (int k = 0; k < kS; ++k) {
-        if (freek[k]) P.free_at[s][tb + fr++] = i0 + k;
+    for (int k = 0; k < kS; ++k)
         if (valid[k]) {
             P.row_at[s][tb + vr] = i0 + k;
             P.rowcell[s][tb + vr] = cell[k];
             P.rowE[s][tb + vr] = child[k];
             ++vr;
         }
-    }
-    // one reduction for the counters: (graze, metab, death) packed 21 bits each, + energy
+    // one pass of reductions: (graze, metab, death) packed 21 bits each, eaten, energy
     unsigned long long cnt = (static_cast<unsigned long long>(n_graze) << 42) |
                              (static_cast<unsigned long long>(n_metab) << 21) | n_death;
-    long long fx = fx_removed;
+    long long fxr = fx_removed;
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-        fx += __shfl_xor_sync(0xffffffffu, fx, d);
+        fxr += __shfl_xor_sync(0xffffffffu, fxr, d);
+        n_eaten += __shfl_xor_sync(0xffffffffu, n_eaten, d);
     }
     if ((threadIdx.x & 31) == 0) {
-        s_red[threadIdx.x >> 5] = static_cast<long long>(cnt);
-        s_red2[threadIdx.x >> 5] = fx;
+        s_cnt[threadIdx.x >> 5] = cnt;
+        s_fx[threadIdx.x >> 5] = fxr;
+        s_eat[threadIdx.x >> 5] = n_eaten;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        unsigned long long c = 0;
+        unsigned long long c = 0, eaten = 0;
         long long x_sum = 0;
         for (int w = 0; w < kT / 32; ++w) {
-            c += static_cast<unsigned long long>(s_red[w]);
-            x_sum += s_red2[w];
+            c += s_cnt[w];
+            x_sum += s_fx[w];
+            eaten += s_eat[w];
         }
         const unsigned long long g_sum = c >> 42, m_sum = (c >> 21) & 0x1FFFFF, d_sum = c & 0x1FFFFF;
         Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
@@ -542,164 +660,21 @@ __device__ void update_phase(const Params& P, unsigned b) {
         }
         if (m_sum) atomicAdd(&ev->metabolized[s], m_sum);
         if (d_sum) atomicAdd(&ev->deaths[s], d_sum);
+        if (eaten && !P.crowded) atomicAdd(&ev->sheep_eaten, eaten);
         if (x_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_removed_fx[s]), static_cast<unsigned long long>(x_sum));
     }
 }
 
-// ============================================================== phase 4: spawn
-// Rank-match (lifecycle.cpp:144-195): the k-th free slot (ascending) receives the k-th valid
-// row (ascending parent slot), k < pairs = min(F, Q); fresh ids next_id + k. Every spawn
-// block scans the per-tile counts of its (replica, species) in shared memory and maps each
-// global rank to (tile, local offset) by binary search. Block 0 of each (replica, species)
-// advances the counters (double-buffered by step parity), writes the metrics row and the
-// ledger totals; the sheep block also closes the grass count (lazy regrow, see the cell words).
-__device__ __forceinline__ int find_tile(const unsigned long long* pre, int tiles, unsigned k, bool free_rank) {
-    int lo = 0, hi = tiles - 1;  // largest t with prefix(t) <= k
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        const unsigned v = free_rank ? hi31(pre[mid]) : lo31(pre[mid]);
-        if (v <= k)
-            lo = mid;
-        else
-            hi = mid - 1;
-    }
-    return lo;
-}
-
-__device__ void spawn_phase(const Params& P, unsigned b, unsigned long long* s_pre) {
-    // s_pre: [tiles + 1] exclusive prefix of the tile counts (dynamic shared memory)
-    __shared__ unsigned long long s_scan[kT / 32 + 1];
-    __shared__ long long s_red[kT / 32];
-    if (b == 0 && threadIdx.x == 0) {  // phases 1-2 of this step are complete
-        P.ctl->occ[0] = P.ctl->occ[1] = 0;
-        P.ctl->pool_top = 0;
-    }
-    const int rs = b / P.spawn_cps, local = b % P.spawn_cps;
-    const int s = rs / P.R, r = rs % P.R;
-    const int tiles = P.tiles[s];
-    const int p = static_cast<int>(P.epoch & 1);
-    const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
-    unsigned long long carry = 0;  // block-wide exclusive scan of the tile counts (chunks of kT)
-    for (int t0 = 0; t0 < tiles; t0 += kT) {
-        const int t = t0 + threadIdx.x;
-        const unsigned long long v = t < tiles ? tc[t] : 0ULL;
-        unsigned long long tot;
-        const unsigned long long ex = block_excl_scan<kT>(v, s_scan, &tot);
-        if (t < tiles) s_pre[t] = carry + ex;
-        carry += tot;
-        __syncthreads();
-    }
-    const int F = static_cast<int>(hi31(carry)), Q = static_cast<int>(lo31(carry));
-    const int pairs = F < Q ? F : Q;
-    SpeciesRep* sr = &P.rep[static_cast<size_t>(r) * 2 + s];
-    const long long base_id = sr->next_id[p];
-    const size_t rb = static_cast<size_t>(r) * P.Npad[s];
-    long long fx_dropped = 0;
-    for (int k = local * kT + threadIdx.x; k < Q; k += P.spawn_cps * kT) {
-        const int vt = find_tile(s_pre, tiles, static_cast<unsigned>(k), false);
-        const size_t vrow = rb + static_cast<size_t>(vt) * kTile + (k - lo31(s_pre[vt]));
-        if (k < pairs) {
-            const int ft = find_tile(s_pre, tiles, static_cast<unsigned>(k), true);
-            const size_t fpos = rb + static_cast<size_t>(ft) * kTile + (k - hi31(s_pre[ft]));
-            const size_t slot = rb + P.free_at[s][fpos];
-            P.active[s][slot] = 1;
-            P.cell[s][slot] = P.rowcell[s][vrow];
-            P.energy[s][slot] = P.rowE[s][vrow];
-            P.age[s][slot] = 0;
-            P.id[s][slot] = base_id + k;
-        } else {
-            fx_dropped += to_fx(P.rowE[s][vrow]);  // predation.cpp:121-135
-        }
-    }
-    Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
-    if (Q > pairs) {
-        const long long tot = block_sum<long long>(fx_dropped, s_red);
-        if (threadIdx.x == 0 && tot)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_dropped_fx[s]), static_cast<unsigned long long>(tot));
-    }
-    if (local == 0 && threadIdx.x == 0) {
-        sr->next_id[p ^ 1] = base_id + pairs;
-        sr->num_active[p ^ 1] = P.N[s] - F + pairs;
-        sr->base_id = base_id;
-        sr->pairs = pairs;
-        sr->Q = Q;
-        atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
-        atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
-        long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
-        row[s] = P.N[s] - F + pairs;
-        if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
-        if (s == 0) {  // ready cells after this step's (lazy) regrow: - grazed + those due now
-            unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.epoch % P.due_ring];
-            const long long ng = P.n_grass[r] - static_cast<long long>(ev->grass_eaten) + *due;
-            *due = 0;
-            P.n_grass[r] = ng;
-            row[2] = ng;
-        }
-    }
-}
-
-// ============================================================== step kernels
-// One launch per phase (per-kernel timing / profiling) ...
-__global__ void __launch_bounds__(kT) k_move(Params P) { move_phase(P, blockIdx.x, gridDim.x); }
-__global__ void __launch_bounds__(kT) k_cells(Params P) { cells_phase(P, blockIdx.x * kT + threadIdx.x, gridDim.x * kT); }
-__global__ void __launch_bounds__(kT, 4) k_update(Params P) { update_phase(P, blockIdx.x); }
-__global__ void __launch_bounds__(kT) k_spawn(Params P) {
+// ============================================================== kernels
+__global__ void __launch_bounds__(kT) k_move(Params P) {
     extern __shared__ unsigned long long s_pre[];
-    spawn_phase(P, blockIdx.x, s_pre);
+    move_phase<true>(P, blockIdx.x, gridDim.x, s_pre);
 }
-
-__device__ __forceinline__ unsigned long long globaltimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-
-// ... or the whole step as ONE persistent cooperative kernel: every CTA walks each phase's
-// work items and the phases are separated by grid-wide barriers instead of kernel boundaries.
-__global__ void __launch_bounds__(kT, 4) k_step(Params P) {
+__global__ void __launch_bounds__(kT) k_finalize(Params P) {
     extern __shared__ unsigned long long s_pre[];
-    cg::grid_group grid = cg::this_grid();
-    const bool stamp = P.phase_ns != nullptr && blockIdx.x == 0 && threadIdx.x == 0;
-    unsigned long long t0 = stamp ? globaltimer() : 0, t1;
-    const unsigned n1 = static_cast<unsigned>(P.R * (P.mtiles[0] + P.mtiles[1]));
-    for (unsigned b = blockIdx.x; b < n1; b += gridDim.x) {
-        move_phase(P, b, n1);
-        __syncthreads();
-    }
-    grid.sync();
-    if (stamp) {
-        t1 = globaltimer();
-        P.phase_ns[0] += t1 - t0;
-        t0 = t1;
-    }
-    cells_phase(P, blockIdx.x * kT + threadIdx.x, gridDim.x * kT);
-    grid.sync();
-    if (stamp) {
-        t1 = globaltimer();
-        P.phase_ns[1] += t1 - t0;
-        t0 = t1;
-    }
-    const unsigned n3 = static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
-    for (unsigned b = blockIdx.x; b < n3; b += gridDim.x) {
-        update_phase(P, b);
-        __syncthreads();
-    }
-    grid.sync();
-    if (stamp) {
-        t1 = globaltimer();
-        P.phase_ns[2] += t1 - t0;
-        t0 = t1;
-    }
-    const unsigned n4 = static_cast<unsigned>(P.spawn_ctas);
-    for (unsigned b = blockIdx.x; b < n4; b += gridDim.x) {
-        spawn_phase(P, b, s_pre);
-        __syncthreads();
-    }
-    if (P.phase_ns != nullptr) {
-        grid.sync();
-        if (stamp) P.phase_ns[3] += globaltimer() - t0;
-    }
+    move_phase<false>(P, blockIdx.x, gridDim.x, s_pre);
 }
+__global__ void __launch_bounds__(kT) k_update(Params P) { update_phase(P, blockIdx.x); }
 
 // ============================================================== init (create_agents)
 // predation.cpp:22-33 + lifecycle.cpp:53-85: x, y, energy drawn for ALL slots from
@@ -750,12 +725,32 @@ __global__ void k_clear_cells(uint4* cw, size_t n) {
     }
 }
 
+// L2 flush between timed steps: overwrite a buffer larger than the 126 MB L2, then read a
+// second one so L2 is left holding CLEAN lines (otherwise the timed step would pay for
+// writing back the flush buffer's dirty lines, traffic that is not part of the workload).
+__global__ void k_flush(uint4* p, size_t n) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = make_uint4(static_cast<unsigned>(i), 0u, 0u, 0u);
+}
+__global__ void k_flush_read(const uint4* p, size_t n, unsigned* sink) {
+    unsigned acc = 0;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const uint4 v = p[i];
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+    }
+    if (acc == 0x9E3779B9u) *sink = acc;  // practically never; keeps the loads alive
+}
+
 }  // namespace abmx_pred
 
 // ====================================================================== host engine
 namespace abmx_pred {
 
-static const char* kKernelNames[kNumKernels] = {"k_move", "k_cells", "k_update", "k_spawn"};
+static const char* kKernelNames[kNumKernels] = {"k_move", "k_cells", "k_update"};
+static void* const kKernelFns[kNumKernels] = {reinterpret_cast<void*>(k_move), reinterpret_cast<void*>(k_cells),
+                                              reinterpret_cast<void*>(k_update)};
 
 const char* kernel_name(int k) { return (k >= 0 && k < kNumKernels) ? kKernelNames[k] : ""; }
 
@@ -770,10 +765,8 @@ const char* kernel_name(int k) { return (k >= 0 && k < kNumKernels) ? kKernelNam
 
 Engine::~Engine() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
-    for (auto& ev : tev)
-        if (ev) cudaEventDestroy(ev);
-    for (void* p : allocs) cudaFree(p);
     if (graph) cudaGraphDestroy(graph);
+    for (void* p : allocs) cudaFree(p);
     if (d_run_metrics) cudaFree(d_run_metrics);
     if (flush_buf) cudaFree(flush_buf);
     if (stream) cudaStreamDestroy(stream);
@@ -833,12 +826,9 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     const int N[2] = {c.sheep_capacity, c.wolf_capacity};
     for (int s = 0; s < 2; ++s) {
         P.N[s] = N[s];
-        P.Npad[s] = (N[s] + 15) / 16 * 16;
-        if (P.Npad[s] == 0) P.Npad[s] = 16;
-        P.tiles[s] = (N[s] + kTile - 1) / kTile;
-        if (P.tiles[s] == 0) P.tiles[s] = 1;
-        P.mtiles[s] = (N[s] + kMTile - 1) / kMTile;
-        if (P.mtiles[s] == 0) P.mtiles[s] = 1;
+        P.Npad[s] = (N[s] + kTile - 1) / kTile * kTile;  // whole tiles per replica
+        if (P.Npad[s] == 0) P.Npad[s] = kTile;
+        P.tiles[s] = P.Npad[s] / kTile;
     }
     P.gain[0] = c.energy_gain_sheep;
     P.gain[1] = c.energy_gain_wolf;
@@ -849,14 +839,12 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     P.delay = c.regrow_delay >= 1 ? static_cast<int>(c.regrow_delay) : 0;
     P.due_ring = 256;  // must exceed the longest pending countdown (regrow_delay)
     while (P.due_ring <= P.delay) P.due_ring *= 2;
-    const int maxN = N[0] > N[1] ? N[0] : N[1];
-    P.spawn_cps = maxN / 8192;
-    if (P.spawn_cps < 1) P.spawn_cps = 1;
-    if (P.spawn_cps > 64) P.spawn_cps = 64;
-    P.spawn_ctas = 2 * R * P.spawn_cps;
+    // crowded grid (more slots than cells): the per-agent list walks of the pull pairing
+    // could become long, so pairing runs sort-based in k_cells instead
+    P.crowded = (static_cast<long long>(N[0]) + N[1]) > C ? 1 : 0;
     {
-        const long long agents = static_cast<long long>(R) * (N[0] + N[1]);
-        long long k2 = (agents + kT - 1) / kT;
+        const long long wolves = static_cast<long long>(R) * N[1];
+        long long k2 = (wolves + kT - 1) / kT;
         if (k2 > abmx_internal::num_sms() * 8LL) k2 = abmx_internal::num_sms() * 8LL;
         P.k2_ctas = static_cast<int>(k2 > 0 ? k2 : 1);
     }
@@ -875,12 +863,12 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         AL(P.id[s], n * 8);
         AL(P.next[s], n * 4);
         AL(P.flag[s], n);
-        AL(P.occ[s], n * 8);
-        AL(P.free_at[s], n * 4);
         AL(P.row_at[s], n * 4);
         AL(P.rowcell[s], n * 4);
         AL(P.rowE[s], n * 8);
+        AL(P.birth_child[s], n * 4);
     }
+    AL(P.occ, static_cast<size_t>(R) * P.Npad[1] * 8);
     AL(P.n_grass, sizeof(long long) * R);
     AL(P.due_count, sizeof(unsigned) * P.due_ring * R);
     AL(P.cw, static_cast<size_t>(R) * P.Cpad * 16);
@@ -895,39 +883,33 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
 #undef AL
     P.seeds = d_seeds;
     CK(cudaMemcpyAsync(d_seeds, seeds, sizeof(unsigned long long) * R, cudaMemcpyHostToDevice, stream));
-    for (int s = 0; s < 2; ++s) {
-        CK(cudaMemsetAsync(P.next[s], 0xFF, static_cast<size_t>(R) * P.Npad[s] * 4, stream));
-    }
+    for (int s = 0; s < 2; ++s) CK(cudaMemsetAsync(P.next[s], 0xFF, static_cast<size_t>(R) * P.Npad[s] * 4, stream));
     CK(cudaMemsetAsync(P.due_count, 0, sizeof(unsigned) * P.due_ring * R, stream));
-    {
-        std::vector<long long> ng(static_cast<size_t>(R), C);
-        CK(cudaMemcpy(P.n_grass, ng.data(), sizeof(long long) * R, cudaMemcpyHostToDevice));
-    }
     CK(cudaMemsetAsync(P.status, 0, static_cast<size_t>(2) * R * P.status_stride * 8, stream));
-    spawn_smem = static_cast<size_t>(P.status_stride + 1) * 8;
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_spawn), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(spawn_smem)));
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_step), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(spawn_smem)));
-    {
-        int per_sm = 0;
-        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step, kT, spawn_smem));
-        coop_grid = per_sm * abmx_internal::num_sms();  // 0: k_step cannot be co-resident
-    }
     CK(cudaMemsetAsync(P.ev, 0, sizeof(Events) * 2 * R, stream));
     CK(cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream));
+    {
+        std::vector<long long> ng(static_cast<size_t>(R), C);
+        CK(cudaMemcpyAsync(P.n_grass, ng.data(), sizeof(long long) * R, cudaMemcpyHostToDevice, stream));
+        std::vector<SpeciesRep> rep(static_cast<size_t>(2) * R);
+        for (int r = 0; r < R; ++r) {
+            rep[2 * r + 0] = SpeciesRep{{c.n_sheep0, c.n_sheep0}, {c.n_sheep0, c.n_sheep0}, 0, 0};
+            rep[2 * r + 1] = SpeciesRep{{c.n_wolves0, c.n_wolves0}, {c.n_wolves0, c.n_wolves0}, 0, 0};
+        }
+        CK(cudaMemcpyAsync(P.rep, rep.data(), sizeof(SpeciesRep) * rep.size(), cudaMemcpyHostToDevice, stream));
+        CK(cudaStreamSynchronize(stream));  // the host vectors must be consumed
+    }
+    move_smem = static_cast<size_t>(P.status_stride + 1) * 8;
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_move), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(move_smem)));
+    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_finalize), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            static_cast<int>(move_smem)));
     P.epoch = 1;
     P.t = 1;
     P.metrics = d_metrics_step;
     P.metrics_stride = 1;
     P.run_step = 0;
-    std::vector<SpeciesRep> rep(static_cast<size_t>(2) * R);
-    for (int r = 0; r < R; ++r) {
-        rep[2 * r + 0] = SpeciesRep{{c.n_sheep0, c.n_sheep0}, {c.n_sheep0, c.n_sheep0}, 0, 0, 0};
-        rep[2 * r + 1] = SpeciesRep{{c.n_wolves0, c.n_wolves0}, {c.n_wolves0, c.n_wolves0}, 0, 0, 0};
-    }
-    CK(cudaMemcpyAsync(P.rep, rep.data(), sizeof(SpeciesRep) * rep.size(), cudaMemcpyHostToDevice, stream));
-    CK(cudaStreamSynchronize(stream));  // rep (a host vector) must be consumed
+    P.pending = 0;
     const int g = abmx_internal::num_sms() * 8;
     (void)cudaGetLastError();
     k_init_species<<<g, 256, 0, stream>>>(P, 0, c.n_sheep0);
@@ -936,72 +918,28 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     abmx_internal::count_launch(3);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
-    for (int k = 0; k < kNumKernels; ++k) {
-        CK(cudaEventCreate(&tev[2 * k]));
-        CK(cudaEventCreate(&tev[2 * k + 1]));
-    }
     return ABMX_OK;
 }
 
 unsigned Engine::grid(int k) const {
     const Params& P = params;
-    switch (k) {
-        case 0: return static_cast<unsigned>(P.R * (P.mtiles[0] + P.mtiles[1]));
-        case 1: return static_cast<unsigned>(P.k2_ctas);
-        case 2: return static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
-        default: return static_cast<unsigned>(P.spawn_ctas);
-    }
+    if (k == 1) return static_cast<unsigned>(P.k2_ctas);
+    return static_cast<unsigned>(P.R * (P.tiles[0] + P.tiles[1]));
 }
-
-static void* const kKernelFns[kNumKernels] = {reinterpret_cast<void*>(k_move), reinterpret_cast<void*>(k_cells),
-                                              reinterpret_cast<void*>(k_update), reinterpret_cast<void*>(k_spawn)};
-
-void Engine::launch_step_kernels(bool timed) {
-    void* args[1] = {&params};
-    for (int k = 0; k < kNumKernels; ++k) {
-        if (timed) cudaEventRecord(tev[2 * k], stream);
-        cudaLaunchKernel(kKernelFns[k], dim3(grid(k)), dim3(kT), args, k == 3 ? spawn_smem : 0, stream);
-        if (timed) cudaEventRecord(tev[2 * k + 1], stream);
-    }
-    abmx_internal::count_launch(kNumKernels);
-}
-
-int Engine::accumulate_times() {
-    CK(cudaEventSynchronize(tev[2 * kNumKernels - 1]));
-    for (int k = 0; k < kNumKernels; ++k) {
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, tev[2 * k], tev[2 * k + 1]));
-        kernel_ms[k] += ms;
-        kernel_launches[k] += 1;
-    }
-    return ABMX_OK;
-}
-
-// The step's varying scalars (epoch, t, metrics row, blend flag) are kernel PARAMETERS kept on
-// the host: nothing on the device has to advance them, and a graph replay only needs its
-// kernel nodes' parameters refreshed.
-int Engine::set_t(long long t) {
-    params.t = t;
-    return ABMX_OK;
-}
-
-int Engine::set_metrics_target(long long* d_metrics, unsigned stride) {
-    params.metrics = d_metrics;
-    params.metrics_stride = stride;
-    params.run_step = 0;
-    return ABMX_OK;
-}
+size_t Engine::smem(int k) const { return k == 0 ? move_smem : 0; }
+bool Engine::launched(int k) const { return k != 1 || params.crowded; }
 
 int Engine::build_graph() {
     CK(cudaGraphCreate(&graph, 0));
     void* args[1] = {&params};
     cudaGraphNode_t prev = nullptr;
     for (int k = 0; k < kNumKernels; ++k) {
+        if (!launched(k)) continue;
         cudaKernelNodeParams kp{};
         kp.func = kKernelFns[k];
         kp.gridDim = dim3(grid(k));
         kp.blockDim = dim3(kT);
-        kp.sharedMemBytes = k == 3 ? static_cast<unsigned>(spawn_smem) : 0;
+        kp.sharedMemBytes = static_cast<unsigned>(smem(k));
         kp.kernelParams = args;
         CK(cudaGraphAddKernelNode(&nodes[k], graph, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
         prev = nodes[k];
@@ -1010,94 +948,142 @@ int Engine::build_graph() {
     return ABMX_OK;
 }
 
+// One step's kernels. With `ev` (2 events per kernel) every kernel is bracketed by CUDA events
+// and launched directly; otherwise the graph is launched with refreshed node parameters.
+int Engine::enqueue_step(cudaEvent_t* ev) {
+    params.epoch = host_epoch;
+    if (host_epoch % kEpochClear == 0)  // epoch tags must not alias stale words
+        k_clear_cells<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(params.cw, static_cast<size_t>(R) * params.Cpad);
+    void* args[1] = {&params};
+    if (ev) {
+        for (int k = 0; k < kNumKernels; ++k) {
+            if (!launched(k)) continue;
+            CK(cudaEventRecord(ev[2 * k], stream));
+            CK(cudaLaunchKernel(kKernelFns[k], dim3(grid(k)), dim3(kT), args, smem(k), stream));
+            CK(cudaEventRecord(ev[2 * k + 1], stream));
+            abmx_internal::count_launch(1);
+        }
+    } else {
+        if (!graph_exec) {
+            int rc = build_graph();
+            if (rc) return rc;
+        }
+        for (int k = 0; k < kNumKernels; ++k) {
+            if (!launched(k)) continue;
+            cudaKernelNodeParams kp{};
+            kp.func = kKernelFns[k];
+            kp.gridDim = dim3(grid(k));
+            kp.blockDim = dim3(kT);
+            kp.sharedMemBytes = static_cast<unsigned>(smem(k));
+            kp.kernelParams = args;
+            CK(cudaGraphExecKernelNodeSetParams(graph_exec, nodes[k], &kp));
+            abmx_internal::count_launch(1);
+        }
+        CK(cudaGraphLaunch(graph_exec, stream));
+    }
+    // this step's births stay pending until the next k_move (or k_finalize) applies them
+    params.needs_blend = 0;
+    params.pending = 1;
+    params.birth_epoch = host_epoch;
+    params.birth_row = params.run_step;
+    params.t += 1;
+    params.run_step += 1;
+    ++host_epoch;
+    return ABMX_OK;
+}
+
+int Engine::finalize() {
+    if (!params.pending) return ABMX_OK;
+    void* args[1] = {&params};
+    (void)cudaGetLastError();
+    CK(cudaLaunchKernel(reinterpret_cast<void*>(k_finalize), dim3(grid(0)), dim3(kT), args, move_smem, stream));
+    abmx_internal::count_launch(1);
+    params.pending = 0;
+    return ABMX_OK;
+}
+
+int Engine::set_t(long long t) {
+    params.t = t;
+    return ABMX_OK;
+}
+
+int Engine::set_metrics_target(long long* d_metrics, unsigned stride) {
+    int rc = finalize();  // a pending birth row belongs to the previous target
+    if (rc) return rc;
+    params.metrics = d_metrics;
+    params.metrics_stride = stride;
+    params.run_step = 0;
+    return ABMX_OK;
+}
+
 int Engine::launch_steps(long long steps) {
     (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated runtime calls
-    if (!timing && !fused && !graph_exec) {
-        int rc = build_graph();
-        if (rc) return rc;
-    }
     for (long long q = 0; q < steps; ++q) {
-        params.epoch = host_epoch;
-        if (host_epoch % kEpochClear == 0)  // epoch8 must not alias a stale list head
-            CK(cudaMemsetAsync(params.cw, 0, static_cast<size_t>(R) * params.Cpad * 16, stream));
-        if (timing) {
-            launch_step_kernels(true);
-            int rc = accumulate_times();
-            if (rc) return rc;
-        } else if (fused) {
-            void* args[1] = {&params};
-            CK(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(k_step), dim3(coop_grid), dim3(kT), args,
-                                           spawn_smem, stream));
-            abmx_internal::count_launch(1);
-        } else {
-            void* args[1] = {&params};
-            for (int k = 0; k < kNumKernels; ++k) {
-                cudaKernelNodeParams kp{};
-                kp.func = kKernelFns[k];
-                kp.gridDim = dim3(grid(k));
-                kp.blockDim = dim3(kT);
-                kp.sharedMemBytes = k == 3 ? static_cast<unsigned>(spawn_smem) : 0;
-                kp.kernelParams = args;
-                CK(cudaGraphExecKernelNodeSetParams(graph_exec, nodes[k], &kp));
-            }
-            CK(cudaGraphLaunch(graph_exec, stream));
-            abmx_internal::count_launch(kNumKernels);
-        }
-        params.needs_blend = 0;
-        params.t += 1;
-        params.run_step += 1;
-        ++host_epoch;
+        int rc = enqueue_step(nullptr);
+        if (rc) return rc;
     }
     CK(cudaGetLastError());
     return ABMX_OK;
 }
 
 int Engine::step(long long t) {
-    int rc = set_t(t);
-    CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
-    rc = set_metrics_target(d_metrics_step, 1);
+    int rc = set_metrics_target(d_metrics_step, 1);
     if (rc) return rc;
+    CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
+    set_t(t);
     rc = launch_steps(1);
+    if (rc) return rc;
+    rc = finalize();
     last_run_steps = 0;
     return rc;
 }
 
-int Engine::run_async(long long t0, long long steps) {
-    if (steps <= 0) return ABMX_OK;
+int Engine::prepare_run(long long t0, long long steps) {
     if (steps > 0x7FFFFFFFLL) {
         abmx_internal::set_error("too many steps in one run");
         return ABMX_E_DOMAIN;
     }
-    int rc = set_t(t0);
-    if (rc) return rc;
     const size_t mbytes = sizeof(long long) * 4 * static_cast<size_t>(R) * static_cast<size_t>(steps);
+    int rc = finalize();
+    if (rc) return rc;
     if (mbytes > run_metrics_bytes) {
         CK(cudaStreamSynchronize(stream));
         if (d_run_metrics) cudaFree(d_run_metrics);
-
         CK(cudaMalloc(&d_run_metrics, mbytes));
         run_metrics_bytes = mbytes;
     }
     CK(cudaMemsetAsync(d_run_metrics, 0, mbytes, stream));
     rc = set_metrics_target(d_run_metrics, static_cast<unsigned>(steps));
     if (rc) return rc;
+    set_t(t0);
+    return ABMX_OK;
+}
+
+int Engine::run_async(long long t0, long long steps) {
+    if (steps <= 0) return ABMX_OK;
+    int rc = prepare_run(t0, steps);
+    if (rc) return rc;
     rc = launch_steps(steps);
+    if (rc) return rc;
+    rc = finalize();
     last_run_steps = steps;
     return rc;
 }
 
 int Engine::fetch_run_metrics(double* out) {
+    int rc = finalize();
+    if (rc) return rc;
     const size_t n = static_cast<size_t>(R) * static_cast<size_t>(last_run_steps) * 4;
     std::vector<long long> h(n);
-    if (n) {
-        CK(cudaMemcpyAsync(h.data(), d_run_metrics, n * sizeof(long long), cudaMemcpyDeviceToHost, stream));
-    }
+    if (n) CK(cudaMemcpyAsync(h.data(), d_run_metrics, n * sizeof(long long), cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
     for (size_t i = 0; i < n; ++i) out[i] = static_cast<double>(h[i]);
     return ABMX_OK;
 }
 
 int Engine::last_metrics(long long* out) {
+    int rc = finalize();
+    if (rc) return rc;
     if (last_run_steps == 0) {
         CK(cudaMemcpyAsync(out, d_metrics_step, sizeof(long long) * 4 * R, cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
@@ -1113,6 +1099,8 @@ int Engine::last_metrics(long long* out) {
 }
 
 int Engine::last_events(abmx_predation_events* out) {
+    int rc = finalize();
+    if (rc) return rc;
     const int p = static_cast<int>((host_epoch - 1) & 1);
     std::vector<Events> h(static_cast<size_t>(R));
     CK(cudaMemcpyAsync(h.data(), params.ev + static_cast<size_t>(p) * R, sizeof(Events) * R, cudaMemcpyDeviceToHost, stream));
@@ -1137,6 +1125,8 @@ int Engine::last_events(abmx_predation_events* out) {
 
 int Engine::export_species(int r, int s, uint8_t* active, int64_t* ids, int64_t* types, int64_t* ages,
                            int64_t* x, int64_t* y, double* energy, int32_t* num_active, int64_t* next_id) {
+    int rc = finalize();
+    if (rc) return rc;
     const Params& P = params;
     const size_t n = static_cast<size_t>(P.N[s]);
     const size_t off = static_cast<size_t>(r) * P.Npad[s];
@@ -1166,6 +1156,8 @@ int Engine::export_species(int r, int s, uint8_t* active, int64_t* ids, int64_t*
 int Engine::import_species(int r, int s, const uint8_t* active, const int64_t* ids, const int64_t* ages,
                            const int64_t* x, const int64_t* y, const double* energy, int32_t num_active,
                            int64_t next_id) {
+    int rc = finalize();
+    if (rc) return rc;
     const Params& P = params;
     const size_t n = static_cast<size_t>(P.N[s]);
     std::vector<uint8_t> act(n);
@@ -1179,20 +1171,12 @@ int Engine::import_species(int r, int s, const uint8_t* active, const int64_t* i
             return ABMX_E_DOMAIN;
         }
         age[i] = static_cast<int>(ages[i]);
-        if (act[i]) {
-            if (x[i] < 0 || x[i] >= P.W || y[i] < 0 || y[i] >= P.H) {
-                abmx_internal::set_error("active agent outside the lattice");
-                return ABMX_E_DOMAIN;
-            }
-            cell[i] = static_cast<int>(y[i] * P.W + x[i]);
-        } else {
-            // placeholder state must be representable; step_agents blends it to zero
-            if (x[i] < 0 || x[i] >= P.W || y[i] < 0 || y[i] >= P.H) {
-                abmx_internal::set_error("placeholder coordinates outside the lattice");
-                return ABMX_E_DOMAIN;
-            }
-            cell[i] = static_cast<int>(y[i] * P.W + x[i]);
+        if (x[i] < 0 || x[i] >= P.W || y[i] < 0 || y[i] >= P.H) {
+            abmx_internal::set_error(act[i] ? "active agent outside the lattice"
+                                            : "placeholder coordinates outside the lattice");
+            return ABMX_E_DOMAIN;
         }
+        cell[i] = static_cast<int>(y[i] * P.W + x[i]);
     }
     if (pop != num_active) {
         abmx_internal::set_error("num_active must equal popcount(active)");
@@ -1220,6 +1204,8 @@ int Engine::import_species(int r, int s, const uint8_t* active, const int64_t* i
 // Lazy regrow (see the cell words): at the end of the last completed step E, a cell is ready
 // iff due <= E, and its reference counter is regrow = due - E (predation.cpp:252-258).
 int Engine::export_world(int r, uint8_t* ready, int64_t* regrow) {
+    int rc = finalize();
+    if (rc) return rc;
     const Params& P = params;
     const size_t C = static_cast<size_t>(P.C);
     std::vector<uint4> w(C);
@@ -1241,6 +1227,8 @@ int Engine::export_world(int r, uint8_t* ready, int64_t* regrow) {
 }
 
 int Engine::import_world(int r, const uint8_t* ready, const int64_t* regrow) {
+    int rc = finalize();
+    if (rc) return rc;
     Params& P = params;
     const size_t C = static_cast<size_t>(P.C);
     const unsigned long long E = host_epoch - 1;
@@ -1276,9 +1264,11 @@ int Engine::import_world(int r, const uint8_t* ready, const int64_t* regrow) {
     return ABMX_OK;
 }
 
+// (parent slot, child slot) of the last step's births: the k-th valid row (tile-local rows
+// concatenated in tile order) and the child slot recorded when the birth was applied.
 int Engine::birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t cap) {
-    // pairs are stored tile-locally (k_update) and matched by global rank (k_spawn): rebuild
-    // the k-th valid row and the k-th free slot from the per-tile counts
+    int rc = finalize();
+    if (rc) return rc;
     const Params& P = params;
     SpeciesRep sr;
     const int tiles = P.tiles[s];
@@ -1287,56 +1277,23 @@ int Engine::birth_pairs(int r, int s, int32_t* parent, int32_t* child, int32_t c
     CK(cudaMemcpyAsync(tc.data(), P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride,
                        tiles * sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream));
     const size_t off = static_cast<size_t>(r) * P.Npad[s];
-    std::vector<int> rows(static_cast<size_t>(P.Npad[s])), frees(static_cast<size_t>(P.Npad[s]));
+    std::vector<int> rows(static_cast<size_t>(P.Npad[s])), kids(static_cast<size_t>(P.Npad[s]));
     CK(cudaMemcpyAsync(rows.data(), P.row_at[s] + off, rows.size() * 4, cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(frees.data(), P.free_at[s] + off, frees.size() * 4, cudaMemcpyDeviceToHost, stream));
+    CK(cudaMemcpyAsync(kids.data(), P.birth_child[s] + off, kids.size() * 4, cudaMemcpyDeviceToHost, stream));
     CK(cudaStreamSynchronize(stream));
-    int k = 0, kf = 0;
+    int k = 0;
     for (int t = 0; t < tiles && k < sr.pairs; ++t) {
         const int nv = static_cast<int>(abmx_dev::lo31(tc[t]));
         for (int j = 0; j < nv && k < sr.pairs; ++j, ++k)
             if (k < cap) parent[k] = rows[static_cast<size_t>(t) * kTile + j];
     }
-    for (int t = 0; t < tiles && kf < sr.pairs; ++t) {
-        const int nf = static_cast<int>(abmx_dev::hi31(tc[t]));
-        for (int j = 0; j < nf && kf < sr.pairs; ++j, ++kf)
-            if (kf < cap) child[kf] = frees[static_cast<size_t>(t) * kTile + j];
-    }
+    for (k = 0; k < sr.pairs && k < cap; ++k) child[k] = kids[static_cast<size_t>(k)];
     return sr.pairs;
-}
-
-// L2 flush between timed steps: overwrite a buffer larger than the 126 MB L2, then read a
-// second one so L2 is left holding CLEAN lines (otherwise the timed step would pay for
-// writing back the flush buffer's dirty lines, traffic that is not part of the workload).
-__global__ void k_flush(uint4* p, size_t n) {
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x)
-        p[i] = make_uint4(static_cast<unsigned>(i), 0u, 0u, 0u);
-}
-__global__ void k_flush_read(const uint4* p, size_t n, unsigned* sink) {
-    unsigned acc = 0;
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const uint4 v = p[i];
-        acc ^= v.x ^ v.y ^ v.z ^ v.w;
-    }
-    if (acc == 0x9E3779B9u) *sink = acc;  // practically never; keeps the loads alive
 }
 
 int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_kernel, double* step_ms) {
     if (steps <= 0) return ABMX_OK;
-    int rc = set_t(t0);
-    if (rc) return rc;
-    const size_t mbytes = sizeof(long long) * 4 * static_cast<size_t>(R) * static_cast<size_t>(steps);
-    if (mbytes > run_metrics_bytes) {
-        CK(cudaStreamSynchronize(stream));
-        if (d_run_metrics) cudaFree(d_run_metrics);
-
-        CK(cudaMalloc(&d_run_metrics, mbytes));
-        run_metrics_bytes = mbytes;
-    }
-    CK(cudaMemsetAsync(d_run_metrics, 0, mbytes, stream));
-    rc = set_metrics_target(d_run_metrics, static_cast<unsigned>(steps));
+    int rc = prepare_run(t0, steps);
     if (rc) return rc;
     if (flush_bytes > flush_cap) {
         if (flush_buf) cudaFree(flush_buf);
@@ -1344,12 +1301,12 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
         CK(cudaMemset(flush_buf, 0, 2 * flush_bytes + 64));
         flush_cap = flush_bytes;
     }
-    // per-kernel mode records 2 events around every kernel of every step and synchronises
-    // only at the end, so host launch latency never lands inside a kernel's bracket
+    // per-kernel mode records 2 events around every kernel of every step and synchronises only
+    // at the end, so host launch latency never lands inside a kernel's bracket
     const size_t per_step = per_kernel ? 2 * kNumKernels : 2;
     std::vector<cudaEvent_t> ev(per_step * static_cast<size_t>(steps));
     for (auto& e : ev) CK(cudaEventCreate(&e));
-    if (!per_kernel && !fused && !graph_exec) {
+    if (!per_kernel && !graph_exec) {
         rc = build_graph();
         if (rc) return rc;
     }
@@ -1363,27 +1320,16 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
         }
         cudaEvent_t* e = &ev[per_step * static_cast<size_t>(q)];
         if (per_kernel) {
-            params.epoch = host_epoch;
-            if (host_epoch % kEpochClear == 0)
-                k_clear_cells<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(params.cw, static_cast<size_t>(R) * params.Cpad);
-            void* args[1] = {&params};
-            for (int k = 0; k < kNumKernels; ++k) {
-                CK(cudaEventRecord(e[2 * k], stream));
-                CK(cudaLaunchKernel(kKernelFns[k], dim3(grid(k)), dim3(kT), args, k == 3 ? spawn_smem : 0, stream));
-                CK(cudaEventRecord(e[2 * k + 1], stream));
-            }
-            abmx_internal::count_launch(kNumKernels);
-            params.needs_blend = 0;
-            params.t += 1;
-            params.run_step += 1;
-            ++host_epoch;
+            rc = enqueue_step(e);
         } else {
             CK(cudaEventRecord(e[0], stream));
-            rc = launch_steps(1);
-            if (rc) return rc;
+            rc = enqueue_step(nullptr);
             CK(cudaEventRecord(e[1], stream));
         }
+        if (rc) return rc;
     }
+    rc = finalize();  // the last step's births (outside the timed brackets)
+    if (rc) return rc;
     CK(cudaStreamSynchronize(stream));
     for (long long q = 0; q < steps; ++q) {
         cudaEvent_t* e = &ev[per_step * static_cast<size_t>(q)];
@@ -1391,6 +1337,7 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
         if (per_kernel) {
             double tot = 0.0;
             for (int k = 0; k < kNumKernels; ++k) {
+                if (!launched(k)) continue;
                 CK(cudaEventElapsedTime(&ms, e[2 * k], e[2 * k + 1]));
                 kernel_ms[k] += ms;
                 kernel_launches[k] += 1;

@@ -263,17 +263,19 @@ def test_golden_run_batch_from_reference(abmx):
         assert np.array_equal(got, np.array(g["metrics"])), path
 
 
-@pytest.mark.parametrize("mode", [0, 1])
-def test_fused_and_graph_modes_identical(abmx, oracle, mode):
-    """The cooperative single-kernel step and the per-phase graph give the oracle's states."""
+@pytest.mark.parametrize("cfgname", ["sparse", "crowded"])
+def test_timed_per_kernel_path_identical(abmx, oracle, cfgname):
+    """bench(per_kernel) launches the kernels directly (not the graph): same states; both the
+    list-walk pairing (sparse grid) and the sort-based pairing kernel (crowded grid)."""
+    cfgd = tiny(width=40, height=40, n_sheep0=200, n_wolves0=60) if cfgname == "sparse" else tiny()
     seed = abmx.replica_seeds(7, 1)[0]
-    gpu, orc = make_pair(abmx, oracle, tiny(width=30, height=30, n_sheep0=200, n_wolves0=60), seed)
-    gpu.set_mode(mode)
-    got = gpu.run(1, 30)[0]
+    gpu, orc = make_pair(abmx, oracle, cfgd, seed)
+    ms, got = gpu.bench(1, 30, flush_bytes=0, per_kernel=True)
     for t in range(1, 31):
         orc.step(t)
-        assert got[t - 1].astype(np.int64).tolist() == orc.metrics(), t
-    assert_same_state(gpu, orc, f"mode {mode}")
+        assert got[0, t - 1].astype(np.int64).tolist() == orc.metrics(), t
+    assert_same_state(gpu, orc, cfgname)
+    assert (ms > 0).all()
 
 
 @pytest.mark.parametrize("delay", [1, 2, 300])

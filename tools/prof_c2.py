@@ -13,7 +13,6 @@ ap.add_argument("--warmup", type=int, default=5)
 ap.add_argument("--ensemble", action="store_true", help="profile the C3 SMEM ensemble kernel")
 ap.add_argument("--flush", type=int, default=256 << 20, help="L2 flush bytes before each step (0 = warm)")
 ap.add_argument("--graph", action="store_true", help="whole-step launches (default: per-kernel launches)")
-ap.add_argument("--mode", type=int, default=1, help="0 fused cooperative step, 1 per-phase graph")
 a = ap.parse_args()
 if a.ensemble:
     cfg = abmx.PredationConfig(width=100, height=100, n_sheep0=600, n_wolves0=400,
@@ -24,13 +23,9 @@ if a.ensemble:
 cfg = abmx.PredationConfig(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000,
                            sheep_capacity=524288, wolf_capacity=524288)
 m = abmx.PredationModel(cfg, abmx.replica_seeds(7, 1)[0])
-m.set_mode(a.mode)
 m.bench(1, a.warmup, a.flush, per_kernel=not a.graph)
-if a.graph and a.mode == 0:
-    m.phase_times(True)
 ms, met = m.bench(a.warmup + 1, a.steps, a.flush, per_kernel=not a.graph)
-if a.graph and a.mode == 0:
-    print("phase us", [round(x / a.steps / 1000, 2) for x in m.phase_times(False)])
+
 if not a.graph:
     print("kernel ms", {k: round(v[0] / max(v[1], 1) * 1000, 2) for k, v in m.kernel_times().items()})
 print("steps ms", [round(x, 4) for x in ms], "metrics", met[0, -1].tolist())
