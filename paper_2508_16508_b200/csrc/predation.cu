@@ -52,35 +52,69 @@ __device__ __forceinline__ long long to_fx(double e) {
     return __double2ll_rn(__dmul_rn(e, 1048576.0));
 }
 
-__device__ __forceinline__ void load4_u8(const uint8_t* p, uint8_t (&v)[kS]) {
-    const uint32_t w = *reinterpret_cast<const uint32_t*>(p);
+// kS-wide vector accesses of one thread's consecutive slots (kS = 8: 8 B of u8, 32 B of i32,
+// 64 B of f64 per thread and column)
+__device__ __forceinline__ void loadk_u8(const uint8_t* p, uint8_t (&v)[kS]) {
+    static_assert(kS == 2 || kS == 4 || kS == 8, "2, 4 or 8 slots per thread");
+    unsigned long long w;
+    if constexpr (kS == 8) {
+        w = *reinterpret_cast<const unsigned long long*>(p);
+    } else if constexpr (kS == 4) {
+        w = *reinterpret_cast<const uint32_t*>(p);
+    } else {
+        w = *reinterpret_cast<const unsigned short*>(p);
+    }
 #pragma unroll
     for (int k = 0; k < kS; ++k) v[k] = static_cast<uint8_t>(w >> (8 * k));
 }
-__device__ __forceinline__ void store4_u8(uint8_t* p, const uint8_t (&v)[kS]) {
-    *reinterpret_cast<uint32_t*>(p) =
-        v[0] | (v[1] << 8) | (v[2] << 16) | (static_cast<uint32_t>(v[3]) << 24);
+__device__ __forceinline__ void storek_u8(uint8_t* p, const uint8_t (&v)[kS]) {
+    unsigned long long w = 0;
+#pragma unroll
+    for (int k = 0; k < kS; ++k) w |= static_cast<unsigned long long>(v[k]) << (8 * k);
+    if constexpr (kS == 8) {
+        *reinterpret_cast<unsigned long long*>(p) = w;
+    } else if constexpr (kS == 4) {
+        *reinterpret_cast<uint32_t*>(p) = static_cast<uint32_t>(w);
+    } else {
+        *reinterpret_cast<unsigned short*>(p) = static_cast<unsigned short>(w);
+    }
 }
-__device__ __forceinline__ void load4_f64(const double* p, double (&v)[kS]) {
-    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = b.x;
-    v[3] = b.y;
+__device__ __forceinline__ void loadk_f64(const double* p, double (&v)[kS]) {
+#pragma unroll
+    for (int q = 0; q < kS / 2; ++q) {
+        const double2 d = reinterpret_cast<const double2*>(p)[q];
+        v[2 * q] = d.x;
+        v[2 * q + 1] = d.y;
+    }
 }
-__device__ __forceinline__ void store4_f64(double* p, const double (&v)[kS]) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v[0], v[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
+__device__ __forceinline__ void storek_f64(double* p, const double (&v)[kS]) {
+#pragma unroll
+    for (int q = 0; q < kS / 2; ++q) reinterpret_cast<double2*>(p)[q] = make_double2(v[2 * q], v[2 * q + 1]);
 }
-__device__ __forceinline__ void load4_i32(const int* p, int (&v)[kS]) {
-    const int4 a = *reinterpret_cast<const int4*>(p);
-    v[0] = a.x;
-    v[1] = a.y;
-    v[2] = a.z;
-    v[3] = a.w;
+__device__ __forceinline__ void loadk_i32(const int* p, int (&v)[kS]) {
+    if constexpr (kS == 2) {
+        const int2 a = *reinterpret_cast<const int2*>(p);
+        v[0] = a.x;
+        v[1] = a.y;
+    } else {
+#pragma unroll
+        for (int q = 0; q < kS / 4; ++q) {
+            const int4 a = reinterpret_cast<const int4*>(p)[q];
+            v[4 * q] = a.x;
+            v[4 * q + 1] = a.y;
+            v[4 * q + 2] = a.z;
+            v[4 * q + 3] = a.w;
+        }
+    }
 }
-__device__ __forceinline__ void store4_i32(int* p, const int (&v)[kS]) {
-    *reinterpret_cast<int4*>(p) = make_int4(v[0], v[1], v[2], v[3]);
+__device__ __forceinline__ void storek_i32(int* p, const int (&v)[kS]) {
+    if constexpr (kS == 2) {
+        *reinterpret_cast<int2*>(p) = make_int2(v[0], v[1]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < kS / 4; ++q)
+            reinterpret_cast<int4*>(p)[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+    }
 }
 
 template <class T>
@@ -166,19 +200,19 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
             memset(&ev[rr], 0, sizeof(Events));
     }
     // dense species: issue the column loads together with the mask load
-    uint8_t act[kS] = {0, 0, 0, 0};
-    int cell[kS] = {0, 0, 0, 0}, age[kS] = {0, 0, 0, 0};
+    uint8_t act[kS] = {};
+    int cell[kS] = {}, age[kS] = {};
     const bool live = i0 < N;
     if (live) {
         if (kMove && s == 0) {
-            load4_i32(P.cell[s] + base, cell);
-            load4_i32(P.age[s] + base, age);
+            loadk_i32(P.cell[s] + base, cell);
+            loadk_i32(P.age[s] + base, age);
         }
-        load4_u8(P.active[s] + base, act);
+        loadk_u8(P.active[s] + base, act);
     }
 
     // ---------------- (a) births of step P.birth_epoch (rank-match, lifecycle.cpp:144-195)
-    bool born[kS] = {false, false, false, false};
+    bool born[kS] = {};
     bool born_any = false;
     if (P.pending) {
         const int tiles = P.tiles[s];
@@ -271,7 +305,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
             }
         }
         if (!kMove && born_any) {
-            store4_u8(P.active[s] + base, act);
+            storek_u8(P.active[s] + base, act);
 #pragma unroll
             for (int k = 0; k < kS; ++k)
                 if (born[k]) {
@@ -285,13 +319,14 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
     // ---------------- (b) move + bin
     const unsigned e8 = epoch8(epoch), tag = min_tag(epoch);
     const unsigned long long key = split(split(split(P.seeds[r], 3), static_cast<unsigned long long>(P.t)), s);
-    const bool any = (act[0] | act[1] | act[2] | act[3]) != 0;
-    bool first[kS] = {false, false, false, false};
+    bool any = false;
+    for (int k = 0; k < kS; ++k) any |= act[k] != 0;
+    bool first[kS] = {};
     if (live && any) {
         if (s == 1) {  // sparse species: columns only where something lives (newborns keep theirs)
             int c2[kS], a2[kS];
-            load4_i32(P.cell[s] + base, c2);
-            load4_i32(P.age[s] + base, a2);
+            loadk_i32(P.cell[s] + base, c2);
+            loadk_i32(P.age[s] + base, a2);
 #pragma unroll
             for (int k = 0; k < kS; ++k)
                 if (!born[k]) {
@@ -328,9 +363,9 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
                 P.next[s][base + k] = cur ? static_cast<int>(old[k] & kNil) : -1;
                 first[k] = P.crowded && s == 1 && !cur;
             }
-        store4_i32(P.cell[s] + base, cell);
-        store4_i32(P.age[s] + base, age);
-        if (born_any) store4_u8(P.active[s] + base, act);
+        storek_i32(P.cell[s] + base, cell);
+        storek_i32(P.age[s] + base, age);
+        if (born_any) storek_u8(P.active[s] + base, act);
     }
     if (live && P.needs_blend) {  // step_agents masks placeholder state back to defaults
 #pragma unroll
@@ -341,7 +376,8 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
             }
     }
     if (P.crowded && s == 1) {  // block-aggregated append of the cells this thread's wolves opened
-        const unsigned nfirst = first[0] + first[1] + first[2] + first[3];
+        unsigned nfirst = 0;
+        for (int k = 0; k < kS; ++k) nfirst += first[k];
         unsigned long long total;
         const unsigned long long off = block_excl_scan<kT>(nfirst, s_scan, &total);
         if (threadIdx.x == 0 && total) s_base = atomicAdd(&P.ctl->occ, static_cast<unsigned>(total));
@@ -497,28 +533,31 @@ __device__ void update_phase(const Params& P, unsigned b) {
     const size_t sb = static_cast<size_t>(r) * P.Npad[0], wb = static_cast<size_t>(r) * P.Npad[1];
     const double gain = P.gain[s], metab = P.metab, prob = P.prob[s], frac = P.frac;
 
-    uint8_t act[kS] = {0, 0, 0, 0};
-    double E[kS] = {0.0, 0.0, 0.0, 0.0}, child[kS] = {0.0, 0.0, 0.0, 0.0};
-    int cell[kS] = {0, 0, 0, 0};
-    bool valid[kS] = {false, false, false, false}, freek[kS] = {false, false, false, false};
+    uint8_t act[kS] = {};
+    double E[kS] = {}, child[kS] = {};
+    int cell[kS] = {};
+    bool valid[kS] = {}, freek[kS] = {};
     unsigned n_graze = 0, n_metab = 0, n_death = 0, n_eaten = 0;
     long long fx_removed = 0;
     if (i0 < N) {
-        uint8_t flg[kS] = {0, 0, 0, 0};
+        uint8_t flg[kS] = {};
         if (s == 0) {  // dense species: issue the column loads with the mask
-            load4_f64(P.energy[s] + base, E);
-            load4_i32(P.cell[s] + base, cell);
+            loadk_f64(P.energy[s] + base, E);
+            loadk_i32(P.cell[s] + base, cell);
         }
-        load4_u8(P.active[s] + base, act);
-        if (P.crowded) load4_u8(P.flag[s] + base, flg);
-        const bool any = (act[0] | act[1] | act[2] | act[3]) != 0;
+        loadk_u8(P.active[s] + base, act);
+        if (P.crowded) loadk_u8(P.flag[s] + base, flg);
+        bool any = false;
+    for (int k = 0; k < kS; ++k) any |= act[k] != 0;
         if (s == 1 && any) {
-            load4_f64(P.energy[s] + base, E);
-            load4_i32(P.cell[s] + base, cell);
+            loadk_f64(P.energy[s] + base, E);
+            loadk_i32(P.cell[s] + base, cell);
         }
-        if (P.crowded && (flg[0] | flg[1] | flg[2] | flg[3])) {
-            const uint8_t z[kS] = {0, 0, 0, 0};
-            store4_u8(P.flag[s] + base, z);
+        bool anyflg = false;
+        for (int k = 0; k < kS; ++k) anyflg |= flg[k] != 0;
+        if (P.crowded && anyflg) {
+            const uint8_t z[kS] = {};
+            storek_u8(P.flag[s] + base, z);
         }
         if (any) {
             // the cell word of every live agent (list heads, lowest sheep slot, grass due)
@@ -593,9 +632,9 @@ __device__ void update_phase(const Params& P, unsigned b) {
             }
             freek[k] = !alive && i < N;
         }
-        if (any) store4_f64(P.energy[s] + base, E);
+        if (any) storek_f64(P.energy[s] + base, E);
         if (died_any) {
-            store4_u8(P.active[s] + base, act);
+            storek_u8(P.active[s] + base, act);
 #pragma unroll
             for (int k = 0; k < kS; ++k)
                 if (!act[k] && i0 + k < N) {
@@ -666,7 +705,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
 }
 
 // ============================================================== kernels
-__global__ void __launch_bounds__(kT) k_move(Params P) {
+__global__ void __launch_bounds__(kT, kMinB) k_move(Params P) {
     extern __shared__ unsigned long long s_pre[];
     move_phase<true>(P, blockIdx.x, gridDim.x, s_pre);
 }
@@ -674,7 +713,7 @@ __global__ void __launch_bounds__(kT) k_finalize(Params P) {
     extern __shared__ unsigned long long s_pre[];
     move_phase<false>(P, blockIdx.x, gridDim.x, s_pre);
 }
-__global__ void __launch_bounds__(kT) k_update(Params P) { update_phase(P, blockIdx.x); }
+__global__ void __launch_bounds__(kT, kMinB) k_update(Params P) { update_phase(P, blockIdx.x); }
 
 // ============================================================== init (create_agents)
 // predation.cpp:22-33 + lifecycle.cpp:53-85: x, y, energy drawn for ALL slots from

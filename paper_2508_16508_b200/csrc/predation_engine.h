@@ -12,8 +12,18 @@
 
 namespace abmx_pred {
 
-constexpr int kT = 256;          // threads per CTA
-constexpr int kS = 4;            // slots per thread
+#ifndef ABMX_PRED_KT
+#define ABMX_PRED_KT 256
+#endif
+#ifndef ABMX_PRED_KS
+#define ABMX_PRED_KS 4
+#endif
+#ifndef ABMX_PRED_MINB
+#define ABMX_PRED_MINB 4
+#endif
+constexpr int kT = ABMX_PRED_KT;      // threads per CTA
+constexpr int kS = ABMX_PRED_KS;      // slots per thread (2, 4 or 8)
+constexpr int kMinB = ABMX_PRED_MINB; // CTAs per SM the hot kernels are register-limited to
 constexpr int kTile = kT * kS;   // slots per tile (k_move and k_update use the same tiling)
 constexpr int kNumKernels = 3;   // k_move, k_cells (crowded grids only), k_update
 constexpr int kEpochClear = 128; // cell tags are cleared every kEpochClear steps (epoch8 period 255)

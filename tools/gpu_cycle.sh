@@ -9,6 +9,6 @@ tail -3 gpurun_out/t_$TAG.log
 timeout 600 python bench.py ${BENCH_ARGS:---no-cpu-baseline} > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo bench_rc=$?
 if [ -z "$NO_NCU" ]; then
   python tools/prof_c2.py > gpurun_out/prof_plain_$TAG.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"${2:-k_move|k_update|k_cells|k_spawn}" -s 20 -c 4 \
+  ncu --set full --clock-control none --import-source on -k regex:"${2:-k_move|k_update|k_cells|k_spawn}" -s 8 -c 4 \
       -o gpurun_out/prof_$TAG python tools/prof_c2.py > gpurun_out/ncu_$TAG.log 2>&1; echo ncu_rc=$?
 fi

@@ -9,7 +9,13 @@ n = int(sys.argv[3]) if len(sys.argv) > 3 else 14
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "-k", kern, "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
-hdr, data = rows[1], rows[2:]
+hdr = rows[1]
+data = []
+for row in rows[2:]:  # first kernel instance only
+    if row and row[0] == "Kernel Name":
+        break
+    if len(row) == len(hdr):
+        data.append(row)
 si = hdr.index("Warp Stall Sampling (All Samples)")
 val = lambda r: int(r[si]) if r[si].isdigit() else 0
 print("total samples", sum(val(r) for r in data))
