@@ -180,6 +180,34 @@ __device__ __forceinline__ int find_tile(const unsigned long long* pre, int tile
     return lo;
 }
 
+// Bookkeeping of step P.birth_epoch for (replica r, species s) once its totals F (free slots)
+// and Q (valid parent rows) are known: counters (double-buffered by parity), the ledger, the
+// metrics row (predation.cpp:281-287) and, for sheep, the lazy-regrow grass count. Run either
+// by tile 0 of k_move / k_finalize (P.book) or by k_book (the per-call step graph).
+__device__ void book_step(const Params& P, int s, int r, int F, int Q) {
+    const int pb = static_cast<int>(P.birth_epoch & 1);
+    const int N = P.N[s];
+    const int pairs = F < Q ? F : Q;
+    SpeciesRep* sr = &P.rep[static_cast<size_t>(r) * 2 + s];
+    Events* ev = P.ev + static_cast<size_t>(pb) * P.R + r;
+    sr->next_id[pb ^ 1] = sr->next_id[pb] + pairs;
+    sr->num_active[pb ^ 1] = N - F + pairs;
+    sr->pairs = pairs;
+    sr->Q = Q;
+    atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
+    atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
+    long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
+    row[s] = N - F + pairs;
+    if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
+    if (s == 0) {  // ready cells after that step's (lazy) regrow: - grazed + those due
+        unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.birth_epoch % P.due_ring];
+        const long long ng = P.n_grass[r] - static_cast<long long>(ev->grass_eaten) + *due;
+        *due = 0;
+        P.n_grass[r] = ng;
+        row[2] = ng;
+    }
+}
+
 // ============================================================== k_move / k_finalize
 // kMove = false: k_finalize (births + counters only).
 template <bool kMove>
@@ -285,24 +313,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
         Events* ev = P.ev + static_cast<size_t>(pb) * P.R + r;
         if (threadIdx.x == 0) {
             if (fx_tot) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_dropped_fx[s]), static_cast<unsigned long long>(fx_tot));
-            if (tile == 0) {  // counters, ledger and the metrics row of step birth_epoch
-                sr->next_id[pb ^ 1] = base_id + pairs;
-                sr->num_active[pb ^ 1] = N - F + pairs;
-                sr->pairs = pairs;
-                sr->Q = Q;
-                atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
-                atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
-                long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
-                row[s] = N - F + pairs;
-                if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
-                if (s == 0) {  // ready cells after that step's (lazy) regrow: - grazed + those due
-                    unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.birth_epoch % P.due_ring];
-                    const long long ng = P.n_grass[r] - static_cast<long long>(ev->grass_eaten) + *due;
-                    *due = 0;
-                    P.n_grass[r] = ng;
-                    row[2] = ng;
-                }
-            }
+            if (tile == 0 && P.book) book_step(P, s, r, F, Q);
         }
         if (!kMove && born_any) {
             storek_u8(P.active[s] + base, act);
@@ -715,6 +726,25 @@ __global__ void __launch_bounds__(kT) k_finalize(Params P) {
 }
 __global__ void __launch_bounds__(kT, kMinB) k_update(Params P) { update_phase(P, blockIdx.x); }
 
+// k_book: one CTA per replica, both species: totals of the tile counts -> book_step, then the
+// finished metrics row goes straight to mapped host memory (collect_metrics needs no copy).
+__global__ void __launch_bounds__(kT) k_book(Params P) {
+    __shared__ unsigned long long s_red[kT / 32];
+    const int r = blockIdx.x;
+    for (int s = 0; s < 2; ++s) {
+        const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
+        unsigned long long v = 0;
+        for (int t = threadIdx.x; t < P.tiles[s]; t += kT) v += tc[t];
+        const unsigned long long tot = block_sum<unsigned long long>(v, s_red);
+        if (threadIdx.x == 0) book_step(P, s, r, static_cast<int>(hi31(tot)), static_cast<int>(lo31(tot)));
+    }
+    if (threadIdx.x == 0 && P.host_row) {
+        const long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
+        long long* h = P.host_row + static_cast<size_t>(r) * 4;
+        for (int q = 0; q < 4; ++q) h[q] = row[q];
+    }
+}
+
 // ============================================================== init (create_agents)
 // predation.cpp:22-33 + lifecycle.cpp:53-85: x, y, energy drawn for ALL slots from
 // seed.split(20|21).split(CreateField=1).split(ordinal); slots >= n0 reset to placeholders.
@@ -805,6 +835,9 @@ const char* kernel_name(int k) { return (k >= 0 && k < kNumKernels) ? kKernelNam
 Engine::~Engine() {
     if (graph_exec) cudaGraphExecDestroy(graph_exec);
     if (graph) cudaGraphDestroy(graph);
+    if (step_exec) cudaGraphExecDestroy(step_exec);
+    if (h_metrics_pinned) cudaFreeHost(h_metrics_pinned);
+    if (step_graph) cudaGraphDestroy(step_graph);
     for (void* p : allocs) cudaFree(p);
     if (d_run_metrics) cudaFree(d_run_metrics);
     if (flush_buf) cudaFree(flush_buf);
@@ -949,6 +982,7 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     P.metrics_stride = 1;
     P.run_step = 0;
     P.pending = 0;
+    P.book = 1;
     const int g = abmx_internal::num_sms() * 8;
     (void)cudaGetLastError();
     k_init_species<<<g, 256, 0, stream>>>(P, 0, c.n_sheep0);
@@ -957,6 +991,9 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     abmx_internal::count_launch(3);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h_metrics_pinned), sizeof(long long) * 4 * R, cudaHostAllocMapped));
+    memset(h_metrics_pinned, 0, sizeof(long long) * 4 * R);
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_metrics_dev), h_metrics_pinned, 0));
     return ABMX_OK;
 }
 
@@ -1023,6 +1060,7 @@ int Engine::enqueue_step(cudaEvent_t* ev) {
     // this step's births stay pending until the next k_move (or k_finalize) applies them
     params.needs_blend = 0;
     params.pending = 1;
+    params.book = 1;
     params.birth_epoch = host_epoch;
     params.birth_row = params.run_step;
     params.t += 1;
@@ -1038,6 +1076,7 @@ int Engine::finalize() {
     CK(cudaLaunchKernel(reinterpret_cast<void*>(k_finalize), dim3(grid(0)), dim3(kT), args, move_smem, stream));
     abmx_internal::count_launch(1);
     params.pending = 0;
+    params.book = 1;
     return ABMX_OK;
 }
 
@@ -1047,11 +1086,14 @@ int Engine::set_t(long long t) {
 }
 
 int Engine::set_metrics_target(long long* d_metrics, unsigned stride) {
-    int rc = finalize();  // a pending birth row belongs to the previous target
-    if (rc) return rc;
+    if (params.pending && params.book) {  // a pending, unbooked row belongs to the previous target
+        int rc = finalize();
+        if (rc) return rc;
+    }
     params.metrics = d_metrics;
     params.metrics_stride = stride;
     params.run_step = 0;
+    host_row_valid = false;
     return ABMX_OK;
 }
 
@@ -1065,16 +1107,69 @@ int Engine::launch_steps(long long steps) {
     return ABMX_OK;
 }
 
+// PredationModel::step(t) as ONE graph launch: zero the metrics row, the step's kernels, then
+// k_book completes the metrics row and counters; the births stay pending (booked) and are
+// applied by the next k_move, or by k_finalize before any state read.
 int Engine::step(long long t) {
-    int rc = set_metrics_target(d_metrics_step, 1);
+    int rc = set_metrics_target(d_metrics_step, 1);  // also applies any births still pending
     if (rc) return rc;
-    CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
     set_t(t);
-    rc = launch_steps(1);
-    if (rc) return rc;
-    rc = finalize();
+    (void)cudaGetLastError();
+    params.epoch = host_epoch;
+    if (host_epoch % kEpochClear == 0)
+        k_clear_cells<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(params.cw, static_cast<size_t>(R) * params.Cpad);
+    Params fin = params;  // k_book: the bookkeeping of this very step
+    fin.birth_epoch = host_epoch;
+    fin.birth_row = params.run_step;
+    fin.host_row = h_metrics_dev;
+    void* args[1] = {&params};
+    void* fargs[1] = {&fin};
+    auto kparams = [&](int k, void** a) {
+        cudaKernelNodeParams kp{};
+        kp.func = k < kNumKernels ? kKernelFns[k] : reinterpret_cast<void*>(k_book);
+        kp.gridDim = dim3(k < kNumKernels ? grid(k) : static_cast<unsigned>(R));
+        kp.blockDim = dim3(kT);
+        kp.sharedMemBytes = static_cast<unsigned>(k < kNumKernels ? smem(k) : 0);
+        kp.kernelParams = a;
+        return kp;
+    };
+    if (!step_exec) {
+        CK(cudaGraphCreate(&step_graph, 0));
+        cudaMemsetParams mp{};
+        mp.dst = d_metrics_step;
+        mp.value = 0;
+        mp.elementSize = 4;
+        mp.width = static_cast<size_t>(R) * 4 * 2;  // R rows of 4 int64
+        mp.height = 1;
+        cudaGraphNode_t prev;
+        CK(cudaGraphAddMemsetNode(&prev, step_graph, nullptr, 0, &mp));
+        for (int k = 0; k <= kNumKernels; ++k) {
+            if (k < kNumKernels && !launched(k)) continue;
+            const cudaKernelNodeParams kp = kparams(k, k < kNumKernels ? args : fargs);
+            CK(cudaGraphAddKernelNode(&step_nodes[k], step_graph, &prev, 1, &kp));
+            prev = step_nodes[k];
+        }
+        CK(cudaGraphInstantiate(&step_exec, step_graph, 0));
+    }
+    for (int k = 0; k <= kNumKernels; ++k) {
+        if (k < kNumKernels && !launched(k)) continue;
+        const cudaKernelNodeParams kp = kparams(k, k < kNumKernels ? args : fargs);
+        CK(cudaGraphExecKernelNodeSetParams(step_exec, step_nodes[k], &kp));
+        abmx_internal::count_launch(1);
+    }
+    CK(cudaGraphLaunch(step_exec, stream));
+    params.needs_blend = 0;
+    params.pending = 1;  // births still to apply ...
+    params.book = 0;     // ... but already booked
+    params.birth_epoch = host_epoch;
+    params.birth_row = params.run_step;
+    params.t += 1;
+    params.run_step += 1;
+    ++host_epoch;
     last_run_steps = 0;
-    return rc;
+    host_row_valid = true;
+    CK(cudaGetLastError());
+    return ABMX_OK;
 }
 
 int Engine::prepare_run(long long t0, long long steps) {
@@ -1121,9 +1216,16 @@ int Engine::fetch_run_metrics(double* out) {
 }
 
 int Engine::last_metrics(long long* out) {
-    int rc = finalize();
-    if (rc) return rc;
+    if (params.pending && params.book) {  // the last row is filled by the births pass
+        int rc = finalize();
+        if (rc) return rc;
+    }
     if (last_run_steps == 0) {
+        if (host_row_valid) {  // k_book of the last step() wrote the row to mapped memory
+            CK(cudaStreamSynchronize(stream));
+            memcpy(out, h_metrics_pinned, sizeof(long long) * 4 * R);
+            return ABMX_OK;
+        }
         CK(cudaMemcpyAsync(out, d_metrics_step, sizeof(long long) * 4 * R, cudaMemcpyDeviceToHost, stream));
         CK(cudaStreamSynchronize(stream));
         return ABMX_OK;

@@ -60,7 +60,9 @@ struct Params {
     long long* metrics;              // [R][metrics_stride][4]
     unsigned run_step, metrics_stride, needs_blend, pending;
     unsigned long long birth_epoch;  // step whose births k_move / k_finalize apply (if pending)
-    unsigned birth_row, pad0;        // metrics row of that step
+    unsigned birth_row;              // metrics row of that step
+    unsigned book;                   // 1: the births pass also does that step's bookkeeping
+    long long* host_row;             // k_book: mapped host copy of the metrics row (or null)
     // model constants
     int R, W, H, Cpad;
     long long C;
@@ -104,6 +106,12 @@ struct Engine {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t graph_exec = nullptr;
     cudaGraphNode_t nodes[kNumKernels] = {};
+    cudaGraph_t step_graph = nullptr;          // the API step: memset row, kernels, k_finalize
+    cudaGraphExec_t step_exec = nullptr;
+    cudaGraphNode_t step_nodes[kNumKernels + 1] = {};
+    long long* h_metrics_pinned = nullptr;     // mapped pinned copy of the step() metrics row
+    long long* h_metrics_dev = nullptr;        //   ... its device alias (written by k_book)
+    bool host_row_valid = false;               // the mapped row holds the last step()'s row
     std::vector<void*> allocs;
     long long device_bytes = 0;
     unsigned long long* d_seeds = nullptr;
