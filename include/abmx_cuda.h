@@ -177,6 +177,76 @@ int abmx_ensemble_run(const abmx_predation_config* cfg, uint64_t master, int32_t
 /* 1 if the SMEM-resident path supports cfg */
 int abmx_ensemble_smem_fits(const abmx_predation_config* cfg);
 
+/* ======================================================================= 4. agent sets
+ * The generic lifecycle and subset operations on an AgentSet whose
+ * columns live in device memory. Callbacks (std::function ApplyFn / SlotUpdateFn,
+ * kernels.hpp:62-102) cannot cross a C-ABI, so the apply is a COLUMN COPY: state column c of
+ * a paired slot receives column c of its row (a NULL row column leaves that state column
+ * alone). All entries are stream-ordered on `stream` (cudaStream_t as void*); counts stay in
+ * device memory. Element sizes are 1, 4 or 8 bytes (bool / int32 / int64 / f64 columns). */
+typedef struct abmx_column {
+    void* data;         /* device pointer, capacity (state) or m (rows) elements */
+    int32_t elem_size;  /* 1, 4 or 8 */
+    int32_t pad;
+} abmx_column;
+
+/* AgentSet (agent_set.hpp:15-77). counters: device int64[3] = {num_active, next_id,
+ * retired count}; retired: device int64[capacity] id stack (used when recycle_ids). */
+typedef struct abmx_agent_set {
+    int32_t capacity;
+    int32_t recycle_ids;          /* AgentSet::set_id_recycling (agent_set.hpp:45-52) */
+    uint8_t* active;
+    int64_t* ids;
+    int64_t* types;
+    int64_t* ages;
+    int64_t* counters;
+    int64_t* retired;
+    int32_t n_state;
+    int32_t n_extra;
+    const abmx_column* state;     /* host array of n_state device columns (reset on removal) */
+    const abmx_column* extra;     /* params / policy columns: moved by permute and sort only */
+} abmx_agent_set;
+
+/* remove_agents (lifecycle.cpp:124-142): live slots with kill[i] != 0 are reset (active, id,
+ * age, state zeroed; type kept, agent_set.cpp:45-58); with recycle_ids their ids are pushed on
+ * the retired stack in slot order. d_killed (nullable, device int64): number removed. */
+int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* d_killed,
+                       void* stream);
+/* spawn_agents (lifecycle.cpp:144-195): the k-th free slot receives the k-th valid row
+ * (copy apply), id = retired.pop() while recycling and non-empty else next_id++, age 0,
+ * type = agent_type if set_type. d_slots[k] / d_rows[k] (nullable, device int32, capacity /
+ * m entries): pair k. d_result (nullable, device int64[2]): {spawned, dropped}. */
+int abmx_agents_spawn(const abmx_agent_set* s, int32_t m, const uint8_t* d_valid,
+                      const abmx_column* rows, int32_t set_type, int64_t agent_type,
+                      int32_t* d_slots, int32_t* d_rows, int64_t* d_result, void* stream);
+/* set_agents_rm / set_agents_sci (kernels.cpp:116-153) with the copy apply: the k-th target
+ * slot receives the k-th valid row, k < min(popcount(target), popcount(valid)). With a copy
+ * apply RM and SCI coincide (kernels.hpp:96-99). d_result (nullable): {pairs, valid rows}. */
+int abmx_agents_set_rm(const abmx_agent_set* s, const uint8_t* d_target, int32_t m,
+                       const uint8_t* d_valid, const abmx_column* rows, int32_t* d_slots,
+                       int32_t* d_rows, int64_t* d_result, void* stream);
+int abmx_agents_set_sci(const abmx_agent_set* s, const uint8_t* d_target, int32_t m,
+                        const uint8_t* d_valid, const abmx_column* rows, int32_t* d_slots,
+                        int32_t* d_rows, int64_t* d_result, void* stream);
+/* set_agents_mask (kernels.cpp:155-167): state column c [i] = values[c][i] where mask[i]. */
+int abmx_agents_set_mask(const abmx_agent_set* s, const uint8_t* d_mask,
+                         const abmx_column* values, void* stream);
+/* select_agents / compact_mask (kernels.cpp:23-35): stable partition, true indices first;
+ * d_count (device int64) = number of true entries. */
+int abmx_agents_select(const uint8_t* d_mask, int32_t n, int32_t* d_indices, int64_t* d_count,
+                       void* stream);
+/* sort_agents (kernels.cpp:52-73): stable permutation by an f64 key (ascending or
+ * descending); ABMX_E_DOMAIN (nothing written) if an active slot has a non-finite key.
+ * Synchronises `stream` once for that check. */
+int abmx_agents_sort_perm(const double* d_key, const uint8_t* d_active, int32_t n,
+                          int32_t descending, int32_t* d_perm, void* stream);
+/* permute_agents (agent_set.cpp:92-108): every column c[i] = c[perm[i]] (gather); indices
+ * outside [0, capacity) give ABMX_E_DOMAIN. */
+int abmx_agents_permute(const abmx_agent_set* s, const int32_t* d_perm, void* stream);
+/* sort_perm + permute; d_perm (nullable) receives the permutation. */
+int abmx_agents_sort(const abmx_agent_set* s, const double* d_key, int32_t descending,
+                     int32_t* d_perm, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,56 @@ int32_t orc_pair(const uint8_t* target, int32_t n, const uint8_t* valid, int32_t
     return p < q ? p : q;
 }
 
+/* lifecycle.cpp:124-142 + agent_set.cpp:45-58 */
+int32_t orc_remove_agents(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* e,
+                          double* w, uint8_t* f, const uint8_t* kill, int recycle,
+                          int64_t* retired, int32_t* n_retired) {
+    int32_t killed = 0;
+    for (int32_t i = 0; i < cap; ++i) {
+        if (!(active[i] && kill[i])) continue;
+        if (recycle) retired[(*n_retired)++] = ids[i];
+        active[i] = 0;
+        ids[i] = 0;
+        ages[i] = 0;
+        e[i] = 0;
+        w[i] = 0.0;
+        f[i] = 0;
+        ++killed;
+    }
+    return killed;
+}
+
+/* lifecycle.cpp:144-195: pairs in ascending slot order (k-th free slot <-> k-th valid row) */
+int32_t orc_spawn_agents(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* types,
+                         int64_t* e, double* w, uint8_t* f, int64_t* next_id, int recycle,
+                         int64_t* retired, int32_t* n_retired, int32_t m, const int64_t* re,
+                         const double* rw, const uint8_t* rf, const uint8_t* valid, int set_type,
+                         int64_t agent_type, int32_t* slots, int32_t* rows, int32_t* dropped) {
+    int32_t q = 0, k = 0, j = 0;
+    for (int32_t r = 0; r < m; ++r) q += valid[r] != 0;
+    for (int32_t i = 0; i < cap; ++i) {
+        if (active[i]) continue;
+        while (j < m && !valid[j]) ++j;
+        if (j >= m) break;
+        slots[k] = i;
+        rows[k] = j;
+        e[i] = re[j];
+        w[i] = rw[j];
+        f[i] = rf[j];
+        active[i] = 1;
+        if (recycle && *n_retired > 0)
+            ids[i] = retired[--(*n_retired)];
+        else
+            ids[i] = (*next_id)++;
+        ages[i] = 0;
+        if (set_type) types[i] = agent_type;
+        ++k;
+        ++j;
+    }
+    *dropped = q - k;
+    return k;
+}
+
 /* kernels.cpp:52-73: std::stable_sort of the identity permutation by key; here a
  * bottom-up merge sort (also stable). */
 int orc_sort_perm(const double* key, const uint8_t* active, int32_t n, int descending,

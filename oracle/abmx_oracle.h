@@ -46,6 +46,23 @@ void orc_blend_u8(const uint8_t* mask, const uint8_t* a, const uint8_t* b, uint8
 int32_t orc_pair(const uint8_t* target, int32_t n, const uint8_t* valid, int32_t m,
                  int32_t* slots, int32_t* rows);
 
+/* remove_agents (lifecycle.cpp:124-142) on an e/w/f set: active &= !kill on live slots, killed
+ * slots reset to placeholders (agent_set.cpp:45-58: active, id, age and state zeroed, type
+ * kept). With recycle, killed ids are pushed on the retired stack in slot order. Returns the
+ * number killed. */
+int32_t orc_remove_agents(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* e,
+                          double* w, uint8_t* f, const uint8_t* kill, int recycle,
+                          int64_t* retired, int32_t* n_retired);
+
+/* spawn_agents (lifecycle.cpp:144-195) with the copy apply: the k-th free slot receives the
+ * k-th valid row; id = retired.pop() while the stack is non-empty (recycle), else next_id++;
+ * age 0; type = agent_type when set_type. Returns spawned; writes dropped, slots, rows. */
+int32_t orc_spawn_agents(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* types,
+                         int64_t* e, double* w, uint8_t* f, int64_t* next_id, int recycle,
+                         int64_t* retired, int32_t* n_retired, int32_t m, const int64_t* re,
+                         const double* rw, const uint8_t* rf, const uint8_t* valid, int set_type,
+                         int64_t agent_type, int32_t* slots, int32_t* rows, int32_t* dropped);
+
 /* Stable sort permutation by an f64 key (kernels.cpp:52-73). Returns 0, or 2 when an
  * active slot has a non-finite key (DomainError). */
 int orc_sort_perm(const double* key, const uint8_t* active, int32_t n, int descending,

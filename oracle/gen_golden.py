@@ -24,6 +24,12 @@ def b64(a):
     return base64.b64encode(np.ascontiguousarray(a).tobytes()).decode()
 
 
+def ewf_b64(st):
+    d = {k: b64(st[k]) for k, _ in pyoracle.EWF}
+    d.update(next_id=st["next_id"], retired=b64(st["retired"]), num_active=st["num_active"])
+    return d
+
+
 def c1(**kw):
     d = dict(width=100, height=100, n_sheep0=600, n_wolves0=400, sheep_capacity=1024,
              wolf_capacity=1024, energy_gain_sheep=4.0, energy_gain_wolf=20.0, metabolism=1.0,
@@ -159,6 +165,37 @@ def main():
             assert rc == 0
             out["sort_desc" if desc else "sort_asc"] = {"ids": b64(oi), "e": b64(oe)}
         sub.append({"cap": cap, "m": m, "inputs": {k: b64(v) for k, v in inst.items()}, "out": out})
+    # ---- lifecycle: remove_agents then spawn_agents, chained cycles, id recycling on/off
+    life = []
+    g = np.random.default_rng(4242)
+    for trial in range(40):
+        cap = int(g.integers(0, 80))
+        recycle = bool(trial % 2)
+        act = (g.random(cap) < g.random()).astype(np.uint8)
+        st = pyoracle.new_ewf_state(act, np.where(act, np.arange(cap), 0), g.integers(0, 9, cap) * act,
+                                    np.full(cap, 3), g.integers(-50, 50, cap) * act,
+                                    g.uniform(-4, 4, cap) * act, (g.random(cap) < 0.5) * act,
+                                    next_id=cap, recycle=recycle)
+        case = {"cap": cap, "recycle": recycle, "init": ewf_b64(st), "cycles": []}
+        for cyc in range(4):
+            kill = (g.random(cap) < g.random()).astype(np.uint8)
+            m = int(g.integers(0, 2 * cap + 2))
+            rows = {"e": g.integers(1000, 2000, m).astype(np.int64), "w": g.uniform(-9, 9, m),
+                    "f": (g.random(m) < 0.5).astype(np.uint8)}
+            valid = (g.random(m) < g.random()).astype(np.uint8)
+            set_type = bool(g.integers(0, 2))
+            atype = int(g.integers(-2, 5))
+            st, o = ref.lifecycle(st, kill, rows, valid, set_type, atype)
+            case["cycles"].append({
+                "kill": b64(kill), "m": m, "rows": {k: b64(v) for k, v in rows.items()},
+                "valid": b64(valid), "set_type": set_type, "agent_type": atype,
+                "out": ewf_b64(st), "killed": o["killed"], "spawned": o["spawned"],
+                "dropped": o["dropped"], "slots": b64(o["slots"]), "rows_used": b64(o["rows"])})
+        life.append(case)
+    json.dump({"source": "reference remove_agents + spawn_agents (lifecycle.cpp:124-195), copy apply, "
+                         "id recycling on odd cases", "cases": life},
+              open(os.path.join(OUT, "lifecycle.json"), "w"))
+
     json.dump({"source": "reference set_agents_rm/_sci, compact_mask, sort_agents with the e/w/f "
                          "copy-apply of tests/support/oracle.cpp", "cases": sub},
               open(os.path.join(OUT, "subset.json"), "w"))

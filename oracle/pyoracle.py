@@ -97,6 +97,29 @@ def state_arrays(sheep: dict, wolves: dict, world=None):
     return out
 
 
+EWF = (("active", np.uint8), ("ids", np.int64), ("ages", np.int64), ("types", np.int64),
+       ("e", np.int64), ("w", np.float64), ("f", np.uint8))
+
+
+def new_ewf_state(active, ids, ages, types, e, w, f, next_id, recycle=False, retired=()):
+    """An AgentSet with state columns e:i64, w:f64, f:bool (tests/support/oracle.cpp)."""
+    st = {k: np.array(v, dt) for (k, dt), v in zip(EWF, (active, ids, ages, types, e, w, f))}
+    st.update(next_id=int(next_id), recycle=bool(recycle), retired=np.array(retired, np.int64),
+              num_active=int(np.count_nonzero(st["active"])))
+    return st
+
+
+def copy_ewf(st):
+    return {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in st.items()}
+
+
+def _ewf_ptrs(st, with_types):
+    keys = ("active", "ids", "ages", "types", "e", "w", "f") if with_types else \
+        ("active", "ids", "ages", "e", "w", "f")
+    pt = {"active": u8p, "ids": i64p, "ages": i64p, "types": i64p, "e": i64p, "w": f64p, "f": u8p}
+    return [_p(st[k], pt[k]) for k in keys]
+
+
 class _Base:
     lib: C.CDLL
     prefix: str
@@ -136,6 +159,13 @@ class Oracle(_Base):
         L.orc_pair.argtypes = [u8p, C.c_int32, u8p, C.c_int32, i32p, i32p]
         L.orc_sort_perm.restype = C.c_int
         L.orc_sort_perm.argtypes = [f64p, u8p, C.c_int32, C.c_int, i32p]
+        L.orc_remove_agents.restype = C.c_int32
+        L.orc_remove_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, u8p, C.c_int,
+                                        i64p, i32p]
+        L.orc_spawn_agents.restype = C.c_int32
+        L.orc_spawn_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, i64p, f64p, u8p, i64p,
+                                       C.c_int, i64p, i32p, C.c_int32, i64p, f64p, u8p, u8p,
+                                       C.c_int, C.c_int64, i32p, i32p, i32p]
         L.orc_pred_create.restype = C.c_void_p
         L.orc_pred_create.argtypes = [C.POINTER(Cfg), C.c_uint64]
         L.orc_pred_free.argtypes = [C.c_void_p]
@@ -208,6 +238,36 @@ class Oracle(_Base):
         if rc:
             raise ValueError("non-finite sort key on an active slot")
         return p[:k.size].copy()
+
+    def lifecycle(self, st, kill, rows, valid, set_type=False, agent_type=0):
+        """remove_agents(kill) then spawn_agents(rows, copy apply) on an e/w/f set
+        (lifecycle.cpp:124-195). `st` is an ewf state dict (see new_ewf_state)."""
+        st = copy_ewf(st)
+        cap = st["active"].size
+        kill = np.ascontiguousarray(kill, np.uint8)
+        ret = np.zeros(cap + 1, np.int64)
+        ret[:st["retired"].size] = st["retired"]
+        nret = C.c_int32(st["retired"].size)
+        killed = self.lib.orc_remove_agents(cap, *_ewf_ptrs(st, False), _p(kill, u8p),
+                                            int(st["recycle"]), _p(ret, i64p), C.byref(nret))
+        m = valid.size
+        re, rw, rf = (np.ascontiguousarray(rows[k], dt) for k, dt in
+                      (("e", np.int64), ("w", np.float64), ("f", np.uint8)))
+        valid = np.ascontiguousarray(valid, np.uint8)
+        slots = np.empty(max(cap, 1), np.int32)
+        rws = np.empty(max(cap, 1), np.int32)
+        dropped = C.c_int32(0)
+        nid = C.c_int64(st["next_id"])
+        k = self.lib.orc_spawn_agents(cap, *_ewf_ptrs(st, True), C.byref(nid), int(st["recycle"]),
+                                      _p(ret, i64p), C.byref(nret), m, _p(re, i64p),
+                                      _p(rw, f64p), _p(rf, u8p), _p(valid, u8p), int(set_type),
+                                      agent_type, _p(slots, i32p), _p(rws, i32p),
+                                      C.byref(dropped))
+        st["next_id"] = nid.value
+        st["retired"] = ret[:nret.value].copy()
+        st["num_active"] = int(st["active"].sum())
+        return st, {"killed": int(killed), "spawned": int(k), "dropped": dropped.value,
+                    "slots": slots[:k].copy(), "rows": rws[:k].copy()}
 
     # predation
     def pred(self, cfg, seed):
@@ -324,6 +384,38 @@ class Reference(_Base):
         L.ref_sort_agents.restype = C.c_int
         L.ref_sort_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, f64p, C.c_int,
                                       u8p, i64p, i64p, i64p, f64p, u8p]
+        L.ref_lifecycle.restype = C.c_int32
+        L.ref_lifecycle.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, i64p, f64p, u8p, i64p, C.c_int,
+                                    i64p, i32p, u8p, C.c_int32, i64p, f64p, u8p, u8p, C.c_int,
+                                    C.c_int64, i32p, i32p, i32p, i32p]
+
+    def lifecycle(self, st, kill, rows, valid, set_type=False, agent_type=0):
+        """The reference's remove_agents then spawn_agents (same contract as Oracle.lifecycle)."""
+        st = copy_ewf(st)
+        cap = st["active"].size
+        kill = np.ascontiguousarray(kill, np.uint8)
+        ret = np.zeros(cap + 1, np.int64)
+        ret[:st["retired"].size] = st["retired"]
+        nret = C.c_int32(st["retired"].size)
+        re, rw, rf = (np.ascontiguousarray(rows[k], dt) for k, dt in
+                      (("e", np.int64), ("w", np.float64), ("f", np.uint8)))
+        valid = np.ascontiguousarray(valid, np.uint8)
+        slots = np.empty(max(cap, 1), np.int32)
+        rws = np.empty(max(cap, 1), np.int32)
+        dropped = C.c_int32(0)
+        na = C.c_int32(0)
+        nid = C.c_int64(st["next_id"])
+        killed = int(((st["active"] != 0) & (kill != 0)).sum())
+        k = self.lib.ref_lifecycle(cap, *_ewf_ptrs(st, True), C.byref(nid), int(st["recycle"]),
+                                   _p(ret, i64p), C.byref(nret), _p(kill, u8p), valid.size,
+                                   _p(re, i64p), _p(rw, f64p), _p(rf, u8p), _p(valid, u8p),
+                                   int(set_type), agent_type, _p(slots, i32p), _p(rws, i32p),
+                                   C.byref(dropped), C.byref(na))
+        st["next_id"] = nid.value
+        st["retired"] = ret[:nret.value].copy()
+        st["num_active"] = na.value
+        return st, {"killed": killed, "spawned": int(k), "dropped": dropped.value,
+                    "slots": slots[:k].copy(), "rows": rws[:k].copy()}
 
     def split(self, k, i): return self.lib.ref_rng_split(k, i)
     def draw(self, k, c): return self.lib.ref_rng_draw(k, c)

@@ -397,4 +397,36 @@ int32_t ref_remove_agents(int32_t cap, uint8_t* active, int64_t* ids, int64_t* a
     return out.num_active();
 }
 
+// One lifecycle cycle on the reference (lifecycle.cpp:124-195): remove_agents(kill) then
+// spawn_agents(rows, copy apply), with optional id recycling. The retired-id stack is passed
+// in and out so cycles chain. Returns spawned; writes dropped, slots, rows, num_active.
+int32_t ref_lifecycle(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* types,
+                      int64_t* e, double* w, uint8_t* f, int64_t* next_id, int recycle,
+                      int64_t* retired, int32_t* n_retired, const uint8_t* kill, int32_t m,
+                      const int64_t* re, const double* rw, const uint8_t* rf, const uint8_t* valid,
+                      int set_type, int64_t agent_type, int32_t* slots, int32_t* rows,
+                      int32_t* dropped, int32_t* num_active) {
+    AgentSet set = make_ewf_set(cap, active, ids, ages, e, w, f);
+    for (int32_t i = 0; i < cap; ++i) set.types_mut()[static_cast<size_t>(i)] = types[i];
+    set.set_next_id(*next_id);
+    set.set_id_recycling(recycle != 0);
+    set.retired_ids().assign(retired, retired + *n_retired);
+    AgentSet mid = remove_agents(set, std::span<const uint8_t>(kill, static_cast<size_t>(cap)));
+    const UpdateBatch b = make_ewf_batch(m, re, rw, rf, valid);
+    SpawnOutcome o = set_type ? spawn_agents(mid, b, ewf_copy(), agent_type)
+                              : spawn_agents(mid, b, ewf_copy());
+    export_ewf(o.set, active, ids, ages, e, w, f);
+    for (int32_t i = 0; i < cap; ++i) types[i] = o.set.types()[static_cast<size_t>(i)];
+    *next_id = o.set.next_id();
+    *n_retired = static_cast<int32_t>(o.set.retired_ids().size());
+    std::copy(o.set.retired_ids().begin(), o.set.retired_ids().end(), retired);
+    for (size_t k = 0; k < o.slots.size(); ++k) {
+        slots[k] = static_cast<int32_t>(o.slots[k]);
+        rows[k] = static_cast<int32_t>(o.rows[k]);
+    }
+    *dropped = static_cast<int32_t>(o.dropped);
+    *num_active = static_cast<int32_t>(o.set.num_active());
+    return static_cast<int32_t>(o.spawned);
+}
+
 }  // extern "C"

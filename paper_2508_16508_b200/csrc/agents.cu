@@ -1,0 +1,749 @@
+// agents.cu — device agent sets: the reference's generic lifecycle and subset operations on
+// HBM-resident columns.
+//
+//   remove_agents   lifecycle.cpp:124-142 + reset_slot agent_set.cpp:45-58
+//   spawn_agents    lifecycle.cpp:144-195 (rank-match of free slots and valid rows, fresh or
+//                   recycled ids, age 0, optional type), copy apply of the row columns
+//   set_agents_rm / set_agents_sci   kernels.cpp:116-153 with a column-copy apply: each pair
+//                   writes only its own slot from its own row, so RM and SCI coincide
+//   set_agents_mask kernels.cpp:155-167 (independent per-slot writes)
+//   select_agents   compact_mask kernels.cpp:23-35 (stable partition, trues first)
+//   sort_agents     kernels.cpp:52-73: stable LSD radix sort of order-preserving 64-bit keys,
+//                   then permute_agents (agent_set.cpp:92-108)
+//
+// Every pass is an HBM-streaming integer kernel: ticket-ordered single-pass selection with
+// decoupled lookback, then a gather/scatter over the selected pairs only. Counts stay in
+// device memory, so a whole remove -> spawn cycle is stream-ordered with no host round trip.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/abmx_cuda.h"
+#include "abmx_device.cuh"
+#include "abmx_internal.h"
+
+using namespace abmx_dev;
+
+namespace abmx_agents {
+
+constexpr int kT = 256;
+constexpr int kItems = 16;
+constexpr int kTile = kT * kItems;
+constexpr int kMaxCols = 12;  // columns per launch (more are processed in chunks)
+
+struct Cols {  // kernel-parameter column list: dst[c][slot] <- src[c][row]
+    void* dst[kMaxCols];
+    const void* src[kMaxCols];
+    int sz[kMaxCols];
+    int n;
+};
+
+struct ScanWs {
+    unsigned ticket;
+    unsigned pad;
+    unsigned long long status[1];  // [tiles]
+};
+
+__device__ __forceinline__ void copy_elem(void* dst, long long i, const void* src, long long j, int sz) {
+    if (sz == 8)
+        static_cast<unsigned long long*>(dst)[i] = static_cast<const unsigned long long*>(src)[j];
+    else if (sz == 4)
+        static_cast<unsigned*>(dst)[i] = static_cast<const unsigned*>(src)[j];
+    else
+        static_cast<uint8_t*>(dst)[i] = static_cast<const uint8_t*>(src)[j];
+}
+__device__ __forceinline__ void zero_elem(void* dst, long long i, int sz) {
+    if (sz == 8)
+        static_cast<unsigned long long*>(dst)[i] = 0ULL;
+    else if (sz == 4)
+        static_cast<unsigned*>(dst)[i] = 0u;
+    else
+        static_cast<uint8_t*>(dst)[i] = 0;
+}
+
+__device__ __forceinline__ void load16(const uint8_t* p, size_t base, size_t n, uint8_t (&b)[kItems]) {
+    if (p == nullptr) {
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) b[k] = 0;
+        return;
+    }
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0 && base + kItems <= n) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p + base);
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) b[k] = static_cast<uint8_t>(w[k >> 2] >> (8 * (k & 3)));
+    } else {
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) b[k] = base + k < n ? p[base + k] : 0;
+    }
+}
+
+enum SelMode { kSelMask = 0, kSelFree = 1, kSelKill = 2 };
+
+// list[k] = k-th selected index in ascending order; *count = number selected (last tile).
+//   kSelMask: mask[i] != 0      kSelFree: active[i] == 0      kSelKill: active[i] && mask[i]
+template <int kMode>
+__global__ void __launch_bounds__(kT) k_select(const uint8_t* __restrict__ mask, const uint8_t* __restrict__ active,
+                                               size_t n, int32_t* __restrict__ list, long long* __restrict__ count,
+                                               ScanWs* ws) {
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_look[kT / 32 + 2];
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const size_t base = static_cast<size_t>(tile) * kTile + static_cast<size_t>(threadIdx.x) * kItems;
+    uint8_t m[kItems], a[kItems];
+    load16(kMode == kSelFree ? nullptr : mask, base, n, m);
+    load16(kMode == kSelMask ? nullptr : active, base, n, a);
+    bool sel[kItems];
+    unsigned cnt = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const bool in = base + k < n;
+        sel[k] = in && (kMode == kSelMask ? m[k] != 0 : kMode == kSelFree ? a[k] == 0 : (a[k] != 0 && m[k] != 0));
+        cnt += sel[k];
+    }
+    unsigned long long total;
+    const unsigned long long excl = block_excl_scan<kT>(cnt, s_scan, &total);
+    __syncthreads();
+    const unsigned long long pre = block_lookback<kT>(ws->status, static_cast<int>(tile), total, s_look);
+    unsigned long long pos = pre + excl;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k)
+        if (sel[k]) list[pos++] = static_cast<int32_t>(base + k);
+    if (tile == gridDim.x - 1 && threadIdx.x == 0) *count = static_cast<long long>(pre + total);
+}
+
+struct Life {  // lifecycle fields of a set (agent_set.hpp:15-77)
+    uint8_t* active;
+    long long* ids;
+    long long* ages;
+    long long* types;
+    long long* counters;  // [3]: num_active, next_id, retired count
+    long long* retired;   // retired-id stack (recycle only)
+    int recycle;
+};
+
+// Pair k (k < min(*p, *q)): slot = slots[k] <- row = rows[k]. With `spawn` the slot also
+// becomes a fresh agent (lifecycle.cpp:170-185): active, id (recycled LIFO first), age 0, type.
+__global__ void __launch_bounds__(kT) k_pair_apply(const int32_t* __restrict__ slots, const int32_t* __restrict__ rows,
+                                                   const long long* p, const long long* q, Cols C, int spawn,
+                                                   Life L, int set_type, long long agent_type) {
+    const long long r = min(*p, *q);
+    long long top = 0, nid = 0;
+    if (spawn) {
+        nid = L.counters[1];
+        top = L.recycle ? L.counters[2] : 0;
+    }
+    for (long long k = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; k < r;
+         k += static_cast<long long>(gridDim.x) * kT) {
+        const int slot = slots[k], row = rows[k];
+        for (int c = 0; c < C.n; ++c)
+            if (C.src[c]) copy_elem(C.dst[c], slot, C.src[c], row, C.sz[c]);
+        if (spawn) {
+            L.active[slot] = 1;
+            L.ids[slot] = k < top ? L.retired[top - 1 - k] : nid + (k - top);
+            L.ages[slot] = 0;
+            if (set_type) L.types[slot] = agent_type;
+        }
+    }
+}
+
+// Counters after a spawn (lifecycle.cpp:186-194); out = {spawned, dropped}.
+__global__ void k_spawn_commit(const long long* p, const long long* q, Life L, long long* out) {
+    const long long r = min(*p, *q);
+    const long long top = L.recycle ? L.counters[2] : 0;
+    const long long used = min(top, r);
+    L.counters[0] += r;
+    L.counters[1] += r - used;
+    if (L.recycle) L.counters[2] = top - used;
+    if (out) {
+        out[0] = r;
+        out[1] = *q - r;
+    }
+}
+
+// {pairs, valid rows} of a set_agents_rm / _sci call
+__global__ void k_pair_result(const long long* p, const long long* q, long long* out) {
+    const long long r = min(*p, *q);
+    out[0] = r;
+    out[1] = *q;
+}
+
+// remove_agents: killed slot k of the slot-ordered kill list is reset; its id is pushed on
+// the retired stack at top + k (the reference pushes in ascending slot order).
+__global__ void __launch_bounds__(kT) k_remove_apply(const int32_t* __restrict__ list, const long long* count,
+                                                     Cols C, Life L) {
+    const long long nk = *count;
+    const long long top = L.recycle ? L.counters[2] : 0;
+    for (long long k = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; k < nk;
+         k += static_cast<long long>(gridDim.x) * kT) {
+        const int slot = list[k];
+        if (L.recycle) L.retired[top + k] = L.ids[slot];
+        L.active[slot] = 0;
+        L.ids[slot] = 0;
+        L.ages[slot] = 0;
+        for (int c = 0; c < C.n; ++c) zero_elem(C.dst[c], slot, C.sz[c]);
+    }
+}
+__global__ void k_remove_commit(const long long* count, Life L, long long* out) {
+    const long long nk = *count;
+    L.counters[0] -= nk;
+    if (L.recycle) L.counters[2] += nk;
+    if (out) *out = nk;
+}
+
+// set_agents_mask with per-slot source values: dst[c][i] <- src[c][i] where mask[i].
+__global__ void __launch_bounds__(kT) k_mask_apply(const uint8_t* __restrict__ mask, size_t n, Cols C) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT)
+        if (mask[i])
+            for (int c = 0; c < C.n; ++c)
+                if (C.src[c]) copy_elem(C.dst[c], i, C.src[c], i, C.sz[c]);
+}
+
+// gather: dst[c][i] <- src[c][perm[i]] (permute_agents, agent_set.cpp:92-108)
+__global__ void __launch_bounds__(kT) k_gather(const int32_t* __restrict__ perm, size_t n, Cols C) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT) {
+        const int j = perm[i];
+        for (int c = 0; c < C.n; ++c) copy_elem(C.dst[c], i, C.src[c], j, C.sz[c]);
+    }
+}
+__global__ void k_check_perm(const int32_t* __restrict__ perm, size_t n, unsigned* bad) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        if (perm[i] < 0 || static_cast<size_t>(perm[i]) >= n) atomicOr(bad, 1u);
+}
+
+// ------------------------------------------------------------------ stable radix sort
+// Order-preserving key: -0.0 folds onto +0.0 (they compare equal under `<`), negatives are
+// bit-inverted, positives get the sign bit; descending inverts the result, so equal keys keep
+// slot order either way (std::stable_sort). NaN keys (placeholders only: an active slot with
+// a non-finite key is rejected) sort beyond +/-inf by their sign bit.
+__global__ void __launch_bounds__(kT) k_sort_keys(const double* __restrict__ key, const uint8_t* __restrict__ active,
+                                                  size_t n, int descending, unsigned long long* __restrict__ keys,
+                                                  int32_t* __restrict__ vals, unsigned* bad) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT) {
+        double k = key[i];
+        if (active[i] && !isfinite(k)) atomicOr(bad, 1u);
+        if (k == 0.0) k = 0.0;
+        unsigned long long u = static_cast<unsigned long long>(__double_as_longlong(k));
+        u = (u >> 63) ? ~u : (u | (1ULL << 63));
+        keys[i] = descending ? ~u : u;
+        vals[i] = static_cast<int32_t>(i);
+    }
+}
+
+// per-tile digit histogram, digit-major: hist[d * tiles + tile]
+__global__ void __launch_bounds__(kT) k_hist(const unsigned long long* __restrict__ keys, size_t n, int shift,
+                                             unsigned* __restrict__ hist, int tiles) {
+    __shared__ unsigned h[256];
+    h[threadIdx.x] = 0;
+    __syncthreads();
+    const size_t base = static_cast<size_t>(blockIdx.x) * kTile;
+#pragma unroll 4
+    for (int j = 0; j < kItems; ++j) {
+        const size_t i = base + static_cast<size_t>(j) * kT + threadIdx.x;
+        if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255], 1u);
+    }
+    __syncthreads();
+    hist[static_cast<size_t>(threadIdx.x) * tiles + blockIdx.x] = h[threadIdx.x];
+}
+
+// one CTA per digit: exclusive scan of that digit's tile counts; total -> dtot[d]
+__global__ void __launch_bounds__(kT) k_digit_scan(unsigned* __restrict__ hist, int tiles, unsigned* __restrict__ dtot) {
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    unsigned* h = hist + static_cast<size_t>(blockIdx.x) * tiles;
+    unsigned long long carry = 0;
+    for (int t0 = 0; t0 < tiles; t0 += kT) {
+        const int t = t0 + threadIdx.x;
+        const unsigned v = t < tiles ? h[t] : 0u;
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan<kT>(v, s_scan, &tot);
+        if (t < tiles) h[t] = static_cast<unsigned>(carry + ex);
+        carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) dtot[blockIdx.x] = static_cast<unsigned>(carry);
+}
+
+// Stable scatter of one tile. Keys are visited in kItems rounds of kT consecutive keys
+// (round-major = index order); within a round, warps are ordered and lanes ranked by
+// __match_any_sync, so equal digits keep their input order.
+__global__ void __launch_bounds__(kT) k_scatter(const unsigned long long* __restrict__ kin, const int32_t* __restrict__ vin,
+                                                unsigned long long* __restrict__ kout, int32_t* __restrict__ vout,
+                                                size_t n, int shift, const unsigned* __restrict__ hist,
+                                                const unsigned* __restrict__ dtot, int tiles) {
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ unsigned s_base[256];
+    __shared__ unsigned s_w[kT / 32][256];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    {
+        unsigned long long tot;
+        const unsigned long long ex = block_excl_scan<kT>(dtot[tid], s_scan, &tot);
+        s_base[tid] = static_cast<unsigned>(ex) + hist[static_cast<size_t>(tid) * tiles + blockIdx.x];
+    }
+#pragma unroll
+    for (int w = 0; w < kT / 32; ++w) s_w[w][tid] = 0;
+    __syncthreads();
+    const size_t base = static_cast<size_t>(blockIdx.x) * kTile;
+    for (int j = 0; j < kItems; ++j) {
+        const size_t i = base + static_cast<size_t>(j) * kT + tid;
+        const bool ok = i < n;
+        unsigned long long key = 0;
+        int32_t val = 0;
+        if (ok) {
+            key = kin[i];
+            val = vin[i];
+        }
+        const unsigned d = ok ? static_cast<unsigned>((key >> shift) & 255) : 256u;
+        const unsigned peers = __match_any_sync(0xffffffffu, d);
+        const unsigned rank = __popc(peers & ((1u << lane) - 1u));
+        if (ok && rank == 0) s_w[warp][d] = __popc(peers);
+        __syncthreads();
+        unsigned run = 0;
+#pragma unroll
+        for (int w = 0; w < kT / 32; ++w) {
+            const unsigned c = s_w[w][tid];
+            s_w[w][tid] = run;
+            run += c;
+        }
+        __syncthreads();
+        if (ok) {
+            const unsigned pos = s_base[d] + s_w[warp][d] + rank;
+            kout[pos] = key;
+            vout[pos] = val;
+        }
+        __syncthreads();
+        s_base[tid] += run;
+#pragma unroll
+        for (int w = 0; w < kT / 32; ++w) s_w[w][tid] = 0;
+        __syncthreads();
+    }
+}
+
+}  // namespace abmx_agents
+
+// ====================================================================== host side
+using namespace abmx_agents;
+
+namespace {
+
+#define CKA(x)                                                                        \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            abmx_internal::set_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+            return ABMX_E_CUDA;                                                       \
+        }                                                                             \
+    } while (0)
+
+int grid_for(size_t n) {
+    const size_t g = (n + kT - 1) / kT;
+    const size_t cap = static_cast<size_t>(abmx_internal::num_sms()) * 8;
+    return static_cast<int>(g < cap ? (g > 0 ? g : 1) : cap);
+}
+
+bool elem_ok(int sz) { return sz == 1 || sz == 4 || sz == 8; }
+
+int check_set(const abmx_agent_set* s) {
+    if (!s) {
+        abmx_internal::set_error("null agent set");
+        return ABMX_E_ARG;
+    }
+    if (s->capacity < 0) {
+        abmx_internal::set_error("negative capacity");  // agent_set.cpp:27-28
+        return ABMX_E_CAPACITY;
+    }
+    if (s->capacity > 0 && (!s->active || !s->ids || !s->ages || !s->types || !s->counters)) {
+        abmx_internal::set_error("agent set is missing a lifecycle column");
+        return ABMX_E_SCHEMA;
+    }
+    if (s->recycle_ids && !s->retired) {
+        abmx_internal::set_error("recycle_ids needs a retired-id stack of capacity entries");
+        return ABMX_E_SCHEMA;
+    }
+    if (s->n_state < 0 || s->n_extra < 0 || (s->n_state && !s->state) || (s->n_extra && !s->extra)) {
+        abmx_internal::set_error("bad column list");
+        return ABMX_E_SCHEMA;
+    }
+    for (int c = 0; c < s->n_state; ++c)
+        if (!elem_ok(s->state[c].elem_size) || (s->capacity && !s->state[c].data)) {
+            abmx_internal::set_error("state columns need 1, 4 or 8 byte elements");
+            return ABMX_E_SCHEMA;
+        }
+    for (int c = 0; c < s->n_extra; ++c)
+        if (!elem_ok(s->extra[c].elem_size) || (s->capacity && !s->extra[c].data)) {
+            abmx_internal::set_error("extra columns need 1, 4 or 8 byte elements");
+            return ABMX_E_SCHEMA;
+        }
+    return ABMX_OK;
+}
+
+Life life_of(const abmx_agent_set* s) {
+    return Life{s->active, reinterpret_cast<long long*>(s->ids), reinterpret_cast<long long*>(s->ages),
+                reinterpret_cast<long long*>(s->types), reinterpret_cast<long long*>(s->counters),
+                reinterpret_cast<long long*>(s->retired), s->recycle_ids ? 1 : 0};
+}
+
+// Scratch for one call, stream-ordered (freed with cudaFreeAsync after the last use).
+struct Scratch {
+    cudaStream_t st;
+    std::vector<void*> ptrs;
+    explicit Scratch(cudaStream_t s) : st(s) {}
+    ~Scratch() {
+        for (void* p : ptrs) cudaFreeAsync(p, st);
+    }
+    cudaError_t get(void** p, size_t bytes) {
+        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+        if (e == cudaSuccess) ptrs.push_back(*p);
+        return e;
+    }
+};
+
+// slot-ordered selection list + device count
+template <int kMode>
+int select_list(const uint8_t* mask, const uint8_t* active, size_t n, int32_t* list, long long* count,
+                Scratch& sc) {
+    cudaStream_t st = sc.st;
+    if (n == 0) {
+        CKA(cudaMemsetAsync(count, 0, sizeof(long long), st));
+        return ABMX_OK;
+    }
+    const size_t tiles = (n + kTile - 1) / kTile;
+    void* ws = nullptr;
+    const size_t wsb = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
+    CKA(sc.get(&ws, wsb));
+    CKA(cudaMemsetAsync(ws, 0, wsb, st));
+    k_select<kMode><<<static_cast<unsigned>(tiles), kT, 0, st>>>(mask, active, n, list, count,
+                                                                 static_cast<ScanWs*>(ws));
+    abmx_internal::count_launch();
+    CKA(cudaGetLastError());
+    return ABMX_OK;
+}
+
+// launch `fn(Cols)` over column chunks of at most kMaxCols
+template <class F>
+int for_col_chunks(int ncols, F&& fn) {
+    for (int c0 = 0; c0 < ncols || (ncols == 0 && c0 == 0); c0 += kMaxCols) {
+        const int cn = ncols - c0 < kMaxCols ? ncols - c0 : kMaxCols;
+        int rc = fn(c0, cn > 0 ? cn : 0);
+        if (rc) return rc;
+        if (ncols == 0) break;
+    }
+    return ABMX_OK;
+}
+
+// shared pairing core of spawn / set_rm / set_sci
+int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int32_t m, const uint8_t* d_valid,
+              const abmx_column* rows, int set_type, int64_t agent_type, int32_t* d_slots, int32_t* d_rows,
+              int64_t* d_out, void* stream) {
+    int rc = check_set(s);
+    if (rc) return rc;
+    if (m < 0 || (m > 0 && !d_valid)) {
+        abmx_internal::set_error("bad update batch");
+        return ABMX_E_ARG;
+    }
+    if (!spawn && s->capacity > 0 && !d_target) {
+        abmx_internal::set_error("null target mask");
+        return ABMX_E_ARG;
+    }
+    for (int c = 0; c < s->n_state; ++c)
+        if (rows && rows[c].data && rows[c].elem_size != s->state[c].elem_size) {
+            abmx_internal::set_error("row column element size differs from its state column");
+            return ABMX_E_SCHEMA;
+        }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();
+    Scratch sc(st);
+    const size_t n = static_cast<size_t>(s->capacity);
+    int32_t* slots = d_slots;
+    int32_t* rws = d_rows;
+    long long* cnt = nullptr;  // [2]: p, q
+    CKA(sc.get(reinterpret_cast<void**>(&cnt), 2 * sizeof(long long)));
+    if (!slots) CKA(sc.get(reinterpret_cast<void**>(&slots), n * 4));
+    if (!rws) CKA(sc.get(reinterpret_cast<void**>(&rws), static_cast<size_t>(m) * 4));
+    if (spawn)
+        rc = select_list<kSelFree>(nullptr, s->active, n, slots, cnt, sc);
+    else
+        rc = select_list<kSelMask>(d_target, nullptr, n, slots, cnt, sc);
+    if (rc) return rc;
+    rc = select_list<kSelMask>(d_valid, nullptr, static_cast<size_t>(m), rws, cnt + 1, sc);
+    if (rc) return rc;
+    const Life L = life_of(s);
+    const size_t pairs_max = n < static_cast<size_t>(m) ? n : static_cast<size_t>(m);
+    rc = for_col_chunks(s->n_state, [&](int c0, int cn) {
+        Cols C{};
+        C.n = 0;
+        for (int c = 0; c < cn; ++c) {
+            if (!rows || !rows[c0 + c].data) continue;  // the apply leaves this column alone
+            C.dst[C.n] = s->state[c0 + c].data;
+            C.src[C.n] = rows[c0 + c].data;
+            C.sz[C.n] = s->state[c0 + c].elem_size;
+            ++C.n;
+        }
+        const int sp = spawn && c0 == 0;  // lifecycle fields once
+        if (C.n == 0 && !sp) return static_cast<int>(ABMX_OK);
+        k_pair_apply<<<grid_for(pairs_max), kT, 0, st>>>(slots, rws, cnt, cnt + 1, C, sp, L, set_type, agent_type);
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        return static_cast<int>(ABMX_OK);
+    });
+    if (rc) return rc;
+    if (spawn) {
+        k_spawn_commit<<<1, 1, 0, st>>>(cnt, cnt + 1, L, reinterpret_cast<long long*>(d_out));
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+    } else if (d_out) {
+        // {pairs, valid rows}
+        k_pair_result<<<1, 1, 0, st>>>(cnt, cnt + 1, reinterpret_cast<long long*>(d_out));
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+    }
+    return ABMX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* d_killed, void* stream) {
+    int rc = check_set(s);
+    if (rc) return rc;
+    if (s->capacity > 0 && !d_kill) {
+        abmx_internal::set_error("null kill mask");
+        return ABMX_E_ARG;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();
+    Scratch sc(st);
+    const size_t n = static_cast<size_t>(s->capacity);
+    int32_t* list = nullptr;
+    long long* cnt = nullptr;
+    CKA(sc.get(reinterpret_cast<void**>(&list), n * 4));
+    CKA(sc.get(reinterpret_cast<void**>(&cnt), sizeof(long long)));
+    rc = select_list<kSelKill>(d_kill, s->active, n, list, cnt, sc);
+    if (rc) return rc;
+    const Life L = life_of(s);
+    // lifecycle fields with the first chunk; the retired push reads ids before they are zeroed
+    rc = for_col_chunks(s->n_state, [&](int c0, int cn) {
+        Cols C{};
+        C.n = cn;
+        for (int c = 0; c < cn; ++c) {
+            C.dst[c] = s->state[c0 + c].data;
+            C.src[c] = nullptr;
+            C.sz[c] = s->state[c0 + c].elem_size;
+        }
+        if (c0 == 0) {
+            k_remove_apply<<<grid_for(n), kT, 0, st>>>(list, cnt, C, L);
+        } else {  // further chunks: state columns only (lifecycle fields already reset)
+            Life none = L;
+            none.recycle = 0;
+            // the lifecycle writes are idempotent, but active was already cleared: reuse the list
+            k_remove_apply<<<grid_for(n), kT, 0, st>>>(list, cnt, C, none);
+        }
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        return static_cast<int>(ABMX_OK);
+    });
+    if (rc) return rc;
+    k_remove_commit<<<1, 1, 0, st>>>(cnt, L, reinterpret_cast<long long*>(d_killed));
+    abmx_internal::count_launch();
+    CKA(cudaGetLastError());
+    return ABMX_OK;
+}
+
+int abmx_agents_spawn(const abmx_agent_set* s, int32_t m, const uint8_t* d_valid, const abmx_column* rows,
+                      int32_t set_type, int64_t agent_type, int32_t* d_slots, int32_t* d_rows, int64_t* d_result,
+                      void* stream) {
+    return pair_rows(s, nullptr, true, m, d_valid, rows, set_type, agent_type, d_slots, d_rows, d_result, stream);
+}
+
+int abmx_agents_set_rm(const abmx_agent_set* s, const uint8_t* d_target, int32_t m, const uint8_t* d_valid,
+                       const abmx_column* rows, int32_t* d_slots, int32_t* d_rows, int64_t* d_result,
+                       void* stream) {
+    return pair_rows(s, d_target, false, m, d_valid, rows, 0, 0, d_slots, d_rows, d_result, stream);
+}
+
+int abmx_agents_set_sci(const abmx_agent_set* s, const uint8_t* d_target, int32_t m, const uint8_t* d_valid,
+                        const abmx_column* rows, int32_t* d_slots, int32_t* d_rows, int64_t* d_result,
+                        void* stream) {
+    // the column-copy apply reads only its own slot and row: SCI == RM (kernels.hpp:96-99)
+    return pair_rows(s, d_target, false, m, d_valid, rows, 0, 0, d_slots, d_rows, d_result, stream);
+}
+
+int abmx_agents_set_mask(const abmx_agent_set* s, const uint8_t* d_mask, const abmx_column* values,
+                         void* stream) {
+    int rc = check_set(s);
+    if (rc) return rc;
+    if (s->capacity == 0) return ABMX_OK;
+    if (!d_mask || !values) {
+        abmx_internal::set_error("null mask or values");
+        return ABMX_E_ARG;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();
+    const size_t n = static_cast<size_t>(s->capacity);
+    return for_col_chunks(s->n_state, [&](int c0, int cn) {
+        Cols C{};
+        C.n = 0;
+        for (int c = 0; c < cn; ++c) {
+            if (!values[c0 + c].data) continue;
+            if (values[c0 + c].elem_size != s->state[c0 + c].elem_size) {
+                abmx_internal::set_error("value column element size differs from its state column");
+                return static_cast<int>(ABMX_E_SCHEMA);
+            }
+            C.dst[C.n] = s->state[c0 + c].data;
+            C.src[C.n] = values[c0 + c].data;
+            C.sz[C.n] = s->state[c0 + c].elem_size;
+            ++C.n;
+        }
+        if (C.n == 0) return static_cast<int>(ABMX_OK);
+        k_mask_apply<<<grid_for(n), kT, 0, st>>>(d_mask, n, C);
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        return static_cast<int>(ABMX_OK);
+    });
+}
+
+int abmx_agents_select(const uint8_t* d_mask, int32_t n, int32_t* d_indices, int64_t* d_count, void* stream) {
+    if (n < 0 || (n > 0 && (!d_mask || !d_indices)) || !d_count) {
+        abmx_internal::set_error("bad select arguments");
+        return ABMX_E_ARG;
+    }
+    (void)cudaGetLastError();
+    cudaError_t e = abmx_internal::launch_compact_indices(d_mask, d_indices, static_cast<size_t>(n),
+                                                          reinterpret_cast<unsigned long long*>(d_count),
+                                                          static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) {
+        abmx_internal::set_error(std::string("select: ") + cudaGetErrorString(e));
+        return ABMX_E_CUDA;
+    }
+    return ABMX_OK;
+}
+
+int abmx_agents_sort_perm(const double* d_key, const uint8_t* d_active, int32_t n, int32_t descending,
+                          int32_t* d_perm, void* stream) {
+    if (n < 0 || (n > 0 && (!d_key || !d_active || !d_perm))) {
+        abmx_internal::set_error("bad sort arguments");
+        return ABMX_E_ARG;
+    }
+    if (n == 0) return ABMX_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();
+    Scratch sc(st);
+    const size_t N = static_cast<size_t>(n);
+    const int tiles = static_cast<int>((N + kTile - 1) / kTile);
+    unsigned long long *k0, *k1;
+    int32_t* v1;
+    unsigned *hist, *dtot, *bad;
+    CKA(sc.get(reinterpret_cast<void**>(&k0), N * 8));
+    CKA(sc.get(reinterpret_cast<void**>(&k1), N * 8));
+    CKA(sc.get(reinterpret_cast<void**>(&v1), N * 4));
+    CKA(sc.get(reinterpret_cast<void**>(&hist), static_cast<size_t>(tiles) * 256 * 4));
+    CKA(sc.get(reinterpret_cast<void**>(&dtot), 256 * 4 + 16));
+    bad = dtot + 256;
+    CKA(cudaMemsetAsync(bad, 0, 4, st));
+    k_sort_keys<<<grid_for(N), kT, 0, st>>>(d_key, d_active, N, descending ? 1 : 0, k0, d_perm, bad);
+    abmx_internal::count_launch();
+    CKA(cudaGetLastError());
+    unsigned h_bad = 0;
+    CKA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+    CKA(cudaStreamSynchronize(st));
+    if (h_bad) {
+        abmx_internal::set_error("non-finite sort key on an active slot");  // kernels.cpp:57-60
+        return ABMX_E_DOMAIN;
+    }
+    // 8 passes of 8 bits; after an even number of passes the result is back in (k0, d_perm)
+    unsigned long long* kin = k0;
+    unsigned long long* kout = k1;
+    int32_t* vin = d_perm;
+    int32_t* vout = v1;
+    for (int shift = 0; shift < 64; shift += 8) {
+        k_hist<<<tiles, kT, 0, st>>>(kin, N, shift, hist, tiles);
+        k_digit_scan<<<256, kT, 0, st>>>(hist, tiles, dtot);
+        k_scatter<<<tiles, kT, 0, st>>>(kin, vin, kout, vout, N, shift, hist, dtot, tiles);
+        abmx_internal::count_launch(3);
+        CKA(cudaGetLastError());
+        unsigned long long* tk = kin;
+        kin = kout;
+        kout = tk;
+        int32_t* tv = vin;
+        vin = vout;
+        vout = tv;
+    }
+    return ABMX_OK;
+}
+
+int abmx_agents_permute(const abmx_agent_set* s, const int32_t* d_perm, void* stream) {
+    int rc = check_set(s);
+    if (rc) return rc;
+    const size_t n = static_cast<size_t>(s->capacity);
+    if (n == 0) return ABMX_OK;
+    if (!d_perm) {
+        abmx_internal::set_error("null permutation");
+        return ABMX_E_ARG;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();
+    Scratch sc(st);
+    unsigned* bad = nullptr;
+    CKA(sc.get(reinterpret_cast<void**>(&bad), 4));
+    CKA(cudaMemsetAsync(bad, 0, 4, st));
+    k_check_perm<<<grid_for(n), kT, 0, st>>>(d_perm, n, bad);
+    abmx_internal::count_launch();
+    unsigned h_bad = 0;
+    CKA(cudaMemcpyAsync(&h_bad, bad, 4, cudaMemcpyDeviceToHost, st));
+    CKA(cudaStreamSynchronize(st));
+    if (h_bad) {
+        abmx_internal::set_error("permutation index outside [0, capacity)");
+        return ABMX_E_DOMAIN;
+    }
+    // every column: gather into scratch, copy back (out-of-place gather, in-place result)
+    std::vector<abmx_column> cols;
+    cols.push_back({s->active, 1, 0});
+    cols.push_back({s->ids, 8, 0});
+    cols.push_back({s->types, 8, 0});
+    cols.push_back({s->ages, 8, 0});
+    for (int c = 0; c < s->n_state; ++c) cols.push_back(s->state[c]);
+    for (int c = 0; c < s->n_extra; ++c) cols.push_back(s->extra[c]);
+    std::vector<void*> tmp(cols.size());
+    for (size_t c = 0; c < cols.size(); ++c) CKA(sc.get(&tmp[c], n * static_cast<size_t>(cols[c].elem_size)));
+    rc = for_col_chunks(static_cast<int>(cols.size()), [&](int c0, int cn) {
+        Cols C{};
+        C.n = cn;
+        for (int c = 0; c < cn; ++c) {
+            C.dst[c] = tmp[c0 + c];
+            C.src[c] = cols[c0 + c].data;
+            C.sz[c] = cols[c0 + c].elem_size;
+        }
+        k_gather<<<grid_for(n), kT, 0, st>>>(d_perm, n, C);
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        return static_cast<int>(ABMX_OK);
+    });
+    if (rc) return rc;
+    for (size_t c = 0; c < cols.size(); ++c)
+        CKA(cudaMemcpyAsync(cols[c].data, tmp[c], n * static_cast<size_t>(cols[c].elem_size),
+                            cudaMemcpyDeviceToDevice, st));
+    return ABMX_OK;
+}
+
+int abmx_agents_sort(const abmx_agent_set* s, const double* d_key, int32_t descending, int32_t* d_perm,
+                     void* stream) {
+    int rc = check_set(s);
+    if (rc) return rc;
+    const size_t n = static_cast<size_t>(s->capacity);
+    if (n == 0) return ABMX_OK;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch sc(st);
+    int32_t* perm = d_perm;
+    if (!perm) CKA(sc.get(reinterpret_cast<void**>(&perm), n * 4));
+    rc = abmx_agents_sort_perm(d_key, s->active, s->capacity, descending, perm, stream);
+    if (rc) return rc;
+    return abmx_agents_permute(s, perm, stream);
+}
+
+}  // extern "C"

@@ -47,3 +47,39 @@ def state_hash(model, replica=0):
     s = model.export_species(0, replica)
     w = model.export_species(1, replica)
     return pyoracle.fnv1a(pyoracle.state_arrays(s, w, model.export_world(replica)))
+
+
+# ---------------------------------------------------------------- e/w/f agent sets (golden)
+def b64arr(s, dt):
+    import base64
+    return np.frombuffer(base64.b64decode(s), dtype=dt).copy()
+
+
+def ewf_decode(d, recycle):
+    """An ewf state dict (pyoracle.new_ewf_state layout) from its golden encoding."""
+    st = {k: b64arr(d[k], dt) for k, dt in pyoracle.EWF}
+    st.update(next_id=d["next_id"], recycle=recycle, retired=b64arr(d["retired"], np.int64),
+              num_active=d["num_active"])
+    return st
+
+
+def ewf_equal(a, b, what=""):
+    for k, _ in pyoracle.EWF:
+        x, y = np.asarray(a[k]), np.asarray(b[k])
+        if k == "w":
+            x, y = x.view(np.uint64), y.view(np.uint64)
+        assert np.array_equal(x, y), (what, k, x, y)
+    assert a["next_id"] == b["next_id"], (what, "next_id")
+    assert np.array_equal(a["retired"], b["retired"]), (what, "retired")
+    assert a["num_active"] == b["num_active"], (what, "num_active")
+
+
+def lifecycle_cycles(case):
+    """Yield (kill, rows, valid, set_type, agent_type, expected_state, expected_outcome)."""
+    for c in case["cycles"]:
+        rows = {"e": b64arr(c["rows"]["e"], np.int64), "w": b64arr(c["rows"]["w"], np.float64),
+                "f": b64arr(c["rows"]["f"], np.uint8)}
+        out = {"killed": c["killed"], "spawned": c["spawned"], "dropped": c["dropped"],
+               "slots": b64arr(c["slots"], np.int32), "rows": b64arr(c["rows_used"], np.int32)}
+        yield (b64arr(c["kill"], np.uint8), rows, b64arr(c["valid"], np.uint8), c["set_type"],
+               c["agent_type"], ewf_decode(c["out"], case["recycle"]), out)

@@ -154,3 +154,19 @@ def test_oracle_equals_live_reference(oracle, reference):
         for t in range(1, 31):
             assert a.step(t) == b.step(t)
             assert a.hash(True) == b.hash(True), (seed, t)
+
+
+def test_lifecycle_golden(oracle):
+    """remove_agents + spawn_agents chained over 4 cycles, with and without id recycling
+    (lifecycle.cpp:124-195): the C restatement reproduces the reference bit for bit."""
+    from helpers import ewf_decode, ewf_equal, lifecycle_cycles
+    cases = load("lifecycle.json")["cases"]
+    assert any(c["recycle"] for c in cases) and not all(c["recycle"] for c in cases)
+    for i, case in enumerate(cases):
+        st = ewf_decode(case["init"], case["recycle"])
+        for j, (kill, rows, valid, st_t, at, want, wo) in enumerate(lifecycle_cycles(case)):
+            st, o = oracle.lifecycle(st, kill, rows, valid, st_t, at)
+            ewf_equal(st, want, (i, j))
+            for k in ("killed", "spawned", "dropped"):
+                assert o[k] == wo[k], (i, j, k)
+            assert np.array_equal(o["slots"], wo["slots"]) and np.array_equal(o["rows"], wo["rows"])

@@ -28,4 +28,6 @@ ms, met = m.bench(a.warmup + 1, a.steps, a.flush, per_kernel=not a.graph)
 
 if not a.graph:
     print("kernel ms", {k: round(v[0] / max(v[1], 1) * 1000, 2) for k, v in m.kernel_times().items()})
+import statistics  # noqa: E402
+print("step ms median", round(statistics.median(ms), 5), "min", round(min(ms), 5))
 print("steps ms", [round(x, 4) for x in ms], "metrics", met[0, -1].tolist())
