@@ -239,10 +239,47 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
         loadk_u8(P.active[s] + base, act);
     }
 
+    if (kMove) {  // zero the group counters this step's k_update accumulates into
+        unsigned long long* gz = P.group + static_cast<size_t>(epoch & 1) * 2 * P.R * P.groups;
+        for (unsigned q = b * kT + threadIdx.x; q < 2u * P.R * P.groups; q += nb * kT) gz[q] = 0ULL;
+    }
+
     // ---------------- (a) births of step P.birth_epoch (rank-match, lifecycle.cpp:144-195)
     bool born[kS] = {};
     bool born_any = false;
+    bool full = false;
     if (P.pending) {
+        // Births fill the LOWEST free slots, so only the first tiles holding free slots receive
+        // any. The 32-tile group totals bound the free slots before this tile from below: if
+        // that bound already covers every pair (and no row is dropped), skip the full scan.
+        __shared__ unsigned long long s_gt[2];
+        if (threadIdx.x < 32) {
+            const unsigned long long* gp =
+                P.group + (static_cast<size_t>(P.birth_epoch & 1) * 2 * P.R + static_cast<size_t>(s) * P.R + r) * P.groups;
+            const int gme = tile / kGroup;
+            unsigned long long tot = 0, bef = 0;
+            for (int g = threadIdx.x; g < P.groups; g += 32) {
+                const unsigned long long v = gp[g];
+                tot += v;
+                if (g < gme) bef += v;
+            }
+            tot = warp_sum(tot);
+            bef = warp_sum(bef);
+            if (threadIdx.x == 0) {
+                s_gt[0] = tot;
+                s_gt[1] = bef;
+            }
+        }
+        __syncthreads();
+        const unsigned F = hi31(s_gt[0]), Q = lo31(s_gt[0]);
+        const unsigned pairs = F < Q ? F : Q;
+        full = tile == 0 || Q > F || hi31(s_gt[1]) < pairs;
+    }
+#ifdef ABMX_EXP_NO_BIRTHS  // timing ablation only (results are wrong)
+    if (false) {
+#else
+    if (full) {
+#endif
         const int tiles = P.tiles[s];
         const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
         unsigned long long carry = 0;  // exclusive prefix of the tile counts -> s_pre
@@ -585,7 +622,11 @@ __device__ void update_phase(const Params& P, unsigned b) {
                         ++n_graze;
                     }
             }
+#ifdef ABMX_EXP_NO_PAIR  // timing ablation only
+            if (false) {
+#else
             if (!P.crowded) {
+#endif
                 // predation (predation.cpp:197-239): in a cell holding wolves and sheep the k-th
                 // wolf by slot takes the k-th sheep by slot; each agent finds its own rank with
                 // a walk over the cell's (short) lists
@@ -701,6 +742,10 @@ __device__ void update_phase(const Params& P, unsigned b) {
         const unsigned long long g_sum = c >> 42, m_sum = (c >> 21) & 0x1FFFFF, d_sum = c & 0x1FFFFF;
         Events* ev = P.ev + static_cast<size_t>(p) * P.R + r;
         P.status[(static_cast<size_t>(s) * P.R + r) * P.status_stride + tile] = tile_total;
+        if (tile_total)  // packed (free, valid): both fields add without carry (each < 2^31)
+            atomicAdd(&P.group[(static_cast<size_t>(p) * 2 * P.R + static_cast<size_t>(s) * P.R + r) * P.groups +
+                               tile / kGroup],
+                      tile_total);
         if (g_sum) {
             atomicAdd(&ev->grass_eaten, g_sum);
             if (P.delay >= 1)  // every cell grazed this step comes due at the same epoch
@@ -945,6 +990,8 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     AL(P.due_count, sizeof(unsigned) * P.due_ring * R);
     AL(P.cw, static_cast<size_t>(R) * P.Cpad * 16);
     AL(P.status, static_cast<size_t>(2) * R * P.status_stride * 8);
+    P.groups = (P.status_stride + kGroup - 1) / kGroup;
+    AL(P.group, static_cast<size_t>(2) * 2 * R * P.groups * 8);
     P.pool_size = static_cast<long long>(R) * (P.Npad[0] + P.Npad[1]);
     AL(P.pool, static_cast<size_t>(P.pool_size) * 4);
     AL(P.ctl, sizeof(Ctl));
@@ -958,6 +1005,7 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     for (int s = 0; s < 2; ++s) CK(cudaMemsetAsync(P.next[s], 0xFF, static_cast<size_t>(R) * P.Npad[s] * 4, stream));
     CK(cudaMemsetAsync(P.due_count, 0, sizeof(unsigned) * P.due_ring * R, stream));
     CK(cudaMemsetAsync(P.status, 0, static_cast<size_t>(2) * R * P.status_stride * 8, stream));
+    CK(cudaMemsetAsync(P.group, 0, static_cast<size_t>(2) * 2 * R * P.groups * 8, stream));
     CK(cudaMemsetAsync(P.ev, 0, sizeof(Events) * 2 * R, stream));
     CK(cudaMemsetAsync(P.ctl, 0, sizeof(Ctl), stream));
     {

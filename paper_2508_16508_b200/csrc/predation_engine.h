@@ -26,6 +26,7 @@ constexpr int kS = ABMX_PRED_KS;      // slots per thread (2, 4 or 8)
 constexpr int kMinB = ABMX_PRED_MINB; // CTAs per SM the hot kernels are register-limited to
 constexpr int kTile = kT * kS;   // slots per tile (k_move and k_update use the same tiling)
 constexpr int kNumKernels = 3;   // k_move, k_cells (crowded grids only), k_update
+constexpr int kGroup = 32;       // tiles per group counter (births fast path in k_move)
 constexpr int kEpochClear = 128; // cell tags are cleared every kEpochClear steps (epoch8 period 255)
 
 // Device control block (counters shared by the kernels of a step).
@@ -88,6 +89,8 @@ struct Params {
     long long* n_grass;      // [R] ready cells after the last step
     unsigned* due_count;     // [R][due_ring] cells coming due at each epoch (mod ring)
     unsigned long long* status;  // [species][R][status_stride] packed (free, valid) per tile
+    unsigned long long* group;   // [parity][species][R][groups] packed (free, valid) per kGroup tiles
+    int groups;
     unsigned long long* occ;     // crowded grids: wolf cells (replica << 32 | cell)
     int* pool;
     long long pool_size;
