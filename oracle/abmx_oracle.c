@@ -504,5 +504,226 @@ int orc_run_batch(const orc_pred_config* cfg, uint64_t master, int32_t replicas,
     return 0;
 }
 
+
+/* ------------------------------------------------------------------ traffic */
+/* rng.hpp:33-35 stream tags */
+enum { ORC_TRAFFIC_SIGNAL = 5, ORC_TRAFFIC_PROPOSE = 6, ORC_TRAFFIC_SPAWN = 7 };
+
+orc_traffic* orc_traffic_create(const orc_traffic_config* cfg, uint64_t seed) {
+    if (cfg->period < 1 || cfg->length < 1) return NULL;
+    orc_traffic* m = (orc_traffic*)calloc(1, sizeof(orc_traffic));
+    m->length = cfg->length;
+    m->period = cfg->period;
+    /* SignalSchedule::from_config (traffic.cpp:8-17) */
+    long long gl = llround((double)cfg->period * cfg->green_fraction);
+    m->green_len = gl < 0 ? 0 : (gl > cfg->period ? cfg->period : gl);
+    m->phase = orc_uniform_int(orc_split(seed, ORC_TRAFFIC_SIGNAL), 0, 0, cfg->period);
+    m->seed = seed;
+    /* Road::empty (traffic.cpp:19-29): capacity 3*length, lane/cell int columns */
+    const size_t n = (size_t)(3 * cfg->length);
+    m->capacity = (int32_t)n;
+    m->active = (uint8_t*)calloc(n, 1);
+    m->ids = (int64_t*)calloc(n, 8);
+    m->ages = (int64_t*)calloc(n, 8);
+    m->lane = (int64_t*)calloc(n, 8);
+    m->cell = (int64_t*)calloc(n, 8);
+    m->occupancy = (int32_t*)malloc(n * 4);
+    for (size_t i = 0; i < n; ++i) m->occupancy[i] = -1;
+    return m;
+}
+
+void orc_traffic_free(orc_traffic* m) {
+    if (!m) return;
+    free(m->active);
+    free(m->ids);
+    free(m->ages);
+    free(m->lane);
+    free(m->cell);
+    free(m->occupancy);
+    free(m);
+}
+
+int orc_traffic_rebuild(orc_traffic* m) {
+    const int32_t n = m->capacity;
+    for (int32_t c = 0; c < n; ++c) m->occupancy[c] = -1;
+    for (int32_t i = 0; i < n; ++i) {
+        if (!m->active[i]) continue;
+        const int64_t c = m->lane[i] * m->length + m->cell[i];
+        if (m->occupancy[c] != -1) return 1;
+        m->occupancy[c] = i;
+    }
+    return 0;
+}
+
+void orc_traffic_propose(const orc_traffic* m, uint64_t stream, int green, uint8_t* kind,
+                         int64_t* to_lane, int64_t* to_cell) {
+    for (int32_t i = 0; i < m->capacity; ++i) {
+        kind[i] = 0;
+        to_lane[i] = 0;
+        to_cell[i] = 0;
+        if (!m->active[i]) continue;
+        const int64_t lane = m->lane[i], cell = m->cell[i];
+        if (cell == m->length - 1) { /* exit column: no draw */
+            kind[i] = green ? 2 : 0;
+            continue;
+        }
+        int64_t opt[3];
+        int n = 0;
+        opt[n++] = lane; /* forward, forward-left, forward-right */
+        if (lane > 0) opt[n++] = lane - 1;
+        if (lane < 2) opt[n++] = lane + 1;
+        const int64_t pick = orc_uniform_int(stream, (uint64_t)i, 0, n);
+        kind[i] = 1;
+        to_lane[i] = opt[pick];
+        to_cell[i] = cell + 1;
+    }
+}
+
+int orc_traffic_resolve(const orc_traffic* m, const uint8_t* kind, const int64_t* to_lane,
+                        const int64_t* to_cell, uint8_t* accepted) {
+    const int32_t n = m->capacity;
+    const size_t cells = (size_t)n;
+    int32_t* winner = (int32_t*)malloc(cells * 4);
+    int* prio_of = (int*)malloc(cells * sizeof(int));
+    for (size_t c = 0; c < cells; ++c) {
+        winner[c] = -1;
+        prio_of[c] = 99;
+    }
+    int rc = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        accepted[i] = 0;
+    }
+    for (int32_t i = 0; i < n && !rc; ++i) {
+        if (!m->active[i]) continue;
+        if (kind[i] == 2) {
+            accepted[i] = 1; /* exit pseudo-cell: no capacity limit */
+        } else if (kind[i] == 1) {
+            const int64_t tl = to_lane[i], tc = to_cell[i];
+            if (tl < 0 || tl >= 3 || tc < 0 || tc >= m->length) {
+                rc = 2; /* ContractError */
+                break;
+            }
+            const size_t target = (size_t)(tl * m->length + tc);
+            const int prio = m->lane[i] == tl ? 0 : (m->lane[i] == tl - 1 ? 1 : 2);
+            if (prio < prio_of[target]) {
+                prio_of[target] = prio;
+                winner[target] = i;
+            }
+        }
+    }
+    /* fixed point, in the reference's round / cell order (traffic.cpp:124-138) */
+    for (int64_t round = 0; round < m->length && !rc; ++round) {
+        int changed = 0;
+        for (size_t c = 0; c < cells; ++c) {
+            const int32_t w = winner[c];
+            if (w < 0 || accepted[w]) continue;
+            const int32_t occ = m->occupancy[c];
+            if (occ < 0 || accepted[occ]) {
+                accepted[w] = 1;
+                changed = 1;
+            }
+        }
+        if (!changed) break;
+    }
+    free(winner);
+    free(prio_of);
+    return rc;
+}
+
+/* spawn_cars (traffic.cpp:143-184) + spawn_agents' pairing (lifecycle.cpp:144-195) */
+static int64_t orc_traffic_spawn(orc_traffic* m, uint64_t stream) {
+    const int64_t k = orc_uniform_int(stream, 0, 0, 4);
+    int64_t lanes[3] = {0, 1, 2};
+    for (int64_t i = 0; i < (k < 2 ? k : 2); ++i) {
+        const int64_t j = i + orc_uniform_int(stream, (uint64_t)(1 + i), 0, 3 - i);
+        const int64_t tmp = lanes[i];
+        lanes[i] = lanes[j];
+        lanes[j] = tmp;
+    }
+    int64_t row_lane[3];
+    int valid[3] = {0, 0, 0};
+    for (int64_t r = 0; r < (k < 3 ? k : 3); ++r) {
+        if (m->occupancy[lanes[r] * m->length] != -1) continue; /* occupied entry */
+        row_lane[r] = lanes[r];
+        valid[r] = 1;
+    }
+    int64_t spawned = 0;
+    int r = 0;
+    for (int32_t i = 0; i < m->capacity; ++i) {
+        if (m->active[i]) continue;
+        while (r < 3 && !valid[r]) ++r;
+        if (r >= 3) break;
+        m->active[i] = 1;
+        m->lane[i] = row_lane[r];
+        m->cell[i] = 0;
+        m->ids[i] = m->next_id++;
+        m->ages[i] = 0;
+        ++spawned;
+        ++r;
+    }
+    m->num_active += (int32_t)spawned;
+    orc_traffic_rebuild(m);
+    return spawned;
+}
+
+void orc_traffic_step(orc_traffic* m, int64_t t) {
+    const int green = (((t + m->phase) % m->period + m->period) % m->period) < m->green_len;
+    const size_t n = (size_t)m->capacity;
+    uint8_t* kind = (uint8_t*)malloc(n);
+    int64_t* tl = (int64_t*)malloc(n * 8);
+    int64_t* tc = (int64_t*)malloc(n * 8);
+    uint8_t* acc = (uint8_t*)malloc(n);
+    orc_traffic_propose(m, orc_split(orc_split(m->seed, ORC_TRAFFIC_PROPOSE), (uint64_t)t), green,
+                        kind, tl, tc);
+    orc_traffic_resolve(m, kind, tl, tc, acc);
+    int64_t exited = 0;
+    for (size_t i = 0; i < n; ++i) {
+        if (!acc[i]) continue;
+        if (kind[i] == 1) { /* set_agents_mask: lane / cell <- target */
+            m->lane[i] = tl[i];
+            m->cell[i] = tc[i];
+        } else if (kind[i] == 2 && m->active[i]) { /* remove_agents -> reset_slot */
+            m->active[i] = 0;
+            m->ids[i] = 0;
+            m->ages[i] = 0;
+            m->lane[i] = 0;
+            m->cell[i] = 0;
+            ++exited;
+        }
+    }
+    m->num_active -= (int32_t)exited;
+    orc_traffic_rebuild(m);
+    m->spawned = orc_traffic_spawn(m, orc_split(orc_split(m->seed, ORC_TRAFFIC_SPAWN), (uint64_t)t));
+    m->exited = exited;
+    m->green = green;
+    m->spawned_total += m->spawned;
+    m->exited_total += exited;
+    free(kind);
+    free(tl);
+    free(tc);
+    free(acc);
+}
+
+void orc_traffic_metrics(const orc_traffic* m, double* out4) {
+    out4[0] = (double)m->num_active;
+    out4[1] = (double)m->spawned;
+    out4[2] = (double)m->exited;
+    out4[3] = m->green ? 1.0 : 0.0;
+}
+
+int orc_traffic_run_batch(const orc_traffic_config* cfg, uint64_t master, int32_t replicas,
+                          int64_t steps, double* out) {
+    for (int32_t r = 0; r < replicas; ++r) {
+        orc_traffic* m = orc_traffic_create(cfg, orc_replica_seed(master, r));
+        if (!m) return 1;
+        for (int64_t t = 1; t <= steps; ++t) {
+            orc_traffic_step(m, t);
+            orc_traffic_metrics(m, out + ((size_t)r * (size_t)steps + (size_t)(t - 1)) * 4);
+        }
+        orc_traffic_free(m);
+    }
+    return 0;
+}
+
 /* FNV-1a-64 helper for state hashes (test bookkeeping, not a reference algorithm) */
 uint64_t orc_fnv1a(uint64_t h, const void* data, size_t n) { return fnv(h, data, n); }

@@ -117,6 +117,43 @@ int64_t* orc_pred_regrow(orc_pred* p);
 int orc_run_batch(const orc_pred_config* cfg, uint64_t master, int32_t replicas, int64_t steps,
                   double* metrics_out);
 
+/* ---- traffic (include/abmx/models/traffic.hpp, src/models/traffic.cpp) ---- */
+typedef struct {
+    int64_t length, period;
+    double green_fraction;
+} orc_traffic_config;
+
+typedef struct {
+    int64_t length, period, green_len, phase;
+    uint64_t seed;
+    int32_t capacity, num_active;
+    int64_t next_id;
+    uint8_t* active;
+    int64_t *ids, *ages, *lane, *cell;
+    int32_t* occupancy;                 /* [3*length]: slot or -1 */
+    int64_t spawned, exited, green;     /* last step (RoadStepStats) */
+    int64_t spawned_total, exited_total;
+} orc_traffic;
+
+/* NULL on DomainError (length < 1 or period < 1, traffic.cpp:8-9,20-21) */
+orc_traffic* orc_traffic_create(const orc_traffic_config* cfg, uint64_t seed);
+void orc_traffic_free(orc_traffic* m);
+/* rebuild occupancy from the car columns; 1 if two cars share a cell (traffic.cpp:31-44) */
+int orc_traffic_rebuild(orc_traffic* m);
+/* propose_moves (traffic.cpp:47-80): kind 0 stay / 1 move / 2 exit */
+void orc_traffic_propose(const orc_traffic* m, uint64_t stream, int green, uint8_t* kind,
+                         int64_t* to_lane, int64_t* to_cell);
+/* resolve_conflicts (traffic.cpp:82-140); returns 2 on a proposal outside the road */
+int orc_traffic_resolve(const orc_traffic* m, const uint8_t* kind, const int64_t* to_lane,
+                        const int64_t* to_cell, uint8_t* accepted);
+/* step_road (traffic.cpp:186-222) + model totals (traffic.cpp:228-232) */
+void orc_traffic_step(orc_traffic* m, int64_t t);
+/* collect_metrics (traffic.cpp:234-238): n_cars, spawned, exited, signal_green */
+void orc_traffic_metrics(const orc_traffic* m, double* out4);
+/* run_batch of TrafficModel: metrics [K][T][4] */
+int orc_traffic_run_batch(const orc_traffic_config* cfg, uint64_t master, int32_t replicas,
+                          int64_t steps, double* metrics_out);
+
 /* FNV-1a-64 continuation over raw bytes (start h = 0xcbf29ce484222325) */
 uint64_t orc_fnv1a(uint64_t h, const void* data, size_t n);
 

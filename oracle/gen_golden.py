@@ -165,6 +165,70 @@ def main():
             assert rc == 0
             out["sort_desc" if desc else "sort_asc"] = {"ids": b64(oi), "e": b64(oe)}
         sub.append({"cap": cap, "m": m, "inputs": {k: b64(v) for k, v in inst.items()}, "out": out})
+    # ---- traffic (traffic.cpp): trajectories, step_road on random roads, resolve cases, batch
+    traf = {"models": [], "step_road": [], "resolve": [], "batch": None}
+    for L, period, gf, seed, T in ((7, 10, 0.5, 123, 100), (12, 10, 0.5, 55, 40), (5, 10, 0.0, 17, 60),
+                                   (1, 10, 0.5, 9, 30), (100, 10, 0.5, 3, 150), (40, 7, 0.3, 77, 120),
+                                   (3, 1, 1.0, 5, 20), (2000, 10, 0.5, 2024, 100)):
+        m = ref.traffic(L, period, gf, seed)
+        rows, hashes = [], []
+        for t in range(1, T + 1):
+            m.step(t)
+            rows.append(m.metrics().tolist())
+            if t % 10 == 0 or t == T:
+                e = m.export()
+                hashes.append([t, pyoracle.fnv1a([e[k] for k, _ in pyoracle.TRAFFIC_FIELDS] +
+                                                 [e["occupancy"], np.array([e["next_id"]], np.int64)])])
+        e = m.export()
+        traf["models"].append({"length": L, "period": period, "green_fraction": gf, "seed": seed,
+                               "steps": T, "phase": m.phase, "green_len": m.green_len,
+                               "metrics": rows, "hashes": hashes,
+                               "final": {k: b64(e[k]) for k, _ in pyoracle.TRAFFIC_FIELDS} |
+                                        {"occupancy": b64(e["occupancy"]), "next_id": e["next_id"]}})
+    g2 = np.random.default_rng(777)
+    for trial in range(40):
+        L = int(g2.integers(1, 30))
+        n = 3 * L
+        dens = g2.random()
+        occ = g2.random(n) < dens
+        slots = g2.permutation(n)[:int(occ.sum())]
+        st = {k: np.zeros(n, dt) for k, dt in pyoracle.TRAFFIC_FIELDS}
+        for cidx, slot in zip(np.flatnonzero(occ), slots):
+            st["active"][slot] = 1
+            st["lane"][slot] = cidx // L
+            st["cell"][slot] = cidx % L
+            st["ids"][slot] = slot
+            st["ages"][slot] = int(g2.integers(0, 5))
+        st["next_id"] = n
+        period = int(g2.integers(1, 12))
+        gf = float(g2.random())
+        seed = int(g2.integers(0, 1 << 62))
+        t = int(g2.integers(1, 1000))
+        out, stats = ref.traffic_step_road(st, L, period, gf, seed, t)
+        traf["step_road"].append({"length": L, "period": period, "green_fraction": gf, "seed": seed,
+                                  "t": t, "in": {k: b64(st[k]) for k, _ in pyoracle.TRAFFIC_FIELDS} |
+                                  {"next_id": st["next_id"]},
+                                  "out": {k: b64(out[k]) for k, _ in pyoracle.TRAFFIC_FIELDS} |
+                                  {"occupancy": b64(out["occupancy"]), "next_id": out["next_id"]},
+                                  "stats": stats.tolist()})
+        # resolve with random (mostly legal, sometimes illegal) proposals on the same road
+        kind = np.where(st["active"] == 1, g2.integers(0, 3, n), 0).astype(np.uint8)
+        to_lane = np.clip(st["lane"] + g2.integers(-1, 2, n), 0, 2)
+        to_cell = st["cell"] + 1
+        if trial % 7 == 3:
+            to_lane = to_lane + 2  # some targets outside the road
+        to_cell = np.where(kind == 1, to_cell, 0)
+        rc, acc = ref.traffic_resolve(L, st["active"], st["lane"], st["cell"], kind, to_lane, to_cell)
+        traf["resolve"].append({"length": L, "active": b64(st["active"]), "lane": b64(st["lane"]),
+                                "cell": b64(st["cell"]), "kind": b64(kind),
+                                "to_lane": b64(to_lane.astype(np.int64)),
+                                "to_cell": b64(to_cell.astype(np.int64)), "rc": rc,
+                                "accepted": b64(acc)})
+    rows, _ = ref.traffic_run_batch(20, 10, 0.5, 99, 8, 40, threads=4)
+    traf["batch"] = {"length": 20, "period": 10, "green_fraction": 0.5, "master": 99, "replicas": 8,
+                     "steps": 40, "metrics": rows.tolist()}
+    json.dump(traf, open(os.path.join(OUT, "traffic.json"), "w"))
+
     # ---- lifecycle: remove_agents then spawn_agents, chained cycles, id recycling on/off
     life = []
     g = np.random.default_rng(4242)

@@ -120,6 +120,23 @@ def _ewf_ptrs(st, with_types):
     return [_p(st[k], pt[k]) for k in keys]
 
 
+class OrcTrafficCfg(C.Structure):
+    _fields_ = [("length", C.c_int64), ("period", C.c_int64), ("green_fraction", C.c_double)]
+
+
+class OrcTraffic(C.Structure):
+    _fields_ = [("length", C.c_int64), ("period", C.c_int64), ("green_len", C.c_int64),
+                ("phase", C.c_int64), ("seed", C.c_uint64), ("capacity", C.c_int32),
+                ("num_active", C.c_int32), ("next_id", C.c_int64), ("active", u8p),
+                ("ids", i64p), ("ages", i64p), ("lane", i64p), ("cell", i64p),
+                ("occupancy", i32p), ("spawned", C.c_int64), ("exited", C.c_int64),
+                ("green", C.c_int64), ("spawned_total", C.c_int64), ("exited_total", C.c_int64)]
+
+
+TRAFFIC_FIELDS = (("active", np.uint8), ("ids", np.int64), ("ages", np.int64),
+                  ("lane", np.int64), ("cell", np.int64))
+
+
 class _Base:
     lib: C.CDLL
     prefix: str
@@ -159,6 +176,19 @@ class Oracle(_Base):
         L.orc_pair.argtypes = [u8p, C.c_int32, u8p, C.c_int32, i32p, i32p]
         L.orc_sort_perm.restype = C.c_int
         L.orc_sort_perm.argtypes = [f64p, u8p, C.c_int32, C.c_int, i32p]
+        L.orc_traffic_create.restype = C.POINTER(OrcTraffic)
+        L.orc_traffic_create.argtypes = [C.POINTER(OrcTrafficCfg), C.c_uint64]
+        L.orc_traffic_free.argtypes = [C.POINTER(OrcTraffic)]
+        L.orc_traffic_rebuild.restype = C.c_int
+        L.orc_traffic_rebuild.argtypes = [C.POINTER(OrcTraffic)]
+        L.orc_traffic_propose.argtypes = [C.POINTER(OrcTraffic), C.c_uint64, C.c_int, u8p, i64p, i64p]
+        L.orc_traffic_resolve.restype = C.c_int
+        L.orc_traffic_resolve.argtypes = [C.POINTER(OrcTraffic), u8p, i64p, i64p, u8p]
+        L.orc_traffic_step.argtypes = [C.POINTER(OrcTraffic), C.c_int64]
+        L.orc_traffic_metrics.argtypes = [C.POINTER(OrcTraffic), f64p]
+        L.orc_traffic_run_batch.restype = C.c_int
+        L.orc_traffic_run_batch.argtypes = [C.POINTER(OrcTrafficCfg), C.c_uint64, C.c_int32,
+                                            C.c_int64, f64p]
         L.orc_remove_agents.restype = C.c_int32
         L.orc_remove_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, u8p, C.c_int,
                                         i64p, i32p]
@@ -238,6 +268,18 @@ class Oracle(_Base):
         if rc:
             raise ValueError("non-finite sort key on an active slot")
         return p[:k.size].copy()
+
+    # traffic
+    def traffic(self, length, period=10, green_fraction=0.5, seed=0):
+        return OracleTraffic(self, length, period, green_fraction, seed)
+
+    def traffic_run_batch(self, length, period, green_fraction, master, replicas, steps):
+        out = np.zeros((replicas, steps, 4))
+        cfg = OrcTrafficCfg(length, period, green_fraction)
+        rc = self.lib.orc_traffic_run_batch(C.byref(cfg), master, replicas, steps, _p(out, f64p))
+        if rc:
+            raise ValueError("bad traffic config")
+        return out
 
     def lifecycle(self, st, kill, rows, valid, set_type=False, agent_type=0):
         """remove_agents(kill) then spawn_agents(rows, copy apply) on an e/w/f set
@@ -384,10 +426,73 @@ class Reference(_Base):
         L.ref_sort_agents.restype = C.c_int
         L.ref_sort_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, f64p, C.c_int,
                                       u8p, i64p, i64p, i64p, f64p, u8p]
+        L.ref_traffic_create.restype = C.c_void_p
+        L.ref_traffic_create.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_uint64]
+        L.ref_traffic_free.argtypes = [C.c_void_p]
+        L.ref_traffic_step.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_traffic_metrics.argtypes = [C.c_void_p, f64p]
+        L.ref_traffic_phase.restype = C.c_int64
+        L.ref_traffic_phase.argtypes = [C.c_void_p]
+        L.ref_traffic_green_len.restype = C.c_int64
+        L.ref_traffic_green_len.argtypes = [C.c_void_p]
+        L.ref_traffic_export.argtypes = [C.c_void_p, u8p, i64p, i64p, i64p, i64p, i32p, i64p, i32p]
+        L.ref_traffic_run.restype = C.c_double
+        L.ref_traffic_run.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.ref_traffic_step_road.restype = C.c_int
+        L.ref_traffic_step_road.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_int64,
+                                            u8p, i64p, i64p, i64p, i64p, i32p, i64p, i64p]
+        L.ref_traffic_resolve.restype = C.c_int
+        L.ref_traffic_resolve.argtypes = [C.c_int64, u8p, i64p, i64p, u8p, i64p, i64p, u8p]
+        L.ref_traffic_run_batch.restype = C.c_double
+        L.ref_traffic_run_batch.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_int32,
+                                            C.c_int64, C.c_int, f64p]
         L.ref_lifecycle.restype = C.c_int32
         L.ref_lifecycle.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, i64p, f64p, u8p, i64p, C.c_int,
                                     i64p, i32p, u8p, C.c_int32, i64p, f64p, u8p, u8p, C.c_int,
                                     C.c_int64, i32p, i32p, i32p, i32p]
+
+    # traffic
+    def traffic(self, length, period=10, green_fraction=0.5, seed=0):
+        return RefTraffic(self, length, period, green_fraction, seed)
+
+    def traffic_run_batch(self, length, period, green_fraction, master, replicas, steps,
+                          threads=0):
+        out = np.zeros((replicas, steps, 4))
+        wall = self.lib.ref_traffic_run_batch(length, period, green_fraction, master, replicas,
+                                              steps, threads, _p(out, f64p))
+        if wall < 0:
+            raise ValueError("bad traffic config")
+        return out, wall
+
+    def traffic_step_road(self, st, length, period, green_fraction, seed, t):
+        """step_road on an arbitrary road state (dict of TRAFFIC_FIELDS + next_id)."""
+        st = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in st.items()}
+        for k, dt in TRAFFIC_FIELDS:
+            st[k] = np.ascontiguousarray(st[k], dt)
+        occ = np.empty(3 * length, np.int32)
+        nid = C.c_int64(st["next_id"])
+        stats = np.zeros(3, np.int64)
+        rc = self.lib.ref_traffic_step_road(length, period, green_fraction, seed, t,
+                                            _p(st["active"], u8p), _p(st["ids"], i64p),
+                                            _p(st["ages"], i64p), _p(st["lane"], i64p),
+                                            _p(st["cell"], i64p), _p(occ, i32p), C.byref(nid),
+                                            _p(stats, i64p))
+        if rc:
+            raise ValueError("two cars occupy one road cell")
+        st["occupancy"] = occ
+        st["next_id"] = nid.value
+        return st, stats
+
+    def traffic_resolve(self, length, active, lane, cell, kind, to_lane, to_cell):
+        n = 3 * length
+        acc = np.zeros(n, np.uint8)
+        a = [np.ascontiguousarray(x, dt) for x, dt in ((active, np.uint8), (lane, np.int64),
+                                                      (cell, np.int64), (kind, np.uint8),
+                                                      (to_lane, np.int64), (to_cell, np.int64))]
+        rc = self.lib.ref_traffic_resolve(length, _p(a[0], u8p), _p(a[1], i64p), _p(a[2], i64p),
+                                          _p(a[3], u8p), _p(a[4], i64p), _p(a[5], i64p),
+                                          _p(acc, u8p))
+        return rc, acc
 
     def lifecycle(self, st, kill, rows, valid, set_type=False, agent_type=0):
         """The reference's remove_agents then spawn_agents (same contract as Oracle.lifecycle)."""
@@ -525,3 +630,106 @@ class RefPred:
         ch = np.empty(max(n, 1), np.int32)
         k = self.r.lib.ref_pred_birth_pairs(self.h, s, _p(par, i32p), _p(ch, i32p), n)
         return list(zip(par[:k].tolist(), ch[:k].tolist()))
+
+
+class OracleTraffic:
+    """TrafficModel restated in C (orc_traffic_*)."""
+
+    def __init__(self, o: Oracle, length, period, green_fraction, seed):
+        self.o = o
+        cfg = OrcTrafficCfg(length, period, green_fraction)
+        self.h = o.lib.orc_traffic_create(C.byref(cfg), seed)
+        if not self.h:
+            raise ValueError("bad traffic config")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.lib.orc_traffic_free(self.h)
+            self.h = None
+
+    @property
+    def m(self):
+        return self.h.contents
+
+    def step(self, t):
+        self.o.lib.orc_traffic_step(self.h, t)
+
+    def metrics(self):
+        out = np.zeros(4)
+        self.o.lib.orc_traffic_metrics(self.h, _p(out, f64p))
+        return out
+
+    def export(self):
+        m = self.m
+        n = m.capacity
+        d = {k: np.ctypeslib.as_array(getattr(m, k), (n,)).copy() for k, _ in TRAFFIC_FIELDS}
+        d["occupancy"] = np.ctypeslib.as_array(m.occupancy, (n,)).copy()
+        d.update(next_id=m.next_id, num_active=m.num_active)
+        return d
+
+    def load(self, st):
+        """Overwrite the road (arrays + next_id); returns 1 if two cars share a cell."""
+        m = self.m
+        n = m.capacity
+        for k, dt in TRAFFIC_FIELDS:
+            np.ctypeslib.as_array(getattr(m, k), (n,))[:] = np.asarray(st[k], dt)
+        m.next_id = st["next_id"]
+        m.num_active = int(np.count_nonzero(st["active"]))
+        return self.o.lib.orc_traffic_rebuild(self.h)
+
+    def resolve(self, kind, to_lane, to_cell):
+        n = self.m.capacity
+        acc = np.zeros(n, np.uint8)
+        a = [np.ascontiguousarray(x, dt) for x, dt in ((kind, np.uint8), (to_lane, np.int64),
+                                                      (to_cell, np.int64))]
+        rc = self.o.lib.orc_traffic_resolve(self.h, _p(a[0], u8p), _p(a[1], i64p), _p(a[2], i64p),
+                                            _p(acc, u8p))
+        return rc, acc
+
+
+class RefTraffic:
+    """The reference TrafficModel (oracle/_ref)."""
+
+    def __init__(self, r: Reference, length, period, green_fraction, seed):
+        self.r = r
+        self.length = length
+        self.h = r.lib.ref_traffic_create(length, period, green_fraction, seed)
+        if not self.h:
+            raise ValueError("bad traffic config")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.r.lib.ref_traffic_free(self.h)
+            self.h = None
+
+    def step(self, t):
+        self.r.lib.ref_traffic_step(self.h, t)
+
+    def run(self, t0, steps):
+        return self.r.lib.ref_traffic_run(self.h, t0, steps)
+
+    def metrics(self):
+        out = np.zeros(4)
+        self.r.lib.ref_traffic_metrics(self.h, _p(out, f64p))
+        return out
+
+    @property
+    def phase(self):
+        return self.r.lib.ref_traffic_phase(self.h)
+
+    @property
+    def green_len(self):
+        return self.r.lib.ref_traffic_green_len(self.h)
+
+    def export(self):
+        n = 3 * self.length
+        d = {k: np.zeros(n, dt) for k, dt in TRAFFIC_FIELDS}
+        occ = np.zeros(n, np.int32)
+        nid = C.c_int64(0)
+        na = C.c_int32(0)
+        self.r.lib.ref_traffic_export(self.h, _p(d["active"], u8p), _p(d["ids"], i64p),
+                                      _p(d["ages"], i64p), _p(d["lane"], i64p),
+                                      _p(d["cell"], i64p), _p(occ, i32p), C.byref(nid),
+                                      C.byref(na))
+        d.update(occupancy=occ, next_id=nid.value, num_active=na.value)
+        return d

@@ -10,6 +10,7 @@
 //   * replica_seeds / run_batch                     include/abmx/batch.hpp:48-54
 //   * set_agents_rm / _sci / _mask, select, sort     include/abmx/kernels.hpp:47-106
 //   * spawn_agents / remove_agents / step_agents    include/abmx/lifecycle.hpp:54-86
+//   * TrafficModel / step_road / resolve_conflicts  include/abmx/models/traffic.hpp:60-110
 // Nothing here re-implements reference behaviour; every call forwards.
 #include <chrono>
 #include <cstdint>
@@ -21,6 +22,7 @@
 #include "abmx/kernels.hpp"
 #include "abmx/lifecycle.hpp"
 #include "abmx/models/predation.hpp"
+#include "abmx/models/traffic.hpp"
 #include "abmx/rng.hpp"
 #include "abmx/simd/kernels.hpp"
 
@@ -427,6 +429,145 @@ int32_t ref_lifecycle(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages,
     *dropped = static_cast<int32_t>(o.dropped);
     *num_active = static_cast<int32_t>(o.set.num_active());
     return static_cast<int32_t>(o.spawned);
+}
+
+
+// ---------------------------------------------------------------- traffic (traffic.hpp)
+// A road is passed as flat arrays over capacity 3*length: active, ids, ages, lane, cell,
+// plus num_active / next_id; occupancy [3*length] is written on export.
+namespace {
+Road road_from(int64_t length, const uint8_t* active, const int64_t* ids, const int64_t* ages,
+               const int64_t* lane, const int64_t* cell, int64_t next_id) {
+    Road road = Road::empty(length);
+    const auto n = static_cast<size_t>(road.cars.capacity());
+    Index na = 0;
+    for (size_t i = 0; i < n; ++i) {
+        road.cars.active_mut()[i] = active[i];
+        road.cars.ids_mut()[i] = ids[i];
+        road.cars.ages_mut()[i] = ages[i];
+        road.cars.state_mut().ints("lane")[i] = lane[i];
+        road.cars.state_mut().ints("cell")[i] = cell[i];
+        na += active[i] ? 1 : 0;
+    }
+    road.cars.set_num_active(na);
+    road.cars.set_next_id(next_id);
+    road.rebuild_occupancy();
+    return road;
+}
+void road_to(const Road& road, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* lane,
+             int64_t* cell, int32_t* occupancy, int64_t* next_id) {
+    const auto n = static_cast<size_t>(road.cars.capacity());
+    for (size_t i = 0; i < n; ++i) {
+        active[i] = road.cars.active()[i];
+        ids[i] = road.cars.ids()[i];
+        ages[i] = road.cars.ages()[i];
+        lane[i] = road.cars.state().ints("lane")[i];
+        cell[i] = road.cars.state().ints("cell")[i];
+        if (occupancy) occupancy[i] = road.occupancy[i];
+    }
+    *next_id = road.cars.next_id();
+}
+}  // namespace
+
+void* ref_traffic_create(int64_t length, int64_t period, double green_fraction, uint64_t seed) {
+    try {
+        TrafficConfig cfg{length, period, green_fraction};
+        return new TrafficModel(cfg, RngState{seed});
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+void ref_traffic_free(void* h) { delete static_cast<TrafficModel*>(h); }
+void ref_traffic_step(void* h, int64_t t) { static_cast<TrafficModel*>(h)->step(t); }
+void ref_traffic_metrics(void* h, double* out4) {
+    std::vector<std::vector<double>> rows;
+    static_cast<TrafficModel*>(h)->collect_metrics(rows);
+    for (int k = 0; k < 4; ++k) out4[k] = rows[0][static_cast<size_t>(k)];
+}
+int64_t ref_traffic_phase(void* h) { return static_cast<TrafficModel*>(h)->schedule().phase; }
+int64_t ref_traffic_green_len(void* h) { return static_cast<TrafficModel*>(h)->schedule().green_len; }
+void ref_traffic_export(void* h, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* lane,
+                        int64_t* cell, int32_t* occupancy, int64_t* next_id, int32_t* num_active) {
+    const Road& road = static_cast<TrafficModel*>(h)->road();
+    road_to(road, active, ids, ages, lane, cell, occupancy, next_id);
+    *num_active = static_cast<int32_t>(road.cars.num_active());
+}
+// double wall ms of the steps t0..t0+steps-1
+double ref_traffic_run(void* h, int64_t t0, int64_t steps) {
+    auto* m = static_cast<TrafficModel*>(h);
+    const auto a = std::chrono::steady_clock::now();
+    for (int64_t t = t0; t < t0 + steps; ++t) m->step(t);
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+}
+
+// step_road on an arbitrary road (traffic.cpp:186-222): state in/out; stats out {spawned,
+// exited, green}. Returns 0, or 1 on DomainError (two cars in one cell).
+int ref_traffic_step_road(int64_t length, int64_t period, double green_fraction, uint64_t seed,
+                          int64_t t, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* lane,
+                          int64_t* cell, int32_t* occupancy, int64_t* next_id, int64_t* stats3) {
+    try {
+        const TrafficConfig cfg{length, period, green_fraction};
+        const SignalSchedule sched = SignalSchedule::from_config(cfg, RngState{seed});
+        Road road = road_from(length, active, ids, ages, lane, cell, *next_id);
+        RoadStepStats st;
+        Road out = step_road(road, sched, RngState{seed}, t, &st);
+        road_to(out, active, ids, ages, lane, cell, occupancy, next_id);
+        stats3[0] = st.spawned;
+        stats3[1] = st.exited;
+        stats3[2] = st.signal_green ? 1 : 0;
+        return 0;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+// resolve_conflicts with given proposals (kind 0 stay / 1 move / 2 exit). Returns 0, 1 on
+// DomainError (bad road), 2 on ContractError (target outside the road).
+int ref_traffic_resolve(int64_t length, const uint8_t* active, const int64_t* lane,
+                        const int64_t* cell, const uint8_t* kind, const int64_t* to_lane,
+                        const int64_t* to_cell, uint8_t* accepted) {
+    const auto n = static_cast<size_t>(3 * length);
+    std::vector<int64_t> z(n, 0);
+    std::unique_ptr<Road> rp;
+    try {
+        rp = std::make_unique<Road>(road_from(length, active, z.data(), z.data(), lane, cell, 0));
+    } catch (const std::exception&) {
+        return 1;
+    }
+    const Road& road = *rp;
+    Proposals p;
+    p.kind.resize(n);
+    p.to_lane.assign(to_lane, to_lane + n);
+    p.to_cell.assign(to_cell, to_cell + n);
+    for (size_t i = 0; i < n; ++i) p.kind[i] = static_cast<MoveKind>(kind[i]);
+    try {
+        const Mask acc = resolve_conflicts(road, p);
+        std::memcpy(accepted, acc.data(), n);
+        return 0;
+    } catch (const ContractError&) {
+        return 2;
+    } catch (const std::exception&) {
+        return 1;
+    }
+}
+
+double ref_traffic_run_batch(int64_t length, int64_t period, double green_fraction,
+                             uint64_t master, int32_t replicas, int64_t steps, int threads,
+                             double* metrics_out) {
+    try {
+        const auto model = TrafficModel::descriptor(TrafficConfig{length, period, green_fraction});
+        const auto seeds = replica_seeds(RngState{master}, replicas);
+        double wall = 0.0;
+        const Trajectory tr = run_batch(model, seeds, steps, threads, &wall);
+        if (metrics_out) {
+            size_t k = 0;
+            for (const auto& row : tr.rows)
+                for (double v : row.values) metrics_out[k++] = v;
+        }
+        return wall;
+    } catch (const std::exception&) {
+        return -1.0;
+    }
 }
 
 }  // extern "C"

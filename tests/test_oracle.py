@@ -170,3 +170,56 @@ def test_lifecycle_golden(oracle):
             for k in ("killed", "spawned", "dropped"):
                 assert o[k] == wo[k], (i, j, k)
             assert np.array_equal(o["slots"], wo["slots"]) and np.array_equal(o["rows"], wo["rows"])
+
+
+def _traffic_state(d):
+    import pyoracle
+    st = {k: arr(d[k], dt).copy() for k, dt in pyoracle.TRAFFIC_FIELDS}
+    st["next_id"] = d["next_id"]
+    if "occupancy" in d:
+        st["occupancy"] = arr(d["occupancy"], np.int32).copy()
+    return st
+
+
+def test_traffic_golden(oracle):
+    """TrafficModel trajectories, step_road on random roads, resolve_conflicts (incl. contract
+    errors) and run_batch rows (traffic.cpp:47-238): the C restatement matches the reference."""
+    import pyoracle
+    g = load("traffic.json")
+    for mcase in g["models"]:
+        m = oracle.traffic(mcase["length"], mcase["period"], mcase["green_fraction"], mcase["seed"])
+        assert (m.m.phase, m.m.green_len) == (mcase["phase"], mcase["green_len"])
+        hashes = dict((t, h) for t, h in mcase["hashes"])
+        for t in range(1, mcase["steps"] + 1):
+            m.step(t)
+            assert m.metrics().tolist() == mcase["metrics"][t - 1], (mcase["length"], t)
+            if t in hashes:
+                e = m.export()
+                h = pyoracle.fnv1a([e[k] for k, _ in pyoracle.TRAFFIC_FIELDS] +
+                                   [e["occupancy"], np.array([e["next_id"]], np.int64)])
+                assert h == hashes[t], (mcase["length"], t)
+    for c in g["step_road"]:
+        m = oracle.traffic(c["length"], c["period"], c["green_fraction"], c["seed"])
+        assert m.load(_traffic_state(c["in"])) == 0
+        m.step(c["t"])
+        e = m.export()
+        want = _traffic_state(c["out"])
+        for k in ("active", "ids", "ages", "lane", "cell", "occupancy"):
+            assert np.array_equal(e[k], want[k]), k
+        assert e["next_id"] == want["next_id"]
+        assert [m.m.spawned, m.m.exited, m.m.green] == c["stats"]
+    for c in g["resolve"]:
+        m = oracle.traffic(c["length"])
+        st = {"active": arr(c["active"], np.uint8), "ids": np.zeros(3 * c["length"], np.int64),
+              "ages": np.zeros(3 * c["length"], np.int64), "lane": arr(c["lane"], np.int64),
+              "cell": arr(c["cell"], np.int64), "next_id": 0}
+        m.load(st)
+        rc, acc = m.resolve(arr(c["kind"], np.uint8), arr(c["to_lane"], np.int64),
+                            arr(c["to_cell"], np.int64))
+        assert rc == c["rc"]
+        if rc == 0:
+            assert np.array_equal(acc, arr(c["accepted"], np.uint8))
+    b = g["batch"]
+    got = oracle.traffic_run_batch(b["length"], b["period"], b["green_fraction"], b["master"],
+                                   b["replicas"], b["steps"])
+    assert np.array_equal(got, np.array(b["metrics"]))
