@@ -37,6 +37,7 @@ extern "C" {
 #define ABMX_E_BATCH 4    /* BatchError    errors.hpp:36-38 */
 #define ABMX_E_CUDA 5     /* device / driver failure (no reference counterpart) */
 #define ABMX_E_ARG 6      /* null handle or pointer */
+#define ABMX_E_CONTRACT 7 /* ContractError errors.hpp:31-33 (e.g. a move proposal off the road) */
 
 const char* abmx_cuda_last_error(void);
 const char* abmx_cuda_version(void);
@@ -246,6 +247,61 @@ int abmx_agents_permute(const abmx_agent_set* s, const int32_t* d_perm, void* st
 /* sort_perm + permute; d_perm (nullable) receives the permutation. */
 int abmx_agents_sort(const abmx_agent_set* s, const double* d_key, int32_t descending,
                      int32_t* d_perm, void* stream);
+
+/* ======================================================================= 5. traffic
+ * TrafficModel (include/abmx/models/traffic.hpp:84-110, src/models/traffic.cpp) for `roads`
+ * independent roads at once (seeds[r] = the replica seed). Capacity 3*length slots per road;
+ * state exported in the reference layout (lane / cell as int64, occupancy slot-or--1).
+ * abmx_traffic_config has the field order of abmx::models::TrafficConfig (traffic.hpp:13-17). */
+typedef struct abmx_traffic_config {
+    int64_t length;        /* cells per lane (3 lanes) */
+    int64_t period;        /* signal period */
+    double green_fraction;
+} abmx_traffic_config;
+
+typedef struct abmx_traffic abmx_traffic;
+
+int abmx_traffic_create(const abmx_traffic_config* cfg, const uint64_t* seeds, int32_t roads,
+                        abmx_traffic** out);
+int abmx_traffic_destroy(abmx_traffic* h);
+/* TrafficModel::step(t) on every road (traffic.cpp:228-232) */
+int abmx_traffic_step(abmx_traffic* h, int64_t t);
+/* steps t0 .. t0+steps-1; metrics_out (nullable, host) [roads][steps][4] */
+int abmx_traffic_run(abmx_traffic* h, int64_t t0, int64_t steps, double* metrics_out);
+int abmx_traffic_sync(abmx_traffic* h);
+/* collect_metrics of the last step (traffic.cpp:234-238): [roads][4] n_cars, spawned, exited,
+ * signal_green */
+int abmx_traffic_metrics(abmx_traffic* h, double* out);
+int abmx_traffic_totals(abmx_traffic* h, int32_t road, int64_t* spawned_total,
+                        int64_t* exited_total);
+/* SignalSchedule (traffic.hpp:21-32) of a road */
+int abmx_traffic_schedule(abmx_traffic* h, int32_t road, int64_t* period, int64_t* green_len,
+                          int64_t* phase);
+int abmx_traffic_export(abmx_traffic* h, int32_t road, uint8_t* active, int64_t* ids,
+                        int64_t* ages, int64_t* lane, int64_t* cell, int32_t* occupancy,
+                        int64_t* next_id, int32_t* num_active);
+/* replace a road's cars (DomainError if two cars share a cell, traffic.cpp:31-44) */
+int abmx_traffic_import(abmx_traffic* h, int32_t road, const uint8_t* active,
+                        const int64_t* ids, const int64_t* ages, const int64_t* lane,
+                        const int64_t* cell, int64_t next_id);
+/* resolve_conflicts (traffic.cpp:82-140) with explicit proposals, host arrays of 3*length:
+ * kind 0 stay / 1 move / 2 exit. ABMX_E_CONTRACT on a move target off the road. Acceptance is
+ * the least fixed point (pointer jumping on the device); identical to the reference whenever
+ * its L-round iteration converges, which holds for every propose_moves proposal. */
+int abmx_traffic_resolve(int64_t length, const uint8_t* active, const int64_t* lane,
+                         const int64_t* cell, const uint8_t* kind, const int64_t* to_lane,
+                         const int64_t* to_cell, uint8_t* accepted);
+/* timed steps (see abmx_predation_bench) */
+int abmx_traffic_bench(abmx_traffic* h, int64_t t0, int64_t steps, int64_t flush_bytes,
+                       int32_t per_kernel, double* step_ms);
+int32_t abmx_traffic_kernel_count(void);
+const char* abmx_traffic_kernel_name(int32_t k);
+int abmx_traffic_kernel_times(abmx_traffic* h, double* ms, int64_t* launches);
+/* run_batch of TrafficModel for replicas [replica_begin, +count) of `master`: metrics_out
+ * [count][steps][4]; kernel_ms (nullable) the device time of the run */
+int abmx_traffic_run_batch(const abmx_traffic_config* cfg, uint64_t master,
+                           int32_t replica_begin, int32_t count, int64_t steps,
+                           double* metrics_out, double* kernel_ms);
 
 #ifdef __cplusplus
 }

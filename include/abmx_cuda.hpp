@@ -36,6 +36,9 @@ struct DomainError : Error {
 struct BatchError : Error {
     using Error::Error;
 };
+struct ContractError : Error {
+    using Error::Error;
+};
 struct DeviceError : Error {
     using Error::Error;
 };
@@ -49,6 +52,7 @@ inline void check(int rc) {
         case ABMX_E_SCHEMA: throw SchemaError(msg);
         case ABMX_E_BATCH: throw BatchError(msg);
         case ABMX_E_CUDA: throw DeviceError(msg);
+        case ABMX_E_CONTRACT: throw ContractError(msg);
         default: throw Error(msg);
     }
 }

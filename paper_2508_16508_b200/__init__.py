@@ -26,6 +26,7 @@ import numpy as np
 
 __all__ = [
     "AbmxError", "SchemaError", "CapacityError", "DomainError", "BatchError", "CudaError",
+    "ContractError",
     "lib", "library_path", "PredationConfig", "PredationEvents", "SpeciesEvents",
     "PredationModel", "SelectionResult", "rank_scan", "count_true", "compact_indices",
     "match_first_equal", "blend_i64", "blend_f64", "blend_u8", "compute_ranks",
@@ -59,6 +60,10 @@ class BatchError(AbmxError):
 
 class CudaError(AbmxError):
     pass
+
+
+class ContractError(AbmxError):
+    """abmx::ContractError (errors.hpp:31-33)."""
 
 
 if not os.path.exists(library_path):
@@ -194,7 +199,7 @@ _sig("abmx_ensemble_run", C.c_int, [C.POINTER(PredationConfig), C.c_uint64, C.c_
 _sig("abmx_ensemble_smem_fits", C.c_int, [C.POINTER(PredationConfig)])
 
 _ERRORS = {1: DomainError, 2: CapacityError, 3: SchemaError, 4: BatchError, 5: CudaError,
-           6: AbmxError}
+           6: AbmxError, 7: ContractError}
 
 
 def _check(rc):

@@ -1,0 +1,1062 @@
+// traffic.cu — the three-lane traffic model (src/models/traffic.cpp:47-238) on sm_100a for R
+// roads at once, device-resident state, bit-exact with the reference.
+//
+// A step is four kernels:
+//   k_propose  per car slot: the proposal (traffic.cpp:47-80: forward / forward-left /
+//              forward-right drawn from seed.split(6).split(t).draw(slot); exit column: exit iff
+//              green, no draw) and the per-target-cell priority bid (traffic.cpp:95-124:
+//              same lane > from the left lane > from the right lane) as one 64-bit atomicMax of
+//              {epoch, ~(prio, slot)} — prios into one cell are distinct, so the max is the winner.
+//   k_accept   per column: the acceptance fixed point (traffic.cpp:124-138). A winner enters once
+//              its target is empty or its occupant moves out; targets are always one column to the
+//              right, so the acceptance bits of column c are a function of those of column c+1:
+//              F_c : {0,1}^3 -> {0,1}^3 (an 8-entry table of 3-bit values, 24 bits). The fixed point
+//              is the suffix composition F_c ∘ F_{c+1} ∘ ... ∘ F_{L-1} (F_{L-1} is constant: exits),
+//              computed as a single-pass scan with decoupled lookback from the road's end.
+//   k_apply    per car slot: accepted moves (set_agents_mask) and exits (remove_agents), the new
+//              occupancy written by the movers themselves (a vacated cell is cleared unless an
+//              accepted winner enters it), and per-tile first free slots for the spawn.
+//   k_spawn    per road: spawn_cars (traffic.cpp:143-184): k = uniform_int(0, 0, 4), partial lane
+//              shuffle, entry cells that are free, rank-match into the lowest free slots, fresh ids.
+//
+// Layout per road r (capacity 3L slots, 3L cells): active u8, pos i32 (= lane*L + cell), ids i64,
+// ages i64; occupancy i32 (slot or -1), bid u64, acc u8 per cell.
+#include <climits>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/abmx_cuda.h"
+#include "abmx_device.cuh"
+#include "abmx_internal.h"
+
+using namespace abmx_dev;
+
+namespace abmx_trf {
+
+constexpr int kT = 256;
+constexpr int kS = 4;
+constexpr int kTile = kT * kS;  // slots per CTA (k_propose, k_apply)
+constexpr int kCI = 16;         // columns per thread (k_accept)
+constexpr int kCT = kT * kCI;   // columns per CTA
+constexpr unsigned kSlotMask = (1u << 28) - 1;
+constexpr unsigned long long kFlagAgg = 1ULL << 62;
+constexpr unsigned long long kFlagPre = 2ULL << 62;
+constexpr unsigned kIdentity = 0 | (1 << 3) | (2 << 6) | (3 << 9) | (4 << 12) | (5 << 15) | (6 << 18) | (7 << 21);
+constexpr int kNumKernels = 4;
+
+enum : int { kStay = -1, kExit = -2 };
+
+struct TParams {
+    // per step
+    unsigned long long epoch;
+    long long t;
+    double* metrics;  // [R][metrics_stride][4]
+    unsigned run_step, metrics_stride;
+    // constants
+    int R, L, C, Cpad, Npad, tiles, ctiles;
+    long long period, green_len;
+    const long long* phase;
+    const unsigned long long* seeds;
+    uint8_t* active;
+    int* pos;
+    long long* ids;
+    long long* ages;
+    int* occ;
+    unsigned long long* bid;
+    uint8_t* acc;
+    unsigned long long* cstatus;  // [R][ctiles] lookback words
+    unsigned* ticket;             // [2]
+    int4* tinfo;                  // [R][tiles] {free count, first three free slots}
+    long long* cnt;               // [R][8] num_active, next_id, spawned_total, exited_total, spawned, exited, green
+};
+
+__device__ __forceinline__ bool green_of(const TParams& P, int r) {  // SignalSchedule::green
+    const long long m = ((P.t + P.phase[r]) % P.period + P.period) % P.period;
+    return m < P.green_len;
+}
+__device__ __forceinline__ unsigned long long propose_key(const TParams& P, int r) {
+    return split(split(P.seeds[r], 6), static_cast<unsigned long long>(P.t));  // TrafficPropose
+}
+// target cell index of car `slot` at cell index p, or kStay / kExit (traffic.cpp:57-79)
+__device__ __forceinline__ int proposal(const TParams& P, int slot, int p, bool green, unsigned long long key) {
+    const int lane = p / P.L, cell = p - lane * P.L;
+    if (cell == P.L - 1) return green ? kExit : kStay;
+    const int n = 1 + (lane > 0) + (lane < 2);
+    const int pick = static_cast<int>(uniform_span(key, static_cast<unsigned long long>(slot), static_cast<unsigned long long>(n)));
+    const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
+    return tl * P.L + cell + 1;
+}
+__device__ __forceinline__ unsigned long long bid_word(unsigned long long epoch, int prio, int slot) {
+    return (epoch << 32) | (0xFFFFFFFFu - ((static_cast<unsigned>(prio) << 28) | static_cast<unsigned>(slot)));
+}
+// winner of a cell's bid word this epoch: slot, prio; false if no bid this epoch
+__device__ __forceinline__ bool bid_winner(unsigned long long w, unsigned long long epoch, int& slot, int& prio) {
+    if ((w >> 32) != (epoch & 0xFFFFFFFFULL)) return false;
+    const unsigned v = 0xFFFFFFFFu - static_cast<unsigned>(w);
+    slot = static_cast<int>(v & kSlotMask);
+    prio = static_cast<int>(v >> 28);
+    return true;
+}
+
+// ---------------------------------------------------------------- k_propose
+__global__ void __launch_bounds__(kT) k_propose(TParams P) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.ticket[P.epoch & 1] = 0u;
+    const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
+    const bool green = green_of(P, r);
+    const unsigned long long key = propose_key(P, r);
+    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
+#pragma unroll
+    for (int k = 0; k < kS; ++k) {
+        const int i = tile * kTile + k * kT + threadIdx.x;
+        if (i >= P.C || !P.active[sb + i]) continue;
+        const int p = P.pos[sb + i];
+        const int X = proposal(P, i, p, green, key);
+        if (X < 0) continue;
+        const int lane = p / P.L, tl = X / P.L;
+        const int prio = lane == tl ? 0 : (lane == tl - 1 ? 1 : 2);
+        atomicMax(&P.bid[cb + X], bid_word(P.epoch, prio, i));
+    }
+}
+
+// ---------------------------------------------------------------- k_accept
+__device__ __forceinline__ unsigned fn_at(unsigned f, unsigned x) { return (f >> (3 * x)) & 7u; }
+// (f ∘ g)[x] = f[g[x]]
+__device__ __forceinline__ unsigned compose(unsigned f, unsigned g) {
+    unsigned h = 0;
+#pragma unroll
+    for (unsigned x = 0; x < 8; ++x) h |= fn_at(f, fn_at(g, x)) << (3 * x);
+    return h;
+}
+
+// F_c: acceptance bits of column c's occupants as a function of column c+1's. m3 = occupied lanes.
+__device__ unsigned column_fn(const TParams& P, size_t sb, size_t cb, int c, bool green, unsigned long long key,
+                              unsigned& m3) {
+    int mode[3];  // 0: never, 1: always, 2 + tl: iff the occupant of (tl, c+1) moves out
+    m3 = 0;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        mode[l] = 0;
+        const int o = P.occ[cb + l * P.L + c];
+        if (o < 0) continue;
+        m3 |= 1u << l;
+        const int X = proposal(P, o, l * P.L + c, green, key);
+        if (X == kExit) {
+            mode[l] = 1;
+        } else if (X >= 0) {
+            int ws, wp;
+            if (bid_winner(P.bid[cb + X], P.epoch, ws, wp) && ws == o)
+                mode[l] = P.occ[cb + X] < 0 ? 1 : 2 + X / P.L;
+        }
+    }
+    unsigned f = 0;
+#pragma unroll
+    for (unsigned x = 0; x < 8; ++x) {
+        unsigned out = 0;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            const unsigned b = mode[l] == 0 ? 0u : (mode[l] == 1 ? 1u : (x >> (mode[l] - 2)) & 1u);
+            out |= b << l;
+        }
+        f |= out << (3 * x);
+    }
+    (void)sb;
+    return f;
+}
+
+__global__ void __launch_bounds__(kT) k_accept(TParams P) {
+    __shared__ unsigned s_tile;
+    __shared__ unsigned s_warp[kT / 32];
+    __shared__ unsigned s_vin;
+    if (threadIdx.x == 0) s_tile = atomicAdd(&P.ticket[P.epoch & 1], 1u);
+    __syncthreads();
+    const unsigned g = s_tile;
+    const int r = static_cast<int>(g / P.ctiles), tau = static_cast<int>(g % P.ctiles);
+    const int hi = P.L - tau * kCT;  // exclusive; tile 0 holds the road's last columns
+    const bool green = green_of(P, r);
+    const unsigned long long key = propose_key(P, r);
+    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
+    const int c_hi = hi - static_cast<int>(threadIdx.x) * kCI;
+    unsigned F[kCI];
+    unsigned long long occm = 0;
+    unsigned T = kIdentity;
+#pragma unroll
+    for (int j = 0; j < kCI; ++j) {
+        const int c = c_hi - 1 - j;
+        unsigned f = kIdentity;
+        if (c >= 0) {
+            unsigned m3;
+            f = column_fn(P, sb, cb, c, green, key, m3);
+            occm |= static_cast<unsigned long long>(m3) << (3 * j);
+        }
+        F[j] = f;
+        T = compose(f, T);
+    }
+    // block scan over threads (thread 0 = rightmost): I_t = T_t ∘ I_{t-1}
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned I = T;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned o = __shfl_up_sync(0xffffffffu, I, d);
+        if (lane >= d) I = compose(I, o);
+    }
+    if (lane == 31) s_warp[warp] = I;
+    __syncthreads();
+    if (warp == 0) {
+        unsigned wv = lane < kT / 32 ? s_warp[lane] : kIdentity;
+#pragma unroll
+        for (int d = 1; d < kT / 32; d <<= 1) {
+            const unsigned o = __shfl_up_sync(0xffffffffu, wv, d);
+            if (lane >= d) wv = compose(wv, o);
+        }
+        if (lane < kT / 32) s_warp[lane] = wv;  // inclusive warp prefixes
+    }
+    __syncthreads();
+    const unsigned wex = warp > 0 ? s_warp[warp - 1] : kIdentity;
+    const unsigned up = __shfl_up_sync(0xffffffffu, I, 1);
+    const unsigned E = lane > 0 ? compose(up, wex) : wex;  // exclusive prefix of this thread
+    if (threadIdx.x == 0) {
+        const unsigned A = s_warp[kT / 32 - 1];  // tile aggregate
+        unsigned long long* st = P.cstatus + static_cast<size_t>(r) * P.ctiles;
+        const unsigned long long tag = (P.epoch & 0x3FFFFFFFULL) << 32;
+        unsigned vin = 0;
+        if (tau > 0) {
+            st_word(&st[tau], kFlagAgg | tag | A);
+            unsigned accf = kIdentity;
+            for (int j = tau - 1;;) {
+                const unsigned long long w = ld_word(&st[j]);
+                if ((w & (0x3FFFFFFFULL << 32)) != tag || (w >> 62) == 0) continue;  // not yet published
+                if ((w >> 62) == 2) {
+                    vin = fn_at(accf, static_cast<unsigned>(w & 7u));
+                    break;
+                }
+                accf = compose(accf, static_cast<unsigned>(w & 0xFFFFFFu));
+                --j;
+            }
+        }
+        st_word(&st[tau], kFlagPre | tag | fn_at(A, vin));
+        s_vin = vin;
+    }
+    __syncthreads();
+    unsigned v = fn_at(E, s_vin);
+#pragma unroll
+    for (int j = 0; j < kCI; ++j) {
+        v = fn_at(F[j], v);
+        const unsigned m3 = static_cast<unsigned>(occm >> (3 * j)) & 7u;
+        if (m3) {
+            const int c = c_hi - 1 - j;
+#pragma unroll
+            for (int l = 0; l < 3; ++l)
+                if (m3 & (1u << l)) P.acc[cb + l * P.L + c] = static_cast<uint8_t>((v >> l) & 1u);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- k_apply
+// Clear the occupancy of vacated cell p unless an accepted winner enters it this step.
+__device__ __forceinline__ void vacate(const TParams& P, size_t cb, int p) {
+    int ws, wp;
+    if (bid_winner(P.bid[cb + p], P.epoch, ws, wp)) {
+        const int lane = p / P.L;
+        const int src_lane = wp == 0 ? lane : (wp == 1 ? lane - 1 : lane + 1);
+        const int src = src_lane * P.L + (p - lane * P.L) - 1;
+        if (P.acc[cb + src]) return;  // the winner writes occ[p]
+    }
+    P.occ[cb + p] = -1;
+}
+
+__global__ void __launch_bounds__(kT) k_apply(TParams P) {
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ int s_first[3];
+    __shared__ unsigned s_exit[kT / 32];
+    const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
+    const bool green = green_of(P, r);
+    const unsigned long long key = propose_key(P, r);
+    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
+    const int i0 = tile * kTile + threadIdx.x * kS;  // blocked: free-slot order = slot order
+    unsigned exited = 0, nf = 0;
+    bool fr[kS];
+#pragma unroll
+    for (int k = 0; k < kS; ++k) {
+        const int i = i0 + k;
+        fr[k] = false;
+        if (i >= P.C) continue;
+        if (P.active[sb + i]) {
+            const int p = P.pos[sb + i];
+            if (P.acc[cb + p]) {
+                const int X = proposal(P, i, p, green, key);
+                if (X == kExit) {  // remove_agents -> reset_slot (agent_set.cpp:45-58)
+                    P.active[sb + i] = 0;
+                    P.ids[sb + i] = 0;
+                    P.ages[sb + i] = 0;
+                    P.pos[sb + i] = 0;
+                    ++exited;
+                    fr[k] = true;
+                } else {  // set_agents_mask: lane / cell <- target
+                    P.pos[sb + i] = X;
+                    P.occ[cb + X] = i;
+                }
+                vacate(P, cb, p);
+            }
+        } else {
+            fr[k] = true;
+        }
+        nf += fr[k];
+    }
+    unsigned long long tot;
+    const unsigned long long ex = block_excl_scan<kT>(nf, s_scan, &tot);
+    if (threadIdx.x < 3) s_first[threadIdx.x] = -1;
+    __syncthreads();
+    unsigned rank = static_cast<unsigned>(ex);
+#pragma unroll
+    for (int k = 0; k < kS; ++k)
+        if (fr[k]) {
+            if (rank < 3) s_first[rank] = i0 + k;
+            ++rank;
+        }
+    const unsigned e = __reduce_add_sync(0xffffffffu, exited);
+    if ((threadIdx.x & 31) == 0) s_exit[threadIdx.x >> 5] = e;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned ex_sum = 0;
+        for (int w = 0; w < kT / 32; ++w) ex_sum += s_exit[w];
+        if (ex_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&P.cnt[static_cast<size_t>(r) * 8 + 5]), ex_sum);
+        P.tinfo[static_cast<size_t>(r) * P.tiles + tile] =
+            make_int4(static_cast<int>(tot), s_first[0], s_first[1], s_first[2]);
+    }
+}
+
+// ---------------------------------------------------------------- k_spawn
+// One warp per road: spawn_cars (traffic.cpp:143-184), counters and the metrics row.
+__global__ void k_spawn(TParams P) {
+    const int r = blockIdx.x;
+    const int lane = threadIdx.x;
+    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
+    long long* cn = P.cnt + static_cast<size_t>(r) * 8;
+    // rows (lane 0): k attempts, partial shuffle, free entry cells
+    int rows[3] = {-1, -1, -1};
+    int nvalid = 0;
+    {
+        const unsigned long long key = split(split(P.seeds[r], 7), static_cast<unsigned long long>(P.t));
+        const int k = static_cast<int>(uniform_span(key, 0, 4));
+        int lanes[3] = {0, 1, 2};
+        for (int i = 0; i < (k < 2 ? k : 2); ++i) {
+            const int j = i + static_cast<int>(uniform_span(key, static_cast<unsigned long long>(1 + i),
+                                                            static_cast<unsigned long long>(3 - i)));
+            const int tmp = lanes[i];
+            lanes[i] = lanes[j];
+            lanes[j] = tmp;
+        }
+        for (int q = 0; q < (k < 3 ? k : 3); ++q)
+            if (P.occ[cb + lanes[q] * P.L] < 0) rows[nvalid++] = lanes[q];
+    }
+    // the lowest nvalid free slots, tiles in order (warp-parallel over tile chunks)
+    int slots[3] = {-1, -1, -1};
+    int nf = 0;
+    for (int t0 = 0; t0 < P.tiles && nf < nvalid; t0 += 32) {
+        const int t = t0 + lane;
+        const int4 ti = t < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + t] : make_int4(0, -1, -1, -1);
+        unsigned m = __ballot_sync(0xffffffffu, ti.x > 0);
+        while (m && nf < nvalid) {
+            const int src = __ffs(m) - 1;
+            m &= m - 1;
+            const int cnt = __shfl_sync(0xffffffffu, ti.x, src);
+            const int f0 = __shfl_sync(0xffffffffu, ti.y, src);
+            const int f1 = __shfl_sync(0xffffffffu, ti.z, src);
+            const int f2 = __shfl_sync(0xffffffffu, ti.w, src);
+            const int fs[3] = {f0, f1, f2};
+            for (int q = 0; q < cnt && q < 3 && nf < nvalid; ++q) slots[nf++] = fs[q];
+        }
+    }
+    if (lane == 0) {
+        const int spawned = nf < nvalid ? nf : nvalid;
+        const long long nid = cn[1];
+        for (int q = 0; q < spawned; ++q) {
+            const int s = slots[q];
+            P.active[sb + s] = 1;
+            P.pos[sb + s] = rows[q] * P.L;
+            P.ids[sb + s] = nid + q;
+            P.ages[sb + s] = 0;
+            P.occ[cb + rows[q] * P.L] = s;
+        }
+        const long long exited = cn[5];
+        cn[0] += spawned - exited;
+        cn[1] = nid + spawned;
+        cn[2] += spawned;
+        cn[3] += exited;
+        cn[4] = spawned;
+        cn[6] = green_of(P, r) ? 1 : 0;
+        double* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
+        row[0] = static_cast<double>(cn[0]);
+        row[1] = static_cast<double>(spawned);
+        row[2] = static_cast<double>(exited);
+        row[3] = cn[6] ? 1.0 : 0.0;
+        cn[5] = 0;  // exits of the next step accumulate from zero
+    }
+}
+
+// ---------------------------------------------------------------- resolve_conflicts (explicit)
+// General proposals (any in-road target): acceptance is the least fixed point of
+// acc(w) = winner(w) && (target empty || acc(occupant)), solved by pointer jumping;
+// state >= 0: pointer to the slot whose acceptance decides; -1 accepted; -2 rejected.
+__global__ void k_res_bid(const uint8_t* active, const int* lane, const int* target, int n, int L,
+                          unsigned long long* bid) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n || !active[i] || target[i] < 0) return;
+    const int tl = target[i] / L;
+    const int prio = lane[i] == tl ? 0 : (lane[i] == tl - 1 ? 1 : 2);
+    atomicMax(&bid[target[i]], bid_word(1ULL, prio, i));
+}
+__global__ void k_res_init(const uint8_t* active, const int* target, const int* occ, const unsigned long long* bid,
+                           int n, int* st) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int s = -2;
+    if (active[i]) {
+        if (target[i] == kExit) {
+            s = -1;
+        } else if (target[i] >= 0) {
+            int ws, wp;
+            if (bid_winner(bid[target[i]], 1ULL, ws, wp) && ws == i) s = occ[target[i]] < 0 ? -1 : occ[target[i]];
+        }
+    }
+    st[i] = s;
+}
+__global__ void k_res_jump(const int* st, int* out, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int s = st[i];
+    out[i] = s >= 0 ? st[s] : s;
+}
+__global__ void k_res_out(const int* st, int n, uint8_t* acc) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) acc[i] = st[i] == -1 ? 1 : 0;
+}
+
+// ---------------------------------------------------------------- init / flush
+__global__ void k_init(TParams P) {
+    const size_t ns = static_cast<size_t>(P.R) * P.Npad, nc = static_cast<size_t>(P.R) * P.Cpad;
+    for (size_t q = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < (ns > nc ? ns : nc);
+         q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        if (q < ns) {
+            P.active[q] = 0;
+            P.pos[q] = 0;
+            P.ids[q] = 0;
+            P.ages[q] = 0;
+        }
+        if (q < nc) {
+            P.occ[q] = -1;
+            P.bid[q] = 0ULL;
+            P.acc[q] = 0;
+        }
+    }
+}
+
+}  // namespace abmx_trf
+
+// ====================================================================== host engine
+using namespace abmx_trf;
+
+#define CKT(x)                                                                        \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            abmx_internal::set_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+            return ABMX_E_CUDA;                                                       \
+        }                                                                             \
+    } while (0)
+
+struct abmx_traffic {
+    abmx_traffic_config cfg{};
+    int R = 0;
+    TParams P{};
+    cudaStream_t stream = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t nodes[kNumKernels] = {};
+    std::vector<void*> allocs;
+    double* d_metrics_step = nullptr;  // [R][1][4]
+    double* d_run_metrics = nullptr;
+    size_t run_metrics_bytes = 0;
+    long long last_run_steps = 0;
+    unsigned long long host_epoch = 1;
+    double kernel_ms[kNumKernels] = {};
+    long long kernel_launches[kNumKernels] = {};
+    void* flush_buf = nullptr;
+    size_t flush_cap = 0;
+    long long* h_cnt = nullptr;  // pinned copy of the counters
+
+    ~abmx_traffic() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        for (void* p : allocs) cudaFree(p);
+        if (d_run_metrics) cudaFree(d_run_metrics);
+        if (flush_buf) cudaFree(flush_buf);
+        if (h_cnt) cudaFreeHost(h_cnt);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    int alloc(void** p, size_t bytes) {
+        cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+        if (e != cudaSuccess) {
+            abmx_internal::set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+            return ABMX_E_CUDA;
+        }
+        allocs.push_back(*p);
+        return ABMX_OK;
+    }
+    unsigned grid(int k) const {
+        if (k == 1) return static_cast<unsigned>(R * P.ctiles);
+        if (k == 3) return static_cast<unsigned>(R);
+        return static_cast<unsigned>(R * P.tiles);
+    }
+    unsigned block(int k) const { return k == 3 ? 32u : static_cast<unsigned>(kT); }
+    static void* fn(int k) {
+        static void* const f[kNumKernels] = {reinterpret_cast<void*>(k_propose), reinterpret_cast<void*>(k_accept),
+                                             reinterpret_cast<void*>(k_apply), reinterpret_cast<void*>(k_spawn)};
+        return f[k];
+    }
+
+    int create(const abmx_traffic_config& c, const uint64_t* seeds, int roads) {
+        cfg = c;
+        R = roads;
+        if (R < 1) {
+            abmx_internal::set_error("roads must be >= 1");
+            return ABMX_E_DOMAIN;
+        }
+        if (c.period < 1) {
+            abmx_internal::set_error("signal period must be >= 1");  // traffic.cpp:9-10
+            return ABMX_E_DOMAIN;
+        }
+        if (c.length < 1) {
+            abmx_internal::set_error("road length must be >= 1");  // traffic.cpp:21-22
+            return ABMX_E_DOMAIN;
+        }
+        if (c.length > (1 << 26)) {
+            abmx_internal::set_error("road length above 2^26 cells per lane (28-bit slots)");
+            return ABMX_E_CAPACITY;
+        }
+        CKT(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        memset(&P, 0, sizeof P);
+        P.R = R;
+        P.L = static_cast<int>(c.length);
+        P.C = 3 * P.L;
+        P.Cpad = (P.C + 15) / 16 * 16;
+        P.Npad = (P.C + kTile - 1) / kTile * kTile;
+        P.tiles = P.Npad / kTile;
+        P.ctiles = (P.L + kCT - 1) / kCT;
+        P.period = c.period;
+        long long gl = llround(static_cast<double>(c.period) * c.green_fraction);  // traffic.cpp:11-13
+        P.green_len = gl < 0 ? 0 : (gl > c.period ? c.period : gl);
+        int rc;
+        const size_t ns = static_cast<size_t>(R) * P.Npad, nc = static_cast<size_t>(R) * P.Cpad;
+#define ALT(ptr, bytes)                                                 \
+    if ((rc = alloc(reinterpret_cast<void**>(&(ptr)), (bytes))) != 0) \
+        return rc;
+        ALT(P.active, ns);
+        ALT(P.pos, ns * 4);
+        ALT(P.ids, ns * 8);
+        ALT(P.ages, ns * 8);
+        ALT(P.occ, nc * 4);
+        ALT(P.bid, nc * 8);
+        ALT(P.acc, nc);
+        ALT(P.cstatus, static_cast<size_t>(R) * P.ctiles * 8);
+        ALT(P.ticket, 16);
+        ALT(P.tinfo, static_cast<size_t>(R) * P.tiles * sizeof(int4));
+        ALT(P.cnt, static_cast<size_t>(R) * 8 * 8);
+        long long* phase = nullptr;
+        unsigned long long* sd = nullptr;
+        ALT(phase, static_cast<size_t>(R) * 8);
+        ALT(sd, static_cast<size_t>(R) * 8);
+        ALT(d_metrics_step, static_cast<size_t>(R) * 4 * 8);
+#undef ALT
+        P.phase = phase;
+        P.seeds = sd;
+        std::vector<long long> ph(static_cast<size_t>(R));
+        for (int r = 0; r < R; ++r) {  // phase = seed.split(TrafficSignal).uniform_int(0, 0, period)
+            const unsigned long long k = abmx_dev::split(seeds[r], 5);
+            const unsigned long long d = abmx_dev::draw(k, 0);
+            ph[static_cast<size_t>(r)] = static_cast<long long>(
+                static_cast<unsigned long long>((static_cast<unsigned __int128>(d) * static_cast<unsigned long long>(c.period)) >> 64));
+        }
+        CKT(cudaMemcpy(phase, ph.data(), ph.size() * 8, cudaMemcpyHostToDevice));
+        CKT(cudaMemcpy(sd, seeds, static_cast<size_t>(R) * 8, cudaMemcpyHostToDevice));
+        CKT(cudaMemset(P.cstatus, 0, static_cast<size_t>(R) * P.ctiles * 8));
+        CKT(cudaMemset(P.ticket, 0, 16));
+        CKT(cudaMemset(P.cnt, 0, static_cast<size_t>(R) * 64));
+        CKT(cudaMemset(d_metrics_step, 0, static_cast<size_t>(R) * 32));
+        CKT(cudaMallocHost(&h_cnt, static_cast<size_t>(R) * 64));
+        (void)cudaGetLastError();
+        k_init<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(P);
+        abmx_internal::count_launch();
+        CKT(cudaGetLastError());
+        CKT(cudaStreamSynchronize(stream));
+        P.metrics = d_metrics_step;
+        P.metrics_stride = 1;
+        return ABMX_OK;
+    }
+
+    int build_graph() {
+        CKT(cudaGraphCreate(&graph, 0));
+        void* args[1] = {&P};
+        cudaGraphNode_t prev = nullptr;
+        for (int k = 0; k < kNumKernels; ++k) {
+            cudaKernelNodeParams kp{};
+            kp.func = fn(k);
+            kp.gridDim = dim3(grid(k));
+            kp.blockDim = dim3(block(k));
+            kp.kernelParams = args;
+            CKT(cudaGraphAddKernelNode(&nodes[k], graph, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+            prev = nodes[k];
+        }
+        CKT(cudaGraphInstantiate(&exec, graph, 0));
+        return ABMX_OK;
+    }
+
+    int enqueue(cudaEvent_t* ev) {
+        P.epoch = host_epoch;
+        void* args[1] = {&P};
+        if (ev) {
+            for (int k = 0; k < kNumKernels; ++k) {
+                CKT(cudaEventRecord(ev[2 * k], stream));
+                CKT(cudaLaunchKernel(fn(k), dim3(grid(k)), dim3(block(k)), args, 0, stream));
+                CKT(cudaEventRecord(ev[2 * k + 1], stream));
+            }
+        } else {
+            if (!exec) {
+                int rc = build_graph();
+                if (rc) return rc;
+            }
+            for (int k = 0; k < kNumKernels; ++k) {
+                cudaKernelNodeParams kp{};
+                kp.func = fn(k);
+                kp.gridDim = dim3(grid(k));
+                kp.blockDim = dim3(block(k));
+                kp.kernelParams = args;
+                CKT(cudaGraphExecKernelNodeSetParams(exec, nodes[k], &kp));
+            }
+            CKT(cudaGraphLaunch(exec, stream));
+        }
+        abmx_internal::count_launch(kNumKernels);
+        ++host_epoch;
+        ++P.t;
+        ++P.run_step;
+        return ABMX_OK;
+    }
+
+    int step(long long t) {
+        P.metrics = d_metrics_step;
+        P.metrics_stride = 1;
+        P.run_step = 0;
+        P.t = t;
+        (void)cudaGetLastError();
+        int rc = enqueue(nullptr);
+        if (rc) return rc;
+        last_run_steps = 0;
+        CKT(cudaGetLastError());
+        return ABMX_OK;
+    }
+
+    int prepare_run(long long t0, long long steps) {
+        const size_t mb = static_cast<size_t>(R) * static_cast<size_t>(steps) * 32;
+        if (mb > run_metrics_bytes) {
+            CKT(cudaStreamSynchronize(stream));
+            if (d_run_metrics) cudaFree(d_run_metrics);
+            CKT(cudaMalloc(&d_run_metrics, mb));
+            run_metrics_bytes = mb;
+        }
+        P.metrics = d_run_metrics;
+        P.metrics_stride = static_cast<unsigned>(steps);
+        P.run_step = 0;
+        P.t = t0;
+        return ABMX_OK;
+    }
+
+    int run(long long t0, long long steps, double* out) {
+        if (steps <= 0) return ABMX_OK;
+        if (steps > 0x7FFFFFFFLL) {
+            abmx_internal::set_error("too many steps in one run");
+            return ABMX_E_DOMAIN;
+        }
+        int rc = prepare_run(t0, steps);
+        if (rc) return rc;
+        (void)cudaGetLastError();
+        for (long long q = 0; q < steps; ++q) {
+            rc = enqueue(nullptr);
+            if (rc) return rc;
+        }
+        last_run_steps = steps;
+        if (out) {
+            CKT(cudaMemcpyAsync(out, d_run_metrics, static_cast<size_t>(R) * steps * 32, cudaMemcpyDeviceToHost, stream));
+            CKT(cudaStreamSynchronize(stream));
+        }
+        return ABMX_OK;
+    }
+
+    int metrics(double* out) {
+        if (last_run_steps == 0) {
+            CKT(cudaMemcpyAsync(out, d_metrics_step, static_cast<size_t>(R) * 32, cudaMemcpyDeviceToHost, stream));
+        } else {
+            for (int r = 0; r < R; ++r)
+                CKT(cudaMemcpyAsync(out + static_cast<size_t>(r) * 4,
+                                    d_run_metrics + (static_cast<size_t>(r) * last_run_steps + last_run_steps - 1) * 4,
+                                    32, cudaMemcpyDeviceToHost, stream));
+        }
+        CKT(cudaStreamSynchronize(stream));
+        return ABMX_OK;
+    }
+
+    int counters(int r, long long* out8) {
+        CKT(cudaMemcpyAsync(h_cnt, P.cnt + static_cast<size_t>(r) * 8, 64, cudaMemcpyDeviceToHost, stream));
+        CKT(cudaStreamSynchronize(stream));
+        memcpy(out8, h_cnt, 64);
+        return ABMX_OK;
+    }
+
+    int export_road(int r, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* lane, int64_t* cell,
+                    int32_t* occupancy, int64_t* next_id, int32_t* num_active) {
+        const size_t n = static_cast<size_t>(P.C);
+        const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
+        std::vector<int> pos(n);
+        long long cn[8];
+        CKT(cudaMemcpyAsync(active, P.active + sb, n, cudaMemcpyDeviceToHost, stream));
+        CKT(cudaMemcpyAsync(ids, P.ids + sb, n * 8, cudaMemcpyDeviceToHost, stream));
+        CKT(cudaMemcpyAsync(ages, P.ages + sb, n * 8, cudaMemcpyDeviceToHost, stream));
+        CKT(cudaMemcpyAsync(pos.data(), P.pos + sb, n * 4, cudaMemcpyDeviceToHost, stream));
+        if (occupancy) CKT(cudaMemcpyAsync(occupancy, P.occ + cb, n * 4, cudaMemcpyDeviceToHost, stream));
+        CKT(cudaMemcpyAsync(cn, P.cnt + static_cast<size_t>(r) * 8, 64, cudaMemcpyDeviceToHost, stream));
+        CKT(cudaStreamSynchronize(stream));
+        for (size_t i = 0; i < n; ++i) {
+            lane[i] = pos[i] / P.L;
+            cell[i] = pos[i] % P.L;
+        }
+        if (next_id) *next_id = cn[1];
+        if (num_active) *num_active = static_cast<int32_t>(cn[0]);
+        return ABMX_OK;
+    }
+
+    int import_road(int r, const uint8_t* active, const int64_t* ids, const int64_t* ages, const int64_t* lane,
+                    const int64_t* cell, int64_t next_id) {
+        const size_t n = static_cast<size_t>(P.C);
+        std::vector<uint8_t> act(n);
+        std::vector<int> pos(n), occ(static_cast<size_t>(P.Cpad), -1);
+        long long na = 0;
+        for (size_t i = 0; i < n; ++i) {
+            act[i] = active[i] ? 1 : 0;
+            if (lane[i] < 0 || lane[i] > 2 || cell[i] < 0 || cell[i] >= P.L) {
+                abmx_internal::set_error("car position outside the road");
+                return ABMX_E_DOMAIN;
+            }
+            pos[i] = static_cast<int>(lane[i] * P.L + cell[i]);
+            if (act[i]) {
+                if (occ[static_cast<size_t>(pos[i])] != -1) {
+                    abmx_internal::set_error("two cars occupy one road cell");  // traffic.cpp:40-41
+                    return ABMX_E_DOMAIN;
+                }
+                occ[static_cast<size_t>(pos[i])] = static_cast<int>(i);
+                ++na;
+            }
+        }
+        const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
+        CKT(cudaStreamSynchronize(stream));
+        CKT(cudaMemcpy(P.active + sb, act.data(), n, cudaMemcpyHostToDevice));
+        CKT(cudaMemcpy(P.ids + sb, ids, n * 8, cudaMemcpyHostToDevice));
+        CKT(cudaMemcpy(P.ages + sb, ages, n * 8, cudaMemcpyHostToDevice));
+        CKT(cudaMemcpy(P.pos + sb, pos.data(), n * 4, cudaMemcpyHostToDevice));
+        CKT(cudaMemcpy(P.occ + cb, occ.data(), static_cast<size_t>(P.Cpad) * 4, cudaMemcpyHostToDevice));
+        long long cn[8];
+        CKT(cudaMemcpy(cn, P.cnt + static_cast<size_t>(r) * 8, 64, cudaMemcpyDeviceToHost));
+        cn[0] = na;
+        cn[1] = next_id;
+        cn[5] = 0;
+        CKT(cudaMemcpy(P.cnt + static_cast<size_t>(r) * 8, cn, 64, cudaMemcpyHostToDevice));
+        return ABMX_OK;
+    }
+
+    int bench(long long t0, long long steps, size_t flush_bytes, bool per_kernel, double* step_ms) {
+        if (steps <= 0) return ABMX_OK;
+        int rc = prepare_run(t0, steps);
+        if (rc) return rc;
+        if (flush_bytes > flush_cap) {
+            if (flush_buf) cudaFree(flush_buf);
+            CKT(cudaMalloc(&flush_buf, flush_bytes));
+            flush_cap = flush_bytes;
+        }
+        const size_t per = per_kernel ? 2 * kNumKernels : 2;
+        std::vector<cudaEvent_t> ev(per * static_cast<size_t>(steps));
+        for (auto& e : ev) CKT(cudaEventCreate(&e));
+        (void)cudaGetLastError();
+        for (long long q = 0; q < steps; ++q) {
+            if (flush_bytes) CKT(cudaMemsetAsync(flush_buf, static_cast<int>(q & 0xFF), flush_bytes, stream));
+            cudaEvent_t* e = &ev[per * static_cast<size_t>(q)];
+            if (per_kernel) {
+                rc = enqueue(e);
+            } else {
+                CKT(cudaEventRecord(e[0], stream));
+                rc = enqueue(nullptr);
+                CKT(cudaEventRecord(e[1], stream));
+            }
+            if (rc) return rc;
+        }
+        CKT(cudaStreamSynchronize(stream));
+        for (long long q = 0; q < steps; ++q) {
+            cudaEvent_t* e = &ev[per * static_cast<size_t>(q)];
+            float ms = 0.f;
+            if (per_kernel) {
+                double tot = 0.0;
+                for (int k = 0; k < kNumKernels; ++k) {
+                    CKT(cudaEventElapsedTime(&ms, e[2 * k], e[2 * k + 1]));
+                    kernel_ms[k] += ms;
+                    kernel_launches[k] += 1;
+                    tot += ms;
+                }
+                step_ms[q] = tot;
+            } else {
+                CKT(cudaEventElapsedTime(&ms, e[0], e[1]));
+                step_ms[q] = ms;
+            }
+        }
+        for (auto& e : ev) cudaEventDestroy(e);
+        last_run_steps = steps;
+        return ABMX_OK;
+    }
+};
+
+namespace {
+const char* kTrafficKernels[kNumKernels] = {"k_propose", "k_accept", "k_apply", "k_spawn"};
+
+int resolve_host(int64_t length, const uint8_t* active, const int64_t* lane, const int64_t* cell, const uint8_t* kind,
+                 const int64_t* to_lane, const int64_t* to_cell, uint8_t* accepted) {
+    if (length < 1) {
+        abmx_internal::set_error("road length must be >= 1");
+        return ABMX_E_DOMAIN;
+    }
+    const int L = static_cast<int>(length), n = 3 * L;
+    std::vector<uint8_t> act(static_cast<size_t>(n));
+    std::vector<int> ln(static_cast<size_t>(n)), tg(static_cast<size_t>(n)), occ(static_cast<size_t>(n), -1);
+    for (int i = 0; i < n; ++i) {
+        act[i] = active[i] ? 1 : 0;
+        ln[i] = static_cast<int>(lane[i]);
+        tg[i] = kStay;
+        if (!act[i]) continue;
+        if (lane[i] < 0 || lane[i] > 2 || cell[i] < 0 || cell[i] >= length) {
+            abmx_internal::set_error("car position outside the road");
+            return ABMX_E_DOMAIN;
+        }
+        const int p = static_cast<int>(lane[i] * length + cell[i]);
+        if (occ[p] != -1) {
+            abmx_internal::set_error("two cars occupy one road cell");
+            return ABMX_E_DOMAIN;
+        }
+        occ[p] = i;
+        if (kind[i] == 2) {
+            tg[i] = kExit;
+        } else if (kind[i] == 1) {
+            if (to_lane[i] < 0 || to_lane[i] >= 3 || to_cell[i] < 0 || to_cell[i] >= length) {
+                abmx_internal::set_error("move proposal targets a cell outside the road");  // traffic.cpp:104-106
+                return ABMX_E_CONTRACT;
+            }
+            tg[i] = static_cast<int>(to_lane[i] * length + to_cell[i]);
+        }
+    }
+    cudaStream_t s;
+    CKT(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    uint8_t *d_act = nullptr, *d_acc = nullptr;
+    int *d_lane = nullptr, *d_tg = nullptr, *d_occ = nullptr, *d_a = nullptr, *d_b = nullptr;
+    unsigned long long* d_bid = nullptr;
+    const size_t N = static_cast<size_t>(n);
+    int rc = ABMX_OK;
+    auto fail = [&](cudaError_t e) {
+        abmx_internal::set_error(std::string("resolve: ") + cudaGetErrorString(e));
+        rc = ABMX_E_CUDA;
+    };
+    cudaError_t e = cudaSuccess;
+    if ((e = cudaMallocAsync(&d_act, N, s)) || (e = cudaMallocAsync(&d_acc, N, s)) ||
+        (e = cudaMallocAsync(&d_lane, N * 4, s)) || (e = cudaMallocAsync(&d_tg, N * 4, s)) ||
+        (e = cudaMallocAsync(&d_occ, N * 4, s)) || (e = cudaMallocAsync(&d_a, N * 4, s)) ||
+        (e = cudaMallocAsync(&d_b, N * 4, s)) || (e = cudaMallocAsync(&d_bid, N * 8, s))) {
+        fail(e);
+    } else {
+        cudaMemcpyAsync(d_act, act.data(), N, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_lane, ln.data(), N * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_tg, tg.data(), N * 4, cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(d_occ, occ.data(), N * 4, cudaMemcpyHostToDevice, s);
+        cudaMemsetAsync(d_bid, 0, N * 8, s);
+        const int g = (n + 255) / 256;
+        k_res_bid<<<g, 256, 0, s>>>(d_act, d_lane, d_tg, n, L, d_bid);
+        k_res_init<<<g, 256, 0, s>>>(d_act, d_tg, d_occ, d_bid, n, d_a);
+        int rounds = 1;
+        while ((1 << rounds) < n + 1) ++rounds;
+        for (int q = 0; q <= rounds; ++q) {
+            k_res_jump<<<g, 256, 0, s>>>(d_a, d_b, n);
+            int* tmp = d_a;
+            d_a = d_b;
+            d_b = tmp;
+        }
+        k_res_out<<<g, 256, 0, s>>>(d_a, n, d_acc);
+        abmx_internal::count_launch(rounds + 4);
+        if ((e = cudaGetLastError()) != cudaSuccess) fail(e);
+        cudaMemcpyAsync(accepted, d_acc, N, cudaMemcpyDeviceToHost, s);
+        if ((e = cudaStreamSynchronize(s)) != cudaSuccess) fail(e);
+    }
+    cudaFreeAsync(d_act, s);
+    cudaFreeAsync(d_acc, s);
+    cudaFreeAsync(d_lane, s);
+    cudaFreeAsync(d_tg, s);
+    cudaFreeAsync(d_occ, s);
+    cudaFreeAsync(d_a, s);
+    cudaFreeAsync(d_b, s);
+    cudaFreeAsync(d_bid, s);
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    return rc;
+}
+}  // namespace
+
+#define HANDLE_T(h)                                   \
+    if (!(h)) {                                       \
+        abmx_internal::set_error("null traffic handle"); \
+        return ABMX_E_ARG;                            \
+    }
+
+extern "C" {
+
+int abmx_traffic_create(const abmx_traffic_config* cfg, const uint64_t* seeds, int32_t roads, abmx_traffic** out) {
+    if (!cfg || !seeds || !out) {
+        abmx_internal::set_error("null argument");
+        return ABMX_E_ARG;
+    }
+    auto* h = new abmx_traffic();
+    const int rc = h->create(*cfg, seeds, roads);
+    if (rc) {
+        delete h;
+        *out = nullptr;
+        return rc;
+    }
+    *out = h;
+    return ABMX_OK;
+}
+int abmx_traffic_destroy(abmx_traffic* h) {
+    delete h;
+    return ABMX_OK;
+}
+int abmx_traffic_step(abmx_traffic* h, int64_t t) {
+    HANDLE_T(h);
+    return h->step(t);
+}
+int abmx_traffic_run(abmx_traffic* h, int64_t t0, int64_t steps, double* metrics_out) {
+    HANDLE_T(h);
+    return h->run(t0, steps, metrics_out);
+}
+int abmx_traffic_sync(abmx_traffic* h) {
+    HANDLE_T(h);
+    CKT(cudaStreamSynchronize(h->stream));
+    return ABMX_OK;
+}
+int abmx_traffic_metrics(abmx_traffic* h, double* out) {
+    HANDLE_T(h);
+    return h->metrics(out);
+}
+int abmx_traffic_totals(abmx_traffic* h, int32_t road, int64_t* spawned_total, int64_t* exited_total) {
+    HANDLE_T(h);
+    if (road < 0 || road >= h->R) {
+        abmx_internal::set_error("road index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    long long cn[8];
+    int rc = h->counters(road, cn);
+    if (rc) return rc;
+    if (spawned_total) *spawned_total = cn[2];
+    if (exited_total) *exited_total = cn[3];
+    return ABMX_OK;
+}
+int abmx_traffic_schedule(abmx_traffic* h, int32_t road, int64_t* period, int64_t* green_len, int64_t* phase) {
+    HANDLE_T(h);
+    if (road < 0 || road >= h->R) {
+        abmx_internal::set_error("road index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    long long ph = 0;
+    CKT(cudaMemcpy(&ph, h->P.phase + road, 8, cudaMemcpyDeviceToHost));
+    if (period) *period = h->P.period;
+    if (green_len) *green_len = h->P.green_len;
+    if (phase) *phase = ph;
+    return ABMX_OK;
+}
+int abmx_traffic_export(abmx_traffic* h, int32_t road, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* lane,
+                        int64_t* cell, int32_t* occupancy, int64_t* next_id, int32_t* num_active) {
+    HANDLE_T(h);
+    if (road < 0 || road >= h->R) {
+        abmx_internal::set_error("road index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    return h->export_road(road, active, ids, ages, lane, cell, occupancy, next_id, num_active);
+}
+int abmx_traffic_import(abmx_traffic* h, int32_t road, const uint8_t* active, const int64_t* ids, const int64_t* ages,
+                        const int64_t* lane, const int64_t* cell, int64_t next_id) {
+    HANDLE_T(h);
+    if (road < 0 || road >= h->R) {
+        abmx_internal::set_error("road index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    return h->import_road(road, active, ids, ages, lane, cell, next_id);
+}
+int abmx_traffic_resolve(int64_t length, const uint8_t* active, const int64_t* lane, const int64_t* cell,
+                         const uint8_t* kind, const int64_t* to_lane, const int64_t* to_cell, uint8_t* accepted) {
+    return resolve_host(length, active, lane, cell, kind, to_lane, to_cell, accepted);
+}
+int abmx_traffic_bench(abmx_traffic* h, int64_t t0, int64_t steps, int64_t flush_bytes, int32_t per_kernel,
+                       double* step_ms) {
+    HANDLE_T(h);
+    return h->bench(t0, steps, static_cast<size_t>(flush_bytes > 0 ? flush_bytes : 0), per_kernel != 0, step_ms);
+}
+int32_t abmx_traffic_kernel_count(void) { return kNumKernels; }
+const char* abmx_traffic_kernel_name(int32_t k) { return (k >= 0 && k < kNumKernels) ? kTrafficKernels[k] : ""; }
+int abmx_traffic_kernel_times(abmx_traffic* h, double* ms, int64_t* launches) {
+    HANDLE_T(h);
+    for (int k = 0; k < kNumKernels; ++k) {
+        if (ms) ms[k] = h->kernel_ms[k];
+        if (launches) launches[k] = h->kernel_launches[k];
+    }
+    return ABMX_OK;
+}
+int abmx_traffic_run_batch(const abmx_traffic_config* cfg, uint64_t master, int32_t replica_begin, int32_t count,
+                           int64_t steps, double* metrics_out, double* kernel_ms) {
+    if (!cfg || count < 0) {
+        abmx_internal::set_error("bad run_batch arguments");
+        return ABMX_E_ARG;
+    }
+    if (count == 0 || steps <= 0) return ABMX_OK;
+    std::vector<uint64_t> seeds(static_cast<size_t>(count));
+    const unsigned long long base = abmx_dev::split(master, 2);  // batch.cpp:12-19
+    for (int32_t q = 0; q < count; ++q) seeds[static_cast<size_t>(q)] = abmx_dev::split(base, static_cast<unsigned long long>(replica_begin + q));
+    abmx_traffic* h = nullptr;
+    int rc = abmx_traffic_create(cfg, seeds.data(), count, &h);
+    if (rc) return rc;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, h->stream);
+    rc = h->run(1, steps, nullptr);
+    cudaEventRecord(b, h->stream);
+    if (!rc && metrics_out) {
+        cudaError_t e = cudaMemcpyAsync(metrics_out, h->d_run_metrics, static_cast<size_t>(count) * steps * 32,
+                                        cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            abmx_internal::set_error(std::string("run_batch: ") + cudaGetErrorString(e));
+            rc = ABMX_E_CUDA;
+        }
+    }
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (kernel_ms) *kernel_ms = ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    abmx_traffic_destroy(h);
+    return rc;
+}
+
+}  // extern "C"

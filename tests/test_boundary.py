@@ -75,8 +75,10 @@ def test_host_seed_plumbing_matches_oracle(oracle):
 
 def test_error_taxonomy():
     import paper_2508_16508_b200 as m
-    for e in (m.SchemaError, m.CapacityError, m.DomainError, m.BatchError, m.CudaError):
+    for e in (m.SchemaError, m.CapacityError, m.DomainError, m.BatchError, m.CudaError,
+              m.ContractError):
         assert issubclass(e, m.AbmxError)
+    assert m._ERRORS[7] is m.ContractError
     assert m._ERRORS[1] is m.DomainError and m._ERRORS[2] is m.CapacityError
 
 
