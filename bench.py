@@ -149,6 +149,67 @@ def reference_arm(args, world):
     print(json.dumps(line))
 
 
+
+# ---------------------------------------------------------------------- traffic (§8f rank 1)
+TRAFFIC_L = 349_526          # C4: one road, capacity 3L = 1,048,578 slots
+ROADS, ROADS_L, ROADS_STEPS = 3496, 100, 1000  # C4 roads variant (paper Table 3 shape)
+
+
+def traffic_section(args, rank, world, allreduce, dist):
+    """C4 on the device: one long road per rank (device-timed steps, L2 flushed), the roads
+    variant sharded by contiguous road blocks, and the reference CPU on bounded samples."""
+    import numpy as np
+    import paper_2508_16508_b200 as abmx
+    from paper_2508_16508_b200 import traffic as T
+    K, W = args.steps, args.warmup
+    seed = abmx.replica_seeds(MASTER_SEED, world)[rank]
+    m = T.TrafficModel(T.TrafficConfig(TRAFFIC_L, 10, 0.5), seed)
+    m.bench(1, W, FLUSH_BYTES)
+    step_ms = m.bench(W + 1, K, FLUSH_BYTES)
+    tot = allreduce(float(np.sum(step_ms)), dist.ReduceOp.MAX if dist else None)
+    m.bench(W + K + 1, max(3, min(K, 10)), FLUSH_BYTES, per_kernel=True)
+    kt = {k: v[0] / max(v[1], 1) for k, v in m.kernel_times().items()}
+    m.close()
+    cap = 3 * TRAFFIC_L
+    alg = 26 * cap  # SURVEY §8d: 2N(lane 4 + cell 4 + active 1) + 2(3L)(occupancy 4)
+    per = ROADS // world
+    begin = rank * per
+    count = per if rank < world - 1 else ROADS - begin
+    T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, min(count, 64), 5, begin=begin)
+    _, rk = T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS,
+                        begin=begin)
+    rk = allreduce(rk, dist.ReduceOp.MAX if dist else None)
+    out = {"workload": f"C4: one road L={TRAFFIC_L} (capacity {cap} slots) per GPU, period 10, "
+                       f"green 0.5, seed {MASTER_SEED}",
+           "value": world * cap * K / (tot / 1e3), "unit": UNIT, "ms_per_step": tot / K,
+           "per_kernel_ms": kt,
+           "step_effective_gbs": alg / (tot / K / 1e3) / 1e9,
+           "roads": {"workload": f"{ROADS} roads x L={ROADS_L}, {ROADS_STEPS} steps (run_batch)",
+                     "value": ROADS * 3 * ROADS_L * ROADS_STEPS / (rk / 1e3), "unit": UNIT,
+                     "device_ms": rk}}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+        if os.path.exists(pyoracle.REF_SO):
+            ref = pyoracle.Reference()
+            r = ref.traffic(TRAFFIC_L, 10, 0.5, seed)
+            n = 20
+            wall = r.run(1, n)
+            out["cpu_baseline"] = {"value": cap * n / (wall / 1e3), "unit": UNIT, "cores": 1,
+                                   "kind": "reference",
+                                   "sample": f"reference TrafficModel::step, C4 steps 1..{n}, "
+                                             f"1 thread ({wall / 1e3:.1f} s)"}
+            threads = os.cpu_count() or 1
+            ns = 300
+            _, wall_b = ref.traffic_run_batch(ROADS_L, 10, 0.5, MASTER_SEED, ROADS, ns,
+                                              threads=threads)
+            out["roads"]["cpu_baseline"] = {
+                "value": ROADS * 3 * ROADS_L * ns / (wall_b / 1e3), "unit": UNIT, "cores": threads,
+                "kind": "reference",
+                "sample": f"reference run_batch(TrafficModel), {ROADS} roads x {ns} steps, "
+                          f"{threads} threads ({wall_b / 1e3:.1f} s)"}
+    return out
+
 # ---------------------------------------------------------------------- our arm
 def kernel_bytes(cfg, births, deaths):
     """SURVEY §8d algorithmic bytes per step, B = 42*N_tot + 2*C + 8*(births+deaths),
@@ -293,6 +354,8 @@ def our_arm(args, rank, world, local_rank, dist):
                "note": "state stays on chip for all steps; effective GB/s uses SURVEY §8d bytes "
                        "and may exceed HBM peak"}
 
+    traffic = None if args.no_traffic else traffic_section(args, rank, world, allreduce, dist)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -317,7 +380,7 @@ def our_arm(args, rank, world, local_rank, dist):
                            "timing": "CUDA events per step on the engine stream; max over ranks"},
                 "live_agent_steps_per_s": live_all / (max_ms / 1e3),
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-                "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens}
+                "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens, "traffic": traffic}
         print(json.dumps(line))
 
 
@@ -330,6 +393,7 @@ def main():
     ap.add_argument("--cpu-steps", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ensemble", action="store_true")
+    ap.add_argument("--no-traffic", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rules: >= 3 warm-up steps

@@ -302,6 +302,11 @@ int abmx_traffic_kernel_times(abmx_traffic* h, double* ms, int64_t* launches);
 int abmx_traffic_run_batch(const abmx_traffic_config* cfg, uint64_t master,
                            int32_t replica_begin, int32_t count, int64_t steps,
                            double* metrics_out, double* kernel_ms);
+/* the same with an explicit path: 0 auto, 1 one shared-memory-resident CTA per road (roads up
+ * to 3*length <= 32767 cells), 2 the batched HBM engine */
+int abmx_traffic_run_batch_path(const abmx_traffic_config* cfg, uint64_t master,
+                                int32_t replica_begin, int32_t count, int64_t steps,
+                                int32_t path, double* metrics_out, double* kernel_ms);
 
 #ifdef __cplusplus
 }

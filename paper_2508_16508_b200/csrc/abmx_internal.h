@@ -7,6 +7,8 @@
 
 #include <cuda_runtime.h>
 
+#include "../../include/abmx_cuda.h"
+
 namespace abmx_internal {
 
 int num_sms();
@@ -27,5 +29,10 @@ cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_
 template <class T>
 cudaError_t launch_blend(const uint8_t* d_mask, const T* d_a, const T* d_b, T* d_out, size_t n,
                          cudaStream_t s);
+
+// traffic run_batch on the SMEM-resident path (traffic_ens.cu)
+bool traffic_ens_fits(const struct abmx_traffic_config& cfg);
+int traffic_ensemble_run(const struct abmx_traffic_config& cfg, const uint64_t* seeds, int count, long long steps,
+                         double* metrics_out, double* kernel_ms);
 
 }  // namespace abmx_internal

@@ -36,15 +36,14 @@ using namespace abmx_dev;
 
 namespace abmx_trf {
 
-constexpr int kT = 256;
+// CTA sizes are template parameters chosen per road length at create(): slot kernels use
+// NT threads x kS slots per CTA, k_accept NA threads x kCI columns per CTA (short roads get small
+// CTAs, long roads large ones so the decoupled lookback crosses few tiles).
 constexpr int kS = 4;
-constexpr int kTile = kT * kS;  // slots per CTA (k_propose, k_apply)
-constexpr int kCI = 16;         // columns per thread (k_accept)
-constexpr int kCT = kT * kCI;   // columns per CTA
+constexpr int kCI = 4;  // columns per thread in k_accept: one int4 of occupants per lane
 constexpr unsigned kSlotMask = (1u << 28) - 1;
 constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagPre = 2ULL << 62;
-constexpr unsigned kIdentity = 0 | (1 << 3) | (2 << 6) | (3 << 9) | (4 << 12) | (5 << 15) | (6 << 18) | (7 << 21);
 constexpr int kNumKernels = 4;
 
 enum : int { kStay = -1, kExit = -2 };
@@ -56,7 +55,8 @@ struct TParams {
     double* metrics;  // [R][metrics_stride][4]
     unsigned run_step, metrics_stride;
     // constants
-    int R, L, C, Cpad, Npad, tiles, ctiles;
+    int R, L, Lp, C, Cpad, Npad, tiles, ctiles;  // C = 3L slots; cells lane*Lp + cell
+    int tile_slots, tile_cols;                  // slots per slot-kernel CTA, columns per k_accept CTA
     long long period, green_len;
     const long long* phase;
     const unsigned long long* seeds;
@@ -82,12 +82,12 @@ __device__ __forceinline__ unsigned long long propose_key(const TParams& P, int 
 }
 // target cell index of car `slot` at cell index p, or kStay / kExit (traffic.cpp:57-79)
 __device__ __forceinline__ int proposal(const TParams& P, int slot, int p, bool green, unsigned long long key) {
-    const int lane = p / P.L, cell = p - lane * P.L;
+    const int lane = p / P.Lp, cell = p - lane * P.Lp;
     if (cell == P.L - 1) return green ? kExit : kStay;
     const int n = 1 + (lane > 0) + (lane < 2);
     const int pick = static_cast<int>(uniform_span(key, static_cast<unsigned long long>(slot), static_cast<unsigned long long>(n)));
     const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
-    return tl * P.L + cell + 1;
+    return tl * P.Lp + cell + 1;
 }
 __device__ __forceinline__ unsigned long long bid_word(unsigned long long epoch, int prio, int slot) {
     return (epoch << 32) | (0xFFFFFFFFu - ((static_cast<unsigned>(prio) << 28) | static_cast<unsigned>(slot)));
@@ -102,7 +102,8 @@ __device__ __forceinline__ bool bid_winner(unsigned long long w, unsigned long l
 }
 
 // ---------------------------------------------------------------- k_propose
-__global__ void __launch_bounds__(kT) k_propose(TParams P) {
+template <int NT>
+__global__ void __launch_bounds__(NT) k_propose(TParams P) {
     if (blockIdx.x == 0 && threadIdx.x == 0) P.ticket[P.epoch & 1] = 0u;
     const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
     const bool green = green_of(P, r);
@@ -110,86 +111,113 @@ __global__ void __launch_bounds__(kT) k_propose(TParams P) {
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
 #pragma unroll
     for (int k = 0; k < kS; ++k) {
-        const int i = tile * kTile + k * kT + threadIdx.x;
+        const int i = tile * NT * kS + k * NT + threadIdx.x;
         if (i >= P.C || !P.active[sb + i]) continue;
         const int p = P.pos[sb + i];
         const int X = proposal(P, i, p, green, key);
         if (X < 0) continue;
-        const int lane = p / P.L, tl = X / P.L;
+        const int lane = p / P.Lp, tl = X / P.Lp;
         const int prio = lane == tl ? 0 : (lane == tl - 1 ? 1 : 2);
         atomicMax(&P.bid[cb + X], bid_word(P.epoch, prio, i));
     }
 }
 
 // ---------------------------------------------------------------- k_accept
-__device__ __forceinline__ unsigned fn_at(unsigned f, unsigned x) { return (f >> (3 * x)) & 7u; }
-// (f ∘ g)[x] = f[g[x]]
-__device__ __forceinline__ unsigned compose(unsigned f, unsigned g) {
+// A column map sends each output lane to a constant or to ONE input lane, so it is stored as
+// three 3-bit modes (lane l: 0 never, 1 always, 2 + k: iff input bit k) — 9 bits — and maps
+// compose lane by lane: (f ∘ g)_l = f_l < 2 ? f_l : g_{f_l - 2}.
+constexpr unsigned kIdentityFn = 2u | (3u << 3) | (4u << 6);
+__device__ __forceinline__ unsigned mode_of(unsigned f, int l) { return (f >> (3 * l)) & 7u; }
+__device__ __forceinline__ unsigned compose(unsigned f, unsigned g) {  // f ∘ g
     unsigned h = 0;
 #pragma unroll
-    for (unsigned x = 0; x < 8; ++x) h |= fn_at(f, fn_at(g, x)) << (3 * x);
+    for (int l = 0; l < 3; ++l) {
+        const unsigned m = mode_of(f, l);
+        h |= (m < 2 ? m : mode_of(g, static_cast<int>(m) - 2)) << (3 * l);
+    }
     return h;
 }
-
-// F_c: acceptance bits of column c's occupants as a function of column c+1's. m3 = occupied lanes.
-__device__ unsigned column_fn(const TParams& P, size_t sb, size_t cb, int c, bool green, unsigned long long key,
-                              unsigned& m3) {
-    int mode[3];  // 0: never, 1: always, 2 + tl: iff the occupant of (tl, c+1) moves out
-    m3 = 0;
+__device__ __forceinline__ unsigned apply_fn(unsigned f, unsigned v) {  // f(v), v = 3 bits
+    unsigned out = 0;
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
-        mode[l] = 0;
-        const int o = P.occ[cb + l * P.L + c];
-        if (o < 0) continue;
-        m3 |= 1u << l;
-        const int X = proposal(P, o, l * P.L + c, green, key);
-        if (X == kExit) {
-            mode[l] = 1;
-        } else if (X >= 0) {
-            int ws, wp;
-            if (bid_winner(P.bid[cb + X], P.epoch, ws, wp) && ws == o)
-                mode[l] = P.occ[cb + X] < 0 ? 1 : 2 + X / P.L;
-        }
+        const unsigned m = mode_of(f, l);
+        out |= (m < 2 ? m : (v >> (m - 2)) & 1u) << l;
     }
-    unsigned f = 0;
-#pragma unroll
-    for (unsigned x = 0; x < 8; ++x) {
-        unsigned out = 0;
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            const unsigned b = mode[l] == 0 ? 0u : (mode[l] == 1 ? 1u : (x >> (mode[l] - 2)) & 1u);
-            out |= b << l;
-        }
-        f |= out << (3 * x);
-    }
-    (void)sb;
-    return f;
+    return out;
 }
 
-__global__ void __launch_bounds__(kT) k_accept(TParams P) {
+template <int NA>
+__global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __shared__ unsigned s_tile;
-    __shared__ unsigned s_warp[kT / 32];
+    __shared__ unsigned s_warp[NA / 32];
     __shared__ unsigned s_vin;
-    if (threadIdx.x == 0) s_tile = atomicAdd(&P.ticket[P.epoch & 1], 1u);
+    // tiles of one road depend on their right neighbours: ticket order guarantees progress
+    if (threadIdx.x == 0) s_tile = P.ctiles > 1 ? atomicAdd(&P.ticket[P.epoch & 1], 1u) : blockIdx.x;
     __syncthreads();
     const unsigned g = s_tile;
     const int r = static_cast<int>(g / P.ctiles), tau = static_cast<int>(g % P.ctiles);
-    const int hi = P.L - tau * kCT;  // exclusive; tile 0 holds the road's last columns
+    // tile 0 holds the road's last columns; columns L..Lp-1 are empty padding (-1)
+    const int hi = P.Lp - tau * NA * kCI;
     const bool green = green_of(P, r);
     const unsigned long long key = propose_key(P, r);
-    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
-    const int c_hi = hi - static_cast<int>(threadIdx.x) * kCI;
-    unsigned F[kCI];
-    unsigned long long occm = 0;
-    unsigned T = kIdentity;
+    const size_t cb = static_cast<size_t>(r) * P.Cpad;
+    const int c_lo = hi - (static_cast<int>(threadIdx.x) + 1) * kCI;  // multiple of 4
+    // occupants of this thread's 4 columns x 3 lanes (column c_lo + q)
+    int o[3][kCI];
 #pragma unroll
-    for (int j = 0; j < kCI; ++j) {
-        const int c = c_hi - 1 - j;
-        unsigned f = kIdentity;
-        if (c >= 0) {
-            unsigned m3;
-            f = column_fn(P, sb, cb, c, green, key, m3);
-            occm |= static_cast<unsigned long long>(m3) << (3 * j);
+    for (int l = 0; l < 3; ++l) {
+        int4 v4 = make_int4(-1, -1, -1, -1);
+        if (c_lo >= 0) v4 = *reinterpret_cast<const int4*>(&P.occ[cb + l * P.Lp + c_lo]);
+        o[l][0] = v4.x;
+        o[l][1] = v4.y;
+        o[l][2] = v4.z;
+        o[l][3] = v4.w;
+    }
+    // proposals (no memory), then every bid word, then the targets' occupants: three batched
+    // rounds of independent loads instead of a dependent chain per column
+    int X[3][kCI];
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int q = 0; q < kCI; ++q)
+            X[l][q] = o[l][q] >= 0 ? proposal(P, o[l][q], l * P.Lp + c_lo + q, green, key) : kStay;
+    unsigned long long bw[3][kCI];
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int q = 0; q < kCI; ++q) bw[l][q] = X[l][q] >= 0 ? P.bid[cb + X[l][q]] : 0ULL;
+    int ox[3][kCI];  // occupant of the target if this car won it, else kStay (lost / no move)
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int q = 0; q < kCI; ++q) {
+            int ws, wp;
+            const bool won = X[l][q] >= 0 && bid_winner(bw[l][q], P.epoch, ws, wp) && ws == o[l][q];
+            ox[l][q] = won ? P.occ[cb + X[l][q]] : kStay - 1;
+        }
+    unsigned F[kCI];
+    unsigned occm = 0;
+    unsigned T = kIdentityFn;
+#pragma unroll
+    for (int j = 0; j < kCI; ++j) {  // j = 0 is the rightmost column of this thread
+        const int q = kCI - 1 - j;
+        unsigned f = kIdentityFn;
+        if (c_lo + q >= 0) {
+            f = 0;
+#pragma unroll
+            for (int l = 0; l < 3; ++l) {
+                // mode: 0 never, 1 always, 2 + tl iff the occupant of (tl, c+1) moves out
+                unsigned m = 0;
+                if (o[l][q] >= 0) {
+                    occm |= 1u << (3 * j + l);
+                    if (X[l][q] == kExit)
+                        m = 1;
+                    else if (ox[l][q] != kStay - 1)
+                        m = ox[l][q] < 0 ? 1u : 2u + static_cast<unsigned>(X[l][q] / P.Lp);
+                }
+                f |= m << (3 * l);
+            }
         }
         F[j] = f;
         T = compose(f, T);
@@ -205,51 +233,71 @@ __global__ void __launch_bounds__(kT) k_accept(TParams P) {
     if (lane == 31) s_warp[warp] = I;
     __syncthreads();
     if (warp == 0) {
-        unsigned wv = lane < kT / 32 ? s_warp[lane] : kIdentity;
+        unsigned wv = lane < NA / 32 ? s_warp[lane] : kIdentityFn;
 #pragma unroll
-        for (int d = 1; d < kT / 32; d <<= 1) {
+        for (int d = 1; d < NA / 32; d <<= 1) {
             const unsigned o = __shfl_up_sync(0xffffffffu, wv, d);
             if (lane >= d) wv = compose(wv, o);
         }
-        if (lane < kT / 32) s_warp[lane] = wv;  // inclusive warp prefixes
+        if (lane < NA / 32) s_warp[lane] = wv;  // inclusive warp prefixes
     }
     __syncthreads();
-    const unsigned wex = warp > 0 ? s_warp[warp - 1] : kIdentity;
+    const unsigned wex = warp > 0 ? s_warp[warp - 1] : kIdentityFn;
     const unsigned up = __shfl_up_sync(0xffffffffu, I, 1);
     const unsigned E = lane > 0 ? compose(up, wex) : wex;  // exclusive prefix of this thread
-    if (threadIdx.x == 0) {
-        const unsigned A = s_warp[kT / 32 - 1];  // tile aggregate
+    if (warp == 0) {  // decoupled lookback, 32 predecessors per round
+        const unsigned A = s_warp[NA / 32 - 1];  // tile aggregate
         unsigned long long* st = P.cstatus + static_cast<size_t>(r) * P.ctiles;
         const unsigned long long tag = (P.epoch & 0x3FFFFFFFULL) << 32;
         unsigned vin = 0;
         if (tau > 0) {
-            st_word(&st[tau], kFlagAgg | tag | A);
-            unsigned accf = kIdentity;
-            for (int j = tau - 1;;) {
-                const unsigned long long w = ld_word(&st[j]);
-                if ((w & (0x3FFFFFFFULL << 32)) != tag || (w >> 62) == 0) continue;  // not yet published
-                if ((w >> 62) == 2) {
-                    vin = fn_at(accf, static_cast<unsigned>(w & 7u));
+            if (lane == 0) st_word(&st[tau], kFlagAgg | tag | A);
+            unsigned accf = kIdentityFn;  // composition of the aggregates passed so far
+            for (int base = tau - 1;; base -= 32) {
+                const int j = base - lane;  // lane 0 = nearest predecessor
+                unsigned long long w = 0;
+                unsigned fl = j >= 0 ? 0u : 2u;  // beyond the road's first tile: never reached
+                do {  // all lanes stay in the loop until every predecessor has published
+                    if (fl == 0) {
+                        w = ld_word(&st[j]);
+                        fl = ((w & (0x3FFFFFFFULL << 32)) == tag) ? static_cast<unsigned>(w >> 62) : 0u;
+                    }
+                } while (__any_sync(0xffffffffu, fl == 0));
+                // every lane now holds an aggregate (1) or a prefix (2); the lanes BEFORE the
+                // first prefix contribute their aggregates, the first prefix ends the walk
+                const unsigned pre = __ballot_sync(0xffffffffu, fl == 2);
+                const int first = pre ? __ffs(pre) - 1 : 32;
+                unsigned f = lane < first ? static_cast<unsigned>(w & 0x1FFu) : kIdentityFn;
+                // ordered reduction: result = f_0 ∘ f_1 ∘ ... (lane 0 nearest)
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const unsigned o = __shfl_down_sync(0xffffffffu, f, d);
+                    if (lane + d < 32) f = compose(f, o);
+                }
+                accf = compose(accf, __shfl_sync(0xffffffffu, f, 0));
+                if (first < 32) {
+                    const unsigned pv = static_cast<unsigned>(__shfl_sync(0xffffffffu, w, first) & 7u);
+                    vin = apply_fn(accf, pv);
                     break;
                 }
-                accf = compose(accf, static_cast<unsigned>(w & 0xFFFFFFu));
-                --j;
             }
         }
-        st_word(&st[tau], kFlagPre | tag | fn_at(A, vin));
-        s_vin = vin;
+        if (lane == 0) {
+            st_word(&st[tau], kFlagPre | tag | apply_fn(A, vin));
+            s_vin = vin;
+        }
     }
     __syncthreads();
-    unsigned v = fn_at(E, s_vin);
+    unsigned v = apply_fn(E, s_vin);
 #pragma unroll
     for (int j = 0; j < kCI; ++j) {
-        v = fn_at(F[j], v);
-        const unsigned m3 = static_cast<unsigned>(occm >> (3 * j)) & 7u;
+        v = apply_fn(F[j], v);
+        const unsigned m3 = (occm >> (3 * j)) & 7u;
         if (m3) {
-            const int c = c_hi - 1 - j;
+            const int c = c_lo + kCI - 1 - j;
 #pragma unroll
             for (int l = 0; l < 3; ++l)
-                if (m3 & (1u << l)) P.acc[cb + l * P.L + c] = static_cast<uint8_t>((v >> l) & 1u);
+                if (m3 & (1u << l)) P.acc[cb + l * P.Lp + c] = static_cast<uint8_t>((v >> l) & 1u);
         }
     }
 }
@@ -259,23 +307,24 @@ __global__ void __launch_bounds__(kT) k_accept(TParams P) {
 __device__ __forceinline__ void vacate(const TParams& P, size_t cb, int p) {
     int ws, wp;
     if (bid_winner(P.bid[cb + p], P.epoch, ws, wp)) {
-        const int lane = p / P.L;
+        const int lane = p / P.Lp;
         const int src_lane = wp == 0 ? lane : (wp == 1 ? lane - 1 : lane + 1);
-        const int src = src_lane * P.L + (p - lane * P.L) - 1;
+        const int src = src_lane * P.Lp + (p - lane * P.Lp) - 1;
         if (P.acc[cb + src]) return;  // the winner writes occ[p]
     }
     P.occ[cb + p] = -1;
 }
 
-__global__ void __launch_bounds__(kT) k_apply(TParams P) {
-    __shared__ unsigned long long s_scan[kT / 32 + 1];
+template <int NT>
+__global__ void __launch_bounds__(NT) k_apply(TParams P) {
+    __shared__ unsigned long long s_scan[NT / 32 + 1];
     __shared__ int s_first[3];
-    __shared__ unsigned s_exit[kT / 32];
+    __shared__ unsigned s_exit[NT / 32];
     const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
     const bool green = green_of(P, r);
     const unsigned long long key = propose_key(P, r);
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
-    const int i0 = tile * kTile + threadIdx.x * kS;  // blocked: free-slot order = slot order
+    const int i0 = tile * NT * kS + threadIdx.x * kS;  // blocked: free-slot order = slot order
     unsigned exited = 0, nf = 0;
     bool fr[kS];
 #pragma unroll
@@ -306,7 +355,7 @@ __global__ void __launch_bounds__(kT) k_apply(TParams P) {
         nf += fr[k];
     }
     unsigned long long tot;
-    const unsigned long long ex = block_excl_scan<kT>(nf, s_scan, &tot);
+    const unsigned long long ex = block_excl_scan<NT>(nf, s_scan, &tot);
     if (threadIdx.x < 3) s_first[threadIdx.x] = -1;
     __syncthreads();
     unsigned rank = static_cast<unsigned>(ex);
@@ -321,7 +370,7 @@ __global__ void __launch_bounds__(kT) k_apply(TParams P) {
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned ex_sum = 0;
-        for (int w = 0; w < kT / 32; ++w) ex_sum += s_exit[w];
+        for (int w = 0; w < NT / 32; ++w) ex_sum += s_exit[w];
         if (ex_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&P.cnt[static_cast<size_t>(r) * 8 + 5]), ex_sum);
         P.tinfo[static_cast<size_t>(r) * P.tiles + tile] =
             make_int4(static_cast<int>(tot), s_first[0], s_first[1], s_first[2]);
@@ -350,7 +399,7 @@ __global__ void k_spawn(TParams P) {
             lanes[j] = tmp;
         }
         for (int q = 0; q < (k < 3 ? k : 3); ++q)
-            if (P.occ[cb + lanes[q] * P.L] < 0) rows[nvalid++] = lanes[q];
+            if (P.occ[cb + lanes[q] * P.Lp] < 0) rows[nvalid++] = lanes[q];
     }
     // the lowest nvalid free slots, tiles in order (warp-parallel over tile chunks)
     int slots[3] = {-1, -1, -1};
@@ -376,10 +425,10 @@ __global__ void k_spawn(TParams P) {
         for (int q = 0; q < spawned; ++q) {
             const int s = slots[q];
             P.active[sb + s] = 1;
-            P.pos[sb + s] = rows[q] * P.L;
+            P.pos[sb + s] = rows[q] * P.Lp;
             P.ids[sb + s] = nid + q;
             P.ages[sb + s] = 0;
-            P.occ[cb + rows[q] * P.L] = s;
+            P.occ[cb + rows[q] * P.Lp] = s;
         }
         const long long exited = cn[5];
         cn[0] += spawned - exited;
@@ -511,11 +560,34 @@ struct abmx_traffic {
         if (k == 3) return static_cast<unsigned>(R);
         return static_cast<unsigned>(R * P.tiles);
     }
-    unsigned block(int k) const { return k == 3 ? 32u : static_cast<unsigned>(kT); }
-    static void* fn(int k) {
-        static void* const f[kNumKernels] = {reinterpret_cast<void*>(k_propose), reinterpret_cast<void*>(k_accept),
-                                             reinterpret_cast<void*>(k_apply), reinterpret_cast<void*>(k_spawn)};
-        return f[k];
+    int nt = 256, na = 1024;  // CTA sizes of the slot kernels and of k_accept
+    void* fns[kNumKernels] = {};
+    unsigned block(int k) const {
+        return k == 3 ? 32u : static_cast<unsigned>(k == 1 ? na : nt);
+    }
+    void* fn(int k) const { return fns[k]; }
+    void pick_kernels() {
+        // slot kernels: the smallest CTA covering a road (32..256 threads x 4 slots)
+        nt = 32;
+        while (nt < 256 && nt * kS < P.C) nt *= 2;
+        // k_accept: the smallest CTA covering a road's columns, else 1024 threads (few tiles)
+        na = 32;
+        while (na < 1024 && na * kCI < P.Lp) na *= 2;
+        switch (nt) {
+            case 32: fns[0] = reinterpret_cast<void*>(k_propose<32>); fns[2] = reinterpret_cast<void*>(k_apply<32>); break;
+            case 64: fns[0] = reinterpret_cast<void*>(k_propose<64>); fns[2] = reinterpret_cast<void*>(k_apply<64>); break;
+            case 128: fns[0] = reinterpret_cast<void*>(k_propose<128>); fns[2] = reinterpret_cast<void*>(k_apply<128>); break;
+            default: fns[0] = reinterpret_cast<void*>(k_propose<256>); fns[2] = reinterpret_cast<void*>(k_apply<256>); break;
+        }
+        switch (na) {
+            case 32: fns[1] = reinterpret_cast<void*>(k_accept<32>); break;
+            case 64: fns[1] = reinterpret_cast<void*>(k_accept<64>); break;
+            case 128: fns[1] = reinterpret_cast<void*>(k_accept<128>); break;
+            case 256: fns[1] = reinterpret_cast<void*>(k_accept<256>); break;
+            case 512: fns[1] = reinterpret_cast<void*>(k_accept<512>); break;
+            default: fns[1] = reinterpret_cast<void*>(k_accept<1024>); break;
+        }
+        fns[3] = reinterpret_cast<void*>(k_spawn);
     }
 
     int create(const abmx_traffic_config& c, const uint64_t* seeds, int roads) {
@@ -542,10 +614,14 @@ struct abmx_traffic {
         P.R = R;
         P.L = static_cast<int>(c.length);
         P.C = 3 * P.L;
-        P.Cpad = (P.C + 15) / 16 * 16;
-        P.Npad = (P.C + kTile - 1) / kTile * kTile;
-        P.tiles = P.Npad / kTile;
-        P.ctiles = (P.L + kCT - 1) / kCT;
+        P.Lp = (P.L + 3) / 4 * 4;  // lane stride: aligned int4 column groups in k_accept
+        P.Cpad = (3 * P.Lp + 15) / 16 * 16;
+        pick_kernels();
+        P.tile_slots = nt * kS;
+        P.tile_cols = na * kCI;
+        P.Npad = (P.C + P.tile_slots - 1) / P.tile_slots * P.tile_slots;
+        P.tiles = P.Npad / P.tile_slots;
+        P.ctiles = (P.Lp + P.tile_cols - 1) / P.tile_cols;
         P.period = c.period;
         long long gl = llround(static_cast<double>(c.period) * c.green_fraction);  // traffic.cpp:11-13
         P.green_len = gl < 0 ? 0 : (gl > c.period ? c.period : gl);
@@ -724,13 +800,17 @@ struct abmx_traffic {
         CKT(cudaMemcpyAsync(ids, P.ids + sb, n * 8, cudaMemcpyDeviceToHost, stream));
         CKT(cudaMemcpyAsync(ages, P.ages + sb, n * 8, cudaMemcpyDeviceToHost, stream));
         CKT(cudaMemcpyAsync(pos.data(), P.pos + sb, n * 4, cudaMemcpyDeviceToHost, stream));
-        if (occupancy) CKT(cudaMemcpyAsync(occupancy, P.occ + cb, n * 4, cudaMemcpyDeviceToHost, stream));
+        std::vector<int> occ_dev(static_cast<size_t>(3 * P.Lp));
+        if (occupancy) CKT(cudaMemcpyAsync(occ_dev.data(), P.occ + cb, occ_dev.size() * 4, cudaMemcpyDeviceToHost, stream));
         CKT(cudaMemcpyAsync(cn, P.cnt + static_cast<size_t>(r) * 8, 64, cudaMemcpyDeviceToHost, stream));
         CKT(cudaStreamSynchronize(stream));
         for (size_t i = 0; i < n; ++i) {
-            lane[i] = pos[i] / P.L;
-            cell[i] = pos[i] % P.L;
+            lane[i] = pos[i] / P.Lp;
+            cell[i] = pos[i] % P.Lp;
         }
+        if (occupancy)
+            for (int l = 0; l < 3; ++l)
+                for (int c = 0; c < P.L; ++c) occupancy[l * P.L + c] = occ_dev[static_cast<size_t>(l * P.Lp + c)];
         if (next_id) *next_id = cn[1];
         if (num_active) *num_active = static_cast<int32_t>(cn[0]);
         return ABMX_OK;
@@ -748,7 +828,7 @@ struct abmx_traffic {
                 abmx_internal::set_error("car position outside the road");
                 return ABMX_E_DOMAIN;
             }
-            pos[i] = static_cast<int>(lane[i] * P.L + cell[i]);
+            pos[i] = static_cast<int>(lane[i] * P.Lp + cell[i]);
             if (act[i]) {
                 if (occ[static_cast<size_t>(pos[i])] != -1) {
                     abmx_internal::set_error("two cars occupy one road cell");  // traffic.cpp:40-41
@@ -1023,14 +1103,30 @@ int abmx_traffic_kernel_times(abmx_traffic* h, double* ms, int64_t* launches) {
 }
 int abmx_traffic_run_batch(const abmx_traffic_config* cfg, uint64_t master, int32_t replica_begin, int32_t count,
                            int64_t steps, double* metrics_out, double* kernel_ms) {
+    return abmx_traffic_run_batch_path(cfg, master, replica_begin, count, steps, 0, metrics_out, kernel_ms);
+}
+
+int abmx_traffic_run_batch_path(const abmx_traffic_config* cfg, uint64_t master, int32_t replica_begin, int32_t count,
+                                int64_t steps, int32_t path, double* metrics_out, double* kernel_ms) {
     if (!cfg || count < 0) {
         abmx_internal::set_error("bad run_batch arguments");
         return ABMX_E_ARG;
+    }
+    if (cfg->period < 1 || cfg->length < 1) {
+        abmx_internal::set_error(cfg->period < 1 ? "signal period must be >= 1" : "road length must be >= 1");
+        return ABMX_E_DOMAIN;
     }
     if (count == 0 || steps <= 0) return ABMX_OK;
     std::vector<uint64_t> seeds(static_cast<size_t>(count));
     const unsigned long long base = abmx_dev::split(master, 2);  // batch.cpp:12-19
     for (int32_t q = 0; q < count; ++q) seeds[static_cast<size_t>(q)] = abmx_dev::split(base, static_cast<unsigned long long>(replica_begin + q));
+    const bool smem_ok = abmx_internal::traffic_ens_fits(*cfg);
+    if (path == 1 && !smem_ok) {
+        abmx_internal::set_error("road too long for the shared-memory path");
+        return ABMX_E_CAPACITY;
+    }
+    if (path == 1 || (path == 0 && smem_ok))
+        return abmx_internal::traffic_ensemble_run(*cfg, seeds.data(), count, steps, metrics_out, kernel_ms);
     abmx_traffic* h = nullptr;
     int rc = abmx_traffic_create(cfg, seeds.data(), count, &h);
     if (rc) return rc;

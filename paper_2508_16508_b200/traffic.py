@@ -63,6 +63,8 @@ _sig("abmx_traffic_kernel_name", C.c_char_p, [C.c_int32])
 _sig("abmx_traffic_kernel_times", C.c_int, [C.c_void_p, _f64p, _i64p])
 _sig("abmx_traffic_run_batch", C.c_int, [_CP, C.c_uint64, C.c_int32, C.c_int32, C.c_int64, _f64p,
                                          _f64p])
+_sig("abmx_traffic_run_batch_path", C.c_int, [_CP, C.c_uint64, C.c_int32, C.c_int32, C.c_int64,
+                                              C.c_int32, _f64p, _f64p])
 
 
 def _p(a, t):
@@ -195,12 +197,14 @@ def resolve_conflicts(length: int, active, lane, cell, kind, to_lane, to_cell) -
     return acc
 
 
-def run_batch(cfg: TrafficConfig, master: int, replicas: int, steps: int, *, begin: int = 0):
-    """run_batch of TrafficModel (batch.cpp:21-101): ([replicas, steps, 4], device ms)."""
+def run_batch(cfg: TrafficConfig, master: int, replicas: int, steps: int, *, begin: int = 0,
+              path: int = 0):
+    """run_batch of TrafficModel (batch.cpp:21-101): ([replicas, steps, 4], device ms).
+    path: 0 auto, 1 shared-memory CTA per road, 2 batched HBM engine."""
     out = np.zeros((replicas, steps, 4))
     ms = C.c_double()
-    _check(lib.abmx_traffic_run_batch(C.byref(cfg), master, begin, replicas, steps,
-                                      _p(out, _f64p), C.byref(ms)))
+    _check(lib.abmx_traffic_run_batch_path(C.byref(cfg), master, begin, replicas, steps, path,
+                                           _p(out, _f64p), C.byref(ms)))
     return out, ms.value
 
 

@@ -88,10 +88,11 @@ def test_resolve_golden(abmx, T):
             assert np.array_equal(T.resolve_conflicts(*args), dec(c["accepted"], np.uint8)), i
 
 
-def test_run_batch_golden(T):
+@pytest.mark.parametrize("path", [1, 2])
+def test_run_batch_golden(T, path):
     b = load()["batch"]
     rows, _ = T.run_batch(T.TrafficConfig(b["length"], b["period"], b["green_fraction"]),
-                          b["master"], b["replicas"], b["steps"])
+                          b["master"], b["replicas"], b["steps"], path=path)
     assert np.array_equal(rows, np.array(b["metrics"]))
 
 
@@ -209,9 +210,19 @@ def test_dense_roads_vs_oracle(T, oracle, L, dens, seed):
         assert_road(dev.road(), ref.export(), t)
 
 
-def test_many_roads_vs_oracle(T, oracle):
-    """Batched roads (replica seeds) against the oracle's run_batch."""
-    cfg = T.TrafficConfig(100, 10, 0.5)
-    rows, _ = T.run_batch(cfg, 11, 300, 200)
-    want = oracle.traffic_run_batch(100, 10, 0.5, 11, 300, 200)
+@pytest.mark.parametrize("path", [1, 2])
+@pytest.mark.parametrize("L,period,gf", [(100, 10, 0.5), (1, 3, 0.7), (7, 1, 1.0), (2000, 13, 0.2),
+                                         (333, 10, 0.0)])
+def test_many_roads_vs_oracle(T, oracle, path, L, period, gf):
+    """Batched roads (replica seeds) on both run_batch paths against the oracle's run_batch."""
+    cfg = T.TrafficConfig(L, period, gf)
+    rows, _ = T.run_batch(cfg, 11, 150, 200, path=path)
+    want = oracle.traffic_run_batch(L, period, gf, 11, 150, 200)
     assert np.array_equal(rows, want)
+
+
+def test_run_batch_path_limits(abmx, T):
+    with pytest.raises(abmx.CapacityError):
+        T.run_batch(T.TrafficConfig(20000, 10, 0.5), 1, 2, 2, path=1)
+    with pytest.raises(abmx.DomainError):
+        T.run_batch(T.TrafficConfig(10, 0, 0.5), 1, 2, 2)
