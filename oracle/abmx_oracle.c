@@ -725,5 +725,267 @@ int orc_traffic_run_batch(const orc_traffic_config* cfg, uint64_t master, int32_
     return 0;
 }
 
+
+/* ------------------------------------------------------------------ finance */
+enum { ORC_FIN_PLACE = 8 }; /* rng.hpp:36-37 */
+#define ORC_TICK 0x1p-7     /* finance.hpp:37 kPriceTick */
+
+double orc_quantize_price(double raw) {
+    double p = round(raw / ORC_TICK) * ORC_TICK;
+    if (p < ORC_TICK) p = ORC_TICK;
+    return p;
+}
+
+static void orc_book_init(orc_book* b, int32_t cap, double init_price) {
+    b->capacity = cap;
+    b->num_active = 0;
+    b->next_id = 0;
+    b->active = (uint8_t*)calloc((size_t)cap + 1, 1);
+    b->ids = (int64_t*)calloc((size_t)cap + 1, 8);
+    b->ages = (int64_t*)calloc((size_t)cap + 1, 8);
+    b->trader = (int64_t*)calloc((size_t)cap + 1, 8);
+    b->side = (int64_t*)calloc((size_t)cap + 1, 8);
+    b->qty = (int64_t*)calloc((size_t)cap + 1, 8);
+    b->placed = (int64_t*)calloc((size_t)cap + 1, 8);
+    b->price = (double*)calloc((size_t)cap + 1, 8);
+    b->last_price = orc_quantize_price(init_price);
+    b->dropped = 0;
+    b->volume = 0;
+    b->clearing = 0.0;
+}
+
+static void orc_book_reset_slot(orc_book* b, int32_t i) { /* agent_set.cpp:45-58 */
+    b->active[i] = 0;
+    b->ids[i] = 0;
+    b->ages[i] = 0;
+    b->trader[i] = 0;
+    b->side[i] = 0;
+    b->qty[i] = 0;
+    b->placed[i] = 0;
+    b->price[i] = 0.0;
+    b->num_active -= 1;
+}
+
+orc_fin* orc_fin_create(const orc_fin_config* cfg, uint64_t seed) {
+    if (cfg->books < 1 || cfg->traders < 0 || cfg->book_capacity < 1 || cfg->qmax < 1) return NULL;
+    orc_fin* m = (orc_fin*)calloc(1, sizeof(orc_fin));
+    m->cfg = *cfg;
+    m->seed = seed;
+    m->cash = (double*)calloc((size_t)cfg->traders + 1, 8);
+    m->holdings = (int64_t*)calloc((size_t)(cfg->books * cfg->traders) + 1, 8);
+    m->books = (orc_book*)calloc((size_t)cfg->books, sizeof(orc_book));
+    for (int64_t k = 0; k < cfg->books; ++k) orc_book_init(&m->books[k], (int32_t)cfg->book_capacity, cfg->init_price);
+    return m;
+}
+
+void orc_fin_free(orc_fin* m) {
+    if (!m) return;
+    for (int64_t k = 0; k < m->cfg.books; ++k) {
+        orc_book* b = &m->books[k];
+        free(b->active);
+        free(b->ids);
+        free(b->ages);
+        free(b->trader);
+        free(b->side);
+        free(b->qty);
+        free(b->placed);
+        free(b->price);
+    }
+    free(m->books);
+    free(m->cash);
+    free(m->holdings);
+    free(m);
+}
+
+/* place_orders (finance.cpp:74-123): row i = trader i; spawn into the lowest free slots */
+static void orc_fin_place(const orc_fin* m, orc_book* b, uint64_t stream, int64_t t) {
+    const orc_fin_config* c = &m->cfg;
+    int64_t q = 0, spawned = 0;
+    int32_t slot = 0;
+    for (int64_t i = 0; i < c->traders; ++i) {
+        const uint64_t base = 4 * (uint64_t)i;
+        if (!(orc_uniform_double(stream, base) < c->p_order)) continue;
+        const int64_t side = orc_uniform_int(stream, base + 1, 0, 2);
+        const double eps = -c->delta + 2.0 * c->delta * orc_uniform_double(stream, base + 2);
+        const int64_t qty = orc_uniform_int(stream, base + 3, 1, c->qmax + 1);
+        const double price = orc_quantize_price(b->last_price * (1.0 + eps));
+        ++q;
+        while (slot < b->capacity && b->active[slot]) ++slot;
+        if (slot >= b->capacity) continue; /* no free slot left: dropped */
+        b->active[slot] = 1;
+        b->ids[slot] = b->next_id++;
+        b->ages[slot] = 0;
+        b->trader[slot] = i;
+        b->side[slot] = side;
+        b->price[slot] = price;
+        b->qty[slot] = qty;
+        b->placed[slot] = t;
+        b->num_active += 1;
+        ++spawned;
+    }
+    b->dropped = q - spawned;
+}
+
+/* sorted_side comparator (finance.cpp:27-36): price (desc for buys), placed, id */
+static const orc_book* g_sort_book;
+static int g_sort_desc;
+static int orc_fin_before(int32_t a, int32_t bb) {
+    const orc_book* b = g_sort_book;
+    if (b->price[a] != b->price[bb]) return g_sort_desc ? b->price[a] > b->price[bb] : b->price[a] < b->price[bb];
+    if (b->placed[a] != b->placed[bb]) return b->placed[a] < b->placed[bb];
+    return b->ids[a] < b->ids[bb];
+}
+static void orc_fin_sort(int32_t* v, int32_t n) { /* stable insertion sort (n is small) */
+    for (int32_t i = 1; i < n; ++i) {
+        const int32_t x = v[i];
+        int32_t j = i - 1;
+        while (j >= 0 && orc_fin_before(x, v[j])) {
+            v[j + 1] = v[j];
+            --j;
+        }
+        v[j + 1] = x;
+    }
+}
+
+int32_t orc_fin_match(orc_book* b, int64_t* f_trader, int64_t* f_side, int64_t* f_qty, double* f_amount) {
+    const int32_t n = b->capacity;
+    int32_t* buys = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int32_t* sells = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n + 1));
+    int64_t* bcum = (int64_t*)malloc(8 * (size_t)(n + 1));
+    int64_t* scum = (int64_t*)malloc(8 * (size_t)(n + 1));
+    int32_t nb = 0, ns = 0, nf = 0;
+    for (int32_t i = 0; i < n; ++i) {
+        if (!b->active[i]) continue;
+        if (b->side[i] == 0)
+            buys[nb++] = i;
+        else if (b->side[i] == 1)
+            sells[ns++] = i;
+    }
+    g_sort_book = b;
+    g_sort_desc = 1;
+    orc_fin_sort(buys, nb);
+    g_sort_desc = 0;
+    orc_fin_sort(sells, ns);
+    int64_t run = 0;
+    for (int32_t i = 0; i < nb; ++i) bcum[i] = (run += b->qty[buys[i]]);
+    run = 0;
+    for (int32_t j = 0; j < ns; ++j) scum[j] = (run += b->qty[sells[j]]);
+    b->volume = 0;
+    int64_t volume = 0;
+    if (nb > 0 && ns > 0) {
+        for (int32_t i = 0; i < nb; ++i) {
+            int32_t feasible = 0; /* upper_bound of the buy price in the ascending sell prices */
+            while (feasible < ns && !(b->price[buys[i]] < b->price[sells[feasible]])) ++feasible;
+            if (feasible == 0) continue;
+            const int64_t v = bcum[i] < scum[feasible - 1] ? bcum[i] : scum[feasible - 1];
+            if (v > volume) volume = v;
+        }
+    }
+    if (volume > 0) {
+        int32_t mb = 0, ms = 0;
+        while (bcum[mb] < volume) ++mb;
+        while (scum[ms] < volume) ++ms;
+        const double clearing = (b->price[buys[mb]] + b->price[sells[ms]]) / 2.0;
+        uint8_t* exhausted = (uint8_t*)calloc((size_t)n + 1, 1);
+        for (int side = 0; side < 2; ++side) {
+            const int32_t* v = side == 0 ? buys : sells;
+            const int32_t cnt = side == 0 ? nb : ns;
+            int64_t remaining = volume;
+            for (int32_t j = 0; j < cnt && remaining > 0; ++j) {
+                const int32_t i = v[j];
+                const int64_t f = b->qty[i] < remaining ? b->qty[i] : remaining;
+                b->qty[i] -= f;
+                remaining -= f;
+                if (b->qty[i] == 0) exhausted[i] = 1;
+                if (f_trader) {
+                    f_trader[nf] = b->trader[i];
+                    f_side[nf] = side;
+                    f_qty[nf] = f;
+                    f_amount[nf] = (double)f * clearing;
+                }
+                ++nf;
+            }
+        }
+        for (int32_t i = 0; i < n; ++i)
+            if (exhausted[i] && b->active[i]) orc_book_reset_slot(b, i);
+        free(exhausted);
+        b->last_price = clearing;
+        b->volume = volume;
+        b->clearing = clearing;
+    }
+    free(buys);
+    free(sells);
+    free(bcum);
+    free(scum);
+    return nf;
+}
+
+void orc_fin_step(orc_fin* m, int64_t t) {
+    const orc_fin_config* c = &m->cfg;
+    const uint64_t root = orc_split(orc_split(m->seed, ORC_FIN_PLACE), (uint64_t)t);
+    for (int64_t k = 0; k < c->books; ++k) orc_fin_place(m, &m->books[k], orc_split(root, (uint64_t)k), t);
+    const size_t cap = (size_t)c->book_capacity + 1;
+    int64_t* ft = (int64_t*)malloc(8 * cap * 2);
+    int64_t* fs = (int64_t*)malloc(8 * cap * 2);
+    int64_t* fq = (int64_t*)malloc(8 * cap * 2);
+    double* fa = (double*)malloc(8 * cap * 2);
+    for (int64_t k = 0; k < c->books; ++k) { /* settlement folds books in order */
+        const int32_t nf = orc_fin_match(&m->books[k], ft, fs, fq, fa);
+        int64_t* h = m->holdings + k * c->traders;
+        for (int32_t q = 0; q < nf; ++q) {
+            if (fs[q] == 0) {
+                m->cash[ft[q]] -= fa[q];
+                h[ft[q]] += fq[q];
+            } else {
+                m->cash[ft[q]] += fa[q];
+                h[ft[q]] -= fq[q];
+            }
+        }
+    }
+    free(ft);
+    free(fs);
+    free(fq);
+    free(fa);
+    for (int64_t k = 0; k < c->books; ++k) { /* cancel at the age limit (finance.cpp:236-245) */
+        orc_book* b = &m->books[k];
+        for (int32_t i = 0; i < b->capacity; ++i)
+            if (b->active[i] && t - b->placed[i] >= c->max_order_age) orc_book_reset_slot(b, i);
+    }
+}
+
+void orc_fin_metrics(const orc_fin* m, double* rows) {
+    for (int64_t k = 0; k < m->cfg.books; ++k) {
+        const orc_book* b = &m->books[k];
+        int64_t nb = 0, ns = 0;
+        for (int32_t i = 0; i < b->capacity; ++i) {
+            if (!b->active[i]) continue;
+            if (b->side[i] == 0)
+                ++nb;
+            else
+                ++ns;
+        }
+        double* r = rows + k * 6;
+        r[0] = (double)k;
+        r[1] = b->last_price;
+        r[2] = (double)nb;
+        r[3] = (double)ns;
+        r[4] = (double)b->volume;
+        r[5] = (double)b->dropped;
+    }
+}
+
+int orc_fin_run_batch(const orc_fin_config* cfg, uint64_t master, int32_t replicas, int64_t steps, double* rows) {
+    for (int32_t r = 0; r < replicas; ++r) {
+        orc_fin* m = orc_fin_create(cfg, orc_replica_seed(master, r));
+        if (!m) return 1;
+        for (int64_t t = 1; t <= steps; ++t) {
+            orc_fin_step(m, t);
+            orc_fin_metrics(m, rows + (((size_t)r * (size_t)steps + (size_t)(t - 1)) * (size_t)cfg->books) * 6);
+        }
+        orc_fin_free(m);
+    }
+    return 0;
+}
+
 /* FNV-1a-64 helper for state hashes (test bookkeeping, not a reference algorithm) */
 uint64_t orc_fnv1a(uint64_t h, const void* data, size_t n) { return fnv(h, data, n); }

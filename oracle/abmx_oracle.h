@@ -154,6 +154,45 @@ void orc_traffic_metrics(const orc_traffic* m, double* out4);
 int orc_traffic_run_batch(const orc_traffic_config* cfg, uint64_t master, int32_t replicas,
                           int64_t steps, double* metrics_out);
 
+/* ---- finance (include/abmx/models/finance.hpp, src/models/finance.cpp) ---- */
+typedef struct {
+    int64_t books, traders, book_capacity;
+    double p_order, delta;
+    int64_t qmax, max_order_age;
+    double init_price;
+} orc_fin_config;
+
+typedef struct {
+    int32_t capacity, num_active;
+    int64_t next_id;
+    uint8_t* active;
+    int64_t *ids, *ages, *trader, *side, *qty, *placed;
+    double* price;
+    double last_price;
+    int64_t dropped, volume; /* dropped_this_step, last_trades.volume */
+    double clearing;
+} orc_book;
+
+typedef struct {
+    orc_fin_config cfg;
+    uint64_t seed;
+    double* cash;       /* [traders] */
+    int64_t* holdings;  /* [books][traders] */
+    orc_book* books;    /* [books] */
+} orc_fin;
+
+double orc_quantize_price(double raw);                 /* finance.cpp:56-61 */
+orc_fin* orc_fin_create(const orc_fin_config* cfg, uint64_t seed);  /* init_market */
+void orc_fin_free(orc_fin* m);
+void orc_fin_step(orc_fin* m, int64_t t);             /* step_market */
+void orc_fin_metrics(const orc_fin* m, double* rows); /* [books][6] collect_metrics */
+/* match_book (finance.cpp:125-190) on one book; fills (trader, side, qty, amount) appended
+ * into the arrays (capacity entries each, nullable); returns the number of fills */
+int32_t orc_fin_match(orc_book* b, int64_t* f_trader, int64_t* f_side, int64_t* f_qty,
+                      double* f_amount);
+int orc_fin_run_batch(const orc_fin_config* cfg, uint64_t master, int32_t replicas,
+                      int64_t steps, double* rows); /* [K][T][books][6] */
+
 /* FNV-1a-64 continuation over raw bytes (start h = 0xcbf29ce484222325) */
 uint64_t orc_fnv1a(uint64_t h, const void* data, size_t n);
 

@@ -229,6 +229,55 @@ def main():
                      "steps": 40, "metrics": rows.tolist()}
     json.dump(traf, open(os.path.join(OUT, "traffic.json"), "w"))
 
+    # ---- finance (finance.cpp): trajectories + final markets, match_book cases, batch rows
+    fin = {"models": [], "match": [], "batch": None, "quantize": []}
+    for kw, seed, T in ((dict(), 123, 100), (dict(book_capacity=64, books=3), 31, 40),
+                        (dict(traders=6, books=1, book_capacity=2, p_order=1.0), 5, 10),
+                        (dict(traders=0, books=2, book_capacity=8), 9, 10),
+                        (dict(traders=50, book_capacity=100, max_order_age=3, delta=0.3, qmax=3), 7, 80),
+                        (dict(traders=200, books=2, book_capacity=300, p_order=0.9, init_price=0.5), 11, 60)):
+        m = ref.fin(seed, **kw)
+        rows = []
+        for t in range(1, T + 1):
+            m.step(t)
+            rows.append(m.metrics().tolist())
+        cash, hold = m.traders()
+        books = []
+        for k in range(m.cfg.books):
+            b = m.book(k)
+            books.append({name: b64(b[name]) for name, _ in pyoracle.BOOK_FIELDS} |
+                         {"last_price": b["last_price"], "next_id": b["next_id"],
+                          "num_active": b["num_active"]})
+        fin["models"].append({"cfg": kw, "seed": seed, "steps": T, "metrics": rows,
+                              "cash": b64(cash), "holdings": b64(hold), "books": books})
+    g3 = np.random.default_rng(2718)
+    for trial in range(120):
+        cap = int(g3.integers(1, 64))
+        n = int(g3.integers(0, cap + 1))
+        book = {name: np.zeros(cap, dt) for name, dt in pyoracle.BOOK_FIELDS}
+        slots = g3.permutation(cap)[:n]
+        for j, s_ in enumerate(slots):
+            book["active"][s_] = 1
+            book["ids"][s_] = j
+            book["trader"][s_] = j % 7
+            book["side"][s_] = int(g3.integers(0, 2))
+            book["price"][s_] = ref.lib.ref_fin_quantize(float(g3.uniform(90, 110)))
+            book["qty"][s_] = int(g3.integers(1, 11))
+            book["placed"][s_] = int(g3.integers(0, 5))
+        book["next_id"] = n
+        out, fills, sc = ref.fin_match(book, 100.0)
+        fin["match"].append({"cap": cap, "in": {k: b64(book[k]) for k, _ in pyoracle.BOOK_FIELDS} |
+                             {"next_id": n},
+                             "out": {k: b64(out[k]) for k, _ in pyoracle.BOOK_FIELDS},
+                             "fills": {k: b64(v) for k, v in fills.items()},
+                             "last_price": sc[0], "volume": int(sc[2]), "clearing": sc[3]})
+    rows, _ = ref.fin_run_batch(99, 6, 30, threads=3, book_capacity=64)
+    fin["batch"] = {"cfg": {"book_capacity": 64}, "master": 99, "replicas": 6, "steps": 30,
+                    "rows": rows.tolist()}
+    for x in (0.0, 1e-9, 0.00390625, 0.0039, 99.99609375, 100.001953125, 100.0029, -5.0, 1e6 + 0.3):
+        fin["quantize"].append([x, ref.lib.ref_fin_quantize(x)])
+    json.dump(fin, open(os.path.join(OUT, "finance.json"), "w"))
+
     # ---- lifecycle: remove_agents then spawn_agents, chained cycles, id recycling on/off
     life = []
     g = np.random.default_rng(4242)

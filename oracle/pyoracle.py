@@ -133,6 +133,39 @@ class OrcTraffic(C.Structure):
                 ("green", C.c_int64), ("spawned_total", C.c_int64), ("exited_total", C.c_int64)]
 
 
+class FinCfg(C.Structure):
+    """FinanceConfig (finance.hpp:13-22), same order (shared by orc_fin_config / ref_fin_config)."""
+    _fields_ = [("books", C.c_int64), ("traders", C.c_int64), ("book_capacity", C.c_int64),
+                ("p_order", C.c_double), ("delta", C.c_double), ("qmax", C.c_int64),
+                ("max_order_age", C.c_int64), ("init_price", C.c_double)]
+
+
+FIN_DEFAULTS = dict(books=5, traders=10, book_capacity=1000, p_order=0.5, delta=0.05, qmax=10,
+                    max_order_age=20, init_price=100.0)
+
+
+def fin_cfg(**kw) -> FinCfg:
+    d = dict(FIN_DEFAULTS)
+    d.update(kw)
+    return FinCfg(**d)
+
+
+class OrcBook(C.Structure):
+    _fields_ = [("capacity", C.c_int32), ("num_active", C.c_int32), ("next_id", C.c_int64),
+                ("active", u8p), ("ids", i64p), ("ages", i64p), ("trader", i64p), ("side", i64p),
+                ("qty", i64p), ("placed", i64p), ("price", f64p), ("last_price", C.c_double),
+                ("dropped", C.c_int64), ("volume", C.c_int64), ("clearing", C.c_double)]
+
+
+class OrcFin(C.Structure):
+    _fields_ = [("cfg", FinCfg), ("seed", C.c_uint64), ("cash", f64p), ("holdings", i64p),
+                ("books", C.POINTER(OrcBook))]
+
+
+BOOK_FIELDS = (("active", np.uint8), ("ids", np.int64), ("trader", np.int64), ("side", np.int64),
+               ("price", np.float64), ("qty", np.int64), ("placed", np.int64))
+
+
 TRAFFIC_FIELDS = (("active", np.uint8), ("ids", np.int64), ("ages", np.int64),
                   ("lane", np.int64), ("cell", np.int64))
 
@@ -189,6 +222,17 @@ class Oracle(_Base):
         L.orc_traffic_run_batch.restype = C.c_int
         L.orc_traffic_run_batch.argtypes = [C.POINTER(OrcTrafficCfg), C.c_uint64, C.c_int32,
                                             C.c_int64, f64p]
+        L.orc_quantize_price.restype = C.c_double
+        L.orc_quantize_price.argtypes = [C.c_double]
+        L.orc_fin_create.restype = C.POINTER(OrcFin)
+        L.orc_fin_create.argtypes = [C.POINTER(FinCfg), C.c_uint64]
+        L.orc_fin_free.argtypes = [C.POINTER(OrcFin)]
+        L.orc_fin_step.argtypes = [C.POINTER(OrcFin), C.c_int64]
+        L.orc_fin_metrics.argtypes = [C.POINTER(OrcFin), f64p]
+        L.orc_fin_match.restype = C.c_int32
+        L.orc_fin_match.argtypes = [C.POINTER(OrcBook), i64p, i64p, i64p, f64p]
+        L.orc_fin_run_batch.restype = C.c_int
+        L.orc_fin_run_batch.argtypes = [C.POINTER(FinCfg), C.c_uint64, C.c_int32, C.c_int64, f64p]
         L.orc_remove_agents.restype = C.c_int32
         L.orc_remove_agents.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, u8p, C.c_int,
                                         i64p, i32p]
@@ -268,6 +312,20 @@ class Oracle(_Base):
         if rc:
             raise ValueError("non-finite sort key on an active slot")
         return p[:k.size].copy()
+
+    # finance
+    def fin(self, seed, **cfg):
+        return OracleFin(self, fin_cfg(**cfg), seed)
+
+    def fin_run_batch(self, master, replicas, steps, **cfg):
+        c = fin_cfg(**cfg)
+        out = np.zeros((replicas, steps, c.books, 6))
+        if self.lib.orc_fin_run_batch(C.byref(c), master, replicas, steps, _p(out, f64p)):
+            raise ValueError("bad finance config")
+        return out
+
+    def quantize_price(self, x):
+        return self.lib.orc_quantize_price(x)
 
     # traffic
     def traffic(self, length, period=10, green_fraction=0.5, seed=0):
@@ -446,10 +504,56 @@ class Reference(_Base):
         L.ref_traffic_run_batch.restype = C.c_double
         L.ref_traffic_run_batch.argtypes = [C.c_int64, C.c_int64, C.c_double, C.c_uint64, C.c_int32,
                                             C.c_int64, C.c_int, f64p]
+        L.ref_fin_create.restype = C.c_void_p
+        L.ref_fin_create.argtypes = [C.POINTER(FinCfg), C.c_uint64]
+        L.ref_fin_free.argtypes = [C.c_void_p]
+        L.ref_fin_step.argtypes = [C.c_void_p, C.c_int64]
+        L.ref_fin_run.restype = C.c_double
+        L.ref_fin_run.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.ref_fin_metrics.argtypes = [C.c_void_p, f64p]
+        L.ref_fin_export_book.argtypes = [C.c_void_p, C.c_int32, u8p, i64p, i64p, i64p, f64p, i64p,
+                                          i64p, f64p]
+        L.ref_fin_export_traders.argtypes = [C.c_void_p, f64p, i64p]
+        L.ref_fin_match.restype = C.c_int32
+        L.ref_fin_match.argtypes = [C.c_int32, C.c_double, u8p, i64p, i64p, i64p, f64p, i64p, i64p,
+                                    C.c_int64, i64p, i64p, i64p, f64p, f64p]
+        L.ref_fin_quantize.restype = C.c_double
+        L.ref_fin_quantize.argtypes = [C.c_double]
+        L.ref_fin_run_batch.restype = C.c_double
+        L.ref_fin_run_batch.argtypes = [C.POINTER(FinCfg), C.c_uint64, C.c_int32, C.c_int64, C.c_int,
+                                        f64p]
         L.ref_lifecycle.restype = C.c_int32
         L.ref_lifecycle.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, i64p, f64p, u8p, i64p, C.c_int,
                                     i64p, i32p, u8p, C.c_int32, i64p, f64p, u8p, u8p, C.c_int,
                                     C.c_int64, i32p, i32p, i32p, i32p]
+
+    # finance
+    def fin(self, seed, **cfg):
+        return RefFin(self, fin_cfg(**cfg), seed)
+
+    def fin_run_batch(self, master, replicas, steps, threads=0, **cfg):
+        c = fin_cfg(**cfg)
+        out = np.zeros((replicas, steps, c.books, 6))
+        wall = self.lib.ref_fin_run_batch(C.byref(c), master, replicas, steps, threads, _p(out, f64p))
+        if wall < 0:
+            raise ValueError("bad finance config")
+        return out, wall
+
+    def fin_match(self, book: dict, last_price: float):
+        """match_book on a book (dict of BOOK_FIELDS + next_id): (book', fills, scalars)."""
+        b = {k: np.array(book[k], dt) for k, dt in BOOK_FIELDS}
+        cap = b["active"].size
+        ft, fs, fq = (np.zeros(2 * cap + 1, np.int64) for _ in range(3))
+        fa = np.zeros(2 * cap + 1)
+        sc = np.zeros(6)
+        n = self.lib.ref_fin_match(cap, last_price, *(_p(b[k], t) for k, t in (
+            ("active", u8p), ("ids", i64p), ("trader", i64p), ("side", i64p), ("price", f64p),
+            ("qty", i64p), ("placed", i64p))), int(book.get("next_id", 0)), _p(ft, i64p),
+            _p(fs, i64p), _p(fq, i64p), _p(fa, f64p), _p(sc, f64p))
+        if n < 0:
+            raise ValueError("match_book failed")
+        fills = {"trader": ft[:n], "side": fs[:n], "qty": fq[:n], "amount": fa[:n]}
+        return b, fills, sc
 
     # traffic
     def traffic(self, length, period=10, green_fraction=0.5, seed=0):
@@ -733,3 +837,87 @@ class RefTraffic:
                                       C.byref(na))
         d.update(occupancy=occ, next_id=nid.value, num_active=na.value)
         return d
+
+
+class OracleFin:
+    """FinanceModel restated in C (orc_fin_*)."""
+
+    def __init__(self, o: Oracle, cfg: FinCfg, seed):
+        self.o = o
+        self.cfg = cfg
+        self.h = o.lib.orc_fin_create(C.byref(cfg), seed)
+        if not self.h:
+            raise ValueError("bad finance config")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.o.lib.orc_fin_free(self.h)
+            self.h = None
+
+    def step(self, t):
+        self.o.lib.orc_fin_step(self.h, t)
+
+    def metrics(self):
+        out = np.zeros((self.cfg.books, 6))
+        self.o.lib.orc_fin_metrics(self.h, _p(out, f64p))
+        return out
+
+    def book(self, k):
+        b = self.h.contents.books[k]
+        n = b.capacity
+        d = {name: np.ctypeslib.as_array(getattr(b, name), (n,)).copy() for name, _ in BOOK_FIELDS}
+        d.update(last_price=b.last_price, dropped=b.dropped, volume=b.volume, next_id=b.next_id,
+                 num_active=b.num_active)
+        return d
+
+    def traders(self):
+        m = self.h.contents
+        T, K = self.cfg.traders, self.cfg.books
+        cash = np.ctypeslib.as_array(m.cash, (T + 1,))[:T].copy()
+        hold = np.ctypeslib.as_array(m.holdings, (K * T + 1,))[:K * T].reshape(K, T).copy()
+        return cash, hold
+
+
+class RefFin:
+    """The reference FinanceModel (oracle/_ref)."""
+
+    def __init__(self, r: Reference, cfg: FinCfg, seed):
+        self.r = r
+        self.cfg = cfg
+        self.h = r.lib.ref_fin_create(C.byref(cfg), seed)
+        if not self.h:
+            raise ValueError("bad finance config")
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.r.lib.ref_fin_free(self.h)
+            self.h = None
+
+    def step(self, t):
+        self.r.lib.ref_fin_step(self.h, t)
+
+    def run(self, t0, steps):
+        return self.r.lib.ref_fin_run(self.h, t0, steps)
+
+    def metrics(self):
+        out = np.zeros((self.cfg.books, 6))
+        self.r.lib.ref_fin_metrics(self.h, _p(out, f64p))
+        return out
+
+    def book(self, k):
+        n = self.cfg.book_capacity
+        d = {name: np.zeros(n, dt) for name, dt in BOOK_FIELDS}
+        sc = np.zeros(6)
+        self.r.lib.ref_fin_export_book(self.h, k, *(_p(d[name], t) for name, t in (
+            ("active", u8p), ("ids", i64p), ("trader", i64p), ("side", i64p), ("price", f64p),
+            ("qty", i64p), ("placed", i64p))), _p(sc, f64p))
+        d.update(last_price=sc[0], dropped=int(sc[1]), volume=int(sc[2]), next_id=int(sc[4]),
+                 num_active=int(sc[5]))
+        return d
+
+    def traders(self):
+        T, K = self.cfg.traders, self.cfg.books
+        cash = np.zeros(T + 1)
+        hold = np.zeros(K * T + 1, np.int64)
+        self.r.lib.ref_fin_export_traders(self.h, _p(cash, f64p), _p(hold, i64p))
+        return cash[:T], hold[:K * T].reshape(K, T)

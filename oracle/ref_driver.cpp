@@ -11,6 +11,7 @@
 //   * set_agents_rm / _sci / _mask, select, sort     include/abmx/kernels.hpp:47-106
 //   * spawn_agents / remove_agents / step_agents    include/abmx/lifecycle.hpp:54-86
 //   * TrafficModel / step_road / resolve_conflicts  include/abmx/models/traffic.hpp:60-110
+//   * FinanceModel / match_book / run_batch          include/abmx/models/finance.hpp:21-97
 // Nothing here re-implements reference behaviour; every call forwards.
 #include <chrono>
 #include <cstdint>
@@ -23,6 +24,7 @@
 #include "abmx/lifecycle.hpp"
 #include "abmx/models/predation.hpp"
 #include "abmx/models/traffic.hpp"
+#include "abmx/models/finance.hpp"
 #include "abmx/rng.hpp"
 #include "abmx/simd/kernels.hpp"
 
@@ -563,6 +565,136 @@ double ref_traffic_run_batch(int64_t length, int64_t period, double green_fracti
             size_t k = 0;
             for (const auto& row : tr.rows)
                 for (double v : row.values) metrics_out[k++] = v;
+        }
+        return wall;
+    } catch (const std::exception&) {
+        return -1.0;
+    }
+}
+
+
+// ---------------------------------------------------------------- finance (finance.hpp)
+struct ref_fin_config {
+    int64_t books, traders, book_capacity;
+    double p_order, delta;
+    int64_t qmax, max_order_age;
+    double init_price;
+};
+namespace {
+FinanceConfig fin_cfg(const ref_fin_config* c) {
+    FinanceConfig f;
+    f.books = c->books;
+    f.traders = c->traders;
+    f.book_capacity = c->book_capacity;
+    f.p_order = c->p_order;
+    f.delta = c->delta;
+    f.qmax = c->qmax;
+    f.max_order_age = c->max_order_age;
+    f.init_price = c->init_price;
+    return f;
+}
+void book_to(const Book& b, uint8_t* active, int64_t* ids, int64_t* trader, int64_t* side, double* price,
+             int64_t* qty, int64_t* placed, double* scalars /* last_price, dropped, volume, clearing, next_id, num_active */) {
+    const auto n = static_cast<size_t>(b.orders.capacity());
+    for (size_t i = 0; i < n; ++i) {
+        active[i] = b.orders.active()[i];
+        ids[i] = b.orders.ids()[i];
+        trader[i] = b.orders.state().ints("trader")[i];
+        side[i] = b.orders.state().ints("side")[i];
+        price[i] = b.orders.state().reals("price")[i];
+        qty[i] = b.orders.state().ints("qty")[i];
+        placed[i] = b.orders.state().ints("placed")[i];
+    }
+    scalars[0] = b.last_price;
+    scalars[1] = static_cast<double>(b.dropped_this_step);
+    scalars[2] = static_cast<double>(b.last_trades.volume);
+    scalars[3] = b.last_trades.clearing_price;
+    scalars[4] = static_cast<double>(b.orders.next_id());
+    scalars[5] = static_cast<double>(b.orders.num_active());
+}
+}  // namespace
+
+void* ref_fin_create(const ref_fin_config* c, uint64_t seed) {
+    try {
+        return new FinanceModel(fin_cfg(c), RngState{seed});
+    } catch (const std::exception&) {
+        return nullptr;
+    }
+}
+void ref_fin_free(void* h) { delete static_cast<FinanceModel*>(h); }
+void ref_fin_step(void* h, int64_t t) { static_cast<FinanceModel*>(h)->step(t); }
+double ref_fin_run(void* h, int64_t t0, int64_t steps) {
+    auto* m = static_cast<FinanceModel*>(h);
+    const auto a = std::chrono::steady_clock::now();
+    for (int64_t t = t0; t < t0 + steps; ++t) m->step(t);
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+}
+void ref_fin_metrics(void* h, double* rows) {
+    std::vector<std::vector<double>> out;
+    static_cast<FinanceModel*>(h)->collect_metrics(out);
+    size_t k = 0;
+    for (const auto& row : out)
+        for (double v : row) rows[k++] = v;
+}
+void ref_fin_export_book(void* h, int32_t book, uint8_t* active, int64_t* ids, int64_t* trader, int64_t* side,
+                         double* price, int64_t* qty, int64_t* placed, double* scalars) {
+    book_to(static_cast<FinanceModel*>(h)->market().books[static_cast<size_t>(book)], active, ids, trader, side,
+            price, qty, placed, scalars);
+}
+void ref_fin_export_traders(void* h, double* cash, int64_t* holdings /* [books][traders] */) {
+    const MarketState& s = static_cast<FinanceModel*>(h)->market();
+    const auto n = static_cast<size_t>(s.traders.capacity());
+    for (size_t i = 0; i < n; ++i) cash[i] = s.traders.state().reals("cash")[i];
+    for (size_t k = 0; k < s.books.size(); ++k)
+        for (size_t i = 0; i < n; ++i) holdings[k * n + i] = s.traders.state().ints("holdings_" + std::to_string(k))[i];
+}
+// match_book on a book given as arrays (capacity cap, last price); book arrays are updated,
+// fills written (trader, side, qty, amount); returns the number of fills, -1 on error.
+int32_t ref_fin_match(int32_t cap, double last_price, uint8_t* active, int64_t* ids, int64_t* trader, int64_t* side,
+                      double* price, int64_t* qty, int64_t* placed, int64_t next_id, int64_t* f_trader,
+                      int64_t* f_side, int64_t* f_qty, double* f_amount, double* scalars) {
+    try {
+        Book b = Book::empty(cap, 0, last_price);
+        Index na = 0;
+        for (int32_t i = 0; i < cap; ++i) {
+            const auto u = static_cast<size_t>(i);
+            b.orders.active_mut()[u] = active[i];
+            b.orders.ids_mut()[u] = ids[i];
+            b.orders.state_mut().ints("trader")[u] = trader[i];
+            b.orders.state_mut().ints("side")[u] = side[i];
+            b.orders.state_mut().reals("price")[u] = price[i];
+            b.orders.state_mut().ints("qty")[u] = qty[i];
+            b.orders.state_mut().ints("placed")[u] = placed[i];
+            na += active[i] ? 1 : 0;
+        }
+        b.orders.set_num_active(na);
+        b.orders.set_next_id(next_id);
+        b.last_price = last_price;
+        auto [out, summary] = match_book(b);
+        book_to(out, active, ids, trader, side, price, qty, placed, scalars);
+        for (size_t k = 0; k < summary.fills.size(); ++k) {
+            f_trader[k] = summary.fills[k].trader;
+            f_side[k] = summary.fills[k].side;
+            f_qty[k] = summary.fills[k].qty;
+            f_amount[k] = summary.fills[k].amount;
+        }
+        return static_cast<int32_t>(summary.fills.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+double ref_fin_quantize(double raw) { return quantize_price(raw); }
+double ref_fin_run_batch(const ref_fin_config* c, uint64_t master, int32_t replicas, int64_t steps, int threads,
+                         double* rows) {
+    try {
+        const auto model = FinanceModel::descriptor(fin_cfg(c));
+        const auto seeds = replica_seeds(RngState{master}, replicas);
+        double wall = 0.0;
+        const Trajectory tr = run_batch(model, seeds, steps, threads, &wall);
+        if (rows) {
+            size_t k = 0;
+            for (const auto& row : tr.rows)
+                for (double v : row.values) rows[k++] = v;
         }
         return wall;
     } catch (const std::exception&) {

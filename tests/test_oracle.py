@@ -223,3 +223,29 @@ def test_traffic_golden(oracle):
     got = oracle.traffic_run_batch(b["length"], b["period"], b["green_fraction"], b["master"],
                                    b["replicas"], b["steps"])
     assert np.array_equal(got, np.array(b["metrics"]))
+
+
+def test_finance_golden(oracle):
+    """FinanceModel trajectories (metrics every step, final books, cash, holdings), match_book on
+    random books (price-time priority, partial fills, exhausted removal), run_batch rows and
+    quantize_price (finance.cpp): the C restatement matches the reference bit for bit."""
+    import pyoracle
+    g = load("finance.json")
+    for x, want in g["quantize"]:
+        assert oracle.quantize_price(x) == want
+    for mc in g["models"]:
+        m = oracle.fin(mc["seed"], **mc["cfg"])
+        for t in range(1, mc["steps"] + 1):
+            m.step(t)
+            assert m.metrics().tolist() == mc["metrics"][t - 1], (mc["cfg"], t)
+        cash, hold = m.traders()
+        assert np.array_equal(cash.view(np.uint64), arr(mc["cash"], np.uint64))
+        assert np.array_equal(hold.ravel(), arr(mc["holdings"], np.int64))
+        for k, bk in enumerate(mc["books"]):
+            got = m.book(k)
+            for name, dt in pyoracle.BOOK_FIELDS:
+                assert np.array_equal(got[name], arr(bk[name], dt)), (mc["cfg"], k, name)
+            assert got["next_id"] == bk["next_id"] and got["last_price"] == bk["last_price"]
+    b = g["batch"]
+    got = oracle.fin_run_batch(b["master"], b["replicas"], b["steps"], **b["cfg"])
+    assert np.array_equal(got, np.array(b["rows"]))
