@@ -308,6 +308,54 @@ int abmx_traffic_run_batch_path(const abmx_traffic_config* cfg, uint64_t master,
                                 int32_t replica_begin, int32_t count, int64_t steps,
                                 int32_t path, double* metrics_out, double* kernel_ms);
 
+/* ======================================================================= 6. finance
+ * FinanceModel (include/abmx/models/finance.hpp:21-97, src/models/finance.cpp) for `markets`
+ * independent markets (seeds[m] = replica seed). abmx_finance_config has the field order of
+ * FinanceConfig (finance.hpp:13-22). One CTA per (market, book) with the book resident in shared
+ * memory: book_capacity and traders up to 4096 (CapacityError beyond). Metrics rows are
+ * collect_metrics' (finance.cpp:262-276): book_id, price, n_active_buys, n_active_sells, volume,
+ * orders_dropped — one row per book. */
+typedef struct abmx_finance_config {
+    int64_t books, traders, book_capacity;
+    double p_order, delta;
+    int64_t qmax, max_order_age;
+    double init_price;
+} abmx_finance_config;
+
+typedef struct abmx_finance abmx_finance;
+
+int abmx_finance_create(const abmx_finance_config* cfg, const uint64_t* seeds, int32_t markets,
+                        abmx_finance** out);
+int abmx_finance_destroy(abmx_finance* h);
+/* step_market at t on every market (finance.cpp:203-247) */
+int abmx_finance_step(abmx_finance* h, int64_t t);
+/* steps t0 .. t0+steps-1 in one launch; rows (nullable, host) [markets][steps][books][6] */
+int abmx_finance_run(abmx_finance* h, int64_t t0, int64_t steps, double* rows);
+/* collect_metrics of the last step: [markets][books][6] */
+int abmx_finance_metrics(abmx_finance* h, double* rows);
+/* a book in the reference layout; scalars[6] = last_price, dropped_this_step, last volume,
+ * last clearing price, next_id, num_active */
+int abmx_finance_export_book(abmx_finance* h, int32_t market, int32_t book, uint8_t* active,
+                             int64_t* ids, int64_t* trader, int64_t* side, double* price,
+                             int64_t* qty, int64_t* placed, double* scalars);
+int abmx_finance_import_book(abmx_finance* h, int32_t market, int32_t book,
+                             const uint8_t* active, const int64_t* ids, const int64_t* trader,
+                             const int64_t* side, const double* price, const int64_t* qty,
+                             const int64_t* placed, int64_t next_id, double last_price);
+/* traders' cash [traders] and holdings [books][traders] */
+int abmx_finance_export_traders(abmx_finance* h, int32_t market, double* cash,
+                                int64_t* holdings);
+/* match_book (finance.cpp:125-190) on one host book (arrays updated in place); fills in the
+ * reference order (buys in priority order, then sells); returns the fill count, or -code */
+int32_t abmx_finance_match(int32_t capacity, double last_price, uint8_t* active, int64_t* ids,
+                           int64_t* trader, int64_t* side, double* price, int64_t* qty,
+                           int64_t* placed, int64_t* f_trader, int64_t* f_side, int64_t* f_qty,
+                           double* f_amount, double* scalars);
+double abmx_finance_quantize_price(double raw); /* finance.cpp:56-61 */
+/* run_batch of FinanceModel: rows [count][steps][books][6]; kernel_ms nullable */
+int abmx_finance_run_batch(const abmx_finance_config* cfg, uint64_t master, int32_t replica_begin,
+                           int32_t count, int64_t steps, double* rows, double* kernel_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,845 @@
+// finance.cu — the limit-order-book market (src/models/finance.cpp) on sm_100a for M markets at
+// once, bit-exact with the reference.
+//
+// Books never read trader state (placement reads only the trader params and the book's last
+// price) and holdings_k is written only by book k, so every (market, book) pair is independent:
+// ONE CTA per book, the whole book resident in shared memory across the steps of a launch.
+// Cash is the only value summed across books; every amount is qty x (a multiple of 2^-8) and the
+// sums stay far below 2^45, so all additions are exact and their order cannot change a bit —
+// per-book partial sums are folded into the traders with double atomics.
+//
+// A step of one book (finance.cpp:203-247):
+//   place    traders in order: bernoulli(4i, p), side (4i+1), epsilon (4i+2), qty (4i+3) from
+//            seed.split(8).split(t).split(book); valid rows rank-matched into the lowest free slots
+//            (block scans of the row and free-slot masks), ids next_id + k, placed = t.
+//   match    active orders sorted by (side, price desc for buys / asc for sells, placed, id) with
+//            an in-CTA bitonic sort; cumulative quantities by block scan; the executed volume =
+//            max over buys of min(buy cum, sell cum at the last sell priced <= the buy) (binary
+//            search per buy); marginal orders, midpoint clearing price; fill of sorted order j =
+//            min(qty_j, max(0, volume - cum_{j-1})) — the reference's sequential fill loop in
+//            closed form; exhausted orders removed.
+//   cancel   t - placed >= max_order_age.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/abmx_cuda.h"
+#include "abmx_device.cuh"
+#include "abmx_internal.h"
+
+using namespace abmx_dev;
+
+namespace abmx_fin {
+
+constexpr int kNT = 256;
+constexpr double kTick = 0x1p-7;  // finance.hpp:37
+constexpr unsigned short kPad = 0xFFFF;
+
+struct BookS {  // per-book scalars
+    double last_price, clearing;
+    long long next_id, dropped, volume;
+    int num_active, pad;
+};
+
+struct FParams {
+    int M, K, T, cap, sort_n;  // sort_n: power of two >= cap
+    double p_order, delta, init_price;
+    long long qmax, max_age;
+    long long t0, steps;
+    int match_only;  // 1: one match_book pass, fills recorded (no placement, no cancel)
+    const unsigned long long* seeds;  // [M]
+    // books [M][K][cap]
+    uint8_t* active;
+    long long* ids;
+    int* trader;
+    uint8_t* side;
+    double* price;
+    int* qty;
+    long long* placed;
+    BookS* bs;           // [M][K]
+    double* cash;        // [M][T]
+    long long* holdings; // [M][K][T]
+    double* metrics;     // [M][steps][K][6]
+    // match_only outputs (book 0 of market 0)
+    long long* f_trader;
+    long long* f_side;
+    long long* f_qty;
+    double* f_amount;
+    int* n_fills;
+};
+
+__device__ __forceinline__ double quantize(double raw) {  // finance.cpp:56-61
+    double p = __dmul_rn(round(raw / kTick), kTick);
+    if (p < kTick) p = kTick;
+    return p;
+}
+
+struct Smem {
+    uint8_t* act;
+    long long* id;
+    int* tr;
+    uint8_t* sd;
+    double* pr;
+    int* q;
+    long long* pl;
+    unsigned short* list;  // sorted order (sort_n entries)
+    long long* cum;        // cumulative qty along the sorted list (cap entries)
+    // placement rows (T entries)
+    int* rq;
+    double* rp;
+    uint8_t* rs;
+    int* rt;
+    double* dcash;       // [T] cash delta of this book
+    long long* dhold;    // [T] holdings delta of this book
+};
+
+// sort order: buys before sells; buys by price desc, sells by price asc; then placed, id, slot
+__device__ __forceinline__ bool before(const Smem& S, unsigned short a, unsigned short b) {
+    if (b == kPad) return a != kPad;
+    if (a == kPad) return false;
+    if (S.sd[a] != S.sd[b]) return S.sd[a] < S.sd[b];
+    if (S.pr[a] != S.pr[b]) return S.sd[a] == 0 ? S.pr[a] > S.pr[b] : S.pr[a] < S.pr[b];
+    if (S.pl[a] != S.pl[b]) return S.pl[a] < S.pl[b];
+    if (S.id[a] != S.id[b]) return S.id[a] < S.id[b];
+    return a < b;
+}
+
+__device__ __forceinline__ void reset_slot(const Smem& S, int i) {  // agent_set.cpp:45-58
+    S.act[i] = 0;
+    S.id[i] = 0;
+    S.tr[i] = 0;
+    S.sd[i] = 0;
+    S.pr[i] = 0.0;
+    S.q[i] = 0;
+    S.pl[i] = 0;
+}
+
+template <class T>
+__device__ __forceinline__ T block_sum_nt(T v, T* red) {
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    T s = 0;
+    for (int w = 0; w < kNT / 32; ++w) s += red[w];
+    __syncthreads();
+    return s;
+}
+
+__global__ void __launch_bounds__(kNT) k_fin(FParams P) {
+    extern __shared__ unsigned char smraw[];
+    __shared__ unsigned long long s_scan[kNT / 32 + 1];
+    __shared__ long long s_red[kNT / 32];
+    __shared__ int s_n, s_nb;
+    __shared__ long long s_vol;
+    const int m = blockIdx.x / P.K, k = blockIdx.x % P.K;
+    const int cap = P.cap, T = P.T, N = P.sort_n, tid = threadIdx.x;
+    // shared layout (8-byte fields first)
+    Smem S;
+    unsigned char* p = smraw;
+    S.id = reinterpret_cast<long long*>(p);
+    p += 8 * cap;
+    S.pr = reinterpret_cast<double*>(p);
+    p += 8 * cap;
+    S.pl = reinterpret_cast<long long*>(p);
+    p += 8 * cap;
+    S.cum = reinterpret_cast<long long*>(p);
+    p += 8 * cap;
+    S.rp = reinterpret_cast<double*>(p);
+    p += 8 * T;
+    S.dcash = reinterpret_cast<double*>(p);
+    p += 8 * T;
+    S.dhold = reinterpret_cast<long long*>(p);
+    p += 8 * T;
+    S.tr = reinterpret_cast<int*>(p);
+    p += 4 * cap;
+    S.q = reinterpret_cast<int*>(p);
+    p += 4 * cap;
+    S.rq = reinterpret_cast<int*>(p);
+    p += 4 * T;
+    S.rt = reinterpret_cast<int*>(p);
+    p += 4 * T;
+    S.list = reinterpret_cast<unsigned short*>(p);
+    p += 2 * N;
+    S.act = p;
+    p += cap;
+    S.sd = p;
+    p += cap;
+    S.rs = p;
+    // load the book
+    const size_t bo = (static_cast<size_t>(m) * P.K + k) * cap;
+    for (int i = tid; i < cap; i += kNT) {
+        S.act[i] = P.active[bo + i];
+        S.id[i] = P.ids[bo + i];
+        S.tr[i] = P.trader[bo + i];
+        S.sd[i] = P.side[bo + i];
+        S.pr[i] = P.price[bo + i];
+        S.q[i] = P.qty[bo + i];
+        S.pl[i] = P.placed[bo + i];
+    }
+    for (int i = tid; i < T; i += kNT) {
+        S.dcash[i] = 0.0;
+        S.dhold[i] = 0;
+    }
+    BookS B = P.bs[static_cast<size_t>(m) * P.K + k];
+    __syncthreads();
+    const unsigned long long root = split(P.seeds[m], 8);  // FinancePlace
+    const long long t_end = P.match_only ? P.t0 + 1 : P.t0 + P.steps;
+    for (long long t = P.t0; t < t_end; ++t) {
+        if (!P.match_only) {
+            // ---------------- place_orders (finance.cpp:74-123)
+            const unsigned long long key = split(split(root, static_cast<unsigned long long>(t)),
+                                                 static_cast<unsigned long long>(k));
+            unsigned long long carry = 0;
+            for (int i0 = 0; i0 < T; i0 += kNT) {  // valid rows, compacted in trader order
+                const int i = i0 + tid;
+                bool v = false;
+                int sd = 0, qt = 0;
+                double pr = 0.0;
+                if (i < T) {
+                    const unsigned long long base = 4ULL * static_cast<unsigned long long>(i);
+                    v = uniform_double(key, base) < P.p_order;
+                    if (v) {
+                        sd = static_cast<int>(uniform_span(key, base + 1, 2));
+                        const double eps = __dadd_rn(-P.delta, __dmul_rn(__dmul_rn(2.0, P.delta), uniform_double(key, base + 2)));
+                        qt = 1 + static_cast<int>(uniform_span(key, base + 3, static_cast<unsigned long long>(P.qmax)));
+                        pr = quantize(__dmul_rn(B.last_price, __dadd_rn(1.0, eps)));
+                    }
+                }
+                unsigned long long tot;
+                const unsigned long long ex = block_excl_scan<kNT>(v ? 1ULL : 0ULL, s_scan, &tot);
+                if (v) {
+                    const int r = static_cast<int>(carry + ex);
+                    S.rt[r] = i;
+                    S.rs[r] = static_cast<uint8_t>(sd);
+                    S.rp[r] = pr;
+                    S.rq[r] = qt;
+                }
+                carry += tot;
+                __syncthreads();
+            }
+            const int q = static_cast<int>(carry);
+            // k-th free slot <- k-th valid row (lifecycle.cpp:144-195)
+            unsigned long long fcarry = 0;
+            for (int i0 = 0; i0 < cap && static_cast<long long>(fcarry) < q; i0 += kNT) {
+                const int i = i0 + tid;
+                const bool fr = i < cap && !S.act[i];
+                unsigned long long tot;
+                const unsigned long long ex = block_excl_scan<kNT>(fr ? 1ULL : 0ULL, s_scan, &tot);
+                const long long r = static_cast<long long>(fcarry + ex);
+                if (fr && r < q) {
+                    S.act[i] = 1;
+                    S.id[i] = B.next_id + r;
+                    S.tr[i] = S.rt[r];
+                    S.sd[i] = S.rs[r];
+                    S.pr[i] = S.rp[r];
+                    S.q[i] = S.rq[r];
+                    S.pl[i] = t;
+                }
+                fcarry += tot;
+                __syncthreads();
+            }
+            const int spawned = static_cast<long long>(fcarry) < q ? static_cast<int>(fcarry) : q;
+            B.next_id += spawned;
+            B.num_active += spawned;
+            B.dropped = q - spawned;
+        }
+        // ---------------- match_book (finance.cpp:125-190)
+        {
+            // active orders, then a bitonic sort in priority order
+            unsigned long long carry = 0;
+            for (int i0 = 0; i0 < N; i0 += kNT) {
+                const int i = i0 + tid;
+                const bool a = i < cap && S.act[i];
+                unsigned long long tot;
+                const unsigned long long ex = block_excl_scan<kNT>(a ? 1ULL : 0ULL, s_scan, &tot);
+                if (a) S.list[carry + ex] = static_cast<unsigned short>(i);
+                carry += tot;
+                __syncthreads();
+            }
+            const int n = static_cast<int>(carry);
+            for (int i = n + tid; i < N; i += kNT) S.list[i] = kPad;
+            int ns2 = 1;
+            while (ns2 < n) ns2 <<= 1;  // sort only the first power of two covering n
+            __syncthreads();
+            for (int size = 2; size <= ns2; size <<= 1)
+                for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                    for (int j = tid; j < ns2 / 2; j += kNT) {
+                        const int lo = 2 * j - (j & (stride - 1));
+                        const int hi = lo + stride;
+                        const bool up = (lo & size) == 0;
+                        const unsigned short a = S.list[lo], b = S.list[hi];
+                        if (before(S, b, a) == up) {
+                            S.list[lo] = b;
+                            S.list[hi] = a;
+                        }
+                    }
+                    __syncthreads();
+                }
+            // number of buys, cumulative quantities along the sorted list (per side)
+            long long nbl = 0;
+            unsigned long long qcarry = 0;
+            for (int i0 = 0; i0 < n || (n == 0 && i0 == 0); i0 += kNT) {
+                const int i = i0 + tid;
+                const unsigned short s = i < n ? S.list[i] : kPad;
+                const bool buy = s != kPad && S.sd[s] == 0;
+                nbl += buy;
+                unsigned long long tot;
+                const unsigned long long ex =
+                    block_excl_scan<kNT>(s != kPad ? static_cast<unsigned long long>(S.q[s]) : 0ULL, s_scan, &tot);
+                if (s != kPad) S.cum[i] = static_cast<long long>(qcarry + ex) + S.q[s];
+                qcarry += tot;
+                __syncthreads();
+                if (n == 0) break;
+            }
+            const long long nb = block_sum_nt<long long>(nbl, s_red);
+            if (tid == 0) {
+                s_n = n;
+                s_nb = static_cast<int>(nb);
+            }
+            __syncthreads();
+            const int nbuy = s_nb, nsell = s_n - s_nb;
+            const long long btot = nbuy > 0 ? S.cum[nbuy - 1] : 0;  // sells' cum = cum - btot
+            // executed volume: max over buys of min(buy cum, sell cum at upper_bound(buy price))
+            long long vmax = 0;
+            if (nbuy > 0 && nsell > 0)
+                for (int i = tid; i < nbuy; i += kNT) {
+                    const double bp = S.pr[S.list[i]];
+                    int lo = 0, hi = nsell;  // first sell with price > bp
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (bp < S.pr[S.list[nbuy + mid]])
+                            hi = mid;
+                        else
+                            lo = mid + 1;
+                    }
+                    if (lo == 0) continue;
+                    const long long bc = S.cum[i], sc = S.cum[nbuy + lo - 1] - btot;
+                    const long long v = bc < sc ? bc : sc;
+                    if (v > vmax) vmax = v;
+                }
+            for (int d = 16; d > 0; d >>= 1) {
+                const long long o = __shfl_xor_sync(0xffffffffu, vmax, d);
+                vmax = o > vmax ? o : vmax;
+            }
+            if ((tid & 31) == 0) s_red[tid >> 5] = vmax;
+            __syncthreads();
+            if (tid == 0) {
+                long long v = 0;
+                for (int w = 0; w < kNT / 32; ++w) v = s_red[w] > v ? s_red[w] : v;
+                s_vol = v;
+            }
+            __syncthreads();
+            const long long volume = s_vol;
+            B.volume = 0;
+            if (volume > 0) {
+                // marginal orders: first cum >= volume on each side
+                int mb = 0, ms = 0;
+                {
+                    int lo = 0, hi = nbuy - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (S.cum[mid] >= volume)
+                            hi = mid;
+                        else
+                            lo = mid + 1;
+                    }
+                    mb = lo;
+                    lo = 0;
+                    hi = nsell - 1;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (S.cum[nbuy + mid] - btot >= volume)
+                            hi = mid;
+                        else
+                            lo = mid + 1;
+                    }
+                    ms = lo;
+                }
+                const double clearing = __dadd_rn(S.pr[S.list[mb]], S.pr[S.list[nbuy + ms]]) / 2.0;
+                __syncthreads();  // every thread has read the sorted prices before fills reset slots
+                // fills: sorted order j gets min(qty_j, volume - cum_{j-1}) while positive
+                for (int j = tid; j < n; j += kNT) {
+                    const unsigned short s = S.list[j];
+                    const bool buy = j < nbuy;
+                    const long long before_j = buy ? (j > 0 ? S.cum[j - 1] : 0) : (j > nbuy ? S.cum[j - 1] - btot : 0);
+                    const long long rem = volume - before_j;
+                    if (rem <= 0) continue;
+                    const long long f = S.q[s] < rem ? S.q[s] : rem;
+                    const double amount = __dmul_rn(static_cast<double>(f), clearing);
+                    const int tr = S.tr[s];
+                    if (P.match_only) {
+                        const int fi = buy ? j : (mb + 1) + (j - nbuy);
+                        P.f_trader[fi] = tr;
+                        P.f_side[fi] = buy ? 0 : 1;
+                        P.f_qty[fi] = f;
+                        P.f_amount[fi] = amount;
+                    } else if (tr >= 0 && tr < T) {
+                        atomicAdd(&S.dcash[tr], buy ? -amount : amount);
+                        atomicAdd(reinterpret_cast<unsigned long long*>(&S.dhold[tr]),
+                                  static_cast<unsigned long long>(buy ? f : -f));
+                    }
+                    S.q[s] -= static_cast<int>(f);
+                    if (S.q[s] == 0) reset_slot(S, s);  // exhausted: remove_agents
+                }
+                if (P.match_only && tid == 0) *P.n_fills = (mb + 1) + (ms + 1);
+                B.last_price = clearing;
+                B.clearing = clearing;
+                B.volume = volume;
+            } else if (P.match_only && tid == 0) {
+                *P.n_fills = 0;
+            }
+            __syncthreads();
+        }
+        if (P.match_only) break;
+        // ---------------- cancel at the age limit (finance.cpp:236-245); count the book
+        long long nbl = 0, nsl = 0, na = 0;
+        for (int i = tid; i < cap; i += kNT) {
+            if (!S.act[i]) continue;
+            if (t - S.pl[i] >= P.max_age) {
+                reset_slot(S, i);
+                continue;
+            }
+            ++na;
+            if (S.sd[i] == 0)
+                ++nbl;
+            else
+                ++nsl;
+        }
+        const long long nb = block_sum_nt<long long>(nbl, s_red);
+        const long long nsv = block_sum_nt<long long>(nsl, s_red);
+        B.num_active = static_cast<int>(block_sum_nt<long long>(na, s_red));
+        if (tid == 0) {  // collect_metrics (finance.cpp:262-276)
+            double* row = P.metrics + ((static_cast<size_t>(m) * P.steps + (t - P.t0)) * P.K + k) * 6;
+            row[0] = static_cast<double>(k);
+            row[1] = B.last_price;
+            row[2] = static_cast<double>(nb);
+            row[3] = static_cast<double>(nsv);
+            row[4] = static_cast<double>(B.volume);
+            row[5] = static_cast<double>(B.dropped);
+        }
+        __syncthreads();
+    }
+    // store the book, fold this book's settlement into the traders
+    for (int i = tid; i < cap; i += kNT) {
+        P.active[bo + i] = S.act[i];
+        P.ids[bo + i] = S.id[i];
+        P.trader[bo + i] = S.tr[i];
+        P.side[bo + i] = S.sd[i];
+        P.price[bo + i] = S.pr[i];
+        P.qty[bo + i] = S.q[i];
+        P.placed[bo + i] = S.pl[i];
+    }
+    if (!P.match_only)
+        for (int i = tid; i < T; i += kNT) {
+            if (S.dcash[i] != 0.0) atomicAdd(&P.cash[static_cast<size_t>(m) * T + i], S.dcash[i]);
+            P.holdings[(static_cast<size_t>(m) * P.K + k) * T + i] += S.dhold[i];
+        }
+    if (tid == 0) {
+        if (P.match_only) B.num_active = 0;  // recomputed on the host from the mask
+        P.bs[static_cast<size_t>(m) * P.K + k] = B;
+    }
+}
+
+__global__ void k_fin_init(FParams P, double last_price) {
+    const size_t nb = static_cast<size_t>(P.M) * P.K;
+    const size_t n0 = nb * P.cap, n1 = nb * P.T;
+    const size_t n = n0 > n1 ? n0 : n1;  // covers the orders, the books and every trader array
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        if (i < n0) {
+            P.active[i] = 0;
+            P.ids[i] = 0;
+            P.trader[i] = 0;
+            P.side[i] = 0;
+            P.price[i] = 0.0;
+            P.qty[i] = 0;
+            P.placed[i] = 0;
+        }
+        if (i < nb) P.bs[i] = BookS{last_price, 0.0, 0, 0, 0, 0, 0};
+        if (i < static_cast<size_t>(P.M) * P.T) P.cash[i] = 0.0;
+        if (i < n1) P.holdings[i] = 0;
+    }
+}
+
+}  // namespace abmx_fin
+
+// ====================================================================== host side
+using namespace abmx_fin;
+
+#define CKF(x)                                                                        \
+    do {                                                                              \
+        cudaError_t e_ = (x);                                                         \
+        if (e_ != cudaSuccess) {                                                      \
+            abmx_internal::set_error(std::string(#x) + ": " + cudaGetErrorString(e_)); \
+            return ABMX_E_CUDA;                                                       \
+        }                                                                             \
+    } while (0)
+
+namespace {
+
+double quantize_host(double raw) {
+    double p = std::round(raw / kTick) * kTick;
+    if (p < kTick) p = kTick;
+    return p;
+}
+
+int check_cfg(const abmx_finance_config& c) {
+    if (c.books < 1 || c.traders < 0 || c.book_capacity < 1) {
+        abmx_internal::set_error("finance: books/book_capacity must be >= 1, traders >= 0");  // config.cpp:210-211
+        return ABMX_E_DOMAIN;
+    }
+    if (c.p_order < 0.0 || c.p_order > 1.0) {
+        abmx_internal::set_error("finance: p_order must lie in [0, 1]");
+        return ABMX_E_DOMAIN;
+    }
+    if (c.qmax < 1) {
+        abmx_internal::set_error("finance: qmax must be >= 1");  // uniform_int(1, qmax+1) needs qmax >= 1
+        return ABMX_E_DOMAIN;
+    }
+    if (c.book_capacity > 4096 || c.traders > 4096) {
+        abmx_internal::set_error("finance: book_capacity and traders above 4096 are not supported "
+                                 "(one shared-memory-resident CTA per book)");
+        return ABMX_E_CAPACITY;
+    }
+    return ABMX_OK;
+}
+
+size_t fin_smem(const abmx_finance_config& c, int sort_n) {
+    const size_t cap = static_cast<size_t>(c.book_capacity), T = static_cast<size_t>(c.traders);
+    return 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 2 * cap + T + 64;
+}
+
+}  // namespace
+
+struct abmx_finance {
+    abmx_finance_config cfg{};
+    FParams P{};
+    cudaStream_t stream = nullptr;
+    std::vector<void*> allocs;
+    size_t smem = 0;
+    double* d_metrics = nullptr;
+    size_t metrics_bytes = 0;
+    long long last_steps = 0;
+    int M = 0;
+
+    ~abmx_finance() {
+        for (void* p : allocs) cudaFree(p);
+        if (d_metrics) cudaFree(d_metrics);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    int alloc(void** p, size_t bytes) {
+        cudaError_t e = cudaMalloc(p, bytes ? bytes : 16);
+        if (e != cudaSuccess) {
+            abmx_internal::set_error(std::string("cudaMalloc: ") + cudaGetErrorString(e));
+            return ABMX_E_CUDA;
+        }
+        allocs.push_back(*p);
+        return ABMX_OK;
+    }
+    int create(const abmx_finance_config& c, const uint64_t* seeds, int markets) {
+        int rc = check_cfg(c);
+        if (rc) return rc;
+        if (markets < 1) {
+            abmx_internal::set_error("markets must be >= 1");
+            return ABMX_E_DOMAIN;
+        }
+        cfg = c;
+        M = markets;
+        CKF(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+        memset(&P, 0, sizeof P);
+        P.M = M;
+        P.K = static_cast<int>(c.books);
+        P.T = static_cast<int>(c.traders);
+        P.cap = static_cast<int>(c.book_capacity);
+        P.sort_n = 1;
+        while (P.sort_n < P.cap) P.sort_n <<= 1;
+        P.p_order = c.p_order;
+        P.delta = c.delta;
+        P.init_price = c.init_price;
+        P.qmax = c.qmax;
+        P.max_age = c.max_order_age;
+        const size_t nb = static_cast<size_t>(M) * P.K, n = nb * P.cap;
+#define ALF(ptr, bytes)                                                 \
+    if ((rc = alloc(reinterpret_cast<void**>(&(ptr)), (bytes))) != 0) \
+        return rc;
+        unsigned long long* sd = nullptr;
+        ALF(sd, static_cast<size_t>(M) * 8);
+        ALF(P.active, n);
+        ALF(P.ids, n * 8);
+        ALF(P.trader, n * 4);
+        ALF(P.side, n);
+        ALF(P.price, n * 8);
+        ALF(P.qty, n * 4);
+        ALF(P.placed, n * 8);
+        ALF(P.bs, nb * sizeof(BookS));
+        ALF(P.cash, static_cast<size_t>(M) * P.T * 8);
+        ALF(P.holdings, nb * P.T * 8);
+        ALF(P.f_trader, static_cast<size_t>(P.cap) * 8 + 8);
+        ALF(P.f_side, static_cast<size_t>(P.cap) * 8 + 8);
+        ALF(P.f_qty, static_cast<size_t>(P.cap) * 8 + 8);
+        ALF(P.f_amount, static_cast<size_t>(P.cap) * 8 + 8);
+        ALF(P.n_fills, 8);
+#undef ALF
+        P.seeds = sd;
+        CKF(cudaMemcpy(sd, seeds, static_cast<size_t>(M) * 8, cudaMemcpyHostToDevice));
+        smem = fin_smem(c, P.sort_n);
+        if (smem > 220 * 1024) {
+            abmx_internal::set_error("finance: book_capacity / traders too large for one shared-memory book");
+            return ABMX_E_CAPACITY;
+        }
+        CKF(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_fin), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+        (void)cudaGetLastError();
+        k_fin_init<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(P, quantize_host(c.init_price));
+        abmx_internal::count_launch();
+        CKF(cudaGetLastError());
+        CKF(cudaStreamSynchronize(stream));
+        return ABMX_OK;
+    }
+    int launch(long long t0, long long steps, int match_only) {
+        const size_t mb = static_cast<size_t>(M) * static_cast<size_t>(steps > 0 ? steps : 1) * P.K * 6 * 8;
+        if (mb > metrics_bytes) {
+            CKF(cudaStreamSynchronize(stream));
+            if (d_metrics) cudaFree(d_metrics);
+            CKF(cudaMalloc(&d_metrics, mb));
+            metrics_bytes = mb;
+        }
+        P.metrics = d_metrics;
+        P.t0 = t0;
+        P.steps = steps;
+        P.match_only = match_only;
+        (void)cudaGetLastError();
+        const unsigned grid = match_only ? 1u : static_cast<unsigned>(M * P.K);
+        k_fin<<<grid, kNT, smem, stream>>>(P);
+        abmx_internal::count_launch();
+        CKF(cudaGetLastError());
+        last_steps = steps;
+        return ABMX_OK;
+    }
+};
+
+extern "C" {
+
+int abmx_finance_create(const abmx_finance_config* cfg, const uint64_t* seeds, int32_t markets,
+                        abmx_finance** out) {
+    if (!cfg || !seeds || !out) {
+        abmx_internal::set_error("null argument");
+        return ABMX_E_ARG;
+    }
+    auto* h = new abmx_finance();
+    const int rc = h->create(*cfg, seeds, markets);
+    if (rc) {
+        delete h;
+        *out = nullptr;
+        return rc;
+    }
+    *out = h;
+    return ABMX_OK;
+}
+int abmx_finance_destroy(abmx_finance* h) {
+    delete h;
+    return ABMX_OK;
+}
+int abmx_finance_run(abmx_finance* h, int64_t t0, int64_t steps, double* rows) {
+    if (!h) return ABMX_E_ARG;
+    if (steps <= 0) return ABMX_OK;
+    int rc = h->launch(t0, steps, 0);
+    if (rc) return rc;
+    if (rows) {
+        CKF(cudaMemcpyAsync(rows, h->d_metrics, static_cast<size_t>(h->M) * steps * h->P.K * 48, cudaMemcpyDeviceToHost,
+                            h->stream));
+        CKF(cudaStreamSynchronize(h->stream));
+    }
+    return ABMX_OK;
+}
+int abmx_finance_step(abmx_finance* h, int64_t t) { return abmx_finance_run(h, t, 1, nullptr); }
+int abmx_finance_metrics(abmx_finance* h, double* rows) {
+    if (!h) return ABMX_E_ARG;
+    const size_t per = static_cast<size_t>(h->P.K) * 6;
+    if (h->last_steps <= 0) {
+        for (int m = 0; m < h->M; ++m)
+            for (int k = 0; k < h->P.K; ++k) {
+                double* r = rows + (static_cast<size_t>(m) * h->P.K + k) * 6;
+                r[0] = k;
+                r[1] = quantize_host(h->cfg.init_price);
+                r[2] = r[3] = r[4] = r[5] = 0.0;
+            }
+        return ABMX_OK;
+    }
+    for (int m = 0; m < h->M; ++m)
+        CKF(cudaMemcpyAsync(rows + static_cast<size_t>(m) * per,
+                            h->d_metrics + (static_cast<size_t>(m) * h->last_steps + h->last_steps - 1) * per,
+                            per * 8, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaStreamSynchronize(h->stream));
+    return ABMX_OK;
+}
+int abmx_finance_export_book(abmx_finance* h, int32_t market, int32_t book, uint8_t* active, int64_t* ids,
+                             int64_t* trader, int64_t* side, double* price, int64_t* qty, int64_t* placed,
+                             double* scalars) {
+    if (!h) return ABMX_E_ARG;
+    if (market < 0 || market >= h->M || book < 0 || book >= h->P.K) {
+        abmx_internal::set_error("market / book index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    const size_t cap = static_cast<size_t>(h->P.cap);
+    const size_t bo = (static_cast<size_t>(market) * h->P.K + book) * cap;
+    std::vector<int> tr(cap), q(cap);
+    std::vector<uint8_t> sd(cap);
+    BookS B;
+    CKF(cudaMemcpyAsync(active, h->P.active + bo, cap, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(ids, h->P.ids + bo, cap * 8, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(tr.data(), h->P.trader + bo, cap * 4, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(sd.data(), h->P.side + bo, cap, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(price, h->P.price + bo, cap * 8, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(q.data(), h->P.qty + bo, cap * 4, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(placed, h->P.placed + bo, cap * 8, cudaMemcpyDeviceToHost, h->stream));
+    CKF(cudaMemcpyAsync(&B, h->P.bs + static_cast<size_t>(market) * h->P.K + book, sizeof B, cudaMemcpyDeviceToHost,
+                        h->stream));
+    CKF(cudaStreamSynchronize(h->stream));
+    int na = 0;
+    for (size_t i = 0; i < cap; ++i) {
+        trader[i] = tr[i];
+        side[i] = sd[i];
+        qty[i] = q[i];
+        na += active[i] ? 1 : 0;
+    }
+    if (scalars) {  // last_price, dropped, volume, clearing, next_id, num_active
+        scalars[0] = B.last_price;
+        scalars[1] = static_cast<double>(B.dropped);
+        scalars[2] = static_cast<double>(B.volume);
+        scalars[3] = B.clearing;
+        scalars[4] = static_cast<double>(B.next_id);
+        scalars[5] = na;
+    }
+    return ABMX_OK;
+}
+int abmx_finance_import_book(abmx_finance* h, int32_t market, int32_t book, const uint8_t* active, const int64_t* ids,
+                             const int64_t* trader, const int64_t* side, const double* price, const int64_t* qty,
+                             const int64_t* placed, int64_t next_id, double last_price) {
+    if (!h) return ABMX_E_ARG;
+    if (market < 0 || market >= h->M || book < 0 || book >= h->P.K) {
+        abmx_internal::set_error("market / book index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    const size_t cap = static_cast<size_t>(h->P.cap);
+    const size_t bo = (static_cast<size_t>(market) * h->P.K + book) * cap;
+    std::vector<int> tr(cap), q(cap);
+    std::vector<uint8_t> sd(cap), act(cap);
+    int na = 0;
+    for (size_t i = 0; i < cap; ++i) {
+        act[i] = active[i] ? 1 : 0;
+        na += act[i];
+        if (trader[i] < INT32_MIN || trader[i] > INT32_MAX || qty[i] < INT32_MIN || qty[i] > INT32_MAX ||
+            side[i] < 0 || side[i] > 255) {
+            abmx_internal::set_error("order field outside the device layout");
+            return ABMX_E_DOMAIN;
+        }
+        tr[i] = static_cast<int>(trader[i]);
+        q[i] = static_cast<int>(qty[i]);
+        sd[i] = static_cast<uint8_t>(side[i]);
+    }
+    BookS B{last_price, 0.0, next_id, 0, 0, na, 0};
+    CKF(cudaStreamSynchronize(h->stream));
+    CKF(cudaMemcpy(h->P.active + bo, act.data(), cap, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.ids + bo, ids, cap * 8, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.trader + bo, tr.data(), cap * 4, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.side + bo, sd.data(), cap, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.price + bo, price, cap * 8, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.qty + bo, q.data(), cap * 4, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.placed + bo, placed, cap * 8, cudaMemcpyHostToDevice));
+    CKF(cudaMemcpy(h->P.bs + static_cast<size_t>(market) * h->P.K + book, &B, sizeof B, cudaMemcpyHostToDevice));
+    return ABMX_OK;
+}
+int abmx_finance_export_traders(abmx_finance* h, int32_t market, double* cash, int64_t* holdings) {
+    if (!h) return ABMX_E_ARG;
+    if (market < 0 || market >= h->M) {
+        abmx_internal::set_error("market index out of range");
+        return ABMX_E_DOMAIN;
+    }
+    const size_t T = static_cast<size_t>(h->P.T), K = static_cast<size_t>(h->P.K);
+    if (T) {
+        CKF(cudaMemcpyAsync(cash, h->P.cash + static_cast<size_t>(market) * T, T * 8, cudaMemcpyDeviceToHost, h->stream));
+        CKF(cudaMemcpyAsync(holdings, h->P.holdings + static_cast<size_t>(market) * K * T, K * T * 8,
+                            cudaMemcpyDeviceToHost, h->stream));
+    }
+    CKF(cudaStreamSynchronize(h->stream));
+    return ABMX_OK;
+}
+// match_book (finance.cpp:125-190) on one host book: arrays are updated in place, fills written
+// in the reference order (buys by priority, then sells); returns the number of fills or < 0.
+int32_t abmx_finance_match(int32_t capacity, double last_price, uint8_t* active, int64_t* ids, int64_t* trader,
+                           int64_t* side, double* price, int64_t* qty, int64_t* placed, int64_t* f_trader,
+                           int64_t* f_side, int64_t* f_qty, double* f_amount, double* scalars) {
+    abmx_finance_config c{1, 0, capacity, 0.0, 0.0, 1, 1, last_price};
+    uint64_t seed = 0;
+    abmx_finance* h = nullptr;
+    int rc = abmx_finance_create(&c, &seed, 1, &h);
+    if (rc) return -rc;
+    rc = abmx_finance_import_book(h, 0, 0, active, ids, trader, side, price, qty, placed, 0, last_price);
+    if (!rc) rc = h->launch(0, 1, 1);
+    int nf = 0;
+    if (!rc) {
+        // the engine stream is non-blocking: order the host reads after the match kernel
+        cudaError_t e = cudaStreamSynchronize(h->stream);
+        if (e == cudaSuccess) e = cudaMemcpy(&nf, h->P.n_fills, 4, cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess && nf > 0) {
+            cudaMemcpy(f_trader, h->P.f_trader, static_cast<size_t>(nf) * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(f_side, h->P.f_side, static_cast<size_t>(nf) * 8, cudaMemcpyDeviceToHost);
+            cudaMemcpy(f_qty, h->P.f_qty, static_cast<size_t>(nf) * 8, cudaMemcpyDeviceToHost);
+            e = cudaMemcpy(f_amount, h->P.f_amount, static_cast<size_t>(nf) * 8, cudaMemcpyDeviceToHost);
+        }
+        if (e != cudaSuccess) {
+            abmx_internal::set_error(std::string("finance match: ") + cudaGetErrorString(e));
+            rc = ABMX_E_CUDA;
+        }
+    }
+    if (!rc) rc = abmx_finance_export_book(h, 0, 0, active, ids, trader, side, price, qty, placed, scalars);
+    abmx_finance_destroy(h);
+    return rc ? -rc : nf;
+}
+double abmx_finance_quantize_price(double raw) { return quantize_host(raw); }
+int abmx_finance_run_batch(const abmx_finance_config* cfg, uint64_t master, int32_t replica_begin, int32_t count,
+                           int64_t steps, double* rows, double* kernel_ms) {
+    if (!cfg || count < 0) {
+        abmx_internal::set_error("bad run_batch arguments");
+        return ABMX_E_ARG;
+    }
+    int rc = check_cfg(*cfg);
+    if (rc) return rc;
+    if (count == 0 || steps <= 0) return ABMX_OK;
+    std::vector<uint64_t> seeds(static_cast<size_t>(count));
+    const unsigned long long base = abmx_dev::split(master, 2);  // batch.cpp:12-19
+    for (int32_t q = 0; q < count; ++q)
+        seeds[static_cast<size_t>(q)] = abmx_dev::split(base, static_cast<unsigned long long>(replica_begin + q));
+    abmx_finance* h = nullptr;
+    rc = abmx_finance_create(cfg, seeds.data(), count, &h);
+    if (rc) return rc;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, h->stream);
+    rc = h->launch(1, steps, 0);
+    cudaEventRecord(b, h->stream);
+    if (!rc && rows) {
+        cudaError_t e = cudaMemcpyAsync(rows, h->d_metrics, static_cast<size_t>(count) * steps * h->P.K * 48,
+                                        cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            abmx_internal::set_error(std::string("finance run_batch: ") + cudaGetErrorString(e));
+            rc = ABMX_E_CUDA;
+        }
+    }
+    cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    if (kernel_ms) *kernel_ms = ms;
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    abmx_finance_destroy(h);
+    return rc;
+}
+
+}  // extern "C"

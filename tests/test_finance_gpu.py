@@ -1,0 +1,164 @@
+"""GPU parity: the finance engine (csrc/finance.cu through the C-ABI) against the reference's
+golden vectors (tests/golden/finance.json, from the unmodified reference), the reference's own
+unit cases (test_finance.cpp) and the C oracle.
+
+Bit-exact: metrics rows every step, every order column, cash (as bit patterns) and holdings."""
+import numpy as np
+import pytest
+
+import pyoracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F(abmx):
+    from paper_2508_16508_b200 import finance
+    return finance
+
+
+def load():
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "finance.json")) as f:
+        return json.load(f)
+
+
+def dec(s, dt):
+    import base64
+    return np.frombuffer(base64.b64decode(s), dtype=dt).copy()
+
+
+def cfg_of(F, kw):
+    return F.FinanceConfig(**kw)
+
+
+def assert_book(got, want, what=""):
+    for name, dt in pyoracle.BOOK_FIELDS:
+        g = np.asarray(got[name])
+        w = np.asarray(want[name])
+        if name == "price":
+            g, w = g.view(np.uint64), w.view(np.uint64)
+        assert np.array_equal(g, w), (what, name)
+
+
+def test_quantize_golden(F):
+    for x, want in load()["quantize"]:
+        assert F.quantize_price(x) == want
+
+
+def test_models_golden(F):
+    for mc in load()["models"]:
+        m = F.FinanceModel(cfg_of(F, mc["cfg"]), mc["seed"])
+        for t in range(1, mc["steps"] + 1):
+            m.step(t)
+            assert m.collect_metrics()[0].tolist() == mc["metrics"][t - 1], (mc["cfg"], t)
+        cash, hold = m.traders()
+        assert np.array_equal(cash.view(np.uint64), dec(mc["cash"], np.uint64)), mc["cfg"]
+        assert np.array_equal(hold.ravel(), dec(mc["holdings"], np.int64)), mc["cfg"]
+        for k, bk in enumerate(mc["books"]):
+            got = m.book(k)
+            assert_book(got, {n: dec(bk[n], dt) for n, dt in pyoracle.BOOK_FIELDS}, (mc["cfg"], k))
+            assert got["next_id"] == bk["next_id"] and got["last_price"] == bk["last_price"]
+
+
+def test_models_golden_one_launch(F):
+    """The same trajectories with all steps in ONE launch (book resident in shared memory)."""
+    for mc in load()["models"]:
+        m = F.FinanceModel(cfg_of(F, mc["cfg"]), mc["seed"])
+        rows = m.run(1, mc["steps"])
+        assert np.array_equal(rows[0], np.array(mc["metrics"])), mc["cfg"]
+
+
+def test_match_golden(F):
+    for i, c in enumerate(load()["match"]):
+        book = {n: dec(c["in"][n], dt) for n, dt in pyoracle.BOOK_FIELDS}
+        out, fills, summ = F.match_book(book, 100.0)
+        assert_book(out, {n: dec(c["out"][n], dt) for n, dt in pyoracle.BOOK_FIELDS}, i)
+        for k, dt in (("trader", np.int64), ("side", np.int64), ("qty", np.int64),
+                      ("amount", np.float64)):
+            assert np.array_equal(fills[k], dec(c["fills"][k], dt)), (i, k)
+        assert summ["volume"] == c["volume"] and summ["last_price"] == c["last_price"], i
+
+
+def test_run_batch_golden(F):
+    b = load()["batch"]
+    rows, _ = F.run_batch(cfg_of(F, b["cfg"]), b["master"], b["replicas"], b["steps"])
+    assert np.array_equal(rows, np.array(b["rows"]))
+
+
+def _make_book(cap, orders):
+    d = {n: np.zeros(cap, dt) for n, dt in pyoracle.BOOK_FIELDS}
+    for j, (tr, side, price, qty, placed) in enumerate(orders):
+        d["active"][j] = 1
+        d["ids"][j] = j
+        d["trader"][j] = tr
+        d["side"][j] = side
+        d["price"][j] = price
+        d["qty"][j] = qty
+        d["placed"][j] = placed
+    d["next_id"] = len(orders)
+    return d
+
+
+def test_reference_unit_cases(abmx, F):
+    """test_finance.cpp: worked example, one-sided book, price-time priority, full book, the age
+    limit, conservation, zero traders."""
+    # worked example: V=8, clearing at 100, partial fill at the margin (:116-145)
+    b = _make_book(16, [(1, 0, 101.0, 10, 0), (2, 0, 100.0, 5, 0), (3, 1, 99.0, 8, 0),
+                        (4, 1, 102.0, 4, 0)])
+    out, fills, s = F.match_book(b, 100.0)
+    assert s["volume"] == 8 and s["clearing"] == 100.0 and s["last_price"] == 100.0
+    live = out["active"] == 1
+    assert out["qty"][live & (out["trader"] == 1)].tolist() == [2]
+    assert not (live & (out["trader"] == 3)).any()
+    # one side empty: no volume, book unchanged (:147-153)
+    b = _make_book(8, [(1, 0, 101.0, 3, 0)])
+    out, fills, s = F.match_book(b, 100.0)
+    assert s["volume"] == 0 and len(fills["qty"]) == 0
+    assert_book(out, b)
+    # price-time priority (:190-208)
+    b = _make_book(16, [(1, 0, 101.0, 2, 1), (2, 0, 101.0, 2, 0), (3, 1, 99.0, 3, 0)])
+    _, fills, s = F.match_book(b, 100.0)
+    got = {int(t): int(q) for t, q, sd in zip(fills["trader"], fills["qty"], fills["side"]) if sd == 0}
+    assert s["volume"] == 3 and got.get(2) == 2 and got.get(1) == 1
+    # a full book drops placements and counts them (:227-238)
+    m = F.FinanceModel(F.FinanceConfig(traders=6, books=1, book_capacity=2, p_order=1.0), 5)
+    m.step(1)
+    assert m.book(0)["num_active"] <= 2 and m.collect_metrics()[0, 0, 5] == 4
+    # resting orders are cancelled at the age limit (:240-252)
+    m = F.FinanceModel(F.FinanceConfig(traders=0, books=1, book_capacity=8, max_order_age=3), 6)
+    m.set_book(0, _make_book(8, [(0, 0, 99.0, 1, 0)]), 100.0)
+    for t in (1, 2):
+        m.step(t)
+        assert m.book(0)["num_active"] == 1
+    m.step(3)
+    assert m.book(0)["num_active"] == 0
+    # cash and holdings are conserved over a whole run (:254-275)
+    m = F.FinanceModel(F.FinanceConfig(traders=10, books=3, book_capacity=64), 31)
+    for t in range(1, 41):
+        m.step(t)
+        cash, hold = m.traders()
+        assert cash.sum() == 0.0 and (hold.sum(axis=1) == 0).all()
+    # zero traders: constant prices (:277-287)
+    m = F.FinanceModel(F.FinanceConfig(traders=0, books=2, book_capacity=8), 9)
+    for t in range(1, 11):
+        m.step(t)
+        assert (m.collect_metrics()[0, :, 1] == F.quantize_price(100.0)).all()
+    # configuration errors (config.cpp:210-215)
+    for bad in (dict(books=0), dict(qmax=0), dict(p_order=1.5), dict(book_capacity=0)):
+        with pytest.raises(abmx.DomainError):
+            F.FinanceModel(F.FinanceConfig(**bad), 1)
+    with pytest.raises(abmx.CapacityError):
+        F.FinanceModel(F.FinanceConfig(book_capacity=100000), 1)
+
+
+@pytest.mark.parametrize("kw,K,T", [(dict(), 96, 100), (dict(traders=200, books=2, book_capacity=300,
+                                                               p_order=0.9), 32, 60),
+                                    (dict(traders=1000, books=1, book_capacity=4096, p_order=0.7,
+                                          max_order_age=40), 4, 50)])
+def test_run_batch_vs_oracle(F, oracle, kw, K, T):
+    """C5-shaped ensembles (default FinanceConfig) and heavy books against the C restatement."""
+    rows, _ = F.run_batch(F.FinanceConfig(**kw), 7, K, T)
+    want = oracle.fin_run_batch(7, K, T, **kw)
+    assert np.array_equal(rows, want)

@@ -5,7 +5,7 @@ set -e
 TAG=$1; DEFS=$2
 D=build/variants/$TAG; mkdir -p $D
 F="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC $DEFS"
-for u in table predation ensemble agents traffic traffic_ens capi; do
+for u in table predation ensemble agents traffic traffic_ens finance capi; do
   nvcc $F -Xptxas -v -c paper_2508_16508_b200/csrc/$u.cu -o $D/$u.o 2> $D/$u.ptxas.txt &
 done
 wait
