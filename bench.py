@@ -16,6 +16,9 @@ The line also carries the C3 ensemble (4096 x C1 replicas, sharded over the rank
   roofline   dominant kernel: SURVEY §8d algorithmic bytes apportioned to that kernel
              / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the reference's own C++ step_predation (oracle/_ref, -O3) on this host
+  ensemble / traffic / finance   secondary sections: device times of
+             the C3 ensemble, the C4 road and roads variant, the C5 markets, each with the
+             reference's own CPU run on a bounded sample
 
 `--impl reference` times the reference CPU implementation (oracle/_ref) on the same workload.
 """
@@ -210,6 +213,42 @@ def traffic_section(args, rank, world, allreduce, dist):
                           f"{threads} threads ({wall_b / 1e3:.1f} s)"}
     return out
 
+
+# ---------------------------------------------------------------------- finance (§8f rank 2)
+MARKETS, FIN_STEPS = 1024, 100  # C5: 1024 markets x default FinanceConfig, 100 steps
+
+
+def finance_section(args, rank, world, allreduce, dist):
+    """C5 on the device (markets sharded by contiguous blocks over the ranks) and the reference
+    run_batch on the host for a bounded sample."""
+    from paper_2508_16508_b200 import finance as F
+    cfg = F.FinanceConfig()
+    per = MARKETS // world
+    begin = rank * per
+    count = per if rank < world - 1 else MARKETS - begin
+    F.run_batch(cfg, MASTER_SEED, min(count, 64), 5, begin=begin)
+    _, ms = F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin)
+    ms = allreduce(ms, dist.ReduceOp.MAX if dist else None)
+    slots = MARKETS * cfg.books * cfg.book_capacity
+    out = {"workload": f"C5: {MARKETS} markets x FinanceConfig defaults (5 books x 1000 capacity, "
+                       f"10 traders), {FIN_STEPS} steps (run_batch)",
+           "value": slots * FIN_STEPS / (ms / 1e3), "unit": UNIT, "device_ms": ms,
+           "market_steps_per_s": MARKETS * FIN_STEPS / (ms / 1e3)}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+        if os.path.exists(pyoracle.REF_SO):
+            ref = pyoracle.Reference()
+            threads = os.cpu_count() or 1
+            nm, ns = MARKETS, FIN_STEPS  # the full C5 workload (~1 s on the host)
+            _, wall = ref.fin_run_batch(MASTER_SEED, nm, ns, threads=threads)
+            out["cpu_baseline"] = {
+                "value": nm * cfg.books * cfg.book_capacity * ns / (wall / 1e3), "unit": UNIT,
+                "cores": threads, "kind": "reference",
+                "sample": f"reference run_batch(FinanceModel), {nm} markets x {ns} steps, "
+                          f"{threads} threads ({wall / 1e3:.2f} s)"}
+    return out
+
 # ---------------------------------------------------------------------- our arm
 def kernel_bytes(cfg, births, deaths):
     """SURVEY §8d algorithmic bytes per step, B = 42*N_tot + 2*C + 8*(births+deaths),
@@ -355,6 +394,7 @@ def our_arm(args, rank, world, local_rank, dist):
                        "and may exceed HBM peak"}
 
     traffic = None if args.no_traffic else traffic_section(args, rank, world, allreduce, dist)
+    finance = None if args.no_finance else finance_section(args, rank, world, allreduce, dist)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -380,7 +420,8 @@ def our_arm(args, rank, world, local_rank, dist):
                            "timing": "CUDA events per step on the engine stream; max over ranks"},
                 "live_agent_steps_per_s": live_all / (max_ms / 1e3),
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
-                "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens, "traffic": traffic}
+                "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens, "traffic": traffic,
+                "finance": finance}
         print(json.dumps(line))
 
 
@@ -394,6 +435,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-ensemble", action="store_true")
     ap.add_argument("--no-traffic", action="store_true")
+    ap.add_argument("--no-finance", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rules: >= 3 warm-up steps
