@@ -278,6 +278,18 @@ def main():
         fin["quantize"].append([x, ref.lib.ref_fin_quantize(x)])
     json.dump(fin, open(os.path.join(OUT, "finance.json"), "w"))
 
+    # ---- CSV of run_batch (csv.cpp:16-35) for the three batch models; format_real samples
+    csvs = {"predation": {"cfg": c1(), "master": 3, "replicas": 3, "steps": 12,
+                          "csv": ref.run_csv("predation", 3, 3, 12, pred=c1())},
+            "traffic": {"cfg": [20, 10, 0.5], "master": 5, "replicas": 4, "steps": 25,
+                        "csv": ref.run_csv("traffic", 5, 4, 25, traffic=(20, 10, 0.5))},
+            "finance": {"cfg": {"book_capacity": 64}, "master": 9, "replicas": 2, "steps": 6,
+                        "csv": ref.run_csv("finance", 9, 2, 6, fin={"book_capacity": 64})}}
+    reals = [0.0, -0.0, 1.0, 0.1, 1 / 3, 100.0078125, 1e-5, 123456789012345678.0, 2.5e-310,
+             -7.25, 1e22, 4613.0, 0.00012207031250000001]
+    csvs["format_real"] = [[v, ref.format_real(v)] for v in reals]
+    json.dump(csvs, open(os.path.join(OUT, "csv.json"), "w"))
+
     # ---- lifecycle: remove_agents then spawn_agents, chained cycles, id recycling on/off
     life = []
     g = np.random.default_rng(4242)

@@ -522,10 +522,35 @@ class Reference(_Base):
         L.ref_fin_run_batch.restype = C.c_double
         L.ref_fin_run_batch.argtypes = [C.POINTER(FinCfg), C.c_uint64, C.c_int32, C.c_int64, C.c_int,
                                         f64p]
+        L.ref_run_csv.restype = C.c_int64
+        L.ref_run_csv.argtypes = [C.c_int, C.POINTER(Cfg), C.c_int64, C.c_int64, C.c_double,
+                                  C.POINTER(FinCfg), C.c_uint64, C.c_int32, C.c_int64, C.c_char_p,
+                                  C.c_int64]
+        L.ref_format_real.argtypes = [C.c_double, C.c_char_p]
         L.ref_lifecycle.restype = C.c_int32
         L.ref_lifecycle.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, i64p, f64p, u8p, i64p, C.c_int,
                                     i64p, i32p, u8p, C.c_int32, i64p, f64p, u8p, u8p, C.c_int,
                                     C.c_int64, i32p, i32p, i32p, i32p]
+
+    # CSV (csv.cpp)
+    def run_csv(self, model, master, replicas, steps, pred=None, traffic=(20, 10, 0.5), fin=None):
+        kind = {"predation": 0, "traffic": 1, "finance": 2}[model]
+        pc = to_cfg(pred or {}) if kind == 0 else None
+        fc = fin_cfg(**(fin or {}))
+        L, period, gf = traffic
+        n = self.lib.ref_run_csv(kind, C.byref(pc) if pc is not None else None, L, period, gf,
+                                 C.byref(fc), master, replicas, steps, None, 0)
+        if n < 0:
+            raise ValueError("run failed")
+        buf = C.create_string_buffer(n + 1)
+        self.lib.ref_run_csv(kind, C.byref(pc) if pc is not None else None, L, period, gf,
+                             C.byref(fc), master, replicas, steps, buf, n)
+        return buf.raw[:n].decode()
+
+    def format_real(self, v):
+        buf = C.create_string_buffer(64)
+        self.lib.ref_format_real(v, buf)
+        return buf.value.decode()
 
     # finance
     def fin(self, seed, **cfg):

@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "abmx/batch.hpp"
+#include "abmx/csv.hpp"
 #include "abmx/kernels.hpp"
 #include "abmx/lifecycle.hpp"
 #include "abmx/models/predation.hpp"
@@ -700,6 +701,32 @@ double ref_fin_run_batch(const ref_fin_config* c, uint64_t master, int32_t repli
     } catch (const std::exception&) {
         return -1.0;
     }
+}
+
+
+// ---------------------------------------------------------------- CSV (csv.cpp)
+// trajectory_to_csv of run_batch for one of the three batch models; returns the text length
+// (the text is written only if it fits `cap`), -1 on error. kind 0 predation, 1 traffic,
+// 2 finance; the matching config pointer is used.
+int64_t ref_run_csv(int kind, const ref_pred_config* pc, int64_t length, int64_t period, double green_fraction,
+                    const ref_fin_config* fc, uint64_t master, int32_t replicas, int64_t steps, char* out,
+                    int64_t cap) {
+    try {
+        ModelDescriptor model = kind == 0   ? PredationModel::descriptor(to_cfg(pc))
+                                : kind == 1 ? TrafficModel::descriptor(TrafficConfig{length, period, green_fraction})
+                                            : FinanceModel::descriptor(fin_cfg(fc));
+        const auto seeds = replica_seeds(RngState{master}, replicas);
+        const Trajectory tr = run_batch(model, seeds, steps, 1, nullptr);
+        const std::string csv = trajectory_to_csv(tr);
+        if (static_cast<int64_t>(csv.size()) <= cap) std::memcpy(out, csv.data(), csv.size());
+        return static_cast<int64_t>(csv.size());
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+void ref_format_real(double v, char* out) {
+    const std::string s = format_real(v);
+    std::memcpy(out, s.c_str(), s.size() + 1);
 }
 
 }  // extern "C"
