@@ -155,6 +155,10 @@ int abmx_predation_set_timing(abmx_predation* h, int enabled);
 int32_t abmx_predation_kernel_count(void);
 const char* abmx_predation_kernel_name(int32_t k);
 int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches);
+/* diagnostics: per-CTA phase timestamps (%globaltimer ns) of k_move / k_update, recorded only
+ * by builds compiled with -DABMX_PRED_TRACE; [2][CTAs][8], returns the number of entries */
+int abmx_predation_set_trace(abmx_predation* h, int32_t enable);
+int64_t abmx_predation_trace(abmx_predation* h, uint64_t* out, int64_t cap);
 /* device-resident bytes of h (state + scratch) */
 int64_t abmx_predation_device_bytes(abmx_predation* h);
 /* Device-timed steps t0..t0+steps-1 for benchmarking: before each step an (untimed) write

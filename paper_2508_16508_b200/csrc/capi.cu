@@ -313,6 +313,32 @@ int abmx_predation_set_timing(abmx_predation* h, int enabled) {
 }
 int32_t abmx_predation_kernel_count(void) { return abmx_pred::kNumKernels; }
 const char* abmx_predation_kernel_name(int32_t k) { return abmx_pred::kernel_name(k); }
+// Phase timeline of the next launches (ABMX_PRED_TRACE builds; elsewhere the buffer stays
+// zero). enable = 1 allocates [2 kernels][CTAs][8] stamps.
+int abmx_predation_set_trace(abmx_predation* h, int32_t enable) {
+    HANDLE(h);
+    auto& E = h->eng;
+    if (enable && !E.d_trace) {
+        E.trace_n = static_cast<size_t>(2) * E.grid(0) * 8;
+        if (cudaMalloc(&E.d_trace, E.trace_n * 8) != cudaSuccess) return ABMX_E_CUDA;
+        cudaMemset(E.d_trace, 0, E.trace_n * 8);
+    }
+    E.params.trace = enable ? E.d_trace : nullptr;
+    if (E.graph_exec) {  // graph nodes captured the old parameter block: rebuild on next use
+        cudaGraphExecDestroy(E.graph_exec);
+        cudaGraphDestroy(E.graph);
+        E.graph_exec = nullptr;
+        E.graph = nullptr;
+    }
+    return ABMX_OK;
+}
+int64_t abmx_predation_trace(abmx_predation* h, uint64_t* out, int64_t cap) {
+    if (!h || !h->eng.d_trace) return 0;
+    const size_t n = h->eng.trace_n < static_cast<size_t>(cap) ? h->eng.trace_n : static_cast<size_t>(cap);
+    cudaStreamSynchronize(h->eng.stream);
+    cudaMemcpy(out, h->eng.d_trace, n * 8, cudaMemcpyDeviceToHost);
+    return static_cast<int64_t>(n);
+}
 int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches_out) {
     HANDLE(h);
     for (int k = 0; k < abmx_pred::kNumKernels; ++k) {

@@ -142,6 +142,25 @@ __device__ __forceinline__ T block_sum(T v, T* smem) {
 // x/y/z are current iff their tag equals this step's; the host clears x/y/z (not w) every
 // kEpochClear (= 128) steps, so tags never alias and the .z tag of the current step is the
 // largest alive (a max-reduction keeps it).
+// Phase timeline (ABMX_PRED_TRACE builds only): thread 0 of each CTA stamps %globaltimer.
+#ifdef ABMX_PRED_TRACE
+__device__ __forceinline__ void trace_stamp(const Params& P, int kernel, int point) {
+    if (threadIdx.x == 0 && P.trace) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[(static_cast<size_t>(kernel) * gridDim.x + blockIdx.x) * 8 + point] = t;
+        if (point == 0) {
+            unsigned sm;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+            P.trace[(static_cast<size_t>(kernel) * gridDim.x + blockIdx.x) * 8 + 7] = sm;
+        }
+    }
+}
+#define TRACE(k, p) trace_stamp(P, k, p)
+#else
+#define TRACE(k, p) ((void)0)
+#endif
+
 __device__ __forceinline__ unsigned epoch8(unsigned long long epoch) {
     return static_cast<unsigned>(epoch % 255ULL) + 1u;  // 1..255, never the cleared 0
 }
@@ -216,6 +235,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
     __shared__ long long s_red[kT / 32];
     __shared__ unsigned s_base;
     const unsigned long long epoch = P.epoch;
+    if (kMove) TRACE(0, 0);
     int s, r, tile;
     tile_of(P, b, s, r, tile);
     const int N = P.N[s];
@@ -363,6 +383,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
         }
     }
     if (!kMove) return;
+    TRACE(0, 1);
 
     // ---------------- (b) move + bin
     const unsigned e8 = epoch8(epoch), tag = min_tag(epoch);
@@ -411,10 +432,12 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
                 P.next[s][base + k] = cur ? static_cast<int>(old[k] & kNil) : -1;
                 first[k] = P.crowded && s == 1 && !cur;
             }
+        TRACE(0, 2);
         storek_i32(P.cell[s] + base, cell);
         storek_i32(P.age[s] + base, age);
         if (born_any) storek_u8(P.active[s] + base, act);
     }
+    TRACE(0, 3);
     if (live && P.needs_blend) {  // step_agents masks placeholder state back to defaults
 #pragma unroll
         for (int k = 0; k < kS; ++k)
@@ -568,6 +591,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
     const unsigned long long epoch = P.epoch;
     const int p = static_cast<int>(epoch & 1);
     const unsigned tag = min_tag(epoch), e8 = epoch8(epoch), ep = static_cast<unsigned>(epoch);
+    TRACE(1, 0);
     int s, r, tile;
     tile_of(P, b, s, r, tile);
     if (b == 0 && threadIdx.x == 0) {  // the move (and pairing) of this step are complete
@@ -613,6 +637,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
 #pragma unroll
             for (int k = 0; k < kS; ++k)
                 if (act[k]) cw[k] = P.cw[cidx(P, r, cell[k])];
+            TRACE(1, 1);
             if (s == 0) {  // graze: lowest sheep slot of a ready cell (predation.cpp:178-195)
 #pragma unroll
                 for (int k = 0; k < kS; ++k)
@@ -628,24 +653,48 @@ __device__ void update_phase(const Params& P, unsigned b) {
             if (!P.crowded) {
 #endif
                 // predation (predation.cpp:197-239): in a cell holding wolves and sheep the k-th
-                // wolf by slot takes the k-th sheep by slot; each agent finds its own rank with
-                // a walk over the cell's (short) lists
+                // wolf by slot takes the k-th sheep by slot. Each agent ranks itself in its own
+                // cell list and counts the other species' list; the up to 2*kS walks of a thread
+                // advance in lockstep, so their dependent hops overlap (latency = longest list,
+                // not the sum of all walks).
+                const int* nmine = s == 0 ? P.next[0] + sb : P.next[1] + wb;
+                const int* noth = s == 0 ? P.next[1] + wb : P.next[0] + sb;
+                int cm[kS], co[kS], rank[kS], lo[kS];
+                bool walk = false;
 #pragma unroll
                 for (int k = 0; k < kS; ++k) {
+                    cm[k] = -1;
+                    co[k] = -1;
+                    rank[k] = 0;
+                    lo[k] = 0;
                     if (!act[k] || (cw[k].x >> 24) != e8 || (cw[k].y >> 24) != e8) continue;
                     const int hs = static_cast<int>(cw[k].x & kNil), hw = static_cast<int>(cw[k].y & kNil);
-                    int rank, len_mine, rank_o, len_other;
-                    if (s == 0) {
-                        list_rank(P.next[0] + sb, hs, i0 + k, rank, len_mine);
-                        list_rank(P.next[1] + wb, hw, INT_MAX, rank_o, len_other);
-                    } else {
-                        list_rank(P.next[1] + wb, hw, i0 + k, rank, len_mine);
-                        list_rank(P.next[0] + sb, hs, INT_MAX, rank_o, len_other);
-                    }
-                    flg[k] = rank < len_other;
+                    cm[k] = s == 0 ? hs : hw;
+                    co[k] = s == 0 ? hw : hs;
+                    walk = true;
                 }
+                while (walk) {
+                    int nm[kS], no[kS];
+#pragma unroll
+                    for (int k = 0; k < kS; ++k) {  // all hops of this round issued together
+                        nm[k] = cm[k] >= 0 ? nmine[cm[k]] : -1;
+                        no[k] = co[k] >= 0 ? noth[co[k]] : -1;
+                    }
+                    walk = false;
+#pragma unroll
+                    for (int k = 0; k < kS; ++k) {
+                        if (cm[k] >= 0) rank[k] += cm[k] < i0 + k;
+                        if (co[k] >= 0) ++lo[k];
+                        cm[k] = nm[k];
+                        co[k] = no[k];
+                        walk |= (cm[k] >= 0) | (co[k] >= 0);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < kS; ++k) flg[k] = flg[k] || rank[k] < lo[k];
             }
         }
+        TRACE(1, 2);
         bool died_any = false;
 #pragma unroll
         for (int k = 0; k < kS; ++k) {
@@ -702,6 +751,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
         nf += freek[k];
         nv += valid[k];
     }
+    TRACE(1, 3);
     unsigned long long tile_total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(nf, nv), s_scan, &tile_total);
     // tile-local compaction of the valid parent rows (slot order); k_move concatenates tiles
@@ -758,6 +808,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
         if (eaten && !P.crowded) atomicAdd(&ev->sheep_eaten, eaten);
         if (x_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&ev->e_removed_fx[s]), static_cast<unsigned long long>(x_sum));
     }
+    TRACE(1, 4);
 }
 
 // ============================================================== kernels
@@ -886,6 +937,7 @@ Engine::~Engine() {
     for (void* p : allocs) cudaFree(p);
     if (d_run_metrics) cudaFree(d_run_metrics);
     if (flush_buf) cudaFree(flush_buf);
+    if (d_trace) cudaFree(d_trace);
     if (stream) cudaStreamDestroy(stream);
 }
 

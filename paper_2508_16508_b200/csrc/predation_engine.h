@@ -97,6 +97,7 @@ struct Params {
     Ctl* ctl;
     SpeciesRep* rep;
     Events* ev;
+    unsigned long long* trace;  // ABMX_PRED_TRACE builds: [kernel][CTA][8] %globaltimer stamps
 };
 
 const char* kernel_name(int k);
@@ -128,6 +129,8 @@ struct Engine {
     long long kernel_launches[kNumKernels] = {};
     void* flush_buf = nullptr;
     size_t flush_cap = 0;
+    unsigned long long* d_trace = nullptr;  // phase timeline (tracing builds only)
+    size_t trace_n = 0;
 
     ~Engine();
     int create(const abmx_predation_config& c, const uint64_t* seeds, int replicas);
