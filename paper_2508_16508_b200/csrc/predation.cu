@@ -203,7 +203,9 @@ __device__ __forceinline__ int find_tile(const unsigned long long* pre, int tile
 // and Q (valid parent rows) are known: counters (double-buffered by parity), the ledger, the
 // metrics row (predation.cpp:281-287) and, for sheep, the lazy-regrow grass count. Run either
 // by tile 0 of k_move / k_finalize (P.book) or by k_book (the per-call step graph).
-__device__ void book_step(const Params& P, int s, int r, int F, int Q) {
+// With add_dropped the births_dropped column accumulates atomically (run rows start zeroed);
+// k_book writes the whole row itself instead, so the per-call graph needs no memset.
+__device__ void book_step(const Params& P, int s, int r, int F, int Q, bool add_dropped = true) {
     const int pb = static_cast<int>(P.birth_epoch & 1);
     const int N = P.N[s];
     const int pairs = F < Q ? F : Q;
@@ -217,7 +219,7 @@ __device__ void book_step(const Params& P, int s, int r, int F, int Q) {
     atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
     long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
     row[s] = N - F + pairs;
-    if (Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
+    if (add_dropped && Q - pairs) atomicAdd(reinterpret_cast<unsigned long long*>(&row[3]), static_cast<unsigned long long>(Q - pairs));
     if (s == 0) {  // ready cells after that step's (lazy) regrow: - grazed + those due
         unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.birth_epoch % P.due_ring];
         const long long ng = P.n_grass[r] - static_cast<long long>(ev->grass_eaten) + *due;
@@ -822,22 +824,31 @@ __global__ void __launch_bounds__(kT) k_finalize(Params P) {
 }
 __global__ void __launch_bounds__(kT, kMinB) k_update(Params P) { update_phase(P, blockIdx.x); }
 
-// k_book: one CTA per replica, both species: totals of the tile counts -> book_step, then the
-// finished metrics row goes straight to mapped host memory (collect_metrics needs no copy).
+// k_book: one CTA per replica, both species: totals of the tile counts -> book_step, the
+// births_dropped column (both species) written directly, then the finished metrics row goes
+// straight to mapped host memory (collect_metrics needs no copy).
 __global__ void __launch_bounds__(kT) k_book(Params P) {
     __shared__ unsigned long long s_red[kT / 32];
     const int r = blockIdx.x;
+    long long dropped = 0;
     for (int s = 0; s < 2; ++s) {
         const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
         unsigned long long v = 0;
         for (int t = threadIdx.x; t < P.tiles[s]; t += kT) v += tc[t];
         const unsigned long long tot = block_sum<unsigned long long>(v, s_red);
-        if (threadIdx.x == 0) book_step(P, s, r, static_cast<int>(hi31(tot)), static_cast<int>(lo31(tot)));
+        if (threadIdx.x == 0) {
+            const int F = static_cast<int>(hi31(tot)), Q = static_cast<int>(lo31(tot));
+            book_step(P, s, r, F, Q, false);
+            dropped += Q - (F < Q ? F : Q);
+        }
     }
-    if (threadIdx.x == 0 && P.host_row) {
-        const long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
-        long long* h = P.host_row + static_cast<size_t>(r) * 4;
-        for (int q = 0; q < 4; ++q) h[q] = row[q];
+    if (threadIdx.x == 0) {
+        long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
+        row[3] = dropped;
+        if (P.host_row) {
+            long long* h = P.host_row + static_cast<size_t>(r) * 4;
+            for (int q = 0; q < 4; ++q) h[q] = row[q];
+        }
     }
 }
 
@@ -1207,9 +1218,9 @@ int Engine::launch_steps(long long steps) {
     return ABMX_OK;
 }
 
-// PredationModel::step(t) as ONE graph launch: zero the metrics row, the step's kernels, then
-// k_book completes the metrics row and counters; the births stay pending (booked) and are
-// applied by the next k_move, or by k_finalize before any state read.
+// PredationModel::step(t) as ONE graph launch: the step's kernels, then k_book writes the whole
+// metrics row (and its mapped host copy) and the counters; the births stay pending (booked) and
+// are applied by the next k_move, or by k_finalize before any state read.
 int Engine::step(long long t) {
     int rc = set_metrics_target(d_metrics_step, 1);  // also applies any births still pending
     if (rc) return rc;
@@ -1235,18 +1246,11 @@ int Engine::step(long long t) {
     };
     if (!step_exec) {
         CK(cudaGraphCreate(&step_graph, 0));
-        cudaMemsetParams mp{};
-        mp.dst = d_metrics_step;
-        mp.value = 0;
-        mp.elementSize = 4;
-        mp.width = static_cast<size_t>(R) * 4 * 2;  // R rows of 4 int64
-        mp.height = 1;
-        cudaGraphNode_t prev;
-        CK(cudaGraphAddMemsetNode(&prev, step_graph, nullptr, 0, &mp));
+        cudaGraphNode_t prev = nullptr;
         for (int k = 0; k <= kNumKernels; ++k) {
             if (k < kNumKernels && !launched(k)) continue;
             const cudaKernelNodeParams kp = kparams(k, k < kNumKernels ? args : fargs);
-            CK(cudaGraphAddKernelNode(&step_nodes[k], step_graph, &prev, 1, &kp));
+            CK(cudaGraphAddKernelNode(&step_nodes[k], step_graph, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
             prev = step_nodes[k];
         }
         CK(cudaGraphInstantiate(&step_exec, step_graph, 0));

@@ -17,9 +17,10 @@ L.abmx_predation_trace.argtypes = [C.c_void_p, C.POINTER(C.c_uint64), C.c_int64]
 cfg = abmx.PredationConfig(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000,
                            sheep_capacity=524288, wolf_capacity=524288)
 m = abmx.PredationModel(cfg, abmx.replica_seeds(7, 1)[0])
-m.bench(1, 6, 256 << 20)
+FLUSH = 0 if "--warm" in sys.argv else 256 << 20
+m.bench(1, 6, FLUSH)
 L.abmx_predation_set_trace(m._h, 1)
-m.bench(7, 1, 256 << 20, per_kernel=False)
+m.bench(7, 1, FLUSH, per_kernel=False)
 n = 1 << 16
 buf = (C.c_uint64 * n)()
 got = L.abmx_predation_trace(m._h, buf, n)
