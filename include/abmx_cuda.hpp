@@ -7,6 +7,11 @@
 //       -> abmx::cuda::run_batch / replica_seeds
 //   abmx::simd::KernelTable (include/abmx/simd/kernels.hpp:15-43)
 //       -> abmx::cuda::kernel_table()  (same layout)
+//   abmx::models::TrafficModel / FinanceModel (traffic.hpp:84-110, finance.hpp:80-97)
+//       -> abmx::cuda::TrafficModel / FinanceModel, traffic_run_batch / finance_run_batch,
+//          resolve_conflicts, match_book, quantize_price
+//   AgentSet + remove/spawn/set_agents/select/sort/permute (agent_set.hpp, lifecycle.hpp,
+//   kernels.hpp) -> abmx::cuda::DeviceAgentSet (columns resident in device memory)
 //
 // Errors are thrown as the reference's exception types (errors.hpp:8-40), re-declared here
 // under abmx::cuda so this header does not need the reference tree.
@@ -137,5 +142,152 @@ inline std::vector<double> run_batch(const abmx_predation_config& cfg, std::uint
     check(abmx_ensemble_run(&cfg, master, first, replicas, steps, 0, rows.data(), nullptr));
     return rows;
 }
+
+// ------------------------------------------------------------------------------ traffic
+// TrafficConfig defaults (traffic.hpp:13-17)
+inline abmx_traffic_config default_traffic_config() { return abmx_traffic_config{100, 10, 0.5}; }
+
+// The device-resident drop-in for abmx::models::TrafficModel (one road).
+class TrafficModel {
+public:
+    TrafficModel(const abmx_traffic_config& cfg, std::uint64_t seed) : cap_(3 * cfg.length) {
+        check(abmx_traffic_create(&cfg, &seed, 1, &h_));
+    }
+    ~TrafficModel() { abmx_traffic_destroy(h_); }
+    TrafficModel(const TrafficModel&) = delete;
+    TrafficModel& operator=(const TrafficModel&) = delete;
+
+    void step(std::int64_t t) { check(abmx_traffic_step(h_, t)); }
+    // n_cars, spawned, exited, signal_green (traffic.cpp:234-238)
+    void collect_metrics(std::vector<std::vector<double>>& rows) const {
+        std::vector<double> m(4);
+        check(abmx_traffic_metrics(h_, m.data()));
+        rows.push_back(m);
+    }
+    std::int64_t spawned_total() const {
+        std::int64_t s = 0, e = 0;
+        check(abmx_traffic_totals(h_, 0, &s, &e));
+        return s;
+    }
+    std::int64_t exited_total() const {
+        std::int64_t s = 0, e = 0;
+        check(abmx_traffic_totals(h_, 0, &s, &e));
+        return e;
+    }
+    // occupancy in the reference layout (lane * length + cell -> slot or -1)
+    std::vector<std::int32_t> occupancy() const {
+        std::vector<std::uint8_t> act(cap_);
+        std::vector<std::int64_t> ids(cap_), ages(cap_), lane(cap_), cell(cap_), nid(1);
+        std::vector<std::int32_t> occ(cap_);
+        std::int32_t na = 0;
+        check(abmx_traffic_export(h_, 0, act.data(), ids.data(), ages.data(), lane.data(), cell.data(),
+                                  occ.data(), nid.data(), &na));
+        return occ;
+    }
+    abmx_traffic* handle() const { return h_; }
+
+private:
+    abmx_traffic* h_ = nullptr;
+    std::size_t cap_;
+};
+
+// run_batch of TrafficModel: rows [replicas][steps][4]
+inline std::vector<double> traffic_run_batch(const abmx_traffic_config& cfg, std::uint64_t master,
+                                             std::int32_t replicas, std::int64_t steps, std::int32_t first = 0) {
+    std::vector<double> rows(static_cast<std::size_t>(replicas > 0 ? replicas : 0) *
+                             static_cast<std::size_t>(steps > 0 ? steps : 0) * 4);
+    check(abmx_traffic_run_batch(&cfg, master, first, replicas, steps, rows.data(), nullptr));
+    return rows;
+}
+
+// resolve_conflicts (traffic.cpp:82-140) with explicit proposals (kind 0 stay, 1 move, 2 exit)
+inline std::vector<std::uint8_t> resolve_conflicts(std::int64_t length, const std::vector<std::uint8_t>& active,
+                                                   const std::vector<std::int64_t>& lane,
+                                                   const std::vector<std::int64_t>& cell,
+                                                   const std::vector<std::uint8_t>& kind,
+                                                   const std::vector<std::int64_t>& to_lane,
+                                                   const std::vector<std::int64_t>& to_cell) {
+    std::vector<std::uint8_t> acc(static_cast<std::size_t>(3 * length));
+    check(abmx_traffic_resolve(length, active.data(), lane.data(), cell.data(), kind.data(), to_lane.data(),
+                               to_cell.data(), acc.data()));
+    return acc;
+}
+
+// ------------------------------------------------------------------------------ finance
+// FinanceConfig defaults (finance.hpp:13-22)
+inline abmx_finance_config default_finance_config() {
+    return abmx_finance_config{5, 10, 1000, 0.5, 0.05, 10, 20, 100.0};
+}
+
+inline double quantize_price(double raw) { return abmx_finance_quantize_price(raw); }
+
+// The device-resident drop-in for abmx::models::FinanceModel (one market).
+class FinanceModel {
+public:
+    FinanceModel(const abmx_finance_config& cfg, std::uint64_t seed) : books_(cfg.books) {
+        check(abmx_finance_create(&cfg, &seed, 1, &h_));
+    }
+    ~FinanceModel() { abmx_finance_destroy(h_); }
+    FinanceModel(const FinanceModel&) = delete;
+    FinanceModel& operator=(const FinanceModel&) = delete;
+
+    void step(std::int64_t t) { check(abmx_finance_step(h_, t)); }
+    // one row per book: book_id, price, n_active_buys, n_active_sells, volume, orders_dropped
+    void collect_metrics(std::vector<std::vector<double>>& rows) const {
+        std::vector<double> m(static_cast<std::size_t>(books_) * 6);
+        check(abmx_finance_metrics(h_, m.data()));
+        for (std::int64_t k = 0; k < books_; ++k)
+            rows.emplace_back(m.begin() + k * 6, m.begin() + (k + 1) * 6);
+    }
+    abmx_finance* handle() const { return h_; }
+
+private:
+    abmx_finance* h_ = nullptr;
+    std::int64_t books_;
+};
+
+// run_batch of FinanceModel: rows [replicas][steps][books][6]
+inline std::vector<double> finance_run_batch(const abmx_finance_config& cfg, std::uint64_t master,
+                                             std::int32_t replicas, std::int64_t steps, std::int32_t first = 0) {
+    std::vector<double> rows(static_cast<std::size_t>(replicas > 0 ? replicas : 0) *
+                             static_cast<std::size_t>(steps > 0 ? steps : 0) * static_cast<std::size_t>(cfg.books) * 6);
+    check(abmx_finance_run_batch(&cfg, master, first, replicas, steps, rows.data(), nullptr));
+    return rows;
+}
+
+// ------------------------------------------------------------------------------ agent sets
+// A thin RAII view over abmx_agent_set: the caller owns the device columns (any allocator);
+// the operations mirror lifecycle.hpp / kernels.hpp with the column-copy apply.
+class DeviceAgentSet {
+public:
+    explicit DeviceAgentSet(const abmx_agent_set& s, void* stream = nullptr) : s_(s), stream_(stream) {}
+    void remove(const std::uint8_t* d_kill, std::int64_t* d_killed = nullptr) {
+        check(abmx_agents_remove(&s_, d_kill, d_killed, stream_));
+    }
+    void spawn(std::int32_t m, const std::uint8_t* d_valid, const abmx_column* rows, bool set_type = false,
+               std::int64_t agent_type = 0, std::int32_t* d_slots = nullptr, std::int32_t* d_rows = nullptr,
+               std::int64_t* d_result = nullptr) {
+        check(abmx_agents_spawn(&s_, m, d_valid, rows, set_type ? 1 : 0, agent_type, d_slots, d_rows, d_result,
+                                stream_));
+    }
+    void set_rm(const std::uint8_t* d_target, std::int32_t m, const std::uint8_t* d_valid, const abmx_column* rows) {
+        check(abmx_agents_set_rm(&s_, d_target, m, d_valid, rows, nullptr, nullptr, nullptr, stream_));
+    }
+    void set_sci(const std::uint8_t* d_target, std::int32_t m, const std::uint8_t* d_valid, const abmx_column* rows) {
+        check(abmx_agents_set_sci(&s_, d_target, m, d_valid, rows, nullptr, nullptr, nullptr, stream_));
+    }
+    void set_mask(const std::uint8_t* d_mask, const abmx_column* values) {
+        check(abmx_agents_set_mask(&s_, d_mask, values, stream_));
+    }
+    void sort(const double* d_key, bool descending, std::int32_t* d_perm = nullptr) {
+        check(abmx_agents_sort(&s_, d_key, descending ? 1 : 0, d_perm, stream_));
+    }
+    void permute(const std::int32_t* d_perm) { check(abmx_agents_permute(&s_, d_perm, stream_)); }
+    const abmx_agent_set& raw() const { return s_; }
+
+private:
+    abmx_agent_set s_;
+    void* stream_;
+};
 
 }  // namespace abmx::cuda
