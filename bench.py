@@ -227,12 +227,13 @@ def finance_section(args, rank, world, allreduce, dist):
     begin = rank * per
     count = per if rank < world - 1 else MARKETS - begin
     F.run_batch(cfg, MASTER_SEED, min(count, 64), 5, begin=begin)
-    _, ms = F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin)
-    ms = allreduce(ms, dist.ReduceOp.MAX if dist else None)
+    runs = [F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin)[1] for _ in range(3)]
+    ms = allreduce(statistics.median(runs), dist.ReduceOp.MAX if dist else None)
     slots = MARKETS * cfg.books * cfg.book_capacity
     out = {"workload": f"C5: {MARKETS} markets x FinanceConfig defaults (5 books x 1000 capacity, "
                        f"10 traders), {FIN_STEPS} steps (run_batch)",
            "value": slots * FIN_STEPS / (ms / 1e3), "unit": UNIT, "device_ms": ms,
+           "timing": "median of 3 device-timed run_batch launches",
            "market_steps_per_s": MARKETS * FIN_STEPS / (ms / 1e3)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))

@@ -85,6 +85,9 @@ struct Smem {
     int* q;
     long long* pl;
     unsigned short* list;  // sorted order (sort_n entries)
+    unsigned short* list2; // ping-pong buffer of the sorted order
+    unsigned short* nl;    // this step's new orders, trader order (T entries)
+    unsigned short* nsr;   // ... sorted (T entries)
     long long* cum;        // cumulative qty along the sorted list (cap entries)
     // placement rows (T entries)
     int* rq;
@@ -163,6 +166,13 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     p += 4 * T;
     S.list = reinterpret_cast<unsigned short*>(p);
     p += 2 * N;
+    // the ping-pong order buffer is used only by the merge (before matching) and the compaction
+    // (after it), never while `cum` is live: it aliases `cum` (8*cap >= 2*sort_n bytes)
+    S.list2 = reinterpret_cast<unsigned short*>(S.cum);
+    S.nl = reinterpret_cast<unsigned short*>(p);
+    p += 2 * T;
+    S.nsr = reinterpret_cast<unsigned short*>(p);
+    p += 2 * T;
     S.act = p;
     p += cap;
     S.sd = p;
@@ -184,7 +194,43 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
         S.dhold[i] = 0;
     }
     BookS B = P.bs[static_cast<size_t>(m) * P.K + k];
-    __syncthreads();
+    // The priority order of resting orders never changes (price, placed and id are fixed), so
+    // the sorted order list is built once per launch and then maintained: new orders are
+    // merged in by rank + binary search, filled / cancelled orders compacted out.
+    unsigned short* const L = S.list;
+    unsigned short* const L2 = S.list2;
+    int n = 0;
+    {
+        unsigned long long carry = 0;
+        for (int i0 = 0; i0 < N; i0 += kNT) {
+            const int i = i0 + tid;
+            const bool a = i < cap && S.act[i];
+            unsigned long long tot;
+            const unsigned long long ex = block_excl_scan<kNT>(a ? 1ULL : 0ULL, s_scan, &tot);
+            if (a) L[carry + ex] = static_cast<unsigned short>(i);
+            carry += tot;
+            __syncthreads();
+        }
+        n = static_cast<int>(carry);
+        for (int i = n + tid; i < N; i += kNT) L[i] = kPad;
+        int ns2 = 1;
+        while (ns2 < n) ns2 <<= 1;
+        __syncthreads();
+        for (int size = 2; size <= ns2; size <<= 1)
+            for (int stride = size >> 1; stride > 0; stride >>= 1) {
+                for (int j = tid; j < ns2 / 2; j += kNT) {
+                    const int lo = 2 * j - (j & (stride - 1));
+                    const int hi = lo + stride;
+                    const bool up = (lo & size) == 0;
+                    const unsigned short a = L[lo], b = L[hi];
+                    if (before(S, b, a) == up) {
+                        L[lo] = b;
+                        L[hi] = a;
+                    }
+                }
+                __syncthreads();
+            }
+    }
     const unsigned long long root = split(P.seeds[m], 8);  // FinancePlace
     const long long t_end = P.match_only ? P.t0 + 1 : P.t0 + P.steps;
     for (long long t = P.t0; t < t_end; ++t) {
@@ -237,80 +283,91 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     S.pr[i] = S.rp[r];
                     S.q[i] = S.rq[r];
                     S.pl[i] = t;
+                    S.nl[r] = static_cast<unsigned short>(i);
                 }
                 fcarry += tot;
                 __syncthreads();
             }
             const int spawned = static_cast<long long>(fcarry) < q ? static_cast<int>(fcarry) : q;
             B.next_id += spawned;
-            B.num_active += spawned;
             B.dropped = q - spawned;
-        }
-        // ---------------- match_book (finance.cpp:125-190)
-        {
-            // active orders, then a bitonic sort in priority order
-            unsigned long long carry = 0;
-            for (int i0 = 0; i0 < N; i0 += kNT) {
-                const int i = i0 + tid;
-                const bool a = i < cap && S.act[i];
-                unsigned long long tot;
-                const unsigned long long ex = block_excl_scan<kNT>(a ? 1ULL : 0ULL, s_scan, &tot);
-                if (a) S.list[carry + ex] = static_cast<unsigned short>(i);
-                carry += tot;
+            if (spawned > 0) {
+                // merge: rank the new orders among themselves, then every element's merged
+                // position = its own index + the other list's elements before it
+                for (int j = tid; j < spawned; j += kNT) {
+                    const unsigned short x = S.nl[j];
+                    int rk = 0;
+                    for (int y = 0; y < spawned; ++y) rk += before(S, S.nl[y], x);
+                    S.nsr[rk] = x;
+                }
+                __syncthreads();
+                for (int e = tid; e < n; e += kNT) {
+                    const unsigned short a = L[e];
+                    int lo = 0, hi = spawned;  // new orders before a
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (before(S, S.nsr[mid], a))
+                            lo = mid + 1;
+                        else
+                            hi = mid;
+                    }
+                    L2[e + lo] = a;
+                }
+                for (int j = tid; j < spawned; j += kNT) {
+                    const unsigned short b = S.nsr[j];
+                    int lo = 0, hi = n;  // resting orders before b
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (before(S, L[mid], b))
+                            lo = mid + 1;
+                        else
+                            hi = mid;
+                    }
+                    L2[j + lo] = b;
+                }
+                __syncthreads();
+                n += spawned;
+                for (int e = tid; e < n; e += kNT) L[e] = L2[e];  // back out of the cum alias
                 __syncthreads();
             }
-            const int n = static_cast<int>(carry);
-            for (int i = n + tid; i < N; i += kNT) S.list[i] = kPad;
-            int ns2 = 1;
-            while (ns2 < n) ns2 <<= 1;  // sort only the first power of two covering n
-            __syncthreads();
-            for (int size = 2; size <= ns2; size <<= 1)
-                for (int stride = size >> 1; stride > 0; stride >>= 1) {
-                    for (int j = tid; j < ns2 / 2; j += kNT) {
-                        const int lo = 2 * j - (j & (stride - 1));
-                        const int hi = lo + stride;
-                        const bool up = (lo & size) == 0;
-                        const unsigned short a = S.list[lo], b = S.list[hi];
-                        if (before(S, b, a) == up) {
-                            S.list[lo] = b;
-                            S.list[hi] = a;
-                        }
-                    }
-                    __syncthreads();
-                }
-            // number of buys, cumulative quantities along the sorted list (per side)
-            long long nbl = 0;
+        }
+        // ---------------- match_book (finance.cpp:125-190) on the sorted order list
+        {
+            // cumulative quantities along the sorted list; buys precede sells
             unsigned long long qcarry = 0;
-            for (int i0 = 0; i0 < n || (n == 0 && i0 == 0); i0 += kNT) {
+            for (int i0 = 0; i0 < n; i0 += kNT) {
                 const int i = i0 + tid;
-                const unsigned short s = i < n ? S.list[i] : kPad;
-                const bool buy = s != kPad && S.sd[s] == 0;
-                nbl += buy;
+                const unsigned short s = i < n ? L[i] : kPad;
                 unsigned long long tot;
                 const unsigned long long ex =
                     block_excl_scan<kNT>(s != kPad ? static_cast<unsigned long long>(S.q[s]) : 0ULL, s_scan, &tot);
                 if (s != kPad) S.cum[i] = static_cast<long long>(qcarry + ex) + S.q[s];
                 qcarry += tot;
                 __syncthreads();
-                if (n == 0) break;
             }
-            const long long nb = block_sum_nt<long long>(nbl, s_red);
-            if (tid == 0) {
-                s_n = n;
-                s_nb = static_cast<int>(nb);
+            int nbuy;
+            {
+                int lo = 0, hi = n;  // first sell in the list
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (S.sd[L[mid]] == 0)
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                nbuy = lo;
             }
-            __syncthreads();
-            const int nbuy = s_nb, nsell = s_n - s_nb;
+            const int nsell = n - nbuy;
             const long long btot = nbuy > 0 ? S.cum[nbuy - 1] : 0;  // sells' cum = cum - btot
             // executed volume: max over buys of min(buy cum, sell cum at upper_bound(buy price))
             long long vmax = 0;
             if (nbuy > 0 && nsell > 0)
                 for (int i = tid; i < nbuy; i += kNT) {
-                    const double bp = S.pr[S.list[i]];
+                    const double bp = S.pr[L[i]];
                     int lo = 0, hi = nsell;  // first sell with price > bp
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (bp < S.pr[S.list[nbuy + mid]])
+                        if (bp < S.pr[L[nbuy + mid]])
                             hi = mid;
                         else
                             lo = mid + 1;
@@ -326,17 +383,12 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
             }
             if ((tid & 31) == 0) s_red[tid >> 5] = vmax;
             __syncthreads();
-            if (tid == 0) {
-                long long v = 0;
-                for (int w = 0; w < kNT / 32; ++w) v = s_red[w] > v ? s_red[w] : v;
-                s_vol = v;
-            }
-            __syncthreads();
-            const long long volume = s_vol;
+            long long volume = 0;
+            for (int w = 0; w < kNT / 32; ++w) volume = s_red[w] > volume ? s_red[w] : volume;
             B.volume = 0;
             if (volume > 0) {
                 // marginal orders: first cum >= volume on each side
-                int mb = 0, ms = 0;
+                int mb, ms;
                 {
                     int lo = 0, hi = nbuy - 1;
                     while (lo < hi) {
@@ -358,11 +410,11 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     }
                     ms = lo;
                 }
-                const double clearing = __dadd_rn(S.pr[S.list[mb]], S.pr[S.list[nbuy + ms]]) / 2.0;
+                const double clearing = __dadd_rn(S.pr[L[mb]], S.pr[L[nbuy + ms]]) / 2.0;
                 __syncthreads();  // every thread has read the sorted prices before fills reset slots
                 // fills: sorted order j gets min(qty_j, volume - cum_{j-1}) while positive
                 for (int j = tid; j < n; j += kNT) {
-                    const unsigned short s = S.list[j];
+                    const unsigned short s = L[j];
                     const bool buy = j < nbuy;
                     const long long before_j = buy ? (j > 0 ? S.cum[j - 1] : 0) : (j > nbuy ? S.cum[j - 1] - btot : 0);
                     const long long rem = volume - before_j;
@@ -394,33 +446,46 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
             __syncthreads();
         }
         if (P.match_only) break;
-        // ---------------- cancel at the age limit (finance.cpp:236-245); count the book
-        long long nbl = 0, nsl = 0, na = 0;
-        for (int i = tid; i < cap; i += kNT) {
-            if (!S.act[i]) continue;
-            if (t - S.pl[i] >= P.max_age) {
-                reset_slot(S, i);
-                continue;
+        // ---------------- cancel at the age limit (finance.cpp:236-245) and compact the order
+        // list: one scan of packed (alive, alive buy) counters over the sorted list
+        {
+            unsigned long long carry = 0;
+            for (int i0 = 0; i0 < n; i0 += kNT) {
+                const int i = i0 + tid;
+                bool alive = false, buy = false;
+                unsigned short s = kPad;
+                if (i < n) {
+                    s = L[i];
+                    if (S.act[s]) {
+                        if (t - S.pl[s] >= P.max_age)
+                            reset_slot(S, s);
+                        else
+                            alive = true;
+                    }
+                    buy = alive && S.sd[s] == 0;
+                }
+                unsigned long long tot;
+                const unsigned long long ex = block_excl_scan<kNT>(
+                    (alive ? (1ULL << 32) : 0ULL) | (buy ? 1ULL : 0ULL), s_scan, &tot);
+                if (alive) L2[(carry >> 32) + (ex >> 32)] = s;
+                carry += tot;
+                __syncthreads();
             }
-            ++na;
-            if (S.sd[i] == 0)
-                ++nbl;
-            else
-                ++nsl;
+            n = static_cast<int>(carry >> 32);
+            for (int e = tid; e < n; e += kNT) L[e] = L2[e];  // back out of the cum alias
+            __syncthreads();
+            const long long nb = static_cast<long long>(carry & 0xFFFFFFFFULL);
+            B.num_active = n;
+            if (tid == 0) {  // collect_metrics (finance.cpp:262-276)
+                double* row = P.metrics + ((static_cast<size_t>(m) * P.steps + (t - P.t0)) * P.K + k) * 6;
+                row[0] = static_cast<double>(k);
+                row[1] = B.last_price;
+                row[2] = static_cast<double>(nb);
+                row[3] = static_cast<double>(n - nb);
+                row[4] = static_cast<double>(B.volume);
+                row[5] = static_cast<double>(B.dropped);
+            }
         }
-        const long long nb = block_sum_nt<long long>(nbl, s_red);
-        const long long nsv = block_sum_nt<long long>(nsl, s_red);
-        B.num_active = static_cast<int>(block_sum_nt<long long>(na, s_red));
-        if (tid == 0) {  // collect_metrics (finance.cpp:262-276)
-            double* row = P.metrics + ((static_cast<size_t>(m) * P.steps + (t - P.t0)) * P.K + k) * 6;
-            row[0] = static_cast<double>(k);
-            row[1] = B.last_price;
-            row[2] = static_cast<double>(nb);
-            row[3] = static_cast<double>(nsv);
-            row[4] = static_cast<double>(B.volume);
-            row[5] = static_cast<double>(B.dropped);
-        }
-        __syncthreads();
     }
     // store the book, fold this book's settlement into the traders
     for (int i = tid; i < cap; i += kNT) {
@@ -509,7 +574,7 @@ int check_cfg(const abmx_finance_config& c) {
 
 size_t fin_smem(const abmx_finance_config& c, int sort_n) {
     const size_t cap = static_cast<size_t>(c.book_capacity), T = static_cast<size_t>(c.traders);
-    return 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 2 * cap + T + 64;
+    return 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 4 * T + 2 * cap + T + 64;
 }
 
 }  // namespace
@@ -586,7 +651,7 @@ struct abmx_finance {
         P.seeds = sd;
         CKF(cudaMemcpy(sd, seeds, static_cast<size_t>(M) * 8, cudaMemcpyHostToDevice));
         smem = fin_smem(c, P.sort_n);
-        if (smem > 220 * 1024) {
+        if (smem > 226 * 1024) {  // sm_100: 227 KB of dynamic shared memory per CTA (minus static)
             abmx_internal::set_error("finance: book_capacity / traders too large for one shared-memory book");
             return ABMX_E_CAPACITY;
         }
