@@ -68,3 +68,42 @@ def test_gather_reproduces_run_batch_order(oracle, tmp_path, total):
     got = np.load(out)
     want = oracle.run_batch(CFG, 11, total, steps)
     assert np.array_equal(got, want)
+
+
+def _worker_models(rank, world, port, total, steps, out_path):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import torch.distributed as dist
+    import pyoracle
+    from paper_2508_16508_b200.sharding import gather_rows, shard_range
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    begin, count = shard_range(total, world, rank)
+    o = pyoracle.Oracle()
+    traffic = np.zeros((count, steps, 4))
+    fin = np.zeros((count, steps, 2, 6))
+    for k in range(count):
+        seed = o.replica_seed(13, begin + k)
+        m = o.traffic(15, 10, 0.5, seed)
+        f = o.fin(seed, books=2, book_capacity=32)
+        for t in range(1, steps + 1):
+            m.step(t)
+            f.step(t)
+            traffic[k, t - 1] = m.metrics()
+            fin[k, t - 1] = f.metrics()
+    full_t = gather_rows(traffic, dist)
+    full_f = gather_rows(fin.reshape(count, steps, 12), dist)
+    if rank == 0:
+        np.save(out_path + ".t.npy", full_t)
+        np.save(out_path + ".f.npy", full_f)
+    dist.destroy_process_group()
+
+
+def test_gather_traffic_and_finance_shards(oracle, tmp_path):
+    """The C4 roads / C5 markets shards of bench.py: contiguous replica blocks, one gather."""
+    total, steps = 7, 10
+    out = str(tmp_path / "rows")
+    mp.spawn(_worker_models, args=(2, _free_port(), total, steps, out), nprocs=2, join=True)
+    assert np.array_equal(np.load(out + ".t.npy"), oracle.traffic_run_batch(15, 10, 0.5, 13, total, steps))
+    want_f = oracle.fin_run_batch(13, total, steps, books=2, book_capacity=32)
+    assert np.array_equal(np.load(out + ".f.npy").reshape(total, steps, 2, 6), want_f)
