@@ -21,6 +21,8 @@
 // HBM layout (per species, per replica, stride Npad): active u8, cell i32 (= y*W + x),
 // age i32, energy f64, id i64; the agent type is implied by the species. Per cell one uint4
 // (list heads, lowest sheep slot, grass due epoch — see "per-cell words").
+#include <atomic>
+#include <chrono>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
@@ -848,6 +850,14 @@ __global__ void __launch_bounds__(kT) k_book(Params P) {
         if (P.host_row) {
             long long* h = P.host_row + static_cast<size_t>(r) * 4;
             for (int q = 0; q < 4; ++q) h[q] = row[q];
+            // publish: the last of the R rows of this call bumps the mapped sequence word, so
+            // the host can poll it instead of waiting for the stream to drain
+            __threadfence_system();
+            const unsigned long long done = atomicAdd(P.book_count, 1ULL) + 1ULL;
+            if (done == P.book_seq * static_cast<unsigned long long>(P.R)) {
+                __threadfence_system();
+                *reinterpret_cast<volatile long long*>(P.host_seq) = static_cast<long long>(P.book_seq);
+            }
         }
     }
 }
@@ -944,6 +954,7 @@ Engine::~Engine() {
     if (graph) cudaGraphDestroy(graph);
     if (step_exec) cudaGraphExecDestroy(step_exec);
     if (h_metrics_pinned) cudaFreeHost(h_metrics_pinned);
+    if (d_book_count) cudaFree(d_book_count);
     if (step_graph) cudaGraphDestroy(step_graph);
     for (void* p : allocs) cudaFree(p);
     if (d_run_metrics) cudaFree(d_run_metrics);
@@ -1102,8 +1113,11 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
     abmx_internal::count_launch(3);
     CK(cudaGetLastError());
     CK(cudaMemsetAsync(d_metrics_step, 0, sizeof(long long) * 4 * R, stream));
-    CK(cudaHostAlloc(reinterpret_cast<void**>(&h_metrics_pinned), sizeof(long long) * 4 * R, cudaHostAllocMapped));
-    memset(h_metrics_pinned, 0, sizeof(long long) * 4 * R);
+    // R metrics rows + the sequence word k_book publishes after them
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&h_metrics_pinned), sizeof(long long) * (4 * R + 1), cudaHostAllocMapped));
+    memset(h_metrics_pinned, 0, sizeof(long long) * (4 * R + 1));
+    CK(cudaMalloc(&d_book_count, 8));
+    CK(cudaMemset(d_book_count, 0, 8));
     CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_metrics_dev), h_metrics_pinned, 0));
     return ABMX_OK;
 }
@@ -1233,6 +1247,9 @@ int Engine::step(long long t) {
     fin.birth_epoch = host_epoch;
     fin.birth_row = params.run_step;
     fin.host_row = h_metrics_dev;
+    fin.host_seq = h_metrics_dev + 4 * static_cast<size_t>(R);
+    fin.book_count = d_book_count;
+    fin.book_seq = ++step_seq;
     void* args[1] = {&params};
     void* fargs[1] = {&fin};
     auto kparams = [&](int k, void** a) {
@@ -1326,7 +1343,23 @@ int Engine::last_metrics(long long* out) {
     }
     if (last_run_steps == 0) {
         if (host_row_valid) {  // k_book of the last step() wrote the row to mapped memory
-            CK(cudaStreamSynchronize(stream));
+            // poll the mapped sequence word k_book publishes after the rows (cheaper than the
+            // stream-completion path); a missing word (a fault) falls back to the stream sync,
+            // which reports the error
+            const volatile long long* seq = h_metrics_pinned + 4 * static_cast<size_t>(R);
+            const auto t0 = std::chrono::steady_clock::now();
+            bool seen = false;
+            for (unsigned spin = 0;; ++spin) {
+                if (*seq == static_cast<long long>(step_seq)) {
+                    seen = true;
+                    break;
+                }
+                if ((spin & 1023u) == 1023u &&
+                    std::chrono::steady_clock::now() - t0 > std::chrono::milliseconds(200))
+                    break;
+            }
+            if (!seen) CK(cudaStreamSynchronize(stream));
+            std::atomic_thread_fence(std::memory_order_acquire);
             memcpy(out, h_metrics_pinned, sizeof(long long) * 4 * R);
             return ABMX_OK;
         }

@@ -64,6 +64,9 @@ struct Params {
     unsigned birth_row;              // metrics row of that step
     unsigned book;                   // 1: the births pass also does that step's bookkeeping
     long long* host_row;             // k_book: mapped host copy of the metrics row (or null)
+    long long* host_seq;             //   ... then this mapped sequence word = book_seq
+    unsigned long long* book_count;  //   k_book CTAs done (device; the R-th of a call publishes)
+    unsigned long long book_seq;
     // model constants
     int R, W, H, Cpad;
     long long C;
@@ -116,6 +119,8 @@ struct Engine {
     long long* h_metrics_pinned = nullptr;     // mapped pinned copy of the step() metrics row
     long long* h_metrics_dev = nullptr;        //   ... its device alias (written by k_book)
     bool host_row_valid = false;               // the mapped row holds the last step()'s row
+    unsigned long long step_seq = 0;           // step() calls (the sequence k_book publishes)
+    unsigned long long* d_book_count = nullptr;
     std::vector<void*> allocs;
     long long device_bytes = 0;
     unsigned long long* d_seeds = nullptr;
