@@ -310,3 +310,24 @@ def test_world_import_mid_run(abmx, reference):
         ref.step(t)
         assert_same_state(gpu, ref, f"t={t}")
         assert gpu.collect_metrics()[0].tolist() == ref.metrics(), t
+
+
+def test_per_call_step_paths_agree(abmx):
+    """The per-call path (step + collect_metrics: one graph whose k_book publishes the rows and
+    a sequence word to mapped memory) agrees with run() for a batch of replicas, including
+    switches between the two paths and state reads in between."""
+    cfg = abmx.PredationConfig(**tiny(width=16, height=16, sheep_capacity=600, wolf_capacity=600))
+    seeds = abmx.replica_seeds(5, 4)
+    want = abmx.PredationModel(cfg, seeds).run(1, 30)
+    m = abmx.PredationModel(cfg, seeds)
+    for t in range(1, 11):
+        m.step(t)
+        assert np.array_equal(m.collect_metrics(), want[:, t - 1].astype(np.int64)), t
+    rows = m.run(11, 10)
+    assert np.array_equal(rows, want[:, 10:20])
+    assert np.array_equal(m.collect_metrics(), want[:, 19].astype(np.int64))
+    for t in range(21, 31):
+        m.step(t)
+        if t == 25:
+            m.export_species(0, replica=2)  # a state read applies the pending births
+        assert np.array_equal(m.collect_metrics(), want[:, t - 1].astype(np.int64)), t
