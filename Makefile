@@ -13,7 +13,7 @@ NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -fmad=false -Xcompiler -fPIC -Xcompi
 PKG     := paper_2508_16508_b200
 SRC     := $(PKG)/csrc
 OBJDIR  := build/obj
-CU      := table predation ensemble agents traffic traffic_ens finance capi
+CU      := table predation ensemble agents traffic traffic_ens finance diag capi
 OBJS    := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU)))
 HDRS    := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/abmx_cuda.h
 

@@ -326,12 +326,27 @@ def our_arm(args, rank, world, local_rank, dist):
         except Exception:
             traffic = None
     step_bytes = 42 * capacity(C2) + 2 * C2["width"] * C2["height"] + 8 * bd
+    # the access-pattern ceiling: the same random cell-word atomics / reads, and
+    # nothing else, in the same launch shape and live fractions, L2 flushed, event-timed
+    n_tiles = capacity(C2) // 2 // 1024
+    ls = float(met[0, :, 0].mean()) / C2["sheep_capacity"]
+    lw = float(met[0, :, 1].mean()) / C2["wolf_capacity"]
+    atom_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 0, True)
+    read_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 1, True)
+    access = {"bound": "l2_random_atomics", "unit": "us",
+              "k_move_ceiling": atom_us, "k_move_achieved": avg["k_move"] * 1e3,
+              "k_move_frac": atom_us / (avg["k_move"] * 1e3),
+              "k_update_read_ceiling": read_us, "k_update_achieved": avg["k_update"] * 1e3,
+              "note": "ceiling = event-timed kernel doing ONLY the step's random cell-word "
+                      "atomicExch+atomicMax (k_move) / 16-byte reads (k_update), same grid and "
+                      "live fractions, L2 flushed; frac = ceiling time / kernel time"}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes": kb[dom], "avg_launch_ms": avg[dom],
                 "kernel_share": avg[dom] / step_sum,
                 "per_kernel_ms": avg,
-                "step_effective_gbs": step_bytes / (total_ms / K / 1e3) / 1e9}
+                "step_effective_gbs": step_bytes / (total_ms / K / 1e3) / 1e9,
+                "access_bound": access}
 
     # e2e through the C-ABI: step(t) [H2D t] + collect_metrics [D2H row], L2 flushed between
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")

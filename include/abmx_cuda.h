@@ -155,6 +155,14 @@ int abmx_predation_set_timing(abmx_predation* h, int enabled);
 int32_t abmx_predation_kernel_count(void);
 const char* abmx_predation_kernel_name(int32_t k);
 int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches);
+/* diagnostics: the random-access ceiling of the predation kernels' cell-word pattern (see
+ * DESIGN.md §4): `cells` 16-byte words, sheep_ctas + wolf_ctas CTAs of 256 threads x 4 slots
+ * with the given live fractions; mode 0 = one returning atomicExch per live slot plus one
+ * atomicMax per live sheep, mode 1 = one random 16-byte read per live slot; cold = L2 flushed
+ * before every launch. Event-timed like the bench's per-kernel times (microseconds). */
+int abmx_diag_random_access(int64_t cells, int32_t sheep_ctas, int32_t wolf_ctas, double live_sheep,
+                            double live_wolves, int32_t mode, int32_t cold, int32_t reps,
+                            double* min_us, double* mean_us);
 /* diagnostics: per-CTA phase timestamps (%globaltimer ns) of k_move / k_update, recorded only
  * by builds compiled with -DABMX_PRED_TRACE; [2][CTAs][8], returns the number of entries */
 int abmx_predation_set_trace(abmx_predation* h, int32_t enable);

@@ -197,6 +197,18 @@ _sig("abmx_predation_fetch_metrics", C.c_int, [C.c_void_p, f64p])
 _sig("abmx_ensemble_run", C.c_int, [C.POINTER(PredationConfig), C.c_uint64, C.c_int32, C.c_int32,
                                     C.c_int64, C.c_int32, f64p, f64p])
 _sig("abmx_ensemble_smem_fits", C.c_int, [C.POINTER(PredationConfig)])
+_sig("abmx_diag_random_access", C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                          C.c_int32, C.c_int32, C.c_int32, f64p, f64p])
+
+
+def diag_random_access(cells, sheep_ctas, wolf_ctas, live_sheep, live_wolves, mode=0, cold=True,
+                       reps=10):
+    """Measured ceiling of the predation kernels' cell-word access pattern:
+    (min_us, mean_us) of a kernel doing only those random atomics (mode 0) / reads (mode 1)."""
+    mn, me = C.c_double(), C.c_double()
+    _check(lib.abmx_diag_random_access(cells, sheep_ctas, wolf_ctas, live_sheep, live_wolves, mode,
+                                       int(cold), reps, C.byref(mn), C.byref(me)))
+    return mn.value, me.value
 
 _ERRORS = {1: DomainError, 2: CapacityError, 3: SchemaError, 4: BatchError, 5: CudaError,
            6: AbmxError, 7: ContractError}
