@@ -299,11 +299,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
         const unsigned pairs = F < Q ? F : Q;
         full = tile == 0 || Q > F || hi31(s_gt[1]) < pairs;
     }
-#ifdef ABMX_EXP_NO_BIRTHS  // timing ablation only (results are wrong)
-    if (false) {
-#else
     if (full) {
-#endif
         const int tiles = P.tiles[s];
         const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
         unsigned long long carry = 0;  // exclusive prefix of the tile counts -> s_pre
@@ -651,11 +647,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
                         ++n_graze;
                     }
             }
-#ifdef ABMX_EXP_NO_PAIR  // timing ablation only
-            if (false) {
-#else
             if (!P.crowded) {
-#endif
                 // predation (predation.cpp:197-239): in a cell holding wolves and sheep the k-th
                 // wolf by slot takes the k-th sheep by slot. Each agent ranks itself in its own
                 // cell list and counts the other species' list; the up to 2*kS walks of a thread
