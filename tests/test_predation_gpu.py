@@ -104,7 +104,9 @@ def test_birth_pairs_match_reference(abmx, reference):
 
 @pytest.mark.parametrize("case", ["one_cell_two_sheep", "wolf_and_sheep", "two_wolves_one_sheep",
                                   "overflow", "starve", "regrow_zero", "regrow_negative",
-                                  "crowded_cell"])
+                                  "crowded_cell", "empty_world", "no_wolf_capacity",
+                                  "no_sheep_capacity", "one_row", "one_column", "full_at_start",
+                                  "crowded_multi_tile"])
 def test_unit_cases_vs_reference(abmx, reference, case):
     """tests/test_predation.cpp:89-224 setups, compared field-by-field with the reference."""
     cfgd = tiny()
@@ -128,6 +130,22 @@ def test_unit_cases_vs_reference(abmx, reference, case):
         # long per-cell lists: exercises the pool + heap-sort pairing path
         cfgd = tiny(width=2, height=1, n_sheep0=300, n_wolves0=40, sheep_capacity=400,
                     wolf_capacity=400)
+    elif case == "empty_world":  # test_predation.cpp:63-72, 89-103
+        cfgd = tiny(n_sheep0=0, n_wolves0=0)
+    elif case == "no_wolf_capacity":
+        cfgd = tiny(n_wolves0=0, wolf_capacity=0)
+    elif case == "no_sheep_capacity":
+        cfgd = tiny(n_sheep0=0, sheep_capacity=0)
+    elif case == "one_row":
+        cfgd = tiny(width=64, height=1, n_sheep0=40, n_wolves0=10)
+    elif case == "one_column":
+        cfgd = tiny(width=1, height=64, n_sheep0=40, n_wolves0=10)
+    elif case == "full_at_start":
+        cfgd = tiny(n_sheep0=400, n_wolves0=400, sheep_capacity=400, wolf_capacity=400)
+    elif case == "crowded_multi_tile":
+        # more slots than cells over several 1024-slot tiles: the sort-based k_cells pairing
+        cfgd = tiny(width=30, height=30, n_sheep0=1500, n_wolves0=500, sheep_capacity=2500,
+                    wolf_capacity=2500)
     gpu = abmx.PredationModel(abmx.PredationConfig(**cfgd), seed)
     ref = reference.pred(cfgd, seed)
     if case == "overflow":
