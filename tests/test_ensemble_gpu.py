@@ -42,6 +42,10 @@ def test_replica_offsets_shard_cleanly(abmx, oracle):
     tiny(n_sheep0=8, sheep_capacity=8, reproduce_prob_sheep=1.0),
     c1(sheep_capacity=2000, wolf_capacity=600),
     c1(width=30, height=7, n_sheep0=200, n_wolves0=150, sheep_capacity=3000, wolf_capacity=4000),
+    tiny(n_sheep0=0, n_wolves0=0), tiny(n_wolves0=0, wolf_capacity=0),
+    tiny(n_sheep0=0, sheep_capacity=0), tiny(width=64, height=1, n_sheep0=40, n_wolves0=10),
+    tiny(width=1, height=64, n_sheep0=40, n_wolves0=10), tiny(regrow_delay=-2),
+    tiny(regrow_delay=254), tiny(n_sheep0=400, n_wolves0=400, sheep_capacity=400, wolf_capacity=400),
 ])
 def test_smem_path_edge_configs(abmx, oracle, cfgd):
     got, _ = abmx.run_batch(abmx.PredationConfig(**cfgd), 11, 6, 40, path=1)
