@@ -179,8 +179,12 @@ def traffic_section(args, rank, world, allreduce, dist):
     begin = rank * per
     count = per if rank < world - 1 else ROADS - begin
     T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, min(count, 64), 5, begin=begin)
-    _, rk = T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS,
-                        begin=begin)
+    rows_r, rk = T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS,
+                             begin=begin)
+    gathered = count
+    if dist is not None:  # one all-gather of the metrics rows, replica order
+        from paper_2508_16508_b200.sharding import gather_rows
+        gathered = gather_rows(rows_r, dist, device="cuda").shape[0]
     rk = allreduce(rk, dist.ReduceOp.MAX if dist else None)
     out = {"workload": f"C4: one road L={TRAFFIC_L} (capacity {cap} slots) per GPU, period 10, "
                        f"green 0.5, seed {MASTER_SEED}",
@@ -188,6 +192,7 @@ def traffic_section(args, rank, world, allreduce, dist):
            "per_kernel_ms": kt,
            "step_effective_gbs": alg / (tot / K / 1e3) / 1e9,
            "roads": {"workload": f"{ROADS} roads x L={ROADS_L}, {ROADS_STEPS} steps (run_batch)",
+                     "rows_gathered": gathered,
                      "value": ROADS * 3 * ROADS_L * ROADS_STEPS / (rk / 1e3), "unit": UNIT,
                      "device_ms": rk}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -227,13 +232,18 @@ def finance_section(args, rank, world, allreduce, dist):
     begin = rank * per
     count = per if rank < world - 1 else MARKETS - begin
     F.run_batch(cfg, MASTER_SEED, min(count, 64), 5, begin=begin)
-    runs = [F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin)[1] for _ in range(3)]
-    ms = allreduce(statistics.median(runs), dist.ReduceOp.MAX if dist else None)
+    res = [F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin) for _ in range(3)]
+    ms = allreduce(statistics.median([r[1] for r in res]), dist.ReduceOp.MAX if dist else None)
+    gathered = count
+    if dist is not None:  # one all-gather of the metrics rows, replica order
+        from paper_2508_16508_b200.sharding import gather_rows
+        r0 = res[0][0]
+        gathered = gather_rows(r0.reshape(r0.shape[0], r0.shape[1], -1), dist, device="cuda").shape[0]
     slots = MARKETS * cfg.books * cfg.book_capacity
     out = {"workload": f"C5: {MARKETS} markets x FinanceConfig defaults (5 books x 1000 capacity, "
                        f"10 traders), {FIN_STEPS} steps (run_batch)",
            "value": slots * FIN_STEPS / (ms / 1e3), "unit": UNIT, "device_ms": ms,
-           "timing": "median of 3 device-timed run_batch launches",
+           "timing": "median of 3 device-timed run_batch launches", "markets_gathered": gathered,
            "market_steps_per_s": MARKETS * FIN_STEPS / (ms / 1e3)}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
