@@ -58,3 +58,10 @@ def test_run_batch_errors(abmx):
         abmx.run_batch(abmx.PredationConfig(**c1()), 1, 0, 5)
     with pytest.raises(abmx.DomainError):
         abmx.run_batch(abmx.PredationConfig(**c1()), 1, 2, 0)
+
+
+def test_long_ensemble_run(abmx, oracle):
+    """700 steps of C1 replicas in the on-chip kernel (grass countdowns and per-step list
+    clears over a long run)."""
+    got, _ = abmx.run_batch(abmx.PredationConfig(**c1()), 19, 6, 700, path=1)
+    assert np.array_equal(got, oracle.run_batch(c1(), 19, 6, 700))

@@ -162,3 +162,9 @@ def test_run_batch_vs_oracle(F, oracle, kw, K, T):
     rows, _ = F.run_batch(F.FinanceConfig(**kw), 7, K, T)
     want = oracle.fin_run_batch(7, K, T, **kw)
     assert np.array_equal(rows, want)
+
+
+def test_long_finance_run(F, oracle):
+    """1500 steps in one launch: order ids, ages and the maintained order list over a long run."""
+    rows, _ = F.run_batch(F.FinanceConfig(book_capacity=128, max_order_age=30), 29, 4, 1500)
+    assert np.array_equal(rows, oracle.fin_run_batch(29, 4, 1500, book_capacity=128, max_order_age=30))

@@ -349,3 +349,24 @@ def test_per_call_step_paths_agree(abmx):
         if t == 25:
             m.export_species(0, replica=2)  # a state read applies the pending births
         assert np.array_equal(m.collect_metrics(), want[:, t - 1].astype(np.int64)), t
+
+
+@pytest.mark.parametrize("cfgname", ["tiny", "tiny_delay300", "c1", "crowded"])
+def test_long_runs_cross_epoch_wraparounds(abmx, oracle, cfgname):
+    """700 steps: the 8-bit list tags wrap (255), the cell words are cleared every 128 steps,
+    the lowest-slot tags cycle (128) and, with delay 300, due epochs span several clears. Every
+    metrics row and the final state equal the oracle; a per-call tail after a run() segment."""
+    cfgd = {"tiny": tiny(), "tiny_delay300": tiny(regrow_delay=300),
+            "c1": c1(), "crowded": tiny(width=10, height=10, n_sheep0=150, n_wolves0=60,
+                                        sheep_capacity=400, wolf_capacity=400)}[cfgname]
+    seed = abmx.replica_seeds(9, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, cfgd, seed)
+    rows = gpu.run(1, 650)[0]
+    for t in range(1, 651):
+        orc.step(t)
+        assert rows[t - 1].astype(np.int64).tolist() == orc.metrics(), (cfgname, t)
+    for t in range(651, 701):
+        gpu.step(t)
+        orc.step(t)
+        assert gpu.collect_metrics()[0].tolist() == orc.metrics(), (cfgname, t)
+    assert_same_state(gpu, orc, f"{cfgname} t=700")

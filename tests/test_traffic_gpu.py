@@ -226,3 +226,10 @@ def test_run_batch_path_limits(abmx, T):
         T.run_batch(T.TrafficConfig(20000, 10, 0.5), 1, 2, 2, path=1)
     with pytest.raises(abmx.DomainError):
         T.run_batch(T.TrafficConfig(10, 0, 0.5), 1, 2, 2)
+
+
+@pytest.mark.parametrize("path", [1, 2])
+def test_long_traffic_runs(T, oracle, path):
+    """2000 steps: epoch-tagged bids and lookback words, id growth, signal phases."""
+    rows, _ = T.run_batch(T.TrafficConfig(40, 7, 0.4), 23, 6, 2000, path=path)
+    assert np.array_equal(rows, oracle.traffic_run_batch(40, 7, 0.4, 23, 6, 2000))
