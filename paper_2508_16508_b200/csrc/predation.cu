@@ -1285,6 +1285,19 @@ int Engine::step(long long t) {
     return ABMX_OK;
 }
 
+int Engine::reserve_run(long long steps) {
+    const size_t mbytes = sizeof(long long) * 4 * static_cast<size_t>(R) * static_cast<size_t>(steps);
+    if (mbytes > run_metrics_bytes) {
+        CK(cudaStreamSynchronize(stream));
+        if (d_run_metrics) cudaFree(d_run_metrics);
+        d_run_metrics = nullptr;
+        run_metrics_bytes = 0;
+        CK(cudaMalloc(&d_run_metrics, mbytes));
+        run_metrics_bytes = mbytes;
+    }
+    return ABMX_OK;
+}
+
 int Engine::prepare_run(long long t0, long long steps) {
     if (steps > 0x7FFFFFFFLL) {
         abmx_internal::set_error("too many steps in one run");
@@ -1293,12 +1306,8 @@ int Engine::prepare_run(long long t0, long long steps) {
     const size_t mbytes = sizeof(long long) * 4 * static_cast<size_t>(R) * static_cast<size_t>(steps);
     int rc = finalize();
     if (rc) return rc;
-    if (mbytes > run_metrics_bytes) {
-        CK(cudaStreamSynchronize(stream));
-        if (d_run_metrics) cudaFree(d_run_metrics);
-        CK(cudaMalloc(&d_run_metrics, mbytes));
-        run_metrics_bytes = mbytes;
-    }
+    rc = reserve_run(steps);
+    if (rc) return rc;
     CK(cudaMemsetAsync(d_run_metrics, 0, mbytes, stream));
     rc = set_metrics_target(d_run_metrics, static_cast<unsigned>(steps));
     if (rc) return rc;

