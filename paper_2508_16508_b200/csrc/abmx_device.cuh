@@ -91,6 +91,13 @@ template <int kThreads>
 __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long v,
                                                               unsigned long long* smem,
                                                               unsigned long long* block_total) {
+    if constexpr (kThreads == 32) {  // one-warp CTA: no shared memory, warp barriers only
+        __syncwarp();
+        const unsigned long long incl1 = warp_incl_scan(v);
+        *block_total = __shfl_sync(0xffffffffu, incl1, 31);
+        __syncwarp();
+        return incl1 - v;
+    }
     constexpr int kWarps = kThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned long long incl = warp_incl_scan(v);
@@ -105,6 +112,29 @@ __device__ __forceinline__ unsigned long long block_excl_scan(unsigned long long
     __syncthreads();
     *block_total = smem[kWarps];
     return smem[warp] + incl - v;
+}
+
+// Block exclusive scan of a small count (the block total stays below 2^32).
+template <int kThreads>
+__device__ __forceinline__ unsigned block_excl_count(unsigned v, unsigned long long* smem, unsigned* block_total) {
+    if constexpr (kThreads == 32) {
+        __syncwarp();
+        const int lane = threadIdx.x & 31;
+        unsigned x = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned n = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += n;
+        }
+        *block_total = __shfl_sync(0xffffffffu, x, 31);
+        __syncwarp();
+        return x - v;
+    } else {
+        unsigned long long t;
+        const unsigned long long e = block_excl_scan<kThreads>(v, smem, &t);
+        *block_total = static_cast<unsigned>(t);
+        return static_cast<unsigned>(e);
+    }
 }
 
 // Decoupled lookback (single pass). Called by ONE full warp of the tile after the tile

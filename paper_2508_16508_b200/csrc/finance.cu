@@ -102,16 +102,30 @@ struct Smem {
     double* rp;
     uint8_t* rs;
     int* rt;
+    unsigned long long* key;  // kKeyed: (side, price) priority packed in one word, per slot
     double* dcash;       // [T] cash delta of this book
     long long* dhold;    // [T] holdings delta of this book
 };
 
-// sort order: buys before sells; buys by price desc, sells by price asc; then placed, id, slot
+// (side, price) priority of an order placed by the kernel (side 0/1, price a positive finite
+// double): one unsigned compare orders buys first by price desc, then sells by price asc.
+__device__ __forceinline__ unsigned long long prio_key(uint8_t side, double price) {
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(price));
+    return side ? (1ULL << 63) | b : ~b & 0x7FFFFFFFFFFFFFFFULL;
+}
+
+// sort order: buys before sells; buys by price desc, sells by price asc; then placed, id, slot.
+// kKeyed: every order was placed by this kernel, so (side, price) is the packed key.
+template <bool kKeyed>
 __device__ __forceinline__ bool before(const Smem& S, unsigned short a, unsigned short b) {
     if (b == kPad) return a != kPad;
     if (a == kPad) return false;
-    if (S.sd[a] != S.sd[b]) return S.sd[a] < S.sd[b];
-    if (S.pr[a] != S.pr[b]) return S.sd[a] == 0 ? S.pr[a] > S.pr[b] : S.pr[a] < S.pr[b];
+    if constexpr (kKeyed) {
+        if (S.key[a] != S.key[b]) return S.key[a] < S.key[b];
+    } else {
+        if (S.sd[a] != S.sd[b]) return S.sd[a] < S.sd[b];
+        if (S.pr[a] != S.pr[b]) return S.sd[a] == 0 ? S.pr[a] > S.pr[b] : S.pr[a] < S.pr[b];
+    }
     if (S.pl[a] != S.pl[b]) return S.pl[a] < S.pl[b];
     if (S.id[a] != S.id[b]) return S.id[a] < S.id[b];
     return a < b;
@@ -127,7 +141,7 @@ __device__ __forceinline__ void reset_slot(const Smem& S, int i) {  // agent_set
     S.pl[i] = 0;
 }
 
-template <int kNT>
+template <int kNT, bool kKeyed>
 __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     extern __shared__ unsigned char smraw[];
     __shared__ unsigned long long s_scan[kNT / 32 + 1];
@@ -147,6 +161,8 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     p += 8 * W;
     S.cum = reinterpret_cast<long long*>(p);
     p += 8 * W;
+    S.key = reinterpret_cast<unsigned long long*>(p);
+    if (kKeyed) p += 8 * W;
     S.rp = reinterpret_cast<double*>(p);
     p += 8 * T;
     S.dcash = reinterpret_cast<double*>(p);
@@ -183,6 +199,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
         S.tr[i] = P.trader[bo + i];
         S.sd[i] = P.side[bo + i];
         S.pr[i] = P.price[bo + i];
+        if (kKeyed) S.key[i] = prio_key(S.sd[i], S.pr[i]);
         S.q[i] = P.qty[bo + i];
         S.pl[i] = P.placed[bo + i];
     }
@@ -202,8 +219,8 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
         for (int i0 = 0; i0 < N; i0 += kNT) {
             const int i = i0 + tid;
             const bool a = i < W && S.act[i];
-            unsigned long long tot;
-            const unsigned long long ex = block_excl_scan<kNT>(a ? 1ULL : 0ULL, s_scan, &tot);
+            unsigned tot;
+            const unsigned ex = block_excl_count<kNT>(a ? 1u : 0u, s_scan, &tot);
             if (a) L[carry + ex] = static_cast<unsigned short>(i);
             carry += tot;
             __syncthreads();
@@ -220,7 +237,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     const int hi = lo + stride;
                     const bool up = (lo & size) == 0;
                     const unsigned short a = L[lo], b = L[hi];
-                    if (before(S, b, a) == up) {
+                    if (before<kKeyed>(S, b, a) == up) {
                         L[lo] = b;
                         L[hi] = a;
                     }
@@ -251,8 +268,8 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                         pr = quantize(__dmul_rn(B.last_price, __dadd_rn(1.0, eps)));
                     }
                 }
-                unsigned long long tot;
-                const unsigned long long ex = block_excl_scan<kNT>(v ? 1ULL : 0ULL, s_scan, &tot);
+                unsigned tot;
+                const unsigned ex = block_excl_count<kNT>(v ? 1u : 0u, s_scan, &tot);
                 if (v) {
                     const int r = static_cast<int>(carry + ex);
                     S.rt[r] = i;
@@ -269,8 +286,8 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
             for (int i0 = 0; i0 < W && static_cast<long long>(fcarry) < q; i0 += kNT) {
                 const int i = i0 + tid;
                 const bool fr = i < W && !S.act[i];
-                unsigned long long tot;
-                const unsigned long long ex = block_excl_scan<kNT>(fr ? 1ULL : 0ULL, s_scan, &tot);
+                unsigned tot;
+                const unsigned ex = block_excl_count<kNT>(fr ? 1u : 0u, s_scan, &tot);
                 const long long r = static_cast<long long>(fcarry + ex);
                 if (fr && r < q) {
                     S.act[i] = 1;
@@ -278,6 +295,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     S.tr[i] = S.rt[r];
                     S.sd[i] = S.rs[r];
                     S.pr[i] = S.rp[r];
+                    if (kKeyed) S.key[i] = prio_key(S.rs[r], S.rp[r]);
                     S.q[i] = S.rq[r];
                     S.pl[i] = t;
                     S.nl[r] = static_cast<unsigned short>(i);
@@ -295,7 +313,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 for (int j = tid; j < spawned; j += kNT) {
                     const unsigned short x = S.nl[j];
                     int rk = 0;
-                    for (int y = 0; y < spawned; ++y) rk += before(S, S.nl[y], x);
+                    for (int y = 0; y < spawned; ++y) rk += before<kKeyed>(S, S.nl[y], x);
                     S.nsr[rk] = x;
                 }
                 __syncthreads();
@@ -304,7 +322,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     int lo = 0, hi = spawned;  // new orders before a
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (before(S, S.nsr[mid], a))
+                        if (before<kKeyed>(S, S.nsr[mid], a))
                             lo = mid + 1;
                         else
                             hi = mid;
@@ -316,7 +334,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     int lo = 0, hi = n;  // resting orders before b
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (before(S, L[mid], b))
+                        if (before<kKeyed>(S, L[mid], b))
                             lo = mid + 1;
                         else
                             hi = mid;
@@ -462,11 +480,10 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     }
                     buy = alive && S.sd[s] == 0;
                 }
-                unsigned long long tot;
-                const unsigned long long ex = block_excl_scan<kNT>(
-                    (alive ? (1ULL << 32) : 0ULL) | (buy ? 1ULL : 0ULL), s_scan, &tot);
-                if (alive) L2[(carry >> 32) + (ex >> 32)] = s;
-                carry += tot;
+                unsigned tot;  // packed (alive << 16 | alive buy): at most kNT per field
+                const unsigned ex = block_excl_count<kNT>((alive ? (1u << 16) : 0u) | (buy ? 1u : 0u), s_scan, &tot);
+                if (alive) L2[(carry >> 32) + (ex >> 16)] = s;
+                carry += (static_cast<unsigned long long>(tot >> 16) << 32) | (tot & 0xFFFFu);
                 __syncthreads();
             }
             n = static_cast<int>(carry >> 32);
@@ -570,9 +587,9 @@ int check_cfg(const abmx_finance_config& c) {
     return ABMX_OK;
 }
 
-size_t fin_smem(const abmx_finance_config& c, int window, int sort_n) {
+size_t fin_smem(const abmx_finance_config& c, int window, int sort_n, bool keyed) {
     const size_t cap = static_cast<size_t>(window), T = static_cast<size_t>(c.traders);
-    return 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 4 * T + 2 * cap + T + 64;
+    return (keyed ? 8 * cap : 0) + 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 4 * T + 2 * cap + T + 64;
 }
 
 }  // namespace
@@ -598,12 +615,16 @@ struct abmx_finance {
     bool windowed = true;
     long long last_t = LLONG_MIN;
     int* d_err = nullptr;
-    int set_window(bool use) {
+    bool keyed_ok = false;  // the windowed layout plus the priority keys fits in shared memory
+    static int pow2_at_least(int n) {
+        int q = 1;
+        while (q < n) q <<= 1;
+        return q;
+    }
+    void set_window(bool use, bool keyed) {
         P.W = use ? window : P.cap;
-        P.sort_n = 1;
-        while (P.sort_n < P.W) P.sort_n <<= 1;
-        smem = fin_smem(cfg, P.W, P.sort_n);
-        return ABMX_OK;
+        P.sort_n = pow2_at_least(P.W);
+        smem = fin_smem(cfg, P.W, P.sort_n, keyed);
     }
     int check_err() {  // after a stream sync
         int e = 0;
@@ -682,15 +703,24 @@ struct abmx_finance {
         CKF(cudaMemset(d_err, 0, 8));
         P.seeds = sd;
         CKF(cudaMemcpy(sd, seeds, static_cast<size_t>(M) * 8, cudaMemcpyHostToDevice));
-        set_window(false);  // the whole capacity must fit: the window can be dropped at any time
+        set_window(false, false);  // the whole capacity must fit: the window can be dropped at any time
         if (smem > 226 * 1024) {  // sm_100: 227 KB of dynamic shared memory per CTA (minus static)
             abmx_internal::set_error("finance: book_capacity / traders too large for one shared-memory book");
             return ABMX_E_CAPACITY;
         }
-        CKF(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_fin<kNTLarge>),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        CKF(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_fin<kNTSmall>),
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        {
+            const void* fns[4] = {reinterpret_cast<const void*>(k_fin<kNTLarge, false>),
+                                  reinterpret_cast<const void*>(k_fin<kNTSmall, false>),
+                                  reinterpret_cast<const void*>(k_fin<kNTLarge, true>),
+                                  reinterpret_cast<const void*>(k_fin<kNTSmall, true>)};
+            const size_t ks = fin_smem(cfg, window, pow2_at_least(window), true);
+            // prices stay positive and never NaN (so their bit patterns order them) when the
+            // placement factor 1 + eps stays positive and the initial price is a number
+            keyed_ok = ks <= 226 * 1024 && c.delta < 1.0 && !std::isnan(c.init_price);
+            const int lim = static_cast<int>(keyed_ok && ks > smem ? ks : smem);
+            for (const void* f : fns)
+                CKF(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+        }
         (void)cudaGetLastError();
         k_fin_init<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(P, quantize_host(c.init_price));
         abmx_internal::count_launch();
@@ -720,13 +750,20 @@ struct abmx_finance {
             if (t0 <= last_t) windowed = false;
             last_t = t0 + steps - 1;
         }
-        set_window(windowed && !match_only);
+        const bool keyed = windowed && !match_only && keyed_ok;
+        set_window(windowed && !match_only, keyed);
         (void)cudaGetLastError();
         const unsigned grid = match_only ? 1u : static_cast<unsigned>(M * P.K);
-        if (P.W <= kSmallWindow)
-            k_fin<kNTSmall><<<grid, kNTSmall, smem, stream>>>(P);
-        else
-            k_fin<kNTLarge><<<grid, kNTLarge, smem, stream>>>(P);
+        if (P.W <= kSmallWindow) {
+            if (keyed)
+                k_fin<kNTSmall, true><<<grid, kNTSmall, smem, stream>>>(P);
+            else
+                k_fin<kNTSmall, false><<<grid, kNTSmall, smem, stream>>>(P);
+        } else if (keyed) {
+            k_fin<kNTLarge, true><<<grid, kNTLarge, smem, stream>>>(P);
+        } else {
+            k_fin<kNTLarge, false><<<grid, kNTLarge, smem, stream>>>(P);
+        }
         abmx_internal::count_launch();
         CKF(cudaGetLastError());
         last_steps = steps;

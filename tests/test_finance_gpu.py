@@ -180,6 +180,8 @@ def test_long_finance_run(F, oracle):
     (dict(traders=3, books=1, book_capacity=64, p_order=1.0, max_order_age=0), list(range(1, 30))),
     # a window covering the whole capacity
     (dict(traders=40, books=1, book_capacity=100, p_order=0.8, max_order_age=10), list(range(1, 40))),
+    # delta >= 1: windowed, but without the packed (side, price) priority keys
+    (dict(traders=12, books=2, book_capacity=400, p_order=0.9, max_order_age=5, delta=1.5), list(range(1, 30))),
 ])
 def test_order_window_transitions(F, oracle, kw, ts):
     """The shared-memory order window (finance.cu, abmx_finance::window): per-call steps with
