@@ -246,11 +246,28 @@ def finance_section(args, rank, world, allreduce, dist):
            "value": slots * FIN_STEPS / (ms / 1e3), "unit": UNIT, "device_ms": ms,
            "timing": "median of 3 device-timed run_batch launches after 2 full-size warm-ups", "markets_gathered": gathered,
            "market_steps_per_s": MARKETS * FIN_STEPS / (ms / 1e3)}
+    # SURVEY §8d C5, the alternative reading: ONE market of 1024 books (one CTA per book; the
+    # books share the traders, whose cash the books fold in with exact dyadic atomics). Not
+    # sharded: every rank runs its own copy.
+    one = F.FinanceConfig(books=MARKETS)
+    F.run_batch(one, MASTER_SEED, 1, FIN_STEPS)
+    one_ms = statistics.median([F.run_batch(one, MASTER_SEED, 1, FIN_STEPS)[1] for _ in range(3)])
+    out["one_market"] = {"workload": f"C5 alternative: 1 market x {MARKETS} books (1000 capacity, 10 traders), "
+                                     f"{FIN_STEPS} steps",
+                         "value": MARKETS * one.book_capacity * FIN_STEPS / (one_ms / 1e3), "unit": UNIT,
+                         "device_ms": one_ms}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle
         if os.path.exists(pyoracle.REF_SO):
             ref = pyoracle.Reference()
+            ns1 = 20  # a single market steps its books on one thread (finance.cpp:203-247)
+            _, wall1 = ref.fin_run_batch(MASTER_SEED, 1, ns1, threads=1, books=MARKETS)
+            out["one_market"]["cpu_baseline"] = {
+                "value": MARKETS * one.book_capacity * ns1 / (wall1 / 1e3), "unit": UNIT, "cores": 1,
+                "kind": "reference",
+                "sample": f"reference FinanceModel, 1 market x {MARKETS} books x {ns1} steps, 1 thread "
+                          f"({wall1 / 1e3:.2f} s)"}
             threads = os.cpu_count() or 1
             nm, ns = MARKETS, FIN_STEPS  # the full C5 workload (~1 s on the host)
             _, wall = ref.fin_run_batch(MASTER_SEED, nm, ns, threads=threads)

@@ -156,7 +156,9 @@ def test_reference_unit_cases(abmx, F):
 @pytest.mark.parametrize("kw,K,T", [(dict(), 96, 100), (dict(traders=200, books=2, book_capacity=300,
                                                                p_order=0.9), 32, 60),
                                     (dict(traders=1000, books=1, book_capacity=4096, p_order=0.7,
-                                          max_order_age=40), 4, 50)])
+                                          max_order_age=40), 4, 50),
+                                    # the C5 alternative reading: one market of many books
+                                    (dict(books=256), 1, 60)])
 def test_run_batch_vs_oracle(F, oracle, kw, K, T):
     """C5-shaped ensembles (default FinanceConfig) and heavy books against the C restatement."""
     rows, _ = F.run_batch(F.FinanceConfig(**kw), 7, K, T)
