@@ -35,3 +35,21 @@ for name in ("step+metrics", "step only", "metrics only", "run(K) async", "step+
         m.sync()
     dt = (time.perf_counter() - a) / K * 1e6
     print(f"{name:14s} {dt:8.1f} us/step")
+
+# host-side call costs alone (no waiting): step() returns after the graph launch
+hs = []
+for _ in range(K):
+    a = time.perf_counter()
+    m.step(t)
+    hs.append(time.perf_counter() - a)
+    t += 1
+    m.collect_metrics()
+print(f"{'step() call':14s} {np.median(hs) * 1e6:8.1f} us (host, median)")
+ws = []
+for _ in range(K):
+    m.step(t)
+    t += 1
+    a = time.perf_counter()
+    m.collect_metrics()
+    ws.append(time.perf_counter() - a)
+print(f"{'metrics wait':14s} {np.median(ws) * 1e6:8.1f} us (host, median)")
