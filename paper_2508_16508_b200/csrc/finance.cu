@@ -115,17 +115,19 @@ __device__ __forceinline__ unsigned long long prio_key(uint8_t side, double pric
 }
 
 // sort order: buys before sells; buys by price desc, sells by price asc; then placed, id, slot.
-// kKeyed: every order was placed by this kernel, so (side, price) is the packed key.
+// kKeyed: every order was placed by this kernel (launches with strictly increasing t), so
+// (side, price) is the packed key, and ids -- unique, handed out in placement order -- order
+// (placed, id) on their own.
 template <bool kKeyed>
 __device__ __forceinline__ bool before(const Smem& S, unsigned short a, unsigned short b) {
     if (b == kPad) return a != kPad;
     if (a == kPad) return false;
     if constexpr (kKeyed) {
-        if (S.key[a] != S.key[b]) return S.key[a] < S.key[b];
-    } else {
-        if (S.sd[a] != S.sd[b]) return S.sd[a] < S.sd[b];
-        if (S.pr[a] != S.pr[b]) return S.sd[a] == 0 ? S.pr[a] > S.pr[b] : S.pr[a] < S.pr[b];
+        const unsigned long long ka = S.key[a], kb = S.key[b];
+        return ka != kb ? ka < kb : S.id[a] < S.id[b];
     }
+    if (S.sd[a] != S.sd[b]) return S.sd[a] < S.sd[b];
+    if (S.pr[a] != S.pr[b]) return S.sd[a] == 0 ? S.pr[a] > S.pr[b] : S.pr[a] < S.pr[b];
     if (S.pl[a] != S.pl[b]) return S.pl[a] < S.pl[b];
     if (S.id[a] != S.id[b]) return S.id[a] < S.id[b];
     return a < b;
