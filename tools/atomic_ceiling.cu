@@ -30,7 +30,12 @@ __global__ void __launch_bounds__(kT, 4) k_pattern(uint4* cw, int* out, unsigned
         act[k] = (h & 1023) < live_per_1024 && (sheep || (h >> 10 & 15) == 0);
         c[k] = static_cast<unsigned>((h >> 20) % kCells);
     }
-    if (mode == 0) {
+    if (mode == 2) {  // L2 prefetch of every target line first, then the same atomics
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (act[k]) asm volatile("prefetch.global.L2 [%0];" :: "l"(&cw[c[k]]));
+    }
+    if (mode == 0 || mode == 2) {
 #pragma unroll
         for (int k = 0; k < kS; ++k)
             if (act[k]) old[k] = atomicExch(&w[4 * c[k] + (sheep ? 0 : 1)], salt + k);
@@ -74,8 +79,8 @@ int main() {
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     const unsigned live = 700;  // C2: ~70% of the sheep slots live (~370k of 524k), wolves ~4%
-    const char* names[2] = {"atomics (exch + max)", "random 16B loads"};
-    for (int mode = 0; mode < 2; ++mode)
+    const char* names[3] = {"atomics (exch + max)", "random 16B loads", "prefetch + atomics"};
+    for (int mode = 0; mode < 3; ++mode)
         for (int cold = 1; cold >= 0; --cold) {
             float best = 1e9f, sum = 0.f;
             const int reps = 20;
