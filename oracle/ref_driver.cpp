@@ -558,7 +558,7 @@ double ref_traffic_run_batch(int64_t length, int64_t period, double green_fracti
                              uint64_t master, int32_t replicas, int64_t steps, int threads,
                              double* metrics_out) {
     try {
-        const auto model = TrafficModel::descriptor(TrafficConfig{length, period, green_fraction});
+        const auto model = TrafficModel::descriptor(TrafficConfig{static_cast<abmx::Index>(length), period, green_fraction});
         const auto seeds = replica_seeds(RngState{master}, replicas);
         double wall = 0.0;
         const Trajectory tr = run_batch(model, seeds, steps, threads, &wall);
@@ -713,7 +713,7 @@ int64_t ref_run_csv(int kind, const ref_pred_config* pc, int64_t length, int64_t
                     int64_t cap) {
     try {
         ModelDescriptor model = kind == 0   ? PredationModel::descriptor(to_cfg(pc))
-                                : kind == 1 ? TrafficModel::descriptor(TrafficConfig{length, period, green_fraction})
+                                : kind == 1 ? TrafficModel::descriptor(TrafficConfig{static_cast<abmx::Index>(length), period, green_fraction})
                                             : FinanceModel::descriptor(fin_cfg(fc));
         const auto seeds = replica_seeds(RngState{master}, replicas);
         const Trajectory tr = run_batch(model, seeds, steps, 1, nullptr);
