@@ -474,7 +474,7 @@ void road_to(const Road& road, uint8_t* active, int64_t* ids, int64_t* ages, int
 
 void* ref_traffic_create(int64_t length, int64_t period, double green_fraction, uint64_t seed) {
     try {
-        TrafficConfig cfg{length, period, green_fraction};
+        TrafficConfig cfg{static_cast<abmx::Index>(length), period, green_fraction};
         return new TrafficModel(cfg, RngState{seed});
     } catch (const std::exception&) {
         return nullptr;
@@ -509,7 +509,7 @@ int ref_traffic_step_road(int64_t length, int64_t period, double green_fraction,
                           int64_t t, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* lane,
                           int64_t* cell, int32_t* occupancy, int64_t* next_id, int64_t* stats3) {
     try {
-        const TrafficConfig cfg{length, period, green_fraction};
+        const TrafficConfig cfg{static_cast<abmx::Index>(length), period, green_fraction};
         const SignalSchedule sched = SignalSchedule::from_config(cfg, RngState{seed});
         Road road = road_from(length, active, ids, ages, lane, cell, *next_id);
         RoadStepStats st;
