@@ -12,7 +12,10 @@
 //                                                                              predation.cpp:178-239
 //   3 eat/metabolise/starve/reproduce, one block-wide scan of four packed 16-bit counters
 //     (free/valid x sheep/wolves) and compaction of the valid rows              predation.cpp:241-250
-//   4 free slots pull their rank-matched row (spawn_agents), regrow, metrics   lifecycle.cpp:144-195
+//   4 free slots pull their rank-matched row (spawn_agents), metrics            lifecycle.cpp:144-195
+// Regrow (predation.cpp:252-258) is lazy, as in the large-model engine: a grazed cell stores the
+// step at whose end it is ready again (15 bits, renormalised every 8192 steps) and a ring of
+// 256 due counters keeps the ready count, so no step sweeps the lattice.
 #include <climits>
 #include <cstdint>
 #include <cstring>
@@ -30,6 +33,14 @@ namespace abmx_ens {
 constexpr int kT = 512;
 constexpr int kMaxSPT = 8;
 constexpr unsigned kEnd = 0xFFFFu;
+// grass word per cell (u16): a due step in [0, 0x7FFF], or one of
+constexpr unsigned short kReady = 0x8000u;  // ready (full_grass, or regrown)
+constexpr unsigned short kNever = 0x8001u;  // grazed with regrow_delay <= 0 (never regrows), or padding
+constexpr int kRenorm = 8192;               // due steps older than this are folded into kReady
+
+__device__ __forceinline__ bool grass_ready(unsigned short gv, long long t) {  // at a graze of step t
+    return gv == kReady || (gv < 0x8000u && ((static_cast<unsigned>(t) - 1u - gv) & 0x7FFFu) < 0x4000u);
+}
 
 __constant__ int e_dx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
 __constant__ int e_dy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
@@ -38,7 +49,7 @@ struct EnsParams {
     int W, H, C, Cpad;
     int N[2], n0[2], stride;
     double gain[2], metab, prob[2], frac;
-    unsigned delay_code;
+    int delay;  // regrow_delay (<= 0: a grazed cell never regrows)
     long long steps;
     const unsigned long long* seeds;
     long long* ids;     // [count][2][stride]
@@ -48,11 +59,11 @@ struct EnsParams {
     int* d_cell;
     int* d_age;
     double* d_energy;
-    uint8_t* d_g;       // [count][Cpad]
+    unsigned short* d_g;  // [count][Cpad] grass words
     long long* d_next;  // [count][2]
     int* d_num;         // [count][2]
     // dynamic shared memory carve-up (byte offsets)
-    int o_rowe[2], o_scan, o_cw, o_rowc[2], o_nxt[2], o_pool, o_flag[2], o_g, o_misc, smem;
+    int o_rowe[2], o_scan, o_cw, o_rowc[2], o_nxt[2], o_pool, o_flag[2], o_g, o_due, o_misc, smem;
 };
 
 __device__ __forceinline__ unsigned long long pack4(unsigned a, unsigned b, unsigned c, unsigned d) {
@@ -107,9 +118,9 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
                               reinterpret_cast<unsigned short*>(sm + P.o_nxt[1])};
     unsigned short* pool = reinterpret_cast<unsigned short*>(sm + P.o_pool);
     uint8_t* flag[2] = {sm + P.o_flag[0], sm + P.o_flag[1]};
-    uint8_t* g = sm + P.o_g;
-    unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [0] pool top, [1] grass
-    long long* red = reinterpret_cast<long long*>(sm + P.o_misc + 16);
+    unsigned short* g = reinterpret_cast<unsigned short*>(sm + P.o_g);
+    unsigned* due_cnt = reinterpret_cast<unsigned*>(sm + P.o_due);  // [256] cells due per step
+    unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [0] pool top, [1] grazed this step
 
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned long long seed = P.seeds[r];
@@ -141,11 +152,16 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             if (i < P.N[s]) ids[static_cast<size_t>(s) * P.stride + i] = act[s][k] ? i : 0;
         }
     }
-    for (int c = tid; c < P.Cpad; c += kT) g[c] = c < P.C ? 0 : 255;
+    for (int c = tid; c < P.Cpad; c += kT) g[c] = c < P.C ? kReady : kNever;
+    for (int k = tid; k < 256; k += kT) due_cnt[k] = 0;
     for (int c = tid; c < P.C; c += kT) cw[c] = 0xFFFFFFFFu;
     for (int i = tid; i < P.N[0]; i += kT) flag[0][i] = 0;
     for (int i = tid; i < P.N[1]; i += kT) flag[1][i] = 0;
-    if (tid == 0) misc[0] = 0;
+    if (tid == 0) {
+        misc[0] = 0;
+        misc[1] = 0;
+    }
+    long long n_grass = P.C;  // thread 0: ready cells (full_grass)
     long long next_id[2] = {P.n0[0], P.n0[1]};
     const unsigned long long mroot = split(seed, 3), rroot = split(seed, 4);
     __syncthreads();
@@ -197,8 +213,15 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             const int c = cell[0][k];
             unsigned m = static_cast<unsigned>(i);
             for (unsigned v = cw[c] & 0xFFFFu; v != kEnd; v = nxt[0][v]) m = v < m ? v : m;
-            if (m == static_cast<unsigned>(i) && g[c] == 0) {
-                g[c] = static_cast<uint8_t>(P.delay_code);
+            if (m == static_cast<unsigned>(i) && grass_ready(g[c], t)) {
+                if (P.delay >= 1) {  // ready again at the end of step t + delay - 1
+                    const unsigned due = static_cast<unsigned>(t + P.delay - 1) & 0x7FFFu;
+                    g[c] = static_cast<unsigned short>(due);
+                    atomicAdd(&due_cnt[due & 255u], 1u);
+                } else {
+                    g[c] = kNever;
+                }
+                atomicAdd(&misc[1], 1u);
                 E[0][k] = __dadd_rn(E[0][k], P.gain[0]);
             }
         }
@@ -321,34 +344,21 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             }
             next_id[s] += pairs[s];
         }
-        unsigned ready = 0;
-        unsigned* g32 = reinterpret_cast<unsigned*>(g);
-        for (int w = tid; w < P.Cpad / 4; w += kT) {
-            unsigned x = g32[w], o = 0;
-            bool ch = false;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                unsigned v = (x >> (8 * b)) & 0xFFu;
-                if (v >= 1 && v <= 254) {
-                    --v;
-                    ch = true;
-                }
-                ready += v == 0;
-                o |= v << (8 * b);
+        if (t % kRenorm == 0)  // due steps that have passed become kReady before they alias
+            for (int c = tid; c < P.C; c += kT) {
+                const unsigned short gv = g[c];
+                if (gv < 0x8000u && ((static_cast<unsigned>(t) - gv) & 0x7FFFu) < 0x4000u) g[c] = kReady;
             }
-            if (ch) g32[w] = o;
-        }
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) ready += __shfl_xor_sync(0xffffffffu, ready, d);
-        if ((tid & 31) == 0) red[tid >> 5] = ready;
-        __syncthreads();
         if (tid == 0) {
-            long long grass = 0;
-            for (int w = 0; w < kT / 32; ++w) grass += red[w];
+            // regrow of this step, lazily: - grazed + those due at its end (predation.cpp:252-258)
+            const unsigned slot = static_cast<unsigned>(t) & 255u;
+            n_grass += static_cast<long long>(due_cnt[slot]) - static_cast<long long>(misc[1]);
+            due_cnt[slot] = 0;
+            misc[1] = 0;
             double* row = P.metrics + (static_cast<size_t>(r) * P.steps + (t - 1)) * 4;
             row[0] = static_cast<double>(P.N[0] - F[0] + pairs[0]);
             row[1] = static_cast<double>(P.N[1] - F[1] + pairs[1]);
-            row[2] = static_cast<double>(grass);
+            row[2] = static_cast<double>(n_grass);
             row[3] = static_cast<double>((Q[0] - pairs[0]) + (Q[1] - pairs[1]));
             if (t == P.steps && P.d_num) {
                 P.d_num[2 * r] = P.N[0] - F[0] + pairs[0];
@@ -398,7 +408,8 @@ static int layout(const abmx_predation_config& cfg, EnsParams& P) {
     P.o_pool = take(2 * (N[0] + N[1] + 2), 16);
     P.o_flag[0] = take(N[0] > 0 ? N[0] : 1, 16);
     P.o_flag[1] = take(N[1] > 0 ? N[1] : 1, 16);
-    P.o_g = take(P.Cpad, 16);
+    P.o_g = take(2 * P.Cpad, 16);
+    P.o_due = take(4 * 256, 16);
     P.smem = (off + 15) / 16 * 16;
     return P.smem;
 }
@@ -460,7 +471,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     P.prob[0] = cfg.reproduce_prob_sheep;
     P.prob[1] = cfg.reproduce_prob_wolf;
     P.frac = cfg.reproduce_energy_frac;
-    P.delay_code = cfg.regrow_delay >= 1 ? static_cast<unsigned>(cfg.regrow_delay) : 255u;
+    P.delay = cfg.regrow_delay >= 1 ? static_cast<int>(cfg.regrow_delay) : 0;
     P.steps = steps;
     layout(cfg, P);
     const int spt = spt_for(cfg);
@@ -487,7 +498,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     P.metrics = static_cast<double*>(dmet);
     if (dump) {
         const size_t n = ids_n;
-        const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
+        const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * 2 * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
         CKE(cudaMallocAsync(&ddump, bytes, st));
         char* b = static_cast<char*>(ddump);
         P.d_energy = reinterpret_cast<double*>(b);
@@ -502,7 +513,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
         b += static_cast<size_t>(count) * 2 * 4;
         P.d_active = reinterpret_cast<uint8_t*>(b);
         b += n;
-        P.d_g = reinterpret_cast<uint8_t*>(b);
+        P.d_g = reinterpret_cast<unsigned short*>(b);
     }
     {
         void (*kern)(EnsParams) = nullptr;
@@ -523,7 +534,8 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     if (metrics_out) CKE(cudaMemcpyAsync(metrics_out, dmet, mbytes, cudaMemcpyDeviceToHost, st));
     if (dump) {
         const int r = dump->replica;
-        std::vector<uint8_t> a(P.stride), gg(P.Cpad);
+        std::vector<uint8_t> a(P.stride);
+        std::vector<unsigned short> gg(P.Cpad);
         std::vector<int> c(P.stride), ag(P.stride);
         long long nx[2];
         int nm[2];
@@ -546,15 +558,21 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
         }
         CKE(cudaMemcpyAsync(nx, P.d_next + 2 * r, 16, cudaMemcpyDeviceToHost, st));
         CKE(cudaMemcpyAsync(nm, P.d_num + 2 * r, 8, cudaMemcpyDeviceToHost, st));
-        CKE(cudaMemcpyAsync(gg.data(), P.d_g + static_cast<size_t>(r) * P.Cpad, P.Cpad, cudaMemcpyDeviceToHost, st));
+        CKE(cudaMemcpyAsync(gg.data(), P.d_g + static_cast<size_t>(r) * P.Cpad, 2 * static_cast<size_t>(P.Cpad),
+                            cudaMemcpyDeviceToHost, st));
         CKE(cudaStreamSynchronize(st));
         for (int s = 0; s < 2; ++s) {
             dump->next_id[s] = nx[s];
             dump->num_active[s] = nm[s];
         }
-        for (int cc = 0; cc < P.C; ++cc) {
-            dump->grass_ready[cc] = gg[cc] == 0;
-            dump->regrow[cc] = gg[cc] == 255 ? (cfg.regrow_delay <= 0 ? cfg.regrow_delay : 0) : gg[cc];
+        const unsigned T = static_cast<unsigned>(steps);
+        for (int cc = 0; cc < P.C; ++cc) {  // the reference's (grass_ready, regrow) after step T
+            const unsigned short gv = gg[cc];
+            const bool ready = gv == kReady || (gv < 0x8000u && ((T - gv) & 0x7FFFu) < 0x4000u);
+            dump->grass_ready[cc] = ready;
+            dump->regrow[cc] = ready ? 0
+                                     : (gv == kNever ? (cfg.regrow_delay <= 0 ? cfg.regrow_delay : 0)
+                                                     : static_cast<int64_t>((gv - T) & 0x7FFFu));
         }
     }
     CKE(cudaStreamSynchronize(st));

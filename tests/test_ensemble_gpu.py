@@ -65,3 +65,15 @@ def test_long_ensemble_run(abmx, oracle):
     clears over a long run)."""
     got, _ = abmx.run_batch(abmx.PredationConfig(**c1()), 19, 6, 700, path=1)
     assert np.array_equal(got, oracle.run_batch(c1(), 19, 6, 700))
+
+
+@pytest.mark.parametrize("delay,gain", [(1, 4.0), (30, 4.0), (60, 8.0), (120, 16.0)])
+def test_ensemble_lazy_regrow_past_renormalisation(abmx, oracle, delay, gain):
+    """8500 steps of small grids, past the grass-word renormalisation at step 8192
+    (ensemble.cu kRenorm): the per-step grass count and populations stay bit-exact."""
+    cfg = c1(width=24, height=24, n_sheep0=60, n_wolves0=6, sheep_capacity=512, wolf_capacity=64,
+             regrow_delay=delay, energy_gain_sheep=gain)
+    got, _ = abmx.run_batch(abmx.PredationConfig(**cfg), 23, 3, 8500, path=1)
+    want = oracle.run_batch(cfg, 23, 3, 8500)
+    assert want[:, -1, 0].sum() > 0  # sheep survive, so grazing continues to the end
+    assert np.array_equal(got, want)
