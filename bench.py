@@ -278,6 +278,93 @@ def finance_section(args, rank, world, allreduce, dist):
                           f"{threads} threads ({wall / 1e3:.2f} s)"}
     return out
 
+# ---------------------------------------------------------------------- agent sets (§8 a9/a12/a17)
+AGENT_CAP, AGENT_CYCLES, AGENT_CHURN = 524_288, 20, 14_000  # one C2 species, its per-step churn
+
+
+def agents_section(args, rank):
+    """The generic lifecycle on a C2-sized set: K x (remove_agents(kill), spawn_agents(rows,
+    valid, copy apply)) through the C-ABI on device buffers, L2 flushed before each cycle;
+    the reference's own remove_agents / spawn_agents (oracle/_ref) on the same inputs beside it,
+    and the two final sets compared bit for bit."""
+    import ctypes as C
+    import numpy as np
+    import torch
+    import paper_2508_16508_b200 as abmx
+    from paper_2508_16508_b200 import agents as A
+
+    rng = np.random.default_rng(11)
+    cap, K = AGENT_CAP, AGENT_CYCLES
+    act = (rng.random(cap) < 0.7).astype(np.uint8)
+    st = {"active": act, "ids": np.where(act, np.arange(cap), 0).astype(np.int64),
+          "ages": np.where(act, rng.integers(0, 100, cap), 0).astype(np.int64),
+          "types": np.zeros(cap, np.int64),
+          "e": np.where(act, rng.integers(0, 1000, cap), 0).astype(np.int64),
+          "w": np.where(act, rng.random(cap), 0.0), "f": act.copy()}
+    kills = np.zeros((K + 3, cap), np.uint8)
+    valids = np.zeros((K + 3, cap), np.uint8)
+    for k in range(K + 3):
+        kills[k, rng.choice(cap, AGENT_CHURN, replace=False)] = 1
+        valids[k, rng.choice(cap, AGENT_CHURN, replace=False)] = 1
+    rows = {"e": rng.integers(0, 1000, cap).astype(np.int64), "w": rng.random(cap),
+            "f": np.ones(cap, np.uint8)}
+    dk = torch.from_numpy(kills).cuda()
+    dv = torch.from_numpy(valids).cuda()
+    out = torch.zeros(1, dtype=torch.int64, device="cuda")
+    slots = torch.empty(cap, dtype=torch.int32, device="cuda")
+    rws = torch.empty(cap, dtype=torch.int32, device="cuda")
+    res = torch.zeros(2, dtype=torch.int64, device="cuda")
+
+    def make():
+        s = A.DeviceAgentSet.from_numpy(st, ["e", "w", "f"], next_id=cap)
+        arr, keep = s._rows({k: torch.from_numpy(v).cuda() for k, v in rows.items()}, cap)
+        return s, arr, keep
+
+    def cycle(s, arr, k):
+        stream = s._stream()
+        abmx._check(abmx.lib.abmx_agents_remove(C.byref(s._c), dk[k].data_ptr(), out.data_ptr(), stream))
+        abmx._check(abmx.lib.abmx_agents_spawn(C.byref(s._c), cap, dv[k].data_ptr(), arr, 0, 0,
+                                               slots.data_ptr(), rws.data_ptr(), res.data_ptr(), stream))
+
+    w, warr, wkeep = make()
+    for k in range(3):  # warm-up on a throw-away set
+        cycle(w, warr, K + k)
+    s, arr, keep = make()
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    flush2 = torch.ones(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        flush.fill_(k)
+        flush2.sum()
+        ev[k][0].record()
+        cycle(s, arr, k)
+        ev[k][1].record()
+    torch.cuda.synchronize()
+    ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    out_d = {"workload": f"lifecycle cycles on a {cap}-slot set (e:i64, w:f64, f:u8; 70% live): "
+                         f"remove_agents of {AGENT_CHURN} random slots + spawn_agents of {cap} rows with "
+                         f"{AGENT_CHURN} valid, copy apply; {K} cycles, L2 flushed before each",
+             "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms}
+    if rank == 0 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+        if os.path.exists(pyoracle.REF_SO):
+            ref = pyoracle.Reference()
+            ewf = pyoracle.new_ewf_state(st["active"], st["ids"], st["ages"], st["types"], st["e"],
+                                         st["w"], st["f"], cap)
+            fin, rms = ref.lifecycle_bench(ewf, kills[:K], rows, valids[:K])
+            got = s.to_numpy()
+            exact = all(np.array_equal(got[k], fin[k]) for k in ("active", "ids", "ages", "e", "f")) and \
+                np.array_equal(got["w"].view(np.uint64), fin["w"].view(np.uint64))
+            out_d["bit_exact_vs_reference"] = bool(exact)
+            out_d["cpu_baseline"] = {"value": cap / (rms / 1e3), "unit": "slot-cycles/s", "cores": 1,
+                                     "kind": "reference",
+                                     "sample": f"reference remove_agents + spawn_agents (oracle/_ref), the same "
+                                               f"{K} cycles, 1 thread ({rms:.2f} ms per cycle)"}
+    del flush, flush2
+    return out_d
+
+
 # ---------------------------------------------------------------------- our arm
 def kernel_bytes(cfg, births, deaths):
     """SURVEY §8d algorithmic bytes per step, B = 42*N_tot + 2*C + 8*(births+deaths),
@@ -439,6 +526,7 @@ def our_arm(args, rank, world, local_rank, dist):
 
     traffic = None if args.no_traffic else traffic_section(args, rank, world, allreduce, dist)
     finance = None if args.no_finance else finance_section(args, rank, world, allreduce, dist)
+    agents = None if args.no_agents else agents_section(args, rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -465,7 +553,7 @@ def our_arm(args, rank, world, local_rank, dist):
                 "live_agent_steps_per_s": live_all / (max_ms / 1e3),
                 "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
                 "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens, "traffic": traffic,
-                "finance": finance}
+                "finance": finance, "agents": agents}
         print(json.dumps(line))
 
 
@@ -480,6 +568,7 @@ def main():
     ap.add_argument("--no-ensemble", action="store_true")
     ap.add_argument("--no-traffic", action="store_true")
     ap.add_argument("--no-finance", action="store_true")
+    ap.add_argument("--no-agents", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rules: >= 3 warm-up steps

@@ -527,6 +527,9 @@ class Reference(_Base):
                                   C.POINTER(FinCfg), C.c_uint64, C.c_int32, C.c_int64, C.c_char_p,
                                   C.c_int64]
         L.ref_format_real.argtypes = [C.c_double, C.c_char_p]
+        L.ref_lifecycle_bench.restype = C.c_double
+        L.ref_lifecycle_bench.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, f64p, u8p, C.c_int64,
+                                          C.c_int32, u8p, i64p, f64p, u8p, u8p]
         L.ref_lifecycle.restype = C.c_int32
         L.ref_lifecycle.argtypes = [C.c_int32, u8p, i64p, i64p, i64p, i64p, f64p, u8p, i64p, C.c_int,
                                     i64p, i32p, u8p, C.c_int32, i64p, f64p, u8p, u8p, C.c_int,
@@ -622,6 +625,24 @@ class Reference(_Base):
                                           _p(a[3], u8p), _p(a[4], i64p), _p(a[5], i64p),
                                           _p(acc, u8p))
         return rc, acc
+
+    def lifecycle_bench(self, st, kills, rows, valids):
+        """K timed remove_agents + spawn_agents cycles (kills / valids: [K][cap] u8; rows: e/w/f
+        of `cap` rows). Returns (final ewf state, ms per cycle)."""
+        st = copy_ewf(st)
+        cap = st["active"].size
+        kills = np.ascontiguousarray(kills, np.uint8)
+        valids = np.ascontiguousarray(valids, np.uint8)
+        re, rw, rf = (np.ascontiguousarray(rows[k], dt) for k, dt in
+                      (("e", np.int64), ("w", np.float64), ("f", np.uint8)))
+        ms = self.lib.ref_lifecycle_bench(cap, _p(st["active"], u8p), _p(st["ids"], i64p),
+                                          _p(st["ages"], i64p), _p(st["e"], i64p), _p(st["w"], f64p),
+                                          _p(st["f"], u8p), int(st["next_id"]), kills.shape[0],
+                                          _p(kills, u8p), _p(re, i64p), _p(rw, f64p), _p(rf, u8p),
+                                          _p(valids, u8p))
+        if ms < 0:
+            raise ValueError("reference lifecycle failed")
+        return st, ms
 
     def lifecycle(self, st, kill, rows, valid, set_type=False, agent_type=0):
         """The reference's remove_agents then spawn_agents (same contract as Oracle.lifecycle)."""

@@ -434,6 +434,34 @@ int32_t ref_lifecycle(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages,
     return static_cast<int32_t>(o.spawned);
 }
 
+// Timed lifecycle cycles on the reference (bench.py's agents section): the set is built once,
+// the K spawn batches up front; then K x (remove_agents(kill_k), spawn_agents(batch_k, copy
+// apply)) chained by value as the reference's callers do. Returns wall ms per cycle; the final
+// set is exported in place.
+double ref_lifecycle_bench(int32_t cap, uint8_t* active, int64_t* ids, int64_t* ages, int64_t* e,
+                           double* w, uint8_t* f, int64_t next_id, int32_t K, const uint8_t* kills,
+                           const int64_t* re, const double* rw, const uint8_t* rf, const uint8_t* valids) {
+    try {
+        AgentSet set = make_ewf_set(cap, active, ids, ages, e, w, f);
+        set.set_next_id(next_id);
+        std::vector<UpdateBatch> batches;
+        batches.reserve(static_cast<size_t>(K));
+        for (int32_t k = 0; k < K; ++k)
+            batches.push_back(make_ewf_batch(cap, re, rw, rf, valids + static_cast<size_t>(k) * cap));
+        const auto a = std::chrono::steady_clock::now();
+        for (int32_t k = 0; k < K; ++k) {
+            AgentSet mid = remove_agents(set, std::span<const uint8_t>(kills + static_cast<size_t>(k) * cap,
+                                                                       static_cast<size_t>(cap)));
+            SpawnOutcome o = spawn_agents(mid, batches[static_cast<size_t>(k)], ewf_copy());
+            set = std::move(o.set);
+        }
+        const auto b = std::chrono::steady_clock::now();
+        export_ewf(set, active, ids, ages, e, w, f);
+        return std::chrono::duration<double, std::milli>(b - a).count() / (K > 0 ? K : 1);
+    } catch (const std::exception&) {
+        return -1.0;
+    }
+}
 
 // ---------------------------------------------------------------- traffic (traffic.hpp)
 // A road is passed as flat arrays over capacity 3*length: active, ids, ages, lane, cell,

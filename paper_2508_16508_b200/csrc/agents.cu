@@ -15,6 +15,7 @@
 // decoupled lookback, then a gather/scatter over the selected pairs only. Counts stay in
 // device memory, so a whole remove -> spawn cycle is stream-ordered with no host round trip.
 #include <cmath>
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <string>
@@ -127,11 +128,46 @@ struct Life {  // lifecycle fields of a set (agent_set.hpp:15-77)
     int recycle;
 };
 
+// The last CTA of a kernel to pass here returns true (all others' writes visible). `done` is a
+// zeroed word of the call's scan workspace; null: not the call's last kernel.
+__device__ __forceinline__ bool last_cta(unsigned* done) {
+    __shared__ unsigned s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(done, 1u) == gridDim.x - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_last) __threadfence();
+    return s_last != 0;
+}
+
+// Counters after a spawn (lifecycle.cpp:186-194); out = {spawned, dropped}.
+__device__ __forceinline__ void spawn_commit(const long long* p, const long long* q, const Life& L, long long* out) {
+    const long long r = min(*p, *q);
+    const long long top = L.recycle ? L.counters[2] : 0;
+    const long long used = min(top, r);
+    L.counters[0] += r;
+    L.counters[1] += r - used;
+    if (L.recycle) L.counters[2] = top - used;
+    if (out) {
+        out[0] = r;
+        out[1] = *q - r;
+    }
+}
+__device__ __forceinline__ void remove_commit(const long long* count, const Life& L, long long* out) {
+    const long long nk = *count;
+    L.counters[0] -= nk;
+    if (L.recycle) L.counters[2] += nk;
+    if (out) *out = nk;
+}
+
 // Pair k (k < min(*p, *q)): slot = slots[k] <- row = rows[k]. With `spawn` the slot also
 // becomes a fresh agent (lifecycle.cpp:170-185): active, id (recycled LIFO first), age 0, type.
 __global__ void __launch_bounds__(kT) k_pair_apply(const int32_t* __restrict__ slots, const int32_t* __restrict__ rows,
                                                    const long long* p, const long long* q, Cols C, int spawn,
-                                                   Life L, int set_type, long long agent_type) {
+                                                   Life L, int set_type, long long agent_type, unsigned* done,
+                                                   long long* out) {
     const long long r = min(*p, *q);
     long long top = 0, nid = 0;
     if (spawn) {
@@ -150,20 +186,18 @@ __global__ void __launch_bounds__(kT) k_pair_apply(const int32_t* __restrict__ s
             if (set_type) L.types[slot] = agent_type;
         }
     }
+    if (done && last_cta(done) && threadIdx.x == 0) {  // the call's last kernel: commit
+        if (spawn)
+            spawn_commit(p, q, L, out);
+        else if (out) {
+            out[0] = r;
+            out[1] = *q;
+        }
+    }
 }
 
-// Counters after a spawn (lifecycle.cpp:186-194); out = {spawned, dropped}.
 __global__ void k_spawn_commit(const long long* p, const long long* q, Life L, long long* out) {
-    const long long r = min(*p, *q);
-    const long long top = L.recycle ? L.counters[2] : 0;
-    const long long used = min(top, r);
-    L.counters[0] += r;
-    L.counters[1] += r - used;
-    if (L.recycle) L.counters[2] = top - used;
-    if (out) {
-        out[0] = r;
-        out[1] = *q - r;
-    }
+    spawn_commit(p, q, L, out);
 }
 
 // {pairs, valid rows} of a set_agents_rm / _sci call
@@ -176,7 +210,7 @@ __global__ void k_pair_result(const long long* p, const long long* q, long long*
 // remove_agents: killed slot k of the slot-ordered kill list is reset; its id is pushed on
 // the retired stack at top + k (the reference pushes in ascending slot order).
 __global__ void __launch_bounds__(kT) k_remove_apply(const int32_t* __restrict__ list, const long long* count,
-                                                     Cols C, Life L) {
+                                                     Cols C, Life L, unsigned* done, Life LC, long long* out) {
     const long long nk = *count;
     const long long top = L.recycle ? L.counters[2] : 0;
     for (long long k = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; k < nk;
@@ -188,13 +222,9 @@ __global__ void __launch_bounds__(kT) k_remove_apply(const int32_t* __restrict__
         L.ages[slot] = 0;
         for (int c = 0; c < C.n; ++c) zero_elem(C.dst[c], slot, C.sz[c]);
     }
+    if (done && last_cta(done) && threadIdx.x == 0) remove_commit(count, LC, out);  // the call's last kernel
 }
-__global__ void k_remove_commit(const long long* count, Life L, long long* out) {
-    const long long nk = *count;
-    L.counters[0] -= nk;
-    if (L.recycle) L.counters[2] += nk;
-    if (out) *out = nk;
-}
+__global__ void k_remove_commit(const long long* count, Life L, long long* out) { remove_commit(count, L, out); }
 
 // set_agents_mask with per-slot source values: dst[c][i] <- src[c][i] where mask[i].
 __global__ void __launch_bounds__(kT) k_mask_apply(const uint8_t* __restrict__ mask, size_t n, Cols C) {
@@ -389,10 +419,27 @@ Life life_of(const abmx_agent_set* s) {
 }
 
 // Scratch for one call, stream-ordered (freed with cudaFreeAsync after the last use).
+// Scratch comes from the stream-ordered pool. Its default release threshold (0) hands freed
+// memory back to the driver at every synchronisation, so the next call would map it afresh;
+// keep it cached instead (once per device).
+void keep_async_pool() {
+    static std::atomic<unsigned long long> done{0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
+    if (done.load() >> dev & 1ULL) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        unsigned long long thr = ~0ULL;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    (void)cudaGetLastError();
+    done.fetch_or(1ULL << dev);
+}
+
 struct Scratch {
     cudaStream_t st;
     std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t s) : st(s) {}
+    explicit Scratch(cudaStream_t s) : st(s) { keep_async_pool(); }
     ~Scratch() {
         for (void* p : ptrs) cudaFreeAsync(p, st);
     }
@@ -406,8 +453,9 @@ struct Scratch {
 // slot-ordered selection list + device count
 template <int kMode>
 int select_list(const uint8_t* mask, const uint8_t* active, size_t n, int32_t* list, long long* count,
-                Scratch& sc) {
+                Scratch& sc, unsigned** done = nullptr) {
     cudaStream_t st = sc.st;
+    if (done) *done = nullptr;
     if (n == 0) {
         CKA(cudaMemsetAsync(count, 0, sizeof(long long), st));
         return ABMX_OK;
@@ -419,6 +467,7 @@ int select_list(const uint8_t* mask, const uint8_t* active, size_t n, int32_t* l
     CKA(cudaMemsetAsync(ws, 0, wsb, st));
     k_select<kMode><<<static_cast<unsigned>(tiles), kT, 0, st>>>(mask, active, n, list, count,
                                                                  static_cast<ScanWs*>(ws));
+    if (done) *done = &static_cast<ScanWs*>(ws)->pad;  // zeroed and unused by k_select
     abmx_internal::count_launch();
     CKA(cudaGetLastError());
     return ABMX_OK;
@@ -470,8 +519,10 @@ int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int3
     else
         rc = select_list<kSelMask>(d_target, nullptr, n, slots, cnt, sc);
     if (rc) return rc;
-    rc = select_list<kSelMask>(d_valid, nullptr, static_cast<size_t>(m), rws, cnt + 1, sc);
+    unsigned* done = nullptr;  // the pad word of the second scan's workspace: a zeroed counter
+    rc = select_list<kSelMask>(d_valid, nullptr, static_cast<size_t>(m), rws, cnt + 1, sc, &done);
     if (rc) return rc;
+    bool committed = false;
     const Life L = life_of(s);
     const size_t pairs_max = n < static_cast<size_t>(m) ? n : static_cast<size_t>(m);
     rc = for_col_chunks(s->n_state, [&](int c0, int cn) {
@@ -486,12 +537,17 @@ int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int3
         }
         const int sp = spawn && c0 == 0;  // lifecycle fields once
         if (C.n == 0 && !sp) return static_cast<int>(ABMX_OK);
-        k_pair_apply<<<grid_for(pairs_max), kT, 0, st>>>(slots, rws, cnt, cnt + 1, C, sp, L, set_type, agent_type);
+        const bool last = c0 + kMaxCols >= s->n_state && done;  // fold the commit into it
+        k_pair_apply<<<grid_for(pairs_max), kT, 0, st>>>(slots, rws, cnt, cnt + 1, C, sp, L, set_type, agent_type,
+                                                          last ? done : nullptr,
+                                                          last ? reinterpret_cast<long long*>(d_out) : nullptr);
+        committed = committed || last;
         abmx_internal::count_launch();
         CKA(cudaGetLastError());
         return static_cast<int>(ABMX_OK);
     });
     if (rc) return rc;
+    if (committed) return ABMX_OK;
     if (spawn) {
         k_spawn_commit<<<1, 1, 0, st>>>(cnt, cnt + 1, L, reinterpret_cast<long long*>(d_out));
         abmx_internal::count_launch();
@@ -524,9 +580,11 @@ int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* 
     long long* cnt = nullptr;
     CKA(sc.get(reinterpret_cast<void**>(&list), n * 4));
     CKA(sc.get(reinterpret_cast<void**>(&cnt), sizeof(long long)));
-    rc = select_list<kSelKill>(d_kill, s->active, n, list, cnt, sc);
+    unsigned* done = nullptr;
+    rc = select_list<kSelKill>(d_kill, s->active, n, list, cnt, sc, &done);
     if (rc) return rc;
     const Life L = life_of(s);
+    bool committed = false;
     // lifecycle fields with the first chunk; the retired push reads ids before they are zeroed
     rc = for_col_chunks(s->n_state, [&](int c0, int cn) {
         Cols C{};
@@ -536,19 +594,24 @@ int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* 
             C.src[c] = nullptr;
             C.sz[c] = s->state[c0 + c].elem_size;
         }
+        const bool last = (c0 + kMaxCols >= s->n_state) && done;  // fold the commit into it
+        unsigned* dn = last ? done : nullptr;
+        long long* out = last ? reinterpret_cast<long long*>(d_killed) : nullptr;
         if (c0 == 0) {
-            k_remove_apply<<<grid_for(n), kT, 0, st>>>(list, cnt, C, L);
+            k_remove_apply<<<grid_for(n), kT, 0, st>>>(list, cnt, C, L, dn, L, out);
         } else {  // further chunks: state columns only (lifecycle fields already reset)
             Life none = L;
             none.recycle = 0;
             // the lifecycle writes are idempotent, but active was already cleared: reuse the list
-            k_remove_apply<<<grid_for(n), kT, 0, st>>>(list, cnt, C, none);
+            k_remove_apply<<<grid_for(n), kT, 0, st>>>(list, cnt, C, none, dn, L, out);
         }
+        committed = committed || last;
         abmx_internal::count_launch();
         CKA(cudaGetLastError());
         return static_cast<int>(ABMX_OK);
     });
     if (rc) return rc;
+    if (committed) return ABMX_OK;
     k_remove_commit<<<1, 1, 0, st>>>(cnt, L, reinterpret_cast<long long*>(d_killed));
     abmx_internal::count_launch();
     CKA(cudaGetLastError());
