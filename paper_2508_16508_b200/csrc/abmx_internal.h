@@ -12,6 +12,14 @@
 namespace abmx_internal {
 
 int num_sms();
+// cudaMallocAsync from the device's default pool, kept cached: the pool's default release
+// threshold (0) hands freed memory back at every synchronisation, so the next call would map
+// it afresh (177 -> 52 us per agent-set lifecycle cycle)
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s);
+template <class T>
+cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t s) {
+    return malloc_async(reinterpret_cast<void**>(p), bytes, s);
+}
 void count_launch(int k = 1);          // launches of our own kernels (gpu_launches)
 unsigned long long launches();
 

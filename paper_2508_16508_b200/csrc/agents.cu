@@ -419,32 +419,15 @@ Life life_of(const abmx_agent_set* s) {
 }
 
 // Scratch for one call, stream-ordered (freed with cudaFreeAsync after the last use).
-// Scratch comes from the stream-ordered pool. Its default release threshold (0) hands freed
-// memory back to the driver at every synchronisation, so the next call would map it afresh;
-// keep it cached instead (once per device).
-void keep_async_pool() {
-    static std::atomic<unsigned long long> done{0};
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return;
-    if (done.load() >> dev & 1ULL) return;
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        unsigned long long thr = ~0ULL;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-    (void)cudaGetLastError();
-    done.fetch_or(1ULL << dev);
-}
-
 struct Scratch {
     cudaStream_t st;
     std::vector<void*> ptrs;
-    explicit Scratch(cudaStream_t s) : st(s) { keep_async_pool(); }
+    explicit Scratch(cudaStream_t s) : st(s) {}
     ~Scratch() {
         for (void* p : ptrs) cudaFreeAsync(p, st);
     }
     cudaError_t get(void** p, size_t bytes) {
-        cudaError_t e = cudaMallocAsync(p, bytes ? bytes : 16, st);
+        cudaError_t e = abmx_internal::malloc_async(p, bytes ? bytes : 16, st);
         if (e == cudaSuccess) ptrs.push_back(*p);
         return e;
     }

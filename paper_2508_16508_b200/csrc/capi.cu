@@ -28,6 +28,20 @@ int num_sms() {
     }();
     return n;
 }
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
+    static std::atomic<unsigned long long> kept{0};  // devices whose pool is already set
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !(kept.load() >> dev & 1ULL)) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            unsigned long long thr = ~0ULL;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        (void)cudaGetLastError();
+        kept.fetch_or(1ULL << dev);
+    }
+    return cudaMallocAsync(p, bytes, s);
+}
 void count_launch(int k) { g_launches.fetch_add(static_cast<unsigned long long>(static_cast<long long>(k))); }
 unsigned long long launches() { return g_launches.load(); }
 void set_error(const std::string& msg) { t_error = msg; }

@@ -489,9 +489,9 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     CKE(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
     CKE(cudaEventCreate(&ea));
     CKE(cudaEventCreate(&eb));
-    CKE(cudaMallocAsync(&dseeds, sizeof(unsigned long long) * count, st));
-    CKE(cudaMallocAsync(&dids, ids_n * 8, st));
-    CKE(cudaMallocAsync(&dmet, mbytes, st));
+    CKE(abmx_internal::malloc_async(&dseeds, sizeof(unsigned long long) * count, st));
+    CKE(abmx_internal::malloc_async(&dids, ids_n * 8, st));
+    CKE(abmx_internal::malloc_async(&dmet, mbytes, st));
     CKE(cudaMemcpyAsync(dseeds, seeds, sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, st));
     P.seeds = static_cast<const unsigned long long*>(dseeds);
     P.ids = static_cast<long long*>(dids);
@@ -499,7 +499,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     if (dump) {
         const size_t n = ids_n;
         const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * 2 * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
-        CKE(cudaMallocAsync(&ddump, bytes, st));
+        CKE(abmx_internal::malloc_async(&ddump, bytes, st));
         char* b = static_cast<char*>(ddump);
         P.d_energy = reinterpret_cast<double*>(b);
         b += n * 8;

@@ -289,7 +289,7 @@ cudaError_t launch_rank_scan(const uint8_t* d_mask, int32_t* d_ranks, size_t n, 
     const size_t tiles = (n + kTile - 1) / kTile;
     const size_t ws_bytes = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
     void* ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
+    cudaError_t e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(ws, 0, ws_bytes, s);
     (void)cudaGetLastError();
@@ -319,7 +319,7 @@ cudaError_t launch_compact_indices(const uint8_t* d_mask, int32_t* d_out, size_t
     const size_t tiles = (n + kTile - 1) / kTile;
     const size_t ws_bytes = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
     void* ws = nullptr;
-    e = cudaMallocAsync(&ws, ws_bytes, s);
+    e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(ws, 0, ws_bytes, s);
     (void)cudaGetLastError();
@@ -340,7 +340,7 @@ cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_
     const size_t H = 1ULL << bits;
     const size_t ws_bytes = 256 + H * sizeof(int) + H * sizeof(unsigned long long);
     void* ws = nullptr;
-    cudaError_t e = cudaMallocAsync(&ws, ws_bytes, s);
+    cudaError_t e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
     auto* mws = static_cast<MatchWs*>(ws);
     int* vals = reinterpret_cast<int*>(static_cast<char*>(ws) + 256);

@@ -952,10 +952,10 @@ int resolve_host(int64_t length, const uint8_t* active, const int64_t* lane, con
         rc = ABMX_E_CUDA;
     };
     cudaError_t e = cudaSuccess;
-    if ((e = cudaMallocAsync(&d_act, N, s)) || (e = cudaMallocAsync(&d_acc, N, s)) ||
-        (e = cudaMallocAsync(&d_lane, N * 4, s)) || (e = cudaMallocAsync(&d_tg, N * 4, s)) ||
-        (e = cudaMallocAsync(&d_occ, N * 4, s)) || (e = cudaMallocAsync(&d_a, N * 4, s)) ||
-        (e = cudaMallocAsync(&d_b, N * 4, s)) || (e = cudaMallocAsync(&d_bid, N * 8, s))) {
+    if ((e = abmx_internal::malloc_async(&d_act, N, s)) || (e = abmx_internal::malloc_async(&d_acc, N, s)) ||
+        (e = abmx_internal::malloc_async(&d_lane, N * 4, s)) || (e = abmx_internal::malloc_async(&d_tg, N * 4, s)) ||
+        (e = abmx_internal::malloc_async(&d_occ, N * 4, s)) || (e = abmx_internal::malloc_async(&d_a, N * 4, s)) ||
+        (e = abmx_internal::malloc_async(&d_b, N * 4, s)) || (e = abmx_internal::malloc_async(&d_bid, N * 8, s))) {
         fail(e);
     } else {
         cudaMemcpyAsync(d_act, act.data(), N, cudaMemcpyHostToDevice, s);

@@ -289,9 +289,9 @@ int traffic_ensemble_run(const abmx_traffic_config& cfg, const uint64_t* seeds, 
     const size_t mb = static_cast<size_t>(count) * static_cast<size_t>(steps) * 32;
     int rc = ABMX_OK;
     cudaEvent_t a = nullptr, b = nullptr;
-    if ((e = cudaMallocAsync(&d_seeds, static_cast<size_t>(count) * 8, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&d_phase, static_cast<size_t>(count) * 8, s)) != cudaSuccess ||
-        (e = cudaMallocAsync(&d_metrics, mb, s)) != cudaSuccess ||
+    if ((e = abmx_internal::malloc_async(&d_seeds, static_cast<size_t>(count) * 8, s)) != cudaSuccess ||
+        (e = abmx_internal::malloc_async(&d_phase, static_cast<size_t>(count) * 8, s)) != cudaSuccess ||
+        (e = abmx_internal::malloc_async(&d_metrics, mb, s)) != cudaSuccess ||
         (e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))) !=
             cudaSuccess) {
         set_error(std::string("traffic ensemble: ") + cudaGetErrorString(e));
