@@ -85,7 +85,7 @@ __device__ __forceinline__ unsigned column_map(const Road& R, int L, int c, unsi
 }
 
 template <int kNT>
-__global__ void __launch_bounds__(kNT) k_traffic_ens(EnsP P) {
+__global__ void __launch_bounds__(kNT, 1536 / kNT) k_traffic_ens(EnsP P) {  // 24 roads of 64 threads per SM: C4 roads in one wave
     extern __shared__ unsigned char sm[];
     const int L = P.L, C = P.C;
     Road R;
@@ -148,9 +148,24 @@ __global__ void __launch_bounds__(kNT) k_traffic_ens(EnsP P) {
         // (b) acceptance: suffix composition of the column maps (thread 0 holds the last columns)
         const int c_hi = L - tid * nc;
         unsigned T = kIdentityFn;
-        for (int c = c_hi - 1; c >= c_hi - nc && c >= 0; --c) {
-            unsigned m3;
-            T = compose(column_map(R, L, c, m3), T);
+        // a thread's column maps, kept from the composition for the apply pass (nc <= kCache)
+        constexpr int kCache = 4;
+        unsigned fcache[kCache], mcache[kCache];
+        {
+            int j = 0;
+            for (int c = c_hi - 1; c >= c_hi - nc && c >= 0; --c, ++j) {
+                unsigned m3;
+                const unsigned f = column_map(R, L, c, m3);
+                if (nc <= kCache) {
+#pragma unroll
+                    for (int q = 0; q < kCache; ++q)
+                        if (q == j) {
+                            fcache[q] = f;
+                            mcache[q] = m3;
+                        }
+                }
+                T = compose(f, T);
+            }
         }
         unsigned I = T;
 #pragma unroll
@@ -164,9 +179,20 @@ __global__ void __launch_bounds__(kNT) k_traffic_ens(EnsP P) {
         for (int w = 0; w < warp; ++w) wex = compose(s_warp[w], wex);
         const unsigned up = __shfl_up_sync(0xffffffffu, I, 1);
         unsigned v = apply_fn(lane > 0 ? compose(up, wex) : wex, 0u);
-        for (int c = c_hi - 1; c >= c_hi - nc && c >= 0; --c) {
-            unsigned m3;
-            v = apply_fn(column_map(R, L, c, m3), v);
+        int j = 0;
+        for (int c = c_hi - 1; c >= c_hi - nc && c >= 0; --c, ++j) {
+            unsigned m3, f = 0;
+            if (nc <= kCache) {
+#pragma unroll
+                for (int q = 0; q < kCache; ++q)
+                    if (q == j) {
+                        f = fcache[q];
+                        m3 = mcache[q];
+                    }
+            } else {
+                f = column_map(R, L, c, m3);
+            }
+            v = apply_fn(f, v);
 #pragma unroll
             for (int l = 0; l < 3; ++l)
                 if (m3 & (1u << l)) R.acc[l * L + c] = static_cast<uint8_t>((v >> l) & 1u);
