@@ -41,6 +41,10 @@ namespace abmx_trf {
 // CTAs, long roads large ones so the decoupled lookback crosses few tiles).
 constexpr int kS = 4;
 constexpr int kCI = 4;  // columns per thread in k_accept: one int4 of occupants per lane
+#ifndef ABMX_TRF_NA_MAX
+#define ABMX_TRF_NA_MAX 1024
+#endif
+constexpr int kAcceptMaxNT = ABMX_TRF_NA_MAX;  // k_accept CTA size for long roads
 constexpr unsigned kSlotMask = (1u << 28) - 1;
 constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagPre = 2ULL << 62;
@@ -384,11 +388,18 @@ __global__ void k_spawn(TParams P) {
     const int lane = threadIdx.x;
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
     long long* cn = P.cnt + static_cast<size_t>(r) * 8;
+    // every load the spawn needs that does not depend on the draws, issued together: the seed,
+    // the three entrance cells, the first 32 tiles' free-slot info, the counters
+    const unsigned long long seed = P.seeds[r];
+    const int occ_in[3] = {P.occ[cb], P.occ[cb + P.Lp], P.occ[cb + 2 * static_cast<size_t>(P.Lp)]};
+    int4 ti0 = lane < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + lane] : make_int4(0, -1, -1, -1);
+    const long long nid = cn[1], exited = cn[5], c0 = cn[0], c2 = cn[2], c3 = cn[3];
+    const bool g = green_of(P, r);
     // rows (lane 0): k attempts, partial shuffle, free entry cells
     int rows[3] = {-1, -1, -1};
     int nvalid = 0;
     {
-        const unsigned long long key = split(split(P.seeds[r], 7), static_cast<unsigned long long>(P.t));
+        const unsigned long long key = split(split(seed, 7), static_cast<unsigned long long>(P.t));
         const int k = static_cast<int>(uniform_span(key, 0, 4));
         int lanes[3] = {0, 1, 2};
         for (int i = 0; i < (k < 2 ? k : 2); ++i) {
@@ -399,14 +410,15 @@ __global__ void k_spawn(TParams P) {
             lanes[j] = tmp;
         }
         for (int q = 0; q < (k < 3 ? k : 3); ++q)
-            if (P.occ[cb + lanes[q] * P.Lp] < 0) rows[nvalid++] = lanes[q];
+            if (occ_in[lanes[q]] < 0) rows[nvalid++] = lanes[q];
     }
     // the lowest nvalid free slots, tiles in order (warp-parallel over tile chunks)
     int slots[3] = {-1, -1, -1};
     int nf = 0;
     for (int t0 = 0; t0 < P.tiles && nf < nvalid; t0 += 32) {
         const int t = t0 + lane;
-        const int4 ti = t < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + t] : make_int4(0, -1, -1, -1);
+        const int4 ti = t0 == 0 ? ti0
+                                : (t < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + t] : make_int4(0, -1, -1, -1));
         unsigned m = __ballot_sync(0xffffffffu, ti.x > 0);
         while (m && nf < nvalid) {
             const int src = __ffs(m) - 1;
@@ -421,7 +433,6 @@ __global__ void k_spawn(TParams P) {
     }
     if (lane == 0) {
         const int spawned = nf < nvalid ? nf : nvalid;
-        const long long nid = cn[1];
         for (int q = 0; q < spawned; ++q) {
             const int s = slots[q];
             P.active[sb + s] = 1;
@@ -430,18 +441,18 @@ __global__ void k_spawn(TParams P) {
             P.ages[sb + s] = 0;
             P.occ[cb + rows[q] * P.Lp] = s;
         }
-        const long long exited = cn[5];
-        cn[0] += spawned - exited;
+        const long long n_cars = c0 + spawned - exited;
+        cn[0] = n_cars;
         cn[1] = nid + spawned;
-        cn[2] += spawned;
-        cn[3] += exited;
+        cn[2] = c2 + spawned;
+        cn[3] = c3 + exited;
         cn[4] = spawned;
-        cn[6] = green_of(P, r) ? 1 : 0;
+        cn[6] = g ? 1 : 0;
         double* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
-        row[0] = static_cast<double>(cn[0]);
+        row[0] = static_cast<double>(n_cars);
         row[1] = static_cast<double>(spawned);
         row[2] = static_cast<double>(exited);
-        row[3] = cn[6] ? 1.0 : 0.0;
+        row[3] = g ? 1.0 : 0.0;
         cn[5] = 0;  // exits of the next step accumulate from zero
     }
 }
@@ -572,7 +583,7 @@ struct abmx_traffic {
         while (nt < 256 && nt * kS < P.C) nt *= 2;
         // k_accept: the smallest CTA covering a road's columns, else 1024 threads (few tiles)
         na = 32;
-        while (na < 1024 && na * kCI < P.Lp) na *= 2;
+        while (na < kAcceptMaxNT && na * kCI < P.Lp) na *= 2;
         switch (nt) {
             case 32: fns[0] = reinterpret_cast<void*>(k_propose<32>); fns[2] = reinterpret_cast<void*>(k_apply<32>); break;
             case 64: fns[0] = reinterpret_cast<void*>(k_propose<64>); fns[2] = reinterpret_cast<void*>(k_apply<64>); break;
