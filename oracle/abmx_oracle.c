@@ -245,8 +245,20 @@ static void create_species(orc_species* s, int32_t cap, int32_t n0, int32_t W, i
 }
 
 /* predation.cpp:154-165 */
+/* predation.cpp:154-164: NULL where init_predation throws -- the initial counts
+ * (CapacityError), a negative capacity (lifecycle.cpp:55-58), or an empty draw range for any
+ * slot of a non-empty species (rng.cpp:30-36): x in [0, W), y in [0, H), energy in
+ * [1, 2*trunc(gain) + 1). */
 orc_pred* orc_pred_create(const orc_pred_config* cfg, uint64_t seed) {
     if (cfg->n_sheep0 > cfg->sheep_capacity || cfg->n_wolves0 > cfg->wolf_capacity) return NULL;
+    {
+        const int64_t cap[2] = {cfg->sheep_capacity, cfg->wolf_capacity};
+        const double gain[2] = {cfg->energy_gain_sheep, cfg->energy_gain_wolf};
+        for (int s = 0; s < 2; ++s) {
+            if (cap[s] < 0) return NULL;
+            if (cap[s] > 0 && (cfg->width < 1 || cfg->height < 1 || !(gain[s] >= 1.0))) return NULL;
+        }
+    }
     orc_pred* p = (orc_pred*)calloc(1, sizeof(orc_pred));
     p->cfg = *cfg;
     p->seed = seed;

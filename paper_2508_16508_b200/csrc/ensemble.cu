@@ -25,6 +25,7 @@
 #include "abmx_device.cuh"
 #include "abmx_internal.h"
 #include "ensemble.h"
+#include "predation_engine.h"
 
 using namespace abmx_dev;
 
@@ -445,11 +446,7 @@ bool smem_fits(const abmx_predation_config& cfg) {
 
 int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count, long long steps,
              double* metrics_out, double* kernel_ms, Dump* dump) {
-    if (cfg.n_sheep0 > cfg.sheep_capacity || cfg.n_wolves0 > cfg.wolf_capacity || cfg.n_sheep0 < 0 ||
-        cfg.n_wolves0 < 0) {
-        abmx_internal::set_error("initial counts exceed capacities");
-        return ABMX_E_CAPACITY;
-    }
+    if (const int rc = abmx_pred::check_create(cfg)) return rc;
     if (!smem_fits(cfg)) {
         abmx_internal::set_error("configuration does not fit the SMEM-resident ensemble kernel");
         return ABMX_E_DOMAIN;

@@ -966,6 +966,35 @@ int Engine::alloc(void** p, size_t bytes) {
     return ABMX_OK;
 }
 
+// init_predation's errors, in its order (predation.cpp:154-164): the initial counts, then per
+// species create_agents (lifecycle.cpp:53-85) -- a negative capacity, then the draws of
+// x in [0, W), y in [0, H) and energy in [1, 2*trunc(gain) + 1) for EVERY slot, which throw
+// DomainError on an empty range (rng.cpp:30-36) whenever the species has any slot.
+int check_create(const abmx_predation_config& c) {
+    if (c.n_sheep0 > c.sheep_capacity || c.n_wolves0 > c.wolf_capacity) {
+        abmx_internal::set_error("initial counts exceed capacities");  // predation.cpp:155-156
+        return ABMX_E_CAPACITY;
+    }
+    const long long cap[2] = {c.sheep_capacity, c.wolf_capacity}, n0[2] = {c.n_sheep0, c.n_wolves0};
+    const double gain[2] = {c.energy_gain_sheep, c.energy_gain_wolf};
+    for (int s = 0; s < 2; ++s) {
+        if (cap[s] < 0 || n0[s] < 0) {
+            abmx_internal::set_error("negative capacity");  // lifecycle.cpp:55-58
+            return ABMX_E_CAPACITY;
+        }
+        if (cap[s] == 0) continue;
+        if (c.width < 1 || c.height < 1 || !(gain[s] >= 1.0 && gain[s] < 9.2e18)) {
+            abmx_internal::set_error("uniform_int: empty range");  // 2*trunc(gain)+1 <= 1, or W/H <= 0
+            return ABMX_E_DOMAIN;
+        }
+    }
+    if (c.width < 1 || c.height < 1) {  // an engine limit (the reference builds an empty grid)
+        abmx_internal::set_error("width and height must be >= 1");
+        return ABMX_E_DOMAIN;
+    }
+    return ABMX_OK;
+}
+
 int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_) {
     cfg = c;
     R = R_;
@@ -973,18 +1002,7 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         abmx_internal::set_error("replicas must be >= 1");
         return ABMX_E_DOMAIN;
     }
-    if (c.width < 1 || c.height < 1) {
-        abmx_internal::set_error("width and height must be >= 1");
-        return ABMX_E_DOMAIN;
-    }
-    if (c.sheep_capacity < 0 || c.wolf_capacity < 0 || c.n_sheep0 < 0 || c.n_wolves0 < 0) {
-        abmx_internal::set_error("negative capacity");
-        return ABMX_E_CAPACITY;
-    }
-    if (c.n_sheep0 > c.sheep_capacity || c.n_wolves0 > c.wolf_capacity) {
-        abmx_internal::set_error("initial counts exceed capacities");  // predation.cpp:155-156
-        return ABMX_E_CAPACITY;
-    }
+    if (const int rc = check_create(c)) return rc;
     if (c.sheep_capacity > 0xFFFFFE || c.wolf_capacity > 0xFFFFFE) {
         abmx_internal::set_error("capacity per species above 16,777,214 (24-bit cell-list slots)");
         return ABMX_E_CAPACITY;

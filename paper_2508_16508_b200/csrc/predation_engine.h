@@ -105,6 +105,8 @@ struct Params {
 
 const char* kernel_name(int k);
 
+int check_create(const abmx_predation_config& c);  // init_predation's errors (predation.cu)
+
 struct Engine {
     abmx_predation_config cfg{};
     int R = 0;
