@@ -135,3 +135,81 @@ def test_finance_engine_fuzz(F, oracle, cfg, seed, steps):
 def test_finance_batch_fuzz(F, oracle, cfg, master, replicas, steps):
     got, _ = F.run_batch(F.FinanceConfig(**cfg), master, replicas, steps)
     assert np.array_equal(got, oracle.fin_run_batch(master, replicas, steps, **cfg)), cfg
+
+
+# ---------------------------------------------------------------- KernelTable and agent sets
+@st.composite
+def byte_mask(draw, max_n=70_000):
+    n = draw(st.integers(0, max_n))
+    density = draw(st.sampled_from([0.0, 0.01, 0.3, 0.5, 0.99, 1.0]))
+    seed = draw(st.integers(0, 2**32 - 1))
+    g = np.random.default_rng(seed)
+    m = (g.random(n) < density).astype(np.uint8)
+    hot = m > 0
+    m[hot] = g.integers(1, 256, int(hot.sum()), dtype=np.uint8)  # any nonzero byte is true
+    return m
+
+
+@FUZZ
+@given(m=byte_mask(), m2=byte_mask(max_n=5000), seed=st.integers(0, 2**32 - 1))
+def test_kernel_table_fuzz(abmx, oracle, m, m2, seed):
+    """rank_scan / count_true / compact_indices / match_first_equal / blends (kernels.hpp:15-43)
+    against the scalar restatement."""
+    assert np.array_equal(abmx.rank_scan(m), oracle.rank_scan(m))
+    assert abmx.count_true(m) == oracle.count_true(m)
+    assert np.array_equal(abmx.compact_indices(m), oracle.compact_indices(m))
+    ra, rb = oracle.rank_scan(m2), oracle.rank_scan(m[: 3 * m2.size])
+    assert np.array_equal(abmx.match_first_equal(ra, rb), oracle.match_first_equal(ra, rb))
+    g = np.random.default_rng(seed)
+    n = m.size
+    a64, b64 = (g.integers(-2**63, 2**63 - 1, n, dtype=np.int64) for _ in range(2))
+    assert np.array_equal(abmx.blend_i64(m, a64, b64), oracle.blend("i64", m, a64, b64))
+    fa, fb = a64.view(np.float64), b64.view(np.float64)  # every bit pattern, NaNs included
+    assert np.array_equal(abmx.blend_f64(m, fa, fb).view(np.uint64),
+                          oracle.blend("f64", m, fa, fb).view(np.uint64))
+    ua, ub = (g.integers(0, 256, n, dtype=np.uint8) for _ in range(2))
+    assert np.array_equal(abmx.blend_u8(m, ua, ub), oracle.blend("u8", m, ua, ub))
+
+
+@FUZZ
+@given(cap=st.integers(0, 3000), recycle=st.booleans(), cycles=st.integers(1, 5),
+       seed=st.integers(0, 2**32 - 1), frac=st.sampled_from([0.0, 0.3, 0.6, 1.0]))
+def test_lifecycle_fuzz(abmx, oracle, cap, recycle, cycles, seed, frac):
+    """Chained remove_agents + spawn_agents (copy apply, optional type, id recycling) against the
+    C restatement: every column, the counters, the slots / rows of every pairing."""
+    from paper_2508_16508_b200 import agents as A
+    from test_agents_gpu import EWF_STATE, _random_state, from_dev
+    from helpers import ewf_equal
+    g = np.random.default_rng(seed)
+    st_ = _random_state(g, cap, recycle, frac=frac)
+    dev = A.DeviceAgentSet.from_numpy(st_, EWF_STATE, next_id=st_["next_id"], recycle_ids=recycle,
+                                      retired=st_["retired"])
+    for cyc in range(cycles):
+        kill = (g.random(cap) < g.choice([0.0, 0.1, 0.5, 1.0])).astype(np.uint8)
+        m = int(g.integers(0, 2 * cap + 2))
+        rows = {"e": g.integers(-2**40, 2**40, m).astype(np.int64), "w": g.standard_normal(m),
+                "f": (g.random(m) < 0.5).astype(np.uint8)}
+        valid = (g.random(m) < g.choice([0.0, 0.2, 0.7, 1.0])).astype(np.uint8)
+        set_type = bool(g.integers(0, 2))
+        st_, wo = oracle.lifecycle(st_, kill, rows, valid, set_type, cyc + 3)
+        killed = dev.remove(kill)
+        o = dev.spawn(rows, valid, agent_type=cyc + 3 if set_type else None)
+        assert killed == wo["killed"] and (o.spawned, o.dropped) == (wo["spawned"], wo["dropped"]), cyc
+        assert np.array_equal(o.slots, wo["slots"]) and np.array_equal(o.rows, wo["rows"]), cyc
+        ewf_equal(from_dev(dev, recycle), st_, (cap, cyc))
+
+
+@FUZZ
+@given(n=st.integers(1, 20_000), desc=st.booleans(), seed=st.integers(0, 2**32 - 1),
+       spread=st.sampled_from([3, 40, 1 << 20]))
+def test_sort_perm_fuzz(abmx, oracle, n, desc, seed, spread):
+    """Stable key sort of sort_agents (kernels.cpp:37-73): duplicates, +/-0.0, pinned
+    placeholders, against the scalar restatement."""
+    from paper_2508_16508_b200 import agents as A
+    g = np.random.default_rng(seed)
+    key = g.integers(-spread, spread, n).astype(np.float64) * 0.25
+    key[g.random(n) < 0.05] = -0.0
+    act = (g.random(n) < 0.8).astype(np.uint8)
+    key[act == 0] = -np.inf if desc else np.inf
+    assert np.array_equal(A.sort_perm(key, act, descending=desc),
+                          oracle.sort_perm(key, act, descending=desc))
