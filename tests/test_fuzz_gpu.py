@@ -213,3 +213,73 @@ def test_sort_perm_fuzz(abmx, oracle, n, desc, seed, spread):
     key[act == 0] = -np.inf if desc else np.inf
     assert np.array_equal(A.sort_perm(key, act, descending=desc),
                           oracle.sort_perm(key, act, descending=desc))
+
+
+@FUZZ
+@given(L=st.integers(1, 400), dens=st.sampled_from([0.1, 0.5, 0.9, 1.0]), seed=st.integers(0, 2**32 - 1),
+       reach=st.integers(1, 6), p_bad=st.sampled_from([0.0, 0.0, 0.01]))
+def test_traffic_resolve_fuzz(abmx, T, oracle, L, dens, seed, reach, p_bad):
+    """resolve_conflicts with explicit proposals (traffic.cpp:82-140): random dense roads, moves
+    up to `reach` cells ahead into any lane (acyclic, so the reference's L-round iteration
+    converges), stays, exits, and now and then a move off the road (ContractError on both
+    sides)."""
+    g = np.random.default_rng(seed)
+    n = 3 * L
+    occ = g.random(n) < dens
+    slots = g.permutation(n)[: int(occ.sum())]
+    active = np.zeros(n, np.uint8)
+    lane = np.zeros(n, np.int64)
+    cell = np.zeros(n, np.int64)
+    for c, s in zip(np.flatnonzero(occ), slots):
+        active[s], lane[s], cell[s] = 1, c // L, c % L
+    kind = np.zeros(n, np.uint8)
+    to_lane = np.zeros(n, np.int64)
+    to_cell = np.zeros(n, np.int64)
+    for s in np.flatnonzero(active):
+        r = g.random()
+        if cell[s] == L - 1 or r < 0.1:
+            kind[s] = 2 if cell[s] == L - 1 and r < 0.7 else 0
+        else:
+            kind[s] = 1
+            to_lane[s] = g.integers(0, 3)
+            to_cell[s] = min(L - 1, cell[s] + int(g.integers(1, reach + 1)))
+        if g.random() < p_bad:
+            kind[s], to_lane[s], to_cell[s] = 1, 0, L  # off the road
+    m = oracle.traffic(L)
+    m.load({"active": active, "ids": np.zeros(n, np.int64), "ages": np.zeros(n, np.int64),
+            "lane": lane, "cell": cell, "next_id": 0})
+    rc, want = m.resolve(kind, to_lane, to_cell)
+    if rc != 0:
+        with pytest.raises(abmx.ContractError):
+            T.resolve_conflicts(L, active, lane, cell, kind, to_lane, to_cell)
+        return
+    got = T.resolve_conflicts(L, active, lane, cell, kind, to_lane, to_cell)
+    assert np.array_equal(got, want), (L, dens, seed)
+
+
+@FUZZ
+@given(cap=st.integers(1, 600), frac=st.sampled_from([0.0, 0.2, 0.7, 1.0]), seed=st.integers(0, 2**32 - 1),
+       spread=st.sampled_from([0, 1, 8, 200]), last=st.sampled_from([100.0, 0.25, 3.0e5]))
+def test_match_book_fuzz(F, reference, cap, frac, seed, spread, last):
+    """match_book (finance.cpp:125-190) on random books -- crossing and non-crossing, price /
+    placed / id ties, partial fills -- against the reference build itself."""
+    g = np.random.default_rng(seed)
+    act = (g.random(cap) < frac).astype(np.uint8)
+    book = {"active": act,
+            "ids": np.where(act, g.permutation(cap) + 1000, 0).astype(np.int64),
+            "trader": np.where(act, g.integers(0, 50, cap), 0).astype(np.int64),
+            "side": np.where(act, g.integers(0, 2, cap), 0).astype(np.int64),
+            "price": np.where(act, 100.0 + g.integers(-spread, spread + 1, cap) / 128.0, 0.0),
+            "qty": np.where(act, g.integers(1, 21, cap), 0).astype(np.int64),
+            "placed": np.where(act, g.integers(0, 4, cap), 0).astype(np.int64), "next_id": cap + 2000}
+    got, gf, gs = F.match_book(book, last)
+    want, wf, ws = reference.fin_match(book, last)
+    for name, _ in pyoracle.BOOK_FIELDS:
+        x, y = np.asarray(got[name]), np.asarray(want[name])
+        if name == "price":
+            x, y = x.view(np.uint64), y.view(np.uint64)
+        assert np.array_equal(x, y), (cap, seed, name)
+    for k in ("trader", "side", "qty"):
+        assert np.array_equal(gf[k], wf[k]), (cap, seed, k)
+    assert np.array_equal(gf["amount"].view(np.uint64), wf["amount"].view(np.uint64))
+    assert (gs["last_price"], gs["volume"], gs["clearing"]) == (ws[0], int(ws[2]), ws[3])
