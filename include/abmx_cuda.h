@@ -190,6 +190,29 @@ int abmx_ensemble_run(const abmx_predation_config* cfg, uint64_t master, int32_t
 /* 1 if the SMEM-resident path supports cfg */
 int abmx_ensemble_smem_fits(const abmx_predation_config* cfg);
 
+/* One species in the reference layout (predation.cpp:22-33 fields + AgentSet lifecycle
+ * columns): caller-owned host arrays of the species capacity; num_active / next_id are out. */
+typedef struct abmx_species_arrays {
+    uint8_t* active;
+    int64_t* ids;
+    int64_t* ages;
+    int64_t* x;
+    int64_t* y;
+    double* energy;
+    int32_t num_active;
+    int64_t next_id;
+} abmx_species_arrays;
+
+/* run_batch on the SMEM-resident path, then the final state of batch member `replica`
+ * (0-based within [replica_begin, replica_begin+count)) in the reference layout: what the
+ * reference's PredationModel of that replica holds after `steps` steps. grass_ready / regrow:
+ * [width*height]. ABMX_E_DOMAIN when cfg does not fit the SMEM-resident path. */
+int abmx_ensemble_replica_state(const abmx_predation_config* cfg, uint64_t master,
+                                int32_t replica_begin, int32_t count, int64_t steps,
+                                int32_t replica, abmx_species_arrays* sheep,
+                                abmx_species_arrays* wolves, uint8_t* grass_ready,
+                                int64_t* regrow);
+
 /* ======================================================================= 4. agent sets
  * The generic lifecycle and subset operations on an AgentSet whose
  * columns live in device memory. Callbacks (std::function ApplyFn / SlotUpdateFn,

@@ -196,6 +196,9 @@ _sig("abmx_predation_bench", C.c_int, [C.c_void_p, C.c_int64, C.c_int64, C.c_int
 _sig("abmx_predation_fetch_metrics", C.c_int, [C.c_void_p, f64p])
 _sig("abmx_ensemble_run", C.c_int, [C.POINTER(PredationConfig), C.c_uint64, C.c_int32, C.c_int32,
                                     C.c_int64, C.c_int32, f64p, f64p])
+_sig("abmx_ensemble_replica_state", C.c_int, [C.POINTER(PredationConfig), C.c_uint64, C.c_int32,
+                                                 C.c_int32, C.c_int64, C.c_int32, C.c_void_p,
+                                                 C.c_void_p, u8p, i64p])
 _sig("abmx_ensemble_smem_fits", C.c_int, [C.POINTER(PredationConfig)])
 _sig("abmx_diag_random_access", C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_double, C.c_double,
                                           C.c_int32, C.c_int32, C.c_int32, f64p, f64p])
@@ -476,6 +479,36 @@ class PredationModel:
 
 def smem_fits(cfg: PredationConfig) -> bool:
     return bool(lib.abmx_ensemble_smem_fits(C.byref(cfg)))
+
+
+class _SpeciesArraysC(C.Structure):
+    _fields_ = [("active", C.c_void_p), ("ids", C.c_void_p), ("ages", C.c_void_p), ("x", C.c_void_p),
+                ("y", C.c_void_p), ("energy", C.c_void_p), ("num_active", C.c_int32),
+                ("next_id", C.c_int64)]
+
+
+def ensemble_replica_state(cfg: PredationConfig, master: int, replicas: int, steps: int,
+                           replica: int, *, begin: int = 0):
+    """run_batch on the SMEM-resident path, then batch member `replica`'s final state in the
+    reference layout: (sheep dict, wolves dict, grass_ready, regrow)."""
+    out = []
+    keep = []
+    for n in (cfg.sheep_capacity, cfg.wolf_capacity):
+        d = dict(active=np.zeros(n, np.uint8), ids=np.zeros(n, np.int64), ages=np.zeros(n, np.int64),
+                 x=np.zeros(n, np.int64), y=np.zeros(n, np.int64), energy=np.zeros(n, np.float64))
+        c = _SpeciesArraysC(*(d[k].ctypes.data for k in ("active", "ids", "ages", "x", "y", "energy")), 0, 0)
+        out.append(d)
+        keep.append(c)
+    cells = cfg.width * cfg.height
+    ready = np.zeros(cells, np.uint8)
+    regrow = np.zeros(cells, np.int64)
+    _check(lib.abmx_ensemble_replica_state(C.byref(cfg), master & _M64, begin, replicas, steps, replica,
+                                           C.byref(keep[0]), C.byref(keep[1]), _p(ready, u8p),
+                                           _p(regrow, i64p)))
+    for d, c in zip(out, keep):
+        d["num_active"] = c.num_active
+        d["next_id"] = c.next_id
+    return out[0], out[1], ready, regrow
 
 
 def run_batch(cfg: PredationConfig, master: int, replicas: int, steps: int, *, begin: int = 0,

@@ -381,6 +381,51 @@ int abmx_ensemble_smem_fits(const abmx_predation_config* cfg) {
     return cfg && abmx_ens::smem_fits(*cfg) ? 1 : 0;
 }
 
+int abmx_ensemble_replica_state(const abmx_predation_config* cfg, uint64_t master, int32_t replica_begin,
+                                int32_t count, int64_t steps, int32_t replica, abmx_species_arrays* sheep,
+                                abmx_species_arrays* wolves, uint8_t* grass_ready, int64_t* regrow) {
+    if (!cfg || !sheep || !wolves || !grass_ready || !regrow) {
+        set_error("null argument");
+        return ABMX_E_ARG;
+    }
+    if (count < 1) {
+        set_error("batch needs at least one replica");  // batch.cpp:24-25
+        return ABMX_E_BATCH;
+    }
+    if (steps < 1 || replica < 0 || replica >= count) {
+        set_error("steps must be >= 1 and replica inside the batch");
+        return ABMX_E_DOMAIN;
+    }
+    if (!abmx_ens::smem_fits(*cfg)) {
+        set_error("configuration does not fit the SMEM-resident ensemble kernel");
+        return ABMX_E_DOMAIN;
+    }
+    std::vector<uint64_t> seeds(static_cast<size_t>(count));
+    const unsigned long long root = abmx_dev::split(master, 2);  // batch.cpp:12-19
+    for (int32_t k = 0; k < count; ++k)
+        seeds[static_cast<size_t>(k)] = abmx_dev::split(root, static_cast<unsigned long long>(replica_begin + k));
+    abmx_ens::Dump d{};
+    d.replica = replica;
+    abmx_species_arrays* sp[2] = {sheep, wolves};
+    for (int s = 0; s < 2; ++s) {
+        d.active[s] = sp[s]->active;
+        d.ids[s] = sp[s]->ids;
+        d.ages[s] = sp[s]->ages;
+        d.x[s] = sp[s]->x;
+        d.y[s] = sp[s]->y;
+        d.energy[s] = sp[s]->energy;
+    }
+    d.grass_ready = grass_ready;
+    d.regrow = regrow;
+    const int rc = abmx_ens::run_smem(*cfg, seeds.data(), count, steps, nullptr, nullptr, &d);
+    if (rc) return rc;
+    for (int s = 0; s < 2; ++s) {
+        sp[s]->num_active = d.num_active[s];
+        sp[s]->next_id = d.next_id[s];
+    }
+    return ABMX_OK;
+}
+
 int abmx_ensemble_run(const abmx_predation_config* cfg, uint64_t master, int32_t replica_begin, int32_t count,
                       int64_t steps, int32_t path, double* metrics_out, double* kernel_ms) {
     if (!cfg) {

@@ -77,3 +77,26 @@ def test_ensemble_lazy_regrow_past_renormalisation(abmx, oracle, delay, gain):
     want = oracle.run_batch(cfg, 23, 3, 8500)
     assert want[:, -1, 0].sum() > 0  # sheep survive, so grazing continues to the end
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("cfgd,steps,replica", [(c1(), 100, 3), (tiny(), 60, 0),
+                                                (c1(regrow_delay=0), 40, 1), (c1(regrow_delay=-2), 40, 2),
+                                                (c1(width=24, height=24, n_sheep0=60, n_wolves0=6,
+                                                    sheep_capacity=512, wolf_capacity=64,
+                                                    energy_gain_sheep=8.0, regrow_delay=60), 8300, 1)])
+def test_ensemble_final_state_vs_oracle(abmx, oracle, cfgd, steps, replica):
+    """The on-chip kernel's final state of one batch member -- every agent column, next_id,
+    num_active, grass_ready and the regrow countdowns (lazy regrow converted back, incl. after
+    the renormalisation at step 8192) -- against the oracle's PredationModel of that replica."""
+    from helpers import species_equal
+    master, count = 31, 4
+    sh, wo, ready, regrow = abmx.ensemble_replica_state(abmx.PredationConfig(**cfgd), master, count,
+                                                         steps, replica)
+    orc = oracle.pred(cfgd, oracle.replica_seed(master, replica))
+    for t in range(1, steps + 1):
+        orc.step(t)
+    for s, got in ((0, sh), (1, wo)):
+        want = orc.export_species(s)
+        species_equal({k: v for k, v in got.items()}, want, f"species {s}")
+    wr, wg = orc.export_world()
+    assert np.array_equal(ready, wr) and np.array_equal(regrow, wg)
