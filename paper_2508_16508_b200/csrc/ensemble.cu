@@ -48,6 +48,7 @@ __constant__ int e_dy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
 
 struct EnsParams {
     int W, H, C, Cpad;
+    unsigned long long wdiv;  // ceil(2^40 / W)
     int N[2], n0[2], stride;
     double gain[2], metab, prob[2], frac;
     int delay;  // regrow_delay (<= 0: a grazed cell never regrows)
@@ -169,13 +170,16 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
 
     for (long long t = 1; t <= P.steps; ++t) {
         unsigned long long mk[2], rk[2];
-        {
-            const unsigned long long mt = split(mroot, static_cast<unsigned long long>(t));
-            const unsigned long long rt = split(rroot, static_cast<unsigned long long>(t));
-            mk[0] = split(mt, 0);
-            mk[1] = split(mt, 1);
-            rk[0] = split(rt, 0);
-            rk[1] = split(rt, 1);
+        {  // the step's four stream keys, two splits per lane instead of six: lanes 0/1 derive
+           // the move / reproduce roots of step t, lanes 0..3 the per-species keys, shuffled out
+            const unsigned ln = static_cast<unsigned>(tid) & 31u;
+            const unsigned long long a = split(ln & 1u ? rroot : mroot, static_cast<unsigned long long>(t));
+            const unsigned long long mt = __shfl_sync(0xffffffffu, a, 0), rt = __shfl_sync(0xffffffffu, a, 1);
+            const unsigned long long b = split(ln & 2u ? rt : mt, static_cast<unsigned long long>(ln & 1u));
+            mk[0] = __shfl_sync(0xffffffffu, b, 0);
+            mk[1] = __shfl_sync(0xffffffffu, b, 1);
+            rk[0] = __shfl_sync(0xffffffffu, b, 2);
+            rk[1] = __shfl_sync(0xffffffffu, b, 3);
         }
         // ---- phase 1: move + push onto the per-cell lists
 #pragma unroll
@@ -187,7 +191,9 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
                 const int i = tid * SPT + k;
                 const int u = static_cast<int>(draw(mk[s], static_cast<unsigned long long>(i)) >> 61);
                 const int c = cell[s][k];
-                const int y = c / P.W, x = c - y * P.W;
+                // c / W by multiply-high: exact for c, W < 2^18 (smem_fits bounds C by 2^18)
+                const int y = static_cast<int>((static_cast<unsigned long long>(c) * P.wdiv) >> 40);
+                const int x = c - y * P.W;
                 int nx = x + e_dx[u], ny = y + e_dy[u];
                 nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
                 ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
@@ -456,6 +462,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     P.H = cfg.height;
     P.C = cfg.width * cfg.height;
     P.Cpad = (P.C + 15) / 16 * 16;
+    P.wdiv = ((1ULL << 40) + static_cast<unsigned long long>(P.W) - 1) / static_cast<unsigned long long>(P.W);
     P.N[0] = cfg.sheep_capacity;
     P.N[1] = cfg.wolf_capacity;
     P.n0[0] = cfg.n_sheep0;
