@@ -119,9 +119,14 @@ __global__ void __launch_bounds__(kNT, 1536 / kNT) k_traffic_ens(EnsP P) {  // 2
     // SignalSchedule::green(t) = ((t + phase) mod period) < green_len, advanced incrementally
     long long gm = ((1 + phase) % P.period + P.period) % P.period;
     __syncthreads();
+    // per-road stream roots (TrafficPropose = 6, TrafficSpawn = 7); each step's two keys are
+    // derived once per warp (lane 0 propose, lane 1 spawn) and shuffled out
+    const unsigned long long root6 = split(seed, 6), root7 = split(seed, 7);
     for (long long t = 1; t <= P.steps; ++t, gm = gm + 1 == P.period ? 0 : gm + 1) {
         const bool green = gm < P.green_len;
-        const unsigned long long kp = split(split(seed, 6), static_cast<unsigned long long>(t));
+        const unsigned long long kk = split(lane & 1 ? root7 : root6, static_cast<unsigned long long>(t));
+        const unsigned long long kp = __shfl_sync(0xffffffffu, kk, 0);
+        const unsigned long long ks_step = __shfl_sync(0xffffffffu, kk, 1);
         // (a) propose (traffic.cpp:47-80) and bid for the target cell (priority, then slot)
         for (int x = tid; x < C; x += kNT) R.bid[x] = kNoBid;
         __syncthreads();
@@ -228,7 +233,7 @@ __global__ void __launch_bounds__(kNT, 1536 / kNT) k_traffic_ens(EnsP P) {  // 2
         __syncthreads();
         // (d) spawn_cars (traffic.cpp:143-184) into the lowest free slots; metrics row
         if (warp == 0) {
-            const unsigned long long ks = split(split(seed, 7), static_cast<unsigned long long>(t));
+            const unsigned long long ks = ks_step;
             const int k = static_cast<int>(uniform_span(ks, 0, 4));
             int lanes[3] = {0, 1, 2};
             for (int i = 0; i < (k < 2 ? k : 2); ++i) {
