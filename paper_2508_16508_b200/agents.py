@@ -29,7 +29,7 @@ import numpy as np
 
 from . import (CapacityError, DomainError, SchemaError, _check, lib)
 
-__all__ = ["DeviceAgentSet", "SpawnOutcome", "PairOutcome"]
+__all__ = ["DeviceAgentSet", "SpawnOutcome", "PairOutcome", "ToyResult", "run_toy", "format_int_list"]
 
 _i64p = C.POINTER(C.c_int64)
 _i32p = C.POINTER(C.c_int32)
@@ -341,3 +341,35 @@ def sort_perm(key, active, descending=False, device=None) -> np.ndarray:
                                      perm.data_ptr(),
                                      C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
     return perm[:n].cpu().numpy()
+
+
+@dataclass
+class ToyResult:
+    """toy.hpp: the paper's section 3 example through both subset-update algorithms."""
+    rank_match: list
+    sort_count_iterate: list
+
+
+def run_toy(a, b, device=None) -> ToyResult:
+    """run_toy (src/toy.cpp:34-56) on the device: agents hold `value` = a (all active); the even
+    values are the targets, the odd entries of b the valid rows; each target takes its paired
+    row's value (copy apply), once by rank-match (set_agents_rm) and once by
+    sort-count-iterate (set_agents_sci), each on a fresh copy of the set."""
+    a = np.asarray(a, np.int64)
+    b = np.asarray(b, np.int64)
+    n = a.size
+    base = {"active": np.ones(n, np.uint8), "ids": np.arange(n, dtype=np.int64),
+            "ages": np.zeros(n, np.int64), "value": a}
+    even = (a % 2 == 0).astype(np.uint8)
+    odd = (b % 2 != 0).astype(np.uint8)
+    out = []
+    for op in ("set_rm", "set_sci"):
+        s = DeviceAgentSet.from_numpy(base, ["value"], next_id=n, device=device)
+        getattr(s, op)(even, {"value": b}, odd)
+        out.append([int(v) for v in s.state["value"].cpu().numpy()])
+    return ToyResult(out[0], out[1])
+
+
+def format_int_list(v) -> str:
+    """format_int_list (src/toy.cpp:58-69): "[1, 3, 3, 6]"."""
+    return "[" + ", ".join(str(int(x)) for x in v) + "]"

@@ -237,3 +237,26 @@ def test_permute_and_set_mask(abmx, agents):
     assert np.array_equal(got["e"], np.where(mask, vals["e"], before["e"]))
     assert np.array_equal(got["w"], np.where(mask, vals["w"], before["w"]))
     assert np.array_equal(got["f"], before["f"])
+
+
+def test_toy_known_answer(agents):
+    """test_kernels.cpp:181-185 (the paper's section 3 example): run_toy({2,3,4,6}, {1,4,3})."""
+    r = agents.run_toy([2, 3, 4, 6], [1, 4, 3])
+    assert r.rank_match == [1, 3, 3, 6] and r.sort_count_iterate == [1, 3, 3, 6]
+    assert agents.format_int_list(r.rank_match) == "[1, 3, 3, 6]"
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_toy_rm_equals_sci(agents, seed):
+    """Random toy inputs: rank-match and sort-count-iterate agree, and every even target k takes
+    the k-th odd row (lifecycle.cpp:159-189 pairing by rank)."""
+    g = np.random.default_rng(seed)
+    a = g.integers(0, 50, int(g.integers(0, 300)))
+    b = g.integers(0, 50, int(g.integers(0, 300)))
+    r = agents.run_toy(a, b)
+    assert r.rank_match == r.sort_count_iterate
+    want = a.copy()
+    slots, rows = np.flatnonzero(a % 2 == 0), np.flatnonzero(b % 2 != 0)
+    k = min(slots.size, rows.size)
+    want[slots[:k]] = b[rows[:k]]
+    assert r.rank_match == want.tolist()
