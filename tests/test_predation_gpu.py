@@ -5,7 +5,6 @@ import numpy as np
 import pytest
 
 from helpers import c1, species_equal, state_hash, tiny
-import pyoracle
 
 pytestmark = pytest.mark.gpu
 

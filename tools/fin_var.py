@@ -6,7 +6,6 @@ import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2508_16508_b200 import finance as F  # noqa: E402
-import torch  # noqa: E402
 
 cfg = F.FinanceConfig()
 F.run_batch(cfg, 7, 1024, 100)
