@@ -53,6 +53,7 @@ struct FParams {
     int M, K, T, cap, sort_n;  // sort_n: power of two >= W
     int W;     // order window: every active order of every book lies in slots [0, W) (see launch)
     int* err;  // set if a book ever needed a slot >= W (cannot happen; checked on every readback)
+    long long id_span;  // keyed: alive ids lie in [next_id - id_span, next_id + T*steps)
     double p_order, delta, init_price;
     long long qmax, max_age;
     long long t0, steps;
@@ -103,6 +104,12 @@ struct Smem {
     uint8_t* rs;
     int* rt;
     unsigned long long* key;  // kKeyed: (side, price) priority packed in one word, per slot
+    // kKeyed compact fields: id - idbase, placed and the cumulative quantities in 32 bits (side
+    // and price live in `key`)
+    int* id32;
+    int* pl32;
+    int* cum32;
+    long long idbase;
     double* dcash;       // [T] cash delta of this book
     long long* dhold;    // [T] holdings delta of this book
 };
@@ -112,6 +119,61 @@ struct Smem {
 __device__ __forceinline__ unsigned long long prio_key(uint8_t side, double price) {
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(price));
     return side ? (1ULL << 63) | b : ~b & 0x7FFFFFFFFFFFFFFFULL;
+}
+
+// the price of a packed key (the inverse of prio_key)
+__device__ __forceinline__ double key_price(unsigned long long k) {
+    const unsigned long long b = (k >> 63) ? (k & 0x7FFFFFFFFFFFFFFFULL) : (~k & 0x7FFFFFFFFFFFFFFFULL);
+    return __longlong_as_double(static_cast<long long>(b));
+}
+
+// order fields in either layout
+template <bool kK>
+__device__ __forceinline__ int o_side(const Smem& S, int i) {
+    if constexpr (kK) return static_cast<int>(S.key[i] >> 63);
+    else return S.sd[i];
+}
+template <bool kK>
+__device__ __forceinline__ double o_price(const Smem& S, int i) {
+    if constexpr (kK) return key_price(S.key[i]);
+    else return S.pr[i];
+}
+template <bool kK>
+__device__ __forceinline__ long long o_id(const Smem& S, int i) {
+    if constexpr (kK) return S.idbase + S.id32[i];
+    else return S.id[i];
+}
+template <bool kK>
+__device__ __forceinline__ long long o_placed(const Smem& S, int i) {
+    if constexpr (kK) return S.pl32[i];
+    else return S.pl[i];
+}
+template <bool kK>
+__device__ __forceinline__ long long o_cum(const Smem& S, int j) {
+    if constexpr (kK) return S.cum32[j];
+    else return S.cum[j];
+}
+template <bool kK>
+__device__ __forceinline__ void set_cum(const Smem& S, int j, long long v) {
+    if constexpr (kK) S.cum32[j] = static_cast<int>(v);
+    else S.cum[j] = v;
+}
+template <bool kK>
+__device__ __forceinline__ void set_order(const Smem& S, int i, long long id, int tr, int side, double price,
+                                          int q, long long placed) {
+    S.act[i] = 1;
+    S.tr[i] = tr;
+    S.q[i] = q;
+    if constexpr (kK) {
+        S.id32[i] = static_cast<int>(id - S.idbase);
+        S.pl32[i] = static_cast<int>(placed);
+        S.key[i] = prio_key(static_cast<uint8_t>(side), price);
+    } else {
+        S.id[i] = id;
+        S.sd[i] = static_cast<uint8_t>(side);
+        S.pr[i] = price;
+        S.pl[i] = placed;
+    }
 }
 
 // sort order: buys before sells; buys by price desc, sells by price asc; then placed, id, slot.
@@ -124,7 +186,7 @@ __device__ __forceinline__ bool before(const Smem& S, unsigned short a, unsigned
     if (a == kPad) return false;
     if constexpr (kKeyed) {
         const unsigned long long ka = S.key[a], kb = S.key[b];
-        return ka != kb ? ka < kb : S.id[a] < S.id[b];
+        return ka != kb ? ka < kb : S.id32[a] < S.id32[b];
     }
     if (S.sd[a] != S.sd[b]) return S.sd[a] < S.sd[b];
     if (S.pr[a] != S.pr[b]) return S.sd[a] == 0 ? S.pr[a] > S.pr[b] : S.pr[a] < S.pr[b];
@@ -133,14 +195,21 @@ __device__ __forceinline__ bool before(const Smem& S, unsigned short a, unsigned
     return a < b;
 }
 
+template <bool kK>
 __device__ __forceinline__ void reset_slot(const Smem& S, int i) {  // agent_set.cpp:45-58
     S.act[i] = 0;
-    S.id[i] = 0;
     S.tr[i] = 0;
-    S.sd[i] = 0;
-    S.pr[i] = 0.0;
     S.q[i] = 0;
-    S.pl[i] = 0;
+    if constexpr (kK) {  // stored back as zeros (inactive)
+        S.id32[i] = 0;
+        S.pl32[i] = 0;
+        S.key[i] = 0;
+    } else {
+        S.id[i] = 0;
+        S.sd[i] = 0;
+        S.pr[i] = 0.0;
+        S.pl[i] = 0;
+    }
 }
 
 template <int kNT, bool kKeyed>
@@ -153,24 +222,38 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     const int m = blockIdx.x / P.K, k = blockIdx.x % P.K;
     const int W = P.W, T = P.T, N = P.sort_n, tid = threadIdx.x;
     // shared layout (8-byte fields first)
-    Smem S;
+    Smem S{};
+    const size_t bo = (static_cast<size_t>(m) * P.K + k) * P.cap;
+    BookS B = P.bs[static_cast<size_t>(m) * P.K + k];
     unsigned char* p = smraw;
-    S.id = reinterpret_cast<long long*>(p);
-    p += 8 * W;
-    S.pr = reinterpret_cast<double*>(p);
-    p += 8 * W;
-    S.pl = reinterpret_cast<long long*>(p);
-    p += 8 * W;
-    S.cum = reinterpret_cast<long long*>(p);
-    p += 8 * W;
-    S.key = reinterpret_cast<unsigned long long*>(p);
-    if (kKeyed) p += 8 * W;
+    if constexpr (kKeyed) {
+        S.key = reinterpret_cast<unsigned long long*>(p);
+        p += 8 * W;
+    } else {
+        S.id = reinterpret_cast<long long*>(p);
+        p += 8 * W;
+        S.pr = reinterpret_cast<double*>(p);
+        p += 8 * W;
+        S.pl = reinterpret_cast<long long*>(p);
+        p += 8 * W;
+        S.cum = reinterpret_cast<long long*>(p);
+        p += 8 * W;
+    }
     S.rp = reinterpret_cast<double*>(p);
     p += 8 * T;
     S.dcash = reinterpret_cast<double*>(p);
     p += 8 * T;
     S.dhold = reinterpret_cast<long long*>(p);
     p += 8 * T;
+    if constexpr (kKeyed) {
+        S.id32 = reinterpret_cast<int*>(p);
+        p += 4 * W;
+        S.pl32 = reinterpret_cast<int*>(p);
+        p += 4 * W;
+        S.cum32 = reinterpret_cast<int*>(p);
+        p += 4 * W;
+        S.idbase = B.next_id - P.id_span;
+    }
     S.tr = reinterpret_cast<int*>(p);
     p += 4 * W;
     S.q = reinterpret_cast<int*>(p);
@@ -182,34 +265,41 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     S.list = reinterpret_cast<unsigned short*>(p);
     p += 2 * N;
     // the ping-pong order buffer is used only by the merge (before matching) and the compaction
-    // (after it), never while `cum` is live: it aliases `cum` (8*W >= 2*sort_n bytes: sort_n < 2W)
-    S.list2 = reinterpret_cast<unsigned short*>(S.cum);
+    // (after it), never while the cumulative quantities are live: it aliases them (4*W or 8*W
+    // bytes >= 2*sort_n bytes, since sort_n < 2W)
+    S.list2 = kKeyed ? reinterpret_cast<unsigned short*>(S.cum32) : reinterpret_cast<unsigned short*>(S.cum);
     S.nl = reinterpret_cast<unsigned short*>(p);
     p += 2 * T;
     S.nsr = reinterpret_cast<unsigned short*>(p);
     p += 2 * T;
     S.act = p;
     p += W;
-    S.sd = p;
-    p += W;
+    if constexpr (!kKeyed) {
+        S.sd = p;
+        p += W;
+    }
     S.rs = p;
     // load the book
-    const size_t bo = (static_cast<size_t>(m) * P.K + k) * P.cap;
     for (int i = tid; i < W; i += kNT) {
-        S.act[i] = P.active[bo + i];
-        S.id[i] = P.ids[bo + i];
+        const uint8_t a = P.active[bo + i];
+        S.act[i] = a;
         S.tr[i] = P.trader[bo + i];
-        S.sd[i] = P.side[bo + i];
-        S.pr[i] = P.price[bo + i];
-        if (kKeyed) S.key[i] = prio_key(S.sd[i], S.pr[i]);
         S.q[i] = P.qty[bo + i];
-        S.pl[i] = P.placed[bo + i];
+        if constexpr (kKeyed) {  // windowed books: inactive slots hold zeros
+            S.id32[i] = a ? static_cast<int>(P.ids[bo + i] - S.idbase) : 0;
+            S.pl32[i] = static_cast<int>(P.placed[bo + i]);
+            S.key[i] = a ? prio_key(P.side[bo + i], P.price[bo + i]) : 0ULL;
+        } else {
+            S.id[i] = P.ids[bo + i];
+            S.sd[i] = P.side[bo + i];
+            S.pr[i] = P.price[bo + i];
+            S.pl[i] = P.placed[bo + i];
+        }
     }
     for (int i = tid; i < T; i += kNT) {
         S.dcash[i] = 0.0;
         S.dhold[i] = 0;
     }
-    BookS B = P.bs[static_cast<size_t>(m) * P.K + k];
     // The priority order of resting orders never changes (price, placed and id are fixed), so
     // the sorted order list is built once per launch and then maintained: new orders are
     // merged in by rank + binary search, filled / cancelled orders compacted out.
@@ -292,14 +382,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 const unsigned ex = block_excl_count<kNT>(fr ? 1u : 0u, s_scan, &tot);
                 const long long r = static_cast<long long>(fcarry + ex);
                 if (fr && r < q) {
-                    S.act[i] = 1;
-                    S.id[i] = B.next_id + r;
-                    S.tr[i] = S.rt[r];
-                    S.sd[i] = S.rs[r];
-                    S.pr[i] = S.rp[r];
-                    if (kKeyed) S.key[i] = prio_key(S.rs[r], S.rp[r]);
-                    S.q[i] = S.rq[r];
-                    S.pl[i] = t;
+                    set_order<kKeyed>(S, i, B.next_id + r, S.rt[r], S.rs[r], S.rp[r], S.rq[r], t);
                     S.nl[r] = static_cast<unsigned short>(i);
                 }
                 fcarry += tot;
@@ -359,7 +442,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 unsigned long long tot;
                 const unsigned long long ex =
                     block_excl_scan<kNT>(s != kPad ? static_cast<unsigned long long>(S.q[s]) : 0ULL, s_scan, &tot);
-                if (s != kPad) S.cum[i] = static_cast<long long>(qcarry + ex) + S.q[s];
+                if (s != kPad) set_cum<kKeyed>(S, i, static_cast<long long>(qcarry + ex) + S.q[s]);
                 qcarry += tot;
                 __syncthreads();
             }
@@ -368,7 +451,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 int lo = 0, hi = n;  // first sell in the list
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
-                    if (S.sd[L[mid]] == 0)
+                    if (o_side<kKeyed>(S, L[mid]) == 0)
                         lo = mid + 1;
                     else
                         hi = mid;
@@ -376,22 +459,22 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 nbuy = lo;
             }
             const int nsell = n - nbuy;
-            const long long btot = nbuy > 0 ? S.cum[nbuy - 1] : 0;  // sells' cum = cum - btot
+            const long long btot = nbuy > 0 ? o_cum<kKeyed>(S, nbuy - 1) : 0;  // sells' cum = cum - btot
             // executed volume: max over buys of min(buy cum, sell cum at upper_bound(buy price))
             long long vmax = 0;
             if (nbuy > 0 && nsell > 0)
                 for (int i = tid; i < nbuy; i += kNT) {
-                    const double bp = S.pr[L[i]];
+                    const double bp = o_price<kKeyed>(S, L[i]);
                     int lo = 0, hi = nsell;  // first sell with price > bp
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (bp < S.pr[L[nbuy + mid]])
+                        if (bp < o_price<kKeyed>(S, L[nbuy + mid]))
                             hi = mid;
                         else
                             lo = mid + 1;
                     }
                     if (lo == 0) continue;
-                    const long long bc = S.cum[i], sc = S.cum[nbuy + lo - 1] - btot;
+                    const long long bc = o_cum<kKeyed>(S, i), sc = o_cum<kKeyed>(S, nbuy + lo - 1) - btot;
                     const long long v = bc < sc ? bc : sc;
                     if (v > vmax) vmax = v;
                 }
@@ -411,7 +494,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     int lo = 0, hi = nbuy - 1;
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (S.cum[mid] >= volume)
+                        if (o_cum<kKeyed>(S, mid) >= volume)
                             hi = mid;
                         else
                             lo = mid + 1;
@@ -421,20 +504,21 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     hi = nsell - 1;
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (S.cum[nbuy + mid] - btot >= volume)
+                        if (o_cum<kKeyed>(S, nbuy + mid) - btot >= volume)
                             hi = mid;
                         else
                             lo = mid + 1;
                     }
                     ms = lo;
                 }
-                const double clearing = __dadd_rn(S.pr[L[mb]], S.pr[L[nbuy + ms]]) / 2.0;
+                const double clearing = __dadd_rn(o_price<kKeyed>(S, L[mb]), o_price<kKeyed>(S, L[nbuy + ms])) / 2.0;
                 __syncthreads();  // every thread has read the sorted prices before fills reset slots
                 // fills: sorted order j gets min(qty_j, volume - cum_{j-1}) while positive
                 for (int j = tid; j < n; j += kNT) {
                     const unsigned short s = L[j];
                     const bool buy = j < nbuy;
-                    const long long before_j = buy ? (j > 0 ? S.cum[j - 1] : 0) : (j > nbuy ? S.cum[j - 1] - btot : 0);
+                    const long long before_j =
+                        buy ? (j > 0 ? o_cum<kKeyed>(S, j - 1) : 0) : (j > nbuy ? o_cum<kKeyed>(S, j - 1) - btot : 0);
                     const long long rem = volume - before_j;
                     if (rem <= 0) continue;
                     const long long f = S.q[s] < rem ? S.q[s] : rem;
@@ -452,7 +536,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                                   static_cast<unsigned long long>(buy ? f : -f));
                     }
                     S.q[s] -= static_cast<int>(f);
-                    if (S.q[s] == 0) reset_slot(S, s);  // exhausted: remove_agents
+                    if (S.q[s] == 0) reset_slot<kKeyed>(S, s);  // exhausted: remove_agents
                 }
                 if (P.match_only && tid == 0) *P.n_fills = (mb + 1) + (ms + 1);
                 B.last_price = clearing;
@@ -475,12 +559,12 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 if (i < n) {
                     s = L[i];
                     if (S.act[s]) {
-                        if (t - S.pl[s] >= P.max_age)
-                            reset_slot(S, s);
+                        if (t - o_placed<kKeyed>(S, s) >= P.max_age)
+                            reset_slot<kKeyed>(S, s);
                         else
                             alive = true;
                     }
-                    buy = alive && S.sd[s] == 0;
+                    buy = alive && o_side<kKeyed>(S, s) == 0;
                 }
                 unsigned tot;  // packed (alive << 16 | alive buy): at most kNT per field
                 const unsigned ex = block_excl_count<kNT>((alive ? (1u << 16) : 0u) | (buy ? 1u : 0u), s_scan, &tot);
@@ -506,13 +590,21 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     }
     // store the book, fold this book's settlement into the traders
     for (int i = tid; i < W; i += kNT) {
-        P.active[bo + i] = S.act[i];
-        P.ids[bo + i] = S.id[i];
+        const uint8_t a = S.act[i];
+        P.active[bo + i] = a;
         P.trader[bo + i] = S.tr[i];
-        P.side[bo + i] = S.sd[i];
-        P.price[bo + i] = S.pr[i];
         P.qty[bo + i] = S.q[i];
-        P.placed[bo + i] = S.pl[i];
+        if constexpr (kKeyed) {  // inactive slots are all zeros (reset_slot)
+            P.ids[bo + i] = a ? o_id<kKeyed>(S, i) : 0;
+            P.side[bo + i] = a ? static_cast<uint8_t>(o_side<kKeyed>(S, i)) : 0;
+            P.price[bo + i] = a ? o_price<kKeyed>(S, i) : 0.0;
+            P.placed[bo + i] = a ? o_placed<kKeyed>(S, i) : 0;
+        } else {
+            P.ids[bo + i] = S.id[i];
+            P.side[bo + i] = S.sd[i];
+            P.price[bo + i] = S.pr[i];
+            P.placed[bo + i] = S.pl[i];
+        }
     }
     if (!P.match_only)
         for (int i = tid; i < T; i += kNT) {
@@ -591,7 +683,9 @@ int check_cfg(const abmx_finance_config& c) {
 
 size_t fin_smem(const abmx_finance_config& c, int window, int sort_n, bool keyed) {
     const size_t cap = static_cast<size_t>(window), T = static_cast<size_t>(c.traders);
-    return (keyed ? 8 * cap : 0) + 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 4 * T + 2 * cap + T + 64;
+    if (keyed)  // key 8 + id32 / placed32 / cum32 / trader / qty 4 each + active 1 per slot
+        return 29 * cap + 37 * T + 2 * static_cast<size_t>(sort_n) + 64;
+    return 32 * cap + 24 * T + 8 * cap + 8 * T + 2 * static_cast<size_t>(sort_n) + 4 * T + 2 * cap + T + 64;
 }
 
 }  // namespace
@@ -618,6 +712,13 @@ struct abmx_finance {
     long long last_t = LLONG_MIN;
     int* d_err = nullptr;
     bool keyed_ok = false;  // the windowed layout plus the priority keys fits in shared memory
+    // the keyed layout keeps ids (relative to next_id - id_span), placed and the cumulative
+    // quantities in 32 bits: a launch qualifies when all three ranges fit
+    bool compact_fits(long long t0, long long steps) const {
+        const long long age = cfg.max_order_age > 0 ? cfg.max_order_age : 0;
+        return P.id_span + P.T * steps <= INT32_MAX && t0 - age - 1 >= INT32_MIN && t0 + steps <= INT32_MAX &&
+               cfg.qmax <= INT32_MAX / (window > 0 ? window : 1);
+    }
     static int pow2_at_least(int n) {
         int q = 1;
         while (q < n) q <<= 1;
@@ -627,6 +728,9 @@ struct abmx_finance {
         P.W = use ? window : P.cap;
         P.sort_n = pow2_at_least(P.W);
         smem = fin_smem(cfg, P.W, P.sort_n, keyed);
+#ifdef ABMX_FIN_SMEM_PAD  // occupancy experiments only (tools/fin_nt_sweep.sh)
+        smem += ABMX_FIN_SMEM_PAD;
+#endif
     }
     int check_err() {  // after a stream sync
         int e = 0;
@@ -672,6 +776,7 @@ struct abmx_finance {
             const long long bound = age < P.cap ? c.traders * (age + 1) : P.cap;  // no overflow: T, cap <= 4096
             window = static_cast<int>(bound < P.cap ? (bound > 1 ? bound : 1) : P.cap);
             if (window > P.cap) window = P.cap;
+            P.id_span = c.traders * (age + 1);  // ids handed out while an order stays alive
         }
         P.p_order = c.p_order;
         P.delta = c.delta;
@@ -752,7 +857,7 @@ struct abmx_finance {
             if (t0 <= last_t) windowed = false;
             last_t = t0 + steps - 1;
         }
-        const bool keyed = windowed && !match_only && keyed_ok;
+        const bool keyed = windowed && !match_only && keyed_ok && compact_fits(t0, steps);
         set_window(windowed && !match_only, keyed);
         (void)cudaGetLastError();
         const unsigned grid = match_only ? 1u : static_cast<unsigned>(M * P.K);
