@@ -181,9 +181,16 @@ __device__ __forceinline__ void set_order(const Smem& S, int i, long long id, in
 // (side, price) is the packed key, and ids -- unique, handed out in placement order -- order
 // (placed, id) on their own.
 template <bool kKeyed>
+__device__ __forceinline__ bool before_live(const Smem& S, unsigned short a, unsigned short b);
+template <bool kKeyed>
 __device__ __forceinline__ bool before(const Smem& S, unsigned short a, unsigned short b) {
     if (b == kPad) return a != kPad;
     if (a == kPad) return false;
+    return before_live<kKeyed>(S, a, b);
+}
+// before() for two live orders (no padding entries: the merge's ranks and binary searches)
+template <bool kKeyed>
+__device__ __forceinline__ bool before_live(const Smem& S, unsigned short a, unsigned short b) {
     if constexpr (kKeyed) {
         const unsigned long long ka = S.key[a], kb = S.key[b];
         return ka != kb ? ka < kb : S.id32[a] < S.id32[b];
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                 for (int j = tid; j < spawned; j += kNT) {
                     const unsigned short x = S.nl[j];
                     int rk = 0;
-                    for (int y = 0; y < spawned; ++y) rk += before<kKeyed>(S, S.nl[y], x);
+                    for (int y = 0; y < spawned; ++y) rk += before_live<kKeyed>(S, S.nl[y], x);
                     S.nsr[rk] = x;
                 }
                 __syncthreads();
@@ -407,7 +414,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     int lo = 0, hi = spawned;  // new orders before a
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (before<kKeyed>(S, S.nsr[mid], a))
+                        if (before_live<kKeyed>(S, S.nsr[mid], a))
                             lo = mid + 1;
                         else
                             hi = mid;
@@ -419,7 +426,7 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                     int lo = 0, hi = n;  // resting orders before b
                     while (lo < hi) {
                         const int mid = (lo + hi) >> 1;
-                        if (before<kKeyed>(S, L[mid], b))
+                        if (before_live<kKeyed>(S, L[mid], b))
                             lo = mid + 1;
                         else
                             hi = mid;
@@ -464,14 +471,25 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
             long long vmax = 0;
             if (nbuy > 0 && nsell > 0)
                 for (int i = tid; i < nbuy; i += kNT) {
-                    const double bp = o_price<kKeyed>(S, L[i]);
                     int lo = 0, hi = nsell;  // first sell with price > bp
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (bp < o_price<kKeyed>(S, L[nbuy + mid]))
-                            hi = mid;
-                        else
-                            lo = mid + 1;
+                    if constexpr (kKeyed) {  // sells' keys are 2^63 | bits(price): compare keys
+                        const unsigned long long kb = (1ULL << 63) | (~S.key[L[i]] & 0x7FFFFFFFFFFFFFFFULL);
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (kb < S.key[L[nbuy + mid]])
+                                hi = mid;
+                            else
+                                lo = mid + 1;
+                        }
+                    } else {
+                        const double bp = S.pr[L[i]];
+                        while (lo < hi) {
+                            const int mid = (lo + hi) >> 1;
+                            if (bp < S.pr[L[nbuy + mid]])
+                                hi = mid;
+                            else
+                                lo = mid + 1;
+                        }
                     }
                     if (lo == 0) continue;
                     const long long bc = o_cum<kKeyed>(S, i), sc = o_cum<kKeyed>(S, nbuy + lo - 1) - btot;
