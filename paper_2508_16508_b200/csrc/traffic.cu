@@ -1,26 +1,26 @@
 // traffic.cu — the three-lane traffic model (src/models/traffic.cpp:47-238) on sm_100a for R
 // roads at once, device-resident state, bit-exact with the reference.
 //
-// A step is four kernels:
-//   k_propose  per car slot: the proposal (traffic.cpp:47-80: forward / forward-left /
-//              forward-right drawn from seed.split(6).split(t).draw(slot); exit column: exit iff
-//              green, no draw) and the per-target-cell priority bid (traffic.cpp:95-124:
-//              same lane > from the left lane > from the right lane) as one 64-bit atomicMax of
-//              {epoch, ~(prio, slot)} — prios into one cell are distinct, so the max is the winner.
-//   k_accept   per column: the acceptance fixed point (traffic.cpp:124-138). A winner enters once
-//              its target is empty or its occupant moves out; targets are always one column to the
-//              right, so the acceptance bits of column c are a function of those of column c+1:
-//              F_c : {0,1}^3 -> {0,1}^3 (an 8-entry table of 3-bit values, 24 bits). The fixed point
-//              is the suffix composition F_c ∘ F_{c+1} ∘ ... ∘ F_{L-1} (F_{L-1} is constant: exits),
-//              computed as a single-pass scan with decoupled lookback from the road's end.
+// A step is three kernels:
+//   k_accept   per column, all three lanes: each car's proposal (traffic.cpp:47-80: forward /
+//              forward-left / forward-right drawn from seed.split(6).split(t).draw(slot); exit
+//              column: exit iff green, no draw) and the conflict winner of its target
+//              (traffic.cpp:95-124: same lane > from the left lane > from the right lane). Every
+//              bidder for a cell of column c+1 sits in column c, so the winner needs no global
+//              bids. Then the acceptance fixed point (traffic.cpp:124-138): a winner enters once
+//              its target is empty or its occupant moves out; the acceptance bits of column c
+//              are a function of those of column c+1, F_c : {0,1}^3 -> {0,1}^3 (three 3-bit lane
+//              modes), and the fixed point is the suffix composition F_c ∘ ... ∘ F_{L-1}
+//              (F_{L-1} is constant: exits), a single-pass scan with decoupled lookback from the
+//              road's end. Accepted winners tag the cell they enter (inc words, per epoch).
 //   k_apply    per car slot: accepted moves (set_agents_mask) and exits (remove_agents), the new
-//              occupancy written by the movers themselves (a vacated cell is cleared unless an
-//              accepted winner enters it), and per-tile first free slots for the spawn.
+//              occupancy written by the movers themselves (a vacated cell is cleared unless its
+//              inc word carries this epoch's tag), and per-tile first free slots for the spawn.
 //   k_spawn    per road: spawn_cars (traffic.cpp:143-184): k = uniform_int(0, 0, 4), partial lane
 //              shuffle, entry cells that are free, rank-match into the lowest free slots, fresh ids.
 //
-// Layout per road r (capacity 3L slots, 3L cells): active u8, pos i32 (= lane*L + cell), ids i64,
-// ages i64; occupancy i32 (slot or -1), bid u64, acc u8 per cell.
+// Layout per road r (capacity 3L slots, 3L cells): active u8, pos i32 (= lane*Lp + cell), ids i64,
+// ages i64; occupancy i32 (slot or -1), inc u32, acc u8 per cell.
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -48,7 +48,7 @@ constexpr int kAcceptMaxNT = ABMX_TRF_NA_MAX;  // k_accept CTA size for long roa
 constexpr unsigned kSlotMask = (1u << 28) - 1;
 constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagPre = 2ULL << 62;
-constexpr int kNumKernels = 4;
+constexpr int kNumKernels = 3;  // k_accept, k_apply, k_spawn
 
 enum : int { kStay = -1, kExit = -2 };
 
@@ -69,10 +69,12 @@ struct TParams {
     long long* ids;
     long long* ages;
     int* occ;
-    unsigned long long* bid;
     uint8_t* acc;
     unsigned long long* cstatus;  // [R][ctiles] lookback words
     unsigned* ticket;             // [2]
+    unsigned* inc;                // [R][Cpad] inc_tag(epoch) where an accepted car enters the cell
+    int accept_ticketless;        // 1: every k_accept CTA is co-resident (one wave), so the
+                                  // lookback needs no ticket order: tile = blockIdx.x
     int4* tinfo;                  // [R][tiles] {free count, first three free slots}
     long long* cnt;               // [R][8] num_active, next_id, spawned_total, exited_total, spawned, exited, green
 };
@@ -93,6 +95,10 @@ __device__ __forceinline__ int proposal(const TParams& P, int slot, int p, bool 
     const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
     return tl * P.Lp + cell + 1;
 }
+// tag of an accepted entry into a cell this epoch (never 0, the initial word)
+__device__ __forceinline__ unsigned inc_tag(unsigned long long epoch) {
+    return 0x80000000u | static_cast<unsigned>(epoch & 0x7FFFFFFFULL);
+}
 __device__ __forceinline__ unsigned long long bid_word(unsigned long long epoch, int prio, int slot) {
     return (epoch << 32) | (0xFFFFFFFFu - ((static_cast<unsigned>(prio) << 28) | static_cast<unsigned>(slot)));
 }
@@ -103,27 +109,6 @@ __device__ __forceinline__ bool bid_winner(unsigned long long w, unsigned long l
     slot = static_cast<int>(v & kSlotMask);
     prio = static_cast<int>(v >> 28);
     return true;
-}
-
-// ---------------------------------------------------------------- k_propose
-template <int NT>
-__global__ void __launch_bounds__(NT) k_propose(TParams P) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.ticket[P.epoch & 1] = 0u;
-    const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
-    const bool green = green_of(P, r);
-    const unsigned long long key = propose_key(P, r);
-    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
-#pragma unroll
-    for (int k = 0; k < kS; ++k) {
-        const int i = tile * NT * kS + k * NT + threadIdx.x;
-        if (i >= P.C || !P.active[sb + i]) continue;
-        const int p = P.pos[sb + i];
-        const int X = proposal(P, i, p, green, key);
-        if (X < 0) continue;
-        const int lane = p / P.Lp, tl = X / P.Lp;
-        const int prio = lane == tl ? 0 : (lane == tl - 1 ? 1 : 2);
-        atomicMax(&P.bid[cb + X], bid_word(P.epoch, prio, i));
-    }
 }
 
 // ---------------------------------------------------------------- k_accept
@@ -157,7 +142,8 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __shared__ unsigned s_warp[NA / 32];
     __shared__ unsigned s_vin;
     // tiles of one road depend on their right neighbours: ticket order guarantees progress
-    if (threadIdx.x == 0) s_tile = P.ctiles > 1 ? atomicAdd(&P.ticket[P.epoch & 1], 1u) : blockIdx.x;
+    if (threadIdx.x == 0)
+        s_tile = P.ctiles > 1 && !P.accept_ticketless ? atomicAdd(&P.ticket[P.epoch & 1], 1u) : blockIdx.x;
     __syncthreads();
     const unsigned g = s_tile;
     const int r = static_cast<int>(g / P.ctiles), tau = static_cast<int>(g % P.ctiles);
@@ -178,26 +164,29 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         o[l][2] = v4.z;
         o[l][3] = v4.w;
     }
-    // proposals (no memory), then every bid word, then the targets' occupants: three batched
-    // rounds of independent loads instead of a dependent chain per column
+    // proposals (no memory). Every bidder for a cell of column c+1 sits in column c, which this
+    // thread holds in all three lanes, so the conflict winner (same lane > from the left > from
+    // the right, traffic.cpp:95-124) is decided here without bid words; then the targets'
+    // occupants, one batched round of independent loads
     int X[3][kCI];
 #pragma unroll
     for (int l = 0; l < 3; ++l)
 #pragma unroll
         for (int q = 0; q < kCI; ++q)
             X[l][q] = o[l][q] >= 0 ? proposal(P, o[l][q], l * P.Lp + c_lo + q, green, key) : kStay;
-    unsigned long long bw[3][kCI];
+    int ox[3][kCI];  // occupant of the target if this car won it, else kStay - 1 (lost / no move)
 #pragma unroll
-    for (int l = 0; l < 3; ++l)
+    for (int q = 0; q < kCI; ++q)
 #pragma unroll
-        for (int q = 0; q < kCI; ++q) bw[l][q] = X[l][q] >= 0 ? P.bid[cb + X[l][q]] : 0ULL;
-    int ox[3][kCI];  // occupant of the target if this car won it, else kStay (lost / no move)
+        for (int l = 0; l < 3; ++l) {
+            bool won = X[l][q] >= 0;
+            if (won) {
+                const int tl = X[l][q] / P.Lp;
+                const int pr = l == tl ? 0 : (l == tl - 1 ? 1 : 2);
 #pragma unroll
-    for (int l = 0; l < 3; ++l)
-#pragma unroll
-        for (int q = 0; q < kCI; ++q) {
-            int ws, wp;
-            const bool won = X[l][q] >= 0 && bid_winner(bw[l][q], P.epoch, ws, wp) && ws == o[l][q];
+                for (int l2 = 0; l2 < 3; ++l2)
+                    if (l2 != l && X[l2][q] == X[l][q] && (l2 == tl ? 0 : (l2 == tl - 1 ? 1 : 2)) < pr) won = false;
+            }
             ox[l][q] = won ? P.occ[cb + X[l][q]] : kStay - 1;
         }
     unsigned F[kCI];
@@ -299,9 +288,14 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         const unsigned m3 = (occm >> (3 * j)) & 7u;
         if (m3) {
             const int c = c_lo + kCI - 1 - j;
+            const int q = kCI - 1 - j;
 #pragma unroll
             for (int l = 0; l < 3; ++l)
-                if (m3 & (1u << l)) P.acc[cb + l * P.Lp + c] = static_cast<uint8_t>((v >> l) & 1u);
+                if (m3 & (1u << l)) {
+                    const unsigned a = (v >> l) & 1u;
+                    P.acc[cb + l * P.Lp + c] = static_cast<uint8_t>(a);
+                    if (a && X[l][q] >= 0) P.inc[cb + X[l][q]] = inc_tag(P.epoch);  // the winner enters
+                }
         }
     }
 }
@@ -309,13 +303,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
 // ---------------------------------------------------------------- k_apply
 // Clear the occupancy of vacated cell p unless an accepted winner enters it this step.
 __device__ __forceinline__ void vacate(const TParams& P, size_t cb, int p) {
-    int ws, wp;
-    if (bid_winner(P.bid[cb + p], P.epoch, ws, wp)) {
-        const int lane = p / P.Lp;
-        const int src_lane = wp == 0 ? lane : (wp == 1 ? lane - 1 : lane + 1);
-        const int src = src_lane * P.Lp + (p - lane * P.Lp) - 1;
-        if (P.acc[cb + src]) return;  // the winner writes occ[p]
-    }
+    if (P.inc[cb + p] == inc_tag(P.epoch)) return;  // the accepted winner writes occ[p]
     P.occ[cb + p] = -1;
 }
 
@@ -386,6 +374,7 @@ __global__ void __launch_bounds__(NT) k_apply(TParams P) {
 __global__ void k_spawn(TParams P) {
     const int r = blockIdx.x;
     const int lane = threadIdx.x;
+    if (r == 0 && lane == 0) P.ticket[(P.epoch + 1) & 1] = 0u;  // the next step's k_accept tickets
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
     long long* cn = P.cnt + static_cast<size_t>(r) * 8;
     // every load the spawn needs that does not depend on the draws, issued together: the seed,
@@ -508,7 +497,7 @@ __global__ void k_init(TParams P) {
         }
         if (q < nc) {
             P.occ[q] = -1;
-            P.bid[q] = 0ULL;
+            P.inc[q] = 0u;
             P.acc[q] = 0;
         }
     }
@@ -566,15 +555,15 @@ struct abmx_traffic {
         allocs.push_back(*p);
         return ABMX_OK;
     }
-    unsigned grid(int k) const {
-        if (k == 1) return static_cast<unsigned>(R * P.ctiles);
-        if (k == 3) return static_cast<unsigned>(R);
+    unsigned grid(int k) const {  // k: 0 k_accept, 1 k_apply, 2 k_spawn
+        if (k == 0) return static_cast<unsigned>(R * P.ctiles);
+        if (k == 2) return static_cast<unsigned>(R);
         return static_cast<unsigned>(R * P.tiles);
     }
     int nt = 256, na = 1024;  // CTA sizes of the slot kernels and of k_accept
     void* fns[kNumKernels] = {};
     unsigned block(int k) const {
-        return k == 3 ? 32u : static_cast<unsigned>(k == 1 ? na : nt);
+        return k == 2 ? 32u : static_cast<unsigned>(k == 0 ? na : nt);
     }
     void* fn(int k) const { return fns[k]; }
     void pick_kernels() {
@@ -585,20 +574,20 @@ struct abmx_traffic {
         na = 32;
         while (na < kAcceptMaxNT && na * kCI < P.Lp) na *= 2;
         switch (nt) {
-            case 32: fns[0] = reinterpret_cast<void*>(k_propose<32>); fns[2] = reinterpret_cast<void*>(k_apply<32>); break;
-            case 64: fns[0] = reinterpret_cast<void*>(k_propose<64>); fns[2] = reinterpret_cast<void*>(k_apply<64>); break;
-            case 128: fns[0] = reinterpret_cast<void*>(k_propose<128>); fns[2] = reinterpret_cast<void*>(k_apply<128>); break;
-            default: fns[0] = reinterpret_cast<void*>(k_propose<256>); fns[2] = reinterpret_cast<void*>(k_apply<256>); break;
+            case 32: fns[1] = reinterpret_cast<void*>(k_apply<32>); break;
+            case 64: fns[1] = reinterpret_cast<void*>(k_apply<64>); break;
+            case 128: fns[1] = reinterpret_cast<void*>(k_apply<128>); break;
+            default: fns[1] = reinterpret_cast<void*>(k_apply<256>); break;
         }
         switch (na) {
-            case 32: fns[1] = reinterpret_cast<void*>(k_accept<32>); break;
-            case 64: fns[1] = reinterpret_cast<void*>(k_accept<64>); break;
-            case 128: fns[1] = reinterpret_cast<void*>(k_accept<128>); break;
-            case 256: fns[1] = reinterpret_cast<void*>(k_accept<256>); break;
-            case 512: fns[1] = reinterpret_cast<void*>(k_accept<512>); break;
-            default: fns[1] = reinterpret_cast<void*>(k_accept<1024>); break;
+            case 32: fns[0] = reinterpret_cast<void*>(k_accept<32>); break;
+            case 64: fns[0] = reinterpret_cast<void*>(k_accept<64>); break;
+            case 128: fns[0] = reinterpret_cast<void*>(k_accept<128>); break;
+            case 256: fns[0] = reinterpret_cast<void*>(k_accept<256>); break;
+            case 512: fns[0] = reinterpret_cast<void*>(k_accept<512>); break;
+            default: fns[0] = reinterpret_cast<void*>(k_accept<1024>); break;
         }
-        fns[3] = reinterpret_cast<void*>(k_spawn);
+        fns[2] = reinterpret_cast<void*>(k_spawn);
     }
 
     int create(const abmx_traffic_config& c, const uint64_t* seeds, int roads) {
@@ -633,6 +622,13 @@ struct abmx_traffic {
         P.Npad = (P.C + P.tile_slots - 1) / P.tile_slots * P.tile_slots;
         P.tiles = P.Npad / P.tile_slots;
         P.ctiles = (P.Lp + P.tile_cols - 1) / P.tile_cols;
+        {
+            int per_sm = 0;  // k_accept CTAs resident per SM
+            if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fns[0], na, 0) != cudaSuccess) per_sm = 0;
+            (void)cudaGetLastError();
+            P.accept_ticketless =
+                static_cast<long long>(R) * P.ctiles <= static_cast<long long>(per_sm) * abmx_internal::num_sms() ? 1 : 0;
+        }
         P.period = c.period;
         long long gl = llround(static_cast<double>(c.period) * c.green_fraction);  // traffic.cpp:11-13
         P.green_len = gl < 0 ? 0 : (gl > c.period ? c.period : gl);
@@ -646,7 +642,7 @@ struct abmx_traffic {
         ALT(P.ids, ns * 8);
         ALT(P.ages, ns * 8);
         ALT(P.occ, nc * 4);
-        ALT(P.bid, nc * 8);
+        ALT(P.inc, nc * 4);
         ALT(P.acc, nc);
         ALT(P.cstatus, static_cast<size_t>(R) * P.ctiles * 8);
         ALT(P.ticket, 16);
@@ -915,7 +911,7 @@ struct abmx_traffic {
 };
 
 namespace {
-const char* kTrafficKernels[kNumKernels] = {"k_propose", "k_accept", "k_apply", "k_spawn"};
+const char* kTrafficKernels[kNumKernels] = {"k_accept", "k_apply", "k_spawn"};
 
 int resolve_host(int64_t length, const uint8_t* active, const int64_t* lane, const int64_t* cell, const uint8_t* kind,
                  const int64_t* to_lane, const int64_t* to_cell, uint8_t* accepted) {
