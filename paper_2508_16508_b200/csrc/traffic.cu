@@ -73,16 +73,20 @@ struct TParams {
     unsigned long long* cstatus;  // [R][ctiles] lookback words
     unsigned* ticket;             // [2]
     unsigned* inc;                // [R][Cpad] inc_tag(epoch) where an accepted car enters the cell
+    int spawn_pending;            // 1: k_accept's column-0 tile first runs the PREVIOUS step's
+    long long spawn_t;            //    spawn (step spawn_t, metrics row spawn_row), which a
+    unsigned spawn_row;           //    multi-step run folds into the next step (no k_spawn launch)
     int accept_ticketless;        // 1: every k_accept CTA is co-resident (one wave), so the
                                   // lookback needs no ticket order: tile = blockIdx.x
     int4* tinfo;                  // [R][tiles] {free count, first three free slots}
     long long* cnt;               // [R][8] num_active, next_id, spawned_total, exited_total, spawned, exited, green
 };
 
-__device__ __forceinline__ bool green_of(const TParams& P, int r) {  // SignalSchedule::green
-    const long long m = ((P.t + P.phase[r]) % P.period + P.period) % P.period;
+__device__ __forceinline__ bool green_at(const TParams& P, int r, long long t) {  // SignalSchedule::green
+    const long long m = ((t + P.phase[r]) % P.period + P.period) % P.period;
     return m < P.green_len;
 }
+__device__ __forceinline__ bool green_of(const TParams& P, int r) { return green_at(P, r, P.t); }
 __device__ __forceinline__ unsigned long long propose_key(const TParams& P, int r) {
     return split(split(P.seeds[r], 6), static_cast<unsigned long long>(P.t));  // TrafficPropose
 }
@@ -136,6 +140,8 @@ __device__ __forceinline__ unsigned apply_fn(unsigned f, unsigned v) {  // f(v),
     return out;
 }
 
+__device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, int lane);  // (below)
+
 template <int NA>
 __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __shared__ unsigned s_tile;
@@ -147,6 +153,11 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __syncthreads();
     const unsigned g = s_tile;
     const int r = static_cast<int>(g / P.ctiles), tau = static_cast<int>(g % P.ctiles);
+    if (P.spawn_pending && tau == P.ctiles - 1) {  // the tile holding column 0: the previous
+        if (threadIdx.x < 32)                       // step's spawn first (its entrance cells)
+            spawn_road(P, r, P.spawn_t, P.spawn_row, static_cast<int>(threadIdx.x));
+        __syncthreads();
+    }
     // tile 0 holds the road's last columns; columns L..Lp-1 are empty padding (-1)
     const int hi = P.Lp - tau * NA * kCI;
     const bool green = green_of(P, r);
@@ -309,6 +320,7 @@ __device__ __forceinline__ void vacate(const TParams& P, size_t cb, int p) {
 
 template <int NT>
 __global__ void __launch_bounds__(NT) k_apply(TParams P) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) P.ticket[(P.epoch + 1) & 1] = 0u;  // the next k_accept's tickets
     __shared__ unsigned long long s_scan[NT / 32 + 1];
     __shared__ int s_first[3];
     __shared__ unsigned s_exit[NT / 32];
@@ -371,10 +383,8 @@ __global__ void __launch_bounds__(NT) k_apply(TParams P) {
 
 // ---------------------------------------------------------------- k_spawn
 // One warp per road: spawn_cars (traffic.cpp:143-184), counters and the metrics row.
-__global__ void k_spawn(TParams P) {
-    const int r = blockIdx.x;
-    const int lane = threadIdx.x;
-    if (r == 0 && lane == 0) P.ticket[(P.epoch + 1) & 1] = 0u;  // the next step's k_accept tickets
+// spawn_cars of step t on road r, one warp (lane = 0..31); metrics row `row`
+__device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, int lane) {
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
     long long* cn = P.cnt + static_cast<size_t>(r) * 8;
     // every load the spawn needs that does not depend on the draws, issued together: the seed,
@@ -383,12 +393,12 @@ __global__ void k_spawn(TParams P) {
     const int occ_in[3] = {P.occ[cb], P.occ[cb + P.Lp], P.occ[cb + 2 * static_cast<size_t>(P.Lp)]};
     int4 ti0 = lane < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + lane] : make_int4(0, -1, -1, -1);
     const long long nid = cn[1], exited = cn[5], c0 = cn[0], c2 = cn[2], c3 = cn[3];
-    const bool g = green_of(P, r);
+    const bool g = green_at(P, r, t);
     // rows (lane 0): k attempts, partial shuffle, free entry cells
     int rows[3] = {-1, -1, -1};
     int nvalid = 0;
     {
-        const unsigned long long key = split(split(seed, 7), static_cast<unsigned long long>(P.t));
+        const unsigned long long key = split(split(seed, 7), static_cast<unsigned long long>(t));
         const int k = static_cast<int>(uniform_span(key, 0, 4));
         int lanes[3] = {0, 1, 2};
         for (int i = 0; i < (k < 2 ? k : 2); ++i) {
@@ -437,14 +447,16 @@ __global__ void k_spawn(TParams P) {
         cn[3] = c3 + exited;
         cn[4] = spawned;
         cn[6] = g ? 1 : 0;
-        double* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.run_step) * 4;
-        row[0] = static_cast<double>(n_cars);
-        row[1] = static_cast<double>(spawned);
-        row[2] = static_cast<double>(exited);
-        row[3] = g ? 1.0 : 0.0;
+        double* mrow = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + row) * 4;
+        mrow[0] = static_cast<double>(n_cars);
+        mrow[1] = static_cast<double>(spawned);
+        mrow[2] = static_cast<double>(exited);
+        mrow[3] = g ? 1.0 : 0.0;
         cn[5] = 0;  // exits of the next step accumulate from zero
     }
 }
+
+__global__ void k_spawn(TParams P) { spawn_road(P, blockIdx.x, P.t, P.run_step, threadIdx.x); }
 
 // ---------------------------------------------------------------- resolve_conflicts (explicit)
 // General proposals (any in-road target): acceptance is the least fixed point of
@@ -540,6 +552,8 @@ struct abmx_traffic {
     ~abmx_traffic() {
         if (exec) cudaGraphExecDestroy(exec);
         if (graph) cudaGraphDestroy(graph);
+        if (exec2) cudaGraphExecDestroy(exec2);
+        if (graph2) cudaGraphDestroy(graph2);
         for (void* p : allocs) cudaFree(p);
         if (d_run_metrics) cudaFree(d_run_metrics);
         if (flush_buf) cudaFree(flush_buf);
@@ -680,6 +694,64 @@ struct abmx_traffic {
         return ABMX_OK;
     }
 
+    // the folded step of a multi-step run: [k_accept (+ the previous step's spawn), k_apply]
+    cudaGraph_t graph2 = nullptr;
+    cudaGraphExec_t exec2 = nullptr;
+    cudaGraphNode_t nodes2[2] = {};
+    int build_graph2() {
+        CKT(cudaGraphCreate(&graph2, 0));
+        void* args[1] = {&P};
+        cudaGraphNode_t prev = nullptr;
+        for (int k = 0; k < 2; ++k) {
+            cudaKernelNodeParams kp{};
+            kp.func = fn(k);
+            kp.gridDim = dim3(grid(k));
+            kp.blockDim = dim3(block(k));
+            kp.kernelParams = args;
+            CKT(cudaGraphAddKernelNode(&nodes2[k], graph2, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
+            prev = nodes2[k];
+        }
+        CKT(cudaGraphInstantiate(&exec2, graph2, 0));
+        return ABMX_OK;
+    }
+    // one step of a multi-step run: the spawn of step q-1 rides in step q's k_accept
+    int enqueue_folded(bool pending) {
+        P.epoch = host_epoch;
+        P.spawn_pending = pending ? 1 : 0;
+        P.spawn_t = P.t - 1;
+        P.spawn_row = P.run_step - 1;
+        if (!exec2) {
+            int rc = build_graph2();
+            if (rc) return rc;
+        }
+        void* args[1] = {&P};
+        for (int k = 0; k < 2; ++k) {
+            cudaKernelNodeParams kp{};
+            kp.func = fn(k);
+            kp.gridDim = dim3(grid(k));
+            kp.blockDim = dim3(block(k));
+            kp.kernelParams = args;
+            CKT(cudaGraphExecKernelNodeSetParams(exec2, nodes2[k], &kp));
+        }
+        CKT(cudaGraphLaunch(exec2, stream));
+        P.spawn_pending = 0;
+        abmx_internal::count_launch(2);
+        ++host_epoch;
+        ++P.t;
+        ++P.run_step;
+        return ABMX_OK;
+    }
+    // the last step's spawn of a folded run
+    int spawn_last() {
+        TParams Q = P;
+        Q.t = P.t - 1;
+        Q.run_step = P.run_step - 1;
+        Q.epoch = host_epoch - 1;
+        void* args[1] = {&Q};
+        CKT(cudaLaunchKernel(fn(2), dim3(grid(2)), dim3(block(2)), args, 0, stream));
+        abmx_internal::count_launch(1);
+        return ABMX_OK;
+    }
     int build_graph() {
         CKT(cudaGraphCreate(&graph, 0));
         void* args[1] = {&P};
@@ -766,9 +838,11 @@ struct abmx_traffic {
         if (rc) return rc;
         (void)cudaGetLastError();
         for (long long q = 0; q < steps; ++q) {
-            rc = enqueue(nullptr);
+            rc = enqueue_folded(q > 0);
             if (rc) return rc;
         }
+        rc = spawn_last();
+        if (rc) return rc;
         last_run_steps = steps;
         if (out) {
             CKT(cudaMemcpyAsync(out, d_run_metrics, static_cast<size_t>(R) * steps * 32, cudaMemcpyDeviceToHost, stream));
@@ -879,9 +953,10 @@ struct abmx_traffic {
             cudaEvent_t* e = &ev[per * static_cast<size_t>(q)];
             if (per_kernel) {
                 rc = enqueue(e);
-            } else {
+            } else {  // the folded run step (the last one also takes its own spawn)
                 CKT(cudaEventRecord(e[0], stream));
-                rc = enqueue(nullptr);
+                rc = enqueue_folded(q > 0);
+                if (!rc && q == steps - 1) rc = spawn_last();
                 CKT(cudaEventRecord(e[1], stream));
             }
             if (rc) return rc;
