@@ -86,9 +86,9 @@ enum SelMode { kSelMask = 0, kSelFree = 1, kSelKill = 2 };
 // list[k] = k-th selected index in ascending order; *count = number selected (last tile).
 //   kSelMask: mask[i] != 0      kSelFree: active[i] == 0      kSelKill: active[i] && mask[i]
 template <int kMode>
-__global__ void __launch_bounds__(kT) k_select(const uint8_t* __restrict__ mask, const uint8_t* __restrict__ active,
-                                               size_t n, int32_t* __restrict__ list, long long* __restrict__ count,
-                                               ScanWs* ws) {
+__device__ __forceinline__ void select_tile(const uint8_t* __restrict__ mask, const uint8_t* __restrict__ active,
+                                            size_t n, int32_t* __restrict__ list, long long* __restrict__ count,
+                                            ScanWs* ws, unsigned tiles) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ unsigned s_tile;
     __shared__ unsigned long long s_look[kT / 32 + 2];
@@ -115,7 +115,26 @@ __global__ void __launch_bounds__(kT) k_select(const uint8_t* __restrict__ mask,
 #pragma unroll
     for (int k = 0; k < kItems; ++k)
         if (sel[k]) list[pos++] = static_cast<int32_t>(base + k);
-    if (tile == gridDim.x - 1 && threadIdx.x == 0) *count = static_cast<long long>(pre + total);
+    if (tile == tiles - 1 && threadIdx.x == 0) *count = static_cast<long long>(pre + total);
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(kT) k_select(const uint8_t* __restrict__ mask, const uint8_t* __restrict__ active,
+                                               size_t n, int32_t* __restrict__ list, long long* __restrict__ count,
+                                               ScanWs* ws) {
+    select_tile<kMode>(mask, active, n, list, count, ws, gridDim.x);
+}
+
+// spawn_agents' two independent selections in one launch: the free slots (blocks [0, ta)) and
+// the valid rows (blocks [ta, ta + tb)), each with its own ticket counter and lookback words
+__global__ void __launch_bounds__(kT) k_select_spawn(const uint8_t* __restrict__ active, size_t n,
+                                                     int32_t* __restrict__ slots, long long* cnt_slots, ScanWs* wa,
+                                                     unsigned ta, const uint8_t* __restrict__ valid, size_t m,
+                                                     int32_t* __restrict__ rows, long long* cnt_rows, ScanWs* wb) {
+    if (blockIdx.x < ta)
+        select_tile<kSelFree>(nullptr, active, n, slots, cnt_slots, wa, ta);
+    else
+        select_tile<kSelMask>(valid, nullptr, m, rows, cnt_rows, wb, gridDim.x - ta);
 }
 
 struct Life {  // lifecycle fields of a set (agent_set.hpp:15-77)
@@ -497,14 +516,31 @@ int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int3
     CKA(sc.get(reinterpret_cast<void**>(&cnt), 2 * sizeof(long long)));
     if (!slots) CKA(sc.get(reinterpret_cast<void**>(&slots), n * 4));
     if (!rws) CKA(sc.get(reinterpret_cast<void**>(&rws), static_cast<size_t>(m) * 4));
-    if (spawn)
-        rc = select_list<kSelFree>(nullptr, s->active, n, slots, cnt, sc);
-    else
-        rc = select_list<kSelMask>(d_target, nullptr, n, slots, cnt, sc);
-    if (rc) return rc;
-    unsigned* done = nullptr;  // the pad word of the second scan's workspace: a zeroed counter
-    rc = select_list<kSelMask>(d_valid, nullptr, static_cast<size_t>(m), rws, cnt + 1, sc, &done);
-    if (rc) return rc;
+    unsigned* done = nullptr;  // the pad word of the (second) scan's workspace: a zeroed counter
+    if (spawn && n > 0 && m > 0) {  // both selections in one launch, one workspace memset
+        const size_t ta = (n + kTile - 1) / kTile, tb = (static_cast<size_t>(m) + kTile - 1) / kTile;
+        const size_t wa_b = (sizeof(ScanWs) + ta * sizeof(unsigned long long) + 15) / 16 * 16;
+        const size_t wb_b = sizeof(ScanWs) + tb * sizeof(unsigned long long);
+        void* ws = nullptr;
+        CKA(sc.get(&ws, wa_b + wb_b));
+        CKA(cudaMemsetAsync(ws, 0, wa_b + wb_b, st));
+        ScanWs* wa = static_cast<ScanWs*>(ws);
+        ScanWs* wb = reinterpret_cast<ScanWs*>(static_cast<char*>(ws) + wa_b);
+        k_select_spawn<<<static_cast<unsigned>(ta + tb), kT, 0, st>>>(s->active, n, slots, cnt, wa,
+                                                                       static_cast<unsigned>(ta), d_valid,
+                                                                       static_cast<size_t>(m), rws, cnt + 1, wb);
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        done = &wb->pad;
+    } else {
+        if (spawn)
+            rc = select_list<kSelFree>(nullptr, s->active, n, slots, cnt, sc);
+        else
+            rc = select_list<kSelMask>(d_target, nullptr, n, slots, cnt, sc);
+        if (rc) return rc;
+        rc = select_list<kSelMask>(d_valid, nullptr, static_cast<size_t>(m), rws, cnt + 1, sc, &done);
+        if (rc) return rc;
+    }
     bool committed = false;
     const Life L = life_of(s);
     const size_t pairs_max = n < static_cast<size_t>(m) ? n : static_cast<size_t>(m);
