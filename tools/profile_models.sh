@@ -3,7 +3,7 @@
 TAG=${1:-r01}
 mkdir -p gpurun_out
 python tools/prof_traffic_ncu.py c4 > /dev/null && \
-ncu --set full --clock-control none --import-source on -k regex:"k_propose|k_accept|k_apply|k_spawn" -s 40 -c 4 \
+ncu --set full --clock-control none --import-source on -k regex:"k_accept|k_apply|k_spawn" -s 39 -c 3 \
     -o gpurun_out/trf_c4_$TAG python tools/prof_traffic_ncu.py c4 > gpurun_out/ncu_trf_c4_$TAG.log 2>&1; echo c4_rc=$?
 python tools/prof_traffic_ens.py 100 > /dev/null && \
 ncu --set full --clock-control none --import-source on -k regex:"k_traffic_ens" -c 1 \
