@@ -17,8 +17,10 @@ The line also carries the C3 ensemble (4096 x C1 replicas, sharded over the rank
              / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
   cpu_baseline  the reference's own C++ step_predation (oracle/_ref, -O3) on this host
   ensemble / traffic / finance   secondary sections: device times of
-             the C3 ensemble, the C4 road and roads variant, the C5 markets, each with the
-             reference's own CPU run on a bounded sample
+             the C3 ensemble, the C4 road and roads variant, the C5 markets (and the one-market
+             reading), each with the reference's own CPU run on a bounded sample
+  agents     the generic lifecycle (remove_agents + spawn_agents) on a
+             C2-sized set, bit-compared with the reference's own remove/spawn on the same inputs
 
 `--impl reference` times the reference CPU implementation (oracle/_ref) on the same workload.
 """
