@@ -369,3 +369,20 @@ def test_long_runs_cross_epoch_wraparounds(abmx, oracle, cfgname):
         orc.step(t)
         assert gpu.collect_metrics()[0].tolist() == orc.metrics(), (cfgname, t)
     assert_same_state(gpu, orc, f"{cfgname} t=700")
+
+
+def test_c1_soak_10000_steps(abmx, oracle):
+    """C1 for 10,000 steps in chunks of run() (the cell words cleared 78 times, the 8-bit list
+    and lowest-slot tags wrapping dozens of times, the due ring cycling): every metrics row
+    and the final state equal the oracle."""
+    seed = abmx.replica_seeds(13, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, c1(), seed)
+    t = 1
+    for chunk in (1000, 2500, 37, 3463, 3000):
+        rows = gpu.run(t, chunk)[0]
+        for q in range(chunk):
+            orc.step(t + q)
+            assert rows[q].astype(np.int64).tolist() == orc.metrics(), t + q
+        t += chunk
+    assert t == 10001
+    assert_same_state(gpu, orc, "c1 t=10000")
