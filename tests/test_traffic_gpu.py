@@ -233,3 +233,27 @@ def test_long_traffic_runs(T, oracle, path):
     """2000 steps: epoch-tagged bids and lookback words, id growth, signal phases."""
     rows, _ = T.run_batch(T.TrafficConfig(40, 7, 0.4), 23, 6, 2000, path=path)
     assert np.array_equal(rows, oracle.traffic_run_batch(40, 7, 0.4, 23, 6, 2000))
+
+
+def test_many_long_roads_ticket_order(T, oracle):
+    """16 roads of 100,000 cells: 16 x 25 k_accept tiles exceed one co-resident wave, so the
+    tiles take tickets for the decoupled lookback (the ticket-free path covers one wave). Every
+    road's metrics and final state equal the oracle's TrafficModel of that road."""
+    import paper_2508_16508_b200 as abmx
+    L, R, steps = 100_000, 16, 6
+    seeds = abmx.replica_seeds(21, R)
+    dev = T.TrafficModel(T.TrafficConfig(L, 10, 0.5), seeds)
+    refs = [oracle.traffic(L, 10, 0.5, int(s)) for s in seeds]
+    for t in range(1, steps + 1):
+        dev.step(t)
+        got = dev.collect_metrics()
+        for r, ref in enumerate(refs):
+            ref.step(t)
+            assert got[r].tolist() == ref.metrics().tolist(), (r, t)
+    rows = dev.run(steps + 1, 4)
+    for q in range(4):
+        for r, ref in enumerate(refs):
+            ref.step(steps + 1 + q)
+            assert rows[r, q].tolist() == ref.metrics().tolist(), (r, q)
+    for r in (0, 7, 15):
+        assert_road(dev.road(r), refs[r].export(), r)
