@@ -3,6 +3,8 @@ configurations (tests/fuzz_strategies.py), seeds and step counts. Every engine a
 is exercised: the predation per-call step and run(), the ensemble run_batch on both paths,
 traffic per-call and run_batch on both paths, finance per-call and run_batch. Refused
 configurations must be refused by both sides. Derandomised: every run draws the same examples."""
+import os
+
 import numpy as np
 import pytest
 from hypothesis import HealthCheck, given, settings
@@ -14,7 +16,8 @@ from test_predation_gpu import assert_same_events, assert_same_state
 
 pytestmark = pytest.mark.gpu
 
-FUZZ = settings(max_examples=60, deadline=None, derandomize=True, database=None,
+FUZZ = settings(max_examples=int(os.environ.get("ABMX_FUZZ_EXAMPLES", "60")), deadline=None,
+                derandomize=True, database=None,
                 suppress_health_check=[HealthCheck.function_scoped_fixture])
 
 

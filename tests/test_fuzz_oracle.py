@@ -3,6 +3,8 @@ build (oracle/_ref) on randomly drawn configurations, seeds and step sequences: 
 (events and full-state hash every step), traffic (metrics every step, final road) and finance
 (metrics every step, final books, cash as bit patterns, holdings). Derandomised, so every run
 draws the same examples."""
+import os
+
 import numpy as np
 import pytest
 from hypothesis import given, settings
@@ -11,7 +13,8 @@ from hypothesis import strategies as st
 import pyoracle
 from fuzz_strategies import finance_cfg, predation_cfg, traffic_cfg
 
-FUZZ = settings(max_examples=100, deadline=None, derandomize=True, database=None)
+FUZZ = settings(max_examples=int(os.environ.get("ABMX_FUZZ_EXAMPLES", "100")), deadline=None,
+                derandomize=True, database=None)
 
 
 def _both(make_a, make_b):
