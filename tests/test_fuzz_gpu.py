@@ -46,6 +46,14 @@ def test_predation_engine_fuzz(abmx, oracle, cfg, seed, steps):
 
 
 @FUZZ
+@given(cfg=predation_cfg(max_side=8, max_cap=700), seed=st.integers(0, 2**64 - 1), steps=st.integers(2, 16))
+def test_predation_engine_fuzz_crowded(abmx, oracle, cfg, seed, steps):
+    """Tiny grids with many slots: more slots than cells, so the pairing runs through k_cells
+    (sort-based per-cell pairing, heap sort for long lists)."""
+    test_predation_engine_fuzz.hypothesis.inner_test(abmx, oracle, cfg, seed, steps)
+
+
+@FUZZ
 @given(cfg=predation_cfg(max_side=30, max_cap=300), master=st.integers(0, 2**64 - 1),
        replicas=st.integers(1, 6), steps=st.integers(1, 30))
 def test_ensemble_fuzz(abmx, oracle, cfg, master, replicas, steps):
