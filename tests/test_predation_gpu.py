@@ -386,3 +386,22 @@ def test_c1_soak_10000_steps(abmx, oracle):
         t += chunk
     assert t == 10001
     assert_same_state(gpu, orc, "c1 t=10000")
+
+
+def test_c2_scale_25_steps_both_paths(abmx, oracle):
+    """C2 at full size for 25 steps (the bench's timed window): 10 per-call steps (events every
+    step), then 15 steps in one run(); metrics every step and the full state at the end."""
+    cfgd = c1(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000,
+              sheep_capacity=524288, wolf_capacity=524288)
+    seed = abmx.replica_seeds(7, 1)[0]
+    gpu, orc = make_pair(abmx, oracle, cfgd, seed)
+    for t in range(1, 11):
+        gpu.step(t)
+        oe = orc.step(t)
+        assert gpu.collect_metrics()[0].tolist() == orc.metrics(), t
+        assert_same_events(gpu.last_events(), oe, f"C2 t={t}")
+    rows = gpu.run(11, 15)[0]
+    for t in range(11, 26):
+        orc.step(t)
+        assert rows[t - 11].astype(np.int64).tolist() == orc.metrics(), t
+    assert_same_state(gpu, orc, "C2 t=25")
