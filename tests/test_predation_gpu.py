@@ -388,9 +388,9 @@ def test_c1_soak_10000_steps(abmx, oracle):
     assert_same_state(gpu, orc, "c1 t=10000")
 
 
-def test_c2_scale_25_steps_both_paths(abmx, oracle):
-    """C2 at full size for 25 steps (the bench's timed window): 10 per-call steps (events every
-    step), then 15 steps in one run(); metrics every step and the full state at the end."""
+def test_c2_scale_100_steps_both_paths(abmx, oracle):
+    """C2 at full size for its 100 steps: 10 per-call steps (events every step),
+    then 90 steps in one run(); metrics every step and the full state at the end."""
     cfgd = c1(width=2048, height=2048, n_sheep0=300000, n_wolves0=30000,
               sheep_capacity=524288, wolf_capacity=524288)
     seed = abmx.replica_seeds(7, 1)[0]
@@ -400,8 +400,8 @@ def test_c2_scale_25_steps_both_paths(abmx, oracle):
         oe = orc.step(t)
         assert gpu.collect_metrics()[0].tolist() == orc.metrics(), t
         assert_same_events(gpu.last_events(), oe, f"C2 t={t}")
-    rows = gpu.run(11, 15)[0]
-    for t in range(11, 26):
+    rows = gpu.run(11, 90)[0]
+    for t in range(11, 101):
         orc.step(t)
         assert rows[t - 11].astype(np.int64).tolist() == orc.metrics(), t
-    assert_same_state(gpu, orc, "C2 t=25")
+    assert_same_state(gpu, orc, "C2 t=100")
