@@ -42,6 +42,11 @@ constexpr int kNTSmall = ABMX_FIN_SMALL_NT;  // one warp per book: C5 2.0 ms vs 
 constexpr int kSmallWindow = 512;
 constexpr double kTick = 0x1p-7;  // finance.hpp:37
 constexpr unsigned short kPad = 0xFFFF;
+// Cash amounts are multiples of 2^-8 (quantity x a midpoint of 2^-7 ticks), so every partial
+// sum below 2^45 is exact and the order of the (atomic) additions cannot change a bit. A sum
+// reaching 2^44 leaves that envelope: flagged, reported by the host instead of a result that
+// could differ from the reference's sequential sums.
+constexpr double kCashExact = 0x1p44;
 
 struct BookS {  // per-book scalars
     double last_price, clearing;
@@ -549,7 +554,8 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
                         P.f_qty[fi] = f;
                         P.f_amount[fi] = amount;
                     } else if (tr >= 0 && tr < T) {
-                        atomicAdd(&S.dcash[tr], buy ? -amount : amount);
+                        const double dv = buy ? -amount : amount;
+                        if (fabs(atomicAdd(&S.dcash[tr], dv) + dv) >= kCashExact) atomicOr(P.err, 2);
                         atomicAdd(reinterpret_cast<unsigned long long*>(&S.dhold[tr]),
                                   static_cast<unsigned long long>(buy ? f : -f));
                     }
@@ -626,7 +632,9 @@ __global__ void __launch_bounds__(kNT) k_fin(FParams P) {
     }
     if (!P.match_only)
         for (int i = tid; i < T; i += kNT) {
-            if (S.dcash[i] != 0.0) atomicAdd(&P.cash[static_cast<size_t>(m) * T + i], S.dcash[i]);
+            if (S.dcash[i] != 0.0 &&
+                fabs(atomicAdd(&P.cash[static_cast<size_t>(m) * T + i], S.dcash[i]) + S.dcash[i]) >= kCashExact)
+                atomicOr(P.err, 2);
             P.holdings[(static_cast<size_t>(m) * P.K + k) * T + i] += S.dhold[i];
         }
     if (tid == 0) {
@@ -691,6 +699,10 @@ int check_cfg(const abmx_finance_config& c) {
         abmx_internal::set_error("finance: qmax must be >= 1");  // uniform_int(1, qmax+1) needs qmax >= 1
         return ABMX_E_DOMAIN;
     }
+    if (c.qmax > INT32_MAX) {
+        abmx_internal::set_error("finance: qmax above 2^31-1 is not supported (32-bit order quantities)");
+        return ABMX_E_CAPACITY;
+    }
     if (c.book_capacity > 4096 || c.traders > 4096) {
         abmx_internal::set_error("finance: book_capacity and traders above 4096 are not supported "
                                  "(one shared-memory-resident CTA per book)");
@@ -753,9 +765,14 @@ struct abmx_finance {
     int check_err() {  // after a stream sync
         int e = 0;
         CKF(cudaMemcpy(&e, d_err, 4, cudaMemcpyDeviceToHost));
-        if (e) {
+        if (e & 1) {
             abmx_internal::set_error("finance: an order outside the order window (internal invariant broken)");
             return ABMX_E_CUDA;
+        }
+        if (e & 2) {
+            abmx_internal::set_error("finance: a cash sum reached 2^44, outside the exact-summation envelope "
+                                     "(results could differ from the reference's sequential sums)");
+            return ABMX_E_DOMAIN;
         }
         return ABMX_OK;
     }

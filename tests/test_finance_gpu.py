@@ -216,3 +216,33 @@ def test_order_window_after_import(F, oracle):
     got = m.book(0)
     assert got["active"][30:60].all() and got["num_active"] >= 30
     assert (m.collect_metrics()[0, 0, 2] + m.collect_metrics()[0, 0, 3]) == got["num_active"]
+
+
+@pytest.mark.parametrize("kw,t0", [
+    (dict(traders=12, books=2, book_capacity=300, p_order=0.9, qmax=(1 << 31) - 1), 1),  # cum beyond 32 bits
+    (dict(traders=12, books=2, book_capacity=300, p_order=0.9), (1 << 31) - 6),          # t crosses 2^31
+])
+def test_compact_layout_guards(F, oracle, kw, t0):
+    """Launches whose ids / placed / cumulative quantities would overflow the compact 32-bit
+    order layout run in the full layout (abmx_finance::compact_fits): still bit-exact."""
+    cfg = pyoracle.fin_cfg(**kw)
+    o = pyoracle.OracleFin(oracle, cfg, 77)
+    m = F.FinanceModel(F.FinanceConfig(**kw), 77)
+    rows = m.run(t0, 12)[0]
+    for q in range(12):
+        o.step(t0 + q)
+        assert np.array_equal(rows[q], o.metrics()), (kw, q)
+    for k in range(kw["books"]):
+        assert_book(m.book(k), o.book(k), (kw, k))
+
+
+def test_quantity_and_cash_envelopes(abmx, F):
+    """Order quantities are 32-bit on the device (qmax above 2^31-1 is refused), and a cash sum
+    reaching 2^44 -- beyond which atomic summation order could change bits -- is reported."""
+    with pytest.raises(abmx.CapacityError):
+        F.FinanceModel(F.FinanceConfig(qmax=1 << 35), 1)
+    m = F.FinanceModel(F.FinanceConfig(traders=12, books=2, book_capacity=300, p_order=0.9,
+                                       qmax=(1 << 31) - 1, init_price=1e9), 5)
+    with pytest.raises(abmx.DomainError):
+        m.run(1, 40)
+
