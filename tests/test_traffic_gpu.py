@@ -257,3 +257,19 @@ def test_many_long_roads_ticket_order(T, oracle):
             assert rows[r, q].tolist() == ref.metrics().tolist(), (r, q)
     for r in (0, 7, 15):
         assert_road(dev.road(r), refs[r].export(), r)
+
+
+@pytest.mark.parametrize("period,gf", [((1 << 31) + 5, 0.5), (10**12, 0.999), (1, 1.0), (7, 0.0)])
+def test_extreme_signal_schedules(T, oracle, period, gf):
+    """Signal periods beyond 32 bits and the all-green / all-red extremes (traffic.cpp:11-13,
+    SignalSchedule): phase, green length and every step against the C restatement."""
+    L = 40
+    dev = T.TrafficModel(T.TrafficConfig(L, period, gf), 99)
+    ref = oracle.traffic(L, period, gf, 99)
+    sc = dev.schedule()
+    assert (sc.phase, sc.green_len) == (ref.m.phase, ref.m.green_len)
+    for t in range(1, 120):
+        dev.step(t)
+        ref.step(t)
+        assert dev.collect_metrics()[0].tolist() == ref.metrics().tolist(), (period, t)
+    assert_road(dev.road(), ref.export())
