@@ -17,7 +17,7 @@ from test_predation_gpu import assert_same_events, assert_same_state
 pytestmark = pytest.mark.gpu
 
 FUZZ = settings(max_examples=int(os.environ.get("ABMX_FUZZ_EXAMPLES", "60")), deadline=None,
-                derandomize=True, database=None,
+                derandomize=not os.environ.get("ABMX_FUZZ_RANDOM"), database=None,
                 suppress_health_check=[HealthCheck.function_scoped_fixture])
 
 

@@ -14,7 +14,7 @@ import pyoracle
 from fuzz_strategies import finance_cfg, predation_cfg, traffic_cfg
 
 FUZZ = settings(max_examples=int(os.environ.get("ABMX_FUZZ_EXAMPLES", "100")), deadline=None,
-                derandomize=True, database=None)
+                derandomize=not os.environ.get("ABMX_FUZZ_RANDOM"), database=None)
 
 
 def _both(make_a, make_b):
