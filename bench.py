@@ -525,6 +525,19 @@ def our_arm(args, rank, world, local_rank, dist):
                "effective_gbs": c3_bytes / (kmax / 1e3) / 1e9,
                "note": "state stays on chip for all steps; effective GB/s uses SURVEY §8d bytes "
                        "and may exceed HBM peak"}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            sys.path.insert(0, os.path.join(ROOT, "oracle"))
+            import pyoracle
+            if os.path.exists(pyoracle.REF_SO):
+                ref = pyoracle.Reference()
+                threads = os.cpu_count() or 1
+                nrep = 512  # a bounded sample of C3 (same C1 replicas, all host threads)
+                _, wall = ref.run_batch(C1, MASTER_SEED, nrep, ENSEMBLE_STEPS, threads=threads)
+                ens["cpu_baseline"] = {
+                    "value": nrep * capacity(C1) * ENSEMBLE_STEPS / (wall / 1e3), "unit": UNIT,
+                    "cores": threads, "kind": "reference",
+                    "sample": f"reference run_batch(PredationModel), {nrep} C1 replicas x "
+                              f"{ENSEMBLE_STEPS} steps, {threads} threads ({wall / 1e3:.2f} s)"}
 
     traffic = None if args.no_traffic else traffic_section(args, rank, world, allreduce, dist)
     finance = None if args.no_finance else finance_section(args, rank, world, allreduce, dist)
