@@ -100,3 +100,39 @@ def test_oracle_is_not_linked_into_the_product():
     assert "orc_" not in out and "ref_pred" not in out
     ldd = subprocess.run(["ldd", LIB], capture_output=True, text=True).stdout
     assert "oracle" not in ldd and "abmx_ref" not in ldd
+
+
+def test_integration_snippets_compile(tmp_path):
+    """The C++ in INTEGRATION.md compiles against this repo's headers and, for the reference-side
+    bindings, the reference's own public headers (skipped where /root/reference is absent)."""
+    import re
+    import shutil
+    import subprocess
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc) or not shutil.which("g++"):
+        pytest.skip("reference headers or g++ not available")
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```cpp\n(.*?)```", text, re.S)
+    assert len(blocks) >= 5
+    pre = ('#include <cstdint>\n#include <vector>\n#include "abmx/simd/kernels.hpp"\n#include "abmx/batch.hpp"\n'
+           '#include "abmx/models/predation.hpp"\n#include "abmx/models/traffic.hpp"\n#include "abmx_cuda.hpp"\n')
+    fragments = {  # statement-level snippets: the names the prose around them provides
+        1: "void f1() {\n%s}\n",
+        3: ("void f3() {\nstruct { bool id_recycling() const { return false; } } set;\n"
+            "int32_t cap = 0, m = 0; int64_t species = 0; void* stream = nullptr;\n"
+            "void *d_e = nullptr, *d_w = nullptr, *d_f = nullptr;\n"
+            "uint8_t *d_active = nullptr, *d_kill = nullptr, *d_valid = nullptr;\n"
+            "int64_t *d_ids = nullptr, *d_types = nullptr, *d_ages = nullptr, *d_counters = nullptr,"
+            " *d_retired = nullptr, *d_res = nullptr;\n"
+            "int32_t *d_slots = nullptr, *d_rows = nullptr; abmx_column* rows = nullptr;\n%s}\n"),
+    }
+    body = []
+    for i, b in enumerate(blocks):
+        b = re.sub(r'#include "abmx_cuda\.hp?p?"\n', "", b)
+        body.append(fragments[i] % b if i in fragments else b)
+    src = tmp_path / "integration.cpp"
+    src.write_text(pre + "namespace abmx::models {\n" + "\n".join(body[2:]) + "\n}\n" +
+                   body[0] + "\n" + body[1])
+    r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-I", ref_inc,
+                        "-I", "/usr/local/cuda/include", str(src)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[:2000]
