@@ -187,15 +187,19 @@ __global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, con
     for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
          j += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int v = rb[j];
+        // rank 0 means "not selected" and is never looked up (match_lookup_kernel): skipping it
+        // removes the one hot word every unselected row would hammer
+        if (v == 0) continue;
         if (dense) {
-            atomicMin(&vals[v - ws->vmin], static_cast<int>(j));
+            int* slot = &vals[v - ws->vmin];
+            if (__ldcg(slot) > static_cast<int>(j)) atomicMin(slot, static_cast<int>(j));  // duplicates: skip
         } else {
             const unsigned long long key = (static_cast<unsigned long long>(static_cast<uint32_t>(v)) << 1) | 1ULL;
             unsigned h = hash32(static_cast<uint32_t>(v), bits);
             for (;;) {
                 const unsigned long long prev = atomicCAS(&keys[h], 0ULL, key);
                 if (prev == 0ULL || prev == key) {
-                    atomicMin(&vals[h], static_cast<int>(j));
+                    if (__ldcg(&vals[h]) > static_cast<int>(j)) atomicMin(&vals[h], static_cast<int>(j));
                     break;
                 }
                 h = (h + 1) & mask;

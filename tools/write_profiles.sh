@@ -7,7 +7,7 @@ cp gpurun_out/bench_r01.json profiles/r01_bench.json
   python tools/ncu_launches.py gpurun_out/launches_r01.csv; } > profiles/r01_launches.txt
 python tools/ncu_summary.py gpurun_out/prof_r01.ncu-rep | grep '^{' > /tmp/c2.jsonl
 python tools/ncu_summary.py gpurun_out/c3_final.ncu-rep | grep '^{' | tail -1 > /tmp/c3.jsonl
-{ for f in trf_c4_r01 trf_ens_r01 fin_r01; do python tools/ncu_summary.py gpurun_out/$f.ncu-rep; done; } | grep '^{' > /tmp/models.jsonl
+{ for f in trf_c4_r01 trf_ens_r01 fin_r01 agents_r01 table_r01; do python tools/ncu_summary.py gpurun_out/$f.ncu-rep; done; } | grep '^{' > /tmp/models.jsonl
 python - <<'PY'
 import json, statistics
 def agg(rows):
