@@ -21,6 +21,17 @@ namespace abmx_table {
 constexpr int kThreads = 256;
 constexpr int kItems = 16;  // mask bytes per thread
 constexpr int kTile = kThreads * kItems;
+constexpr int kCountItems = 64;
+#ifndef ABMX_SCAN_ITEMS
+#define ABMX_SCAN_ITEMS 64
+#endif
+constexpr int kScanItems = ABMX_SCAN_ITEMS;  // mask bytes per thread in rank_scan / compact
+constexpr int kScanTile = kThreads * kScanItems;
+#ifndef ABMX_COMPACT_ITEMS
+#define ABMX_COMPACT_ITEMS 64
+#endif
+constexpr int kCompactItems = ABMX_COMPACT_ITEMS;  // the tile is staged in dynamic SMEM
+constexpr int kCompactTile = kThreads * kCompactItems;
 
 struct ScanWs {
     unsigned ticket;
@@ -28,20 +39,30 @@ struct ScanWs {
     unsigned long long status[1];  // [tiles]
 };
 
-__device__ __forceinline__ void load_mask16(const uint8_t* mask, size_t base, size_t n,
-                                            bool vec_ok, uint8_t (&b)[kItems]) {
-    if (vec_ok && base + kItems <= n) {
-        const uint4 v = *reinterpret_cast<const uint4*>(mask + base);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+template <int I>
+__device__ __forceinline__ void load_mask(const uint8_t* mask, size_t base, size_t n, bool vec_ok,
+                                          uint8_t (&b)[I]) {
+    if (vec_ok && base + I <= n) {
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) b[k] = static_cast<uint8_t>(w[k >> 2] >> (8 * (k & 3)));
+        for (int q = 0; q < I / 16; ++q) {
+            const uint4 v = *reinterpret_cast<const uint4*>(mask + base + 16 * q);
+            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) b[16 * q + k] = static_cast<uint8_t>(w[k >> 2] >> (8 * (k & 3)));
+        }
     } else {
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) b[k] = base + k < n ? mask[base + k] : 0;
+        for (int k = 0; k < I; ++k) b[k] = base + k < n ? mask[base + k] : 0;
     }
 }
 
+__device__ __forceinline__ void load_mask16(const uint8_t* mask, size_t base, size_t n,
+                                            bool vec_ok, uint8_t (&b)[kItems]) {
+    load_mask<kItems>(mask, base, n, vec_ok, b);
+}
+
 // ranks[i] = mask[i] ? inclusive_prefix_sum(mask != 0)[i] : 0
+template <int I>
 __global__ void __launch_bounds__(kThreads) rank_scan_kernel(const uint8_t* __restrict__ mask,
                                                              int32_t* __restrict__ ranks, size_t n,
                                                              ScanWs* ws) {
@@ -51,48 +72,45 @@ __global__ void __launch_bounds__(kThreads) rank_scan_kernel(const uint8_t* __re
     if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
-    const size_t base = static_cast<size_t>(tile) * kTile + static_cast<size_t>(threadIdx.x) * kItems;
+    const size_t base = static_cast<size_t>(tile) * (kThreads * I) + static_cast<size_t>(threadIdx.x) * I;
     const bool vec_in = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
-    uint8_t b[kItems];
-    load_mask16(mask, base, n, vec_in, b);
+    uint8_t b[I];
+    load_mask<I>(mask, base, n, vec_in, b);
     unsigned cnt = 0;
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) cnt += b[k] != 0;
+    for (int k = 0; k < I; ++k) cnt += b[k] != 0;
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kThreads>(cnt, s_scan, &total);
     __syncthreads();
     const unsigned long long tile_prefix = block_lookback<kThreads>(ws->status, static_cast<int>(tile), total, s_look);
     int32_t run = static_cast<int32_t>(tile_prefix + excl);
-    int32_t r[kItems];
+    // Stage the tile's ranks in SMEM (row stride I + 1: conflict-free both ways), then store
+    // coalesced; each thread's own 4*I contiguous bytes made every warp store touch 32 sectors.
+    extern __shared__ int32_t s_r[];  // [kThreads * (I + 1)], dynamic
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {
+    for (int k = 0; k < I; ++k) {
         run += b[k] != 0;
-        r[k] = b[k] ? run : 0;
+        s_r[threadIdx.x * (I + 1) + k] = b[k] ? run : 0;
     }
-    const bool vec_out = (reinterpret_cast<uintptr_t>(ranks) & 15) == 0;
-    if (vec_out && base + kItems <= n) {
-        int4* o = reinterpret_cast<int4*>(ranks + base);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) o[q] = make_int4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-    } else {
-#pragma unroll
-        for (int k = 0; k < kItems; ++k)
-            if (base + k < n) ranks[base + k] = r[k];
-    }
+    __syncthreads();
+    const size_t tile_base = static_cast<size_t>(tile) * (kThreads * I);
+    const int tile_n = static_cast<int>(n - tile_base < static_cast<size_t>(kThreads * I) ? n - tile_base
+                                                                                       : kThreads * I);
+    for (int j = threadIdx.x; j < tile_n; j += kThreads) ranks[tile_base + j] = s_r[j + j / I];
 }
 
-// number of nonzero bytes
+// number of nonzero bytes (64 per thread per iteration: four 16-byte loads in flight)
 __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __restrict__ mask,
                                                               size_t n,
                                                               unsigned long long* __restrict__ out) {
     const bool vec = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
     unsigned long long c = 0;
-    for (size_t base = (static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.x) * kItems; base < n;
-         base += static_cast<size_t>(gridDim.x) * kThreads * kItems) {
-        uint8_t b[kItems];
-        load_mask16(mask, base, n, vec, b);
+    for (size_t base = (static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.x) * kCountItems; base < n;
+         base += static_cast<size_t>(gridDim.x) * kThreads * kCountItems) {
+        uint8_t b[kCountItems];
+        load_mask<kCountItems>(mask, base, n, vec, b);
 #pragma unroll
-        for (int k = 0; k < kItems; ++k) c += b[k] != 0;
+        for (int k = 0; k < kCountItems; ++k) c += b[k] != 0;
     }
     c = warp_sum(c);
     __shared__ unsigned long long s[kThreads / 32];
@@ -107,6 +125,7 @@ __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __r
 
 // Stable partition of 0..n-1: true indices first (ascending), then false indices.
 // `true_total` is the precomputed count_true (device memory).
+template <int I>
 __global__ void __launch_bounds__(kThreads) compact_kernel(const uint8_t* __restrict__ mask,
                                                            int32_t* __restrict__ out, size_t n,
                                                            const unsigned long long* __restrict__ true_total,
@@ -117,30 +136,36 @@ __global__ void __launch_bounds__(kThreads) compact_kernel(const uint8_t* __rest
     if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
     __syncthreads();
     const unsigned tile = s_tile;
-    const size_t base = static_cast<size_t>(tile) * kTile + static_cast<size_t>(threadIdx.x) * kItems;
+    const size_t base = static_cast<size_t>(tile) * (kThreads * I) + static_cast<size_t>(threadIdx.x) * I;
     const bool vec_in = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
-    uint8_t b[kItems];
-    load_mask16(mask, base, n, vec_in, b);
+    uint8_t b[I];
+    load_mask<I>(mask, base, n, vec_in, b);
     unsigned cnt = 0;
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) cnt += b[k] != 0;
+    for (int k = 0; k < I; ++k) cnt += b[k] != 0;
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kThreads>(cnt, s_scan, &total);
     __syncthreads();
     const unsigned long long tile_prefix = block_lookback<kThreads>(ws->status, static_cast<int>(tile), total, s_look);
+    // Partition the tile in shared memory (trues then falses, both ascending), then write the
+    // two runs out coalesced: per-thread scattered stores left each warp instruction touching
+    // 32 sectors.
+    extern __shared__ int32_t s_out[];  // [kThreads * I], dynamic
     const size_t T = *true_total;
-    size_t t_run = tile_prefix + excl;  // trues before this thread's first element
-    size_t f_run = base - t_run;     // falses before it
+    const size_t tile_base = static_cast<size_t>(tile) * (kThreads * I);
+    const int tile_n = static_cast<int>(n - tile_base < static_cast<size_t>((kThreads * I)) ? n - tile_base : (kThreads * I));
+    const int ttot = static_cast<int>(total);
+    int t_loc = static_cast<int>(excl);
+    int f_loc = ttot + static_cast<int>(threadIdx.x) * I - static_cast<int>(excl);
 #pragma unroll
-    for (int k = 0; k < kItems; ++k) {
+    for (int k = 0; k < I; ++k) {
         const size_t i = base + k;
-        if (i < n) {
-            if (b[k])
-                out[t_run++] = static_cast<int32_t>(i);
-            else
-                out[T + f_run++] = static_cast<int32_t>(i);
-        }
+        if (i < n) s_out[b[k] ? t_loc++ : f_loc++] = static_cast<int32_t>(i);
     }
+    __syncthreads();
+    const size_t f_dst = T + (tile_base - tile_prefix) - static_cast<size_t>(ttot);
+    for (int j = threadIdx.x; j < tile_n; j += kThreads)
+        out[j < ttot ? tile_prefix + j : f_dst + j] = s_out[j];
 }
 
 // ---------------------------------------------------------------- match_first_equal
@@ -179,6 +204,22 @@ __device__ __forceinline__ unsigned hash32(uint32_t k, unsigned bits) {
 }
 
 // vals[] starts at INT_MAX; keys[] (hash mode) start at 0 = empty, else (key << 1) | 1.
+// Initialise only what the chosen mode reads (after minmax): dense -> vals[0, range);
+// hash -> vals[0, H) and keys[0, H). Memsetting both full tables up front wrote 12*H bytes.
+__global__ void match_init_kernel(const MatchWs* ws, int* __restrict__ vals,
+                                  unsigned long long* __restrict__ keys) {
+    const bool dense = dense_mode(ws);
+    const size_t H = size_t{1} << ws->hbits;
+    const size_t nv = dense ? static_cast<size_t>(static_cast<long long>(ws->vmax) - ws->vmin + 1) : H;
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const int4 fill = make_int4(0x7F7F7F7F, 0x7F7F7F7F, 0x7F7F7F7F, 0x7F7F7F7F);  // > any row
+    for (size_t i = t0; i < nv / 4; i += stride) reinterpret_cast<int4*>(vals)[i] = fill;
+    for (size_t i = (nv & ~size_t{3}) + t0; i < nv; i += stride) vals[i] = 0x7F7F7F7F;
+    if (!dense)
+        for (size_t i = t0; i < H / 2; i += stride) reinterpret_cast<ulonglong2*>(keys)[i] = make_ulonglong2(0, 0);
+}
+
 __global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, const MatchWs* ws,
                                    int* __restrict__ vals, unsigned long long* __restrict__ keys) {
     const bool dense = dense_mode(ws);
@@ -256,16 +297,23 @@ __global__ void __launch_bounds__(kThreads) blend_kernel(const uint8_t* mask, co
         uint8_t m[kItems];
         load_mask16(mask, base, n, vec, m);
         if (vec && base + kItems <= n) {
+            // All loads before any store: `out` may alias a or b (same index only), and
+            // interleaving would let the compiler keep just two loads in flight.
+            constexpr int kVecs = kItems / kPerVec;
+            uint4 va[kVecs], vb[kVecs];
 #pragma unroll
-            for (int q = 0; q < kItems / kPerVec; ++q) {
-                uint4 va = *reinterpret_cast<const uint4*>(a + base + q * kPerVec);
-                const uint4 vb = *reinterpret_cast<const uint4*>(b + base + q * kPerVec);
-                T* ea = reinterpret_cast<T*>(&va);
-                const T* eb = reinterpret_cast<const T*>(&vb);
+            for (int q = 0; q < kVecs; ++q) {
+                va[q] = *reinterpret_cast<const uint4*>(a + base + q * kPerVec);
+                vb[q] = *reinterpret_cast<const uint4*>(b + base + q * kPerVec);
+            }
+#pragma unroll
+            for (int q = 0; q < kVecs; ++q) {
+                T* ea = reinterpret_cast<T*>(&va[q]);
+                const T* eb = reinterpret_cast<const T*>(&vb[q]);
 #pragma unroll
                 for (int k = 0; k < kPerVec; ++k)
                     if (!m[q * kPerVec + k]) ea[k] = eb[k];
-                *reinterpret_cast<uint4*>(out + base + q * kPerVec) = va;
+                *reinterpret_cast<uint4*>(out + base + q * kPerVec) = va[q];
             }
         } else {
 #pragma unroll
@@ -290,14 +338,18 @@ static int grid_for(size_t n, int per_block) {
 
 cudaError_t launch_rank_scan(const uint8_t* d_mask, int32_t* d_ranks, size_t n, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const size_t tiles = (n + kTile - 1) / kTile;
+    const size_t tiles = (n + kScanTile - 1) / kScanTile;
     const size_t ws_bytes = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
     void* ws = nullptr;
     cudaError_t e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(ws, 0, ws_bytes, s);
     (void)cudaGetLastError();
-    rank_scan_kernel<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(d_mask, d_ranks, n,
+    constexpr int smem = kThreads * (kScanItems + 1) * static_cast<int>(sizeof(int32_t));
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        rank_scan_kernel<kScanItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) { cudaFreeAsync(ws, s); return attr; }
+    rank_scan_kernel<kScanItems><<<static_cast<unsigned>(tiles), kThreads, smem, s>>>(d_mask, d_ranks, n,
                                                                       static_cast<ScanWs*>(ws));
     count_launch();
     e = cudaGetLastError();
@@ -310,7 +362,7 @@ cudaError_t launch_count_true(const uint8_t* d_mask, size_t n, unsigned long lon
     cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
     if (n == 0) return cudaGetLastError();
     (void)cudaGetLastError();
-    count_true_kernel<<<grid_for(n, kTile), kThreads, 0, s>>>(d_mask, n, d_out);
+    count_true_kernel<<<grid_for(n, kThreads * kCountItems), kThreads, 0, s>>>(d_mask, n, d_out);
     count_launch();
     return cudaGetLastError();
 }
@@ -320,14 +372,18 @@ cudaError_t launch_compact_indices(const uint8_t* d_mask, int32_t* d_out, size_t
     if (n == 0) return cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
     cudaError_t e = launch_count_true(d_mask, n, d_count, s);
     if (e != cudaSuccess) return e;
-    const size_t tiles = (n + kTile - 1) / kTile;
+    const size_t tiles = (n + kCompactTile - 1) / kCompactTile;
     const size_t ws_bytes = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
     void* ws = nullptr;
     e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
     cudaMemsetAsync(ws, 0, ws_bytes, s);
     (void)cudaGetLastError();
-    compact_kernel<<<static_cast<unsigned>(tiles), kThreads, 0, s>>>(d_mask, d_out, n, d_count,
+    constexpr int smem = kCompactTile * static_cast<int>(sizeof(int32_t));
+    static const cudaError_t attr = cudaFuncSetAttribute(
+        compact_kernel<kCompactItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (attr != cudaSuccess) { cudaFreeAsync(ws, s); return attr; }
+    compact_kernel<kCompactItems><<<static_cast<unsigned>(tiles), kThreads, smem, s>>>(d_mask, d_out, n, d_count,
                                                                     static_cast<ScanWs*>(ws));
     count_launch();
     e = cudaGetLastError();
@@ -351,14 +407,13 @@ cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_
     auto* keys = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256 + H * sizeof(int));
     const MatchWs init{INT_MAX, INT_MIN, bits, 0u};
     cudaMemcpyAsync(mws, &init, sizeof init, cudaMemcpyHostToDevice, s);
-    cudaMemsetAsync(vals, 0x7F, H * sizeof(int), s);  // 0x7F7F7F7F > any row index
-    cudaMemsetAsync(keys, 0, H * sizeof(unsigned long long), s);
     const int gm = grid_for(m, 256), gn = grid_for(n, 256);
     (void)cudaGetLastError();
     minmax_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws);
+    match_init_kernel<<<num_sms() * 8, 256, 0, s>>>(mws, vals, keys);
     match_build_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws, vals, keys);
     match_lookup_kernel<<<gn, 256, 0, s>>>(d_ra, n, mws, vals, keys, d_out);
-    count_launch(3);
+    count_launch(4);
     e = cudaGetLastError();
     cudaFreeAsync(ws, s);
     return e;

@@ -29,3 +29,25 @@ for _ in range(2):
     abmx._check(lib.abmx_cuda_blend_i64_async(vp(mask), vp(a64), vp(b64), vp(o64), C.c_size_t(n), s))
 torch.cuda.synchronize()
 print("ok", int(cnt.item()))
+
+if len(sys.argv) > 1 and sys.argv[1] == "time":
+    # event-timed per-entry medians (L2 is 126 MB; every buffer here is >= 64 MiB)
+    ops = {
+        "rank_scan": lambda: lib.abmx_cuda_rank_scan_async(vp(mask), vp(ranks), C.c_size_t(n), s),
+        "count_true": lambda: lib.abmx_cuda_count_true_async(vp(mask), C.c_size_t(n), vp(cnt), s),
+        "compact_indices": lambda: lib.abmx_cuda_compact_indices_async(vp(mask), vp(out), C.c_size_t(n),
+                                                                        vp(cnt), s),
+        "match_first_equal": lambda: lib.abmx_cuda_match_first_equal_async(
+            vp(ranks), C.c_size_t(n), vp(ranks), C.c_size_t(n // 2), vp(out), s),
+        "blend_i64": lambda: lib.abmx_cuda_blend_i64_async(vp(mask), vp(a64), vp(b64), vp(o64), C.c_size_t(n), s),
+    }
+    for name, f in ops.items():
+        ts = []
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            abmx._check(f())
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        print(f"{name:18s} {sorted(ts)[5] * 1e3:9.1f} us")
