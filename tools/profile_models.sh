@@ -22,5 +22,5 @@ python tools/prof_agents.py > /dev/null && \
 ncu --set full --clock-control none --import-source on -k regex:"k_select|k_pair_apply|k_remove_apply" -s 8 -c 4 \
     -o gpurun_out/agents_$TAG python tools/prof_agents.py > gpurun_out/ncu_agents_$TAG.log 2>&1; echo agents_rc=$?
 python tools/prof_table.py > /dev/null && \
-ncu --set full --clock-control none --import-source on -k regex:"_kernel" -s 7 -c 7 \
+ncu --set full --clock-control none --import-source on -k regex:"_kernel" -s 9 -c 9 \
     -o gpurun_out/table_$TAG python tools/prof_table.py > gpurun_out/ncu_table_$TAG.log 2>&1; echo table_rc=$?
