@@ -99,6 +99,14 @@ __global__ void __launch_bounds__(kThreads) rank_scan_kernel(const uint8_t* __re
     for (int j = threadIdx.x; j < tile_n; j += kThreads) ranks[tile_base + j] = s_r[j + j / I];
 }
 
+// nonzero bytes of a word (SWAR): fold each byte's bits onto its bit 0, then popcount
+__device__ __forceinline__ unsigned nz_bytes(uint32_t w) {
+    uint32_t x = w | (w >> 4);
+    x |= x >> 2;
+    x |= x >> 1;
+    return static_cast<unsigned>(__popc(x & 0x01010101u));
+}
+
 // number of nonzero bytes (64 per thread per iteration: four 16-byte loads in flight)
 __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __restrict__ mask,
                                                               size_t n,
@@ -107,10 +115,18 @@ __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __r
     unsigned long long c = 0;
     for (size_t base = (static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.x) * kCountItems; base < n;
          base += static_cast<size_t>(gridDim.x) * kThreads * kCountItems) {
-        uint8_t b[kCountItems];
-        load_mask<kCountItems>(mask, base, n, vec, b);
+        unsigned part = 0;
+        if (vec && base + kCountItems <= n) {
+            uint4 v[kCountItems / 16];
 #pragma unroll
-        for (int k = 0; k < kCountItems; ++k) c += b[k] != 0;
+            for (int q = 0; q < kCountItems / 16; ++q) v[q] = *reinterpret_cast<const uint4*>(mask + base + 16 * q);
+#pragma unroll
+            for (int q = 0; q < kCountItems / 16; ++q)
+                part += nz_bytes(v[q].x) + nz_bytes(v[q].y) + nz_bytes(v[q].z) + nz_bytes(v[q].w);
+        } else {
+            for (size_t i = base; i < base + kCountItems && i < n; ++i) part += mask[i] != 0;
+        }
+        c += part;
     }
     c = warp_sum(c);
     __shared__ unsigned long long s[kThreads / 32];
