@@ -229,9 +229,10 @@ __global__ void match_init_kernel(const MatchWs* ws, int* __restrict__ vals,
     const size_t nv = dense ? static_cast<size_t>(static_cast<long long>(ws->vmax) - ws->vmin + 1) : H;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const int4 fill = make_int4(0x7F7F7F7F, 0x7F7F7F7F, 0x7F7F7F7F, 0x7F7F7F7F);  // > any row
+    // INT_MAX = "no row": above any row index, and what the lookup maps to -1
+    const int4 fill = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX);
     for (size_t i = t0; i < nv / 4; i += stride) reinterpret_cast<int4*>(vals)[i] = fill;
-    for (size_t i = (nv & ~size_t{3}) + t0; i < nv; i += stride) vals[i] = 0x7F7F7F7F;
+    for (size_t i = (nv & ~size_t{3}) + t0; i < nv; i += stride) vals[i] = INT_MAX;
     if (!dense)
         for (size_t i = t0; i < H / 2; i += stride) reinterpret_cast<ulonglong2*>(keys)[i] = make_ulonglong2(0, 0);
 }

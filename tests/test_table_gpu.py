@@ -53,7 +53,7 @@ def test_match_first_equal_ranks(abmx, oracle, n, m):
     assert np.array_equal(abmx.match_first_equal(ra, rb), oracle.match_first_equal(ra, rb))
 
 
-@pytest.mark.parametrize("spread", [10, 1 << 30])
+@pytest.mark.parametrize("spread", [10, 1000, 1 << 30])  # 1000: dense table with gaps
 def test_match_first_equal_arbitrary_ints(abmx, oracle, spread):
     """Non-rank inputs with duplicates: FIRST match wins (dense and hash table paths)."""
     rng = np.random.default_rng(spread)
@@ -148,3 +148,49 @@ def test_golden_kernel_table_from_reference(abmx):
         assert np.array_equal(abmx.rank_scan(m), np.frombuffer(base64.b64decode(c["ranks"]), np.int32))
         assert np.array_equal(abmx.compact_indices(m), np.frombuffer(base64.b64decode(c["compact"]), np.int32))
         assert abmx.count_true(m) == c["count"]
+
+
+@pytest.mark.parametrize("case", ["zero_heavy", "hashed", "dense_odd", "all_zero", "single"])
+def test_match_first_equal_large(abmx, oracle, case):
+    """Sizes where the table init and the build contention matter: rank-0-heavy rb (rank 0 is
+    never looked up), a hashed table of 2^20 spread values, a dense range that is not a
+    multiple of 4 (the init tail), an all-zero rb, and a single-value rb."""
+    rng = np.random.default_rng(len(case))
+    if case == "zero_heavy":
+        rb = oracle.rank_scan((rng.random(1 << 21) < 0.05).astype(np.uint8))
+        ra = oracle.rank_scan((rng.random(1 << 22) < 0.5).astype(np.uint8))
+    elif case == "hashed":
+        rb = rng.integers(-2**31, 2**31 - 1, 1 << 20).astype(np.int32)
+        ra = np.concatenate([rb[rng.integers(0, rb.size, 1 << 19)],
+                             rng.integers(-2**31, 2**31 - 1, 1 << 19)]).astype(np.int32)
+    elif case == "dense_odd":
+        rb = rng.integers(5, 5 + 1000003, 1 << 20).astype(np.int32)
+        ra = rng.integers(0, 1000013, 1 << 21).astype(np.int32)
+    elif case == "all_zero":
+        rb = np.zeros(1 << 20, np.int32)
+        ra = rng.integers(-3, 4, 1 << 20).astype(np.int32)
+    else:
+        rb = np.full(123457, 42, np.int32)
+        ra = rng.integers(40, 45, 99991).astype(np.int32)
+    assert np.array_equal(abmx.match_first_equal(ra, rb), first_equal_np(ra, rb))
+
+
+def first_equal_np(ra, rb):
+    """O((n+m) log m) restatement of orc_match_first_equal (kernels_scalar.cpp semantics:
+    first j with rb[j] == ra[i], -1 when none or ra[i] == 0), for sizes the O(n*m) C oracle
+    cannot finish; pinned to it by test_first_equal_np_matches_oracle."""
+    vals, first = np.unique(rb, return_index=True)
+    out = np.full(ra.size, -1, np.int32)
+    if vals.size:
+        pos = np.clip(np.searchsorted(vals, ra), 0, vals.size - 1)
+        hit = (vals[pos] == ra) & (ra != 0)
+        out[hit] = first[pos[hit]]
+    return out
+
+
+def test_first_equal_np_matches_oracle(oracle):
+    rng = np.random.default_rng(3)
+    for m in (0, 1, 50, 2000):
+        rb = rng.integers(-20, 20, m).astype(np.int32)
+        ra = rng.integers(-25, 25, 3000).astype(np.int32)
+        assert np.array_equal(first_equal_np(ra, rb), oracle.match_first_equal(ra, rb))
