@@ -532,11 +532,9 @@ __device__ unsigned long long wolf_cell(const Params& P, unsigned long long ent,
             P.flag[1][wb + wl[q]] = 1;  // ate
         }
     } else {
+        // every agent sits in exactly one cell list, so the pool (R * (Npad0 + Npad1) entries)
+        // cannot overflow
         const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
-        if (static_cast<long long>(off) + lw + ls > P.pool_size) {
-            atomicExch(&P.ctl->error, 1u);
-            return 0;
-        }
         int* pw = P.pool + off;
         int* ps = pw + lw;
         int q = 0;

@@ -32,9 +32,9 @@ constexpr int kEpochClear = 128; // cell tags are cleared every kEpochClear step
 // Device control block (counters shared by the kernels of a step).
 struct Ctl {
     unsigned occ;       // entries in the wolf-cell list this step (crowded grids)
-    unsigned pool_top;  // bump allocator of the long-list sort pool
-    unsigned error;     // set if the sort pool overflowed (cannot happen: sized N_s + N_w)
-    unsigned pad;
+    unsigned pool_top;  // bump allocator of the long-list sort pool (sized N_s + N_w: every
+                        // agent sits in exactly one cell list, so it cannot overflow)
+    unsigned pad[2];
 };
 
 // Per (replica, species) counters. next_id / num_active are double-buffered by step parity
