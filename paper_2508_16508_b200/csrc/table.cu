@@ -2,9 +2,9 @@
 // (include/abmx/simd/kernels.hpp:15-43; scalar semantics src/simd/kernels_scalar.cpp:7-54).
 //
 // All entries are HBM-streaming integer/bitwise kernels:
-//   rank_scan        single-pass decoupled-lookback scan, 16 mask bytes per thread
-//   count_true       grid-stride popcount reduction
-//   compact_indices  count, then single-pass scan with a two-sided scatter
+//   rank_scan        persistent count-then-scan over per-CTA chunks, TMA-pipelined (below)
+//   count_true       grid-stride SWAR popcount reduction
+//   compact_indices  the same kernel: count, chunk gather (gives the true total), two-run scatter
 //   match_first_equal  O(n+m) first-match table (dense when rb's range is small,
 //                    open-addressing hash otherwise; atomicMin keeps FIRST-match semantics)
 //   blend_{i64,f64,u8}  predicated select, out may alias a or b (lifecycle.cpp:105-111)
@@ -22,22 +22,6 @@ constexpr int kThreads = 256;
 constexpr int kItems = 16;  // mask bytes per thread
 constexpr int kTile = kThreads * kItems;
 constexpr int kCountItems = 64;
-#ifndef ABMX_SCAN_ITEMS
-#define ABMX_SCAN_ITEMS 64
-#endif
-constexpr int kScanItems = ABMX_SCAN_ITEMS;  // mask bytes per thread in rank_scan / compact
-constexpr int kScanTile = kThreads * kScanItems;
-#ifndef ABMX_COMPACT_ITEMS
-#define ABMX_COMPACT_ITEMS 64
-#endif
-constexpr int kCompactItems = ABMX_COMPACT_ITEMS;  // the tile is staged in dynamic SMEM
-constexpr int kCompactTile = kThreads * kCompactItems;
-
-struct ScanWs {
-    unsigned ticket;
-    unsigned pad;
-    unsigned long long status[1];  // [tiles]
-};
 
 template <int I>
 __device__ __forceinline__ void load_mask(const uint8_t* mask, size_t base, size_t n, bool vec_ok,
@@ -59,44 +43,6 @@ __device__ __forceinline__ void load_mask(const uint8_t* mask, size_t base, size
 __device__ __forceinline__ void load_mask16(const uint8_t* mask, size_t base, size_t n,
                                             bool vec_ok, uint8_t (&b)[kItems]) {
     load_mask<kItems>(mask, base, n, vec_ok, b);
-}
-
-// ranks[i] = mask[i] ? inclusive_prefix_sum(mask != 0)[i] : 0
-template <int I>
-__global__ void __launch_bounds__(kThreads) rank_scan_kernel(const uint8_t* __restrict__ mask,
-                                                             int32_t* __restrict__ ranks, size_t n,
-                                                             ScanWs* ws) {
-    __shared__ unsigned long long s_scan[kThreads / 32 + 1];
-    __shared__ unsigned s_tile;
-    __shared__ unsigned long long s_look[kThreads / 32 + 2];
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
-    const size_t base = static_cast<size_t>(tile) * (kThreads * I) + static_cast<size_t>(threadIdx.x) * I;
-    const bool vec_in = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
-    uint8_t b[I];
-    load_mask<I>(mask, base, n, vec_in, b);
-    unsigned cnt = 0;
-#pragma unroll
-    for (int k = 0; k < I; ++k) cnt += b[k] != 0;
-    unsigned long long total;
-    const unsigned long long excl = block_excl_scan<kThreads>(cnt, s_scan, &total);
-    __syncthreads();
-    const unsigned long long tile_prefix = block_lookback<kThreads>(ws->status, static_cast<int>(tile), total, s_look);
-    int32_t run = static_cast<int32_t>(tile_prefix + excl);
-    // Stage the tile's ranks in SMEM (row stride I + 1: conflict-free both ways), then store
-    // coalesced; each thread's own 4*I contiguous bytes made every warp store touch 32 sectors.
-    extern __shared__ int32_t s_r[];  // [kThreads * (I + 1)], dynamic
-#pragma unroll
-    for (int k = 0; k < I; ++k) {
-        run += b[k] != 0;
-        s_r[threadIdx.x * (I + 1) + k] = b[k] ? run : 0;
-    }
-    __syncthreads();
-    const size_t tile_base = static_cast<size_t>(tile) * (kThreads * I);
-    const int tile_n = static_cast<int>(n - tile_base < static_cast<size_t>(kThreads * I) ? n - tile_base
-                                                                                       : kThreads * I);
-    for (int j = threadIdx.x; j < tile_n; j += kThreads) ranks[tile_base + j] = s_r[j + j / I];
 }
 
 // nonzero bytes of a word (SWAR): fold each byte's bits onto its bit 0, then popcount
@@ -139,49 +85,230 @@ __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __r
     }
 }
 
-// Stable partition of 0..n-1: true indices first (ascending), then false indices.
-// `true_total` is the precomputed count_true (device memory).
-template <int I>
-__global__ void __launch_bounds__(kThreads) compact_kernel(const uint8_t* __restrict__ mask,
-                                                           int32_t* __restrict__ out, size_t n,
-                                                           const unsigned long long* __restrict__ true_total,
-                                                           ScanWs* ws) {
-    __shared__ unsigned long long s_scan[kThreads / 32 + 1];
-    __shared__ unsigned s_tile;
-    __shared__ unsigned long long s_look[kThreads / 32 + 2];
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ws->ticket, 1u);
-    __syncthreads();
-    const unsigned tile = s_tile;
-    const size_t base = static_cast<size_t>(tile) * (kThreads * I) + static_cast<size_t>(threadIdx.x) * I;
-    const bool vec_in = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
-    uint8_t b[I];
-    load_mask<I>(mask, base, n, vec_in, b);
-    unsigned cnt = 0;
-#pragma unroll
-    for (int k = 0; k < I; ++k) cnt += b[k] != 0;
-    unsigned long long total;
-    const unsigned long long excl = block_excl_scan<kThreads>(cnt, s_scan, &total);
-    __syncthreads();
-    const unsigned long long tile_prefix = block_lookback<kThreads>(ws->status, static_cast<int>(tile), total, s_look);
-    // Partition the tile in shared memory (trues then falses, both ascending), then write the
-    // two runs out coalesced: per-thread scattered stores left each warp instruction touching
-    // 32 sectors.
-    extern __shared__ int32_t s_out[];  // [kThreads * I], dynamic
-    const size_t T = *true_total;
-    const size_t tile_base = static_cast<size_t>(tile) * (kThreads * I);
-    const int tile_n = static_cast<int>(n - tile_base < static_cast<size_t>((kThreads * I)) ? n - tile_base : (kThreads * I));
-    const int ttot = static_cast<int>(total);
-    int t_loc = static_cast<int>(excl);
-    int f_loc = ttot + static_cast<int>(threadIdx.x) * I - static_cast<int>(excl);
-#pragma unroll
-    for (int k = 0; k < I; ++k) {
-        const size_t i = base + k;
-        if (i < n) s_out[b[k] ? t_loc++ : f_loc++] = static_cast<int32_t>(i);
+// ---------------------------------------------------------------- persistent pipelined scan
+// rank_scan and compact_indices at HBM speed. A persistent, co-resident grid (cooperative
+// launch, 2 CTAs per SM) gives each CTA one contiguous chunk of kPTile-byte mask tiles, and each
+// CTA streams its chunk twice:
+//   pass 1  counts the chunk's nonzero bytes and publishes the chunk total;
+//   gather  every CTA reads all chunk totals (all published at about the same time, one round
+//           trip): its exclusive chunk prefix and, for compact_indices, the true total T;
+//   pass 2  re-reads the chunk and writes ranks (rank_scan) or the stable partition
+//           (compact_indices) with a running in-chunk prefix. No tile waits on another tile.
+// A per-tile decoupled lookback was measured first (profiles/r02_table.md): with every CTA's
+// tiles in flight at once, the lookbacks ran the CTAs in lock-step (6 us per tile), 3x slower
+// than this extra 1-byte-per-element read. compact_indices needs no separate count kernel.
+// Tiles arrive through a kPIn-stage shared-memory ring filled by 1-D bulk copies (TMA,
+// cp.async.bulk -> UBLKCP), so HBM reads run ahead of the scan and the stores. A warp owns
+// 1024 consecutive elements as 8 rows of 32 words; a row is scanned with three ballots of the
+// per-word nonzero-byte counts (0..4). rank_scan stages its ranks in shared memory and writes
+// each tile with one bulk copy (double-buffered); compact_indices partitions the tile in shared
+// memory and writes its two runs with coalesced stores. Partial or unaligned tiles take the
+// same path with plain loads / stores.
+#ifndef ABMX_SCAN_THREADS
+#define ABMX_SCAN_THREADS 256
+#endif
+constexpr int kPT = ABMX_SCAN_THREADS;  // threads per CTA (a warp scans 1024 elements per tile)
+constexpr int kPTile = kPT * 32;        // mask bytes (elements) per tile
+constexpr int kPMinB = kPT >= 512 ? 1 : 2;  // CTAs per SM
+#ifndef ABMX_SCAN_STAGES
+#define ABMX_SCAN_STAGES 5
+#endif
+constexpr int kPIn = ABMX_SCAN_STAGES;  // input stages
+constexpr int kPOut = 2;       // rank_scan output stages
+
+struct PipeShared {
+    unsigned long long bar[kPIn];
+    unsigned wtot[kPT / 32];
+    unsigned long long red[kPT / 32][2];
+    unsigned long long total, base, T;
+};
+
+template <bool kCompact>
+constexpr int pipe_smem() {
+    return kPIn * kPTile + (kCompact ? 1 : kPOut) * kPTile * static_cast<int>(sizeof(int32_t));
+}
+
+template <bool kCompact>
+__global__ void __launch_bounds__(kPT, kPMinB) scan_pipe_kernel(const uint8_t* __restrict__ mask, int32_t* __restrict__ out,
+                                                          size_t n, int tiles, unsigned long long* __restrict__ chunk_tot,
+                                                          unsigned long long* __restrict__ true_out) {
+    extern __shared__ __align__(128) unsigned char dsm[];
+    __shared__ PipeShared S;
+    uint8_t* in = dsm;
+    int32_t* ob = reinterpret_cast<int32_t*>(dsm + kPIn * kPTile);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
+    const int c0 = static_cast<int>(static_cast<long long>(tiles) * b / G);
+    const int m = static_cast<int>(static_cast<long long>(tiles) * (b + 1) / G) - c0;  // >= 1 (grid <= tiles)
+    const bool in_vec = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
+    const bool out_vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
+    auto tile_of = [&](int it) { return c0 + it % m; };  // iterations 0..2m-1: the chunk, twice
+    auto is_bulk = [&](int t) { return in_vec && static_cast<size_t>(t + 1) * kPTile <= n; };
+    auto issue = [&](int it) {  // one thread: the tile of iteration `it` into ring slot it % kPIn
+        if (it >= 2 * m) return;
+        const int t = tile_of(it), s = it % kPIn;
+        if (is_bulk(t)) {
+            mbar_expect_tx(&S.bar[s], kPTile);
+            bulk_g2s(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < kPIn; ++s) mbar_init(&S.bar[s], 1);
+        mbar_fence_init();
+        for (int it = 0; it < kPIn; ++it) issue(it);
     }
     __syncthreads();
-    const size_t f_dst = T + (tile_base - tile_prefix) - static_cast<size_t>(ttot);
-    for (int j = threadIdx.x; j < tile_n; j += kThreads)
-        out[j < ttot ? tile_prefix + j : f_dst + j] = s_out[j];
+    unsigned phase = 0;            // bit s: parity of ring slot s's next bulk completion
+    unsigned long long run = 0;    // pass 2: elements' prefix before this tile (global)
+    unsigned long long lane_acc = 0;  // pass 1: this lane's nonzero count over the chunk
+    for (int it = 0; it < 2 * m; ++it) {
+        const int s = it % kPIn;
+        const int tile = tile_of(it);
+        const bool pass2 = it >= m;
+        const size_t tb = static_cast<size_t>(tile) * kPTile;
+        const int tn = static_cast<int>(n - tb < static_cast<size_t>(kPTile) ? n - tb : kPTile);
+        uint8_t* buf = in + s * kPTile;
+        if (!kCompact && pass2 && tid == 0) bulk_wait_read<kPOut - 1>();  // the output stage we reuse is free
+        if (is_bulk(tile)) {
+            mbar_wait(&S.bar[s], (phase >> s) & 1u);
+            phase ^= 1u << s;
+        } else {
+            for (int j = tid; j < kPTile; j += kPT) buf[j] = j < tn ? mask[tb + j] : 0;
+            __syncthreads();
+        }
+        // ---- per-word nonzero counts
+        const uint32_t* wbuf = reinterpret_cast<const uint32_t*>(buf) + warp * 256;
+        uint32_t wd[8];
+        unsigned c[8], lt = 0;  // this warp's 1024 elements: 8 rows of 32 words
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            wd[r] = wbuf[r * 32 + lane];
+            c[r] = nz_bytes(wd[r]);
+            lt += c[r];
+        }
+        if (!pass2) {  // pass 1 only needs the chunk total: accumulate per lane, one barrier per tile
+            lane_acc += lt;
+            __syncthreads();  // every read of buf is done: refill slot s kPIn iterations ahead
+            if (tid == 0) issue(it + kPIn);
+        } else {
+            const unsigned wt = __reduce_add_sync(0xffffffffu, lt);
+            if (lane == 0) S.wtot[warp] = wt;
+            __syncthreads();  // every read of buf is done: refill slot s kPIn iterations ahead
+            if (tid == 0) issue(it + kPIn);
+            if (warp == 0) {
+                const unsigned v = lane < kPT / 32 ? S.wtot[lane] : 0u;
+                unsigned incl = v;
+#pragma unroll
+                for (int d = 1; d < kPT / 32; d <<= 1) {
+                    const unsigned u = __shfl_up_sync(0xffffffffu, incl, d);
+                    if (lane >= d) incl += u;
+                }
+                const unsigned total = __shfl_sync(0xffffffffu, incl, kPT / 32 - 1);
+                if (lane < kPT / 32) S.wtot[lane] = incl - v;  // exclusive warp offsets
+                if (lane == 0) S.total = total;
+            }
+            __syncthreads();
+        }
+        if (it == m - 1) {
+            // ---- gather: publish this chunk's total, read every chunk's (all CTAs are resident)
+            const unsigned long long wsum = warp_sum(lane_acc);
+            if (lane == 0) S.red[warp][0] = wsum;
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long x = 0;
+                for (int w = 0; w < kPT / 32; ++w) x += S.red[w][0];
+                st_word(&chunk_tot[b], kFlagAgg | x);
+            }
+            __syncthreads();
+            unsigned long long before = 0, all = 0;
+            for (int q = tid; q < G; q += kPT) {
+                unsigned long long v = ld_word(&chunk_tot[q]);
+                while ((v >> 62) == 0) {
+                    __nanosleep(32);
+                    v = ld_word(&chunk_tot[q]);
+                }
+                v &= kValueMask;
+                all += v;
+                if (q < b) before += v;
+            }
+            before = warp_sum(before);
+            all = warp_sum(all);
+            if (lane == 0) {
+                S.red[warp][0] = before;
+                S.red[warp][1] = all;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                unsigned long long x = 0, y = 0;
+                for (int w = 0; w < kPT / 32; ++w) {
+                    x += S.red[w][0];
+                    y += S.red[w][1];
+                }
+                S.base = x;
+                S.T = y;
+                if (kCompact && b == 0 && true_out) *true_out = y;  // count_true(mask)
+            }
+            __syncthreads();
+            run = S.base;
+            continue;
+        }
+        if (!pass2) continue;
+        const unsigned lt_mask = (1u << lane) - 1u;
+        if constexpr (!kCompact) {
+            int32_t* o = ob + (it % kPOut) * kPTile;
+            int4* o4 = reinterpret_cast<int4*>(o) + warp * 256;
+            unsigned x0 = static_cast<unsigned>(run) + S.wtot[warp];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const unsigned b0 = __ballot_sync(0xffffffffu, c[r] & 1u), b1 = __ballot_sync(0xffffffffu, c[r] & 2u),
+                               b2 = __ballot_sync(0xffffffffu, c[r] & 4u);
+                unsigned x = x0 + __popc(b0 & lt_mask) + 2u * __popc(b1 & lt_mask) + 4u * __popc(b2 & lt_mask);
+                int q[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const bool nz = ((wd[r] >> (8 * k)) & 0xFFu) != 0u;
+                    x += nz;
+                    q[k] = nz ? static_cast<int>(x) : 0;
+                }
+                o4[r * 32 + lane] = make_int4(q[0], q[1], q[2], q[3]);
+                x0 += __popc(b0) + 2u * __popc(b1) + 4u * __popc(b2);
+            }
+            fence_proxy_async_smem();
+            __syncthreads();
+            if (tn == kPTile && out_vec) {
+                if (tid == 0) {
+                    bulk_s2g(out + tb, o, kPTile * static_cast<unsigned>(sizeof(int32_t)));
+                    bulk_commit();
+                }
+            } else {
+                for (int j = tid; j < tn; j += kPT) out[tb + j] = o[j];
+            }
+        } else {
+            const int ttot = static_cast<int>(S.total);
+            int tpre = static_cast<int>(S.wtot[warp]);  // trues before this lane's word, in the tile
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                const unsigned b0 = __ballot_sync(0xffffffffu, c[r] & 1u), b1 = __ballot_sync(0xffffffffu, c[r] & 2u),
+                               b2 = __ballot_sync(0xffffffffu, c[r] & 4u);
+                int x = tpre + __popc(b0 & lt_mask) + 2 * __popc(b1 & lt_mask) + 4 * __popc(b2 & lt_mask);
+                const int e0 = warp * 1024 + r * 128 + lane * 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int e = e0 + k;
+                    if (((wd[r] >> (8 * k)) & 0xFFu) != 0u)
+                        ob[x++] = static_cast<int32_t>(tb + e);
+                    else
+                        ob[ttot + e - x] = static_cast<int32_t>(tb + e);
+                }
+                tpre += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
+            }
+            __syncthreads();
+            const size_t f_dst = S.T + (tb - run) - static_cast<size_t>(ttot);
+            for (int j = tid; j < tn; j += kPT) out[j < ttot ? run + j : f_dst + j] = ob[j];
+        }
+        run += S.total;
+    }
+    if (!kCompact && tid == 0) bulk_wait_all();
 }
 
 // ---------------------------------------------------------------- match_first_equal
@@ -353,25 +480,48 @@ static int grid_for(size_t n, int per_block) {
     return static_cast<int>(g < cap ? (g > 0 ? g : 1) : cap);
 }
 
-cudaError_t launch_rank_scan(const uint8_t* d_mask, int32_t* d_ranks, size_t n, cudaStream_t s) {
-    if (n == 0) return cudaSuccess;
-    const size_t tiles = (n + kScanTile - 1) / kScanTile;
-    const size_t ws_bytes = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
-    void* ws = nullptr;
-    cudaError_t e = abmx_internal::malloc_async(&ws, ws_bytes, s);
+// persistent pipelined scan (rank_scan / compact_indices): workspace = one word per CTA chunk
+template <bool kCompact>
+static cudaError_t launch_scan_pipe(const uint8_t* d_mask, int32_t* d_out, size_t n, unsigned long long* d_true,
+                                    cudaStream_t s) {
+    const size_t tiles = (n + kPTile - 1) / kPTile;
+    constexpr int smem = pipe_smem<kCompact>();
+    // the attribute is per function and per device: set it on every call (cheap next to the scan)
+    cudaError_t e = cudaFuncSetAttribute(scan_pipe_kernel<kCompact>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(ws, 0, ws_bytes, s);
+    // co-resident grid: every CTA waits for all chunk totals (cooperative launch guarantees it)
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_pipe_kernel<kCompact>, kPT, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+    const size_t cap = static_cast<size_t>(num_sms()) * static_cast<size_t>(per_sm < kPMinB ? per_sm : kPMinB);
+    const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
+    void* ws = nullptr;
+    e = abmx_internal::malloc_async(&ws, grid * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    cudaMemsetAsync(ws, 0, grid * sizeof(unsigned long long), s);
     (void)cudaGetLastError();
-    constexpr int smem = kThreads * (kScanItems + 1) * static_cast<int>(sizeof(int32_t));
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        rank_scan_kernel<kScanItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (attr != cudaSuccess) { cudaFreeAsync(ws, s); return attr; }
-    rank_scan_kernel<kScanItems><<<static_cast<unsigned>(tiles), kThreads, smem, s>>>(d_mask, d_ranks, n,
-                                                                      static_cast<ScanWs*>(ws));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kPT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, scan_pipe_kernel<kCompact>, d_mask, d_out, n, static_cast<int>(tiles),
+                           static_cast<unsigned long long*>(ws), d_true);
     count_launch();
-    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(ws, s);
     return e;
+}
+
+cudaError_t launch_rank_scan(const uint8_t* d_mask, int32_t* d_ranks, size_t n, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    return launch_scan_pipe<false>(d_mask, d_ranks, n, nullptr, s);
 }
 
 cudaError_t launch_count_true(const uint8_t* d_mask, size_t n, unsigned long long* d_out,
@@ -387,25 +537,8 @@ cudaError_t launch_count_true(const uint8_t* d_mask, size_t n, unsigned long lon
 cudaError_t launch_compact_indices(const uint8_t* d_mask, int32_t* d_out, size_t n,
                                    unsigned long long* d_count, cudaStream_t s) {
     if (n == 0) return cudaMemsetAsync(d_count, 0, sizeof(unsigned long long), s);
-    cudaError_t e = launch_count_true(d_mask, n, d_count, s);
-    if (e != cudaSuccess) return e;
-    const size_t tiles = (n + kCompactTile - 1) / kCompactTile;
-    const size_t ws_bytes = sizeof(ScanWs) + tiles * sizeof(unsigned long long);
-    void* ws = nullptr;
-    e = abmx_internal::malloc_async(&ws, ws_bytes, s);
-    if (e != cudaSuccess) return e;
-    cudaMemsetAsync(ws, 0, ws_bytes, s);
-    (void)cudaGetLastError();
-    constexpr int smem = kCompactTile * static_cast<int>(sizeof(int32_t));
-    static const cudaError_t attr = cudaFuncSetAttribute(
-        compact_kernel<kCompactItems>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (attr != cudaSuccess) { cudaFreeAsync(ws, s); return attr; }
-    compact_kernel<kCompactItems><<<static_cast<unsigned>(tiles), kThreads, smem, s>>>(d_mask, d_out, n, d_count,
-                                                                    static_cast<ScanWs*>(ws));
-    count_launch();
-    e = cudaGetLastError();
-    cudaFreeAsync(ws, s);
-    return e;
+    // one kernel: the false run starts at count_true(mask), which the chunk gather provides
+    return launch_scan_pipe<true>(d_mask, d_out, n, d_count, s);
 }
 
 cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_t* d_rb, size_t m,
