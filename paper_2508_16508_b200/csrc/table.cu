@@ -312,34 +312,64 @@ __global__ void __launch_bounds__(kPT, kPMinB) scan_pipe_kernel(const uint8_t* _
 }
 
 // ---------------------------------------------------------------- match_first_equal
+// vmin / vmax live in an order-preserving unsigned form, both reduced with atomicMin, so ONE
+// cudaMemsetAsync(0xFF) initialises the workspace (capturable in a graph; no host staging):
+// emin = v ^ 2^31 (min of v), emax = ~(v ^ 2^31) (min of emax = max of v).
 struct MatchWs {
-    int vmin, vmax;
-    unsigned hbits;  // table size = 1 << hbits
-    unsigned pad;
+    unsigned emin, emax;
 };
+__device__ __forceinline__ int ws_vmin(const MatchWs* ws) { return static_cast<int>(ws->emin ^ 0x80000000u); }
+__device__ __forceinline__ int ws_vmax(const MatchWs* ws) { return static_cast<int>(~ws->emax ^ 0x80000000u); }
+
+// Grid-stride loops over 4-element quads (16-byte loads, U quads in flight per thread); a
+// scalar loop covers the tail and unaligned inputs. `f(index, value)` sees every element once.
+template <int U = 2, class F>
+__device__ __forceinline__ void for_each_i32(const int32_t* __restrict__ p, size_t n, F&& f) {
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    size_t done = 0;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+        const size_t quads = n / 4;
+        const int4* q = reinterpret_cast<const int4*>(p);
+        for (size_t i = t0; i < quads; i += U * stride) {
+            int4 a[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) a[u] = i + u * stride < quads ? q[i + u * stride] : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (i + u * stride >= quads) break;
+                const size_t e = 4 * (i + u * stride);
+                f(e, a[u].x);
+                f(e + 1, a[u].y);
+                f(e + 2, a[u].z);
+                f(e + 3, a[u].w);
+            }
+        }
+        done = 4 * quads;
+    }
+    for (size_t j = done + t0; j < n; j += stride) f(j, p[j]);
+}
 
 __global__ void minmax_kernel(const int32_t* __restrict__ rb, size_t m, MatchWs* ws) {
     int lo = INT_MAX, hi = INT_MIN;
-    for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
-         j += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int v = rb[j];
+    for_each_i32<4>(rb, m, [&](size_t, int v) {
         lo = min(lo, v);
         hi = max(hi, v);
-    }
+    });
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
         hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
     }
     if ((threadIdx.x & 31) == 0) {
-        atomicMin(&ws->vmin, lo);
-        atomicMax(&ws->vmax, hi);
+        atomicMin(&ws->emin, static_cast<unsigned>(lo) ^ 0x80000000u);
+        atomicMin(&ws->emax, ~(static_cast<unsigned>(hi) ^ 0x80000000u));
     }
 }
 
-__device__ __forceinline__ bool dense_mode(const MatchWs* ws) {
-    const long long range = static_cast<long long>(ws->vmax) - ws->vmin + 1;
-    return range <= (1LL << ws->hbits);
+__device__ __forceinline__ bool dense_mode(const MatchWs* ws, unsigned bits) {
+    const long long range = static_cast<long long>(ws_vmax(ws)) - ws_vmin(ws) + 1;
+    return range <= (1LL << bits);
 }
 
 __device__ __forceinline__ unsigned hash32(uint32_t k, unsigned bits) {
@@ -349,11 +379,11 @@ __device__ __forceinline__ unsigned hash32(uint32_t k, unsigned bits) {
 // vals[] starts at INT_MAX; keys[] (hash mode) start at 0 = empty, else (key << 1) | 1.
 // Initialise only what the chosen mode reads (after minmax): dense -> vals[0, range);
 // hash -> vals[0, H) and keys[0, H). Memsetting both full tables up front wrote 12*H bytes.
-__global__ void match_init_kernel(const MatchWs* ws, int* __restrict__ vals,
+__global__ void match_init_kernel(const MatchWs* ws, unsigned bits, int* __restrict__ vals,
                                   unsigned long long* __restrict__ keys) {
-    const bool dense = dense_mode(ws);
-    const size_t H = size_t{1} << ws->hbits;
-    const size_t nv = dense ? static_cast<size_t>(static_cast<long long>(ws->vmax) - ws->vmin + 1) : H;
+    const bool dense = dense_mode(ws, bits);
+    const size_t H = size_t{1} << bits;
+    const size_t nv = dense ? static_cast<size_t>(static_cast<long long>(ws_vmax(ws)) - ws_vmin(ws) + 1) : H;
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     // INT_MAX = "no row": above any row index, and what the lookup maps to -1
@@ -364,19 +394,45 @@ __global__ void match_init_kernel(const MatchWs* ws, int* __restrict__ vals,
         for (size_t i = t0; i < H / 2; i += stride) reinterpret_cast<ulonglong2*>(keys)[i] = make_ulonglong2(0, 0);
 }
 
-__global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, const MatchWs* ws,
+__global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, const MatchWs* ws, unsigned bits,
                                    int* __restrict__ vals, unsigned long long* __restrict__ keys) {
-    const bool dense = dense_mode(ws);
-    const unsigned bits = ws->hbits;
+    const bool dense = dense_mode(ws, bits);
     const unsigned mask = (1u << bits) - 1u;
-    for (size_t j = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; j < m;
-         j += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int v = rb[j];
+    const int vmin = ws_vmin(ws);
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (dense && (reinterpret_cast<uintptr_t>(rb) & 15) == 0) {
+        // quads: all 8 first-match checks are issued before any atomic (an atomic between two
+        // checks would serialise them: the compiler cannot move a load across a possibly
+        // aliasing atomic)
+        const size_t quads = m / 4;
+        const int4* q = reinterpret_cast<const int4*>(rb);
+        for (size_t i = t0; i < quads; i += 2 * stride) {
+            const bool two = i + stride < quads;
+            const int4 a = q[i];
+            const int4 b = two ? q[i + stride] : make_int4(0, 0, 0, 0);
+            const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+            int cur[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) cur[k] = v[k] != 0 ? __ldcg(&vals[v[k] - vmin]) : INT_MIN;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int j = static_cast<int>(4 * (k < 4 ? i : i + stride) + (k & 3));
+                if (cur[k] > j) atomicMin(&vals[v[k] - vmin], j);  // rank 0 (never looked up) skipped
+            }
+        }
+        for (size_t j = 4 * quads + t0; j < m; j += stride) {
+            const int v = rb[j];
+            if (v != 0 && __ldcg(&vals[v - vmin]) > static_cast<int>(j)) atomicMin(&vals[v - vmin], static_cast<int>(j));
+        }
+        return;
+    }
+    for_each_i32(rb, m, [&](size_t j, int v) {
         // rank 0 means "not selected" and is never looked up (match_lookup_kernel): skipping it
         // removes the one hot word every unselected row would hammer
-        if (v == 0) continue;
+        if (v == 0) return;
         if (dense) {
-            int* slot = &vals[v - ws->vmin];
+            int* slot = &vals[v - vmin];
             if (__ldcg(slot) > static_cast<int>(j)) atomicMin(slot, static_cast<int>(j));  // duplicates: skip
         } else {
             const unsigned long long key = (static_cast<unsigned long long>(static_cast<uint32_t>(v)) << 1) | 1ULL;
@@ -390,42 +446,59 @@ __global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, con
                 h = (h + 1) & mask;
             }
         }
-    }
+    });
 }
 
-__global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, const MatchWs* ws,
+__device__ __forceinline__ int match_one(int r, bool dense, unsigned bits, long long lo, long long hi, const int* vals,
+                                         const unsigned long long* keys) {
+    if (r == 0 || r < lo || r > hi) return -1;
+    int j = INT_MAX;
+    if (dense) {
+        j = vals[r - lo];
+    } else {
+        const unsigned mask = (1u << bits) - 1u;
+        const unsigned long long key = (static_cast<unsigned long long>(static_cast<uint32_t>(r)) << 1) | 1ULL;
+        unsigned h = hash32(static_cast<uint32_t>(r), bits);
+        for (;;) {
+            const unsigned long long k = keys[h];
+            if (k == key) {
+                j = vals[h];
+                break;
+            }
+            if (k == 0ULL) break;
+            h = (h + 1) & mask;
+        }
+    }
+    return j != INT_MAX ? j : -1;
+}
+
+__global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, const MatchWs* ws, unsigned bits,
                                     const int* __restrict__ vals,
                                     const unsigned long long* __restrict__ keys,
                                     int32_t* __restrict__ row_out) {
-    const bool dense = dense_mode(ws);
-    const unsigned bits = ws->hbits;
-    const unsigned mask = (1u << bits) - 1u;
-    const long long lo = ws->vmin, hi = ws->vmax;
-    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int r = ra[i];
-        int out = -1;
-        if (r != 0 && r >= lo && r <= hi) {
-            int j = INT_MAX;
-            if (dense) {
-                j = vals[r - lo];
-            } else {
-                const unsigned long long key = (static_cast<unsigned long long>(static_cast<uint32_t>(r)) << 1) | 1ULL;
-                unsigned h = hash32(static_cast<uint32_t>(r), bits);
-                for (;;) {
-                    const unsigned long long k = keys[h];
-                    if (k == key) {
-                        j = vals[h];
-                        break;
-                    }
-                    if (k == 0ULL) break;
-                    h = (h + 1) & mask;
-                }
-            }
-            if (j != INT_MAX) out = j;
+    const bool dense = dense_mode(ws, bits);
+    const long long lo = ws_vmin(ws), hi = ws_vmax(ws);
+    const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+    const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    size_t done = 0;
+    if (((reinterpret_cast<uintptr_t>(ra) | reinterpret_cast<uintptr_t>(row_out)) & 15) == 0) {
+        // quads in, quads out; two quads in flight per thread
+        const size_t quads = n / 4;
+        const int4* q = reinterpret_cast<const int4*>(ra);
+        int4* o = reinterpret_cast<int4*>(row_out);
+        for (size_t i = t0; i < quads; i += 2 * stride) {
+            const bool two = i + stride < quads;
+            const int4 a = q[i];
+            const int4 b = two ? q[i + stride] : make_int4(0, 0, 0, 0);
+            o[i] = make_int4(match_one(a.x, dense, bits, lo, hi, vals, keys), match_one(a.y, dense, bits, lo, hi, vals, keys),
+                             match_one(a.z, dense, bits, lo, hi, vals, keys), match_one(a.w, dense, bits, lo, hi, vals, keys));
+            if (two)
+                o[i + stride] = make_int4(match_one(b.x, dense, bits, lo, hi, vals, keys), match_one(b.y, dense, bits, lo, hi, vals, keys),
+                                          match_one(b.z, dense, bits, lo, hi, vals, keys), match_one(b.w, dense, bits, lo, hi, vals, keys));
         }
-        row_out[i] = out;
+        done = 4 * quads;
     }
+    for (size_t j = done + t0; j < n; j += stride) row_out[j] = match_one(ra[j], dense, bits, lo, hi, vals, keys);
 }
 
 // ---------------------------------------------------------------- blends
@@ -555,14 +628,13 @@ cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_
     auto* mws = static_cast<MatchWs*>(ws);
     int* vals = reinterpret_cast<int*>(static_cast<char*>(ws) + 256);
     auto* keys = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 256 + H * sizeof(int));
-    const MatchWs init{INT_MAX, INT_MIN, bits, 0u};
-    cudaMemcpyAsync(mws, &init, sizeof init, cudaMemcpyHostToDevice, s);
-    const int gm = grid_for(m, 256), gn = grid_for(n, 256);
+    cudaMemsetAsync(mws, 0xFF, sizeof(MatchWs), s);  // emin = emax = UINT_MAX (see MatchWs)
+    const int gm = grid_for(m, 256 * 8), gn = grid_for(n, 256 * 8);
     (void)cudaGetLastError();
     minmax_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws);
-    match_init_kernel<<<num_sms() * 8, 256, 0, s>>>(mws, vals, keys);
-    match_build_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws, vals, keys);
-    match_lookup_kernel<<<gn, 256, 0, s>>>(d_ra, n, mws, vals, keys, d_out);
+    match_init_kernel<<<num_sms() * 8, 256, 0, s>>>(mws, bits, vals, keys);
+    match_build_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws, bits, vals, keys);
+    match_lookup_kernel<<<gn, 256, 0, s>>>(d_ra, n, mws, bits, vals, keys, d_out);
     count_launch(4);
     e = cudaGetLastError();
     cudaFreeAsync(ws, s);
