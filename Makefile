@@ -17,9 +17,19 @@ CU      := table predation ensemble agents traffic traffic_ens finance diag capi
 OBJS    := $(addprefix $(OBJDIR)/,$(addsuffix .o,$(CU)))
 HDRS    := $(wildcard $(SRC)/*.h $(SRC)/*.cuh) include/abmx_cuda.h
 
-all: cuda oracle
+all: cuda oracle functor_cases
 
 cuda: $(PKG)/libabmx_cuda.so
+
+# test library: the header-only device functor API (include/abmx_cuda_functors.cuh) on the
+# scenarios tests/test_functors_gpu.py compares with the reference (not part of the product)
+functor_cases: build/libabmx_functor_cases.so
+
+build/libabmx_functor_cases.so: tests/cpp/functor_cases.cu include/abmx_cuda_functors.cuh include/abmx_cuda.hpp \
+		include/abmx_cuda.h $(PKG)/libabmx_cuda.so
+	@mkdir -p build
+	$(NVCC) $(ARCH) -O3 -std=c++17 -fmad=false -Xcompiler -fPIC -Iinclude -shared -o $@ $< \
+		-L$(PKG) -labmx_cuda -Xlinker -rpath,'$$ORIGIN/../$(PKG)'
 
 $(OBJDIR)/%.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -35,4 +45,4 @@ clean:
 	rm -rf build $(PKG)/libabmx_cuda.so
 	$(MAKE) -C oracle clean
 
-.PHONY: all cuda oracle clean
+.PHONY: all cuda oracle functor_cases clean
