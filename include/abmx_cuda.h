@@ -276,6 +276,10 @@ int abmx_agents_select(const uint8_t* d_mask, int32_t n, int32_t* d_indices, int
  * Synchronises `stream` once for that check. */
 int abmx_agents_sort_perm(const double* d_key, const uint8_t* d_active, int32_t n,
                           int32_t descending, int32_t* d_perm, void* stream);
+/* pinned_keys (kernels.cpp:37-50, kernels.hpp:73-79): out[i] = keys[i] on active slots, +inf
+ * (ascending) or -inf (descending) on placeholders, so sort_agents moves them to the tail. */
+int abmx_agents_pinned_keys(const double* d_keys, const uint8_t* d_active, int32_t n, int32_t descending,
+                            double* d_out, void* stream);
 /* permute_agents (agent_set.cpp:92-108): every column c[i] = c[perm[i]] (gather); indices
  * outside [0, capacity) give ABMX_E_DOMAIN. */
 int abmx_agents_permute(const abmx_agent_set* s, const int32_t* d_perm, void* stream);

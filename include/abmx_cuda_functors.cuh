@@ -578,6 +578,12 @@ void spawn_agents(const DeviceAgents& d, const DeviceRows& rows, Apply apply, bo
     if (d_result) detail::ck(cudaMemcpyAsync(d_result, P.result, 16, cudaMemcpyDeviceToDevice, stream));
 }
 
+// pinned_keys (kernels.cpp:37-50): keys of active slots, +inf / -inf on placeholders
+inline void pinned_keys(const DeviceAgents& d, const double* d_keys, bool descending, double* d_out,
+                        cudaStream_t stream = nullptr) {
+    check(abmx_agents_pinned_keys(d_keys, d.raw().active, d.capacity(), descending ? 1 : 0, d_out, stream));
+}
+
 // remove_agents (lifecycle.cpp:124-142) needs no user code: the C-ABI entry, for completeness
 inline void remove_agents(const DeviceAgents& d, const std::uint8_t* d_kill, std::int64_t* d_killed = nullptr,
                           cudaStream_t stream = nullptr) {

@@ -206,4 +206,18 @@ int ref_fc_spawn(int32_t cap, int32_t num_active, uint64_t seed, const uint8_t* 
     });
 }
 
+// pinned_keys (kernels.cpp:37-50) on a set whose active mask is given
+int ref_pinned_keys(int32_t cap, const uint8_t* active, const double* keys, int32_t descending, double* out) {
+    return guarded([&] {
+        FieldBundle st(static_cast<size_t>(cap));
+        AgentSet s(cap, std::move(st), FieldBundle(static_cast<size_t>(cap)));
+        int32_t live = 0;
+        for (int32_t i = 0; i < cap; ++i) live += (s.active_mut()[static_cast<size_t>(i)] = active[i] ? 1 : 0);
+        s.set_num_active(live);
+        const std::vector<double> k = pinned_keys(s, std::span<const double>(keys, static_cast<size_t>(cap)),
+                                                  descending ? SortDirection::Descending : SortDirection::Ascending);
+        std::memcpy(out, k.data(), k.size() * 8);
+    });
+}
+
 }  // extern "C"

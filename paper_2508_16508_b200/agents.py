@@ -64,6 +64,7 @@ for _n in ("abmx_agents_set_rm", "abmx_agents_set_sci"):
               C.c_void_p, C.c_void_p])
 _sig("abmx_agents_set_mask", [_P, C.c_void_p, C.POINTER(_Column), C.c_void_p])
 _sig("abmx_agents_select", [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p])
+_sig("abmx_agents_pinned_keys", [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p])
 _sig("abmx_agents_sort_perm", [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
                                C.c_void_p])
 _sig("abmx_agents_permute", [_P, C.c_void_p, C.c_void_p])
@@ -341,6 +342,22 @@ def sort_perm(key, active, descending=False, device=None) -> np.ndarray:
                                      perm.data_ptr(),
                                      C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
     return perm[:n].cpu().numpy()
+
+
+def pinned_keys(active_keys, active, descending=False, device=None) -> np.ndarray:
+    """pinned_keys (kernels.cpp:37-50): the keys of active slots, +inf (ascending) / -inf
+    (descending) on placeholder slots, computed on the device."""
+    torch = _torch()
+    dev = torch.device(device or "cuda")
+    k = torch.as_tensor(active_keys, dtype=torch.float64, device=dev).contiguous()
+    a = torch.as_tensor(active, device=dev).to(torch.uint8).contiguous()
+    n = int(k.numel())
+    if int(a.numel()) != n:
+        raise DomainError("key length must equal capacity")
+    out = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
+    _check(lib.abmx_agents_pinned_keys(k.data_ptr(), a.data_ptr(), n, int(descending), out.data_ptr(),
+                                       C.c_void_p(torch.cuda.current_stream(dev).cuda_stream)))
+    return out[:n].cpu().numpy()
 
 
 @dataclass

@@ -706,6 +706,35 @@ int abmx_agents_select(const uint8_t* d_mask, int32_t n, int32_t* d_indices, int
     return ABMX_OK;
 }
 
+// pinned_keys (kernels.cpp:37-50): the keys of active slots, +inf (ascending) / -inf (descending)
+// on placeholder slots so they sort to the tail
+static __global__ void k_pinned_keys(const double* __restrict__ keys, const uint8_t* __restrict__ active, size_t n,
+                              double pin, double* __restrict__ out) {
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        out[i] = active[i] ? keys[i] : pin;
+}
+
+int abmx_agents_pinned_keys(const double* d_keys, const uint8_t* d_active, int32_t n, int32_t descending,
+                            double* d_out, void* stream) {
+    if (n < 0 || (n > 0 && (!d_keys || !d_active || !d_out))) {
+        abmx_internal::set_error("bad pinned_keys arguments");
+        return ABMX_E_ARG;
+    }
+    if (n == 0) return ABMX_OK;
+    (void)cudaGetLastError();
+    const double pin = descending ? -HUGE_VAL : HUGE_VAL;
+    k_pinned_keys<<<grid_for(static_cast<size_t>(n)), kT, 0, static_cast<cudaStream_t>(stream)>>>(
+        d_keys, d_active, static_cast<size_t>(n), pin, d_out);
+    abmx_internal::count_launch();
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        abmx_internal::set_error(std::string("pinned_keys: ") + cudaGetErrorString(e));
+        return ABMX_E_CUDA;
+    }
+    return ABMX_OK;
+}
+
 int abmx_agents_sort_perm(const double* d_key, const uint8_t* d_active, int32_t n, int32_t descending,
                           int32_t* d_perm, void* stream) {
     if (n < 0 || (n > 0 && (!d_key || !d_active || !d_perm))) {

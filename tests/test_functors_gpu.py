@@ -150,3 +150,21 @@ def test_remove_then_spawn_with_apply(fc, reference, recycle, set_type, cap, liv
         outs.append((b, sd))
     _same(outs[0][0], outs[1][0], "spawn")
     assert outs[0][1].tolist() == outs[1][1].tolist()
+
+
+@pytest.mark.parametrize("descending", [0, 1])
+@pytest.mark.parametrize("n", [0, 1, 1000, 100003])
+def test_pinned_keys(abmx, reference, n, descending):
+    """pinned_keys (kernels.cpp:37-50) on the device vs the reference."""
+    from paper_2508_16508_b200 import agents
+    rng = np.random.default_rng(n + descending)
+    keys = rng.normal(size=n)
+    active = (rng.random(n) < 0.6).astype(np.uint8)
+    got = agents.pinned_keys(keys, active, bool(descending))
+    want = np.zeros(n)
+    assert reference.lib.ref_pinned_keys(C.c_int32(n), _p(active, u8p), _p(keys, f64p), C.c_int32(descending),
+                                         _p(want, f64p)) == 0
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
+    # sorting the pinned keys keeps every placeholder at the tail
+    perm = agents.sort_perm(got, active, bool(descending))
+    assert (active[perm][:int(active.sum())] == 1).all()
