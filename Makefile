@@ -38,8 +38,8 @@ $(OBJDIR)/%.o: $(SRC)/%.cu $(HDRS)
 $(PKG)/libabmx_cuda.so: $(OBJS)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
-oracle:
-	$(MAKE) -C oracle
+oracle: cuda
+	$(MAKE) -C oracle all ref_cuda
 
 clean:
 	rm -rf build $(PKG)/libabmx_cuda.so

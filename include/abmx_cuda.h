@@ -40,6 +40,13 @@ extern "C" {
 #define ABMX_E_CONTRACT 7 /* ContractError errors.hpp:31-33 (e.g. a move proposal off the road) */
 
 const char* abmx_cuda_last_error(void);
+/* The synchronous KernelTable entries (section 1) return void, as KernelTable fixes their
+ * signatures. A CUDA failure inside one is therefore recorded, not thrown and not fatal: the call
+ * leaves its outputs unwritten (count_true returns -1), abmx_cuda_table_status() turns sticky
+ * ABMX_E_CUDA until abmx_cuda_table_clear_status(), and abmx_cuda_last_error() holds the
+ * calling thread's message. A caller that must fail fast checks the status after its calls. */
+int abmx_cuda_table_status(void);
+void abmx_cuda_table_clear_status(void);
 const char* abmx_cuda_version(void);
 /* number of kernels this library has launched in this process (all threads) */
 uint64_t abmx_cuda_launch_count(void);

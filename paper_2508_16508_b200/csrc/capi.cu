@@ -61,25 +61,47 @@ struct HostCtx {
     }
 };
 
-[[noreturn]] static void die(const char* what, cudaError_t e) {
-    std::fprintf(stderr, "abmx_cuda: %s failed: %s\n", what, cudaGetErrorString(e));
-    std::abort();
+// The synchronous KernelTable entries are void (kernels.hpp:15-43 fixes their signatures), so
+// a CUDA failure cannot be returned. It is recorded instead: a sticky process-wide code
+// (abmx_cuda_table_status) plus the thread's message (abmx_cuda_last_error). The failing call
+// leaves its outputs unwritten (count_true returns -1), and later calls keep running.
+static std::atomic<int> g_table_status{ABMX_OK};
+static bool table_fail(const char* what, cudaError_t e) {
+    (void)cudaGetLastError();  // clear a non-sticky error so later calls can proceed
+    set_error(std::string("KernelTable: ") + what + ": " + cudaGetErrorString(e));
+    int expect = ABMX_OK;
+    g_table_status.compare_exchange_strong(expect, ABMX_E_CUDA);
+    return false;
 }
-#define DIE_ON(x)                              \
-    do {                                       \
-        cudaError_t e_ = (x);                  \
-        if (e_ != cudaSuccess) die(#x, e_);    \
+#define TRY(x)                                          \
+    do {                                                \
+        cudaError_t e_ = (x);                           \
+        if (e_ != cudaSuccess) return table_fail(#x, e_); \
     } while (0)
 
-static HostCtx& host_ctx() {
+static HostCtx* host_ctx() {
     static thread_local HostCtx ctx;
-    if (!ctx.stream) DIE_ON(cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking));
-    return ctx;
+    if (!ctx.stream) {
+        const cudaError_t e = cudaStreamCreateWithFlags(&ctx.stream, cudaStreamNonBlocking);
+        if (e != cudaSuccess) {
+            ctx.stream = nullptr;
+            table_fail("cudaStreamCreateWithFlags", e);
+            return nullptr;
+        }
+    }
+    return &ctx;
 }
 static void* host_buf(HostCtx& c, int k, size_t bytes) {
     if (bytes > c.cap[k]) {
-        if (c.buf[k]) DIE_ON(cudaFree(c.buf[k]));
-        DIE_ON(cudaMalloc(&c.buf[k], bytes));
+        if (c.buf[k]) cudaFree(c.buf[k]);
+        c.buf[k] = nullptr;
+        c.cap[k] = 0;
+        const cudaError_t e = cudaMalloc(&c.buf[k], bytes);
+        if (e != cudaSuccess) {
+            c.buf[k] = nullptr;
+            table_fail("cudaMalloc", e);
+            return nullptr;
+        }
         c.cap[k] = bytes;
     }
     return c.buf[k];
@@ -90,19 +112,77 @@ static void* host_buf(HostCtx& c, int k, size_t bytes) {
 using namespace abmx_internal;
 
 template <class T, class D>
-static void blend_host(const uint8_t* mask, const T* a, const T* b, T* out, size_t n) {
-    if (n == 0) return;
-    HostCtx& c = host_ctx();
-    auto* dm = static_cast<uint8_t*>(host_buf(c, 0, n));
-    auto* da = static_cast<D*>(host_buf(c, 1, n * sizeof(T)));
-    auto* db = static_cast<D*>(host_buf(c, 2, n * sizeof(T)));
-    auto* dout = static_cast<D*>(host_buf(c, 3, n * sizeof(T)));
-    DIE_ON(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(cudaMemcpyAsync(da, a, n * sizeof(T), cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(cudaMemcpyAsync(db, b, n * sizeof(T), cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(launch_blend<D>(dm, da, db, dout, n, c.stream));
-    DIE_ON(cudaMemcpyAsync(out, dout, n * sizeof(T), cudaMemcpyDeviceToHost, c.stream));
-    DIE_ON(cudaStreamSynchronize(c.stream));
+static bool blend_host(const uint8_t* mask, const T* a, const T* b, T* out, size_t n) {
+    if (n == 0) return true;
+    HostCtx* c = host_ctx();
+    if (!c) return false;
+    auto* dm = static_cast<uint8_t*>(host_buf(*c, 0, n));
+    auto* da = static_cast<D*>(host_buf(*c, 1, n * sizeof(T)));
+    auto* db = static_cast<D*>(host_buf(*c, 2, n * sizeof(T)));
+    auto* dout = static_cast<D*>(host_buf(*c, 3, n * sizeof(T)));
+    if (!dm || !da || !db || !dout) return false;
+    TRY(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c->stream));
+    TRY(cudaMemcpyAsync(da, a, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    TRY(cudaMemcpyAsync(db, b, n * sizeof(T), cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_blend<D>(dm, da, db, dout, n, c->stream));
+    TRY(cudaMemcpyAsync(out, dout, n * sizeof(T), cudaMemcpyDeviceToHost, c->stream));
+    TRY(cudaStreamSynchronize(c->stream));
+    return true;
+}
+
+static bool rank_scan_host(const uint8_t* mask, int32_t* ranks, size_t n) {
+    HostCtx* c = host_ctx();
+    if (!c) return false;
+    auto* dm = static_cast<uint8_t*>(host_buf(*c, 0, n));
+    auto* dr = static_cast<int32_t*>(host_buf(*c, 1, n * 4));
+    if (!dm || !dr) return false;
+    TRY(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_rank_scan(dm, dr, n, c->stream));
+    TRY(cudaMemcpyAsync(ranks, dr, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    TRY(cudaStreamSynchronize(c->stream));
+    return true;
+}
+
+static bool count_true_host(const uint8_t* mask, size_t n, unsigned long long* h) {
+    HostCtx* c = host_ctx();
+    if (!c) return false;
+    auto* dm = static_cast<uint8_t*>(host_buf(*c, 0, n));
+    auto* dc = static_cast<unsigned long long*>(host_buf(*c, 1, 8));
+    if (!dm || !dc) return false;
+    TRY(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_count_true(dm, n, dc, c->stream));
+    TRY(cudaMemcpyAsync(h, dc, 8, cudaMemcpyDeviceToHost, c->stream));
+    TRY(cudaStreamSynchronize(c->stream));
+    return true;
+}
+
+static bool compact_host(const uint8_t* mask, int32_t* out, size_t n) {
+    HostCtx* c = host_ctx();
+    if (!c) return false;
+    auto* dm = static_cast<uint8_t*>(host_buf(*c, 0, n));
+    auto* dout = static_cast<int32_t*>(host_buf(*c, 1, n * 4));
+    auto* dc = static_cast<unsigned long long*>(host_buf(*c, 2, 8));
+    if (!dm || !dout || !dc) return false;
+    TRY(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_compact_indices(dm, dout, n, dc, c->stream));
+    TRY(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    TRY(cudaStreamSynchronize(c->stream));
+    return true;
+}
+
+static bool match_host(const int32_t* ra, size_t n, const int32_t* rb, size_t m, int32_t* row_out) {
+    HostCtx* c = host_ctx();
+    if (!c) return false;
+    auto* da = static_cast<int32_t*>(host_buf(*c, 0, n * 4));
+    auto* db = static_cast<int32_t*>(host_buf(*c, 1, (m ? m : 1) * 4));
+    auto* dout = static_cast<int32_t*>(host_buf(*c, 2, n * 4));
+    if (!da || !db || !dout) return false;
+    TRY(cudaMemcpyAsync(da, ra, n * 4, cudaMemcpyHostToDevice, c->stream));
+    if (m) TRY(cudaMemcpyAsync(db, rb, m * 4, cudaMemcpyHostToDevice, c->stream));
+    TRY(launch_match_first_equal(da, n, db, m, dout, c->stream));
+    TRY(cudaMemcpyAsync(row_out, dout, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    TRY(cudaStreamSynchronize(c->stream));
+    return true;
 }
 
 extern "C" {
@@ -112,54 +192,26 @@ const char* abmx_cuda_version(void) { return "abmx-b200 0.1.0 (sm_100a)"; }
 uint64_t abmx_cuda_launch_count(void) { return launches(); }
 
 // ---------------------------------------------------------------- 1. KernelTable (host ptrs)
+int abmx_cuda_table_status(void) { return g_table_status.load(); }
+void abmx_cuda_table_clear_status(void) { g_table_status.store(ABMX_OK); }
+
 void abmx_cuda_rank_scan(const uint8_t* mask, int32_t* ranks, size_t n) {
-    if (n == 0) return;
-    HostCtx& c = host_ctx();
-    auto* dm = static_cast<uint8_t*>(host_buf(c, 0, n));
-    auto* dr = static_cast<int32_t*>(host_buf(c, 1, n * 4));
-    DIE_ON(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(launch_rank_scan(dm, dr, n, c.stream));
-    DIE_ON(cudaMemcpyAsync(ranks, dr, n * 4, cudaMemcpyDeviceToHost, c.stream));
-    DIE_ON(cudaStreamSynchronize(c.stream));
+    if (n) rank_scan_host(mask, ranks, n);
 }
 
 int64_t abmx_cuda_count_true(const uint8_t* mask, size_t n) {
     if (n == 0) return 0;
-    HostCtx& c = host_ctx();
-    auto* dm = static_cast<uint8_t*>(host_buf(c, 0, n));
-    auto* dc = static_cast<unsigned long long*>(host_buf(c, 1, 8));
     unsigned long long h = 0;
-    DIE_ON(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(launch_count_true(dm, n, dc, c.stream));
-    DIE_ON(cudaMemcpyAsync(&h, dc, 8, cudaMemcpyDeviceToHost, c.stream));
-    DIE_ON(cudaStreamSynchronize(c.stream));
-    return static_cast<int64_t>(h);
+    return count_true_host(mask, n, &h) ? static_cast<int64_t>(h) : -1;
 }
 
 void abmx_cuda_compact_indices(const uint8_t* mask, int32_t* out, size_t n) {
-    if (n == 0) return;
-    HostCtx& c = host_ctx();
-    auto* dm = static_cast<uint8_t*>(host_buf(c, 0, n));
-    auto* dout = static_cast<int32_t*>(host_buf(c, 1, n * 4));
-    auto* dc = static_cast<unsigned long long*>(host_buf(c, 2, 8));
-    DIE_ON(cudaMemcpyAsync(dm, mask, n, cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(launch_compact_indices(dm, dout, n, dc, c.stream));
-    DIE_ON(cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, c.stream));
-    DIE_ON(cudaStreamSynchronize(c.stream));
+    if (n) compact_host(mask, out, n);
 }
 
 void abmx_cuda_match_first_equal(const int32_t* ra, size_t n, const int32_t* rb, size_t m,
                                  int32_t* row_out) {
-    if (n == 0) return;
-    HostCtx& c = host_ctx();
-    auto* da = static_cast<int32_t*>(host_buf(c, 0, n * 4));
-    auto* db = static_cast<int32_t*>(host_buf(c, 1, (m ? m : 1) * 4));
-    auto* dout = static_cast<int32_t*>(host_buf(c, 2, n * 4));
-    DIE_ON(cudaMemcpyAsync(da, ra, n * 4, cudaMemcpyHostToDevice, c.stream));
-    if (m) DIE_ON(cudaMemcpyAsync(db, rb, m * 4, cudaMemcpyHostToDevice, c.stream));
-    DIE_ON(launch_match_first_equal(da, n, db, m, dout, c.stream));
-    DIE_ON(cudaMemcpyAsync(row_out, dout, n * 4, cudaMemcpyDeviceToHost, c.stream));
-    DIE_ON(cudaStreamSynchronize(c.stream));
+    if (n) match_host(ra, n, rb, m, row_out);
 }
 
 void abmx_cuda_blend_i64(const uint8_t* mask, const int64_t* a, const int64_t* b, int64_t* out, size_t n) {
