@@ -116,6 +116,13 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------- reference arm
+def bench_config():
+    """The `config` of BOTH arms' JSON lines (identical, so the driver can pair them)."""
+    return {"workload": WORKLOAD, "replicas_per_gpu": 1, "seed": MASTER_SEED,
+            "l2": "GPU arm: L2 flushed before every timed step (untimed 256 MiB write, then 256 MiB "
+                  "read); reference arm: host CPU, no flush"}
+
+
 def reference_arm(args, world):
     """The reference's own CPU implementation (oracle/_ref: the unmodified abmx sources,
     -O3) on this host, same metric/config; rank 0 only."""
@@ -147,7 +154,7 @@ def reference_arm(args, world):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64+int", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "replicas": world},
+            "config": bench_config(),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -158,6 +165,44 @@ def reference_arm(args, world):
 # ---------------------------------------------------------------------- traffic (§8f rank 1)
 TRAFFIC_L = 349_526          # C4: one road, capacity 3L = 1,048,578 slots
 ROADS, ROADS_L, ROADS_STEPS = 3496, 100, 1000  # C4 roads variant (paper Table 3 shape)
+
+
+def golden_fnv(name):
+    """FNV-1a of the reference's own rows for a sharded workload (tests/golden/bench.json,
+    written by oracle/gen_bench_golden.py from the unmodified reference)."""
+    with open(os.path.join(ROOT, "tests", "golden", "bench.json")) as f:
+        return json.load(f)[name]["rows_fnv"]
+
+
+def gather_check(name, rows, rank, dist, device):
+    """one all-gather of the per-replica metrics rows (sharding.gather_rows, replica
+    order), then rank 0 checks the FNV-1a of the whole gathered block against the reference's
+    (single-process run: the local rows are the whole block). Returns (rows gathered, ok)."""
+    from paper_2508_16508_b200.sharding import gather_rows, rows_fnv
+    full = gather_rows(rows, dist, device=device) if dist is not None else rows
+    ok = None
+    if rank == 0:
+        ok = rows_fnv([full]) == golden_fnv(name)
+        if not ok:
+            raise RuntimeError(f"{name}: gathered rows differ from the reference's (FNV)")
+    return int(full.shape[0]), ok
+
+
+def traffic_roads(args, rank, world, allreduce, dist):
+    """C4 roads variant (3496 x L=100, 1000 steps) sharded by contiguous road blocks; one
+    all-gather of the metrics rows, checked on rank 0 against the reference's FNV."""
+    from paper_2508_16508_b200 import traffic as T
+    from paper_2508_16508_b200.sharding import shard_range
+    begin, count = shard_range(ROADS, world, rank)
+    T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS, begin=begin)
+    rows_r, rk = T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS,
+                             begin=begin)
+    gathered, fnv_ok = gather_check("C4_roads", rows_r, rank, dist, args.gather_device)
+    rk = allreduce(rk, dist.ReduceOp.MAX if dist else None)
+    return {"workload": f"{ROADS} roads x L={ROADS_L}, {ROADS_STEPS} steps (run_batch)",
+            "rows_gathered": gathered, "rows_match_reference": fnv_ok,
+            "value": ROADS * 3 * ROADS_L * ROADS_STEPS / (rk / 1e3), "unit": UNIT,
+            "device_ms": rk}
 
 
 def traffic_section(args, rank, world, allreduce, dist):
@@ -177,26 +222,13 @@ def traffic_section(args, rank, world, allreduce, dist):
     m.close()
     cap = 3 * TRAFFIC_L
     alg = 26 * cap  # 2N(lane 4 + cell 4 + active 1) + 2(3L)(occupancy 4)
-    per = ROADS // world
-    begin = rank * per
-    count = per if rank < world - 1 else ROADS - begin
-    T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS, begin=begin)
-    rows_r, rk = T.run_batch(T.TrafficConfig(ROADS_L, 10, 0.5), MASTER_SEED, count, ROADS_STEPS,
-                             begin=begin)
-    gathered = count
-    if dist is not None:  # one all-gather of the metrics rows, replica order
-        from paper_2508_16508_b200.sharding import gather_rows
-        gathered = gather_rows(rows_r, dist, device="cuda").shape[0]
-    rk = allreduce(rk, dist.ReduceOp.MAX if dist else None)
+    roads = traffic_roads(args, rank, world, allreduce, dist)
     out = {"workload": f"C4: one road L={TRAFFIC_L} (capacity {cap} slots) per GPU, period 10, "
                        f"green 0.5, seed {MASTER_SEED}",
            "value": world * cap * K / (tot / 1e3), "unit": UNIT, "ms_per_step": tot / K,
            "per_kernel_ms": kt,
            "step_effective_gbs": alg / (tot / K / 1e3) / 1e9,
-           "roads": {"workload": f"{ROADS} roads x L={ROADS_L}, {ROADS_STEPS} steps (run_batch)",
-                     "rows_gathered": gathered,
-                     "value": ROADS * 3 * ROADS_L * ROADS_STEPS / (rk / 1e3), "unit": UNIT,
-                     "device_ms": rk}}
+           "roads": roads}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle
@@ -230,23 +262,21 @@ def finance_section(args, rank, world, allreduce, dist):
     run_batch on the host for a bounded sample."""
     from paper_2508_16508_b200 import finance as F
     cfg = F.FinanceConfig()
-    per = MARKETS // world
-    begin = rank * per
-    count = per if rank < world - 1 else MARKETS - begin
+    from paper_2508_16508_b200.sharding import shard_range
+    begin, count = shard_range(MARKETS, world, rank)
     for _ in range(2):  # full-size warm-up runs (clocks, allocator, shared-memory carve-out)
         F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin)
     res = [F.run_batch(cfg, MASTER_SEED, count, FIN_STEPS, begin=begin) for _ in range(3)]
     ms = allreduce(statistics.median([r[1] for r in res]), dist.ReduceOp.MAX if dist else None)
-    gathered = count
-    if dist is not None:  # SURVEY §8e: one all-gather of the metrics rows, replica order
-        from paper_2508_16508_b200.sharding import gather_rows
-        r0 = res[0][0]
-        gathered = gather_rows(r0.reshape(r0.shape[0], r0.shape[1], -1), dist, device="cuda").shape[0]
+    r0 = res[0][0]
+    gathered, fnv_ok = gather_check("C5", r0.reshape(r0.shape[0], r0.shape[1], -1), rank, dist,
+                                    args.gather_device)
     slots = MARKETS * cfg.books * cfg.book_capacity
     out = {"workload": f"C5: {MARKETS} markets x FinanceConfig defaults (5 books x 1000 capacity, "
                        f"10 traders), {FIN_STEPS} steps (run_batch)",
            "value": slots * FIN_STEPS / (ms / 1e3), "unit": UNIT, "device_ms": ms,
            "timing": "median of 3 device-timed run_batch launches after 2 full-size warm-ups", "markets_gathered": gathered,
+           "rows_match_reference": fnv_ok,
            "market_steps_per_s": MARKETS * FIN_STEPS / (ms / 1e3)}
     # SURVEY §8d C5, the alternative reading: ONE market of 1024 books (one CTA per book; the
     # books share the traders, whose cash the books fold in with exact dyadic atomics). Not
@@ -379,16 +409,50 @@ def kernel_bytes(cfg, births, deaths):
             "k_update": 17 * n + 8 * deaths}  # energy read+write (2*8) + active write; zeroed ids
 
 
+def ensemble_section(args, rank, world, allreduce, barrier, dist):
+    """C3: 4096 x C1 replicas sharded by contiguous blocks over the ranks (sharding.shard_range);
+    one all-gather of the metrics rows, checked on rank 0 against the reference's FNV."""
+    import paper_2508_16508_b200 as abmx
+    from paper_2508_16508_b200.sharding import shard_range
+    begin, count = shard_range(ENSEMBLE_REPLICAS, world, rank)
+    c1 = abmx.PredationConfig(**C1)
+    abmx.run_batch(c1, MASTER_SEED, min(count, 296), 5, begin=begin, path=1)  # warm-up
+    barrier()
+    rows, kms = abmx.run_batch(c1, MASTER_SEED, count, ENSEMBLE_STEPS, begin=begin, path=1)
+    kmax = allreduce(kms, dist.ReduceOp.MAX if dist else None)
+    gathered, fnv_ok = gather_check("C3", rows, rank, dist, args.gather_device)
+    slots = ENSEMBLE_REPLICAS * capacity(C1) * ENSEMBLE_STEPS
+    c3_bytes = ENSEMBLE_REPLICAS * ENSEMBLE_STEPS * (42 * capacity(C1) + 2 * 100 * 100)
+    ens = {"workload": "C3: 4096 x C1 replicas (100x100, 600+400, caps 1024+1024), 100 steps, "
+                       "SMEM/register-resident CTA per replica",
+           "value": slots / (kmax / 1e3), "unit": UNIT, "kernel_ms": kmax,
+           "replicas_gathered": gathered, "rows_match_reference": fnv_ok, "scaling": "strong",
+           "effective_gbs": c3_bytes / (kmax / 1e3) / 1e9,
+           "note": "state stays on chip for all steps; effective GB/s uses SURVEY §8d bytes "
+                   "and may exceed HBM peak"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import pyoracle
+        if os.path.exists(pyoracle.REF_SO):
+            ref = pyoracle.Reference()
+            threads = os.cpu_count() or 1
+            nrep = 512  # a bounded sample of C3 (same C1 replicas, all host threads)
+            _, wall = ref.run_batch(C1, MASTER_SEED, nrep, ENSEMBLE_STEPS, threads=threads)
+            ens["cpu_baseline"] = {
+                "value": nrep * capacity(C1) * ENSEMBLE_STEPS / (wall / 1e3), "unit": UNIT,
+                "cores": threads, "kind": "reference",
+                "sample": f"reference run_batch(PredationModel), {nrep} C1 replicas x "
+                          f"{ENSEMBLE_STEPS} steps, {threads} threads ({wall / 1e3:.2f} s)"}
+    return ens
+
+
 def our_arm(args, rank, world, local_rank, dist):
     import numpy as np
     import torch
     import paper_2508_16508_b200 as abmx
 
-    torch.cuda.set_device(local_rank)
+    torch.cuda.set_device(local_rank % max(torch.cuda.device_count(), 1))
     K, W = args.steps, args.warmup
-    cfg = abmx.PredationConfig(**C2)
-    seed = abmx.replica_seeds(MASTER_SEED, world)[rank]
-    model = abmx.PredationModel(cfg, seed)
 
     def barrier():
         torch.cuda.synchronize()
@@ -398,9 +462,22 @@ def our_arm(args, rank, world, local_rank, dist):
     def allreduce(x, op):
         if dist is None:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=args.gather_device)
         dist.all_reduce(t, op=op)
         return float(t.item())
+
+    if args.sharded_only:  # the sharded workloads and their gather checks only
+        out = {"n_ranks": world, "backend": args.dist_backend if dist is not None else None,
+               "C3": ensemble_section(args, rank, world, allreduce, barrier, dist),
+               "C4_roads": traffic_roads(args, rank, world, allreduce, dist),
+               "C5": finance_section(args, rank, world, allreduce, dist)}
+        if rank == 0:
+            print(json.dumps({"sharded_check": out}))
+        return
+
+    cfg = abmx.PredationConfig(**C2)
+    seed = abmx.replica_seeds(MASTER_SEED, world)[rank]
+    model = abmx.PredationModel(cfg, seed)
 
     # warm-up (also builds and instantiates the CUDA graph)
     model.bench(1, W, FLUSH_BYTES)
@@ -443,27 +520,41 @@ def our_arm(args, rank, world, local_rank, dist):
         except Exception:
             traffic = None
     step_bytes = 42 * capacity(C2) + 2 * C2["width"] * C2["height"] + 8 * bd
-    # the access-pattern ceiling: the same random cell-word atomics / reads, and
-    # nothing else, in the same launch shape and live fractions, L2 flushed, event-timed
+    # the step's random cell-word accesses alone, in the same launch shape and live fractions, L2
+    # flushed, event-timed: their cost, not a bound (each includes the ~6 us launch + event floor;
+    # profiles/r02_c2_cost_model.md has the per-class measurements and the ncu evidence)
     n_tiles = capacity(C2) // 2 // 1024
     ls = float(met[0, :, 0].mean()) / C2["sheep_capacity"]
     lw = float(met[0, :, 1].mean()) / C2["wolf_capacity"]
     atom_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 0, True)
     read_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 1, True)
-    access = {"bound": "l2_random_atomics", "unit": "us",
-              "k_move_ceiling": atom_us, "k_move_achieved": avg["k_move"] * 1e3,
-              "k_move_frac": atom_us / (avg["k_move"] * 1e3),
-              "k_update_read_ceiling": read_us, "k_update_achieved": avg["k_update"] * 1e3,
-              "note": "ceiling = event-timed kernel doing ONLY the step's random cell-word "
-                      "atomicExch+atomicMax (k_move) / 16-byte reads (k_update), same grid and "
-                      "live fractions, L2 flushed; frac = ceiling time / kernel time"}
+    access = {"unit": "us", "k_move_random_atomics_alone": atom_us, "k_move": avg["k_move"] * 1e3,
+              "k_update_random_reads_alone": read_us, "k_update": avg["k_update"] * 1e3,
+              "note": "event-timed kernels doing ONLY the step's random cell-word atomicExch+atomicMax "
+                      "(k_move) / 16-byte reads (k_update), same grid and live fractions, L2 flushed; "
+                      "see profiles/r02_c2_cost_model.md"}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes": kb[dom], "avg_launch_ms": avg[dom],
                 "kernel_share": avg[dom] / step_sum,
                 "per_kernel_ms": avg,
                 "step_effective_gbs": step_bytes / (total_ms / K / 1e3) / 1e9,
-                "access_bound": access}
+                "random_access_cost": access}
+
+    # warm back-to-back figure beside the flushed headline: run() of K steps, no flush between
+    stream = torch.cuda.ExternalStream(model.stream)
+    model.run(t_next, K, metrics=False)
+    t_next += K
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record(stream)
+    model.run(t_next, K, metrics=False)
+    w1.record(stream)
+    w1.synchronize()
+    t_next += K
+    warm_ms = allreduce(w0.elapsed_time(w1), dist.ReduceOp.MAX if dist else None)
+    warm = {"value": world * capacity(C2) * K / (warm_ms / 1e3), "unit": UNIT, "ms_per_step": warm_ms / K,
+            "note": f"run() of {K} steps back to back on the engine stream (CUDA graph per step, "
+                    "the final births included), L2 NOT flushed between steps: not the headline"}
 
     # e2e through the C-ABI: step(t) [H2D t] + collect_metrics [D2H row], L2 flushed between
     flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
@@ -488,56 +579,7 @@ def our_arm(args, rank, world, local_rank, dist):
     del flush, flush2
     model.close()
 
-    # C3 ensemble, sharded by contiguous replica blocks; NCCL gathers the metrics rows
-    ens = None
-    if not args.no_ensemble:
-        per = ENSEMBLE_REPLICAS // world
-        begin = rank * per
-        count = per if rank < world - 1 else ENSEMBLE_REPLICAS - begin
-        c1 = abmx.PredationConfig(**C1)
-        abmx.run_batch(c1, MASTER_SEED, min(count, 296), 5, begin=begin, path=1)  # warm-up
-        barrier()
-        rows, kms = abmx.run_batch(c1, MASTER_SEED, count, ENSEMBLE_STEPS, begin=begin, path=1)
-        kmax = allreduce(kms, dist.ReduceOp.MAX if dist else None)
-        gathered = ENSEMBLE_REPLICAS
-        if dist is not None:
-            t = torch.from_numpy(rows).cuda()
-            sizes = [ENSEMBLE_REPLICAS // world] * (world - 1)
-            sizes.append(ENSEMBLE_REPLICAS - sum(sizes))
-            bufs = [torch.empty((s, ENSEMBLE_STEPS, 4), dtype=torch.float64, device="cuda")
-                    for s in sizes]
-            if t.shape[0] != sizes[rank]:
-                raise RuntimeError("shard size mismatch")
-            # all_gather needs equal sizes: pad to the largest shard
-            mx = max(sizes)
-            pad = torch.zeros((mx, ENSEMBLE_STEPS, 4), dtype=torch.float64, device="cuda")
-            pad[: t.shape[0]] = t
-            outs = [torch.empty_like(pad) for _ in range(world)]
-            dist.all_gather(outs, pad)
-            gathered = sum(o[:s].shape[0] for o, s in zip(outs, sizes))
-            del bufs
-        slots = ENSEMBLE_REPLICAS * capacity(C1) * ENSEMBLE_STEPS
-        c3_bytes = ENSEMBLE_REPLICAS * ENSEMBLE_STEPS * (42 * capacity(C1) + 2 * 100 * 100)
-        ens = {"workload": "C3: 4096 x C1 replicas (100x100, 600+400, caps 1024+1024), 100 steps, "
-                           "SMEM/register-resident CTA per replica",
-               "value": slots / (kmax / 1e3), "unit": UNIT, "kernel_ms": kmax,
-               "replicas_gathered": gathered, "scaling": "strong",
-               "effective_gbs": c3_bytes / (kmax / 1e3) / 1e9,
-               "note": "state stays on chip for all steps; effective GB/s uses SURVEY §8d bytes "
-                       "and may exceed HBM peak"}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            sys.path.insert(0, os.path.join(ROOT, "oracle"))
-            import pyoracle
-            if os.path.exists(pyoracle.REF_SO):
-                ref = pyoracle.Reference()
-                threads = os.cpu_count() or 1
-                nrep = 512  # a bounded sample of C3 (same C1 replicas, all host threads)
-                _, wall = ref.run_batch(C1, MASTER_SEED, nrep, ENSEMBLE_STEPS, threads=threads)
-                ens["cpu_baseline"] = {
-                    "value": nrep * capacity(C1) * ENSEMBLE_STEPS / (wall / 1e3), "unit": UNIT,
-                    "cores": threads, "kind": "reference",
-                    "sample": f"reference run_batch(PredationModel), {nrep} C1 replicas x "
-                              f"{ENSEMBLE_STEPS} steps, {threads} threads ({wall / 1e3:.2f} s)"}
+    ens = None if args.no_ensemble else ensemble_section(args, rank, world, allreduce, barrier, dist)
 
     traffic = None if args.no_traffic else traffic_section(args, rank, world, allreduce, dist)
     finance = None if args.no_finance else finance_section(args, rank, world, allreduce, dist)
@@ -562,11 +604,11 @@ def our_arm(args, rank, world, local_rank, dist):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
                 "warmup": W, "ms_per_step": max_ms / K, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64+int", "data": "synthetic",
-                "config": {"workload": WORKLOAD, "replicas_per_gpu": 1, "seed": MASTER_SEED,
-                           "l2": "flushed before every timed step (untimed 256 MiB write)",
-                           "timing": "CUDA events per step on the engine stream; max over ranks"},
+                "config": bench_config(),
+                "timing": "CUDA events per step on the engine stream (the last step's births, "
+                          "applied by k_finalize, inside its bracket); max over ranks",
                 "live_agent_steps_per_s": live_all / (max_ms / 1e3),
-                "e2e": e2e, "gpu_launches": int(launches), "clocks": clk.summary(),
+                "e2e": e2e, "warm_run": warm, "gpu_launches": int(launches), "clocks": clk.summary(),
                 "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens, "traffic": traffic,
                 "finance": finance, "agents": agents}
         print(json.dumps(line))
@@ -584,7 +626,13 @@ def main():
     ap.add_argument("--no-traffic", action="store_true")
     ap.add_argument("--no-finance", action="store_true")
     ap.add_argument("--no-agents", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: CPU collectives, for tests)")
+    ap.add_argument("--sharded-only", action="store_true",
+                    help="run only the sharded workloads (C3, C4 roads, C5) and print their "
+                         "gather checks; used by tests/test_bench_sharded_gpu.py")
     args = ap.parse_args()
+    args.gather_device = "cuda" if args.dist_backend == "nccl" else "cpu"
     if args.warmup < 3:
         args.warmup = 3  # timing rules: >= 3 warm-up steps
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -598,8 +646,12 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as D
-        torch.cuda.set_device(local_rank)
-        D.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dev = local_rank % max(torch.cuda.device_count(), 1)
+        torch.cuda.set_device(dev)
+        if args.dist_backend == "nccl":
+            D.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            D.init_process_group("gloo")
         dist = D
     try:
         our_arm(args, rank, world, local_rank, dist)

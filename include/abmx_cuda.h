@@ -48,6 +48,10 @@ const char* abmx_cuda_last_error(void);
 int abmx_cuda_table_status(void);
 void abmx_cuda_table_clear_status(void);
 const char* abmx_cuda_version(void);
+/* FNV-1a-64 of n bytes continuing from h (start with 0xcbf29ce484222325): the checksum the
+ * sharded benchmarks apply to gathered metrics rows (same definition as the reference-state
+ * hashes of the test fixtures). Host-side utility. */
+uint64_t abmx_fnv1a64(uint64_t h, const void* data, size_t n);
 /* number of kernels this library has launched in this process (all threads) */
 uint64_t abmx_cuda_launch_count(void);
 

@@ -189,6 +189,11 @@ extern "C" {
 
 const char* abmx_cuda_last_error(void) { return last_error(); }
 const char* abmx_cuda_version(void) { return "abmx-b200 0.1.0 (sm_100a)"; }
+uint64_t abmx_fnv1a64(uint64_t h, const void* data, size_t n) {
+    const unsigned char* p = static_cast<const unsigned char*>(data);
+    for (size_t i = 0; i < n; ++i) h = (h ^ p[i]) * 0x100000001b3ULL;
+    return h;
+}
 uint64_t abmx_cuda_launch_count(void) { return launches(); }
 
 // ---------------------------------------------------------------- 1. KernelTable (host ptrs)

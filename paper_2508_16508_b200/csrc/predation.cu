@@ -1619,11 +1619,14 @@ int Engine::bench(long long t0, long long steps, size_t flush_bytes, bool per_ke
         } else {
             CK(cudaEventRecord(e[0], stream));
             rc = enqueue_step(nullptr);
+            // the last step's births are applied by k_finalize (the next step's k_move applies
+            // them otherwise): inside the last step's bracket, so every timed step is complete
+            if (!rc && q == steps - 1) rc = finalize();
             CK(cudaEventRecord(e[1], stream));
         }
         if (rc) return rc;
     }
-    rc = finalize();  // the last step's births (outside the timed brackets)
+    rc = finalize();  // per-kernel mode: the last step's births (kernel times only)
     if (rc) return rc;
     CK(cudaStreamSynchronize(stream));
     for (long long q = 0; q < steps; ++q) {

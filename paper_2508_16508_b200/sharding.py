@@ -42,3 +42,22 @@ def gather_rows(rows, dist, device=None):
     outs = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(outs, pad)
     return np.concatenate([o[:c].cpu().numpy() for o, c in zip(outs, counts)], axis=0)
+
+
+def rows_fnv(arrays) -> int:
+    """FNV-1a-64 over the concatenated bytes of `arrays` (abmx_fnv1a64): checks gathered rows
+    against the checksums of the reference's outputs (tests/golden/bench.json)."""
+    import ctypes as C
+
+    import numpy as np
+
+    from . import lib
+
+    f = lib.abmx_fnv1a64
+    f.restype = C.c_uint64
+    f.argtypes = [C.c_uint64, C.c_void_p, C.c_size_t]
+    h = 0xcbf29ce484222325
+    for a in arrays:
+        a = np.ascontiguousarray(a)
+        h = f(h, a.ctypes.data, a.nbytes)
+    return int(h)

@@ -107,3 +107,13 @@ def test_gather_traffic_and_finance_shards(oracle, tmp_path):
     assert np.array_equal(np.load(out + ".t.npy"), oracle.traffic_run_batch(15, 10, 0.5, 13, total, steps))
     want_f = oracle.fin_run_batch(13, total, steps, books=2, book_capacity=32)
     assert np.array_equal(np.load(out + ".f.npy").reshape(total, steps, 2, 6), want_f)
+
+
+def test_rows_fnv_matches_the_fixture_hash():
+    """sharding.rows_fnv (the product's abmx_fnv1a64) is the checksum of the golden fixtures."""
+    import numpy as np
+    import pyoracle
+    from paper_2508_16508_b200.sharding import rows_fnv
+    rng = np.random.default_rng(3)
+    arrays = [rng.random((17, 5, 4)), np.arange(11, dtype=np.int64), np.zeros(0)]
+    assert rows_fnv(arrays) == pyoracle.fnv1a(arrays)
