@@ -156,6 +156,8 @@ def _sig(name, res, args):
 
 
 _sig("abmx_cuda_last_error", C.c_char_p, [])
+_sig("abmx_cuda_table_status", C.c_int, [])
+_sig("abmx_cuda_table_clear_status", None, [])
 _sig("abmx_cuda_version", C.c_char_p, [])
 _sig("abmx_cuda_launch_count", C.c_uint64, [])
 _sig("abmx_cuda_rank_scan", None, [u8p, i32p, C.c_size_t])
@@ -241,18 +243,22 @@ def rank_scan(mask) -> np.ndarray:
     m = _mask(mask)
     out = np.empty(m.size, np.int32)
     lib.abmx_cuda_rank_scan(_p(m, u8p), _p(out, i32p), m.size)
+    _check_table()
     return out
 
 
 def count_true(mask) -> int:
     m = _mask(mask)
-    return int(lib.abmx_cuda_count_true(_p(m, u8p), m.size))
+    n = int(lib.abmx_cuda_count_true(_p(m, u8p), m.size))
+    _check_table()
+    return n
 
 
 def compact_indices(mask) -> np.ndarray:
     m = _mask(mask)
     out = np.empty(m.size, np.int32)
     lib.abmx_cuda_compact_indices(_p(m, u8p), _p(out, i32p), m.size)
+    _check_table()
     return out
 
 
@@ -261,17 +267,39 @@ def match_first_equal(ra, rb) -> np.ndarray:
     b = np.ascontiguousarray(rb, dtype=np.int32)
     out = np.empty(a.size, np.int32)
     lib.abmx_cuda_match_first_equal(_p(a, i32p), a.size, _p(b, i32p), b.size, _p(out, i32p))
+    _check_table()
     return out
 
 
 def _blend(fn, dt, pt, mask, a, b, out=None):
+    """out = mask ? a : b elementwise. Lengths are checked (the C entry reads and writes
+    mask.size elements through raw pointers); `out` must be a C-contiguous array of dtype `dt`
+    and the mask's size, else the result is computed into a fresh array and copied into it."""
     m = _mask(mask)
     a = np.ascontiguousarray(a, dtype=dt)
     b = np.ascontiguousarray(b, dtype=dt)
-    if out is None:
-        out = np.empty(m.size, dt)
-    fn(_p(m, u8p), _p(a, pt), _p(b, pt), _p(out, pt), m.size)
-    return out
+    if a.size != m.size or b.size != m.size:
+        raise ValueError(f"blend: mask has {m.size} elements, a {a.size}, b {b.size}")
+    direct = (out is not None and isinstance(out, np.ndarray) and out.dtype == dt and out.flags.c_contiguous
+              and out.flags.writeable)
+    if out is not None and np.size(out) != m.size:
+        raise ValueError(f"blend: out has {np.size(out)} elements, mask {m.size}")
+    res = out if direct else np.empty(m.size, dt)
+    fn(_p(m, u8p), _p(a, pt), _p(b, pt), _p(res, pt), m.size)
+    _check_table()
+    if out is not None and not direct:
+        out[...] = res.reshape(np.shape(out))
+        return out
+    return res
+
+
+def _check_table():
+    """The synchronous KernelTable entries record CUDA failures instead of aborting
+    (abmx_cuda_table_status): surface one as CudaError."""
+    if lib.abmx_cuda_table_status() != 0:
+        msg = lib.abmx_cuda_last_error().decode()
+        lib.abmx_cuda_table_clear_status()
+        raise CudaError(msg)
 
 
 def blend_i64(mask, a, b, out=None):

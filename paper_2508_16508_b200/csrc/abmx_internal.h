@@ -11,11 +11,17 @@
 
 namespace abmx_internal {
 
-int num_sms();
-// cudaMallocAsync from the device's default pool, kept cached: the pool's default release
-// threshold (0) hands freed memory back at every synchronisation, so the next call would map
-// it afresh (177 -> 52 us per agent-set lifecycle cycle)
+constexpr int kMaxDevices = 64;
+int num_sms();  // of the current device
+// stream-ordered scratch from the library's own per-device pool, kept cached (up to 1 GiB)
+// across synchronisations (177 -> 52 us per agent-set lifecycle cycle)
 cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s);
+// raise (never lower) a kernel's dynamic shared-memory limit on the current device
+cudaError_t raise_dyn_smem(const void* fn, size_t bytes);
+template <class F>
+cudaError_t raise_dyn_smem(F* fn, size_t bytes) {
+    return raise_dyn_smem(reinterpret_cast<const void*>(fn), bytes);
+}
 template <class T>
 cudaError_t malloc_async(T** p, size_t bytes, cudaStream_t s) {
     return malloc_async(reinterpret_cast<void**>(p), bytes, s);

@@ -19,28 +19,72 @@ namespace abmx_internal {
 static std::atomic<unsigned long long> g_launches{0};
 static thread_local std::string t_error;
 
-int num_sms() {
-    static int n = [] {
-        int dev = 0, v = 0;
-        if (cudaGetDevice(&dev) != cudaSuccess) return 148;
-        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 148;
-        return v > 0 ? v : 148;
-    }();
-    return n;
-}
-cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
-    static std::atomic<unsigned long long> kept{0};  // devices whose pool is already set
+static int current_device() {
     int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess && dev >= 0 && dev < 64 && !(kept.load() >> dev & 1ULL)) {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            unsigned long long thr = ~0ULL;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return 0;
+    return dev;
+}
+
+// SM count of the CURRENT device (cached per device: a process may drive several GPUs)
+int num_sms() {
+    static std::atomic<int> cache[kMaxDevices] = {};
+    const int dev = current_device();
+    int n = cache[dev].load(std::memory_order_relaxed);
+    if (n > 0) return n;
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cache[dev].store(v, std::memory_order_relaxed);
+    return v;
+}
+
+// The library's scratch memory comes from its OWN stream-ordered pool per device (the device's
+// default pool, which other libraries in the process use, is left alone). The pool keeps up to
+// kScratchKeep bytes across synchronisations: its default release threshold (0) would hand the
+// memory back at every sync and the next call would map it afresh.
+constexpr unsigned long long kScratchKeep = 1ULL << 30;
+cudaError_t malloc_async(void** p, size_t bytes, cudaStream_t s) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[kMaxDevices] = {};
+    const int dev = current_device();
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (!pools[dev]) {
+            cudaMemPoolProps props{};
+            props.allocType = cudaMemAllocationTypePinned;
+            props.location.type = cudaMemLocationTypeDevice;
+            props.location.id = dev;
+            cudaError_t e = cudaMemPoolCreate(&pools[dev], &props);
+            if (e != cudaSuccess) {
+                pools[dev] = nullptr;
+                return e;
+            }
+            unsigned long long thr = kScratchKeep;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
         }
-        (void)cudaGetLastError();
-        kept.fetch_or(1ULL << dev);
+        pool = pools[dev];
     }
-    return cudaMallocAsync(p, bytes, s);
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+// cudaFuncAttributeMaxDynamicSharedMemorySize is ONE setting per function and device for the
+// whole process: engines of different sizes (and host threads) share it. It only ever grows,
+// under a lock, so a smaller engine created later never lowers the limit a larger one needs.
+cudaError_t raise_dyn_smem(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, const void*>, size_t>> seen;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : seen)
+        if (e.first.first == dev && e.first.second == fn) {
+            if (bytes <= e.second) return cudaSuccess;
+            const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+            if (r == cudaSuccess) e.second = bytes;
+            return r;
+        }
+    const cudaError_t r = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+    if (r == cudaSuccess) seen.push_back({{dev, fn}, bytes});
+    return r;
 }
 void count_launch(int k) { g_launches.fetch_add(static_cast<unsigned long long>(static_cast<long long>(k))); }
 unsigned long long launches() { return g_launches.load(); }

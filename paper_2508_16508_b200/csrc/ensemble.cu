@@ -527,7 +527,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
             case 4: kern = k_ensemble<4>; break;
             default: kern = k_ensemble<8>; break;
         }
-        CKE(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, P.smem));
+        CKE(abmx_internal::raise_dyn_smem(kern, static_cast<size_t>(P.smem)));
         CKE(cudaEventRecord(ea, st));
         (void)cudaGetLastError();
         kern<<<count, kT, P.smem, st>>>(P);

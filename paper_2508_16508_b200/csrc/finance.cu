@@ -861,7 +861,7 @@ struct abmx_finance {
             keyed_ok = ks <= 226 * 1024 && c.delta < 1.0 && !std::isnan(c.init_price);
             const int lim = static_cast<int>(keyed_ok && ks > smem ? ks : smem);
             for (const void* f : fns)
-                CKF(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, lim));
+                CKF(abmx_internal::raise_dyn_smem(f, static_cast<size_t>(lim)));
         }
         (void)cudaGetLastError();
         k_fin_init<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(P, quantize_host(c.init_price));

@@ -1102,10 +1102,8 @@ int Engine::create(const abmx_predation_config& c, const uint64_t* seeds, int R_
         CK(cudaStreamSynchronize(stream));  // the host vectors must be consumed
     }
     move_smem = static_cast<size_t>(P.status_stride + 1) * 8;
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_move), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(move_smem)));
-    CK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k_finalize), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            static_cast<int>(move_smem)));
+    CK(abmx_internal::raise_dyn_smem(k_move, move_smem));
+    CK(abmx_internal::raise_dyn_smem(k_finalize, move_smem));
     P.epoch = 1;
     P.t = 1;
     P.metrics = d_metrics_step;

@@ -559,8 +559,7 @@ static cudaError_t launch_scan_pipe(const uint8_t* d_mask, int32_t* d_out, size_
                                     cudaStream_t s) {
     const size_t tiles = (n + kPTile - 1) / kPTile;
     constexpr int smem = pipe_smem<kCompact>();
-    // the attribute is per function and per device: set it on every call (cheap next to the scan)
-    cudaError_t e = cudaFuncSetAttribute(scan_pipe_kernel<kCompact>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = raise_dyn_smem(scan_pipe_kernel<kCompact>, static_cast<size_t>(smem));
     if (e != cudaSuccess) return e;
     // co-resident grid: every CTA waits for all chunk totals (cooperative launch guarantees it)
     int per_sm = 0;

@@ -323,7 +323,7 @@ int traffic_ensemble_run(const abmx_traffic_config& cfg, const uint64_t* seeds, 
     if ((e = abmx_internal::malloc_async(&d_seeds, static_cast<size_t>(count) * 8, s)) != cudaSuccess ||
         (e = abmx_internal::malloc_async(&d_phase, static_cast<size_t>(count) * 8, s)) != cudaSuccess ||
         (e = abmx_internal::malloc_async(&d_metrics, mb, s)) != cudaSuccess ||
-        (e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem))) !=
+        (e = abmx_internal::raise_dyn_smem(kfn, static_cast<size_t>(smem))) !=
             cudaSuccess) {
         set_error(std::string("traffic ensemble: ") + cudaGetErrorString(e));
         rc = ABMX_E_CUDA;

@@ -246,3 +246,18 @@ def test_quantity_and_cash_envelopes(abmx, F):
     with pytest.raises(abmx.DomainError):
         m.run(1, 40)
 
+
+
+def test_small_market_after_large_keeps_the_large_one_runnable(F):
+    """k_fin's dynamic shared-memory limit is one setting per kernel; a smaller market
+    created after a larger one must not lower it below what the larger one launches with."""
+    big_cfg = F.FinanceConfig(book_capacity=2000, traders=200)  # ~100 KB of book per CTA
+    big = F.FinanceModel(big_cfg, 11)
+    big.run(1, 3)
+    small = F.FinanceModel(F.FinanceConfig(), 12)
+    small.run(1, 3)
+    got = big.run(4, 5)
+    fresh = F.FinanceModel(big_cfg, 11)
+    fresh.run(1, 3)
+    want = fresh.run(4, 5)
+    assert np.array_equal(np.asarray(got), np.asarray(want))

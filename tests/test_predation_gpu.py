@@ -405,3 +405,23 @@ def test_c2_scale_100_steps_both_paths(abmx, oracle):
         orc.step(t)
         assert rows[t - 11].astype(np.int64).tolist() == orc.metrics(), t
     assert_same_state(gpu, orc, "C2 t=100")
+
+
+def test_small_engine_after_large_keeps_the_large_one_runnable(abmx):
+    """the dynamic shared-memory limit is one setting per kernel; creating a smaller
+    engine after a larger one must not lower it below what the larger one launches with."""
+    # 7M sheep slots: k_move's tile-count prefix needs ~55 KB of dynamic shared memory, above
+    # the 48 KB default; the tiny model needs ~1 KB
+    big_cfg = abmx.PredationConfig(**c1(width=1024, height=1024, n_sheep0=200000, n_wolves0=20000,
+                                        sheep_capacity=7000000, wolf_capacity=300000))
+    big = abmx.PredationModel(big_cfg, 5)
+    big.step(1)
+    small = abmx.PredationModel(abmx.PredationConfig(**tiny()), 6)
+    small.step(1)
+    for t in range(2, 5):
+        big.step(t)  # would fail with an invalid-argument launch if the limit had shrunk
+    fresh = abmx.PredationModel(big_cfg, 5)
+    for t in range(1, 5):
+        fresh.step(t)
+    assert big.collect_metrics().tolist() == fresh.collect_metrics().tolist()
+    assert state_hash(big) == state_hash(fresh)

@@ -194,3 +194,20 @@ def test_first_equal_np_matches_oracle(oracle):
         rb = rng.integers(-20, 20, m).astype(np.int32)
         ra = rng.integers(-25, 25, 3000).astype(np.int32)
         assert np.array_equal(first_equal_np(ra, rb), oracle.match_first_equal(ra, rb))
+
+
+def test_blend_checks_lengths_and_out(abmx):
+    m = np.array([1, 0, 1, 0], np.uint8)
+    a = np.arange(4, dtype=np.int64)
+    b = -np.arange(4, dtype=np.int64)
+    with pytest.raises(ValueError):
+        abmx.blend_i64(m, a[:3], b)
+    with pytest.raises(ValueError):
+        abmx.blend_i64(m, a, b, out=np.empty(3, np.int64))
+    out = np.zeros(8, np.int64)[::2]  # non-contiguous: computed, then copied in
+    assert abmx.blend_i64(m, a, b, out=out) is out
+    assert out.tolist() == [0, -1, 2, -3]
+    o32 = np.zeros(4, np.float32)  # another dtype: copied in as well
+    abmx.blend_f64(m, a.astype(np.float64), b.astype(np.float64), out=o32)
+    assert o32.tolist() == [0.0, -1.0, 2.0, -3.0]
+    assert abmx.lib.abmx_cuda_table_status() == 0
