@@ -48,4 +48,4 @@ def test_reference_arm_replicas_on_rank0(reference, world):
     p = run_bench({"RANK": "0", "WORLD_SIZE": str(world), "LOCAL_RANK": "0"}, "--steps", "1")
     assert p.returncode == 0, p.stderr
     d = json.loads(p.stdout.strip().splitlines()[-1])
-    assert d["n_gpus"] == world and d["config"]["replicas"] == world and d["value"] > 0
+    assert d["n_gpus"] == world and d["config"]["replicas_per_gpu"] == 1 and d["value"] > 0
