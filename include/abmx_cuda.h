@@ -178,6 +178,9 @@ int abmx_diag_random_access(int64_t cells, int32_t sheep_ctas, int32_t wolf_ctas
  * by builds compiled with -DABMX_PRED_TRACE; [2][CTAs][8], returns the number of entries */
 int abmx_predation_set_trace(abmx_predation* h, int32_t enable);
 int64_t abmx_predation_trace(abmx_predation* h, uint64_t* out, int64_t cap);
+/* diagnostics: in a -DABMX_CHECKED build, the id of the first device bounds check that failed in
+ * the predation kernels (0 = none); -1 in normal builds */
+int abmx_predation_check_status(void);
 /* device-resident bytes of h (state + scratch) */
 int64_t abmx_predation_device_bytes(abmx_predation* h);
 /* Device-timed steps t0..t0+steps-1 for benchmarking: before each step an (untimed) write

@@ -462,6 +462,7 @@ int abmx_predation_kernel_times(abmx_predation* h, double* ms, int64_t* launches
     }
     return ABMX_OK;
 }
+int abmx_predation_check_status(void) { return abmx_pred::check_status(); }
 int64_t abmx_predation_device_bytes(abmx_predation* h) { return h ? h->eng.device_bytes : 0; }
 int abmx_predation_bench(abmx_predation* h, int64_t t0, int64_t steps, int64_t flush_bytes, int32_t per_kernel,
                          double* step_ms) {

@@ -43,10 +43,26 @@ namespace abmx_pred {
 __constant__ int c_dx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
 __constant__ int c_dy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
 
+// Checked builds (-DABMX_CHECKED, tools/build_variant.sh checked "-DABMX_CHECKED"): every index
+// into the slot columns, the cell words and the list links is bounds-checked on the device; the
+// first failing check id is kept in g_check_fail (abmx_predation_check_status). compute-sanitizer
+// is closed on this GPU pool, so this is the out-of-bounds net of tools/sanitize_smoke.py.
+#ifdef ABMX_CHECKED
+__device__ unsigned g_check_fail;
+#define ABMX_CHECK(cond, id)                                         \
+    do {                                                             \
+        if (!(cond)) atomicCAS(&abmx_pred::g_check_fail, 0u, (id));  \
+    } while (0)
+#else
+#define ABMX_CHECK(cond, id) ((void)0)
+#endif
+
 __device__ __forceinline__ size_t sidx(const Params& P, int s, int r, int i) {
+    ABMX_CHECK(r >= 0 && r < P.R && i >= 0 && i + kS <= P.Npad[s], 1u);
     return static_cast<size_t>(r) * P.Npad[s] + i;
 }
 __device__ __forceinline__ size_t cidx(const Params& P, int r, int c) {
+    ABMX_CHECK(r >= 0 && r < P.R && c >= 0 && c < P.C, 2u);
     return static_cast<size_t>(r) * P.Cpad + c;
 }
 // exact fixed-point image of an energy on the 2^-20 grid (predation.hpp:60-63)
@@ -336,6 +352,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
                 if (static_cast<int>(rank) < pairs) {
                     const int vt = find_tile(s_pre, tiles, rank, false);
                     vrow[k] = vt * kTile + static_cast<int>(rank - lo31(s_pre[vt]));
+                    ABMX_CHECK(vrow[k] >= 0 && vrow[k] < P.Npad[s] && static_cast<int>(rank) < P.Npad[s], 3u);
                     brank[k] = rank;
                     born[k] = true;
                 }
@@ -457,7 +474,10 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
             unsigned pos = s_base + static_cast<unsigned>(off);
 #pragma unroll
             for (int k = 0; k < kS; ++k)
-                if (first[k]) P.occ[pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
+                if (first[k]) {
+                    ABMX_CHECK(pos < static_cast<unsigned>(P.R) * static_cast<unsigned>(P.Npad[1]), 8u);
+                    P.occ[pos++] = (static_cast<unsigned long long>(r) << 32) | static_cast<uint32_t>(cell[k]);
+                }
         }
     }
 }
@@ -510,6 +530,7 @@ __device__ unsigned long long wolf_cell(const Params& P, unsigned long long ent,
     int wl[kSmallList], sl[kSmallList];
     int lw = 0, ls = 0;
     for (int w = w0, v = s0; w >= 0 || v >= 0;) {
+        ABMX_CHECK(w < P.Npad[1] && v < P.Npad[0], 6u);
         const int nw = w >= 0 ? P.next[1][wb + w] : -1;
         const int nv = v >= 0 ? P.next[0][sb + v] : -1;
         if (w >= 0) {
@@ -535,6 +556,7 @@ __device__ unsigned long long wolf_cell(const Params& P, unsigned long long ent,
         // every agent sits in exactly one cell list, so the pool (R * (Npad0 + Npad1) entries)
         // cannot overflow
         const unsigned off = atomicAdd(&P.ctl->pool_top, static_cast<unsigned>(lw + ls));
+        ABMX_CHECK(static_cast<long long>(off) + lw + ls <= P.pool_size, 7u);
         int* pw = P.pool + off;
         int* ps = pw + lw;
         int q = 0;
@@ -671,6 +693,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
                     int nm[kS], no[kS];
 #pragma unroll
                     for (int k = 0; k < kS; ++k) {  // all hops of this round issued together
+                        ABMX_CHECK(cm[k] < P.Npad[s] && co[k] < P.Npad[s ^ 1], 4u);
                         nm[k] = cm[k] >= 0 ? nmine[cm[k]] : -1;
                         no[k] = co[k] >= 0 ? noth[co[k]] : -1;
                     }
@@ -754,6 +777,7 @@ __device__ void update_phase(const Params& P, unsigned b) {
 #pragma unroll
     for (int k = 0; k < kS; ++k)
         if (valid[k]) {
+            ABMX_CHECK(vr >= 0 && vr < kTile, 5u);
             P.row_at[s][tb + vr] = i0 + k;
             P.rowcell[s][tb + vr] = cell[k];
             P.rowE[s][tb + vr] = child[k];
@@ -1209,6 +1233,17 @@ int Engine::finalize() {
     params.pending = 0;
     params.book = 1;
     return ABMX_OK;
+}
+
+// checked builds: the first failing device bounds check (0 = none); -1 in normal builds
+int check_status() {
+#ifdef ABMX_CHECKED
+    unsigned v = 0;
+    if (cudaMemcpyFromSymbol(&v, g_check_fail, sizeof v) != cudaSuccess) return -2;
+    return static_cast<int>(v);
+#else
+    return -1;
+#endif
 }
 
 int Engine::set_t(long long t) {

@@ -106,6 +106,7 @@ struct Params {
 const char* kernel_name(int k);
 
 int check_create(const abmx_predation_config& c);  // init_predation's errors (predation.cu)
+int check_status();  // checked builds: first failing device bounds check; -1 otherwise
 
 struct Engine {
     abmx_predation_config cfg{};
