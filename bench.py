@@ -352,7 +352,12 @@ def agents_section(args, rank):
         arr, keep = s._rows({k: torch.from_numpy(v).cuda() for k, v in rows.items()}, cap)
         return s, arr, keep
 
-    def cycle(s, arr, k):
+    def cycle(s, arr, k):  # abmx_agents_lifecycle: remove + spawn fused into two kernels
+        stream = s._stream()
+        abmx._check(abmx.lib.abmx_agents_lifecycle(C.byref(s._c), dk[k].data_ptr(), cap, dv[k].data_ptr(), arr, 0, 0,
+                                                   out.data_ptr(), res.data_ptr(), stream))
+
+    def cycle_two_calls(s, arr, k):  # the same cycle as abmx_agents_remove + abmx_agents_spawn
         stream = s._stream()
         abmx._check(abmx.lib.abmx_agents_remove(C.byref(s._c), dk[k].data_ptr(), out.data_ptr(), stream))
         abmx._check(abmx.lib.abmx_agents_spawn(C.byref(s._c), cap, dv[k].data_ptr(), arr, 0, 0,
@@ -373,10 +378,24 @@ def agents_section(args, rank):
         ev[k][1].record()
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    s2, arr2, keep2 = make()  # the unfused two-call cycle on the same inputs, for comparison
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    for k in range(K):
+        flush.fill_(k)
+        flush2.sum()
+        ev2[k][0].record()
+        cycle_two_calls(s2, arr2, k)
+        ev2[k][1].record()
+    torch.cuda.synchronize()
+    ms_two = sum(a.elapsed_time(b) for a, b in ev2) / K
+    same = all(np.array_equal(a, b) for a, b in zip(s.to_numpy().values(), s2.to_numpy().values()))
     out_d = {"workload": f"lifecycle cycles on a {cap}-slot set (e:i64, w:f64, f:u8; 70% live): "
                          f"remove_agents of {AGENT_CHURN} random slots + spawn_agents of {cap} rows with "
-                         f"{AGENT_CHURN} valid, copy apply; {K} cycles, L2 flushed before each",
-             "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms}
+                         f"{AGENT_CHURN} valid, copy apply (fused: abmx_agents_lifecycle); {K} cycles, "
+                         f"L2 flushed before each",
+             "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms,
+             "launches_per_cycle": "1 memset + 2 kernels (abmx_agents_lifecycle)",
+             "two_call_ms_per_cycle": ms_two, "fused_equals_two_calls": bool(same)}
     if rank == 0 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle

@@ -63,6 +63,8 @@ for _n in ("abmx_agents_set_rm", "abmx_agents_set_sci"):
     _sig(_n, [_P, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(_Column), C.c_void_p, C.c_void_p,
               C.c_void_p, C.c_void_p])
 _sig("abmx_agents_set_mask", [_P, C.c_void_p, C.POINTER(_Column), C.c_void_p])
+_sig("abmx_agents_lifecycle", [_P, C.c_void_p, C.c_int32, C.c_void_p, C.POINTER(_Column), C.c_int32, C.c_int64,
+                               C.c_void_p, C.c_void_p, C.c_void_p])
 _sig("abmx_agents_select", [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p])
 _sig("abmx_agents_pinned_keys", [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p])
 _sig("abmx_agents_sort_perm", [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_void_p,
@@ -255,6 +257,24 @@ class DeviceAgentSet:
         del keep
         return SpawnOutcome(spawned, dropped, slots[:spawned].cpu().numpy(),
                             rws[:spawned].cpu().numpy())
+
+    def lifecycle(self, kill, rows: dict, valid, agent_type=None):
+        """remove_agents(kill) then spawn_agents(rows, valid) (lifecycle.cpp:124-195) in one
+        fused call (two kernels); returns (removed, spawned, dropped)."""
+        torch = _torch()
+        k = self._mask(kill)
+        v = torch.as_tensor(valid, device=self.device)
+        m = int(v.numel())
+        v = self._mask(v, m)
+        arr, keep = self._rows(rows, m)
+        kd = torch.zeros(1, dtype=torch.int64, device=self.device)
+        res = torch.zeros(2, dtype=torch.int64, device=self.device)
+        _check(lib.abmx_agents_lifecycle(C.byref(self._c), k.data_ptr(), m, v.data_ptr(), arr,
+                                         int(agent_type is not None), int(agent_type or 0), kd.data_ptr(),
+                                         res.data_ptr(), self._stream()))
+        spawned, dropped = (int(x) for x in res.cpu().tolist())
+        del keep
+        return int(kd.item()), spawned, dropped
 
     # -------------------------------------------------------------- subset updates
     def _set_rows(self, fn, target, rows, valid) -> PairOutcome:

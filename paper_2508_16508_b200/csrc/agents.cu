@@ -245,6 +245,103 @@ __global__ void __launch_bounds__(kT) k_remove_apply(const int32_t* __restrict__
 }
 __global__ void k_remove_commit(const long long* count, Life L, long long* out) { remove_commit(count, L, out); }
 
+// ---------------------------------------------------------------- fused lifecycle cycle
+// remove_agents(kill) then spawn_agents(rows, valid) (lifecycle.cpp:124-195) in TWO kernels:
+//   k_life_select  one ticketed single pass over the slot tiles and the row tiles. A slot tile
+//                  counts (killed, free-after-removal) packed, looks back once, resets its killed
+//                  slots on the spot (the retired push goes to top + killed prefix: slot order)
+//                  and lists its free slots; a row tile lists its valid rows.
+//   k_life_apply   pair k < min(F, Q): the k-th free slot takes the k-th valid row; ids pop the
+//                  retired stack (now top + K deep) LIFO first; the last CTA commits the counters.
+struct LifeCounts {  // written by the last slot / row tile
+    long long free_, valid, killed;
+};
+
+__global__ void __launch_bounds__(kT) k_life_select(const uint8_t* __restrict__ kill, size_t n, int32_t* __restrict__ slots,
+                                                    ScanWs* wa, unsigned ta, const uint8_t* __restrict__ valid, size_t m,
+                                                    int32_t* __restrict__ rows, ScanWs* wb, Cols C, Life L,
+                                                    LifeCounts* cnt) {
+    if (blockIdx.x >= ta) {  // row tiles: the valid rows, slot order
+        select_tile<kSelMask>(valid, nullptr, m, rows, &cnt->valid, wb, gridDim.x - ta);
+        return;
+    }
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ unsigned s_tile;
+    __shared__ unsigned long long s_look[kT / 32 + 2];
+    if (threadIdx.x == 0) s_tile = atomicAdd(&wa->ticket, 1u);
+    __syncthreads();
+    const unsigned tile = s_tile;
+    const size_t base = static_cast<size_t>(tile) * kTile + static_cast<size_t>(threadIdx.x) * kItems;
+    uint8_t kk[kItems], a[kItems];
+    load16(kill, base, n, kk);
+    load16(L.active, base, n, a);
+    bool killed[kItems], fr[kItems];
+    unsigned nk = 0, nf = 0;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const bool in = base + k < n;
+        killed[k] = in && a[k] != 0 && kk[k] != 0;
+        fr[k] = in && (a[k] == 0 || killed[k]);  // free once the removal is done
+        nk += killed[k];
+        nf += fr[k];
+    }
+    unsigned long long total;
+    const unsigned long long excl = block_excl_scan<kT>(pack2(nk, nf), s_scan, &total);
+    __syncthreads();
+    const unsigned long long pre = block_lookback<kT>(wa->status, static_cast<int>(tile), total, s_look);
+    const long long top = L.recycle ? L.counters[2] : 0;
+    long long kpos = static_cast<long long>(hi31(pre)) + hi31(excl);  // killed before this thread
+    long long fpos = static_cast<long long>(lo31(pre)) + lo31(excl);      // free before this thread
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const size_t slot = base + k;
+        if (killed[k]) {  // remove_agents: reset_slot (type kept), push the id
+            if (L.recycle) L.retired[top + kpos] = L.ids[slot];
+            ++kpos;
+            L.active[slot] = 0;
+            L.ids[slot] = 0;
+            L.ages[slot] = 0;
+            for (int c = 0; c < C.n; ++c) zero_elem(C.dst[c], static_cast<long long>(slot), C.sz[c]);
+        }
+        if (fr[k]) slots[fpos++] = static_cast<int32_t>(slot);
+    }
+    if (tile == ta - 1 && threadIdx.x == 0) {
+        cnt->killed = static_cast<long long>(hi31(pre) + hi31(total));
+        cnt->free_ = static_cast<long long>(lo31(pre) + lo31(total));
+    }
+}
+
+__global__ void __launch_bounds__(kT) k_life_apply(const int32_t* __restrict__ slots, const int32_t* __restrict__ rows,
+                                                   const LifeCounts* cnt, Cols C, Life L, int set_type,
+                                                   long long agent_type, unsigned* done, long long* out_killed,
+                                                   long long* out) {
+    const long long K = cnt->killed;
+    const long long r = min(cnt->free_, cnt->valid);
+    const long long nid = L.counters[1];
+    const long long top = (L.recycle ? L.counters[2] : 0) + (L.recycle ? K : 0);  // after the pushes
+    for (long long k = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; k < r;
+         k += static_cast<long long>(gridDim.x) * kT) {
+        const int slot = slots[k], row = rows[k];
+        for (int c = 0; c < C.n; ++c)
+            if (C.src[c]) copy_elem(C.dst[c], slot, C.src[c], row, C.sz[c]);
+        L.active[slot] = 1;
+        L.ids[slot] = k < top ? L.retired[top - 1 - k] : nid + (k - top);
+        L.ages[slot] = 0;
+        if (set_type) L.types[slot] = agent_type;
+    }
+    if (last_cta(done) && threadIdx.x == 0) {  // counters (lifecycle.cpp:136-141, 186-194)
+        const long long used = min(top, r);
+        L.counters[0] += r - K;
+        L.counters[1] += r - used;
+        if (L.recycle) L.counters[2] = top - used;
+        if (out_killed) *out_killed = K;
+        if (out) {
+            out[0] = r;
+            out[1] = cnt->valid - r;
+        }
+    }
+}
+
 // set_agents_mask with per-slot source values: dst[c][i] <- src[c][i] where mask[i].
 __global__ void __launch_bounds__(kT) k_mask_apply(const uint8_t* __restrict__ mask, size_t n, Cols C) {
     for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT)
@@ -632,6 +729,72 @@ int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* 
     if (rc) return rc;
     if (committed) return ABMX_OK;
     k_remove_commit<<<1, 1, 0, st>>>(cnt, L, reinterpret_cast<long long*>(d_killed));
+    abmx_internal::count_launch();
+    CKA(cudaGetLastError());
+    return ABMX_OK;
+}
+
+int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_t m, const uint8_t* d_valid,
+                          const abmx_column* rows, int32_t set_type, int64_t agent_type, int64_t* d_killed,
+                          int64_t* d_result, void* stream) {
+    int rc = check_set(s);
+    if (rc) return rc;
+    if ((s->capacity > 0 && !d_kill) || m < 0 || (m > 0 && !d_valid)) {
+        abmx_internal::set_error("bad lifecycle arguments");
+        return ABMX_E_ARG;
+    }
+    for (int c = 0; c < s->n_state; ++c)
+        if (rows && rows[c].data && rows[c].elem_size != s->state[c].elem_size) {
+            abmx_internal::set_error("row column element size differs from its state column");
+            return ABMX_E_SCHEMA;
+        }
+    if (s->capacity == 0 || m == 0 || s->n_state > kMaxCols) {  // the general two-call path
+        rc = abmx_agents_remove(s, d_kill, d_killed, stream);
+        if (rc) return rc;
+        return abmx_agents_spawn(s, m, d_valid, rows, set_type, agent_type, nullptr, nullptr, d_result, stream);
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    (void)cudaGetLastError();
+    Scratch sc(st);
+    const size_t n = static_cast<size_t>(s->capacity);
+    const size_t ta = (n + kTile - 1) / kTile, tb = (static_cast<size_t>(m) + kTile - 1) / kTile;
+    const size_t wa_b = (sizeof(ScanWs) + ta * sizeof(unsigned long long) + 15) / 16 * 16;
+    const size_t wb_b = (sizeof(ScanWs) + tb * sizeof(unsigned long long) + 15) / 16 * 16;
+    const size_t ws_b = (wa_b + wb_b + sizeof(LifeCounts) + 15) / 16 * 16;
+    // one scratch block (host submission is a large part of a cycle): [workspace | slots | rows]
+    void* ws = nullptr;
+    CKA(sc.get(&ws, ws_b + n * 4 + static_cast<size_t>(m) * 4));
+    int32_t* slots = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_b);
+    int32_t* rws = slots + n;
+    CKA(cudaMemsetAsync(ws, 0, ws_b, st));
+    ScanWs* wa = static_cast<ScanWs*>(ws);
+    ScanWs* wb = reinterpret_cast<ScanWs*>(static_cast<char*>(ws) + wa_b);
+    LifeCounts* cnt = reinterpret_cast<LifeCounts*>(static_cast<char*>(ws) + wa_b + wb_b);
+    const Life L = life_of(s);
+    Cols Z{};  // removal: zero every state column
+    Z.n = s->n_state;
+    for (int c = 0; c < s->n_state; ++c) {
+        Z.dst[c] = s->state[c].data;
+        Z.src[c] = nullptr;
+        Z.sz[c] = s->state[c].elem_size;
+    }
+    k_life_select<<<static_cast<unsigned>(ta + tb), kT, 0, st>>>(d_kill, n, slots, wa, static_cast<unsigned>(ta), d_valid,
+                                                                 static_cast<size_t>(m), rws, wb, Z, L, cnt);
+    abmx_internal::count_launch();
+    CKA(cudaGetLastError());
+    Cols A{};  // spawn: copy the row columns given
+    A.n = 0;
+    for (int c = 0; c < s->n_state; ++c) {
+        if (!rows || !rows[c].data) continue;
+        A.dst[A.n] = s->state[c].data;
+        A.src[A.n] = rows[c].data;
+        A.sz[A.n] = s->state[c].elem_size;
+        ++A.n;
+    }
+    const size_t pairs_max = n < static_cast<size_t>(m) ? n : static_cast<size_t>(m);
+    k_life_apply<<<grid_for(pairs_max), kT, 0, st>>>(slots, rws, cnt, A, L, set_type, agent_type, &wa->pad,
+                                                     reinterpret_cast<long long*>(d_killed),
+                                                     reinterpret_cast<long long*>(d_result));
     abmx_internal::count_launch();
     CKA(cudaGetLastError());
     return ABMX_OK;

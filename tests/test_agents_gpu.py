@@ -260,3 +260,33 @@ def test_toy_rm_equals_sci(agents, seed):
     k = min(slots.size, rows.size)
     want[slots[:k]] = b[rows[:k]]
     assert r.rank_match == want.tolist()
+
+
+def test_fused_lifecycle_golden(agents):
+    """abmx_agents_lifecycle (remove + spawn in two kernels) on the reference's 40 four-cycle
+    sequences (tests/golden/lifecycle.json): the same sets and outcomes as the two calls."""
+    for i, case in enumerate(load("lifecycle.json")["cases"]):
+        st = ewf_decode(case["init"], case["recycle"])
+        dev = to_dev(agents, st)
+        for j, (kill, rows, valid, set_type, at, want, wo) in enumerate(lifecycle_cycles(case)):
+            killed, spawned, dropped = dev.lifecycle(kill, rows, valid, agent_type=at if set_type else None)
+            assert (killed, spawned, dropped) == (wo["killed"], wo["spawned"], wo["dropped"]), (i, j)
+            ewf_equal(from_dev(dev, case["recycle"]), want, (i, j))
+
+
+@pytest.mark.parametrize("cap,recycle", [(1 << 20, False), (1 << 20, True), (300_001, True), (5, True)])
+def test_fused_lifecycle_large_vs_oracle(agents, oracle, cap, recycle):
+    g = np.random.default_rng(cap + recycle + 7)
+    st = _random_state(g, cap, recycle)
+    dev = to_dev(agents, st)
+    for cyc in range(3):
+        kill = (g.random(cap) < 0.05 * (cyc + 1)).astype(np.uint8)
+        m = int(g.integers(max(cap // 20, 1), max(cap // 5, 2)))
+        rows = {"e": g.integers(0, 1 << 40, m).astype(np.int64), "w": g.uniform(-1, 1, m),
+                "f": (g.random(m) < 0.5).astype(np.uint8)}
+        valid = (g.random(m) < 0.7).astype(np.uint8)
+        st, wo = oracle.lifecycle(st, kill, rows, valid, True, cyc)
+        killed, spawned, dropped = dev.lifecycle(kill, rows, valid, agent_type=cyc)
+        assert (killed, spawned, dropped) == (wo["killed"], wo["spawned"], wo["dropped"])
+        ewf_equal(from_dev(dev, recycle), st, cyc)
+        assert np.array_equal(dev.types.cpu().numpy(), st["types"])
