@@ -109,7 +109,11 @@ __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __r
 #endif
 constexpr int kPT = ABMX_SCAN_THREADS;  // threads per CTA (a warp scans 1024 elements per tile)
 constexpr int kPTile = kPT * 32;        // mask bytes (elements) per tile
-constexpr int kPMinB = kPT >= 512 ? 1 : 2;  // CTAs per SM
+constexpr int kPMinB = kPT >= 512 ? 1 : 2;  // CTAs per SM (rank_scan: 104 KB of ring + output stages each)
+#ifndef ABMX_COMPACT_CTAS
+#define ABMX_COMPACT_CTAS 3
+#endif
+constexpr int kCMinB = kPT >= 512 ? 1 : ABMX_COMPACT_CTAS;  // compact_indices: 72 KB each
 #ifndef ABMX_SCAN_STAGES
 #define ABMX_SCAN_STAGES 5
 #endif
@@ -125,11 +129,11 @@ struct PipeShared {
 
 template <bool kCompact>
 constexpr int pipe_smem() {
-    return kPIn * kPTile + (kCompact ? 1 : kPOut) * kPTile * static_cast<int>(sizeof(int32_t));
+    return kPIn * kPTile + (kCompact ? kPTile + 16 : kPOut * kPTile) * static_cast<int>(sizeof(int32_t));
 }
 
 template <bool kCompact>
-__global__ void __launch_bounds__(kPT, kPMinB) scan_pipe_kernel(const uint8_t* __restrict__ mask, int32_t* __restrict__ out,
+__global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_kernel(const uint8_t* __restrict__ mask, int32_t* __restrict__ out,
                                                           size_t n, int tiles, unsigned long long* __restrict__ chunk_tot,
                                                           unsigned long long* __restrict__ true_out) {
     extern __shared__ __align__(128) unsigned char dsm[];
@@ -285,6 +289,14 @@ __global__ void __launch_bounds__(kPT, kPMinB) scan_pipe_kernel(const uint8_t* _
             }
         } else {
             const int ttot = static_cast<int>(S.total);
+            // The tile's trues go to out[run, run + ttot), its falses to out[f_dst + ttot, ...).
+            // Each run is laid out in shared memory at the same offset mod 4 as its destination,
+            // so both are written with 16-byte loads and stores (scalar only at the quad edges).
+            const size_t f_dst = S.T + (tb - run) - static_cast<size_t>(ttot);  // + j for false j >= ttot
+            // element offset mod 4 of each run's first destination address
+            const int at = static_cast<int>((reinterpret_cast<uintptr_t>(out + run) >> 2) & 3u);  // true run shift
+            const int fb = ((at + ttot + 3) & ~3) +
+                           static_cast<int>((reinterpret_cast<uintptr_t>(out + f_dst + ttot) >> 2) & 3u);  // false base
             int tpre = static_cast<int>(S.wtot[warp]);  // trues before this lane's word, in the tile
 #pragma unroll
             for (int r = 0; r < 8; ++r) {
@@ -296,15 +308,32 @@ __global__ void __launch_bounds__(kPT, kPMinB) scan_pipe_kernel(const uint8_t* _
                 for (int k = 0; k < 4; ++k) {
                     const int e = e0 + k;
                     if (((wd[r] >> (8 * k)) & 0xFFu) != 0u)
-                        ob[x++] = static_cast<int32_t>(tb + e);
+                        ob[at + x++] = static_cast<int32_t>(tb + e);
                     else
-                        ob[ttot + e - x] = static_cast<int32_t>(tb + e);
+                        ob[fb + e - x] = static_cast<int32_t>(tb + e);  // false rank e - x
                 }
                 tpre += __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
             }
             __syncthreads();
-            const size_t f_dst = S.T + (tb - run) - static_cast<size_t>(ttot);
-            for (int j = tid; j < tn; j += kPT) out[j < ttot ? run + j : f_dst + j] = ob[j];
+            // a run of len elements: dst[0..len) <- ob[o..o+len), (dst - ob + o) multiple of 4 elements
+            auto write_run = [&](int32_t* dst, const int32_t* src, int len) {
+                if (len <= 0) return;
+                const int head = static_cast<int>((4u - (reinterpret_cast<uintptr_t>(dst) >> 2)) & 3u);
+                const int h = head < len ? head : len;
+                if (tid < h) dst[tid] = src[tid];
+                const int body = (len - h) / 4;
+                const int4* s4 = reinterpret_cast<const int4*>(src + h);
+                int4* d4 = reinterpret_cast<int4*>(dst + h);
+                for (int q = tid; q < body; q += kPT) d4[q] = s4[q];
+                const int t0 = h + 4 * body;
+                if (tid < len - t0) dst[t0 + tid] = src[t0 + tid];
+            };
+            if ((reinterpret_cast<uintptr_t>(out) & 3) == 0) {
+                write_run(out + run, ob + at, ttot);
+                write_run(out + f_dst + ttot, ob + fb, tn - ttot);
+            } else {  // unaligned output: plain stores
+                for (int j = tid; j < tn; j += kPT) out[j < ttot ? run + j : f_dst + j] = j < ttot ? ob[at + j] : ob[fb + j - ttot];
+            }
         }
         run += S.total;
     }
@@ -566,7 +595,8 @@ static cudaError_t launch_scan_pipe(const uint8_t* d_mask, int32_t* d_out, size_
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, scan_pipe_kernel<kCompact>, kPT, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorLaunchOutOfResources;
-    const size_t cap = static_cast<size_t>(num_sms()) * static_cast<size_t>(per_sm < kPMinB ? per_sm : kPMinB);
+    constexpr int want = kCompact ? kCMinB : kPMinB;
+    const size_t cap = static_cast<size_t>(num_sms()) * static_cast<size_t>(per_sm < want ? per_sm : want);
     const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
     void* ws = nullptr;
     e = abmx_internal::malloc_async(&ws, grid * sizeof(unsigned long long), s);

@@ -135,6 +135,18 @@ def test_device_pointer_variants_unaligned(abmx, oracle):
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy()[1:], oracle.rank_scan(host[1:]))
     assert int(cnt.item()) == oracle.count_true(host[1:])
+    # compact_indices with the output at every 4-byte offset mod 16 (the two runs' vector stores
+    # align themselves to the destination) and an odd mask offset
+    for off in range(4):
+        o = torch.full((n + 8,), -1, dtype=torch.int32, device="cuda")
+        rc = lib.abmx_cuda_compact_indices_async(C.c_void_p(d.data_ptr() + 1), C.c_void_p(o.data_ptr() + 4 * off),
+                                                 C.c_size_t(n), C.c_void_p(cnt.data_ptr()), C.c_void_p(s))
+        assert rc == 0
+        torch.cuda.synchronize()
+        got = o.cpu().numpy()
+        assert np.array_equal(got[off:off + n], oracle.compact_indices(host[1:])), off
+        assert (got[:off] == -1).all() and (got[off + n:] == -1).all(), off
+        assert int(cnt.item()) == oracle.count_true(host[1:])
 
 
 def test_golden_kernel_table_from_reference(abmx):
