@@ -136,3 +136,21 @@ def test_integration_snippets_compile(tmp_path):
     r = subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-I", ref_inc,
                         "-I", "/usr/local/cuda/include", str(src)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[:2000]
+
+
+def test_integration_functor_snippet_compiles(tmp_path):
+    """The device-functor example in INTEGRATION.md compiles with nvcc against include/."""
+    import re
+    import shutil
+    import subprocess
+    if not shutil.which("nvcc"):
+        pytest.skip("nvcc not available")
+    text = open(os.path.join(ROOT, "INTEGRATION.md")).read()
+    blocks = re.findall(r"```cuda\n(.*?)```", text, re.S)
+    assert blocks
+    src = tmp_path / "functors.cu"
+    src.write_text(blocks[0])
+    r = subprocess.run(["nvcc", "-std=c++17", "-fmad=false", "-gencode", "arch=compute_100a,code=sm_100a", "-c",
+                        "-I", os.path.join(ROOT, "include"), str(src), "-o", str(tmp_path / "functors.o")],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[:2000]
