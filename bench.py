@@ -314,6 +314,63 @@ def finance_section(args, rank, world, allreduce, dist):
 AGENT_CAP, AGENT_CYCLES, AGENT_CHURN = 524_288, 20, 14_000  # one C2 species, its per-step churn
 
 
+def kernel_table_section(args):
+    """The KernelTable entries (include/abmx/simd/kernels.hpp:15-43) on their
+    stream-ordered device-pointer variants, 2^26 elements (every buffer >= 64 MiB), L2 flushed
+    before each rep; event-timed median of 10 reps (the memset of the entry's workspace and its
+    launches included); achieved = algorithmic bytes / that time vs the measured HBM peak."""
+    import ctypes as C
+    import torch
+    import paper_2508_16508_b200 as abmx
+    lib = abmx.lib
+    n = 1 << 26
+    g = torch.Generator(device="cuda").manual_seed(1)
+    mask = (torch.rand(n, device="cuda", generator=g) < 0.5).to(torch.uint8)
+    ranks = torch.empty(n, dtype=torch.int32, device="cuda")
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+    a64 = torch.randint(-2**40, 2**40, (n,), dtype=torch.int64, device="cuda", generator=g)
+    b64 = torch.randint(-2**40, 2**40, (n,), dtype=torch.int64, device="cuda", generator=g)
+    o64 = torch.empty_like(a64)
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+    abmx._check(lib.abmx_cuda_rank_scan_async(vp(mask), vp(ranks), C.c_size_t(n), s))
+    ops = {  # name: (call, algorithmic bytes)
+        "rank_scan": (lambda: lib.abmx_cuda_rank_scan_async(vp(mask), vp(ranks), C.c_size_t(n), s), 5 * n),
+        "count_true": (lambda: lib.abmx_cuda_count_true_async(vp(mask), C.c_size_t(n), vp(cnt), s), n),
+        "compact_indices": (lambda: lib.abmx_cuda_compact_indices_async(vp(mask), vp(out), C.c_size_t(n), vp(cnt), s),
+                            2 * n + 4 * n),
+        "match_first_equal": (lambda: lib.abmx_cuda_match_first_equal_async(vp(ranks), C.c_size_t(n), vp(ranks),
+                                                                             C.c_size_t(n // 2), vp(out), s),
+                              4 * n + 4 * (n // 2) + 4 * n),
+        "blend_i64": (lambda: lib.abmx_cuda_blend_i64_async(vp(mask), vp(a64), vp(b64), vp(o64), C.c_size_t(n), s),
+                      n + 8 * n * 3),
+    }
+    flush = torch.empty(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    flush2 = torch.ones(FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+    peak, _ = hbm_peak()
+    res = {}
+    for name, (f, nbytes) in ops.items():
+        abmx._check(f())
+        ts = []
+        for r in range(10):
+            flush.fill_(r)
+            flush2.sum()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            abmx._check(f())
+            e1.record()
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        us = statistics.median(ts) * 1e3
+        gbs = nbytes / (us / 1e6) / 1e9
+        res[name] = {"us": us, "algorithmic_bytes": nbytes, "achieved_gbs": gbs, "frac": gbs / peak}
+    del flush, flush2
+    return {"workload": "KernelTable entries, 2^26 elements (mask 50% true; match: rb = the first 2^25 ranks), "
+                        "L2 flushed before each rep, event-timed median of 10",
+            "entries": res}
+
+
 def agents_section(args, rank):
     """The generic lifecycle on a C2-sized set: K x (remove_agents(kill), spawn_agents(rows,
     valid, copy apply)) through the C-ABI on device buffers, L2 flushed before each cycle;
@@ -603,6 +660,7 @@ def our_arm(args, rank, world, local_rank, dist):
     traffic = None if args.no_traffic else traffic_section(args, rank, world, allreduce, dist)
     finance = None if args.no_finance else finance_section(args, rank, world, allreduce, dist)
     agents = None if args.no_agents else agents_section(args, rank)
+    ktab = None if args.no_kernel_table else kernel_table_section(args)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -629,7 +687,7 @@ def our_arm(args, rank, world, local_rank, dist):
                 "live_agent_steps_per_s": live_all / (max_ms / 1e3),
                 "e2e": e2e, "warm_run": warm, "gpu_launches": int(launches), "clocks": clk.summary(),
                 "roofline": roofline, "cpu_baseline": cpu, "ensemble": ens, "traffic": traffic,
-                "finance": finance, "agents": agents}
+                "finance": finance, "agents": agents, "kernel_table": ktab}
         print(json.dumps(line))
 
 
@@ -645,6 +703,7 @@ def main():
     ap.add_argument("--no-traffic", action="store_true")
     ap.add_argument("--no-finance", action="store_true")
     ap.add_argument("--no-agents", action="store_true")
+    ap.add_argument("--no-kernel-table", action="store_true")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: CPU collectives, for tests)")
     ap.add_argument("--sharded-only", action="store_true",
