@@ -791,8 +791,12 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
         A.sz[A.n] = s->state[c].elem_size;
         ++A.n;
     }
+    // the pair count is known only on the device: a grid-stride apply over at most 2 CTAs per SM
+    // (a grid sized for min(n, m) pairs launched ~1200 CTAs for C2's ~14k births)
     const size_t pairs_max = n < static_cast<size_t>(m) ? n : static_cast<size_t>(m);
-    k_life_apply<<<grid_for(pairs_max), kT, 0, st>>>(slots, rws, cnt, A, L, set_type, agent_type, &wa->pad,
+    const int g_apply = grid_for(pairs_max) < abmx_internal::num_sms() * 2 ? grid_for(pairs_max)
+                                                                          : abmx_internal::num_sms() * 2;
+    k_life_apply<<<g_apply, kT, 0, st>>>(slots, rws, cnt, A, L, set_type, agent_type, &wa->pad,
                                                      reinterpret_cast<long long*>(d_killed),
                                                      reinterpret_cast<long long*>(d_result));
     abmx_internal::count_launch();
