@@ -5,17 +5,27 @@
 // stays ON CHIP for the entire run: agent columns live in REGISTERS (thread t owns slots
 // t*SPT .. t*SPT+SPT-1 of both species for every step), the lattice and the per-cell lists
 // live in shared memory, and HBM is touched only for the initial draw, the id column
-// (written at births/deaths) and one metrics row per step. Each step is four phases
-// separated by __syncthreads:
+// (written at births/deaths) and one metrics row per step. A step is three phases and three
+// __syncthreads (B1-B3):
 //   1 move + push onto packed per-cell lists (u32: sheep head | wolf head)     lifecycle.cpp:87-122
-//   2 graze (lowest sheep slot per ready cell) + predation (slot-sorted pairing per wolf cell)
-//                                                                              predation.cpp:178-239
-//   3 eat/metabolise/starve/reproduce, one block-wide scan of four packed 16-bit counters
-//     (free/valid x sheep/wolves) and compaction of the valid rows              predation.cpp:241-250
-//   4 free slots pull their rank-matched row (spawn_agents), metrics            lifecycle.cpp:144-195
+//   B1
+//   2 every live agent resolves its own outcome by walking its cell's lists: a sheep's rank
+//     among the cell's sheep decides the graze (rank 0) and whether it is eaten (rank < wolves
+//     in the cell), a wolf's rank decides whether it eats (rank < sheep): the slot-sorted
+//     pairing of predation.cpp:178-239 without a per-cell leader. Then eat / metabolise /
+//     starve / reproduce (predation.cpp:241-250) and a scan of four packed 16-bit counters
+//     (free/valid x sheep/wolves) whose warp totals are combined inside every warp
+//   B2
+//   3 compaction of the valid rows, clear of the lists
+//   B3
+//   4 free slots pull their rank-matched row (spawn_agents, lifecycle.cpp:144-195), metrics;
+//     then phase 1 of the next step follows without a barrier.
 // Regrow (predation.cpp:252-258) is lazy, as in the large-model engine: a grazed cell stores the
 // step at whose end it is ready again (15 bits, renormalised every 8192 steps) and a ring of
 // 256 due counters keeps the ready count, so no step sweeps the lattice.
+// Per slot a thread keeps only cell, energy and one active bit: a dead slot's cell and energy
+// are stale until a birth overwrites them (the dump masks them), and age is the birth step,
+// stored only when a dump asks for it.
 #include <climits>
 #include <cstdint>
 #include <cstring>
@@ -65,7 +75,7 @@ struct EnsParams {
     long long* d_next;  // [count][2]
     int* d_num;         // [count][2]
     // dynamic shared memory carve-up (byte offsets)
-    int o_rowe[2], o_scan, o_cw, o_rowc[2], o_nxt[2], o_pool, o_flag[2], o_g, o_due, o_misc, smem;
+    int o_rowe[2], o_scan, o_cw, o_rowc[2], o_nxt[2], o_g, o_due, o_misc, smem;
 };
 
 __device__ __forceinline__ unsigned long long pack4(unsigned a, unsigned b, unsigned c, unsigned d) {
@@ -76,37 +86,25 @@ __device__ __forceinline__ unsigned f16(unsigned long long v, int k) {  // k = 0
     return static_cast<unsigned>((v >> (48 - 16 * k)) & 0xFFFFu);
 }
 
-__device__ void sort_small(unsigned short* a, int n) {
-    for (int i = 1; i < n; ++i) {
-        const unsigned short v = a[i];
-        int j = i - 1;
-        while (j >= 0 && a[j] > v) {
-            a[j + 1] = a[j];
-            --j;
-        }
-        a[j + 1] = v;
+// Block exclusive scan with ONE barrier: the warp totals are published, then every warp scans
+// them itself with shuffles (kThreads / 32 <= 32 warps).
+template <int kThreads>
+__device__ __forceinline__ unsigned long long scan_1b(unsigned long long v, unsigned long long* smem,
+                                                      unsigned long long* block_total) {
+    constexpr int kWarps = kThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned long long incl = warp_incl_scan(v);
+    if (lane == 31) smem[warp] = incl;
+    __syncthreads();
+    unsigned long long w = lane < kWarps ? smem[lane] : 0ULL;
+#pragma unroll
+    for (int d = 1; d < kWarps; d <<= 1) {
+        const unsigned long long n = __shfl_up_sync(0xffffffffu, w, d);
+        if (lane >= d) w += n;
     }
-}
-__device__ void heap_sort16(unsigned short* a, int n) {
-    auto sift = [&](int root, int end) {
-        for (;;) {
-            int child = 2 * root + 1;
-            if (child >= end) return;
-            if (child + 1 < end && a[child + 1] > a[child]) ++child;
-            if (a[root] >= a[child]) return;
-            const unsigned short t = a[root];
-            a[root] = a[child];
-            a[child] = t;
-            root = child;
-        }
-    };
-    for (int i = n / 2 - 1; i >= 0; --i) sift(i, n);
-    for (int end = n - 1; end > 0; --end) {
-        const unsigned short t = a[0];
-        a[0] = a[end];
-        a[end] = t;
-        sift(0, end);
-    }
+    *block_total = __shfl_sync(0xffffffffu, w, kWarps - 1);
+    const unsigned long long before = __shfl_sync(0xffffffffu, w, warp > 0 ? warp - 1 : 0);
+    return (warp > 0 ? before : 0ULL) + incl - v;
 }
 
 template <int SPT>
@@ -118,19 +116,18 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
     unsigned* rowc[2] = {reinterpret_cast<unsigned*>(sm + P.o_rowc[0]), reinterpret_cast<unsigned*>(sm + P.o_rowc[1])};
     unsigned short* nxt[2] = {reinterpret_cast<unsigned short*>(sm + P.o_nxt[0]),
                               reinterpret_cast<unsigned short*>(sm + P.o_nxt[1])};
-    unsigned short* pool = reinterpret_cast<unsigned short*>(sm + P.o_pool);
-    uint8_t* flag[2] = {sm + P.o_flag[0], sm + P.o_flag[1]};
     unsigned short* g = reinterpret_cast<unsigned short*>(sm + P.o_g);
     unsigned* due_cnt = reinterpret_cast<unsigned*>(sm + P.o_due);  // [256] cells due per step
-    unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [0] pool top, [1] grazed this step
+    unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [1] grazed this step
 
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned long long seed = P.seeds[r];
     long long* ids = P.ids + static_cast<size_t>(r) * 2 * P.stride;
+    auto bit = [](int s, int k) { return 1u << (s * SPT + k); };
 
     // ---- create_species (predation.cpp:22-33, lifecycle.cpp:53-85)
-    bool act[2][SPT];
-    int cell[2][SPT], age[2][SPT], pc[2][SPT], frk[2][SPT];
+    unsigned act = 0;  // bit s*SPT+k: slot tid*SPT+k of species s is active
+    int cell[2][SPT];
     double E[2][SPT];
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -140,29 +137,26 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
 #pragma unroll
         for (int k = 0; k < SPT; ++k) {
             const int i = tid * SPT + k;
-            act[s][k] = i < P.n0[s];
             cell[s][k] = 0;
-            age[s][k] = 0;
             E[s][k] = 0.0;
-            if (act[s][k]) {
+            if (i < P.n0[s]) {
+                act |= bit(s, k);
                 const long long x = static_cast<long long>(__umul64hi(draw(kx, i), static_cast<unsigned long long>(P.W)));
                 const long long y = static_cast<long long>(__umul64hi(draw(ky, i), static_cast<unsigned long long>(P.H)));
                 const long long en = 1 + static_cast<long long>(__umul64hi(draw(ke, i), static_cast<unsigned long long>(ehi - 1)));
                 cell[s][k] = static_cast<int>(y * P.W + x);
                 E[s][k] = static_cast<double>(en);
             }
-            if (i < P.N[s]) ids[static_cast<size_t>(s) * P.stride + i] = act[s][k] ? i : 0;
+            if (i < P.N[s]) {
+                ids[static_cast<size_t>(s) * P.stride + i] = i < P.n0[s] ? i : 0;
+                if (P.d_age) P.d_age[(static_cast<size_t>(r) * 2 + s) * P.stride + i] = 0;  // birth step
+            }
         }
     }
     for (int c = tid; c < P.Cpad; c += kT) g[c] = c < P.C ? kReady : kNever;
     for (int k = tid; k < 256; k += kT) due_cnt[k] = 0;
     for (int c = tid; c < P.C; c += kT) cw[c] = 0xFFFFFFFFu;
-    for (int i = tid; i < P.N[0]; i += kT) flag[0][i] = 0;
-    for (int i = tid; i < P.N[1]; i += kT) flag[1][i] = 0;
-    if (tid == 0) {
-        misc[0] = 0;
-        misc[1] = 0;
-    }
+    if (tid == 0) misc[1] = 0;
     long long n_grass = P.C;  // thread 0: ready cells (full_grass)
     long long next_id[2] = {P.n0[0], P.n0[1]};
     const unsigned long long mroot = split(seed, 3), rroot = split(seed, 4);
@@ -182,12 +176,12 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             rk[1] = __shfl_sync(0xffffffffu, b, 3);
         }
         // ---- phase 1: move + push onto the per-cell lists
+        const unsigned moved = act;  // the slots whose cell words are cleared in phase 3
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
-                pc[s][k] = -1;
-                if (!act[s][k]) continue;
+                if (!(act & bit(s, k))) continue;
                 const int i = tid * SPT + k;
                 const int u = static_cast<int>(draw(mk[s], static_cast<unsigned long long>(i)) >> 61);
                 const int c = cell[s][k];
@@ -199,8 +193,6 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
                 ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
                 const int nc = ny * P.W + nx;
                 cell[s][k] = nc;
-                pc[s][k] = nc;
-                age[s][k] += 1;
                 unsigned old = cw[nc];
                 for (;;) {
                     const unsigned nv = s == 0 ? ((old & 0xFFFF0000u) | static_cast<unsigned>(i))
@@ -211,84 +203,44 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
                 }
                 nxt[s][i] = static_cast<unsigned short>(s == 0 ? (old & 0xFFFFu) : (old >> 16));
             }
-        __syncthreads();
-        // ---- phase 2: graze + predation pairing
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            if (!act[0][k]) continue;
-            const int i = tid * SPT + k;
-            const int c = cell[0][k];
-            unsigned m = static_cast<unsigned>(i);
-            for (unsigned v = cw[c] & 0xFFFFu; v != kEnd; v = nxt[0][v]) m = v < m ? v : m;
-            if (m == static_cast<unsigned>(i) && grass_ready(g[c], t)) {
-                if (P.delay >= 1) {  // ready again at the end of step t + delay - 1
-                    const unsigned due = static_cast<unsigned>(t + P.delay - 1) & 0x7FFFu;
-                    g[c] = static_cast<unsigned short>(due);
-                    atomicAdd(&due_cnt[due & 255u], 1u);
-                } else {
-                    g[c] = kNever;
-                }
-                atomicAdd(&misc[1], 1u);
-                E[0][k] = __dadd_rn(E[0][k], P.gain[0]);
-            }
-        }
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            if (!act[1][k]) continue;
-            const int i = tid * SPT + k;
-            const int c = cell[1][k];
-            const unsigned head = cw[c];
-            if ((head >> 16) != static_cast<unsigned>(i)) continue;  // the list head leads its cell
-            const unsigned s0 = head & 0xFFFFu;
-            if (s0 == kEnd) continue;
-            int lw = 0, ls = 0;
-            for (unsigned v = head >> 16; v != kEnd; v = nxt[1][v]) ++lw;
-            for (unsigned v = s0; v != kEnd; v = nxt[0][v]) ++ls;
-            unsigned short wl_r[8], sl_r[8];
-            unsigned short *wl = wl_r, *sl = sl_r;
-            const bool small = lw <= 8 && ls <= 8;
-            if (!small) {
-                const unsigned off = atomicAdd(&misc[0], static_cast<unsigned>(lw + ls));
-                wl = pool + off;
-                sl = wl + lw;
-            }
-            int q = 0;
-            for (unsigned v = head >> 16; v != kEnd; v = nxt[1][v]) wl[q++] = static_cast<unsigned short>(v);
-            q = 0;
-            for (unsigned v = s0; v != kEnd; v = nxt[0][v]) sl[q++] = static_cast<unsigned short>(v);
-            if (small) {
-                sort_small(wl, lw);
-                sort_small(sl, ls);
-            } else {
-                heap_sort16(wl, lw);
-                heap_sort16(sl, ls);
-            }
-            const int pairs = lw < ls ? lw : ls;
-            for (int p = 0; p < pairs; ++p) {
-                flag[0][sl[p]] = 1;
-                flag[1][wl[p]] = 1;
-            }
-        }
-        __syncthreads();
-        // ---- phase 3: eat / metabolise / starve / reproduce, one packed scan
+        __syncthreads();  // B1: the lists are complete
+        // ---- phase 2: graze, pairing, eat / metabolise / starve / reproduce, one packed scan
+        unsigned freeb = 0, validb = 0;
         unsigned cnt[2][2] = {{0, 0}, {0, 0}};  // [species][free, valid]
-        bool valid[2][SPT];
         double child[2][SPT];
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
                 const int i = tid * SPT + k;
-                valid[s][k] = false;
                 child[s][k] = 0.0;
-                if (pc[s][k] >= 0) cw[pc[s][k]] = 0xFFFFFFFFu;  // clear for the next step
-                bool alive = act[s][k];
-                if (alive && flag[s][i]) {
-                    flag[s][i] = 0;
-                    if (s == 0)
-                        alive = false;  // eaten (predation.cpp:224-238)
-                    else
-                        E[s][k] = __dadd_rn(E[s][k], P.gain[1]);
+                bool alive = act & bit(s, k);
+                if (alive) {
+                    const int c = cell[s][k];
+                    const unsigned head = cw[c];
+                    const unsigned own = s == 0 ? (head & 0xFFFFu) : (head >> 16);
+                    const unsigned other = s == 0 ? (head >> 16) : (head & 0xFFFFu);
+                    int rank = 0;  // slots of this species in the cell below i
+                    for (unsigned v = own; v != kEnd; v = nxt[s][v]) rank += v < static_cast<unsigned>(i);
+                    if (s == 0 && rank == 0 && grass_ready(g[c], t)) {  // the lowest sheep grazes
+                        if (P.delay >= 1) {  // ready again at the end of step t + delay - 1
+                            const unsigned due = static_cast<unsigned>(t + P.delay - 1) & 0x7FFFu;
+                            g[c] = static_cast<unsigned short>(due);
+                            atomicAdd(&due_cnt[due & 255u], 1u);
+                        } else {
+                            g[c] = kNever;
+                        }
+                        atomicAdd(&misc[1], 1u);
+                        E[s][k] = __dadd_rn(E[s][k], P.gain[0]);
+                    }
+                    int n_other = 0;  // the p-th lowest sheep pairs with the p-th lowest wolf
+                    for (unsigned v = other; v != kEnd && n_other <= rank; v = nxt[1 - s][v]) ++n_other;
+                    if (rank < n_other) {
+                        if (s == 0)
+                            alive = false;  // eaten (predation.cpp:224-238)
+                        else
+                            E[s][k] = __dadd_rn(E[s][k], P.gain[1]);
+                    }
                 }
                 if (alive) {
                     E[s][k] = __dsub_rn(E[s][k], P.metab);
@@ -299,31 +251,29 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
                     const double cE = __dmul_rn(floor(__dmul_rn(__dmul_rn(P.frac, E[s][k]), 1048576.0)), 0x1p-20);
                     E[s][k] = __dsub_rn(E[s][k], cE);
                     child[s][k] = cE;
-                    valid[s][k] = true;
+                    validb |= bit(s, k);
+                    ++cnt[s][1];
                 }
-                if (act[s][k] && !alive) {
-                    act[s][k] = false;
-                    cell[s][k] = 0;
-                    age[s][k] = 0;
-                    E[s][k] = 0.0;
+                if ((act & bit(s, k)) && !alive) {
+                    act &= ~bit(s, k);
                     ids[static_cast<size_t>(s) * P.stride + i] = 0;
                 }
-                const bool fr = !alive && i < P.N[s];
-                frk[s][k] = fr ? 1 : -1;
-                cnt[s][0] += fr;
-                cnt[s][1] += valid[s][k];
+                if (!alive && i < P.N[s]) {
+                    freeb |= bit(s, k);
+                    ++cnt[s][0];
+                }
             }
         unsigned long long total;
         const unsigned long long ex =
-            block_excl_scan<kT>(pack4(cnt[0][0], cnt[0][1], cnt[1][0], cnt[1][1]), scan, &total);
-        if (tid == 0) misc[0] = 0;
+            scan_1b<kT>(pack4(cnt[0][0], cnt[0][1], cnt[1][0], cnt[1][1]), scan, &total);  // B2
+        // ---- phase 3: compaction of the valid rows; clear the cell words for the next step
         unsigned run[2][2] = {{f16(ex, 0), f16(ex, 1)}, {f16(ex, 2), f16(ex, 3)}};
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
-                if (frk[s][k] > 0) frk[s][k] = static_cast<int>(run[s][0]++);
-                if (valid[s][k]) {
+                if (moved & bit(s, k)) cw[cell[s][k]] = 0xFFFFFFFFu;
+                if (validb & bit(s, k)) {
                     const unsigned v = run[s][1]++;
                     rowc[s][v] = static_cast<unsigned>(cell[s][k]);
                     rowE[s][v] = child[s][k];
@@ -331,7 +281,7 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             }
         const int F[2] = {static_cast<int>(f16(total, 0)), static_cast<int>(f16(total, 2))};
         const int Q[2] = {static_cast<int>(f16(total, 1)), static_cast<int>(f16(total, 3))};
-        __syncthreads();
+        __syncthreads();  // B3: rows written, cell words cleared
         // ---- phase 4: rank-matched births, regrow, metrics row
         int pairs[2];
 #pragma unroll
@@ -339,14 +289,15 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             pairs[s] = F[s] < Q[s] ? F[s] : Q[s];
 #pragma unroll
             for (int k = 0; k < SPT; ++k) {
-                const int f = frk[s][k];
-                if (f >= 0 && f < pairs[s]) {
+                if (!(freeb & bit(s, k))) continue;
+                const int f = static_cast<int>(run[s][0]++);
+                if (f < pairs[s]) {
                     const int i = tid * SPT + k;
-                    act[s][k] = true;
+                    act |= bit(s, k);
                     cell[s][k] = static_cast<int>(rowc[s][f]);
                     E[s][k] = rowE[s][f];
-                    age[s][k] = 0;
                     ids[static_cast<size_t>(s) * P.stride + i] = next_id[s] + f;
+                    if (P.d_age) P.d_age[(static_cast<size_t>(r) * 2 + s) * P.stride + i] = static_cast<int>(t);
                 }
             }
             next_id[s] += pairs[s];
@@ -373,7 +324,7 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             }
         }
     }
-    if (P.d_active) {
+    if (P.d_active) {  // inactive slots read as zeros; age = steps - birth step
 #pragma unroll
         for (int s = 0; s < 2; ++s)
 #pragma unroll
@@ -381,10 +332,11 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
                 const int i = tid * SPT + k;
                 if (i >= P.N[s]) continue;
                 const size_t q = (static_cast<size_t>(r) * 2 + s) * P.stride + i;
-                P.d_active[q] = act[s][k];
-                P.d_cell[q] = cell[s][k];
-                P.d_age[q] = age[s][k];
-                P.d_energy[q] = E[s][k];
+                const bool a = act & bit(s, k);
+                P.d_active[q] = a;
+                P.d_cell[q] = a ? cell[s][k] : 0;
+                P.d_age[q] = a ? static_cast<int>(P.steps - P.d_age[q]) : 0;
+                P.d_energy[q] = a ? E[s][k] : 0.0;
             }
         for (int c = tid; c < P.Cpad; c += kT) P.d_g[static_cast<size_t>(r) * P.Cpad + c] = g[c];
         if (tid == 0) {
@@ -412,9 +364,6 @@ static int layout(const abmx_predation_config& cfg, EnsParams& P) {
     P.o_rowc[1] = take(4 * (N[1] > 0 ? N[1] : 1), 16);
     P.o_nxt[0] = take(2 * (N[0] > 0 ? N[0] : 1), 16);
     P.o_nxt[1] = take(2 * (N[1] > 0 ? N[1] : 1), 16);
-    P.o_pool = take(2 * (N[0] + N[1] + 2), 16);
-    P.o_flag[0] = take(N[0] > 0 ? N[0] : 1, 16);
-    P.o_flag[1] = take(N[1] > 0 ? N[1] : 1, 16);
     P.o_g = take(2 * P.Cpad, 16);
     P.o_due = take(4 * 256, 16);
     P.smem = (off + 15) / 16 * 16;
