@@ -74,8 +74,10 @@ struct EnsParams {
     unsigned short* d_g;  // [count][Cpad] grass words
     long long* d_next;  // [count][2]
     int* d_num;         // [count][2]
+    unsigned* rowc;     // [count][2][stride] valid rows of the step: cell
+    double* rowe;       // [count][2][stride] and the child's energy
     // dynamic shared memory carve-up (byte offsets)
-    int o_rowe[2], o_scan, o_cw, o_rowc[2], o_nxt[2], o_g, o_due, o_misc, smem;
+    int o_scan, o_cw, o_nxt[2], o_g, o_due, o_misc, smem;
 };
 
 __device__ __forceinline__ unsigned long long pack4(unsigned a, unsigned b, unsigned c, unsigned d) {
@@ -86,15 +88,36 @@ __device__ __forceinline__ unsigned f16(unsigned long long v, int k) {  // k = 0
     return static_cast<unsigned>((v >> (48 - 16 * k)) & 0xFFFFu);
 }
 
-// Block exclusive scan with ONE barrier: the warp totals are published, then every warp scans
-// them itself with shuffles (kThreads / 32 <= 32 warps).
-template <int kThreads>
-__device__ __forceinline__ unsigned long long scan_1b(unsigned long long v, unsigned long long* smem,
-                                                      unsigned long long* block_total) {
+// Block exclusive scan of four packed counters (16-bit fields of a u64, field 0 on top) with
+// ONE barrier: the warp totals are published, then every warp scans them itself with shuffles
+// (kThreads / 32 <= 32 warps). With at most kLane counts per lane and field, a warp's fields stay
+// below 256 when kLane <= 4, so the warp-level part runs on 8-bit fields of a u32.
+__device__ __forceinline__ unsigned long long widen8(unsigned x) {
+    return (static_cast<unsigned long long>(x >> 24) << 48) | (static_cast<unsigned long long>((x >> 16) & 0xFFu) << 32) |
+           (static_cast<unsigned long long>((x >> 8) & 0xFFu) << 16) | (x & 0xFFu);
+}
+template <int kThreads, int kLane>
+__device__ __forceinline__ unsigned long long scan_1b(unsigned c0, unsigned c1, unsigned c2, unsigned c3,
+                                                      unsigned long long* smem, unsigned long long* block_total) {
     constexpr int kWarps = kThreads / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const unsigned long long incl = warp_incl_scan(v);
-    if (lane == 31) smem[warp] = incl;
+    unsigned long long incl, v;
+    if constexpr (kLane <= 4) {
+        const unsigned v32 = (c0 << 24) | (c1 << 16) | (c2 << 8) | c3;
+        unsigned x = v32;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const unsigned n = __shfl_up_sync(0xffffffffu, x, d);
+            if (lane >= d) x += n;
+        }
+        if (lane == 31) smem[warp] = widen8(x);
+        v = 0;
+        incl = widen8(x - v32);  // this lane's exclusive offset within the warp
+    } else {
+        v = pack4(c0, c1, c2, c3);
+        incl = warp_incl_scan(v);
+        if (lane == 31) smem[warp] = incl;
+    }
     __syncthreads();
     unsigned long long w = lane < kWarps ? smem[lane] : 0ULL;
 #pragma unroll
@@ -108,12 +131,10 @@ __device__ __forceinline__ unsigned long long scan_1b(unsigned long long v, unsi
 }
 
 template <int SPT>
-__global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
+__global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
-    double* rowE[2] = {reinterpret_cast<double*>(sm + P.o_rowe[0]), reinterpret_cast<double*>(sm + P.o_rowe[1])};
     unsigned long long* scan = reinterpret_cast<unsigned long long*>(sm + P.o_scan);
     unsigned* cw = reinterpret_cast<unsigned*>(sm + P.o_cw);
-    unsigned* rowc[2] = {reinterpret_cast<unsigned*>(sm + P.o_rowc[0]), reinterpret_cast<unsigned*>(sm + P.o_rowc[1])};
     unsigned short* nxt[2] = {reinterpret_cast<unsigned short*>(sm + P.o_nxt[0]),
                               reinterpret_cast<unsigned short*>(sm + P.o_nxt[1])};
     unsigned short* g = reinterpret_cast<unsigned short*>(sm + P.o_g);
@@ -123,6 +144,10 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned long long seed = P.seeds[r];
     long long* ids = P.ids + static_cast<size_t>(r) * 2 * P.stride;
+    // the valid rows of a step live in a per-replica global scratch (L1/L2-resident, ordered by
+    // B3 like shared memory): keeping them out of SMEM lets three C1 replicas share an SM
+    unsigned* rowc[2] = {P.rowc + static_cast<size_t>(r) * 2 * P.stride, P.rowc + (static_cast<size_t>(r) * 2 + 1) * P.stride};
+    double* rowE[2] = {P.rowe + static_cast<size_t>(r) * 2 * P.stride, P.rowe + (static_cast<size_t>(r) * 2 + 1) * P.stride};
     auto bit = [](int s, int k) { return 1u << (s * SPT + k); };
 
     // ---- create_species (predation.cpp:22-33, lifecycle.cpp:53-85)
@@ -265,7 +290,7 @@ __global__ void __launch_bounds__(kT) k_ensemble(EnsParams P) {
             }
         unsigned long long total;
         const unsigned long long ex =
-            scan_1b<kT>(pack4(cnt[0][0], cnt[0][1], cnt[1][0], cnt[1][1]), scan, &total);  // B2
+            scan_1b<kT, SPT>(cnt[0][0], cnt[0][1], cnt[1][0], cnt[1][1], scan, &total);  // B2
         // ---- phase 3: compaction of the valid rows; clear the cell words for the next step
         unsigned run[2][2] = {{f16(ex, 0), f16(ex, 1)}, {f16(ex, 2), f16(ex, 3)}};
 #pragma unroll
@@ -355,13 +380,9 @@ static int layout(const abmx_predation_config& cfg, EnsParams& P) {
         off += bytes;
         return o;
     };
-    P.o_rowe[0] = take(8 * (N[0] > 0 ? N[0] : 1), 16);
-    P.o_rowe[1] = take(8 * (N[1] > 0 ? N[1] : 1), 16);
     P.o_scan = take(8 * (kT / 32 + 2), 16);
     P.o_misc = take(16 + 8 * (kT / 32), 16);
     P.o_cw = take(4 * P.C, 16);
-    P.o_rowc[0] = take(4 * (N[0] > 0 ? N[0] : 1), 16);
-    P.o_rowc[1] = take(4 * (N[1] > 0 ? N[1] : 1), 16);
     P.o_nxt[0] = take(2 * (N[0] > 0 ? N[0] : 1), 16);
     P.o_nxt[1] = take(2 * (N[1] > 0 ? N[1] : 1), 16);
     P.o_g = take(2 * P.Cpad, 16);
@@ -435,6 +456,7 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     void* dseeds = nullptr;
     void* dids = nullptr;
     void* dmet = nullptr;
+    void* drows = nullptr;
     void* ddump = nullptr;
     const size_t mbytes = sizeof(double) * 4 * static_cast<size_t>(count) * static_cast<size_t>(steps);
     const size_t ids_n = static_cast<size_t>(count) * 2 * P.stride;
@@ -445,10 +467,13 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     CKE(abmx_internal::malloc_async(&dseeds, sizeof(unsigned long long) * count, st));
     CKE(abmx_internal::malloc_async(&dids, ids_n * 8, st));
     CKE(abmx_internal::malloc_async(&dmet, mbytes, st));
+    CKE(abmx_internal::malloc_async(&drows, ids_n * 12, st));
     CKE(cudaMemcpyAsync(dseeds, seeds, sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, st));
     P.seeds = static_cast<const unsigned long long*>(dseeds);
     P.ids = static_cast<long long*>(dids);
     P.metrics = static_cast<double*>(dmet);
+    P.rowe = static_cast<double*>(drows);
+    P.rowc = reinterpret_cast<unsigned*>(static_cast<char*>(drows) + ids_n * 8);
     if (dump) {
         const size_t n = ids_n;
         const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * 2 * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
@@ -536,6 +561,7 @@ done:
         if (dseeds) cudaFreeAsync(dseeds, st);
         if (dids) cudaFreeAsync(dids, st);
         if (dmet) cudaFreeAsync(dmet, st);
+        if (drows) cudaFreeAsync(drows, st);
         if (ddump) cudaFreeAsync(ddump, st);
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
