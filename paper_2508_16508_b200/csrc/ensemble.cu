@@ -49,7 +49,7 @@ constexpr unsigned short kReady = 0x8000u;  // ready (full_grass, or regrown)
 constexpr unsigned short kNever = 0x8001u;  // grazed with regrow_delay <= 0 (never regrows), or padding
 constexpr int kRenorm = 8192;               // due steps older than this are folded into kReady
 
-__device__ __forceinline__ bool grass_ready(unsigned short gv, long long t) {  // at a graze of step t
+__device__ __forceinline__ bool grass_ready(unsigned short gv, int t) {  // at a graze of step t
     return gv == kReady || (gv < 0x8000u && ((static_cast<unsigned>(t) - 1u - gv) & 0x7FFFu) < 0x4000u);
 }
 
@@ -74,8 +74,10 @@ struct EnsParams {
     unsigned short* d_g;  // [count][Cpad] grass words
     long long* d_next;  // [count][2]
     int* d_num;         // [count][2]
-    unsigned* rowc;     // [count][2][stride] valid rows of the step: cell
-    double* rowe;       // [count][2][stride] and the child's energy
+    struct Row {        // a valid row of the step: the child's energy and cell
+        double e;
+        unsigned c, pad;
+    }* rows;            // [count][2][stride]
     // dynamic shared memory carve-up (byte offsets)
     int o_scan, o_cw, o_nxt[2], o_g, o_due, o_misc, smem;
 };
@@ -140,14 +142,14 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
     unsigned short* g = reinterpret_cast<unsigned short*>(sm + P.o_g);
     unsigned* due_cnt = reinterpret_cast<unsigned*>(sm + P.o_due);  // [256] cells due per step
     unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [1] grazed this step
+    long long* ctr = reinterpret_cast<long long*>(sm + P.o_misc + 16);  // next_id[2], n_grass (thread 0)
 
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned long long seed = P.seeds[r];
     long long* ids = P.ids + static_cast<size_t>(r) * 2 * P.stride;
     // the valid rows of a step live in a per-replica global scratch (L1/L2-resident, ordered by
     // B3 like shared memory): keeping them out of SMEM lets three C1 replicas share an SM
-    unsigned* rowc[2] = {P.rowc + static_cast<size_t>(r) * 2 * P.stride, P.rowc + (static_cast<size_t>(r) * 2 + 1) * P.stride};
-    double* rowE[2] = {P.rowe + static_cast<size_t>(r) * 2 * P.stride, P.rowe + (static_cast<size_t>(r) * 2 + 1) * P.stride};
+    EnsParams::Row* rows = P.rows + static_cast<size_t>(r) * 2 * P.stride;
     auto bit = [](int s, int k) { return 1u << (s * SPT + k); };
 
     // ---- create_species (predation.cpp:22-33, lifecycle.cpp:53-85)
@@ -181,13 +183,16 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
     for (int c = tid; c < P.Cpad; c += kT) g[c] = c < P.C ? kReady : kNever;
     for (int k = tid; k < 256; k += kT) due_cnt[k] = 0;
     for (int c = tid; c < P.C; c += kT) cw[c] = 0xFFFFFFFFu;
-    if (tid == 0) misc[1] = 0;
-    long long n_grass = P.C;  // thread 0: ready cells (full_grass)
-    long long next_id[2] = {P.n0[0], P.n0[1]};
+    if (tid == 0) {
+        misc[1] = 0;
+        ctr[0] = P.n0[0];  // next ids: thread 0 adds the step's births between B2 and B3
+        ctr[1] = P.n0[1];
+        ctr[2] = P.C;  // ready cells (full_grass)
+    }
     const unsigned long long mroot = split(seed, 3), rroot = split(seed, 4);
     __syncthreads();
 
-    for (long long t = 1; t <= P.steps; ++t) {
+    for (int t = 1; t <= P.steps; ++t) {  // steps < 2^31 (run_smem)
         unsigned long long mk[2], rk[2];
         {  // the step's four stream keys, two splits per lane instead of six: lanes 0/1 derive
            // the move / reproduce roots of step t, lanes 0..3 the per-species keys, shuffled out
@@ -300,12 +305,16 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 if (moved & bit(s, k)) cw[cell[s][k]] = 0xFFFFFFFFu;
                 if (validb & bit(s, k)) {
                     const unsigned v = run[s][1]++;
-                    rowc[s][v] = static_cast<unsigned>(cell[s][k]);
-                    rowE[s][v] = child[s][k];
+                    rows[s * P.stride + v].e = child[s][k];
+                    rows[s * P.stride + v].c = static_cast<unsigned>(cell[s][k]);
                 }
             }
         const int F[2] = {static_cast<int>(f16(total, 0)), static_cast<int>(f16(total, 2))};
         const int Q[2] = {static_cast<int>(f16(total, 1)), static_cast<int>(f16(total, 3))};
+        if (tid == 0) {  // phase 4 reads ctr[s] - pairs[s] as the first id of the step's births
+            ctr[0] += F[0] < Q[0] ? F[0] : Q[0];
+            ctr[1] += F[1] < Q[1] ? F[1] : Q[1];
+        }
         __syncthreads();  // B3: rows written, cell words cleared
         // ---- phase 4: rank-matched births, regrow, metrics row
         int pairs[2];
@@ -319,13 +328,12 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 if (f < pairs[s]) {
                     const int i = tid * SPT + k;
                     act |= bit(s, k);
-                    cell[s][k] = static_cast<int>(rowc[s][f]);
-                    E[s][k] = rowE[s][f];
-                    ids[static_cast<size_t>(s) * P.stride + i] = next_id[s] + f;
+                    cell[s][k] = static_cast<int>(rows[s * P.stride + f].c);
+                    E[s][k] = rows[s * P.stride + f].e;
+                    ids[static_cast<size_t>(s) * P.stride + i] = ctr[s] - pairs[s] + f;
                     if (P.d_age) P.d_age[(static_cast<size_t>(r) * 2 + s) * P.stride + i] = static_cast<int>(t);
                 }
             }
-            next_id[s] += pairs[s];
         }
         if (t % kRenorm == 0)  // due steps that have passed become kReady before they alias
             for (int c = tid; c < P.C; c += kT) {
@@ -335,7 +343,8 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
         if (tid == 0) {
             // regrow of this step, lazily: - grazed + those due at its end (predation.cpp:252-258)
             const unsigned slot = static_cast<unsigned>(t) & 255u;
-            n_grass += static_cast<long long>(due_cnt[slot]) - static_cast<long long>(misc[1]);
+            const long long n_grass = ctr[2] + static_cast<long long>(due_cnt[slot]) - static_cast<long long>(misc[1]);
+            ctr[2] = n_grass;
             due_cnt[slot] = 0;
             misc[1] = 0;
             double* row = P.metrics + (static_cast<size_t>(r) * P.steps + (t - 1)) * 4;
@@ -365,8 +374,8 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
             }
         for (int c = tid; c < P.Cpad; c += kT) P.d_g[static_cast<size_t>(r) * P.Cpad + c] = g[c];
         if (tid == 0) {
-            P.d_next[2 * r] = next_id[0];
-            P.d_next[2 * r + 1] = next_id[1];
+            P.d_next[2 * r] = ctr[0];
+            P.d_next[2 * r + 1] = ctr[1];
         }
     }
 }
@@ -427,6 +436,10 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
         abmx_internal::set_error("configuration does not fit the SMEM-resident ensemble kernel");
         return ABMX_E_DOMAIN;
     }
+    if (steps > 0x7FFFFFFFLL) {  // the kernel counts steps in 32 bits, as the batched engine does
+        abmx_internal::set_error("steps must be below 2^31");
+        return ABMX_E_DOMAIN;
+    }
     EnsParams P{};
     P.W = cfg.width;
     P.H = cfg.height;
@@ -467,13 +480,12 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     CKE(abmx_internal::malloc_async(&dseeds, sizeof(unsigned long long) * count, st));
     CKE(abmx_internal::malloc_async(&dids, ids_n * 8, st));
     CKE(abmx_internal::malloc_async(&dmet, mbytes, st));
-    CKE(abmx_internal::malloc_async(&drows, ids_n * 12, st));
+    CKE(abmx_internal::malloc_async(&drows, ids_n * sizeof(EnsParams::Row), st));
     CKE(cudaMemcpyAsync(dseeds, seeds, sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, st));
     P.seeds = static_cast<const unsigned long long*>(dseeds);
     P.ids = static_cast<long long*>(dids);
     P.metrics = static_cast<double*>(dmet);
-    P.rowe = static_cast<double*>(drows);
-    P.rowc = reinterpret_cast<unsigned*>(static_cast<char*>(drows) + ids_n * 8);
+    P.rows = static_cast<EnsParams::Row*>(drows);
     if (dump) {
         const size_t n = ids_n;
         const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * 2 * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
