@@ -189,22 +189,25 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
         ctr[1] = P.n0[1];
         ctr[2] = P.C;  // ready cells (full_grass)
     }
-    const unsigned long long mroot = split(seed, 3), rroot = split(seed, 4);
+    // the four stream keys of a step (move, reproduce x sheep, wolves), derived by warp 0 into
+    // SMEM: two splits per lane instead of six, lanes 0/1 the step roots, lanes 0..3 the keys
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm + P.o_misc + 48);
+    if (tid == 0) {
+        keys[4] = split(seed, 3);  // the move and reproduce roots
+        keys[5] = split(seed, 4);
+    }
+    __syncwarp();
+    auto derive_keys = [&](int t) {
+        const unsigned ln = static_cast<unsigned>(tid) & 31u;
+        const unsigned long long a = split(keys[4 + (ln & 1u)], static_cast<unsigned long long>(t));
+        const unsigned long long mt = __shfl_sync(0xffffffffu, a, 0), rt = __shfl_sync(0xffffffffu, a, 1);
+        const unsigned long long b = split(ln & 2u ? rt : mt, static_cast<unsigned long long>(ln & 1u));
+        if (ln < 4) keys[ln] = b;  // mk[0], mk[1], rk[0], rk[1]
+    };
+    if (tid < 32) derive_keys(1);
     __syncthreads();
 
     for (int t = 1; t <= P.steps; ++t) {  // steps < 2^31 (run_smem)
-        unsigned long long mk[2], rk[2];
-        {  // the step's four stream keys, two splits per lane instead of six: lanes 0/1 derive
-           // the move / reproduce roots of step t, lanes 0..3 the per-species keys, shuffled out
-            const unsigned ln = static_cast<unsigned>(tid) & 31u;
-            const unsigned long long a = split(ln & 1u ? rroot : mroot, static_cast<unsigned long long>(t));
-            const unsigned long long mt = __shfl_sync(0xffffffffu, a, 0), rt = __shfl_sync(0xffffffffu, a, 1);
-            const unsigned long long b = split(ln & 2u ? rt : mt, static_cast<unsigned long long>(ln & 1u));
-            mk[0] = __shfl_sync(0xffffffffu, b, 0);
-            mk[1] = __shfl_sync(0xffffffffu, b, 1);
-            rk[0] = __shfl_sync(0xffffffffu, b, 2);
-            rk[1] = __shfl_sync(0xffffffffu, b, 3);
-        }
         // ---- phase 1: move + push onto the per-cell lists
         const unsigned moved = act;  // the slots whose cell words are cleared in phase 3
 #pragma unroll
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
             for (int k = 0; k < SPT; ++k) {
                 if (!(act & bit(s, k))) continue;
                 const int i = tid * SPT + k;
-                const int u = static_cast<int>(draw(mk[s], static_cast<unsigned long long>(i)) >> 61);
+                const int u = static_cast<int>(draw(keys[s], static_cast<unsigned long long>(i)) >> 61);
                 const int c = cell[s][k];
                 // c / W by multiply-high: exact for c, W < 2^18 (smem_fits bounds C by 2^18)
                 const int y = static_cast<int>((static_cast<unsigned long long>(c) * P.wdiv) >> 40);
@@ -277,7 +280,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                     if (E[s][k] <= 0.0) alive = false;
                 }
                 if (alive && E[s][k] > P.metab &&
-                    uniform_double(rk[s], static_cast<unsigned long long>(i)) < P.prob[s]) {
+                    uniform_double(keys[2 + s], static_cast<unsigned long long>(i)) < P.prob[s]) {
                     const double cE = __dmul_rn(floor(__dmul_rn(__dmul_rn(P.frac, E[s][k]), 1048576.0)), 0x1p-20);
                     E[s][k] = __dsub_rn(E[s][k], cE);
                     child[s][k] = cE;
@@ -311,6 +314,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
             }
         const int F[2] = {static_cast<int>(f16(total, 0)), static_cast<int>(f16(total, 2))};
         const int Q[2] = {static_cast<int>(f16(total, 1)), static_cast<int>(f16(total, 3))};
+        if (tid < 32) derive_keys(t + 1);  // phase 2 has read this step's keys (B2)
         if (tid == 0) {  // phase 4 reads ctr[s] - pairs[s] as the first id of the step's births
             ctr[0] += F[0] < Q[0] ? F[0] : Q[0];
             ctr[1] += F[1] < Q[1] ? F[1] : Q[1];
@@ -390,7 +394,7 @@ static int layout(const abmx_predation_config& cfg, EnsParams& P) {
         return o;
     };
     P.o_scan = take(8 * (kT / 32 + 2), 16);
-    P.o_misc = take(16 + 8 * (kT / 32), 16);
+    P.o_misc = take(48 + 8 * 6, 16);  // grazed count, next ids + ready cells, stream keys + roots
     P.o_cw = take(4 * P.C, 16);
     P.o_nxt[0] = take(2 * (N[0] > 0 ? N[0] : 1), 16);
     P.o_nxt[1] = take(2 * (N[1] > 0 ? N[1] : 1), 16);
