@@ -48,6 +48,11 @@ constexpr unsigned kEnd = 0xFFFFu;
 constexpr unsigned short kReady = 0x8000u;  // ready (full_grass, or regrown)
 constexpr unsigned short kNever = 0x8001u;  // grazed with regrow_delay <= 0 (never regrows), or padding
 constexpr int kRenorm = 8192;               // due steps older than this are folded into kReady
+// shared-memory layout: the fixed-size pieces first, then the cell words, grass words, list links
+constexpr int kOffScan = 0;                   // warp totals of the step's scan
+constexpr int kOffMisc = 8 * (kT / 32 + 2);   // grazed count, next ids + ready cells, stream keys
+constexpr int kOffDue = kOffMisc + 96;        // [256] cells due per step
+constexpr int kOffCw = kOffDue + 4 * 256;
 
 __device__ __forceinline__ bool grass_ready(unsigned short gv, int t) {  // at a graze of step t
     return gv == kReady || (gv < 0x8000u && ((static_cast<unsigned>(t) - 1u - gv) & 0x7FFFu) < 0x4000u);
@@ -78,8 +83,7 @@ struct EnsParams {
         double e;
         unsigned c, pad;
     }* rows;            // [count][2][stride]
-    // dynamic shared memory carve-up (byte offsets)
-    int o_scan, o_cw, o_nxt[2], o_g, o_due, o_misc, smem;
+    int smem;  // dynamic shared memory bytes (layout())
 };
 
 __device__ __forceinline__ unsigned long long pack4(unsigned a, unsigned b, unsigned c, unsigned d) {
@@ -135,14 +139,14 @@ __device__ __forceinline__ unsigned long long scan_1b(unsigned c0, unsigned c1, 
 template <int SPT>
 __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) {
     extern __shared__ __align__(16) unsigned char sm[];
-    unsigned long long* scan = reinterpret_cast<unsigned long long*>(sm + P.o_scan);
-    unsigned* cw = reinterpret_cast<unsigned*>(sm + P.o_cw);
-    unsigned short* nxt[2] = {reinterpret_cast<unsigned short*>(sm + P.o_nxt[0]),
-                              reinterpret_cast<unsigned short*>(sm + P.o_nxt[1])};
-    unsigned short* g = reinterpret_cast<unsigned short*>(sm + P.o_g);
-    unsigned* due_cnt = reinterpret_cast<unsigned*>(sm + P.o_due);  // [256] cells due per step
-    unsigned* misc = reinterpret_cast<unsigned*>(sm + P.o_misc);  // [1] grazed this step
-    long long* ctr = reinterpret_cast<long long*>(sm + P.o_misc + 16);  // next_id[2], n_grass (thread 0)
+    // fixed-size pieces and the cell words at constant offsets (immediates, not registers)
+    unsigned long long* scan = reinterpret_cast<unsigned long long*>(sm + kOffScan);
+    unsigned* misc = reinterpret_cast<unsigned*>(sm + kOffMisc);  // [1] grazed this step
+    long long* ctr = reinterpret_cast<long long*>(sm + kOffMisc + 16);  // next_id[2], n_grass (thread 0)
+    unsigned* due_cnt = reinterpret_cast<unsigned*>(sm + kOffDue);  // [256] cells due per step
+    unsigned* cw = reinterpret_cast<unsigned*>(sm + kOffCw);
+    unsigned short* g = reinterpret_cast<unsigned short*>(sm + kOffCw + 4 * P.Cpad);
+    unsigned short* nxt = g + P.Cpad;  // [slot][species]: both species' list links of a slot
 
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned long long seed = P.seeds[r];
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
     }
     // the four stream keys of a step (move, reproduce x sheep, wolves), derived by warp 0 into
     // SMEM: two splits per lane instead of six, lanes 0/1 the step roots, lanes 0..3 the keys
-    unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm + P.o_misc + 48);
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(sm + kOffMisc + 48);
     if (tid == 0) {
         keys[4] = split(seed, 3);  // the move and reproduce roots
         keys[5] = split(seed, 4);
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                     if (prev == old) break;
                     old = prev;
                 }
-                nxt[s][i] = static_cast<unsigned short>(s == 0 ? (old & 0xFFFFu) : (old >> 16));
+                nxt[2 * i + s] = static_cast<unsigned short>(s == 0 ? (old & 0xFFFFu) : (old >> 16));
             }
         __syncthreads();  // B1: the lists are complete
         // ---- phase 2: graze, pairing, eat / metabolise / starve / reproduce, one packed scan
@@ -253,9 +257,13 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                     const unsigned head = cw[c];
                     const unsigned own = s == 0 ? (head & 0xFFFFu) : (head >> 16);
                     const unsigned other = s == 0 ? (head >> 16) : (head & 0xFFFFu);
+                    // the rank matters only to a sheep on ready grass or an agent sharing its cell
+                    // with the other species: most agents skip the walk
+                    const bool ready = s == 0 && grass_ready(g[c], t);
                     int rank = 0;  // slots of this species in the cell below i
-                    for (unsigned v = own; v != kEnd; v = nxt[s][v]) rank += v < static_cast<unsigned>(i);
-                    if (s == 0 && rank == 0 && grass_ready(g[c], t)) {  // the lowest sheep grazes
+                    if (ready || other != kEnd)
+                        for (unsigned v = own; v != kEnd; v = nxt[2 * v + s]) rank += v < static_cast<unsigned>(i);
+                    if (ready && rank == 0) {  // the lowest sheep grazes
                         if (P.delay >= 1) {  // ready again at the end of step t + delay - 1
                             const unsigned due = static_cast<unsigned>(t + P.delay - 1) & 0x7FFFu;
                             g[c] = static_cast<unsigned short>(due);
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                         E[s][k] = __dadd_rn(E[s][k], P.gain[0]);
                     }
                     int n_other = 0;  // the p-th lowest sheep pairs with the p-th lowest wolf
-                    for (unsigned v = other; v != kEnd && n_other <= rank; v = nxt[1 - s][v]) ++n_other;
+                    for (unsigned v = other; v != kEnd && n_other <= rank; v = nxt[2 * v + 1 - s]) ++n_other;
                     if (rank < n_other) {
                         if (s == 0)
                             alive = false;  // eaten (predation.cpp:224-238)
@@ -393,13 +401,10 @@ static int layout(const abmx_predation_config& cfg, EnsParams& P) {
         off += bytes;
         return o;
     };
-    P.o_scan = take(8 * (kT / 32 + 2), 16);
-    P.o_misc = take(48 + 8 * 6, 16);  // grazed count, next ids + ready cells, stream keys + roots
-    P.o_cw = take(4 * P.C, 16);
-    P.o_nxt[0] = take(2 * (N[0] > 0 ? N[0] : 1), 16);
-    P.o_nxt[1] = take(2 * (N[1] > 0 ? N[1] : 1), 16);
-    P.o_g = take(2 * P.Cpad, 16);
-    P.o_due = take(4 * 256, 16);
+    take(kOffCw, 16);  // scan, misc (grazed count, next ids + ready cells, stream keys), due counters
+    take(4 * P.Cpad, 16);  // cell words
+    take(2 * P.Cpad, 16);  // grass words
+    take(4 * (N[0] > N[1] ? N[0] : N[1]), 16);  // list links, both species interleaved
     P.smem = (off + 15) / 16 * 16;
     return P.smem;
 }
