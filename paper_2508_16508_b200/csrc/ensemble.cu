@@ -23,7 +23,7 @@
 // Regrow (predation.cpp:252-258) is lazy, as in the large-model engine: a grazed cell stores the
 // step at whose end it is ready again (15 bits, renormalised every 8192 steps) and a ring of
 // 256 due counters keeps the ready count, so no step sweeps the lattice.
-// Per slot a thread keeps only cell, energy and one active bit: a dead slot's cell and energy
+// Per slot a thread keeps only cell, energy and one active bit: a dead slot's cell, energy and id
 // are stale until a birth overwrites them (the dump masks them), and age is the birth step,
 // stored only when a dump asks for it.
 #include <climits>
@@ -295,10 +295,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                     validb |= bit(s, k);
                     ++cnt[s][1];
                 }
-                if ((act & bit(s, k)) && !alive) {
-                    act &= ~bit(s, k);
-                    ids[static_cast<size_t>(s) * P.stride + i] = 0;
-                }
+                if (!alive) act &= ~bit(s, k);  // a dead slot's id reads as 0 (the dump masks it)
                 if (!alive && i < P.N[s]) {
                     freeb |= bit(s, k);
                     ++cnt[s][0];
@@ -383,6 +380,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 P.d_cell[q] = a ? cell[s][k] : 0;
                 P.d_age[q] = a ? static_cast<int>(P.steps - P.d_age[q]) : 0;
                 P.d_energy[q] = a ? E[s][k] : 0.0;
+                if (!a) ids[static_cast<size_t>(s) * P.stride + i] = 0;
             }
         for (int c = tid; c < P.Cpad; c += kT) P.d_g[static_cast<size_t>(r) * P.Cpad + c] = g[c];
         if (tid == 0) {
