@@ -48,6 +48,7 @@ constexpr unsigned kEnd = 0xFFFFu;
 constexpr unsigned short kReady = 0x8000u;  // ready (full_grass, or regrown)
 constexpr unsigned short kNever = 0x8001u;  // grazed with regrow_delay <= 0 (never regrows), or padding
 constexpr int kRenorm = 8192;               // due steps older than this are folded into kReady
+constexpr int kRecord = 6;                  // per-replica global words per slot index: 2 ids + 2 x 16-byte rows
 // shared-memory layout: the fixed-size pieces first, then the cell words, grass words, list links
 constexpr int kOffScan = 0;                   // warp totals of the step's scan
 constexpr int kOffMisc = 8 * (kT / 32 + 2);   // grazed count, next ids + ready cells, stream keys
@@ -58,8 +59,16 @@ __device__ __forceinline__ bool grass_ready(unsigned short gv, int t) {  // at a
     return gv == kReady || (gv < 0x8000u && ((static_cast<unsigned>(t) - 1u - gv) & 0x7FFFu) < 0x4000u);
 }
 
-__constant__ int e_dx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
-__constant__ int e_dy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+// The eight Moore moves (lifecycle.cpp:87-122 order) as 2-bit fields of immediates: a lookup with
+// a per-thread index into __constant__ memory would serialise across the warp.
+constexpr int kMoveDx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+constexpr int kMoveDy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+constexpr unsigned move_table(const int* d) {
+    unsigned v = 0;
+    for (int u = 0; u < 8; ++u) v |= static_cast<unsigned>(d[u] + 1) << (2 * u);
+    return v;
+}
+constexpr unsigned kDxTable = move_table(kMoveDx), kDyTable = move_table(kMoveDy);
 
 struct EnsParams {
     int W, H, C, Cpad;
@@ -69,7 +78,7 @@ struct EnsParams {
     int delay;  // regrow_delay (<= 0: a grazed cell never regrows)
     long long steps;
     const unsigned long long* seeds;
-    long long* ids;     // [count][2][stride]
+    long long* ids;     // [count] records of kRecord * stride words: ids [2][stride], then rows
     double* metrics;    // [count][steps][4]
     // optional final-state dump
     uint8_t* d_active;  // [count][2][stride]
@@ -82,7 +91,7 @@ struct EnsParams {
     struct Row {        // a valid row of the step: the child's energy and cell
         double e;
         unsigned c, pad;
-    }* rows;            // [count][2][stride]
+    };
     int smem;  // dynamic shared memory bytes (layout())
 };
 
@@ -150,10 +159,11 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
 
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned long long seed = P.seeds[r];
-    long long* ids = P.ids + static_cast<size_t>(r) * 2 * P.stride;
-    // the valid rows of a step live in a per-replica global scratch (L1/L2-resident, ordered by
-    // B3 like shared memory): keeping them out of SMEM lets three C1 replicas share an SM
-    EnsParams::Row* rows = P.rows + static_cast<size_t>(r) * 2 * P.stride;
+    // A replica's global record: its id column, then the valid rows of the step (L1/L2-resident,
+    // ordered by B3 like shared memory; keeping them out of SMEM lets three C1 replicas share an
+    // SM). One base pointer serves both.
+    long long* ids = P.ids + static_cast<size_t>(r) * kRecord * P.stride;
+    EnsParams::Row* rows = reinterpret_cast<EnsParams::Row*>(ids + 2 * P.stride);
     auto bit = [](int s, int k) { return 1u << (s * SPT + k); };
 
     // ---- create_species (predation.cpp:22-33, lifecycle.cpp:53-85)
@@ -225,7 +235,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 // c / W by multiply-high: exact for c, W < 2^18 (smem_fits bounds C by 2^18)
                 const int y = static_cast<int>((static_cast<unsigned long long>(c) * P.wdiv) >> 40);
                 const int x = c - y * P.W;
-                int nx = x + e_dx[u], ny = y + e_dy[u];
+                int nx = x + static_cast<int>((kDxTable >> (2 * u)) & 3u) - 1, ny = y + static_cast<int>((kDyTable >> (2 * u)) & 3u) - 1;
                 nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
                 ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
                 const int nc = ny * P.W + nx;
@@ -476,7 +486,6 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     void* dseeds = nullptr;
     void* dids = nullptr;
     void* dmet = nullptr;
-    void* drows = nullptr;
     void* ddump = nullptr;
     const size_t mbytes = sizeof(double) * 4 * static_cast<size_t>(count) * static_cast<size_t>(steps);
     const size_t ids_n = static_cast<size_t>(count) * 2 * P.stride;
@@ -485,14 +494,12 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
     CKE(cudaEventCreate(&ea));
     CKE(cudaEventCreate(&eb));
     CKE(abmx_internal::malloc_async(&dseeds, sizeof(unsigned long long) * count, st));
-    CKE(abmx_internal::malloc_async(&dids, ids_n * 8, st));
+    CKE(abmx_internal::malloc_async(&dids, ids_n * kRecord / 2 * 8, st));
     CKE(abmx_internal::malloc_async(&dmet, mbytes, st));
-    CKE(abmx_internal::malloc_async(&drows, ids_n * sizeof(EnsParams::Row), st));
     CKE(cudaMemcpyAsync(dseeds, seeds, sizeof(unsigned long long) * count, cudaMemcpyHostToDevice, st));
     P.seeds = static_cast<const unsigned long long*>(dseeds);
     P.ids = static_cast<long long*>(dids);
     P.metrics = static_cast<double*>(dmet);
-    P.rows = static_cast<EnsParams::Row*>(drows);
     if (dump) {
         const size_t n = ids_n;
         const size_t bytes = n * (1 + 4 + 4 + 8) + static_cast<size_t>(count) * 2 * P.Cpad + static_cast<size_t>(count) * 2 * (8 + 4) + 64;
@@ -544,7 +551,8 @@ int run_smem(const abmx_predation_config& cfg, const uint64_t* seeds, int count,
             CKE(cudaMemcpyAsync(c.data(), P.d_cell + q, n * 4, cudaMemcpyDeviceToHost, st));
             CKE(cudaMemcpyAsync(ag.data(), P.d_age + q, n * 4, cudaMemcpyDeviceToHost, st));
             CKE(cudaMemcpyAsync(dump->energy[s], P.d_energy + q, n * 8, cudaMemcpyDeviceToHost, st));
-            CKE(cudaMemcpyAsync(dump->ids[s], P.ids + q, n * 8, cudaMemcpyDeviceToHost, st));
+            CKE(cudaMemcpyAsync(dump->ids[s], P.ids + (static_cast<size_t>(r) * kRecord + s) * P.stride, n * 8,
+                                cudaMemcpyDeviceToHost, st));
             CKE(cudaStreamSynchronize(st));
             for (size_t i = 0; i < n; ++i) {
                 dump->active[s][i] = a[i];
@@ -580,7 +588,6 @@ done:
         if (dseeds) cudaFreeAsync(dseeds, st);
         if (dids) cudaFreeAsync(dids, st);
         if (dmet) cudaFreeAsync(dmet, st);
-        if (drows) cudaFreeAsync(drows, st);
         if (ddump) cudaFreeAsync(ddump, st);
         cudaStreamSynchronize(st);
         cudaStreamDestroy(st);
