@@ -69,6 +69,19 @@ __host__ __device__ __forceinline__ uint32_t hi31(unsigned long long v) {
     return static_cast<uint32_t>((v >> 31) & 0x7FFFFFFFULL);
 }
 
+// The eight Moore moves in the order of lifecycle.cpp:87-122 (u = draw >> 61), as 2-bit fields of
+// immediates: a lookup with a per-thread index into __constant__ memory serialises across the warp.
+constexpr int kMoveDx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
+constexpr int kMoveDy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+constexpr unsigned move_table(const int* d) {
+    unsigned v = 0;
+    for (int u = 0; u < 8; ++u) v |= static_cast<unsigned>(d[u] + 1) << (2 * u);
+    return v;
+}
+constexpr unsigned kDxTable = move_table(kMoveDx), kDyTable = move_table(kMoveDy);
+__device__ __forceinline__ int move_dx(int u) { return static_cast<int>((kDxTable >> (2 * u)) & 3u) - 1; }
+__device__ __forceinline__ int move_dy(int u) { return static_cast<int>((kDyTable >> (2 * u)) & 3u) - 1; }
+
 // Warp-inclusive scan of packed u64 values (fields never overflow by construction).
 __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
     const int lane = threadIdx.x & 31;

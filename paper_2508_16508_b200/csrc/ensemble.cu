@@ -59,16 +59,6 @@ __device__ __forceinline__ bool grass_ready(unsigned short gv, int t) {  // at a
     return gv == kReady || (gv < 0x8000u && ((static_cast<unsigned>(t) - 1u - gv) & 0x7FFFu) < 0x4000u);
 }
 
-// The eight Moore moves (lifecycle.cpp:87-122 order) as 2-bit fields of immediates: a lookup with
-// a per-thread index into __constant__ memory would serialise across the warp.
-constexpr int kMoveDx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
-constexpr int kMoveDy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
-constexpr unsigned move_table(const int* d) {
-    unsigned v = 0;
-    for (int u = 0; u < 8; ++u) v |= static_cast<unsigned>(d[u] + 1) << (2 * u);
-    return v;
-}
-constexpr unsigned kDxTable = move_table(kMoveDx), kDyTable = move_table(kMoveDy);
 
 struct EnsParams {
     int W, H, C, Cpad;
@@ -235,7 +225,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 // c / W by multiply-high: exact for c, W < 2^18 (smem_fits bounds C by 2^18)
                 const int y = static_cast<int>((static_cast<unsigned long long>(c) * P.wdiv) >> 40);
                 const int x = c - y * P.W;
-                int nx = x + static_cast<int>((kDxTable >> (2 * u)) & 3u) - 1, ny = y + static_cast<int>((kDyTable >> (2 * u)) & 3u) - 1;
+                int nx = x + move_dx(u), ny = y + move_dy(u);
                 nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
                 ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
                 const int nc = ny * P.W + nx;

@@ -39,9 +39,7 @@ using namespace abmx_dev;
 
 namespace abmx_pred {
 
-// neighbour order of the move draw (predation.cpp:13-15)
-__constant__ int c_dx[8] = {-1, -1, -1, 0, 0, 1, 1, 1};
-__constant__ int c_dy[8] = {-1, 0, 1, -1, 1, -1, 0, 1};
+// neighbour order of the move draw (predation.cpp:13-15): move_dx / move_dy, abmx_device.cuh
 
 // Checked builds (-DABMX_CHECKED, tools/build_variant.sh checked "-DABMX_CHECKED"): every index
 // into the slot columns, the cell words and the list links is bounds-checked on the device; the
@@ -426,7 +424,7 @@ __device__ void move_phase(const Params& P, unsigned b, unsigned nb, unsigned lo
             const int u = static_cast<int>(draw(key, static_cast<unsigned long long>(i0 + k)) >> 61);
             const int c = cell[k];
             const int y = c / P.W, x = c - y * P.W;
-            int nx = x + c_dx[u], ny = y + c_dy[u];
+            int nx = x + move_dx(u), ny = y + move_dy(u);
             nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
             ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
             cell[k] = ny * P.W + nx;
