@@ -148,12 +148,16 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
     const bool out_vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     auto tile_of = [&](int it) { return c0 + it % m; };  // iterations 0..2m-1: the chunk, twice
     auto is_bulk = [&](int t) { return in_vec && static_cast<size_t>(t + 1) * kPTile <= n; };
+    // The chunk's mask is read twice: pass 1 keeps it in L2 (evict_last; 2^26 bytes fit), pass 2
+    // reads it for the last time and the outputs stream past it (evict_first).
+    const unsigned long long keep = l2_evict_last(), stream = l2_evict_first();
     auto issue = [&](int it) {  // one thread: the tile of iteration `it` into ring slot it % kPIn
         if (it >= 2 * m) return;
         const int t = tile_of(it), s = it % kPIn;
         if (is_bulk(t)) {
             mbar_expect_tx(&S.bar[s], kPTile);
-            bulk_g2s(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s]);
+            bulk_g2s_hint(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s],
+                          it < m ? keep : stream);
         }
     };
     if (tid == 0) {
@@ -281,7 +285,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
             __syncthreads();
             if (tn == kPTile && out_vec) {
                 if (tid == 0) {
-                    bulk_s2g(out + tb, o, kPTile * static_cast<unsigned>(sizeof(int32_t)));
+                    bulk_s2g_hint(out + tb, o, kPTile * static_cast<unsigned>(sizeof(int32_t)), stream);
                     bulk_commit();
                 }
             } else {
@@ -324,7 +328,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
                 const int body = (len - h) / 4;
                 const int4* s4 = reinterpret_cast<const int4*>(src + h);
                 int4* d4 = reinterpret_cast<int4*>(dst + h);
-                for (int q = tid; q < body; q += kPT) d4[q] = s4[q];
+                for (int q = tid; q < body; q += kPT) st_v4_hint(d4 + q, s4[q], stream);
                 const int t0 = h + 4 * body;
                 if (tid < len - t0) dst[t0 + tid] = src[t0 + tid];
             };
@@ -341,9 +345,9 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
 }
 
 // ---------------------------------------------------------------- match_first_equal
-// vmin / vmax live in an order-preserving unsigned form, both reduced with atomicMin, so ONE
-// cudaMemsetAsync(0xFF) initialises the workspace (capturable in a graph; no host staging):
-// emin = v ^ 2^31 (min of v), emax = ~(v ^ 2^31) (min of emax = max of v).
+// vmin / vmax live in an order-preserving unsigned form, both reduced with atomicMin (one pair
+// per CTA), so ONE cudaMemsetAsync(0xFF) initialises the workspace (capturable in a graph; no
+// host staging): emin = v ^ 2^31 (min of v), emax = ~(v ^ 2^31) (min of emax = max of v).
 struct MatchWs {
     unsigned emin, emax;
 };
@@ -352,8 +356,9 @@ __device__ __forceinline__ int ws_vmax(const MatchWs* ws) { return static_cast<i
 
 // Grid-stride loops over 4-element quads (16-byte loads, U quads in flight per thread); a
 // scalar loop covers the tail and unaligned inputs. `f(index, value)` sees every element once.
-template <int U = 2, class F>
+template <int U = 2, bool kStream = false, class F>
 __device__ __forceinline__ void for_each_i32(const int32_t* __restrict__ p, size_t n, F&& f) {
+    const unsigned long long stream = kStream ? l2_evict_first() : 0ULL;  // read once: do not keep in L2
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     size_t done = 0;
@@ -363,7 +368,9 @@ __device__ __forceinline__ void for_each_i32(const int32_t* __restrict__ p, size
         for (size_t i = t0; i < quads; i += U * stride) {
             int4 a[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) a[u] = i + u * stride < quads ? q[i + u * stride] : make_int4(0, 0, 0, 0);
+            for (int u = 0; u < U; ++u)
+                a[u] = i + u * stride < quads ? (kStream ? ld_v4_hint(q + i + u * stride, stream) : q[i + u * stride])
+                                              : make_int4(0, 0, 0, 0);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (i + u * stride >= quads) break;
@@ -381,18 +388,35 @@ __device__ __forceinline__ void for_each_i32(const int32_t* __restrict__ p, size
 
 __global__ void minmax_kernel(const int32_t* __restrict__ rb, size_t m, MatchWs* ws) {
     int lo = INT_MAX, hi = INT_MIN;
-    for_each_i32<4>(rb, m, [&](size_t, int v) {
+    for_each_i32<8, true>(rb, m, [&](size_t, int v) {
         lo = min(lo, v);
         hi = max(hi, v);
     });
+    // one atomic pair per CTA: per-warp atomics on the same two words serialise at one L2 slice
+    __shared__ int s_lo[32], s_hi[32];
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
         lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
         hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
     }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMin(&ws->emin, static_cast<unsigned>(lo) ^ 0x80000000u);
-        atomicMin(&ws->emax, ~(static_cast<unsigned>(hi) ^ 0x80000000u));
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        s_lo[warp] = lo;
+        s_hi[warp] = hi;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        lo = lane < nw ? s_lo[lane] : INT_MAX;
+        hi = lane < nw ? s_hi[lane] : INT_MIN;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) {
+            lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, d));
+            hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, d));
+        }
+        if (lane == 0) {
+            atomicMin(&ws->emin, static_cast<unsigned>(lo) ^ 0x80000000u);
+            atomicMin(&ws->emax, ~(static_cast<unsigned>(hi) ^ 0x80000000u));
+        }
     }
 }
 
@@ -416,8 +440,11 @@ __global__ void match_init_kernel(const MatchWs* ws, unsigned bits, int* __restr
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     // INT_MAX = "no row": above any row index, and what the lookup maps to -1
+    // the table stays in L2 for the build's atomics and the lookup's gathers (evict_last); the
+    // streams of rb, ra and the output pass it by (evict_first)
     const int4 fill = make_int4(INT_MAX, INT_MAX, INT_MAX, INT_MAX);
-    for (size_t i = t0; i < nv / 4; i += stride) reinterpret_cast<int4*>(vals)[i] = fill;
+    const unsigned long long keep = l2_evict_last();
+    for (size_t i = t0; i < nv / 4; i += stride) st_v4_hint(reinterpret_cast<int4*>(vals) + i, fill, keep);
     for (size_t i = (nv & ~size_t{3}) + t0; i < nv; i += stride) vals[i] = INT_MAX;
     if (!dense)
         for (size_t i = t0; i < H / 2; i += stride) reinterpret_cast<ulonglong2*>(keys)[i] = make_ulonglong2(0, 0);
@@ -434,19 +461,28 @@ __global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, con
         // quads: all 8 first-match checks are issued before any atomic (an atomic between two
         // checks would serialise them: the compiler cannot move a load across a possibly
         // aliasing atomic)
+        // kQ quads per thread and iteration: both dependent round trips (the quads, then the
+        // checks) carry 4 * kQ values
+        constexpr int kQ = 4;
+        const unsigned long long stream = l2_evict_first();
         const size_t quads = m / 4;
         const int4* q = reinterpret_cast<const int4*>(rb);
-        for (size_t i = t0; i < quads; i += 2 * stride) {
-            const bool two = i + stride < quads;
-            const int4 a = q[i];
-            const int4 b = two ? q[i + stride] : make_int4(0, 0, 0, 0);
-            const int v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-            int cur[8];
+        for (size_t i = t0; i < quads; i += kQ * stride) {
+            int v[4 * kQ];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) cur[k] = v[k] != 0 ? __ldcg(&vals[v[k] - vmin]) : INT_MIN;
+            for (int u = 0; u < kQ; ++u) {
+                const int4 a = i + u * stride < quads ? ld_v4_hint(q + i + u * stride, stream) : make_int4(0, 0, 0, 0);
+                v[4 * u] = a.x;
+                v[4 * u + 1] = a.y;
+                v[4 * u + 2] = a.z;
+                v[4 * u + 3] = a.w;
+            }
+            int cur[4 * kQ];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const int j = static_cast<int>(4 * (k < 4 ? i : i + stride) + (k & 3));
+            for (int k = 0; k < 4 * kQ; ++k) cur[k] = v[k] != 0 ? __ldcg(&vals[v[k] - vmin]) : INT_MIN;
+#pragma unroll
+            for (int k = 0; k < 4 * kQ; ++k) {
+                const int j = static_cast<int>(4 * (i + (k / 4) * stride) + (k & 3));
                 if (cur[k] > j) atomicMin(&vals[v[k] - vmin], j);  // rank 0 (never looked up) skipped
             }
         }
@@ -515,15 +551,20 @@ __global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, co
         const size_t quads = n / 4;
         const int4* q = reinterpret_cast<const int4*>(ra);
         int4* o = reinterpret_cast<int4*>(row_out);
+        const unsigned long long stream = l2_evict_first();
         for (size_t i = t0; i < quads; i += 2 * stride) {
             const bool two = i + stride < quads;
-            const int4 a = q[i];
-            const int4 b = two ? q[i + stride] : make_int4(0, 0, 0, 0);
-            o[i] = make_int4(match_one(a.x, dense, bits, lo, hi, vals, keys), match_one(a.y, dense, bits, lo, hi, vals, keys),
-                             match_one(a.z, dense, bits, lo, hi, vals, keys), match_one(a.w, dense, bits, lo, hi, vals, keys));
+            const int4 a = ld_v4_hint(q + i, stream);
+            const int4 b = two ? ld_v4_hint(q + i + stride, stream) : make_int4(0, 0, 0, 0);
+            st_v4_hint(o + i,
+                       make_int4(match_one(a.x, dense, bits, lo, hi, vals, keys), match_one(a.y, dense, bits, lo, hi, vals, keys),
+                                 match_one(a.z, dense, bits, lo, hi, vals, keys), match_one(a.w, dense, bits, lo, hi, vals, keys)),
+                       stream);
             if (two)
-                o[i + stride] = make_int4(match_one(b.x, dense, bits, lo, hi, vals, keys), match_one(b.y, dense, bits, lo, hi, vals, keys),
-                                          match_one(b.z, dense, bits, lo, hi, vals, keys), match_one(b.w, dense, bits, lo, hi, vals, keys));
+                st_v4_hint(o + i + stride,
+                           make_int4(match_one(b.x, dense, bits, lo, hi, vals, keys), match_one(b.y, dense, bits, lo, hi, vals, keys),
+                                     match_one(b.z, dense, bits, lo, hi, vals, keys), match_one(b.w, dense, bits, lo, hi, vals, keys)),
+                           stream);
         }
         done = 4 * quads;
     }
