@@ -537,15 +537,15 @@ __device__ __forceinline__ int match_one(int r, bool dense, unsigned bits, long 
     return j != INT_MAX ? j : -1;
 }
 
-__global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, const MatchWs* ws, unsigned bits,
-                                    const int* __restrict__ vals,
-                                    const unsigned long long* __restrict__ keys,
-                                    int32_t* __restrict__ row_out) {
-    const bool dense = dense_mode(ws, bits);
-    const long long lo = ws_vmin(ws), hi = ws_vmax(ws);
+template <bool kDense>
+__device__ __forceinline__ void match_lookup_body(const int32_t* __restrict__ ra, size_t n, unsigned bits, long long lo,
+                                                  long long hi, const int* __restrict__ vals,
+                                                  const unsigned long long* __restrict__ keys,
+                                                  int32_t* __restrict__ row_out) {
     const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
     const size_t t0 = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
     size_t done = 0;
+    auto one = [&](int r) { return match_one(r, kDense, bits, lo, hi, vals, keys); };
     if (((reinterpret_cast<uintptr_t>(ra) | reinterpret_cast<uintptr_t>(row_out)) & 15) == 0) {
         // quads in, quads out; two quads in flight per thread
         const size_t quads = n / 4;
@@ -556,19 +556,23 @@ __global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, co
             const bool two = i + stride < quads;
             const int4 a = ld_v4_hint(q + i, stream);
             const int4 b = two ? ld_v4_hint(q + i + stride, stream) : make_int4(0, 0, 0, 0);
-            st_v4_hint(o + i,
-                       make_int4(match_one(a.x, dense, bits, lo, hi, vals, keys), match_one(a.y, dense, bits, lo, hi, vals, keys),
-                                 match_one(a.z, dense, bits, lo, hi, vals, keys), match_one(a.w, dense, bits, lo, hi, vals, keys)),
-                       stream);
-            if (two)
-                st_v4_hint(o + i + stride,
-                           make_int4(match_one(b.x, dense, bits, lo, hi, vals, keys), match_one(b.y, dense, bits, lo, hi, vals, keys),
-                                     match_one(b.z, dense, bits, lo, hi, vals, keys), match_one(b.w, dense, bits, lo, hi, vals, keys)),
-                           stream);
+            st_v4_hint(o + i, make_int4(one(a.x), one(a.y), one(a.z), one(a.w)), stream);
+            if (two) st_v4_hint(o + i + stride, make_int4(one(b.x), one(b.y), one(b.z), one(b.w)), stream);
         }
         done = 4 * quads;
     }
-    for (size_t j = done + t0; j < n; j += stride) row_out[j] = match_one(ra[j], dense, bits, lo, hi, vals, keys);
+    for (size_t j = done + t0; j < n; j += stride) row_out[j] = one(ra[j]);
+}
+
+__global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, const MatchWs* ws, unsigned bits,
+                                    const int* __restrict__ vals,
+                                    const unsigned long long* __restrict__ keys,
+                                    int32_t* __restrict__ row_out) {
+    const long long lo = ws_vmin(ws), hi = ws_vmax(ws);
+    if (dense_mode(ws, bits))  // uniform: the dense loop compiles without the probing path
+        match_lookup_body<true>(ra, n, bits, lo, hi, vals, keys, row_out);
+    else
+        match_lookup_body<false>(ra, n, bits, lo, hi, vals, keys, row_out);
 }
 
 // ---------------------------------------------------------------- blends
