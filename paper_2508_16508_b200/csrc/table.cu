@@ -120,17 +120,34 @@ constexpr int kCMinB = kPT >= 512 ? 1 : ABMX_COMPACT_CTAS;  // compact_indices: 
 constexpr int kPIn = ABMX_SCAN_STAGES;  // input stages
 constexpr int kPOut = 2;       // rank_scan output stages
 
+// Pass 1 only counts, so the output stages also serve as input slots: the ring is kP1 slots deep
+// there (rank_scan 13, compact_indices 9) and kPIn in pass 2.
+constexpr int kP1Max = 16;
+
 struct PipeShared {
-    unsigned long long bar[kPIn];
+    unsigned long long bar[kP1Max];
     unsigned wtot[kPT / 32];
     unsigned long long red[kPT / 32][2];
     unsigned long long total, base, T;
 };
 
 template <bool kCompact>
-constexpr int pipe_smem() {
+__host__ __device__ constexpr int pipe_smem() {
     return kPIn * kPTile + (kCompact ? kPTile + 16 : kPOut * kPTile) * static_cast<int>(sizeof(int32_t));
 }
+
+#ifdef ABMX_SCAN_TRACE  // per-CTA %globaltimer stamps: start, pass 1 done, gather done, end
+__device__ unsigned long long g_scan_trace[2048][4];
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SCAN_STAMP(k) \
+    if (tid == 0) g_scan_trace[b][k] = gtime()
+#else
+#define SCAN_STAMP(k)
+#endif
 
 template <bool kCompact>
 __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_kernel(const uint8_t* __restrict__ mask, int32_t* __restrict__ out,
@@ -151,39 +168,44 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
     // The chunk's mask is read twice: pass 1 keeps it in L2 (evict_last; 2^26 bytes fit), pass 2
     // reads it for the last time and the outputs stream past it (evict_first).
     const unsigned long long keep = l2_evict_last(), stream = l2_evict_first();
-    auto issue = [&](int it) {  // one thread: the tile of iteration `it` into ring slot it % kPIn
+    constexpr int kP1 = pipe_smem<kCompact>() / kPTile;
+    static_assert(kP1 <= kP1Max && kP1 >= kPIn, "pass-1 ring");
+    auto slot_of = [&](int it) { return it < m ? it % kP1 : (it - m) % kPIn; };
+    auto issue = [&](int it) {  // one thread: the tile of iteration `it` into its ring slot
         if (it >= 2 * m) return;
-        const int t = tile_of(it), s = it % kPIn;
+        const int t = tile_of(it), s = slot_of(it);
         if (is_bulk(t)) {
             mbar_expect_tx(&S.bar[s], kPTile);
             bulk_g2s_hint(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s],
                           it < m ? keep : stream);
         }
     };
+    SCAN_STAMP(0);
     if (tid == 0) {
-        for (int s = 0; s < kPIn; ++s) mbar_init(&S.bar[s], 1);
+        for (int s = 0; s < kP1; ++s) mbar_init(&S.bar[s], 1);
         mbar_fence_init();
-        for (int it = 0; it < kPIn; ++it) issue(it);
+        for (int it = 0; it < kP1 && it < m; ++it) issue(it);  // pass 1 only
     }
     __syncthreads();
     unsigned phase = 0;            // bit s: parity of ring slot s's next bulk completion
     unsigned long long run = 0;    // pass 2: elements' prefix before this tile (global)
     unsigned long long lane_acc = 0;  // pass 1: this lane's nonzero count over the chunk
     for (int it = 0; it < 2 * m; ++it) {
-        const int s = it % kPIn;
+        const int s = slot_of(it);
         const int tile = tile_of(it);
         const bool pass2 = it >= m;
         const size_t tb = static_cast<size_t>(tile) * kPTile;
         const int tn = static_cast<int>(n - tb < static_cast<size_t>(kPTile) ? n - tb : kPTile);
         uint8_t* buf = in + s * kPTile;
         if (!kCompact && pass2 && tid == 0) bulk_wait_read<kPOut - 1>();  // the output stage we reuse is free
-        if (is_bulk(tile)) {
+        const bool bulk = is_bulk(tile);  // uniform
+        if (bulk) {
             mbar_wait(&S.bar[s], (phase >> s) & 1u);
             phase ^= 1u << s;
         } else {
             for (int j = tid; j < kPTile; j += kPT) buf[j] = j < tn ? mask[tb + j] : 0;
-            __syncthreads();
         }
+        if (!bulk) __syncthreads();  // the plain loads are visible (outside the branch)
         // ---- per-word nonzero counts
         const uint32_t* wbuf = reinterpret_cast<const uint32_t*>(buf) + warp * 256;
         uint32_t wd[8];
@@ -196,8 +218,8 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
         }
         if (!pass2) {  // pass 1 only needs the chunk total: accumulate per lane, one barrier per tile
             lane_acc += lt;
-            __syncthreads();  // every read of buf is done: refill slot s kPIn iterations ahead
-            if (tid == 0) issue(it + kPIn);
+            __syncthreads();  // every read of buf is done: refill slot s kP1 iterations ahead
+            if (tid == 0 && it + kP1 < m) issue(it + kP1);
         } else {
             const unsigned wt = __reduce_add_sync(0xffffffffu, lt);
             if (lane == 0) S.wtot[warp] = wt;
@@ -219,6 +241,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
         }
         if (it == m - 1) {
             // ---- gather: publish this chunk's total, read every chunk's (all CTAs are resident)
+            SCAN_STAMP(1);
             const unsigned long long wsum = warp_sum(lane_acc);
             if (lane == 0) S.red[warp][0] = wsum;
             __syncthreads();
@@ -226,16 +249,20 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
                 unsigned long long x = 0;
                 for (int w = 0; w < kPT / 32; ++w) x += S.red[w][0];
                 st_word(&chunk_tot[b], kFlagAgg | x);
+                // one counter of published chunks (release); only this thread polls it (acquire),
+                // instead of every thread spinning on the chunk words
+                unsigned* published = reinterpret_cast<unsigned*>(chunk_tot + G);
+                red_release_add(published, 1u);
+                // every pass-1 slot is consumed (the barrier above): pass 2's first tiles load
+                // while the chunk totals are gathered
+                for (int q = 0; q < kPIn; ++q) issue(m + q);
+                while (ld_acquire_u32(published) < static_cast<unsigned>(G)) {
+                }
             }
-            __syncthreads();
+            __syncthreads();  // thread 0's acquire + the barrier: every chunk word is visible
             unsigned long long before = 0, all = 0;
             for (int q = tid; q < G; q += kPT) {
-                unsigned long long v = ld_word(&chunk_tot[q]);
-                while ((v >> 62) == 0) {
-                    __nanosleep(32);
-                    v = ld_word(&chunk_tot[q]);
-                }
-                v &= kValueMask;
+                const unsigned long long v = ld_word(&chunk_tot[q]) & kValueMask;
                 all += v;
                 if (q < b) before += v;
             }
@@ -257,6 +284,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
                 if (kCompact && b == 0 && true_out) *true_out = y;  // count_true(mask)
             }
             __syncthreads();
+            SCAN_STAMP(2);
             run = S.base;
             continue;
         }
@@ -342,6 +370,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
         run += S.total;
     }
     if (!kCompact && tid == 0) bulk_wait_all();
+    SCAN_STAMP(3);
 }
 
 // ---------------------------------------------------------------- match_first_equal
@@ -616,6 +645,12 @@ __global__ void __launch_bounds__(kThreads) blend_kernel(const uint8_t* mask, co
 
 }  // namespace abmx_table
 
+#ifdef ABMX_SCAN_TRACE
+extern "C" int abmx_scan_trace(unsigned long long* out, int ctas) {
+    return cudaMemcpyFromSymbol(out, abmx_table::g_scan_trace, sizeof(unsigned long long) * 4 * ctas) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 // ====================================================================== launchers
 using namespace abmx_table;
 
@@ -644,9 +679,10 @@ static cudaError_t launch_scan_pipe(const uint8_t* d_mask, int32_t* d_out, size_
     const size_t cap = static_cast<size_t>(num_sms()) * static_cast<size_t>(per_sm < want ? per_sm : want);
     const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
     void* ws = nullptr;
-    e = abmx_internal::malloc_async(&ws, grid * sizeof(unsigned long long), s);
+    const size_t ws_bytes = (grid + 1) * sizeof(unsigned long long);  // chunk totals, published count
+    e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(ws, 0, grid * sizeof(unsigned long long), s);
+    cudaMemsetAsync(ws, 0, ws_bytes, s);
     (void)cudaGetLastError();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
