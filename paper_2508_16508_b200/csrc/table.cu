@@ -127,8 +127,11 @@ constexpr int kP1Max = 16;
 struct PipeShared {
     unsigned long long bar[kP1Max];
     unsigned wtot[kPT / 32];
-    unsigned long long red[kPT / 32][2];
+    unsigned wt1[2][kPT / 32];          // pass 1: warp counts of the last two tiles
+    unsigned long long red[kPT / 32 + 2][2];
     unsigned long long total, base, T;
+    unsigned long long jb[kPIn];        // pass 2: base of the tile queued in each slot
+    int jt[kPIn];                       // ... and the tile (-1: none left)
 };
 
 template <bool kCompact>
@@ -149,6 +152,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define SCAN_STAMP(k)
 #endif
 
+// Workspace of one call (zeroed: the chunk totals and the three counters; the per-tile arrays
+// are fully written before they are read).
+struct ScanWs {
+    unsigned published;    // chunks whose pass-1 total is out
+    unsigned next_tile;    // pass 2: the next unclaimed tile
+};
+
 template <bool kCompact>
 __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_kernel(const uint8_t* __restrict__ mask, int32_t* __restrict__ out,
                                                           size_t n, int tiles, unsigned long long* __restrict__ chunk_tot,
@@ -161,44 +171,61 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
     const int G = static_cast<int>(gridDim.x), b = static_cast<int>(blockIdx.x);
     const int c0 = static_cast<int>(static_cast<long long>(tiles) * b / G);
     const int m = static_cast<int>(static_cast<long long>(tiles) * (b + 1) / G) - c0;  // >= 1 (grid <= tiles)
+    ScanWs* ws = reinterpret_cast<ScanWs*>(chunk_tot + G);
+    unsigned long long* tile_base = reinterpret_cast<unsigned long long*>(ws + 1);  // [tiles] kFlagAgg | base (zeroed)
+    unsigned* tile_cnt = reinterpret_cast<unsigned*>(tile_base + tiles);             // [tiles]
     const bool in_vec = (reinterpret_cast<uintptr_t>(mask) & 15) == 0;
     const bool out_vec = (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    auto tile_of = [&](int it) { return c0 + it % m; };  // iterations 0..2m-1: the chunk, twice
     auto is_bulk = [&](int t) { return in_vec && static_cast<size_t>(t + 1) * kPTile <= n; };
-    // The chunk's mask is read twice: pass 1 keeps it in L2 (evict_last; 2^26 bytes fit), pass 2
-    // reads it for the last time and the outputs stream past it (evict_first).
+    // The mask is read twice: pass 1 keeps it in L2 (evict_last; 2^26 bytes fit), pass 2 reads it
+    // for the last time and the outputs stream past it (evict_first).
     const unsigned long long keep = l2_evict_last(), stream = l2_evict_first();
     constexpr int kP1 = pipe_smem<kCompact>() / kPTile;
     static_assert(kP1 <= kP1Max && kP1 >= kPIn, "pass-1 ring");
-    auto slot_of = [&](int it) { return it < m ? it % kP1 : (it - m) % kPIn; };
-    auto issue = [&](int it) {  // one thread: the tile of iteration `it` into its ring slot
-        if (it >= 2 * m) return;
-        const int t = tile_of(it), s = slot_of(it);
+    auto load = [&](int t, int s, unsigned long long policy) {  // one thread: tile t into ring slot s
         if (is_bulk(t)) {
             mbar_expect_tx(&S.bar[s], kPTile);
-            bulk_g2s_hint(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s],
-                          it < m ? keep : stream);
+            bulk_g2s_hint(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s], policy);
         }
+    };
+    // Pass 2: thread 0 claims the next tile of the whole mask (every CTA draws from one counter,
+    // so the CTAs that stream faster take more tiles) and queues it with its base in a ring slot.
+    // The claims are pipelined in thread 0's registers: the atomic of a claim is issued two
+    // refills before its slot is filled and the load of its base one refill before, so neither
+    // round trip is waited on where it is issued.
+    unsigned q1 = 0;               // stage 1: a claimed tile index (atomic in flight)
+    int q2t = -1;                  // stage 2: a claimed tile (-1: none left) ...
+    unsigned long long q2b = 0;    // ... and its base word (load in flight)
+    auto base_of = [&](int t, unsigned long long w) {  // the owner publishes it right after its gather
+        while ((w >> 62) == 0) w = ld_word(&tile_base[t]);
+        return w & kValueMask;
+    };
+    auto queue = [&](int s, int t, unsigned long long w) {
+        S.jt[s] = t;
+        if (t < 0) return;
+        S.jb[s] = base_of(t, w);
+        load(t, s, stream);
+    };
+    auto refill = [&](int s) {
+        queue(s, q2t, q2b);
+        q2t = q1 < static_cast<unsigned>(tiles) ? static_cast<int>(q1) : -1;
+        if (q2t >= 0) q2b = ld_word(&tile_base[q2t]);
+        q1 = atomicAdd(&ws->next_tile, 1u);
     };
     SCAN_STAMP(0);
     if (tid == 0) {
         for (int s = 0; s < kP1; ++s) mbar_init(&S.bar[s], 1);
         mbar_fence_init();
-        for (int it = 0; it < kP1 && it < m; ++it) issue(it);  // pass 1 only
+        for (int it = 0; it < kP1 && it < m; ++it) load(c0 + it, it, keep);
     }
     __syncthreads();
-    unsigned phase = 0;            // bit s: parity of ring slot s's next bulk completion
-    unsigned long long run = 0;    // pass 2: elements' prefix before this tile (global)
-    unsigned long long lane_acc = 0;  // pass 1: this lane's nonzero count over the chunk
-    for (int it = 0; it < 2 * m; ++it) {
-        const int s = slot_of(it);
-        const int tile = tile_of(it);
-        const bool pass2 = it >= m;
-        const size_t tb = static_cast<size_t>(tile) * kPTile;
+    unsigned phase = 0;  // bit s: parity of ring slot s's next bulk completion
+    // the tile in ring slot s: its words, per-word nonzero counts (0..4) and the lane's total
+    auto fetch = [&](int t, int s, uint32_t* wd, unsigned* c) {
+        const size_t tb = static_cast<size_t>(t) * kPTile;
         const int tn = static_cast<int>(n - tb < static_cast<size_t>(kPTile) ? n - tb : kPTile);
         uint8_t* buf = in + s * kPTile;
-        if (!kCompact && pass2 && tid == 0) bulk_wait_read<kPOut - 1>();  // the output stage we reuse is free
-        const bool bulk = is_bulk(tile);  // uniform
+        const bool bulk = is_bulk(t);  // uniform
         if (bulk) {
             mbar_wait(&S.bar[s], (phase >> s) & 1u);
             phase ^= 1u << s;
@@ -206,89 +233,131 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
             for (int j = tid; j < kPTile; j += kPT) buf[j] = j < tn ? mask[tb + j] : 0;
         }
         if (!bulk) __syncthreads();  // the plain loads are visible (outside the branch)
-        // ---- per-word nonzero counts
         const uint32_t* wbuf = reinterpret_cast<const uint32_t*>(buf) + warp * 256;
-        uint32_t wd[8];
-        unsigned c[8], lt = 0;  // this warp's 1024 elements: 8 rows of 32 words
+        unsigned lt = 0;  // this warp's 1024 elements: 8 rows of 32 words
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
             wd[r] = wbuf[r * 32 + lane];
             c[r] = nz_bytes(wd[r]);
             lt += c[r];
         }
-        if (!pass2) {  // pass 1 only needs the chunk total: accumulate per lane, one barrier per tile
-            lane_acc += lt;
-            __syncthreads();  // every read of buf is done: refill slot s kP1 iterations ahead
-            if (tid == 0 && it + kP1 < m) issue(it + kP1);
-        } else {
-            const unsigned wt = __reduce_add_sync(0xffffffffu, lt);
-            if (lane == 0) S.wtot[warp] = wt;
-            __syncthreads();  // every read of buf is done: refill slot s kPIn iterations ahead
-            if (tid == 0) issue(it + kPIn);
-            if (warp == 0) {
-                const unsigned v = lane < kPT / 32 ? S.wtot[lane] : 0u;
-                unsigned incl = v;
+        return lt;
+    };
+    // ---- pass 1: the chunk's tiles, counted (per tile, for the tile bases)
+    unsigned long long lane_acc = 0;
+    for (int it = 0; it < m; ++it) {
+        uint32_t wd[8];
+        unsigned c[8];
+        const unsigned lt = fetch(c0 + it, it % kP1, wd, c);
+        lane_acc += lt;
+        const unsigned wt = __reduce_add_sync(0xffffffffu, lt);
+        if (lane == 0) S.wt1[it & 1][warp] = wt;
+        __syncthreads();  // every read of the slot is done: refill it kP1 tiles ahead
+        if (tid == 0) {
+            unsigned x = 0;
 #pragma unroll
-                for (int d = 1; d < kPT / 32; d <<= 1) {
-                    const unsigned u = __shfl_up_sync(0xffffffffu, incl, d);
-                    if (lane >= d) incl += u;
-                }
-                const unsigned total = __shfl_sync(0xffffffffu, incl, kPT / 32 - 1);
-                if (lane < kPT / 32) S.wtot[lane] = incl - v;  // exclusive warp offsets
-                if (lane == 0) S.total = total;
-            }
-            __syncthreads();
+            for (int w = 0; w < kPT / 32; ++w) x += S.wt1[it & 1][w];
+            tile_cnt[c0 + it] = x;
+            if (it + kP1 < m) load(c0 + it + kP1, (it + kP1) % kP1, keep);
         }
-        if (it == m - 1) {
-            // ---- gather: publish this chunk's total, read every chunk's (all CTAs are resident)
-            SCAN_STAMP(1);
-            const unsigned long long wsum = warp_sum(lane_acc);
-            if (lane == 0) S.red[warp][0] = wsum;
-            __syncthreads();
-            if (tid == 0) {
-                unsigned long long x = 0;
-                for (int w = 0; w < kPT / 32; ++w) x += S.red[w][0];
-                st_word(&chunk_tot[b], kFlagAgg | x);
-                // one counter of published chunks (release); only this thread polls it (acquire),
-                // instead of every thread spinning on the chunk words
-                unsigned* published = reinterpret_cast<unsigned*>(chunk_tot + G);
-                red_release_add(published, 1u);
-                // every pass-1 slot is consumed (the barrier above): pass 2's first tiles load
-                // while the chunk totals are gathered
-                for (int q = 0; q < kPIn; ++q) issue(m + q);
-                while (ld_acquire_u32(published) < static_cast<unsigned>(G)) {
-                }
+    }
+    // ---- gather: publish this chunk's total, read every chunk's (all CTAs are resident)
+    SCAN_STAMP(1);
+    {
+        const unsigned long long wsum = warp_sum(lane_acc);
+        if (lane == 0) S.red[warp][0] = wsum;
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long x = 0;
+            for (int w = 0; w < kPT / 32; ++w) x += S.red[w][0];
+            st_word(&chunk_tot[b], kFlagAgg | x);
+            // one counter of published chunks (release); only this thread polls it (acquire)
+            red_release_add(&ws->published, 1u);
+            while (ld_acquire_u32(&ws->published) < static_cast<unsigned>(G)) {
             }
-            __syncthreads();  // thread 0's acquire + the barrier: every chunk word is visible
-            unsigned long long before = 0, all = 0;
-            for (int q = tid; q < G; q += kPT) {
-                const unsigned long long v = ld_word(&chunk_tot[q]) & kValueMask;
-                all += v;
-                if (q < b) before += v;
-            }
-            before = warp_sum(before);
-            all = warp_sum(all);
-            if (lane == 0) {
-                S.red[warp][0] = before;
-                S.red[warp][1] = all;
-            }
-            __syncthreads();
-            if (tid == 0) {
-                unsigned long long x = 0, y = 0;
-                for (int w = 0; w < kPT / 32; ++w) {
-                    x += S.red[w][0];
-                    y += S.red[w][1];
-                }
-                S.base = x;
-                S.T = y;
-                if (kCompact && b == 0 && true_out) *true_out = y;  // count_true(mask)
-            }
-            __syncthreads();
-            SCAN_STAMP(2);
-            run = S.base;
-            continue;
         }
-        if (!pass2) continue;
+        __syncthreads();  // thread 0's acquire + the barrier: every chunk word is visible
+        unsigned long long before = 0, all = 0;
+        for (int q = tid; q < G; q += kPT) {
+            const unsigned long long v = ld_word(&chunk_tot[q]) & kValueMask;
+            all += v;
+            if (q < b) before += v;
+        }
+        before = warp_sum(before);
+        all = warp_sum(all);
+        if (lane == 0) {
+            S.red[warp][0] = before;
+            S.red[warp][1] = all;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            unsigned long long x = 0, y = 0;
+            for (int w = 0; w < kPT / 32; ++w) {
+                x += S.red[w][0];
+                y += S.red[w][1];
+            }
+            S.base = x;
+            S.T = y;
+            if (kCompact && b == 0 && true_out) *true_out = y;  // count_true(mask)
+        }
+        __syncthreads();
+        // the chunk's tile bases: chunk base + exclusive prefix of its tile counts
+        unsigned long long carry = S.base;
+        for (int k0 = 0; k0 < m; k0 += kPT) {
+            const int k = k0 + tid;
+            const unsigned long long v = k < m ? tile_cnt[c0 + k] : 0ULL;
+            unsigned long long tot;
+            const unsigned long long ex = block_excl_scan<kPT>(v, &S.red[0][0], &tot);
+            if (k < m) st_word(&tile_base[c0 + k], kFlagAgg | (carry + ex));
+            carry += tot;
+            __syncthreads();  // S.red is reused by the next round / below
+        }
+        if (tid == 0) {  // every pass-1 slot is consumed: the first kPIn claims (one atomic, the
+                         // base loads in flight together), then prime the pipeline
+            const unsigned t0 = atomicAdd(&ws->next_tile, static_cast<unsigned>(kPIn));
+            unsigned long long w[kPIn];
+#pragma unroll
+            for (int s = 0; s < kPIn; ++s) w[s] = t0 + s < static_cast<unsigned>(tiles) ? ld_word(&tile_base[t0 + s]) : 0ULL;
+#pragma unroll
+            for (int s = 0; s < kPIn; ++s) queue(s, t0 + s < static_cast<unsigned>(tiles) ? static_cast<int>(t0 + s) : -1, w[s]);
+            q1 = atomicAdd(&ws->next_tile, 1u);
+            q2t = q1 < static_cast<unsigned>(tiles) ? static_cast<int>(q1) : -1;
+            if (q2t >= 0) q2b = ld_word(&tile_base[q2t]);
+            q1 = atomicAdd(&ws->next_tile, 1u);
+        }
+        __syncthreads();
+    }
+    SCAN_STAMP(2);
+    // ---- pass 2: claimed tiles, ranked / partitioned from their bases
+    for (int p = 0;; ++p) {
+        const int s = p % kPIn;
+        const int tile = S.jt[s];
+        if (tile < 0) break;  // the counter ran out (uniform)
+        const unsigned long long run = S.jb[s];
+        const size_t tb = static_cast<size_t>(tile) * kPTile;
+        const int tn = static_cast<int>(n - tb < static_cast<size_t>(kPTile) ? n - tb : kPTile);
+        if (!kCompact && tid == 0) bulk_wait_read<kPOut - 1>();  // the output stage we reuse is free
+        uint32_t wd[8];
+        unsigned c[8];
+        const unsigned lt = fetch(tile, s, wd, c);
+        const unsigned wt = __reduce_add_sync(0xffffffffu, lt);
+        if (lane == 0) S.wtot[warp] = wt;
+        __syncthreads();  // every read of the slot is done: claim and refill it kPIn tiles ahead
+        if (tid == 0) refill(s);
+        if (warp == 0) {
+            const unsigned v = lane < kPT / 32 ? S.wtot[lane] : 0u;
+            unsigned incl = v;
+#pragma unroll
+            for (int d = 1; d < kPT / 32; d <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += u;
+            }
+            const unsigned total = __shfl_sync(0xffffffffu, incl, kPT / 32 - 1);
+            if (lane < kPT / 32) S.wtot[lane] = incl - v;  // exclusive warp offsets
+            if (lane == 0) S.total = total;
+        }
+        __syncthreads();
+        const int it = p;  // output stage
         const unsigned lt_mask = (1u << lane) - 1u;
         if constexpr (!kCompact) {
             int32_t* o = ob + (it % kPOut) * kPTile;
@@ -367,7 +436,6 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
                 for (int j = tid; j < tn; j += kPT) out[j < ttot ? run + j : f_dst + j] = j < ttot ? ob[at + j] : ob[fb + j - ttot];
             }
         }
-        run += S.total;
     }
     if (!kCompact && tid == 0) bulk_wait_all();
     SCAN_STAMP(3);
@@ -679,10 +747,12 @@ static cudaError_t launch_scan_pipe(const uint8_t* d_mask, int32_t* d_out, size_
     const size_t cap = static_cast<size_t>(num_sms()) * static_cast<size_t>(per_sm < want ? per_sm : want);
     const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
     void* ws = nullptr;
-    const size_t ws_bytes = (grid + 1) * sizeof(unsigned long long);  // chunk totals, published count
+    // chunk totals, counters and flagged tile bases (zeroed), then the tile counts (written before read)
+    const size_t zero_bytes = grid * sizeof(unsigned long long) + sizeof(ScanWs) + tiles * sizeof(unsigned long long);
+    const size_t ws_bytes = zero_bytes + tiles * sizeof(unsigned);
     e = abmx_internal::malloc_async(&ws, ws_bytes, s);
     if (e != cudaSuccess) return e;
-    cudaMemsetAsync(ws, 0, ws_bytes, s);
+    cudaMemsetAsync(ws, 0, zero_bytes, s);
     (void)cudaGetLastError();
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
