@@ -30,6 +30,20 @@ def test_rank_scan_count_compact(abmx, oracle, n):
         assert np.array_equal(abmx.compact_indices(m), oracle.compact_indices(m)), (n, density)
 
 
+def test_scan_full_size_repeated(abmx, oracle):
+    """The bench size (2^26) plus an odd tail, several masks back to back: every pass-2 tile is
+    claimed from the global counter with a flagged base published by another CTA, so a lost or
+    stale base shows up as a wrong rank."""
+    rng = np.random.default_rng(26)
+    n = (1 << 26) + 12345
+    for density in (0.5, 0.01, 0.99):
+        m = masks(rng, n, density)
+        want = oracle.rank_scan(m)
+        for _ in range(2):
+            assert np.array_equal(abmx.rank_scan(m), want), density
+        assert np.array_equal(abmx.compact_indices(m), oracle.compact_indices(m)), density
+
+
 def test_literal_examples(abmx):
     """test_kernels.cpp:48-52, 73-92."""
     assert abmx.compute_ranks([0, 0, 0]).tolist() == [0, 0, 0]
