@@ -409,7 +409,7 @@ def agents_section(args, rank):
         arr, keep = s._rows({k: torch.from_numpy(v).cuda() for k, v in rows.items()}, cap)
         return s, arr, keep
 
-    def cycle(s, arr, k):  # abmx_agents_lifecycle: remove + spawn fused into two kernels
+    def cycle(s, arr, k):  # abmx_agents_lifecycle: remove + spawn fused into one cooperative kernel
         stream = s._stream()
         abmx._check(abmx.lib.abmx_agents_lifecycle(C.byref(s._c), dk[k].data_ptr(), cap, dv[k].data_ptr(), arr, 0, 0,
                                                    out.data_ptr(), res.data_ptr(), stream))
@@ -451,7 +451,7 @@ def agents_section(args, rank):
                          f"{AGENT_CHURN} valid, copy apply (fused: abmx_agents_lifecycle); {K} cycles, "
                          f"L2 flushed before each",
              "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms,
-             "launches_per_cycle": "1 memset + 2 kernels (abmx_agents_lifecycle)",
+             "launches_per_cycle": "1 memset + 1 cooperative kernel (abmx_agents_lifecycle, k_life_coop)",
              "two_call_ms_per_cycle": ms_two, "fused_equals_two_calls": bool(same)}
     if rank == 0 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))

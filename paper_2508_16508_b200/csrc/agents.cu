@@ -342,6 +342,145 @@ __global__ void __launch_bounds__(kT) k_life_apply(const int32_t* __restrict__ s
     }
 }
 
+// The same cycle as ONE cooperative kernel when every tile CTA is co-resident (k_life_coop):
+//   count   each CTA (one slot or row tile) counts (killed, free) or valid, publishes the total and
+//           arrives at barrier 1 (a release increment; thread 0 alone polls the counter)
+//   write   every CTA reads all tile totals (its prefix, K, F, Q): slot tiles reset their killed
+//           slots (ids pushed at top + killed prefix, slot order) and list their free slots of
+//           rank < r = min(F, Q); row tiles list their valid rows of rank < r; barrier 2
+//   pair    pairs k < r over the whole grid; block 0 commits the counters after barrier 2
+//           (every CTA read the old ones before barrier 1)
+// Two counter barriers replace the ticket + lookback of k_life_select and the last-CTA
+// handshake of k_life_apply.
+struct LifeWs {
+    unsigned arrived[2];        // CTAs past the count / the write phase (zeroed)
+    unsigned long long tot[1];  // [G] kFlagAgg | pack2(killed, free) (slot tile) or pack2(0, valid)
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned G) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        red_release_add(ctr, 1u);
+        while (ld_acquire_u32(ctr) < G) {
+        }
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ kill, size_t n, unsigned ta,
+                                                  const uint8_t* __restrict__ valid, size_t m,
+                                                  int32_t* __restrict__ slots, int32_t* __restrict__ rows, LifeWs* ws,
+                                                  Cols Z, Cols A, Life L, int set_type, long long agent_type,
+                                                  long long* out_killed, long long* out) {
+    __shared__ unsigned long long s_scan[kT / 32 + 1];
+    __shared__ unsigned long long s_red[kT / 32][5];
+    __shared__ unsigned long long s_v[5];
+    const unsigned G = gridDim.x, b = blockIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const bool slot_tile = b < ta;
+    const size_t base = static_cast<size_t>(slot_tile ? b : b - ta) * kTile + static_cast<size_t>(tid) * kItems;
+    // the counters before the cycle (block 0 rewrites them after barrier 2)
+    const long long live0 = L.counters[0], nid = L.counters[1];
+    const long long top0 = L.recycle ? L.counters[2] : 0;
+    // ---- count
+    bool s1[kItems], s2[kItems];  // slot tile: killed, free once removed; row tile: -, valid
+    unsigned c1 = 0, c2 = 0;
+    {
+        uint8_t x[kItems], a[kItems];
+        load16(slot_tile ? kill : valid, base, slot_tile ? n : m, x);
+        load16(slot_tile ? L.active : nullptr, base, n, a);
+#pragma unroll
+        for (int k = 0; k < kItems; ++k) {
+            const bool in = base + k < (slot_tile ? n : m);
+            s1[k] = slot_tile && in && a[k] != 0 && x[k] != 0;
+            s2[k] = in && (slot_tile ? (a[k] == 0 || s1[k]) : x[k] != 0);
+            c1 += s1[k];
+            c2 += s2[k];
+        }
+    }
+    unsigned long long total;
+    const unsigned long long excl = block_excl_scan<kT>(pack2(c1, c2), s_scan, &total);
+    if (tid == 0) st_word(&ws->tot[b], kFlagAgg | total);
+    grid_barrier(&ws->arrived[0], G);
+    // ---- every tile total: this tile's prefix, K (killed), F (free), Q (valid)
+    unsigned long long pk = 0, pf = 0, K = 0, F = 0, Q = 0;
+    for (unsigned q = tid; q < G; q += kT) {
+        const unsigned long long v = ld_word(&ws->tot[q]);
+        if (q < ta) {
+            K += hi31(v);
+            F += lo31(v);
+        } else {
+            Q += lo31(v);
+        }
+        if (q < b && (q < ta) == slot_tile) {
+            pk += hi31(v);
+            pf += lo31(v);
+        }
+    }
+    {
+        unsigned long long v5[5] = {pk, pf, K, F, Q};
+#pragma unroll
+        for (int i = 0; i < 5; ++i) v5[i] = warp_sum(v5[i]);
+        if (lane == 0)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) s_red[warp][i] = v5[i];
+        __syncthreads();
+        if (tid < 5) {
+            unsigned long long x = 0;
+            for (int w = 0; w < kT / 32; ++w) x += s_red[w][tid];
+            s_v[tid] = x;
+        }
+        __syncthreads();
+    }
+    K = s_v[2];
+    F = s_v[3];
+    Q = s_v[4];
+    const long long r = static_cast<long long>(F < Q ? F : Q);
+    // ---- write
+    long long kpos = static_cast<long long>(s_v[0]) + hi31(excl);  // killed before this thread
+    long long fpos = static_cast<long long>(s_v[1]) + lo31(excl);  // free (or valid) before this thread
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+        const size_t i = base + k;
+        if (s1[k]) {  // remove_agents: reset_slot (type kept), push the id
+            if (L.recycle) L.retired[top0 + kpos] = L.ids[i];
+            ++kpos;
+            L.active[i] = 0;
+            L.ids[i] = 0;
+            L.ages[i] = 0;
+            for (int c = 0; c < Z.n; ++c) zero_elem(Z.dst[c], static_cast<long long>(i), Z.sz[c]);
+        }
+        if (s2[k]) {
+            if (fpos < r) (slot_tile ? slots : rows)[fpos] = static_cast<int32_t>(i);
+            ++fpos;
+        }
+    }
+    __threadfence();  // this CTA's lists, resets and pushes, GPU-wide before barrier 2
+    grid_barrier(&ws->arrived[1], G);
+    const long long top = top0 + (L.recycle ? static_cast<long long>(K) : 0);  // after the pushes
+    if (b == 0 && tid == 0) {  // counters (lifecycle.cpp:136-141, 186-194)
+        const long long used = top < r ? top : r;
+        L.counters[0] = live0 - static_cast<long long>(K) + r;
+        L.counters[1] = nid + r - used;
+        if (L.recycle) L.counters[2] = top - used;
+        if (out_killed) *out_killed = static_cast<long long>(K);
+        if (out) {
+            out[0] = r;
+            out[1] = static_cast<long long>(Q) - r;
+        }
+    }
+    // ---- pair: the k-th free slot takes the k-th valid row
+    for (long long k = static_cast<long long>(b) * kT + tid; k < r; k += static_cast<long long>(G) * kT) {
+        const int slot = slots[k], row = rows[k];
+        for (int c = 0; c < A.n; ++c)
+            if (A.src[c]) copy_elem(A.dst[c], slot, A.src[c], row, A.sz[c]);
+        L.active[slot] = 1;
+        L.ids[slot] = k < top ? L.retired[top - 1 - k] : nid + (k - top);
+        L.ages[slot] = 0;
+        if (set_type) L.types[slot] = agent_type;
+    }
+}
+
 // set_agents_mask with per-slot source values: dst[c][i] <- src[c][i] where mask[i].
 __global__ void __launch_bounds__(kT) k_mask_apply(const uint8_t* __restrict__ mask, size_t n, Cols C) {
     for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT)
@@ -758,6 +897,58 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
     Scratch sc(st);
     const size_t n = static_cast<size_t>(s->capacity);
     const size_t ta = (n + kTile - 1) / kTile, tb = (static_cast<size_t>(m) + kTile - 1) / kTile;
+    Cols Z{};  // removal: zero every state column
+    Z.n = s->n_state;
+    for (int c = 0; c < s->n_state; ++c) {
+        Z.dst[c] = s->state[c].data;
+        Z.src[c] = nullptr;
+        Z.sz[c] = s->state[c].elem_size;
+    }
+    Cols A{};  // spawn: copy the row columns given
+    A.n = 0;
+    for (int c = 0; c < s->n_state; ++c) {
+        if (!rows || !rows[c].data) continue;
+        A.dst[A.n] = s->state[c].data;
+        A.src[A.n] = rows[c].data;
+        A.sz[A.n] = s->state[c].elem_size;
+        ++A.n;
+    }
+    const Life L = life_of(s);
+    static int coop_per_sm[abmx_internal::kMaxDevices] = {};  // co-resident k_life_coop CTAs per SM
+    int dev = 0;
+    CKA(cudaGetDevice(&dev));
+    if (dev >= 0 && dev < abmx_internal::kMaxDevices && coop_per_sm[dev] == 0) {
+        int per = 0;
+        CKA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_life_coop, kT, 0));
+        coop_per_sm[dev] = per > 0 ? per : -1;
+    }
+    const long long coop_cap = dev >= 0 && dev < abmx_internal::kMaxDevices && coop_per_sm[dev] > 0
+                                   ? static_cast<long long>(coop_per_sm[dev]) * abmx_internal::num_sms()
+                                   : 0;
+    if (static_cast<long long>(ta + tb) <= coop_cap) {  // one cooperative kernel
+        const size_t ws_b = (sizeof(LifeWs) + (ta + tb) * sizeof(unsigned long long) + 15) / 16 * 16;
+        void* ws = nullptr;
+        CKA(sc.get(&ws, ws_b + n * 4 + static_cast<size_t>(m) * 4));
+        int32_t* slots = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_b);
+        int32_t* rws = slots + n;
+        CKA(cudaMemsetAsync(ws, 0, sizeof(unsigned) * 2, st));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(ta + tb));
+        cfg.blockDim = dim3(kT);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CKA(cudaLaunchKernelEx(&cfg, k_life_coop, d_kill, n, static_cast<unsigned>(ta), d_valid, static_cast<size_t>(m),
+                               slots, rws, static_cast<LifeWs*>(ws), Z, A, L, static_cast<int>(set_type),
+                               static_cast<long long>(agent_type), reinterpret_cast<long long*>(d_killed),
+                               reinterpret_cast<long long*>(d_result)));
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        return ABMX_OK;
+    }
     const size_t wa_b = (sizeof(ScanWs) + ta * sizeof(unsigned long long) + 15) / 16 * 16;
     const size_t wb_b = (sizeof(ScanWs) + tb * sizeof(unsigned long long) + 15) / 16 * 16;
     const size_t ws_b = (wa_b + wb_b + sizeof(LifeCounts) + 15) / 16 * 16;
@@ -770,27 +961,10 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
     ScanWs* wa = static_cast<ScanWs*>(ws);
     ScanWs* wb = reinterpret_cast<ScanWs*>(static_cast<char*>(ws) + wa_b);
     LifeCounts* cnt = reinterpret_cast<LifeCounts*>(static_cast<char*>(ws) + wa_b + wb_b);
-    const Life L = life_of(s);
-    Cols Z{};  // removal: zero every state column
-    Z.n = s->n_state;
-    for (int c = 0; c < s->n_state; ++c) {
-        Z.dst[c] = s->state[c].data;
-        Z.src[c] = nullptr;
-        Z.sz[c] = s->state[c].elem_size;
-    }
     k_life_select<<<static_cast<unsigned>(ta + tb), kT, 0, st>>>(d_kill, n, slots, wa, static_cast<unsigned>(ta), d_valid,
                                                                  static_cast<size_t>(m), rws, wb, Z, L, cnt);
     abmx_internal::count_launch();
     CKA(cudaGetLastError());
-    Cols A{};  // spawn: copy the row columns given
-    A.n = 0;
-    for (int c = 0; c < s->n_state; ++c) {
-        if (!rows || !rows[c].data) continue;
-        A.dst[A.n] = s->state[c].data;
-        A.src[A.n] = rows[c].data;
-        A.sz[A.n] = s->state[c].elem_size;
-        ++A.n;
-    }
     // the pair count is known only on the device: a grid-stride apply over at most 2 CTAs per SM
     // (a grid sized for min(n, m) pairs launched ~1200 CTAs for C2's ~14k births)
     const size_t pairs_max = n < static_cast<size_t>(m) ? n : static_cast<size_t>(m);
