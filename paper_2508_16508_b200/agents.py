@@ -260,7 +260,8 @@ class DeviceAgentSet:
 
     def lifecycle(self, kill, rows: dict, valid, agent_type=None):
         """remove_agents(kill) then spawn_agents(rows, valid) (lifecycle.cpp:124-195) in one
-        fused call (two kernels); returns (removed, spawned, dropped)."""
+        fused call (one cooperative kernel; two kernels for sets whose tiles do not fit on the GPU
+        at once); returns (removed, spawned, dropped)."""
         torch = _torch()
         k = self._mask(kill)
         v = torch.as_tensor(valid, device=self.device)

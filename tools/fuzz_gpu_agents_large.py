@@ -1,7 +1,7 @@
 """Time-boxed random campaign: device agent sets against the C restatement at sizes where the
 single-pass selections span many tiles (capacities up to 300,000): chained remove_agents +
-spawn_agents cycles (random densities, id recycling on / off, optional type) and the stable
-key sort.   python tools/fuzz_gpu_agents_large.py [seconds]"""
+spawn_agents cycles, half of them as the fused abmx_agents_lifecycle call (random densities, id
+recycling on / off, optional type) and the stable key sort.   python tools/fuzz_gpu_agents_large.py [seconds]"""
 import os
 import random
 import sys
@@ -22,7 +22,7 @@ o = pyoracle.Oracle()
 rng = random.Random(int(os.environ.get("SEED", "8")))
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 300
 t0 = time.time()
-nl = ns = 0
+nl = ns = nf = 0
 while time.time() - t0 < budget:
     g = np.random.default_rng(rng.getrandbits(32))
     cap = rng.randint(0, 300_000)
@@ -39,10 +39,15 @@ while time.time() - t0 < budget:
             valid = (g.random(m) < rng.choice([0.0, 0.05, 0.5, 1.0])).astype(np.uint8)
             set_type = rng.random() < 0.5
             st, wo = o.lifecycle(st, kill, rows, valid, set_type, cyc + 1)
-            killed = dev.remove(kill)
-            out = dev.spawn(rows, valid, agent_type=cyc + 1 if set_type else None)
-            assert killed == wo["killed"] and (out.spawned, out.dropped) == (wo["spawned"], wo["dropped"]), (cap, cyc)
-            assert np.array_equal(out.slots, wo["slots"]) and np.array_equal(out.rows, wo["rows"]), (cap, cyc)
+            if rng.random() < 0.5:  # the fused cycle (one cooperative kernel when the tiles fit)
+                killed, spawned, dropped = dev.lifecycle(kill, rows, valid, agent_type=cyc + 1 if set_type else None)
+                assert (killed, spawned, dropped) == (wo["killed"], wo["spawned"], wo["dropped"]), (cap, cyc)
+                nf += 1
+            else:
+                killed = dev.remove(kill)
+                out = dev.spawn(rows, valid, agent_type=cyc + 1 if set_type else None)
+                assert killed == wo["killed"] and (out.spawned, out.dropped) == (wo["spawned"], wo["dropped"]), (cap, cyc)
+                assert np.array_equal(out.slots, wo["slots"]) and np.array_equal(out.rows, wo["rows"]), (cap, cyc)
             ewf_equal(from_dev(dev, recycle), st, (cap, cyc))
         nl += 1
     else:
@@ -54,4 +59,4 @@ while time.time() - t0 < budget:
         key[act == 0] = -np.inf if desc else np.inf
         assert np.array_equal(A.sort_perm(key, act, descending=desc), o.sort_perm(key, act, descending=desc)), n
         ns += 1
-print("lifecycle sets", nl, "sorts", ns, "all bit-exact")
+print("lifecycle sets", nl, "(fused cycles", nf, ") sorts", ns, "all bit-exact")
