@@ -435,6 +435,9 @@ def agents_section(args, rank):
         ev[k][1].record()
     torch.cuda.synchronize()
     ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    w2, warr2, wkeep2 = make()
+    for k in range(3):  # warm-up of the two-call path too (its own scratch sizes, first launches)
+        cycle_two_calls(w2, warr2, K + k)
     s2, arr2, keep2 = make()  # the unfused two-call cycle on the same inputs, for comparison
     ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     for k in range(K):

@@ -147,9 +147,15 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __shared__ unsigned s_tile;
     __shared__ unsigned s_warp[NA / 32];
     __shared__ unsigned s_vin;
+    __shared__ unsigned long long s_key;
+    __shared__ int s_green;
     // tiles of one road depend on their right neighbours: ticket order guarantees progress
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
         s_tile = P.ctiles > 1 && !P.accept_ticketless ? atomicAdd(&P.ticket[P.epoch & 1], 1u) : blockIdx.x;
+        const int r0 = static_cast<int>(s_tile / P.ctiles);  // the road's light and propose key, once
+        s_green = green_of(P, r0);                            // per CTA (64-bit modulo, two splits)
+        s_key = propose_key(P, r0);
+    }
     __syncthreads();
     const unsigned g = s_tile;
     const int r = static_cast<int>(g / P.ctiles), tau = static_cast<int>(g % P.ctiles);
@@ -160,8 +166,8 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     }
     // tile 0 holds the road's last columns; columns L..Lp-1 are empty padding (-1)
     const int hi = P.Lp - tau * NA * kCI;
-    const bool green = green_of(P, r);
-    const unsigned long long key = propose_key(P, r);
+    const bool green = s_green != 0;
+    const unsigned long long key = s_key;
     const size_t cb = static_cast<size_t>(r) * P.Cpad;
     const int c_lo = hi - (static_cast<int>(threadIdx.x) + 1) * kCI;  // multiple of 4
     // occupants of this thread's 4 columns x 3 lanes (column c_lo + q)
@@ -325,8 +331,15 @@ __global__ void __launch_bounds__(NT) k_apply(TParams P) {
     __shared__ int s_first[3];
     __shared__ unsigned s_exit[NT / 32];
     const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
-    const bool green = green_of(P, r);
-    const unsigned long long key = propose_key(P, r);
+    __shared__ unsigned long long s_key;
+    __shared__ int s_green;
+    if (threadIdx.x == 0) {  // the road's light and propose key, once per CTA
+        s_green = green_of(P, r);
+        s_key = propose_key(P, r);
+    }
+    __syncthreads();
+    const bool green = s_green != 0;
+    const unsigned long long key = s_key;
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
     const int i0 = tile * NT * kS + threadIdx.x * kS;  // blocked: free-slot order = slot order
     unsigned exited = 0, nf = 0;
