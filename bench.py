@@ -607,11 +607,14 @@ def our_arm(args, rank, world, local_rank, dist):
     lw = float(met[0, :, 1].mean()) / C2["wolf_capacity"]
     atom_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 0, True)
     read_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 1, True)
-    access = {"unit": "us", "k_move_random_atomics_alone": atom_us, "k_move": avg["k_move"] * 1e3,
+    none_us, _ = abmx.diag_random_access(C2["width"] * C2["height"], n_tiles, n_tiles, ls, lw, 2, True)
+    access = {"unit": "us", "launch_shape_alone": none_us,
+              "k_move_random_atomics_alone": atom_us, "k_move": avg["k_move"] * 1e3,
               "k_update_random_reads_alone": read_us, "k_update": avg["k_update"] * 1e3,
               "note": "event-timed kernels doing ONLY the step's random cell-word atomicExch+atomicMax "
-                      "(k_move) / 16-byte reads (k_update), same grid and live fractions, L2 flushed; "
-                      "see profiles/r02_c2_cost_model.md"}
+                      "(k_move) / 16-byte reads (k_update) / nothing (launch shape and hashing), same "
+                      "grid and live fractions, L2 flushed clean; the random-access ceiling and the "
+                      "sum-of-floors accounting are in profiles/r02_c2_cost_model.md §6"}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "algorithmic_bytes": kb[dom], "avg_launch_ms": avg[dom],

@@ -208,8 +208,9 @@ _sig("abmx_diag_random_access", C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.c_d
 
 def diag_random_access(cells, sheep_ctas, wolf_ctas, live_sheep, live_wolves, mode=0, cold=True,
                        reps=10):
-    """Measured ceiling of the predation kernels' cell-word access pattern:
-    (min_us, mean_us) of a kernel doing only those random atomics (mode 0) / reads (mode 1)."""
+    """Measured cost of the predation kernels' cell-word access pattern:
+    (min_us, mean_us) of a kernel doing only those random atomics (mode 0) / 16-byte reads
+    (mode 1) / nothing but the launch shape and hashing (mode 2); cold = L2 flushed clean."""
     mn, me = C.c_double(), C.c_double()
     _check(lib.abmx_diag_random_access(cells, sheep_ctas, wolf_ctas, live_sheep, live_wolves, mode,
                                        int(cold), reps, C.byref(mn), C.byref(me)))

@@ -51,6 +51,10 @@ __global__ void __launch_bounds__(kT, 4) k_access(uint4* cw, unsigned cells, int
 #pragma unroll
         for (int k = 0; k < kS; ++k)
             if (act[k]) acc += old[k];
+    } else if (mode == 2) {  // no access: the launch shape, the hashing and the store only
+#pragma unroll
+        for (int k = 0; k < kS; ++k)
+            if (act[k]) acc += static_cast<int>(c[k]);
     } else {
         uint4 v[kS];
 #pragma unroll
@@ -67,6 +71,14 @@ __global__ void k_flush_d(uint4* p, size_t n, unsigned s) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<size_t>(gridDim.x) * blockDim.x)
         p[i] = make_uint4(s, static_cast<unsigned>(i), 0, 0);
+}
+// then read it back, so L2 holds clean lines (as bench.py's flush: no write-backs in the timed kernel)
+__global__ void k_flush_read_d(const uint4* p, size_t n, int* out) {
+    unsigned acc = 0;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        acc += p[i].x;
+    if (acc == 0x12345678u) *out = static_cast<int>(acc);
 }
 
 }  // namespace
@@ -96,9 +108,10 @@ extern "C" int abmx_diag_random_access(int64_t cells, int32_t sheep_ctas, int32_
         double best = 1e30, sum = 0.0;
         for (int r = 0; r < reps + 3; ++r) {
             const unsigned salt = cold ? 1000u + static_cast<unsigned>(r) : 77u;
-            if (cold)
+            if (cold) {
                 k_flush_d<<<abmx_internal::num_sms() * 4, 256>>>(fl, flush_n, static_cast<unsigned>(r));
-            else
+                k_flush_read_d<<<abmx_internal::num_sms() * 4, 256>>>(fl, flush_n, out);
+            } else
                 k_access<<<grid, kT>>>(cw, static_cast<unsigned>(cells), out, salt, mode, sheep_ctas, ls, lw);
             cudaEventRecord(a);
             k_access<<<grid, kT>>>(cw, static_cast<unsigned>(cells), out, salt, mode, sheep_ctas, ls, lw);
@@ -111,7 +124,7 @@ extern "C" int abmx_diag_random_access(int64_t cells, int32_t sheep_ctas, int32_
                 sum += ms;
             }
         }
-        abmx_internal::count_launch(2 * (reps + 3));
+        abmx_internal::count_launch((cold ? 3 : 2) * (reps + 3));
         if (cudaGetLastError() != cudaSuccess) {
             abmx_internal::set_error("diag: launch failed");
             rc = ABMX_E_CUDA;
