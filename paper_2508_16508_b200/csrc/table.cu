@@ -19,31 +19,7 @@ using namespace abmx_dev;
 namespace abmx_table {
 
 constexpr int kThreads = 256;
-constexpr int kItems = 16;  // mask bytes per thread
-constexpr int kTile = kThreads * kItems;
 constexpr int kCountItems = 64;
-
-template <int I>
-__device__ __forceinline__ void load_mask(const uint8_t* mask, size_t base, size_t n, bool vec_ok,
-                                          uint8_t (&b)[I]) {
-    if (vec_ok && base + I <= n) {
-#pragma unroll
-        for (int q = 0; q < I / 16; ++q) {
-            const uint4 v = *reinterpret_cast<const uint4*>(mask + base + 16 * q);
-            const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int k = 0; k < 16; ++k) b[16 * q + k] = static_cast<uint8_t>(w[k >> 2] >> (8 * (k & 3)));
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < I; ++k) b[k] = base + k < n ? mask[base + k] : 0;
-    }
-}
-
-__device__ __forceinline__ void load_mask16(const uint8_t* mask, size_t base, size_t n,
-                                            bool vec_ok, uint8_t (&b)[kItems]) {
-    load_mask<kItems>(mask, base, n, vec_ok, b);
-}
 
 // nonzero bytes of a word (SWAR): fold each byte's bits onto its bit 0, then popcount
 __device__ __forceinline__ unsigned nz_bytes(uint32_t w) {
@@ -675,7 +651,7 @@ __global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, co
 // ---------------------------------------------------------------- blends
 // Blend, lane-contiguous: a warp owns 32 * kV consecutive 16-byte vectors of a / b / out; at
 // step q lane l takes vector q * 32 + l (and the mask bytes of its elements), so every load and
-// store instruction covers 512 contiguous bytes. A lane owning kItems consecutive elements made
+// store instruction covers 512 contiguous bytes. A lane owning 16 consecutive elements made
 // each instruction touch 32 different lines: 420 us for 2^26 i64 against 236 us for torch.where.
 template <int B>
 struct MaskChunk;  // the mask bytes of one 16-byte vector of elements
