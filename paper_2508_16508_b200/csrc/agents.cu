@@ -352,6 +352,18 @@ __global__ void __launch_bounds__(kT) k_life_apply(const int32_t* __restrict__ s
 //           (every CTA read the old ones before barrier 1)
 // Two counter barriers replace the ticket + lookback of k_life_select and the last-CTA
 // handshake of k_life_apply.
+#ifdef ABMX_LIFE_TRACE  // per-CTA %globaltimer stamps: start, counted, barrier 1, written, barrier 2, end
+__device__ unsigned long long g_life_trace[4096][7];
+#define LIFE_STAMP(k)                                                          \
+    if (threadIdx.x == 0) {                                                    \
+        unsigned long long t_;                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+        if (blockIdx.x < 4096) g_life_trace[blockIdx.x][k] = t_;               \
+    }
+#else
+#define LIFE_STAMP(k)
+#endif
+
 struct LifeWs {
     unsigned arrived[2];        // CTAs past the count / the write phase (zeroed)
     unsigned long long tot[1];  // [G] kFlagAgg | pack2(killed, free) (slot tile) or pack2(0, valid)
@@ -377,6 +389,7 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     __shared__ unsigned long long s_v[5];
     const unsigned G = gridDim.x, b = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    LIFE_STAMP(0);
     const bool slot_tile = b < ta;
     const size_t base = static_cast<size_t>(slot_tile ? b : b - ta) * kTile + static_cast<size_t>(tid) * kItems;
     // the counters before the cycle (block 0 rewrites them after barrier 2)
@@ -401,7 +414,9 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(c1, c2), s_scan, &total);
     if (tid == 0) st_word(&ws->tot[b], kFlagAgg | total);
+    LIFE_STAMP(1);
     grid_barrier(&ws->arrived[0], G);
+    LIFE_STAMP(2);
     // ---- every tile total: this tile's prefix, K (killed), F (free), Q (valid)
     unsigned long long pk = 0, pf = 0, K = 0, F = 0, Q = 0;
     for (unsigned q = tid; q < G; q += kT) {
@@ -436,6 +451,7 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     F = s_v[3];
     Q = s_v[4];
     const long long r = static_cast<long long>(F < Q ? F : Q);
+    LIFE_STAMP(6);
     // ---- write
     long long kpos = static_cast<long long>(s_v[0]) + hi31(excl);  // killed before this thread
     long long fpos = static_cast<long long>(s_v[1]) + lo31(excl);  // free (or valid) before this thread
@@ -455,8 +471,10 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
             ++fpos;
         }
     }
-    __threadfence();  // this CTA's lists, resets and pushes, GPU-wide before barrier 2
+    // barrier 2 orders this CTA's list, resets and pushes: bar.sync, then thread 0's release
+    LIFE_STAMP(3);
     grid_barrier(&ws->arrived[1], G);
+    LIFE_STAMP(4);
     const long long top = top0 + (L.recycle ? static_cast<long long>(K) : 0);  // after the pushes
     if (b == 0 && tid == 0) {  // counters (lifecycle.cpp:136-141, 186-194)
         const long long used = top < r ? top : r;
@@ -469,16 +487,17 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
             out[1] = static_cast<long long>(Q) - r;
         }
     }
-    // ---- pair: the k-th free slot takes the k-th valid row
-    for (long long k = static_cast<long long>(b) * kT + tid; k < r; k += static_cast<long long>(G) * kT) {
-        const int slot = slots[k], row = rows[k];
+    // ---- pair: the k-th free slot takes the k-th valid row, one pair per thread over the grid
+    for (long long q = static_cast<long long>(b) * kT + tid; q < r; q += static_cast<long long>(G) * kT) {
+        const int slot = slots[q], row = rows[q];
         for (int c = 0; c < A.n; ++c)
             if (A.src[c]) copy_elem(A.dst[c], slot, A.src[c], row, A.sz[c]);
         L.active[slot] = 1;
-        L.ids[slot] = k < top ? L.retired[top - 1 - k] : nid + (k - top);
+        L.ids[slot] = q < top ? L.retired[top - 1 - q] : nid + (q - top);
         L.ages[slot] = 0;
         if (set_type) L.types[slot] = agent_type;
     }
+    LIFE_STAMP(5);
 }
 
 // set_agents_mask with per-slot source values: dst[c][i] <- src[c][i] where mask[i].
@@ -872,6 +891,12 @@ int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* 
     CKA(cudaGetLastError());
     return ABMX_OK;
 }
+
+#ifdef ABMX_LIFE_TRACE
+extern "C" int abmx_life_trace(unsigned long long* out, int ctas) {
+    return cudaMemcpyFromSymbol(out, abmx_agents::g_life_trace, sizeof(unsigned long long) * 7 * ctas) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_t m, const uint8_t* d_valid,
                           const abmx_column* rows, int32_t set_type, int64_t agent_type, int64_t* d_killed,
