@@ -417,6 +417,11 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
     SCAN_STAMP(3);
 }
 
+// Programmatic dependent launch: a kernel launched with programmatic stream serialization may
+// start while its predecessor drains; griddepcontrol.wait blocks until the predecessor has
+// completed and its memory is visible.
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // ---------------------------------------------------------------- match_first_equal
 // vmin / vmax live in an order-preserving unsigned form, both reduced with atomicMin (one pair
 // per CTA), so ONE cudaMemsetAsync(0xFF) initialises the workspace (capturable in a graph; no
@@ -507,6 +512,7 @@ __device__ __forceinline__ unsigned hash32(uint32_t k, unsigned bits) {
 // hash -> vals[0, H) and keys[0, H). Memsetting both full tables up front wrote 12*H bytes.
 __global__ void match_init_kernel(const MatchWs* ws, unsigned bits, int* __restrict__ vals,
                                   unsigned long long* __restrict__ keys) {
+    grid_dep_wait();  // launched early (PDL): the previous kernel's writes are visible after this
     const bool dense = dense_mode(ws, bits);
     const size_t H = size_t{1} << bits;
     const size_t nv = dense ? static_cast<size_t>(static_cast<long long>(ws_vmax(ws)) - ws_vmin(ws) + 1) : H;
@@ -525,6 +531,7 @@ __global__ void match_init_kernel(const MatchWs* ws, unsigned bits, int* __restr
 
 __global__ void match_build_kernel(const int32_t* __restrict__ rb, size_t m, const MatchWs* ws, unsigned bits,
                                    int* __restrict__ vals, unsigned long long* __restrict__ keys) {
+    grid_dep_wait();  // launched early (PDL): the previous kernel's writes are visible after this
     const bool dense = dense_mode(ws, bits);
     const unsigned mask = (1u << bits) - 1u;
     const int vmin = ws_vmin(ws);
@@ -641,6 +648,7 @@ __global__ void match_lookup_kernel(const int32_t* __restrict__ ra, size_t n, co
                                     const int* __restrict__ vals,
                                     const unsigned long long* __restrict__ keys,
                                     int32_t* __restrict__ row_out) {
+    grid_dep_wait();  // launched early (PDL): the build's table is visible after this
     const long long lo = ws_vmin(ws), hi = ws_vmax(ws);
     if (dense_mode(ws, bits))  // uniform: the dense loop compiles without the probing path
         match_lookup_body<true>(ra, n, bits, lo, hi, vals, keys, row_out);
@@ -812,11 +820,32 @@ cudaError_t launch_match_first_equal(const int32_t* d_ra, size_t n, const int32_
     const int gm = grid_for(m, 256 * 8), gn = grid_for(n, 256 * 8);
     (void)cudaGetLastError();
     minmax_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws);
-    match_init_kernel<<<num_sms() * 8, 256, 0, s>>>(mws, bits, vals, keys);
-    match_build_kernel<<<gm, 256, 0, s>>>(d_rb, m, mws, bits, vals, keys);
-    match_lookup_kernel<<<gn, 256, 0, s>>>(d_ra, n, mws, bits, vals, keys, d_out);
+    // init, build and lookup launch with programmatic stream serialization (each waits in-kernel
+    // for its predecessor), so their launch latency overlaps the predecessor's tail
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    auto cfg_of = [&](unsigned grid) {
+        cudaLaunchConfig_t c{};
+        c.gridDim = dim3(grid);
+        c.blockDim = dim3(256);
+        c.stream = s;
+        c.attrs = pdl;
+        c.numAttrs = 1;
+        return c;
+    };
+    cudaLaunchConfig_t c1 = cfg_of(static_cast<unsigned>(num_sms() * 8)), c2 = cfg_of(static_cast<unsigned>(gm)),
+                       c3 = cfg_of(static_cast<unsigned>(gn));
+    e = cudaLaunchKernelEx(&c1, match_init_kernel, static_cast<const MatchWs*>(mws), bits, vals, keys);
+    if (e == cudaSuccess)
+        e = cudaLaunchKernelEx(&c2, match_build_kernel, static_cast<const int32_t*>(d_rb), m,
+                               static_cast<const MatchWs*>(mws), bits, vals, keys);
+    if (e == cudaSuccess)
+        e = cudaLaunchKernelEx(&c3, match_lookup_kernel, static_cast<const int32_t*>(d_ra), n,
+                               static_cast<const MatchWs*>(mws), bits, static_cast<const int*>(vals),
+                               static_cast<const unsigned long long*>(keys), d_out);
     count_launch(4);
-    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(ws, s);
     return e;
 }
