@@ -471,6 +471,16 @@ __device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, i
 
 __global__ void k_spawn(TParams P) { spawn_road(P, blockIdx.x, P.t, P.run_step, threadIdx.x); }
 
+// the bench's L2 flush: after the memset of a buffer larger than L2, read it back so L2 holds
+// clean lines (as the predation bench): the timed step pays no write-backs of the flush buffer
+__global__ void k_flush_read_t(const uint4* p, size_t n, unsigned* sink) {
+    unsigned a = 0;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        a += p[i].x;
+    if (a == 0x12345678u) *sink = a;
+}
+
 // ---------------------------------------------------------------- resolve_conflicts (explicit)
 // General proposals (any in-road target): acceptance is the least fixed point of
 // acc(w) = winner(w) && (target empty || acc(occupant)), solved by pointer jumping;
@@ -714,15 +724,13 @@ struct abmx_traffic {
     int build_graph2() {
         CKT(cudaGraphCreate(&graph2, 0));
         void* args[1] = {&P};
-        cudaGraphNode_t prev = nullptr;
         for (int k = 0; k < 2; ++k) {
             cudaKernelNodeParams kp{};
             kp.func = fn(k);
             kp.gridDim = dim3(grid(k));
             kp.blockDim = dim3(block(k));
             kp.kernelParams = args;
-            CKT(cudaGraphAddKernelNode(&nodes2[k], graph2, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
-            prev = nodes2[k];
+            CKT(cudaGraphAddKernelNode(&nodes2[k], graph2, k ? &nodes2[k - 1] : nullptr, k ? 1 : 0, &kp));
         }
         CKT(cudaGraphInstantiate(&exec2, graph2, 0));
         return ABMX_OK;
@@ -768,15 +776,13 @@ struct abmx_traffic {
     int build_graph() {
         CKT(cudaGraphCreate(&graph, 0));
         void* args[1] = {&P};
-        cudaGraphNode_t prev = nullptr;
         for (int k = 0; k < kNumKernels; ++k) {
             cudaKernelNodeParams kp{};
             kp.func = fn(k);
             kp.gridDim = dim3(grid(k));
             kp.blockDim = dim3(block(k));
             kp.kernelParams = args;
-            CKT(cudaGraphAddKernelNode(&nodes[k], graph, prev ? &prev : nullptr, prev ? 1 : 0, &kp));
-            prev = nodes[k];
+            CKT(cudaGraphAddKernelNode(&nodes[k], graph, k ? &nodes[k - 1] : nullptr, k ? 1 : 0, &kp));
         }
         CKT(cudaGraphInstantiate(&exec, graph, 0));
         return ABMX_OK;
@@ -962,7 +968,11 @@ struct abmx_traffic {
         for (auto& e : ev) CKT(cudaEventCreate(&e));
         (void)cudaGetLastError();
         for (long long q = 0; q < steps; ++q) {
-            if (flush_bytes) CKT(cudaMemsetAsync(flush_buf, static_cast<int>(q & 0xFF), flush_bytes, stream));
+            if (flush_bytes) {
+                CKT(cudaMemsetAsync(flush_buf, static_cast<int>(q & 0xFF), flush_bytes, stream));
+                k_flush_read_t<<<abmx_internal::num_sms() * 4, 256, 0, stream>>>(
+                    static_cast<const uint4*>(flush_buf), flush_bytes / 16, reinterpret_cast<unsigned*>(flush_buf));
+            }
             cudaEvent_t* e = &ev[per * static_cast<size_t>(q)];
             if (per_kernel) {
                 rc = enqueue(e);
