@@ -57,8 +57,17 @@ __global__ void __launch_bounds__(kThreads) count_true_kernel(const uint8_t* __r
     if (threadIdx.x < 32) {
         unsigned long long v = threadIdx.x < kThreads / 32 ? s[threadIdx.x] : 0ULL;
         v = warp_sum(v);
+        // launched with programmatic serialization after the zeroing of *out: wait for it only here
+        asm volatile("griddepcontrol.wait;" ::: "memory");
         if (threadIdx.x == 0 && v) atomicAdd(out, v);
     }
+}
+
+// zero n words (a kernel, not a memset node, so that the next kernel can launch programmatically)
+__global__ void zero_words_kernel(unsigned long long* p, size_t n) {
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x)
+        p[i] = 0ULL;
 }
 
 // ---------------------------------------------------------------- persistent pipelined scan
@@ -787,12 +796,25 @@ cudaError_t launch_rank_scan(const uint8_t* d_mask, int32_t* d_ranks, size_t n, 
 
 cudaError_t launch_count_true(const uint8_t* d_mask, size_t n, unsigned long long* d_out,
                               cudaStream_t s) {
-    cudaMemsetAsync(d_out, 0, sizeof(unsigned long long), s);
-    if (n == 0) return cudaGetLastError();
     (void)cudaGetLastError();
-    count_true_kernel<<<grid_for(n, kThreads * kCountItems), kThreads, 0, s>>>(d_mask, n, d_out);
-    count_launch();
-    return cudaGetLastError();
+    zero_words_kernel<<<1, 32, 0, s>>>(d_out, 1);
+    if (n == 0) {
+        count_launch();
+        return cudaGetLastError();
+    }
+    // the count streams the mask while the zeroing runs; it waits for it only before its atomic
+    cudaLaunchAttribute pdl[1];
+    pdl[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t c{};
+    c.gridDim = dim3(static_cast<unsigned>(grid_for(n, kThreads * kCountItems)));
+    c.blockDim = dim3(kThreads);
+    c.stream = s;
+    c.attrs = pdl;
+    c.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&c, count_true_kernel, d_mask, n, d_out);
+    count_launch(2);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_compact_indices(const uint8_t* d_mask, int32_t* d_out, size_t n,
