@@ -90,6 +90,17 @@ constexpr unsigned kDxTable = move_table(kMoveDx), kDyTable = move_table(kMoveDy
 __device__ __forceinline__ int move_dx(int u) { return static_cast<int>((kDxTable >> (2 * u)) & 3u) - 1; }
 __device__ __forceinline__ int move_dy(int u) { return static_cast<int>((kDyTable >> (2 * u)) & 3u) - 1; }
 
+// Device asserts of checked builds (-DABMX_CHECKED; compute-sanitizer is closed on the GPU pool):
+// a failed condition traps, so the launch fails with an error the caller sees. No code otherwise.
+#ifdef ABMX_CHECKED
+#define ABMX_ASSERT(cond) \
+    do {                  \
+        if (!(cond)) __trap(); \
+    } while (0)
+#else
+#define ABMX_ASSERT(cond) ((void)0)
+#endif
+
 // Warp-inclusive scan of packed u64 values (fields never overflow by construction).
 __device__ __forceinline__ unsigned long long warp_incl_scan(unsigned long long v) {
     const int lane = threadIdx.x & 31;

@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 nx = nx < 0 ? nx + P.W : (nx >= P.W ? nx - P.W : nx);
                 ny = ny < 0 ? ny + P.H : (ny >= P.H ? ny - P.H : ny);
                 const int nc = ny * P.W + nx;
+                ABMX_ASSERT(nc >= 0 && nc < P.C && i < P.N[s]);
                 cell[s][k] = nc;
                 unsigned old = cw[nc];
                 for (;;) {
@@ -262,7 +263,10 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                     const bool ready = s == 0 && grass_ready(g[c], t);
                     int rank = 0;  // slots of this species in the cell below i
                     if (ready || other != kEnd)
-                        for (unsigned v = own; v != kEnd; v = nxt[2 * v + s]) rank += v < static_cast<unsigned>(i);
+                        for (unsigned v = own; v != kEnd; v = nxt[2 * v + s]) {
+                        ABMX_ASSERT(v < static_cast<unsigned>(P.N[s]));
+                        rank += v < static_cast<unsigned>(i);
+                    }
                     if (ready && rank == 0) {  // the lowest sheep grazes
                         if (P.delay >= 1) {  // ready again at the end of step t + delay - 1
                             const unsigned due = static_cast<unsigned>(t + P.delay - 1) & 0x7FFFu;
@@ -313,6 +317,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 if (moved & bit(s, k)) cw[cell[s][k]] = 0xFFFFFFFFu;
                 if (validb & bit(s, k)) {
                     const unsigned v = run[s][1]++;
+                    ABMX_ASSERT(v < static_cast<unsigned>(P.N[s]));
                     rows[s * P.stride + v].e = child[s][k];
                     rows[s * P.stride + v].c = static_cast<unsigned>(cell[s][k]);
                 }
@@ -336,6 +341,7 @@ __global__ void __launch_bounds__(kT, SPT <= 2 ? 3 : 1) k_ensemble(EnsParams P) 
                 const int f = static_cast<int>(run[s][0]++);
                 if (f < pairs[s]) {
                     const int i = tid * SPT + k;
+                    ABMX_ASSERT(f < P.N[s] && i < P.N[s] && rows[s * P.stride + f].c < static_cast<unsigned>(P.C));
                     act |= bit(s, k);
                     cell[s][k] = static_cast<int>(rows[s * P.stride + f].c);
                     E[s][k] = rows[s * P.stride + f].e;

@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
     constexpr int kP1 = pipe_smem<kCompact>() / kPTile;
     static_assert(kP1 <= kP1Max && kP1 >= kPIn, "pass-1 ring");
     auto load = [&](int t, int s, unsigned long long policy) {  // one thread: tile t into ring slot s
+        ABMX_ASSERT(t >= 0 && t < tiles && s >= 0 && s < kP1);
         if (is_bulk(t)) {
             mbar_expect_tx(&S.bar[s], kPTile);
             bulk_g2s_hint(in + s * kPTile, mask + static_cast<size_t>(t) * kPTile, kPTile, &S.bar[s], policy);
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
         const int tile = S.jt[s];
         if (tile < 0) break;  // the counter ran out (uniform)
         const unsigned long long run = S.jb[s];
+        ABMX_ASSERT(tile < tiles && run <= n);
         const size_t tb = static_cast<size_t>(tile) * kPTile;
         const int tn = static_cast<int>(n - tb < static_cast<size_t>(kPTile) ? n - tb : kPTile);
         if (!kCompact && tid == 0) bulk_wait_read<kPOut - 1>();  // the output stage we reuse is free
@@ -393,6 +395,7 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int e = e0 + k;
+                    ABMX_ASSERT(at + x < kPTile + 16 && fb + e - x < kPTile + 16 && fb + e - x >= 0);
                     if (((wd[r] >> (8 * k)) & 0xFFu) != 0u)
                         ob[at + x++] = static_cast<int32_t>(tb + e);
                     else
