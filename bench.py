@@ -591,11 +591,13 @@ def our_arm(args, rank, world, local_rank, dist):
     dom = max(avg, key=avg.get)
     peak, peak_src = hbm_peak()
     achieved = kb[dom] / (avg[dom] / 1e3) / 1e9
-    traffic = None
+    traffic, in_step = None, None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            tj = json.load(open(tpath))
+            traffic = tj.get(dom)
+            in_step = tj.get("_in_step")
         except Exception:
             traffic = None
     step_bytes = 42 * capacity(C2) + 2 * C2["width"] * C2["height"] + 8 * bd
@@ -621,7 +623,9 @@ def our_arm(args, rank, world, local_rank, dist):
                 "kernel_share": avg[dom] / step_sum,
                 "per_kernel_ms": avg,
                 "step_effective_gbs": step_bytes / (total_ms / K / 1e3) / 1e9,
-                "random_access_cost": access}
+                "random_access_cost": access,
+                "step_dram_bytes_in_step": in_step.get("step_dram_bytes") if in_step else None,
+                "step_algorithmic_bytes": kb["k_move"] + kb["k_update"]}
 
     # warm back-to-back figure beside the flushed headline: run() of K steps, no flush between
     stream = torch.cuda.ExternalStream(model.stream)
