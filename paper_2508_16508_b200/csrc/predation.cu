@@ -863,12 +863,17 @@ __global__ void __launch_bounds__(kT) k_book(Params P) {
             long long* h = P.host_row + static_cast<size_t>(r) * 4;
             for (int q = 0; q < 4; ++q) h[q] = row[q];
             // publish: the last of the R rows of this call bumps the mapped sequence word, so
-            // the host can poll it instead of waiting for the stream to drain
+            // the host can poll it instead of waiting for the stream to drain. One replica is
+            // its own last row: one system fence, no counter round trip.
             __threadfence_system();
-            const unsigned long long done = atomicAdd(P.book_count, 1ULL) + 1ULL;
-            if (done == P.book_seq * static_cast<unsigned long long>(P.R)) {
-                __threadfence_system();
+            if (P.R == 1) {
                 *reinterpret_cast<volatile long long*>(P.host_seq) = static_cast<long long>(P.book_seq);
+            } else {
+                const unsigned long long done = atomicAdd(P.book_count, 1ULL) + 1ULL;
+                if (done == P.book_seq * static_cast<unsigned long long>(P.R)) {
+                    __threadfence_system();
+                    *reinterpret_cast<volatile long long*>(P.host_seq) = static_cast<long long>(P.book_seq);
+                }
             }
         }
     }
