@@ -842,38 +842,82 @@ __global__ void __launch_bounds__(kT, kMinB) k_update(Params P) { update_phase(P
 // births_dropped column (both species) written directly, then the finished metrics row goes
 // straight to mapped host memory (collect_metrics needs no copy).
 __global__ void __launch_bounds__(kT) k_book(Params P) {
-    __shared__ unsigned long long s_red[kT / 32];
+    // book_step for both species (its bookkeeping, inlined), with every input thread 0 needs from
+    // the step's kernels loaded first and both species' tile totals in one round of loads and one
+    // reduction: k_book sits on the per-call step's critical path, before the host sees the row
+    __shared__ unsigned long long s_red[2][kT / 32];
     const int r = blockIdx.x;
-    long long dropped = 0;
+    const int pb = static_cast<int>(P.birth_epoch & 1);
+    Events* ev = P.ev + static_cast<size_t>(pb) * P.R + r;
+    unsigned* due = &P.due_count[static_cast<size_t>(r) * P.due_ring + P.birth_epoch % P.due_ring];
+    long long nid[2] = {0, 0}, ng0 = 0;
+    unsigned long long eaten = 0;
+    unsigned duev = 0;
+    if (threadIdx.x == 0) {
+        nid[0] = P.rep[static_cast<size_t>(r) * 2].next_id[pb];
+        nid[1] = P.rep[static_cast<size_t>(r) * 2 + 1].next_id[pb];
+        ng0 = P.n_grass[r];
+        eaten = ev->grass_eaten;
+        duev = *due;
+    }
+    unsigned long long v[2] = {0, 0};
+#pragma unroll
     for (int s = 0; s < 2; ++s) {
         const unsigned long long* tc = P.status + (static_cast<size_t>(s) * P.R + r) * P.status_stride;
-        unsigned long long v = 0;
-        for (int t = threadIdx.x; t < P.tiles[s]; t += kT) v += tc[t];
-        const unsigned long long tot = block_sum<unsigned long long>(v, s_red);
-        if (threadIdx.x == 0) {
-            const int F = static_cast<int>(hi31(tot)), Q = static_cast<int>(lo31(tot));
-            book_step(P, s, r, F, Q, false);
-            dropped += Q - (F < Q ? F : Q);
-        }
+        for (int t = threadIdx.x; t < P.tiles[s]; t += kT) v[s] += tc[t];
     }
-    if (threadIdx.x == 0) {
-        long long* row = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
-        row[3] = dropped;
-        if (P.host_row) {
-            long long* h = P.host_row + static_cast<size_t>(r) * 4;
-            for (int q = 0; q < 4; ++q) h[q] = row[q];
-            // publish: the last of the R rows of this call bumps the mapped sequence word, so
-            // the host can poll it instead of waiting for the stream to drain. One replica is
-            // its own last row: one system fence, no counter round trip.
-            __threadfence_system();
-            if (P.R == 1) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s)
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) v[s] += __shfl_xor_sync(0xffffffffu, v[s], d);
+    if ((threadIdx.x & 31) == 0) {
+        s_red[0][threadIdx.x >> 5] = v[0];
+        s_red[1][threadIdx.x >> 5] = v[1];
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    long long row[4];
+    long long dropped = 0;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {  // book_step (above) for species s
+        unsigned long long tot = 0;
+        for (int w = 0; w < kT / 32; ++w) tot += s_red[s][w];
+        const int F = static_cast<int>(hi31(tot)), Q = static_cast<int>(lo31(tot));
+        const int N = P.N[s];
+        const int pairs = F < Q ? F : Q;
+        SpeciesRep* sr = &P.rep[static_cast<size_t>(r) * 2 + s];
+        sr->next_id[pb ^ 1] = nid[s] + pairs;
+        sr->num_active[pb ^ 1] = N - F + pairs;
+        sr->pairs = pairs;
+        sr->Q = Q;
+        atomicAdd(&ev->births[s], static_cast<unsigned long long>(pairs));
+        atomicAdd(&ev->dropped[s], static_cast<unsigned long long>(Q - pairs));
+        row[s] = N - F + pairs;
+        dropped += Q - pairs;
+    }
+    const long long ng = ng0 - static_cast<long long>(eaten) + duev;  // ready cells after the lazy regrow
+    *due = 0;
+    P.n_grass[r] = ng;
+    row[2] = ng;
+    row[3] = dropped;
+    long long* mrow = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + P.birth_row) * 4;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) mrow[q] = row[q];
+    if (P.host_row) {
+        long long* h = P.host_row + static_cast<size_t>(r) * 4;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) h[q] = row[q];
+        // publish: the last of the R rows of this call bumps the mapped sequence word, so
+        // the host can poll it instead of waiting for the stream to drain. One replica is
+        // its own last row: one system fence, no counter round trip.
+        __threadfence_system();
+        if (P.R == 1) {
+            *reinterpret_cast<volatile long long*>(P.host_seq) = static_cast<long long>(P.book_seq);
+        } else {
+            const unsigned long long done = atomicAdd(P.book_count, 1ULL) + 1ULL;
+            if (done == P.book_seq * static_cast<unsigned long long>(P.R)) {
+                __threadfence_system();
                 *reinterpret_cast<volatile long long*>(P.host_seq) = static_cast<long long>(P.book_seq);
-            } else {
-                const unsigned long long done = atomicAdd(P.book_count, 1ULL) + 1ULL;
-                if (done == P.book_seq * static_cast<unsigned long long>(P.R)) {
-                    __threadfence_system();
-                    *reinterpret_cast<volatile long long*>(P.host_seq) = static_cast<long long>(P.book_seq);
-                }
             }
         }
     }
