@@ -939,17 +939,22 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
         ++A.n;
     }
     const Life L = life_of(s);
-    static int coop_per_sm[abmx_internal::kMaxDevices] = {};  // co-resident k_life_coop CTAs per SM
+    // co-resident k_life_coop CTAs per SM, per device (computed once; racing writers store the
+    // same value)
+    static std::atomic<int> coop_per_sm[abmx_internal::kMaxDevices] = {};
     int dev = 0;
     CKA(cudaGetDevice(&dev));
-    if (dev >= 0 && dev < abmx_internal::kMaxDevices && coop_per_sm[dev] == 0) {
-        int per = 0;
-        CKA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_life_coop, kT, 0));
-        coop_per_sm[dev] = per > 0 ? per : -1;
+    int per_sm = 0;
+    if (dev >= 0 && dev < abmx_internal::kMaxDevices) {
+        per_sm = coop_per_sm[dev].load(std::memory_order_relaxed);
+        if (per_sm == 0) {
+            int per = 0;
+            CKA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_life_coop, kT, 0));
+            per_sm = per > 0 ? per : -1;
+            coop_per_sm[dev].store(per_sm, std::memory_order_relaxed);
+        }
     }
-    const long long coop_cap = dev >= 0 && dev < abmx_internal::kMaxDevices && coop_per_sm[dev] > 0
-                                   ? static_cast<long long>(coop_per_sm[dev]) * abmx_internal::num_sms()
-                                   : 0;
+    const long long coop_cap = per_sm > 0 ? static_cast<long long>(per_sm) * abmx_internal::num_sms() : 0;
     if (static_cast<long long>(ta + tb) <= coop_cap) {  // one cooperative kernel
         const size_t ws_b = (sizeof(LifeWs) + (ta + tb) * sizeof(unsigned long long) + 15) / 16 * 16;
         void* ws = nullptr;
