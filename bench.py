@@ -10,17 +10,23 @@ scaling, no data-path collective; the per-rank summary rows are gathered with NC
 The line also carries the C3 ensemble (4096 x C1 replicas, sharded over the ranks).
 
   value      capacity slot-steps/s over all ranks, device-timed (CUDA events per step,
-             L2 flushed by an untimed 256 MiB write before every timed step), max over ranks
+             L2 flushed before every timed step: an untimed 256 MiB write, then a 256 MiB read
+             so L2 holds clean lines), max over ranks
   e2e        the same metric through the C-ABI call a user makes: abmx_predation_step(t)
              (H2D of t) + abmx_predation_metrics (D2H of the metrics row), host wall clock
   roofline   dominant kernel: SURVEY §8d algorithmic bytes apportioned to that kernel
-             / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs
+             / its CUDA-event duration, against MEASURED_PEAKS.json hbm_gbs; plus
+             random_access_cost: the step's random cell-word atomics / reads alone and the
+             bare launch shape, event-timed (the bound; profiles/r02_c2_cost_model.md), and
+             step_dram_bytes_in_step: one ncu range over k_move + k_update (profiles/)
   cpu_baseline  the reference's own C++ step_predation (oracle/_ref, -O3) on this host
   ensemble / traffic / finance   secondary sections: device times of
              the C3 ensemble, the C4 road and roads variant, the C5 markets (and the one-market
              reading), each with the reference's own CPU run on a bounded sample
   agents     the generic lifecycle (remove_agents + spawn_agents) on a
              C2-sized set, bit-compared with the reference's own remove/spawn on the same inputs
+  kernel_table  the KernelTable device entries (rank_scan, count_true, compact_indices,
+             match_first_equal, blend_i64) on 2^26 elements, L2 flushed, event-timed
 
 `--impl reference` times the reference CPU implementation (oracle/_ref) on the same workload.
 """
