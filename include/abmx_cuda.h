@@ -270,8 +270,9 @@ int abmx_agents_spawn(const abmx_agent_set* s, int32_t m, const uint8_t* d_valid
                       const abmx_column* rows, int32_t set_type, int64_t agent_type,
                       int32_t* d_slots, int32_t* d_rows, int64_t* d_result, void* stream);
 /* One lifecycle cycle: remove_agents(kill) then spawn_agents(rows, valid) (lifecycle.cpp:124-195)
- * fused: one cooperative kernel (count, barrier, removal in place + selection lists, barrier,
- * pairing apply) when the set's tiles fit on the GPU at once, else two kernels (one selection
+ * fused: one cooperative kernel with one grid barrier (count + tile-local free/killed-id lists,
+ * barrier, removal in place + rows placed into their free slots) when the set's tiles fit on the
+ * GPU at once, else two kernels (one selection
  * pass with the removal applied in place, one pairing apply); results identical to
  * abmx_agents_remove followed by abmx_agents_spawn. d_killed (nullable, device int64) = removed;
  * d_result (nullable, device int64[2]) = {spawned, dropped}. */

@@ -47,13 +47,30 @@ struct ScanWs {
     unsigned long long status[1];  // [tiles]
 };
 
-__device__ __forceinline__ void copy_elem(void* dst, long long i, const void* src, long long j, int sz) {
+__device__ __forceinline__ unsigned long long load_elem(const void* src, long long j, int sz) {
+    if (sz == 8) return static_cast<const unsigned long long*>(src)[j];
+    if (sz == 4) return static_cast<const unsigned*>(src)[j];
+    return static_cast<const uint8_t*>(src)[j];
+}
+__device__ __forceinline__ void store_elem(void* dst, long long i, unsigned long long v, int sz) {
     if (sz == 8)
-        static_cast<unsigned long long*>(dst)[i] = static_cast<const unsigned long long*>(src)[j];
+        static_cast<unsigned long long*>(dst)[i] = v;
     else if (sz == 4)
-        static_cast<unsigned*>(dst)[i] = static_cast<const unsigned*>(src)[j];
+        static_cast<unsigned*>(dst)[i] = static_cast<unsigned>(v);
     else
-        static_cast<uint8_t*>(dst)[i] = static_cast<const uint8_t*>(src)[j];
+        static_cast<uint8_t*>(dst)[i] = static_cast<uint8_t>(v);
+}
+// dst[c][slot] <- src[c][row] for every column with a source: all loads issued before the first
+// store (a store may alias a later column's source as far as the compiler knows, so the plain
+// per-column copy serialises one random DRAM round trip per column)
+__device__ __forceinline__ void copy_cols(const Cols& C, long long slot, long long row) {
+    unsigned long long v[kMaxCols];
+#pragma unroll
+    for (int c = 0; c < kMaxCols; ++c)
+        if (c < C.n && C.src[c]) v[c] = load_elem(C.src[c], row, C.sz[c]);
+#pragma unroll
+    for (int c = 0; c < kMaxCols; ++c)
+        if (c < C.n && C.src[c]) store_elem(C.dst[c], slot, v[c], C.sz[c]);
 }
 __device__ __forceinline__ void zero_elem(void* dst, long long i, int sz) {
     if (sz == 8)
@@ -196,8 +213,7 @@ __global__ void __launch_bounds__(kT) k_pair_apply(const int32_t* __restrict__ s
     for (long long k = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; k < r;
          k += static_cast<long long>(gridDim.x) * kT) {
         const int slot = slots[k], row = rows[k];
-        for (int c = 0; c < C.n; ++c)
-            if (C.src[c]) copy_elem(C.dst[c], slot, C.src[c], row, C.sz[c]);
+        copy_cols(C, slot, row);
         if (spawn) {
             L.active[slot] = 1;
             L.ids[slot] = k < top ? L.retired[top - 1 - k] : nid + (k - top);
@@ -322,8 +338,7 @@ __global__ void __launch_bounds__(kT) k_life_apply(const int32_t* __restrict__ s
     for (long long k = static_cast<long long>(blockIdx.x) * kT + threadIdx.x; k < r;
          k += static_cast<long long>(gridDim.x) * kT) {
         const int slot = slots[k], row = rows[k];
-        for (int c = 0; c < C.n; ++c)
-            if (C.src[c]) copy_elem(C.dst[c], slot, C.src[c], row, C.sz[c]);
+        copy_cols(C, slot, row);
         L.active[slot] = 1;
         L.ids[slot] = k < top ? L.retired[top - 1 - k] : nid + (k - top);
         L.ages[slot] = 0;
@@ -342,18 +357,26 @@ __global__ void __launch_bounds__(kT) k_life_apply(const int32_t* __restrict__ s
     }
 }
 
-// The same cycle as ONE cooperative kernel when every tile CTA is co-resident (k_life_coop):
-//   count   each CTA (one slot or row tile) counts (killed, free) or valid, publishes the total and
-//           arrives at barrier 1 (a release increment; thread 0 alone polls the counter)
-//   write   every CTA reads all tile totals (its prefix, K, F, Q): slot tiles reset their killed
-//           slots (ids pushed at top + killed prefix, slot order) and list their free slots of
-//           rank < r = min(F, Q); row tiles list their valid rows of rank < r; barrier 2
-//   pair    pairs k < r over the whole grid; block 0 commits the counters after barrier 2
-//           (every CTA read the old ones before barrier 1)
-// Two counter barriers replace the ticket + lookback of k_life_select and the last-CTA
-// handshake of k_life_apply.
-#ifdef ABMX_LIFE_TRACE  // per-CTA %globaltimer stamps: start, counted, barrier 1, written, barrier 2, end
-__device__ unsigned long long g_life_trace[4096][7];
+// The same cycle as ONE cooperative kernel with ONE grid barrier, when every tile CTA is
+// co-resident (k_life_coop):
+//   count   each CTA (one slot or row tile) counts (killed, free) or valid; a slot tile also
+//           writes its tile-local lists (free slots by local rank, and the ids of its killed
+//           slots by local kill rank), which need no global information; every CTA publishes
+//           its totals and arrives at the barrier (a release increment; thread 0 alone polls)
+//   resolve every CTA scans all tile totals into shared memory: K (killed), F (free), Q (valid),
+//           r = min(F, Q), its own prefix, and the per-slot-tile prefixes that map a global free
+//           rank (or kill rank) to (tile, local rank) by binary search
+//   write   slot tiles push their killed ids (retired[top + kill rank]) and reset their killed
+//           slots; a killed slot of free rank < r is refilled this cycle, so only the state
+//           columns the spawn does not write are zeroed there. Row tiles place their valid rows
+//           of rank q < r directly: the q-th free slot from the tile lists, the id popped LIFO
+//           (an id pushed this cycle comes from the killed-id lists, not from retired[], which
+//           another CTA may still be writing). The reset and the placement write disjoint words.
+// Block 0 commits the counters after the barrier (every CTA read the old ones before it).
+// One counter barrier replaces the ticket + lookback of k_life_select, the last-CTA handshake of
+// k_life_apply, and the second barrier + slot/row pair lists of the previous two-barrier kernel.
+#ifdef ABMX_LIFE_TRACE  // per-CTA %globaltimer stamps: start, counted, barrier, written, -, end, resolved
+__device__ unsigned long long g_life_trace[4096][8];
 #define LIFE_STAMP(k)                                                          \
     if (threadIdx.x == 0) {                                                    \
         unsigned long long t_;                                                 \
@@ -364,9 +387,12 @@ __device__ unsigned long long g_life_trace[4096][7];
 #define LIFE_STAMP(k)
 #endif
 
+constexpr int kCoopMaxTiles = 2048;  // slot + row tiles of one k_life_coop grid (shared prefix array)
+
 struct LifeWs {
-    unsigned arrived[2];        // CTAs past the count / the write phase (zeroed)
-    unsigned long long tot[1];  // [G] kFlagAgg | pack2(killed, free) (slot tile) or pack2(0, valid)
+    unsigned arrived;           // CTAs past the count phase (zeroed before the launch)
+    unsigned pad;
+    unsigned long long tot[1];  // [G] pack2(killed, free) (slot tile) or pack2(0, valid) (row tile)
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned G) {
@@ -379,24 +405,50 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned G) {
     __syncthreads();
 }
 
+// largest t in [0, cnt) with field(pref[t]) <= q: the tile holding global rank q (empty tiles
+// share their successor's prefix and are skipped by taking the last such t)
+template <bool kHi>
+__device__ __forceinline__ unsigned tile_of_rank(const unsigned long long* pref, unsigned cnt, unsigned long long q) {
+    unsigned lo = 0, hi = cnt;  // answer in [lo, hi)
+    while (hi - lo > 1) {
+        const unsigned mid = (lo + hi) >> 1;
+        const unsigned v = kHi ? hi31(pref[mid]) : lo31(pref[mid]);
+        if (v <= q)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
 __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ kill, size_t n, unsigned ta,
                                                   const uint8_t* __restrict__ valid, size_t m,
-                                                  int32_t* __restrict__ slots, int32_t* __restrict__ rows, LifeWs* ws,
-                                                  Cols Z, Cols A, Life L, int set_type, long long agent_type,
-                                                  long long* out_killed, long long* out) {
+                                                  int32_t* __restrict__ free_list, long long* __restrict__ kill_ids,
+                                                  LifeWs* ws, Cols Z, unsigned z_refill, Cols A, Life L, int set_type,
+                                                  long long agent_type, long long* out_killed, long long* out) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
-    __shared__ unsigned long long s_red[kT / 32][5];
-    __shared__ unsigned long long s_v[5];
+    __shared__ unsigned long long s_pref[kCoopMaxTiles + 1];  // exclusive tile prefixes, [G] = total
+    __shared__ long long s_cnt[3];
+    __shared__ int32_t s_rows[kTile];  // row tile: its valid rows, by local rank
     const unsigned G = gridDim.x, b = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     LIFE_STAMP(0);
     const bool slot_tile = b < ta;
-    const size_t base = static_cast<size_t>(slot_tile ? b : b - ta) * kTile + static_cast<size_t>(tid) * kItems;
-    // the counters before the cycle (block 0 rewrites them after barrier 2)
-    const long long live0 = L.counters[0], nid = L.counters[1];
-    const long long top0 = L.recycle ? L.counters[2] : 0;
+    const size_t tile_base = static_cast<size_t>(slot_tile ? b : b - ta) * kTile;
+    const size_t base = tile_base + static_cast<size_t>(tid) * kItems;
+    // the counters before the cycle (block 0 rewrites them after the barrier), read into shared
+    // memory at kernel start: left in registers, the compiler sank the loads past the barrier,
+    // a cold DRAM round trip on the critical path
+    if (tid == 0) {
+        s_cnt[0] = L.counters[0];
+        s_cnt[1] = L.counters[1];
+        s_cnt[2] = L.recycle ? L.counters[2] : 0;
+    }
     // ---- count
-    bool s1[kItems], s2[kItems];  // slot tile: killed, free once removed; row tile: -, valid
+    // bit k of m1 / m2: slot tile: killed / free once removed; row tile: - / valid. Bit masks
+    // keep the per-slot flags in two registers, so the loops over them stay rolled (the kernel
+    // runs once per CTA: unrolled straight-line code is fetched cold, instruction line by line)
+    unsigned m1 = 0, m2 = 0;
     unsigned c1 = 0, c2 = 0;
     {
         uint8_t x[kItems], a[kItems];
@@ -405,77 +457,69 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const bool in = base + k < (slot_tile ? n : m);
-            s1[k] = slot_tile && in && a[k] != 0 && x[k] != 0;
-            s2[k] = in && (slot_tile ? (a[k] == 0 || s1[k]) : x[k] != 0);
-            c1 += s1[k];
-            c2 += s2[k];
+            const bool k1 = slot_tile && in && a[k] != 0 && x[k] != 0;
+            const bool k2 = in && (slot_tile ? (a[k] == 0 || k1) : x[k] != 0);
+            m1 |= static_cast<unsigned>(k1) << k;
+            m2 |= static_cast<unsigned>(k2) << k;
+            c1 += k1;
+            c2 += k2;
         }
     }
+    if (L.recycle)  // the killed slots' ids are read below, after the scan: start them now
+        for (unsigned mm = m1; mm; mm &= mm - 1) prefetch_l2(L.ids + base + (__ffs(static_cast<int>(mm)) - 1));
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(c1, c2), s_scan, &total);
-    if (tid == 0) st_word(&ws->tot[b], kFlagAgg | total);
+    if (slot_tile) {  // tile-local lists: free slots (killed included) and killed ids, in slot order
+        unsigned lf = lo31(excl), lk = hi31(excl);
+#pragma unroll 1
+        for (unsigned mm = m2; mm; mm &= mm - 1) {
+            const unsigned k = static_cast<unsigned>(__ffs(static_cast<int>(mm)) - 1);
+            free_list[tile_base + lf++] = static_cast<int32_t>(base + k);
+            if (L.recycle && ((m1 >> k) & 1u)) kill_ids[tile_base + lk++] = L.ids[base + k];
+        }
+    } else {  // the tile's valid rows in shared memory (placed one per thread after the barrier);
+              // their row values start towards L2 now
+        unsigned lv = lo31(excl);
+#pragma unroll 1
+        for (unsigned mm = m2; mm; mm &= mm - 1) {
+            const size_t row = base + static_cast<unsigned>(__ffs(static_cast<int>(mm)) - 1);
+            s_rows[lv++] = static_cast<int32_t>(row);
+            for (int c = 0; c < A.n; ++c)
+                if (A.src[c]) prefetch_l2(static_cast<const uint8_t*>(A.src[c]) + row * A.sz[c]);
+        }
+    }
+    if (tid == 0) ws->tot[b] = total;
     LIFE_STAMP(1);
-    grid_barrier(&ws->arrived[0], G);
+    grid_barrier(&ws->arrived, G);
     LIFE_STAMP(2);
-    // ---- every tile total: this tile's prefix, K (killed), F (free), Q (valid)
-    unsigned long long pk = 0, pf = 0, K = 0, F = 0, Q = 0;
-    for (unsigned q = tid; q < G; q += kT) {
-        const unsigned long long v = ld_word(&ws->tot[q]);
-        if (q < ta) {
-            K += hi31(v);
-            F += lo31(v);
-        } else {
-            Q += lo31(v);
-        }
-        if (q < b && (q < ta) == slot_tile) {
-            pk += hi31(v);
-            pf += lo31(v);
-        }
-    }
+    // ---- resolve: exclusive prefixes over all tiles (slot tiles first: the lo field of a row
+    // tile's prefix is F + its valid prefix; F + Q < 2^31 since the grid is co-resident)
     {
-        unsigned long long v5[5] = {pk, pf, K, F, Q};
+        constexpr int kPer = (kCoopMaxTiles + kT - 1) / kT;
+        unsigned long long v[kPer], sum = 0;
 #pragma unroll
-        for (int i = 0; i < 5; ++i) v5[i] = warp_sum(v5[i]);
-        if (lane == 0)
-#pragma unroll
-            for (int i = 0; i < 5; ++i) s_red[warp][i] = v5[i];
-        __syncthreads();
-        if (tid < 5) {
-            unsigned long long x = 0;
-            for (int w = 0; w < kT / 32; ++w) x += s_red[w][tid];
-            s_v[tid] = x;
+        for (int e = 0; e < kPer; ++e) {
+            const unsigned q = static_cast<unsigned>(tid) * kPer + e;
+            v[e] = q < G ? ws->tot[q] : 0ULL;
+            sum += v[e];
         }
+        unsigned long long all;
+        unsigned long long run = block_excl_scan<kT>(sum, s_scan, &all);
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const unsigned q = static_cast<unsigned>(tid) * kPer + e;
+            if (q < G) s_pref[q] = run;
+            run += v[e];
+        }
+        if (tid == 0) s_pref[G] = all;
         __syncthreads();
     }
-    K = s_v[2];
-    F = s_v[3];
-    Q = s_v[4];
+    const unsigned long long at_ta = s_pref[ta];
+    const unsigned long long K = hi31(at_ta), F = lo31(at_ta), Q = lo31(s_pref[G]) - F;
     const long long r = static_cast<long long>(F < Q ? F : Q);
-    LIFE_STAMP(6);
-    // ---- write
-    long long kpos = static_cast<long long>(s_v[0]) + hi31(excl);  // killed before this thread
-    long long fpos = static_cast<long long>(s_v[1]) + lo31(excl);  // free (or valid) before this thread
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-        const size_t i = base + k;
-        if (s1[k]) {  // remove_agents: reset_slot (type kept), push the id
-            if (L.recycle) L.retired[top0 + kpos] = L.ids[i];
-            ++kpos;
-            L.active[i] = 0;
-            L.ids[i] = 0;
-            L.ages[i] = 0;
-            for (int c = 0; c < Z.n; ++c) zero_elem(Z.dst[c], static_cast<long long>(i), Z.sz[c]);
-        }
-        if (s2[k]) {
-            if (fpos < r) (slot_tile ? slots : rows)[fpos] = static_cast<int32_t>(i);
-            ++fpos;
-        }
-    }
-    // barrier 2 orders this CTA's list, resets and pushes: bar.sync, then thread 0's release
-    LIFE_STAMP(3);
-    grid_barrier(&ws->arrived[1], G);
-    LIFE_STAMP(4);
+    const long long live0 = s_cnt[0], nid = s_cnt[1], top0 = s_cnt[2];
     const long long top = top0 + (L.recycle ? static_cast<long long>(K) : 0);  // after the pushes
+    LIFE_STAMP(6);
     if (b == 0 && tid == 0) {  // counters (lifecycle.cpp:136-141, 186-194)
         const long long used = top < r ? top : r;
         L.counters[0] = live0 - static_cast<long long>(K) + r;
@@ -487,15 +531,54 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
             out[1] = static_cast<long long>(Q) - r;
         }
     }
-    // ---- pair: the k-th free slot takes the k-th valid row, one pair per thread over the grid
-    for (long long q = static_cast<long long>(b) * kT + tid; q < r; q += static_cast<long long>(G) * kT) {
-        const int slot = slots[q], row = rows[q];
-        for (int c = 0; c < A.n; ++c)
-            if (A.src[c]) copy_elem(A.dst[c], slot, A.src[c], row, A.sz[c]);
-        L.active[slot] = 1;
-        L.ids[slot] = q < top ? L.retired[top - 1 - q] : nid + (q - top);
-        L.ages[slot] = 0;
-        if (set_type) L.types[slot] = agent_type;
+    // ---- write
+    const unsigned long long own = s_pref[b];
+    if (slot_tile) {  // remove_agents: reset_slot (type kept), push the id (slot order)
+        const long long kpos0 = static_cast<long long>(hi31(own)) + hi31(excl);
+        const long long fpos0 = static_cast<long long>(lo31(own)) + lo31(excl);
+#pragma unroll 1
+        for (unsigned mm = m1; mm; mm &= mm - 1) {
+            const unsigned k = static_cast<unsigned>(__ffs(static_cast<int>(mm)) - 1);
+            const unsigned below = (1u << k) - 1u;
+            const size_t i = base + k;
+            const unsigned lk = hi31(excl) + __popc(m1 & below);
+            if (L.recycle) L.retired[top0 + kpos0 + __popc(m1 & below)] = kill_ids[tile_base + lk];
+            if (fpos0 + __popc(m2 & below) < r) {  // refilled below: zero what the spawn leaves
+                for (int c = 0; c < Z.n; ++c)
+                    if ((z_refill >> c) & 1u) zero_elem(Z.dst[c], static_cast<long long>(i), Z.sz[c]);
+            } else {
+                L.active[i] = 0;
+                L.ids[i] = 0;
+                L.ages[i] = 0;
+                for (int c = 0; c < Z.n; ++c) zero_elem(Z.dst[c], static_cast<long long>(i), Z.sz[c]);
+            }
+        }
+    } else {  // spawn_agents: the q-th valid row fills the q-th free slot (tile rows over the threads)
+        const long long q0 = static_cast<long long>(lo31(own)) - static_cast<long long>(F);
+        const long long cnt = static_cast<long long>(lo31(total)) < r - q0 ? lo31(total) : r - q0;
+#pragma unroll 1
+        for (long long j = tid; j < cnt; j += kT) {
+            const long long q = q0 + j;
+            const int row = s_rows[j];
+            const unsigned t = tile_of_rank<false>(s_pref, ta, static_cast<unsigned long long>(q));
+            const int slot = free_list[static_cast<size_t>(t) * kTile + (q - lo31(s_pref[t]))];
+            long long id = nid + (q - top);
+            if (q < top) {
+                const long long e = top - 1 - q;  // stack entry popped
+                if (e >= top0) {                  // pushed this cycle: killed id of kill rank e - top0
+                    const unsigned long long j = static_cast<unsigned long long>(e - top0);
+                    const unsigned t2 = tile_of_rank<true>(s_pref, ta, j);
+                    id = kill_ids[static_cast<size_t>(t2) * kTile + (j - hi31(s_pref[t2]))];
+                } else {
+                    id = L.retired[e];
+                }
+            }
+            copy_cols(A, slot, static_cast<long long>(row));
+            L.active[slot] = 1;
+            L.ids[slot] = id;
+            L.ages[slot] = 0;
+            if (set_type) L.types[slot] = agent_type;
+        }
     }
     LIFE_STAMP(5);
 }
@@ -503,16 +586,14 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
 // set_agents_mask with per-slot source values: dst[c][i] <- src[c][i] where mask[i].
 __global__ void __launch_bounds__(kT) k_mask_apply(const uint8_t* __restrict__ mask, size_t n, Cols C) {
     for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT)
-        if (mask[i])
-            for (int c = 0; c < C.n; ++c)
-                if (C.src[c]) copy_elem(C.dst[c], i, C.src[c], i, C.sz[c]);
+        if (mask[i]) copy_cols(C, static_cast<long long>(i), static_cast<long long>(i));
 }
 
 // gather: dst[c][i] <- src[c][perm[i]] (permute_agents, agent_set.cpp:92-108)
 __global__ void __launch_bounds__(kT) k_gather(const int32_t* __restrict__ perm, size_t n, Cols C) {
     for (size_t i = static_cast<size_t>(blockIdx.x) * kT + threadIdx.x; i < n; i += static_cast<size_t>(gridDim.x) * kT) {
         const int j = perm[i];
-        for (int c = 0; c < C.n; ++c) copy_elem(C.dst[c], i, C.src[c], j, C.sz[c]);
+        copy_cols(C, static_cast<long long>(i), j);  // every gather column has a source
     }
 }
 __global__ void k_check_perm(const int32_t* __restrict__ perm, size_t n, unsigned* bad) {
@@ -894,7 +975,7 @@ int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* 
 
 #ifdef ABMX_LIFE_TRACE
 extern "C" int abmx_life_trace(unsigned long long* out, int ctas) {
-    return cudaMemcpyFromSymbol(out, abmx_agents::g_life_trace, sizeof(unsigned long long) * 7 * ctas) == cudaSuccess ? 0 : -1;
+    return cudaMemcpyFromSymbol(out, abmx_agents::g_life_trace, sizeof(unsigned long long) * 8 * ctas) == cudaSuccess ? 0 : -1;
 }
 #endif
 
@@ -955,13 +1036,21 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
         }
     }
     const long long coop_cap = per_sm > 0 ? static_cast<long long>(per_sm) * abmx_internal::num_sms() : 0;
-    if (static_cast<long long>(ta + tb) <= coop_cap) {  // one cooperative kernel
+    if (static_cast<long long>(ta + tb) <= coop_cap && ta + tb <= static_cast<size_t>(kCoopMaxTiles)) {
+        // one cooperative kernel; scratch: [workspace | free slots per slot tile | killed ids]
         const size_t ws_b = (sizeof(LifeWs) + (ta + tb) * sizeof(unsigned long long) + 15) / 16 * 16;
+        const size_t lists = ta * kTile;
         void* ws = nullptr;
-        CKA(sc.get(&ws, ws_b + n * 4 + static_cast<size_t>(m) * 4));
-        int32_t* slots = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_b);
-        int32_t* rws = slots + n;
-        CKA(cudaMemsetAsync(ws, 0, sizeof(unsigned) * 2, st));
+        CKA(sc.get(&ws, ws_b + lists * 4 + (s->recycle_ids ? lists * 8 : 0)));
+        int32_t* free_list = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_b);
+        long long* kill_ids = s->recycle_ids ? reinterpret_cast<long long*>(free_list + lists) : nullptr;
+        unsigned z_refill = 0;  // state columns a refilled killed slot still zeroes: those without a row column
+        for (int c = 0; c < Z.n; ++c) {
+            bool written = false;
+            for (int e = 0; e < A.n; ++e) written = written || A.dst[e] == Z.dst[c];
+            if (!written) z_refill |= 1u << c;
+        }
+        CKA(cudaMemsetAsync(ws, 0, sizeof(unsigned), st));
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(static_cast<unsigned>(ta + tb));
         cfg.blockDim = dim3(kT);
@@ -972,7 +1061,7 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         CKA(cudaLaunchKernelEx(&cfg, k_life_coop, d_kill, n, static_cast<unsigned>(ta), d_valid, static_cast<size_t>(m),
-                               slots, rws, static_cast<LifeWs*>(ws), Z, A, L, static_cast<int>(set_type),
+                               free_list, kill_ids, static_cast<LifeWs*>(ws), Z, z_refill, A, L, static_cast<int>(set_type),
                                static_cast<long long>(agent_type), reinterpret_cast<long long*>(d_killed),
                                reinterpret_cast<long long*>(d_result)));
         abmx_internal::count_launch();

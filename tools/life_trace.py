@@ -2,7 +2,7 @@
 flushed clean first, from a -DABMX_LIFE_TRACE build:
     tools/build_variant.sh lifetrace "-DABMX_LIFE_TRACE"
     ABMX_CUDA_LIB=build/variants/lifetrace/libabmx_cuda.so python tools/life_trace.py
-Stamps per CTA: start, counted, barrier 1 passed, written, barrier 2 passed, end."""
+Stamps per CTA: start, counted (lists written), barrier passed, prefixes resolved, end."""
 import ctypes as C
 import os
 import sys
@@ -25,7 +25,7 @@ out = torch.zeros(4, dtype=torch.int64, device="cuda")
 res = torch.zeros(2, dtype=torch.int64, device="cuda")
 flush = torch.empty((256 << 20) // 4, dtype=torch.int32, device="cuda")
 flush2 = torch.ones((256 << 20) // 4, dtype=torch.int32, device="cuda")
-labels = ["start", "counted", "barrier1", "written", "barrier2", "end", "reduced"]
+labels = {0: "start", 1: "counted", 2: "barrier", 6: "resolved", 5: "end"}
 for rep in range(4):
     kill = np.zeros(cap, np.uint8)
     kill[rng.choice(cap, churn, replace=False)] = 1
@@ -39,10 +39,13 @@ for rep in range(4):
                                                out.data_ptr(), res.data_ptr(), s._stream()))
     torch.cuda.synchronize()
 G = 256
-buf = np.zeros((G, 7), np.uint64)
+buf = np.zeros((G, 8), np.uint64)
 assert abmx.lib.abmx_life_trace(buf.ctypes.data_as(C.POINTER(C.c_uint64)), G) == 0
 tr = (buf.astype(np.int64) - int(buf[:, 0].min())) / 1e3
 print(f"k_life_coop, {G} CTAs, last of 4 flushed cycles (us from the first CTA start)")
-for k, lab in enumerate(labels):
-    v = tr[:, k]
-    print(f"  {lab:9s} p0 {v.min():6.2f}  p50 {np.median(v):6.2f}  p90 {np.percentile(v, 90):6.2f}  max {v.max():6.2f}")
+ta = G // 2  # slot tiles first (C2's set: 128 slot tiles, 128 row tiles)
+for name, rows_ in (("all", slice(0, G)), ("slot tiles", slice(0, ta)), ("row tiles", slice(ta, G))):
+    print(f" {name}:")
+    for k, lab in labels.items():
+        v = tr[rows_, k]
+        print(f"  {lab:9s} p0 {v.min():6.2f}  p50 {np.median(v):6.2f}  p90 {np.percentile(v, 90):6.2f}  max {v.max():6.2f}")
