@@ -290,3 +290,34 @@ def test_fused_lifecycle_large_vs_oracle(agents, oracle, cap, recycle):
         assert (killed, spawned, dropped) == (wo["killed"], wo["spawned"], wo["dropped"])
         ewf_equal(from_dev(dev, recycle), st, cyc)
         assert np.array_equal(dev.types.cpu().numpy(), st["types"])
+
+
+@pytest.mark.parametrize("cols", [(), ("e",), ("w", "f"), ("e", "w", "f")])
+@pytest.mark.parametrize("cap,recycle", [(5, True), (4097, False), (300_001, True)])
+def test_fused_lifecycle_partial_rows(agents, cap, recycle, cols):
+    """Spawn rows that carry only some state columns: a killed slot refilled in the same cycle
+    keeps zeros in the columns the rows do not carry (reset_slot, then the copy apply leaves
+    them alone). The one-barrier cooperative kernel zeroes exactly those columns there, so the
+    fused call must equal remove + spawn on an identical set. Inactive slots hold non-zero
+    values here, so a free slot that was never killed keeps them in the missing columns."""
+    g = np.random.default_rng(cap * 7 + len(cols) + recycle)
+    st = _random_state(g, cap, recycle)
+    st["e"] = g.integers(-1000, 1000, cap).astype(np.int64)  # garbage in inactive slots too
+    st["w"] = g.uniform(-5, 5, cap)
+    fused, split = to_dev(agents, st), to_dev(agents, st)
+    for cyc in range(3):
+        kill = (g.random(cap) < 0.2).astype(np.uint8)
+        m = int(g.integers(1, cap + 3))
+        full = {"e": g.integers(0, 1 << 40, m).astype(np.int64), "w": g.uniform(-1, 1, m),
+                "f": (g.random(m) < 0.5).astype(np.uint8)}
+        rows = {k: full[k] for k in cols}
+        valid = (g.random(m) < 0.6).astype(np.uint8)
+        at = cyc + 2 if cyc % 2 else None
+        got = fused.lifecycle(kill, rows, valid, agent_type=at)
+        killed = split.remove(kill)
+        out = split.spawn(rows, valid, agent_type=at)
+        assert got == (killed, out.spawned, out.dropped), (cap, cols, cyc)
+        a, b = from_dev(fused, recycle), from_dev(split, recycle)
+        for k in b:
+            assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), (cap, cols, cyc, k)
+        assert np.array_equal(fused.types.cpu().numpy(), split.types.cpu().numpy())
