@@ -446,8 +446,8 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     }
     // ---- count
     // bit k of m1 / m2: slot tile: killed / free once removed; row tile: - / valid. Bit masks
-    // keep the per-slot flags in two registers, so the loops over them stay rolled (the kernel
-    // runs once per CTA: unrolled straight-line code is fetched cold, instruction line by line)
+    // keep the per-slot flags in two registers, so the loops over them stay rolled and visit
+    // only the set bits (the unrolled 16-way version was ~3 µs slower in the trace)
     unsigned m1 = 0, m2 = 0;
     unsigned c1 = 0, c2 = 0;
     {
