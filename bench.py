@@ -461,7 +461,10 @@ def agents_section(args, rank):
                          f"L2 flushed before each",
              "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms,
              "launches_per_cycle": "1 memset + 1 cooperative kernel (abmx_agents_lifecycle, k_life_coop)",
-             "two_call_ms_per_cycle": ms_two, "fused_equals_two_calls": bool(same)}
+             "two_call_ms_per_cycle": ms_two,
+             "two_call_launches_per_cycle": "2 x (1 memset + 1 cooperative kernel): abmx_agents_remove and "
+                                            "abmx_agents_spawn, each one k_life_coop",
+             "fused_equals_two_calls": bool(same)}
     if rank == 0 and not args.no_cpu_baseline:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import pyoracle

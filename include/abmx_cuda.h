@@ -259,13 +259,15 @@ typedef struct abmx_agent_set {
 
 /* remove_agents (lifecycle.cpp:124-142): live slots with kill[i] != 0 are reset (active, id,
  * age, state zeroed; type kept, agent_set.cpp:45-58); with recycle_ids their ids are pushed on
- * the retired stack in slot order. d_killed (nullable, device int64): number removed. */
+ * the retired stack in slot order. d_killed (nullable, device int64): number removed.
+ * One cooperative launch when the set's tiles fit on the GPU at once (see lifecycle below). */
 int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* d_killed,
                        void* stream);
 /* spawn_agents (lifecycle.cpp:144-195): the k-th free slot receives the k-th valid row
  * (copy apply), id = retired.pop() while recycling and non-empty else next_id++, age 0,
  * type = agent_type if set_type. d_slots[k] / d_rows[k] (nullable, device int32, capacity /
- * m entries): pair k. d_result (nullable, device int64[2]): {spawned, dropped}. */
+ * m entries): pair k, k < spawned. d_result (nullable, device int64[2]): {spawned, dropped}.
+ * One cooperative launch when the set's tiles fit on the GPU at once (see lifecycle below). */
 int abmx_agents_spawn(const abmx_agent_set* s, int32_t m, const uint8_t* d_valid,
                       const abmx_column* rows, int32_t set_type, int64_t agent_type,
                       int32_t* d_slots, int32_t* d_rows, int64_t* d_result, void* stream);

@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
                                                   const uint8_t* __restrict__ valid, size_t m,
                                                   int32_t* __restrict__ free_list, long long* __restrict__ kill_ids,
                                                   LifeWs* ws, Cols Z, unsigned z_refill, Cols A, Life L, int set_type,
-                                                  long long agent_type, long long* out_killed, long long* out) {
+                                                  long long agent_type, long long* out_killed, long long* out,
+                                                  int32_t* pair_slots, int32_t* pair_rows) {
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ unsigned long long s_pref[kCoopMaxTiles + 1];  // exclusive tile prefixes, [G] = total
     __shared__ long long s_cnt[3];
@@ -469,12 +470,13 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
         for (unsigned mm = m1; mm; mm &= mm - 1) prefetch_l2(L.ids + base + (__ffs(static_cast<int>(mm)) - 1));
     unsigned long long total;
     const unsigned long long excl = block_excl_scan<kT>(pack2(c1, c2), s_scan, &total);
-    if (slot_tile) {  // tile-local lists: free slots (killed included) and killed ids, in slot order
+    if (slot_tile) {  // tile-local lists: free slots (killed included; only when rows follow) and
+                      // killed ids, in slot order
         unsigned lf = lo31(excl), lk = hi31(excl);
 #pragma unroll 1
-        for (unsigned mm = m2; mm; mm &= mm - 1) {
+        for (unsigned mm = G > ta ? m2 : m1; mm; mm &= mm - 1) {
             const unsigned k = static_cast<unsigned>(__ffs(static_cast<int>(mm)) - 1);
-            free_list[tile_base + lf++] = static_cast<int32_t>(base + k);
+            if (G > ta) free_list[tile_base + lf++] = static_cast<int32_t>(base + k);
             if (L.recycle && ((m1 >> k) & 1u)) kill_ids[tile_base + lk++] = L.ids[base + k];
         }
     } else {  // the tile's valid rows in shared memory (placed one per thread after the barrier);
@@ -574,6 +576,8 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
                 }
             }
             copy_cols(A, slot, static_cast<long long>(row));
+            if (pair_slots) pair_slots[q] = slot;  // spawn_agents' pair lists (abmx_agents_spawn)
+            if (pair_rows) pair_rows[q] = row;
             L.active[slot] = 1;
             L.ids[slot] = id;
             L.ages[slot] = 0;
@@ -823,6 +827,85 @@ int for_col_chunks(int ncols, F&& fn) {
     return ABMX_OK;
 }
 
+constexpr int kNoCoop = -1000;  // life_coop: the cooperative kernel does not apply
+
+// One cooperative k_life_coop launch for remove (m == 0), spawn (d_kill == nullptr) or both, when
+// the set has at most kMaxCols state columns and its ta + tb tiles are co-resident; kNoCoop
+// otherwise (the caller takes its multi-kernel path). Arguments are checked by the caller.
+static int life_coop(const abmx_agent_set* s, const uint8_t* d_kill, int32_t m, const uint8_t* d_valid,
+                     const abmx_column* rows, int32_t set_type, int64_t agent_type, int64_t* d_killed,
+                     int64_t* d_result, int32_t* d_slots, int32_t* d_rows, cudaStream_t st) {
+    if (s->capacity == 0 || s->n_state > kMaxCols || (!d_kill && m == 0)) return kNoCoop;
+    const size_t n = static_cast<size_t>(s->capacity);
+    const size_t ta = (n + kTile - 1) / kTile, tb = (static_cast<size_t>(m) + kTile - 1) / kTile;
+    Cols Z{};  // removal: zero every state column
+    Z.n = s->n_state;
+    for (int c = 0; c < s->n_state; ++c) {
+        Z.dst[c] = s->state[c].data;
+        Z.src[c] = nullptr;
+        Z.sz[c] = s->state[c].elem_size;
+    }
+    Cols A{};  // spawn: copy the row columns given
+    A.n = 0;
+    for (int c = 0; c < s->n_state; ++c) {
+        if (!rows || !rows[c].data) continue;
+        A.dst[A.n] = s->state[c].data;
+        A.src[A.n] = rows[c].data;
+        A.sz[A.n] = s->state[c].elem_size;
+        ++A.n;
+    }
+    const Life L = life_of(s);
+    // co-resident k_life_coop CTAs per SM, per device (computed once; racing writers store the
+    // same value)
+    static std::atomic<int> coop_per_sm[abmx_internal::kMaxDevices] = {};
+    int dev = 0;
+    CKA(cudaGetDevice(&dev));
+    int per_sm = 0;
+    if (dev >= 0 && dev < abmx_internal::kMaxDevices) {
+        per_sm = coop_per_sm[dev].load(std::memory_order_relaxed);
+        if (per_sm == 0) {
+            int per = 0;
+            CKA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_life_coop, kT, 0));
+            per_sm = per > 0 ? per : -1;
+            coop_per_sm[dev].store(per_sm, std::memory_order_relaxed);
+        }
+    }
+    const long long coop_cap = per_sm > 0 ? static_cast<long long>(per_sm) * abmx_internal::num_sms() : 0;
+    if (static_cast<long long>(ta + tb) > coop_cap || ta + tb > static_cast<size_t>(kCoopMaxTiles)) return kNoCoop;
+    {  // one cooperative kernel; scratch: [workspace | free slots per slot tile | killed ids]
+        Scratch sc(st);
+        const size_t ws_b = (sizeof(LifeWs) + (ta + tb) * sizeof(unsigned long long) + 15) / 16 * 16;
+        const size_t lists = ta * kTile;
+        void* ws = nullptr;
+        CKA(sc.get(&ws, ws_b + lists * 4 + (s->recycle_ids ? lists * 8 : 0)));
+        int32_t* free_list = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_b);
+        long long* kill_ids = s->recycle_ids ? reinterpret_cast<long long*>(free_list + lists) : nullptr;
+        unsigned z_refill = 0;  // state columns a refilled killed slot still zeroes: those without a row column
+        for (int c = 0; c < Z.n; ++c) {
+            bool written = false;
+            for (int e = 0; e < A.n; ++e) written = written || A.dst[e] == Z.dst[c];
+            if (!written) z_refill |= 1u << c;
+        }
+        CKA(cudaMemsetAsync(ws, 0, sizeof(unsigned), st));
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(static_cast<unsigned>(ta + tb));
+        cfg.blockDim = dim3(kT);
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        CKA(cudaLaunchKernelEx(&cfg, k_life_coop, d_kill, n, static_cast<unsigned>(ta), d_valid, static_cast<size_t>(m),
+                               free_list, kill_ids, static_cast<LifeWs*>(ws), Z, z_refill, A, L, static_cast<int>(set_type),
+                               static_cast<long long>(agent_type), reinterpret_cast<long long*>(d_killed),
+                               reinterpret_cast<long long*>(d_result), d_slots, d_rows));
+        abmx_internal::count_launch();
+        CKA(cudaGetLastError());
+        return ABMX_OK;
+    }
+}
+
 // shared pairing core of spawn / set_rm / set_sci
 int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int32_t m, const uint8_t* d_valid,
               const abmx_column* rows, int set_type, int64_t agent_type, int32_t* d_slots, int32_t* d_rows,
@@ -844,6 +927,10 @@ int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int3
         }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     (void)cudaGetLastError();
+    if (spawn) {  // one cooperative kernel when the tiles fit (pairs k < spawned listed)
+        rc = life_coop(s, nullptr, m, d_valid, rows, set_type, agent_type, nullptr, d_out, d_slots, d_rows, st);
+        if (rc != kNoCoop) return rc;
+    }
     Scratch sc(st);
     const size_t n = static_cast<size_t>(s->capacity);
     int32_t* slots = d_slots;
@@ -929,6 +1016,8 @@ int abmx_agents_remove(const abmx_agent_set* s, const uint8_t* d_kill, int64_t* 
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     (void)cudaGetLastError();
+    rc = life_coop(s, d_kill, 0, nullptr, nullptr, 0, 0, d_killed, nullptr, nullptr, nullptr, st);
+    if (rc != kNoCoop) return rc;
     Scratch sc(st);
     const size_t n = static_cast<size_t>(s->capacity);
     int32_t* list = nullptr;
@@ -1000,6 +1089,8 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
     }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     (void)cudaGetLastError();
+    rc = life_coop(s, d_kill, m, d_valid, rows, set_type, agent_type, d_killed, d_result, nullptr, nullptr, st);
+    if (rc != kNoCoop) return rc;
     Scratch sc(st);
     const size_t n = static_cast<size_t>(s->capacity);
     const size_t ta = (n + kTile - 1) / kTile, tb = (static_cast<size_t>(m) + kTile - 1) / kTile;
@@ -1020,54 +1111,6 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
         ++A.n;
     }
     const Life L = life_of(s);
-    // co-resident k_life_coop CTAs per SM, per device (computed once; racing writers store the
-    // same value)
-    static std::atomic<int> coop_per_sm[abmx_internal::kMaxDevices] = {};
-    int dev = 0;
-    CKA(cudaGetDevice(&dev));
-    int per_sm = 0;
-    if (dev >= 0 && dev < abmx_internal::kMaxDevices) {
-        per_sm = coop_per_sm[dev].load(std::memory_order_relaxed);
-        if (per_sm == 0) {
-            int per = 0;
-            CKA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_life_coop, kT, 0));
-            per_sm = per > 0 ? per : -1;
-            coop_per_sm[dev].store(per_sm, std::memory_order_relaxed);
-        }
-    }
-    const long long coop_cap = per_sm > 0 ? static_cast<long long>(per_sm) * abmx_internal::num_sms() : 0;
-    if (static_cast<long long>(ta + tb) <= coop_cap && ta + tb <= static_cast<size_t>(kCoopMaxTiles)) {
-        // one cooperative kernel; scratch: [workspace | free slots per slot tile | killed ids]
-        const size_t ws_b = (sizeof(LifeWs) + (ta + tb) * sizeof(unsigned long long) + 15) / 16 * 16;
-        const size_t lists = ta * kTile;
-        void* ws = nullptr;
-        CKA(sc.get(&ws, ws_b + lists * 4 + (s->recycle_ids ? lists * 8 : 0)));
-        int32_t* free_list = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + ws_b);
-        long long* kill_ids = s->recycle_ids ? reinterpret_cast<long long*>(free_list + lists) : nullptr;
-        unsigned z_refill = 0;  // state columns a refilled killed slot still zeroes: those without a row column
-        for (int c = 0; c < Z.n; ++c) {
-            bool written = false;
-            for (int e = 0; e < A.n; ++e) written = written || A.dst[e] == Z.dst[c];
-            if (!written) z_refill |= 1u << c;
-        }
-        CKA(cudaMemsetAsync(ws, 0, sizeof(unsigned), st));
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(static_cast<unsigned>(ta + tb));
-        cfg.blockDim = dim3(kT);
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = 1;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        CKA(cudaLaunchKernelEx(&cfg, k_life_coop, d_kill, n, static_cast<unsigned>(ta), d_valid, static_cast<size_t>(m),
-                               free_list, kill_ids, static_cast<LifeWs*>(ws), Z, z_refill, A, L, static_cast<int>(set_type),
-                               static_cast<long long>(agent_type), reinterpret_cast<long long*>(d_killed),
-                               reinterpret_cast<long long*>(d_result)));
-        abmx_internal::count_launch();
-        CKA(cudaGetLastError());
-        return ABMX_OK;
-    }
     const size_t wa_b = (sizeof(ScanWs) + ta * sizeof(unsigned long long) + 15) / 16 * 16;
     const size_t wb_b = (sizeof(ScanWs) + tb * sizeof(unsigned long long) + 15) / 16 * 16;
     const size_t ws_b = (wa_b + wb_b + sizeof(LifeCounts) + 15) / 16 * 16;

@@ -321,3 +321,29 @@ def test_fused_lifecycle_partial_rows(agents, cap, recycle, cols):
         for k in b:
             assert np.array_equal(np.asarray(a[k]), np.asarray(b[k])), (cap, cols, cyc, k)
         assert np.array_equal(fused.types.cpu().numpy(), split.types.cpu().numpy())
+
+
+def test_lifecycle_beyond_cooperative_grid_vs_oracle(agents, oracle):
+    """A set with more tiles than one cooperative grid holds (2049 slot tiles of 4096 > 2048):
+    remove / spawn / the fused cycle take the multi-kernel paths (lookback selections and the
+    pair apply), against the C restatement."""
+    cap = 2048 * 4096 + 5
+    g = np.random.default_rng(2049)
+    st = _random_state(g, cap, True)
+    dev = to_dev(agents, st)
+    for cyc in range(2):
+        kill = (g.random(cap) < 0.02).astype(np.uint8)
+        m = 200_000
+        rows = {"e": g.integers(0, 1 << 40, m).astype(np.int64), "w": g.uniform(-1, 1, m),
+                "f": (g.random(m) < 0.5).astype(np.uint8)}
+        valid = (g.random(m) < 0.7).astype(np.uint8)
+        st, wo = oracle.lifecycle(st, kill, rows, valid, True, cyc + 1)
+        if cyc == 0:
+            got = dev.lifecycle(kill, rows, valid, agent_type=cyc + 1)
+            assert got == (wo["killed"], wo["spawned"], wo["dropped"])
+        else:
+            assert dev.remove(kill) == wo["killed"]
+            out = dev.spawn(rows, valid, agent_type=cyc + 1)
+            assert (out.spawned, out.dropped) == (wo["spawned"], wo["dropped"])
+            assert np.array_equal(out.slots, wo["slots"]) and np.array_equal(out.rows, wo["rows"])
+        ewf_equal(from_dev(dev, True), st, cyc)
