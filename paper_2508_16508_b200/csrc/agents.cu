@@ -426,7 +426,10 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
                                                   int32_t* __restrict__ free_list, long long* __restrict__ kill_ids,
                                                   LifeWs* ws, Cols Z, unsigned z_refill, Cols A, Life L, int set_type,
                                                   long long agent_type, long long* out_killed, long long* out,
-                                                  int32_t* pair_slots, int32_t* pair_rows) {
+                                                  int32_t* pair_slots, int32_t* pair_rows, int rm) {
+    // rm != 0: set_agents_rm / _sci with the copy apply (kernels.cpp:116-153): `kill` is the
+    // target mask, the k-th target slot takes the k-th valid row, and nothing else changes (no
+    // removal, no lifecycle fields, no counters); out = {pairs, valid rows}
     __shared__ unsigned long long s_scan[kT / 32 + 1];
     __shared__ unsigned long long s_pref[kCoopMaxTiles + 1];  // exclusive tile prefixes, [G] = total
     __shared__ long long s_cnt[3];
@@ -454,12 +457,12 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     {
         uint8_t x[kItems], a[kItems];
         load16(slot_tile ? kill : valid, base, slot_tile ? n : m, x);
-        load16(slot_tile ? L.active : nullptr, base, n, a);
+        load16(slot_tile && !rm ? L.active : nullptr, base, n, a);
 #pragma unroll
         for (int k = 0; k < kItems; ++k) {
             const bool in = base + k < (slot_tile ? n : m);
-            const bool k1 = slot_tile && in && a[k] != 0 && x[k] != 0;
-            const bool k2 = in && (slot_tile ? (a[k] == 0 || k1) : x[k] != 0);
+            const bool k1 = !rm && slot_tile && in && a[k] != 0 && x[k] != 0;
+            const bool k2 = in && (slot_tile && !rm ? (a[k] == 0 || k1) : x[k] != 0);
             m1 |= static_cast<unsigned>(k1) << k;
             m2 |= static_cast<unsigned>(k2) << k;
             c1 += k1;
@@ -524,13 +527,15 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     LIFE_STAMP(6);
     if (b == 0 && tid == 0) {  // counters (lifecycle.cpp:136-141, 186-194)
         const long long used = top < r ? top : r;
-        L.counters[0] = live0 - static_cast<long long>(K) + r;
-        L.counters[1] = nid + r - used;
-        if (L.recycle) L.counters[2] = top - used;
+        if (!rm) {
+            L.counters[0] = live0 - static_cast<long long>(K) + r;
+            L.counters[1] = nid + r - used;
+            if (L.recycle) L.counters[2] = top - used;
+        }
         if (out_killed) *out_killed = static_cast<long long>(K);
         if (out) {
             out[0] = r;
-            out[1] = static_cast<long long>(Q) - r;
+            out[1] = static_cast<long long>(Q) - (rm ? 0 : r);
         }
     }
     // ---- write
@@ -565,7 +570,7 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
             const unsigned t = tile_of_rank<false>(s_pref, ta, static_cast<unsigned long long>(q));
             const int slot = free_list[static_cast<size_t>(t) * kTile + (q - lo31(s_pref[t]))];
             long long id = nid + (q - top);
-            if (q < top) {
+            if (!rm && q < top) {
                 const long long e = top - 1 - q;  // stack entry popped
                 if (e >= top0) {                  // pushed this cycle: killed id of kill rank e - top0
                     const unsigned long long j = static_cast<unsigned long long>(e - top0);
@@ -578,6 +583,7 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
             copy_cols(A, slot, static_cast<long long>(row));
             if (pair_slots) pair_slots[q] = slot;  // spawn_agents' pair lists (abmx_agents_spawn)
             if (pair_rows) pair_rows[q] = row;
+            if (rm) continue;
             L.active[slot] = 1;
             L.ids[slot] = id;
             L.ages[slot] = 0;
@@ -834,8 +840,8 @@ constexpr int kNoCoop = -1000;  // life_coop: the cooperative kernel does not ap
 // otherwise (the caller takes its multi-kernel path). Arguments are checked by the caller.
 static int life_coop(const abmx_agent_set* s, const uint8_t* d_kill, int32_t m, const uint8_t* d_valid,
                      const abmx_column* rows, int32_t set_type, int64_t agent_type, int64_t* d_killed,
-                     int64_t* d_result, int32_t* d_slots, int32_t* d_rows, cudaStream_t st) {
-    if (s->capacity == 0 || s->n_state > kMaxCols || (!d_kill && m == 0)) return kNoCoop;
+                     int64_t* d_result, int32_t* d_slots, int32_t* d_rows, cudaStream_t st, int rm = 0) {
+    if (s->capacity == 0 || s->n_state > kMaxCols || (m == 0 && (rm || !d_kill))) return kNoCoop;
     const size_t n = static_cast<size_t>(s->capacity);
     const size_t ta = (n + kTile - 1) / kTile, tb = (static_cast<size_t>(m) + kTile - 1) / kTile;
     Cols Z{};  // removal: zero every state column
@@ -899,7 +905,7 @@ static int life_coop(const abmx_agent_set* s, const uint8_t* d_kill, int32_t m, 
         CKA(cudaLaunchKernelEx(&cfg, k_life_coop, d_kill, n, static_cast<unsigned>(ta), d_valid, static_cast<size_t>(m),
                                free_list, kill_ids, static_cast<LifeWs*>(ws), Z, z_refill, A, L, static_cast<int>(set_type),
                                static_cast<long long>(agent_type), reinterpret_cast<long long*>(d_killed),
-                               reinterpret_cast<long long*>(d_result), d_slots, d_rows));
+                               reinterpret_cast<long long*>(d_result), d_slots, d_rows, rm));
         abmx_internal::count_launch();
         CKA(cudaGetLastError());
         return ABMX_OK;
@@ -927,8 +933,9 @@ int pair_rows(const abmx_agent_set* s, const uint8_t* d_target, bool spawn, int3
         }
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     (void)cudaGetLastError();
-    if (spawn) {  // one cooperative kernel when the tiles fit (pairs k < spawned listed)
-        rc = life_coop(s, nullptr, m, d_valid, rows, set_type, agent_type, nullptr, d_out, d_slots, d_rows, st);
+    {  // one cooperative kernel when the tiles fit (pairs k < r listed)
+        rc = spawn ? life_coop(s, nullptr, m, d_valid, rows, set_type, agent_type, nullptr, d_out, d_slots, d_rows, st)
+                   : life_coop(s, d_target, m, d_valid, rows, 0, 0, nullptr, d_out, d_slots, d_rows, st, 1);
         if (rc != kNoCoop) return rc;
     }
     Scratch sc(st);

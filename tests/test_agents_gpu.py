@@ -347,3 +347,31 @@ def test_lifecycle_beyond_cooperative_grid_vs_oracle(agents, oracle):
             assert (out.spawned, out.dropped) == (wo["spawned"], wo["dropped"])
             assert np.array_equal(out.slots, wo["slots"]) and np.array_equal(out.rows, wo["rows"])
         ewf_equal(from_dev(dev, True), st, cyc)
+
+
+@pytest.mark.parametrize("cap", [5, 4097, 1 << 20, 2048 * 4096 + 5])
+def test_set_rm_sci_large(agents, cap):
+    """set_agents_rm / _sci with the copy apply at sizes where the selections span many tiles
+    (one cooperative launch up to 2048 tiles, the multi-kernel path beyond): the k-th target
+    slot takes the k-th valid row in the columns given; lifecycle fields and counters stay."""
+    g = np.random.default_rng(cap + 3)
+    st = _random_state(g, cap, True)
+    target = (g.random(cap) < 0.3).astype(np.uint8)
+    m = int(g.integers(1, min(cap, 300_000) + 2))
+    rows = {"e": g.integers(0, 1 << 40, m).astype(np.int64), "f": (g.random(m) < 0.5).astype(np.uint8)}
+    valid = (g.random(m) < 0.5).astype(np.uint8)
+    ts, vr = np.flatnonzero(target), np.flatnonzero(valid)
+    r = min(ts.size, vr.size)
+    for name in ("rm", "sci"):
+        dev = to_dev(agents, st)
+        before = dev.to_numpy()
+        o = (dev.set_rm if name == "rm" else dev.set_sci)(target, rows, valid)
+        got = dev.to_numpy()
+        assert o.pairs == r, name
+        assert np.array_equal(o.slots, ts[:r]) and np.array_equal(o.rows, vr[:r]), name
+        for k in ("e", "f"):
+            want = before[k].copy()
+            want[ts[:r]] = rows[k][vr[:r]]
+            assert np.array_equal(got[k], want), (name, k)
+        for k in ("w", "active", "ids", "ages", "types", "num_active", "next_id", "retired"):
+            assert np.array_equal(np.asarray(got[k]), np.asarray(before[k])), (name, k)
