@@ -67,6 +67,13 @@ int main() {
     }
     printf("4xSetParams+graph+sync    %7.2f us/iter\n", (now_us() - a) / N);
 
+    a = now_us();
+    for (int i = 0; i < N; ++i) {
+        for (int k = 0; k < 4; ++k) cudaLaunchKernel(reinterpret_cast<void*>(k_touch), dim3(1024), dim3(256), args, 0, s);
+        cudaStreamSynchronize(s);
+    }
+    printf("4 direct launches+sync    %7.2f us/iter\n", (now_us() - a) / N);
+
     long long* h;
     cudaHostAlloc(&h, 4096, cudaHostAllocMapped);
     long long* hd;
