@@ -1,7 +1,8 @@
 // traffic.cu — the three-lane traffic model (src/models/traffic.cpp:47-238) on sm_100a for R
 // roads at once, device-resident state, bit-exact with the reference.
 //
-// A step is three kernels:
+// A step is two kernels (one in a multi-step run, which folds each step's spawn into the next
+// step's k_accept):
 //   k_accept   per column, all three lanes: each car's proposal (traffic.cpp:47-80: forward /
 //              forward-left / forward-right drawn from seed.split(6).split(t).draw(slot); exit
 //              column: exit iff green, no draw) and the conflict winner of its target
@@ -12,15 +13,19 @@
 //              are a function of those of column c+1, F_c : {0,1}^3 -> {0,1}^3 (three 3-bit lane
 //              modes), and the fixed point is the suffix composition F_c ∘ ... ∘ F_{L-1}
 //              (F_{L-1} is constant: exits), a single-pass scan with decoupled lookback from the
-//              road's end. Accepted winners tag the cell they enter (inc words, per epoch).
-//   k_apply    per car slot: accepted moves (set_agents_mask) and exits (remove_agents), the new
-//              occupancy written by the movers themselves (a vacated cell is cleared unless its
-//              inc word carries this epoch's tag), and per-tile first free slots for the spawn.
+//              road's end. Then, in the same kernel, the apply: accepted moves (set_agents_mask,
+//              the mover writes its target's occupancy), exits (remove_agents -> reset_slot,
+//              published as the step's exit record) and vacated cells (cleared unless a winner
+//              enters: decided from the cell's own acceptance and the bids of the column to its
+//              left, re-proposed by the thread as a halo).
 //   k_spawn    per road: spawn_cars (traffic.cpp:143-184): k = uniform_int(0, 0, 4), partial lane
-//              shuffle, entry cells that are free, rank-match into the lowest free slots, fresh ids.
+//              shuffle, entry cells that are free, rank-match into the lowest free slots (a
+//              free-slot bitmap with a summary level and a low-water word, merged with the
+//              step's exits), fresh ids.
 //
 // Layout per road r (capacity 3L slots, 3L cells): active u8, pos i32 (= lane*Lp + cell), ids i64,
-// ages i64; occupancy i32 (slot or -1), inc u32, acc u8 per cell.
+// ages i64; occupancy i32 (slot or -1) per cell; free-slot bitmap u32 [Wb] + summary u32 [Ws];
+// exit records int4 [2] (by epoch parity).
 #include <climits>
 #include <cmath>
 #include <cstdint>
@@ -48,7 +53,7 @@ constexpr int kAcceptMaxNT = ABMX_TRF_NA_MAX;  // k_accept CTA size for long roa
 constexpr unsigned kSlotMask = (1u << 28) - 1;
 constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagPre = 2ULL << 62;
-constexpr int kNumKernels = 3;  // k_accept, k_apply, k_spawn
+constexpr int kNumKernels = 2;  // k_accept (with the apply), k_spawn
 
 enum : int { kStay = -1, kExit = -2 };
 
@@ -69,17 +74,19 @@ struct TParams {
     long long* ids;
     long long* ages;
     int* occ;
-    uint8_t* acc;
     unsigned long long* cstatus;  // [R][ctiles] lookback words
     unsigned* ticket;             // [2]
-    unsigned* inc;                // [R][Cpad] inc_tag(epoch) where an accepted car enters the cell
     int spawn_pending;            // 1: k_accept's column-0 tile first runs the PREVIOUS step's
     long long spawn_t;            //    spawn (step spawn_t, metrics row spawn_row), which a
     unsigned spawn_row;           //    multi-step run folds into the next step (no k_spawn launch)
     int accept_ticketless;        // 1: every k_accept CTA is co-resident (one wave), so the
                                   // lookback needs no ticket order: tile = blockIdx.x
-    int4* tinfo;                  // [R][tiles] {free count, first three free slots}
-    long long* cnt;               // [R][8] num_active, next_id, spawned_total, exited_total, spawned, exited, green
+    unsigned* fbits;              // [R][Wb] free-slot bitmap (bit set: slot free), slots < C
+    unsigned* fsum;               // [R][Ws] summary: bit w & 31 of word w >> 5 set iff fbits[w] != 0
+    int Wb, Ws;
+    int4* exits;                  // [R][2] {count, slot x3} exits of the step of epoch parity [e & 1]
+    long long* cnt;               // [R][8] num_active, next_id, spawned_total, exited_total, spawned,
+                                  // exited, green, low-water bitmap word (every word below is 0)
 };
 
 __device__ __forceinline__ bool green_at(const TParams& P, int r, long long t) {  // SignalSchedule::green
@@ -140,7 +147,8 @@ __device__ __forceinline__ unsigned apply_fn(unsigned f, unsigned v) {  // f(v),
     return out;
 }
 
-__device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, int lane);  // (below)
+__device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, unsigned long long ep,
+                           int lane);  // (below)
 
 template <int NA>
 __global__ void __launch_bounds__(NA) k_accept(TParams P) {
@@ -159,9 +167,11 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __syncthreads();
     const unsigned g = s_tile;
     const int r = static_cast<int>(g / P.ctiles), tau = static_cast<int>(g % P.ctiles);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && P.ctiles > 1 && !P.accept_ticketless)
+        P.ticket[(P.epoch + 1) & 1] = 0u;  // the next step's tickets (this step uses epoch & 1)
     if (P.spawn_pending && tau == P.ctiles - 1) {  // the tile holding column 0: the previous
         if (threadIdx.x < 32)                       // step's spawn first (its entrance cells)
-            spawn_road(P, r, P.spawn_t, P.spawn_row, static_cast<int>(threadIdx.x));
+            spawn_road(P, r, P.spawn_t, P.spawn_row, P.epoch - 1, static_cast<int>(threadIdx.x));
         __syncthreads();
     }
     // tile 0 holds the road's last columns; columns L..Lp-1 are empty padding (-1)
@@ -206,6 +216,22 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
             }
             ox[l][q] = won ? P.occ[cb + X[l][q]] : kStay - 1;
         }
+    // the halo: occupants of column c_lo - 1, read now, before any thread or tile of this step
+    // writes occupancy (lane + 1's column c_lo + 3 of its int4; across warps and tiles a load)
+    int oh[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        oh[l] = __shfl_down_sync(0xffffffffu, o[l][kCI - 1], 1);
+        if ((threadIdx.x & 31) == 31) oh[l] = c_lo > 0 ? P.occ[cb + l * P.Lp + c_lo - 1] : -1;
+    }
+    // bit 3q + l of into (q >= 1; q = 0 after the scan, from the halo): a car of column
+    // c_lo + q - 1 won the bid for (l, c_lo + q)
+    unsigned into = 0;
+#pragma unroll
+    for (int q = 1; q < kCI; ++q)
+#pragma unroll
+        for (int l = 0; l < 3; ++l)
+            if (ox[l][q - 1] != kStay - 1) into |= 1u << (3 * q + X[l][q - 1] / P.Lp);
     unsigned F[kCI];
     unsigned occm = 0;
     unsigned T = kIdentityFn;
@@ -297,179 +323,236 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
             s_vin = vin;
         }
     }
-    __syncthreads();
-    unsigned v = apply_fn(E, s_vin);
+    __syncthreads();  // every thread's occupancy loads are done: the writes below may start
+    // acceptance bits: bit 3q + l of accm = the occupant of (l, c_lo + q) moves (or exits)
+    unsigned v = apply_fn(E, s_vin), accm = 0;
 #pragma unroll
     for (int j = 0; j < kCI; ++j) {
         v = apply_fn(F[j], v);
-        const unsigned m3 = (occm >> (3 * j)) & 7u;
-        if (m3) {
-            const int c = c_lo + kCI - 1 - j;
-            const int q = kCI - 1 - j;
+        accm |= (v & ((occm >> (3 * j)) & 7u)) << (3 * (kCI - 1 - j));
+    }
+    // An accepted occupant's cell is vacated unless a winner of the bid for it enters: that
+    // winner is accepted exactly when the cell's occupant leaves (or the cell is empty), so no
+    // other thread's acceptance is needed. For column c_lo the bidders sit in column c_lo - 1
+    // (the halo: the next thread's or tile's), re-proposed here.
+    if (accm & 7u) {  // column c_lo has a leaving car: its halo bids decide the vacate
+        int xh[3];
 #pragma unroll
-            for (int l = 0; l < 3; ++l)
-                if (m3 & (1u << l)) {
-                    const unsigned a = (v >> l) & 1u;
-                    P.acc[cb + l * P.Lp + c] = static_cast<uint8_t>(a);
-                    if (a && X[l][q] >= 0) P.inc[cb + X[l][q]] = inc_tag(P.epoch);  // the winner enters
-                }
+        for (int l = 0; l < 3; ++l) xh[l] = oh[l] >= 0 ? proposal(P, oh[l], l * P.Lp + c_lo - 1, green, key) : kStay;
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            if (xh[l] < 0) continue;
+            const int tl = xh[l] / P.Lp;
+            const int pr = l == tl ? 0 : (l == tl - 1 ? 1 : 2);
+            bool won = true;
+#pragma unroll
+            for (int l2 = 0; l2 < 3; ++l2)
+                if (l2 != l && xh[l2] == xh[l] && (l2 == tl ? 0 : (l2 == tl - 1 ? 1 : 2)) < pr) won = false;
+            if (won) into |= 1u << tl;
         }
     }
-}
-
-// ---------------------------------------------------------------- k_apply
-// Clear the occupancy of vacated cell p unless an accepted winner enters it this step.
-__device__ __forceinline__ void vacate(const TParams& P, size_t cb, int p) {
-    if (P.inc[cb + p] == inc_tag(P.epoch)) return;  // the accepted winner writes occ[p]
-    P.occ[cb + p] = -1;
-}
-
-template <int NT>
-__global__ void __launch_bounds__(NT) k_apply(TParams P) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) P.ticket[(P.epoch + 1) & 1] = 0u;  // the next k_accept's tickets
-    __shared__ unsigned long long s_scan[NT / 32 + 1];
-    __shared__ int s_first[3];
-    __shared__ unsigned s_exit[NT / 32];
-    const int r = blockIdx.x / P.tiles, tile = blockIdx.x % P.tiles;
-    __shared__ unsigned long long s_key;
-    __shared__ int s_green;
-    if (threadIdx.x == 0) {  // the road's light and propose key, once per CTA
-        s_green = green_of(P, r);
-        s_key = propose_key(P, r);
-    }
-    __syncthreads();
-    const bool green = s_green != 0;
-    const unsigned long long key = s_key;
-    const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
-    const int i0 = tile * NT * kS + threadIdx.x * kS;  // blocked: free-slot order = slot order
-    unsigned exited = 0, nf = 0;
-    bool fr[kS];
+    // apply (traffic.cpp:186-238): accepted moves (set_agents_mask: lane / cell <- target, the
+    // mover writes its target's occupancy), exits (remove_agents -> reset_slot), vacated cells
+    const size_t sb = static_cast<size_t>(r) * P.Npad;
+    int4 ex = make_int4(0, -1, -1, -1);
 #pragma unroll
-    for (int k = 0; k < kS; ++k) {
-        const int i = i0 + k;
-        fr[k] = false;
-        if (i >= P.C) continue;
-        if (P.active[sb + i]) {
-            const int p = P.pos[sb + i];
-            if (P.acc[cb + p]) {
-                const int X = proposal(P, i, p, green, key);
-                if (X == kExit) {  // remove_agents -> reset_slot (agent_set.cpp:45-58)
-                    P.active[sb + i] = 0;
-                    P.ids[sb + i] = 0;
-                    P.ages[sb + i] = 0;
-                    P.pos[sb + i] = 0;
-                    ++exited;
-                    fr[k] = true;
-                } else {  // set_agents_mask: lane / cell <- target
-                    P.pos[sb + i] = X;
-                    P.occ[cb + X] = i;
-                }
-                vacate(P, cb, p);
+    for (int q = 0; q < kCI; ++q)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) {
+            if (!((accm >> (3 * q + l)) & 1u)) continue;
+            const int i = o[l][q];
+            if (X[l][q] == kExit) {  // reset_slot (agent_set.cpp:45-58)
+                P.active[sb + i] = 0;
+                P.ids[sb + i] = 0;
+                P.ages[sb + i] = 0;
+                P.pos[sb + i] = 0;
+                if (ex.x == 0)
+                    ex.y = i;
+                else if (ex.x == 1)
+                    ex.z = i;
+                else
+                    ex.w = i;
+                ++ex.x;
+            } else {
+                P.pos[sb + i] = X[l][q];
+                P.occ[cb + X[l][q]] = i;
             }
-        } else {
-            fr[k] = true;
+            if (!((into >> (3 * q + l)) & 1u)) P.occ[cb + l * P.Lp + c_lo + q] = -1;
         }
-        nf += fr[k];
-    }
-    unsigned long long tot;
-    const unsigned long long ex = block_excl_scan<NT>(nf, s_scan, &tot);
-    if (threadIdx.x < 3) s_first[threadIdx.x] = -1;
-    __syncthreads();
-    unsigned rank = static_cast<unsigned>(ex);
-#pragma unroll
-    for (int k = 0; k < kS; ++k)
-        if (fr[k]) {
-            if (rank < 3) s_first[rank] = i0 + k;
-            ++rank;
-        }
-    const unsigned e = __reduce_add_sync(0xffffffffu, exited);
-    if ((threadIdx.x & 31) == 0) s_exit[threadIdx.x >> 5] = e;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned ex_sum = 0;
-        for (int w = 0; w < NT / 32; ++w) ex_sum += s_exit[w];
-        if (ex_sum) atomicAdd(reinterpret_cast<unsigned long long*>(&P.cnt[static_cast<size_t>(r) * 8 + 5]), ex_sum);
-        P.tinfo[static_cast<size_t>(r) * P.tiles + tile] =
-            make_int4(static_cast<int>(tot), s_first[0], s_first[1], s_first[2]);
-    }
+    // the exit column's thread publishes the step's exits (read by this step's spawn)
+    if (c_lo <= P.L - 1 && P.L - 1 < c_lo + kCI) P.exits[static_cast<size_t>(r) * 2 + (P.epoch & 1)] = ex;
 }
 
 // ---------------------------------------------------------------- k_spawn
-// One warp per road: spawn_cars (traffic.cpp:143-184), counters and the metrics row.
-// spawn_cars of step t on road r, one warp (lane = 0..31); metrics row `row`
-__device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, int lane) {
+// spawn_cars of step t on road r (traffic.cpp:143-184), one warp (lane = 0..31); metrics row
+// `row`; ep = the step's epoch (its exit record). The lowest free slots come from the road's
+// free-slot bitmap, searched from the low-water word cnt[7] (every word below it is full), merged
+// with the step's exits (which become free only now, after the step's moves).
+__device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, unsigned long long ep, int lane) {
     const size_t sb = static_cast<size_t>(r) * P.Npad, cb = static_cast<size_t>(r) * P.Cpad;
     long long* cn = P.cnt + static_cast<size_t>(r) * 8;
-    // every load the spawn needs that does not depend on the draws, issued together: the seed,
-    // the three entrance cells, the first 32 tiles' free-slot info, the counters
+    unsigned* fb = P.fbits + static_cast<size_t>(r) * P.Wb;
+    unsigned* fs = P.fsum + static_cast<size_t>(r) * P.Ws;
+    // every load that does not depend on the draws, issued together: the seed, the three
+    // entrance cells, the exit record, the counters
     const unsigned long long seed = P.seeds[r];
     const int occ_in[3] = {P.occ[cb], P.occ[cb + P.Lp], P.occ[cb + 2 * static_cast<size_t>(P.Lp)]};
-    int4 ti0 = lane < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + lane] : make_int4(0, -1, -1, -1);
-    const long long nid = cn[1], exited = cn[5], c0 = cn[0], c2 = cn[2], c3 = cn[3];
+    const int4 ex = P.exits[static_cast<size_t>(r) * 2 + (ep & 1)];
+    const long long nid = cn[1], c0 = cn[0], c2 = cn[2], c3 = cn[3];
+    const int lw = static_cast<int>(cn[7]);
     const bool g = green_at(P, r, t);
-    // rows (lane 0): k attempts, partial shuffle, free entry cells
-    int rows[3] = {-1, -1, -1};
+    // rows: k attempts, partial shuffle, free entry cells. Lane lists are 2-bit fields of one
+    // word (static register indexing: a per-thread array with runtime indices lives in local memory)
+    unsigned rowsw = 0;  // row q (entry lane) in bits 2q..2q+1
     int nvalid = 0;
     {
         const unsigned long long key = split(split(seed, 7), static_cast<unsigned long long>(t));
         const int k = static_cast<int>(uniform_span(key, 0, 4));
-        int lanes[3] = {0, 1, 2};
-        for (int i = 0; i < (k < 2 ? k : 2); ++i) {
+        unsigned lanesw = 0u | (1u << 2) | (2u << 4);  // lanes[i] in bits 2i..2i+1
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            if (i >= k) break;
             const int j = i + static_cast<int>(uniform_span(key, static_cast<unsigned long long>(1 + i),
                                                             static_cast<unsigned long long>(3 - i)));
-            const int tmp = lanes[i];
-            lanes[i] = lanes[j];
-            lanes[j] = tmp;
+            const unsigned li = (lanesw >> (2 * i)) & 3u, lj = (lanesw >> (2 * j)) & 3u;
+            lanesw = (lanesw & ~(3u << (2 * i)) & ~(3u << (2 * j))) | (lj << (2 * i)) | (li << (2 * j));
         }
-        for (int q = 0; q < (k < 3 ? k : 3); ++q)
-            if (occ_in[lanes[q]] < 0) rows[nvalid++] = lanes[q];
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (q >= k) break;
+            const unsigned ln = (lanesw >> (2 * q)) & 3u;
+            if ((ln == 0 ? occ_in[0] : (ln == 1 ? occ_in[1] : occ_in[2])) < 0) {
+                rowsw |= ln << (2 * nvalid);
+                ++nvalid;
+            }
+        }
     }
-    // the lowest nvalid free slots, tiles in order (warp-parallel over tile chunks)
-    int slots[3] = {-1, -1, -1};
-    int nf = 0;
-    for (int t0 = 0; t0 < P.tiles && nf < nvalid; t0 += 32) {
-        const int t = t0 + lane;
-        const int4 ti = t0 == 0 ? ti0
-                                : (t < P.tiles ? P.tinfo[static_cast<size_t>(r) * P.tiles + t] : make_int4(0, -1, -1, -1));
-        unsigned m = __ballot_sync(0xffffffffu, ti.x > 0);
-        while (m && nf < nvalid) {
-            const int src = __ffs(m) - 1;
-            m &= m - 1;
-            const int cnt = __shfl_sync(0xffffffffu, ti.x, src);
-            const int f0 = __shfl_sync(0xffffffffu, ti.y, src);
-            const int f1 = __shfl_sync(0xffffffffu, ti.z, src);
-            const int f2 = __shfl_sync(0xffffffffu, ti.w, src);
-            const int fs[3] = {f0, f1, f2};
-            for (int q = 0; q < cnt && q < 3 && nf < nvalid; ++q) slots[nf++] = fs[q];
+    // the lowest nvalid free slots of the bitmap (warp-uniform), windows of 32 words aligned to
+    // summary words; an empty window jumps ahead through the summary. Absent entries: INT_MAX.
+    int f0 = INT_MAX, f1 = INT_MAX, f2 = INT_MAX;
+    unsigned fw0 = 0u, fw1 = 0u, fw2 = 0u;  // each found slot's bitmap word as loaded
+    int nfb = 0;
+    for (int w0 = lw & ~31; nfb < nvalid && w0 < P.Wb;) {
+        const unsigned word = w0 + lane < P.Wb ? fb[w0 + lane] : 0u;
+        unsigned m = __ballot_sync(0xffffffffu, word != 0u);
+        if (!m) {  // the next non-empty summary word after this window
+            int next = -1;
+            for (int sw0 = (w0 >> 5) + 1; sw0 < P.Ws && next < 0; sw0 += 32) {
+                const unsigned sw = sw0 + lane < P.Ws ? fs[sw0 + lane] : 0u;
+                const unsigned sm = __ballot_sync(0xffffffffu, sw != 0u);
+                if (sm) next = sw0 + __ffs(static_cast<int>(sm)) - 1;
+            }
+            if (next < 0) break;  // no free slot in the bitmap
+            w0 = next << 5;
+            continue;
         }
+        while (m && nfb < nvalid) {
+            const int src = __ffs(static_cast<int>(m)) - 1;
+            m &= m - 1;
+            const unsigned wd0 = __shfl_sync(0xffffffffu, word, src);
+            for (unsigned wd = wd0; wd && nfb < nvalid; wd &= wd - 1) {
+                const int sl = ((w0 + src) << 5) + __ffs(static_cast<int>(wd)) - 1;
+                if (nfb == 0) {
+                    f0 = sl;
+                    fw0 = wd0;
+                } else if (nfb == 1) {
+                    f1 = sl;
+                    fw1 = wd0;
+                } else {
+                    f2 = sl;
+                    fw2 = wd0;
+                }
+                ++nfb;
+            }
+        }
+        w0 += 32;
     }
     if (lane == 0) {
-        const int spawned = nf < nvalid ? nf : nvalid;
-        for (int q = 0; q < spawned; ++q) {
-            const int s = slots[q];
-            P.active[sb + s] = 1;
-            P.pos[sb + s] = rows[q] * P.Lp;
-            P.ids[sb + s] = nid + q;
-            P.ages[sb + s] = 0;
-            P.occ[cb + rows[q] * P.Lp] = s;
+        // the step's exits are free too (sorted here, INT_MAX when absent): the spawned slots are
+        // the lowest nvalid of both lists, the q-th lowest taking row q
+        const int ne = ex.x;
+        int e0 = ne > 0 ? ex.y : INT_MAX, e1 = ne > 1 ? ex.z : INT_MAX, e2 = ne > 2 ? ex.w : INT_MAX;
+        auto cswap = [](int& a, int& b) {
+            const int lo = a < b ? a : b, hi = a < b ? b : a;
+            a = lo;
+            b = hi;
+        };
+        cswap(e0, e1);
+        cswap(e1, e2);
+        cswap(e0, e1);
+        const int fl[3] = {f0, f1, f2}, el[3] = {e0, e1, e2};
+        const unsigned fwl[3] = {fw0, fw1, fw2};
+        int frank[3], erank[3];  // rank in the union (slots are distinct), >= 6 when absent
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            int rf = k, re = k;
+#pragma unroll
+            for (int k2 = 0; k2 < 3; ++k2) {
+                rf += el[k2] < fl[k];
+                re += fl[k2] < el[k];
+            }
+            frank[k] = fl[k] == INT_MAX ? 6 : rf;
+            erank[k] = el[k] == INT_MAX ? 6 : re;
         }
+        const int spawned = nvalid < nfb + ne ? nvalid : nfb + ne;
+        // bitmap: exits not taken become free, slots taken from it leave it; a summary bit is
+        // cleared when its word empties. Every word below the first found one was full, and the
+        // kept exits may lie lower: the new low-water word
+        int lw_new = nfb > 0 ? (f0 >> 5) : lw;
+#pragma unroll
+        for (int u = 0; u < 3; ++u) {
+            if (el[u] == INT_MAX || erank[u] < spawned) continue;
+            const int w = el[u] >> 5;
+            atomicOr(&fb[w], 1u << (el[u] & 31));
+            atomicOr(&fs[w >> 5], 1u << (w & 31));
+            lw_new = w < lw_new ? w : lw_new;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (frank[k] >= spawned) continue;
+            const int w = fl[k] >> 5;
+            atomicAnd(&fb[w], ~(1u << (fl[k] & 31)));
+            unsigned fin = fwl[k];  // the word after this spawn
+#pragma unroll
+            for (int k2 = 0; k2 < 3; ++k2)
+                if (frank[k2] < spawned && (fl[k2] >> 5) == w) fin &= ~(1u << (fl[k2] & 31));
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (el[u] != INT_MAX && erank[u] >= spawned && (el[u] >> 5) == w) fin |= 1u << (el[u] & 31);
+            if (fin == 0u) atomicAnd(&fs[w >> 5], ~(1u << (w & 31)));
+        }
+        // the new cars: the q-th lowest slot takes row q (entry lane), id next_id + q
+#pragma unroll
+        for (int k = 0; k < 6; ++k) {
+            const int rk = k < 3 ? frank[k] : erank[k - 3];
+            if (rk >= spawned) continue;
+            const int sl = k < 3 ? fl[k] : el[k - 3];
+            const int ln = static_cast<int>((rowsw >> (2 * rk)) & 3u);
+            P.active[sb + sl] = 1;
+            P.pos[sb + sl] = ln * P.Lp;
+            P.ids[sb + sl] = nid + rk;
+            P.ages[sb + sl] = 0;
+            P.occ[cb + ln * P.Lp] = sl;
+        }
+        const int exited = ne;
         const long long n_cars = c0 + spawned - exited;
         cn[0] = n_cars;
         cn[1] = nid + spawned;
         cn[2] = c2 + spawned;
         cn[3] = c3 + exited;
         cn[4] = spawned;
+        cn[5] = exited;
         cn[6] = g ? 1 : 0;
+        cn[7] = lw_new;
         double* mrow = P.metrics + (static_cast<size_t>(r) * P.metrics_stride + row) * 4;
         mrow[0] = static_cast<double>(n_cars);
         mrow[1] = static_cast<double>(spawned);
         mrow[2] = static_cast<double>(exited);
         mrow[3] = g ? 1.0 : 0.0;
-        cn[5] = 0;  // exits of the next step accumulate from zero
     }
 }
 
-__global__ void k_spawn(TParams P) { spawn_road(P, blockIdx.x, P.t, P.run_step, threadIdx.x); }
+__global__ void k_spawn(TParams P) { spawn_road(P, blockIdx.x, P.t, P.run_step, P.epoch, threadIdx.x); }
 
 // the bench's L2 flush: after the memset of a buffer larger than L2, read it back so L2 holds
 // clean lines (as the predation bench): the timed step pays no write-backs of the flush buffer
@@ -530,11 +613,23 @@ __global__ void k_init(TParams P) {
             P.ids[q] = 0;
             P.ages[q] = 0;
         }
-        if (q < nc) {
-            P.occ[q] = -1;
-            P.inc[q] = 0u;
-            P.acc[q] = 0;
+        if (q < nc) P.occ[q] = -1;
+    }
+    const size_t nw = static_cast<size_t>(P.R) * P.Wb, nsw = static_cast<size_t>(P.R) * P.Ws;
+    for (size_t q = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; q < (nw > nsw ? nw : nsw);
+         q += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        if (q < nw) {  // every slot < C free
+            const long long s0 = static_cast<long long>(q % P.Wb) * 32;
+            const long long nfree = P.C - s0 < 0 ? 0 : (P.C - s0 > 32 ? 32 : P.C - s0);
+            P.fbits[q] = nfree >= 32 ? 0xFFFFFFFFu : ((1u << nfree) - 1u);
         }
+        if (q < nsw) {
+            const long long w0 = static_cast<long long>(q % P.Ws) * 32;  // words w0.. of this summary word
+            const long long nonempty_words = (P.C + 31) / 32 - w0;       // words holding a slot < C
+            const long long k = nonempty_words < 0 ? 0 : (nonempty_words > 32 ? 32 : nonempty_words);
+            P.fsum[q] = k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u);
+        }
+        if (q < static_cast<size_t>(P.R) * 2) P.exits[q] = make_int4(0, -1, -1, -1);
     }
 }
 
@@ -592,15 +687,13 @@ struct abmx_traffic {
         allocs.push_back(*p);
         return ABMX_OK;
     }
-    unsigned grid(int k) const {  // k: 0 k_accept, 1 k_apply, 2 k_spawn
-        if (k == 0) return static_cast<unsigned>(R * P.ctiles);
-        if (k == 2) return static_cast<unsigned>(R);
-        return static_cast<unsigned>(R * P.tiles);
+    unsigned grid(int k) const {  // k: 0 k_accept, 1 k_spawn
+        return static_cast<unsigned>(k == 0 ? R * P.ctiles : R);
     }
     int nt = 256, na = 1024;  // CTA sizes of the slot kernels and of k_accept
     void* fns[kNumKernels] = {};
     unsigned block(int k) const {
-        return k == 2 ? 32u : static_cast<unsigned>(k == 0 ? na : nt);
+        return k == 1 ? 32u : static_cast<unsigned>(na);
     }
     void* fn(int k) const { return fns[k]; }
     void pick_kernels() {
@@ -610,12 +703,6 @@ struct abmx_traffic {
         // k_accept: the smallest CTA covering a road's columns, else 1024 threads (few tiles)
         na = 32;
         while (na < kAcceptMaxNT && na * kCI < P.Lp) na *= 2;
-        switch (nt) {
-            case 32: fns[1] = reinterpret_cast<void*>(k_apply<32>); break;
-            case 64: fns[1] = reinterpret_cast<void*>(k_apply<64>); break;
-            case 128: fns[1] = reinterpret_cast<void*>(k_apply<128>); break;
-            default: fns[1] = reinterpret_cast<void*>(k_apply<256>); break;
-        }
         switch (na) {
             case 32: fns[0] = reinterpret_cast<void*>(k_accept<32>); break;
             case 64: fns[0] = reinterpret_cast<void*>(k_accept<64>); break;
@@ -624,7 +711,7 @@ struct abmx_traffic {
             case 512: fns[0] = reinterpret_cast<void*>(k_accept<512>); break;
             default: fns[0] = reinterpret_cast<void*>(k_accept<1024>); break;
         }
-        fns[2] = reinterpret_cast<void*>(k_spawn);
+        fns[1] = reinterpret_cast<void*>(k_spawn);
     }
 
     int create(const abmx_traffic_config& c, const uint64_t* seeds, int roads) {
@@ -658,6 +745,8 @@ struct abmx_traffic {
         P.tile_cols = na * kCI;
         P.Npad = (P.C + P.tile_slots - 1) / P.tile_slots * P.tile_slots;
         P.tiles = P.Npad / P.tile_slots;
+        P.Wb = P.Npad / 32;  // Npad is a multiple of tile_slots >= 128
+        P.Ws = (P.Wb + 31) / 32;
         P.ctiles = (P.Lp + P.tile_cols - 1) / P.tile_cols;
         {
             int per_sm = 0;  // k_accept CTAs resident per SM
@@ -679,11 +768,11 @@ struct abmx_traffic {
         ALT(P.ids, ns * 8);
         ALT(P.ages, ns * 8);
         ALT(P.occ, nc * 4);
-        ALT(P.inc, nc * 4);
-        ALT(P.acc, nc);
         ALT(P.cstatus, static_cast<size_t>(R) * P.ctiles * 8);
         ALT(P.ticket, 16);
-        ALT(P.tinfo, static_cast<size_t>(R) * P.tiles * sizeof(int4));
+        ALT(P.fbits, static_cast<size_t>(R) * P.Wb * 4);
+        ALT(P.fsum, static_cast<size_t>(R) * P.Ws * 4);
+        ALT(P.exits, static_cast<size_t>(R) * 2 * sizeof(int4));
         ALT(P.cnt, static_cast<size_t>(R) * 8 * 8);
         long long* phase = nullptr;
         unsigned long long* sd = nullptr;
@@ -717,14 +806,14 @@ struct abmx_traffic {
         return ABMX_OK;
     }
 
-    // the folded step of a multi-step run: [k_accept (+ the previous step's spawn), k_apply]
+    // the folded step of a multi-step run: k_accept (+ the previous step's spawn), one kernel
     cudaGraph_t graph2 = nullptr;
     cudaGraphExec_t exec2 = nullptr;
-    cudaGraphNode_t nodes2[2] = {};
+    cudaGraphNode_t nodes2[1] = {};
     int build_graph2() {
         CKT(cudaGraphCreate(&graph2, 0));
         void* args[1] = {&P};
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 1; ++k) {
             cudaKernelNodeParams kp{};
             kp.func = fn(k);
             kp.gridDim = dim3(grid(k));
@@ -746,7 +835,7 @@ struct abmx_traffic {
             if (rc) return rc;
         }
         void* args[1] = {&P};
-        for (int k = 0; k < 2; ++k) {
+        for (int k = 0; k < 1; ++k) {
             cudaKernelNodeParams kp{};
             kp.func = fn(k);
             kp.gridDim = dim3(grid(k));
@@ -756,7 +845,7 @@ struct abmx_traffic {
         }
         CKT(cudaGraphLaunch(exec2, stream));
         P.spawn_pending = 0;
-        abmx_internal::count_launch(2);
+        abmx_internal::count_launch(1);
         ++host_epoch;
         ++P.t;
         ++P.run_step;
@@ -769,7 +858,7 @@ struct abmx_traffic {
         Q.run_step = P.run_step - 1;
         Q.epoch = host_epoch - 1;
         void* args[1] = {&Q};
-        CKT(cudaLaunchKernel(fn(2), dim3(grid(2)), dim3(block(2)), args, 0, stream));
+        CKT(cudaLaunchKernel(fn(1), dim3(grid(1)), dim3(block(1)), args, 0, stream));
         abmx_internal::count_launch(1);
         return ABMX_OK;
     }
@@ -950,7 +1039,18 @@ struct abmx_traffic {
         cn[0] = na;
         cn[1] = next_id;
         cn[5] = 0;
+        cn[7] = 0;  // low-water bitmap word
         CKT(cudaMemcpy(P.cnt + static_cast<size_t>(r) * 8, cn, 64, cudaMemcpyHostToDevice));
+        // the road's free-slot bitmap and summary from the imported active flags; no exits pending
+        std::vector<unsigned> fbw(static_cast<size_t>(P.Wb), 0u), fsw(static_cast<size_t>(P.Ws), 0u);
+        for (size_t i = 0; i < n; ++i)
+            if (!act[i]) fbw[i >> 5] |= 1u << (i & 31);
+        for (int w = 0; w < P.Wb; ++w)
+            if (fbw[static_cast<size_t>(w)]) fsw[static_cast<size_t>(w >> 5)] |= 1u << (w & 31);
+        CKT(cudaMemcpy(P.fbits + static_cast<size_t>(r) * P.Wb, fbw.data(), fbw.size() * 4, cudaMemcpyHostToDevice));
+        CKT(cudaMemcpy(P.fsum + static_cast<size_t>(r) * P.Ws, fsw.data(), fsw.size() * 4, cudaMemcpyHostToDevice));
+        const int4 none[2] = {make_int4(0, -1, -1, -1), make_int4(0, -1, -1, -1)};
+        CKT(cudaMemcpy(P.exits + static_cast<size_t>(r) * 2, none, sizeof none, cudaMemcpyHostToDevice));
         return ABMX_OK;
     }
 
@@ -1009,7 +1109,7 @@ struct abmx_traffic {
 };
 
 namespace {
-const char* kTrafficKernels[kNumKernels] = {"k_accept", "k_apply", "k_spawn"};
+const char* kTrafficKernels[kNumKernels] = {"k_accept", "k_spawn"};
 
 int resolve_host(int64_t length, const uint8_t* active, const int64_t* lane, const int64_t* cell, const uint8_t* kind,
                  const int64_t* to_lane, const int64_t* to_cell, uint8_t* accepted) {
