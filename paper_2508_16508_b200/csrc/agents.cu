@@ -521,6 +521,7 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     }
     const unsigned long long at_ta = s_pref[ta];
     const unsigned long long K = hi31(at_ta), F = lo31(at_ta), Q = lo31(s_pref[G]) - F;
+    ABMX_ASSERT(G <= static_cast<unsigned>(kCoopMaxTiles) && F <= n && K <= F && Q <= m);
     const long long r = static_cast<long long>(F < Q ? F : Q);
     const long long live0 = s_cnt[0], nid = s_cnt[1], top0 = s_cnt[2];
     const long long top = top0 + (L.recycle ? static_cast<long long>(K) : 0);  // after the pushes
@@ -568,13 +569,16 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
             const long long q = q0 + j;
             const int row = s_rows[j];
             const unsigned t = tile_of_rank<false>(s_pref, ta, static_cast<unsigned long long>(q));
+            ABMX_ASSERT(t < ta && q >= lo31(s_pref[t]) && q < lo31(s_pref[t + 1]) && q < r);
             const int slot = free_list[static_cast<size_t>(t) * kTile + (q - lo31(s_pref[t]))];
+            ABMX_ASSERT(slot >= 0 && static_cast<size_t>(slot) < n && static_cast<size_t>(row) < m);
             long long id = nid + (q - top);
             if (!rm && q < top) {
                 const long long e = top - 1 - q;  // stack entry popped
                 if (e >= top0) {                  // pushed this cycle: killed id of kill rank e - top0
                     const unsigned long long j = static_cast<unsigned long long>(e - top0);
                     const unsigned t2 = tile_of_rank<true>(s_pref, ta, j);
+                    ABMX_ASSERT(t2 < ta && j >= hi31(s_pref[t2]) && j < hi31(s_pref[t2 + 1]));
                     id = kill_ids[static_cast<size_t>(t2) * kTile + (j - hi31(s_pref[t2]))];
                 } else {
                     id = L.retired[e];

@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         for (int l = 0; l < 3; ++l) {
             if (!((accm >> (3 * q + l)) & 1u)) continue;
             const int i = o[l][q];
+            ABMX_ASSERT(i >= 0 && i < P.C && (X[l][q] == kExit || (X[l][q] >= 0 && X[l][q] < 3 * P.Lp)));
             if (X[l][q] == kExit) {  // reset_slot (agent_set.cpp:45-58)
                 P.active[sb + i] = 0;
                 P.ids[sb + i] = 0;
@@ -520,6 +521,7 @@ __device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, u
             for (int u = 0; u < 3; ++u)
                 if (el[u] != INT_MAX && erank[u] >= spawned && (el[u] >> 5) == w) fin |= 1u << (el[u] & 31);
             if (fin == 0u) atomicAnd(&fs[w >> 5], ~(1u << (w & 31)));
+            ABMX_ASSERT(w < P.Wb && (fwl[k] >> (fl[k] & 31)) & 1u);
         }
         // the new cars: the q-th lowest slot takes row q (entry lane), id next_id + q
 #pragma unroll
@@ -528,6 +530,7 @@ __device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, u
             if (rk >= spawned) continue;
             const int sl = k < 3 ? fl[k] : el[k - 3];
             const int ln = static_cast<int>((rowsw >> (2 * rk)) & 3u);
+            ABMX_ASSERT(sl >= 0 && sl < P.C && ln < 3);
             P.active[sb + sl] = 1;
             P.pos[sb + sl] = ln * P.Lp;
             P.ids[sb + sl] = nid + rk;
