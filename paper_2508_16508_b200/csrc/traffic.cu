@@ -106,6 +106,23 @@ __device__ __forceinline__ int proposal(const TParams& P, int slot, int p, bool 
     const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
     return tl * P.Lp + cell + 1;
 }
+// the same with the lane and cell known (no division)
+__device__ __forceinline__ int proposal_lc(const TParams& P, int slot, int lane, int cell, bool green,
+                                          unsigned long long key) {
+    if (cell == P.L - 1) return green ? kExit : kStay;
+    const int n = 1 + (lane > 0) + (lane < 2);
+    const int pick = static_cast<int>(uniform_span(key, static_cast<unsigned long long>(slot), static_cast<unsigned long long>(n)));
+    const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
+    return tl * P.Lp + cell + 1;
+}
+// a[k % 3][k / 3] for a runtime k < 12, by selects (a per-thread array indexed at run time would
+// live in local memory)
+__device__ __forceinline__ int pick12(const int (&a)[3][4], int k) {
+    int v = a[0][0];
+#pragma unroll
+    for (int kk = 1; kk < 12; ++kk) v = k == kk ? a[kk % 3][kk / 3] : v;
+    return v;
+}
 // tag of an accepted entry into a cell this epoch (never 0, the initial word)
 __device__ __forceinline__ unsigned inc_tag(unsigned long long epoch) {
     return 0x80000000u | static_cast<unsigned>(epoch & 0x7FFFFFFFULL);
@@ -150,6 +167,27 @@ __device__ __forceinline__ unsigned apply_fn(unsigned f, unsigned v) {  // f(v),
 __device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, unsigned long long ep,
                            int lane);  // (below)
 
+#ifdef ABMX_TRF_TRACE  // per-CTA %globaltimer stamps of k_accept (thread 0): start, occupants
+                       // used, targets used, block scan, lookback, end
+__device__ unsigned long long g_trf_trace[4096][8];
+__device__ unsigned long long g_trf_warp[32][4];  // the last tile: per warp, lane 0: occupants, targets, maps
+#define TRF_WSTAMP(k)                                                                   \
+    if ((threadIdx.x & 31) == 0 && blockIdx.x == gridDim.x - 1) {                      \
+        unsigned long long t_;                                                          \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+        g_trf_warp[threadIdx.x >> 5][k] = t_;                                           \
+    }
+#define TRF_STAMP(k)                                                           \
+    if (threadIdx.x == 0) {                                                    \
+        unsigned long long t_;                                                 \
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+        if (blockIdx.x < 4096) g_trf_trace[blockIdx.x][k] = t_;                \
+    }
+#else
+#define TRF_STAMP(k)
+#define TRF_WSTAMP(k)
+#endif
+
 template <int NA>
 __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __shared__ unsigned s_tile;
@@ -157,6 +195,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     __shared__ unsigned s_vin;
     __shared__ unsigned long long s_key;
     __shared__ int s_green;
+    TRF_STAMP(0);
     // tiles of one road depend on their right neighbours: ticket order guarantees progress
     if (threadIdx.x == 0) {
         s_tile = P.ctiles > 1 && !P.accept_ticketless ? atomicAdd(&P.ticket[P.epoch & 1], 1u) : blockIdx.x;
@@ -200,7 +239,9 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     for (int l = 0; l < 3; ++l)
 #pragma unroll
         for (int q = 0; q < kCI; ++q)
-            X[l][q] = o[l][q] >= 0 ? proposal(P, o[l][q], l * P.Lp + c_lo + q, green, key) : kStay;
+            X[l][q] = o[l][q] >= 0 ? proposal_lc(P, o[l][q], l, c_lo + q, green, key) : kStay;
+    TRF_STAMP(1);
+    TRF_WSTAMP(0);
     int ox[3][kCI];  // occupant of the target if this car won it, else kStay - 1 (lost / no move)
 #pragma unroll
     for (int q = 0; q < kCI; ++q)
@@ -234,6 +275,8 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
             if (ox[l][q - 1] != kStay - 1) into |= 1u << (3 * q + X[l][q - 1] / P.Lp);
     unsigned F[kCI];
     unsigned occm = 0;
+    TRF_STAMP(2);
+    TRF_WSTAMP(1);
     unsigned T = kIdentityFn;
 #pragma unroll
     for (int j = 0; j < kCI; ++j) {  // j = 0 is the rightmost column of this thread
@@ -258,6 +301,8 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         F[j] = f;
         T = compose(f, T);
     }
+    TRF_STAMP(6);
+    TRF_WSTAMP(2);
     // block scan over threads (thread 0 = rightmost): I_t = T_t ∘ I_{t-1}
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     unsigned I = T;
@@ -268,6 +313,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     }
     if (lane == 31) s_warp[warp] = I;
     __syncthreads();
+    TRF_STAMP(7);
     if (warp == 0) {
         unsigned wv = lane < NA / 32 ? s_warp[lane] : kIdentityFn;
 #pragma unroll
@@ -281,6 +327,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     const unsigned wex = warp > 0 ? s_warp[warp - 1] : kIdentityFn;
     const unsigned up = __shfl_up_sync(0xffffffffu, I, 1);
     const unsigned E = lane > 0 ? compose(up, wex) : wex;  // exclusive prefix of this thread
+    TRF_STAMP(3);
     if (warp == 0) {  // decoupled lookback, 32 predecessors per round
         const unsigned A = s_warp[NA / 32 - 1];  // tile aggregate
         unsigned long long* st = P.cstatus + static_cast<size_t>(r) * P.ctiles;
@@ -324,6 +371,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         }
     }
     __syncthreads();  // every thread's occupancy loads are done: the writes below may start
+    TRF_STAMP(4);
     // acceptance bits: bit 3q + l of accm = the occupant of (l, c_lo + q) moves (or exits)
     unsigned v = apply_fn(E, s_vin), accm = 0;
 #pragma unroll
@@ -334,11 +382,24 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     // An accepted occupant's cell is vacated unless a winner of the bid for it enters: that
     // winner is accepted exactly when the cell's occupant leaves (or the cell is empty), so no
     // other thread's acceptance is needed. For column c_lo the bidders sit in column c_lo - 1
-    // (the halo: the next thread's or tile's), re-proposed here.
+    // (the halo: the next thread's or tile's), re-proposed here. The code from here on is kept
+    // small and rolled: it runs once per thread, usually for no car at all, and after the
+    // bench's L2 flush every instruction line of it is fetched cold (traced: 19.6 KB of
+    // unrolled tail cost every tile ~4.7 us, warm 1.3 us).
     if (accm & 7u) {  // column c_lo has a leaving car: its halo bids decide the vacate
-        int xh[3];
-#pragma unroll
-        for (int l = 0; l < 3; ++l) xh[l] = oh[l] >= 0 ? proposal(P, oh[l], l * P.Lp + c_lo - 1, green, key) : kStay;
+        int xh0 = kStay, xh1 = kStay, xh2 = kStay;
+#pragma unroll 1
+        for (int l = 0; l < 3; ++l) {
+            const int ohl = l == 0 ? oh[0] : (l == 1 ? oh[1] : oh[2]);
+            const int x = ohl >= 0 ? proposal_lc(P, ohl, l, c_lo - 1, green, key) : kStay;
+            if (l == 0)
+                xh0 = x;
+            else if (l == 1)
+                xh1 = x;
+            else
+                xh2 = x;
+        }
+        const int xh[3] = {xh0, xh1, xh2};
 #pragma unroll
         for (int l = 0; l < 3; ++l) {
             if (xh[l] < 0) continue;
@@ -355,33 +416,32 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     // mover writes its target's occupancy), exits (remove_agents -> reset_slot), vacated cells
     const size_t sb = static_cast<size_t>(r) * P.Npad;
     int4 ex = make_int4(0, -1, -1, -1);
-#pragma unroll
-    for (int q = 0; q < kCI; ++q)
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-            if (!((accm >> (3 * q + l)) & 1u)) continue;
-            const int i = o[l][q];
-            ABMX_ASSERT(i >= 0 && i < P.C && (X[l][q] == kExit || (X[l][q] >= 0 && X[l][q] < 3 * P.Lp)));
-            if (X[l][q] == kExit) {  // reset_slot (agent_set.cpp:45-58)
-                P.active[sb + i] = 0;
-                P.ids[sb + i] = 0;
-                P.ages[sb + i] = 0;
-                P.pos[sb + i] = 0;
-                if (ex.x == 0)
-                    ex.y = i;
-                else if (ex.x == 1)
-                    ex.z = i;
-                else
-                    ex.w = i;
-                ++ex.x;
-            } else {
-                P.pos[sb + i] = X[l][q];
-                P.occ[cb + X[l][q]] = i;
-            }
-            if (!((into >> (3 * q + l)) & 1u)) P.occ[cb + l * P.Lp + c_lo + q] = -1;
+#pragma unroll 1
+    for (unsigned mm = accm; mm; mm &= mm - 1) {
+        const int k = __ffs(static_cast<int>(mm)) - 1, q = k / 3, l = k - 3 * q;
+        const int i = pick12(o, k), x = pick12(X, k);
+        ABMX_ASSERT(i >= 0 && i < P.C && (x == kExit || (x >= 0 && x < 3 * P.Lp)));
+        if (x == kExit) {  // reset_slot (agent_set.cpp:45-58)
+            P.active[sb + i] = 0;
+            P.ids[sb + i] = 0;
+            P.ages[sb + i] = 0;
+            P.pos[sb + i] = 0;
+            if (ex.x == 0)
+                ex.y = i;
+            else if (ex.x == 1)
+                ex.z = i;
+            else
+                ex.w = i;
+            ++ex.x;
+        } else {
+            P.pos[sb + i] = x;
+            P.occ[cb + x] = i;
         }
+        if (!((into >> k) & 1u)) P.occ[cb + l * P.Lp + c_lo + q] = -1;
+    }
     // the exit column's thread publishes the step's exits (read by this step's spawn)
     if (c_lo <= P.L - 1 && P.L - 1 < c_lo + kCI) P.exits[static_cast<size_t>(r) * 2 + (P.epoch & 1)] = ex;
+    TRF_STAMP(5);
 }
 
 // ---------------------------------------------------------------- k_spawn
@@ -1110,6 +1170,15 @@ struct abmx_traffic {
         return ABMX_OK;
     }
 };
+
+#ifdef ABMX_TRF_TRACE
+extern "C" int abmx_trf_warp_trace(unsigned long long* out) {
+    return cudaMemcpyFromSymbol(out, abmx_trf::g_trf_warp, sizeof(unsigned long long) * 32 * 4) == cudaSuccess ? 0 : -1;
+}
+extern "C" int abmx_trf_trace(unsigned long long* out, int ctas) {
+    return cudaMemcpyFromSymbol(out, abmx_trf::g_trf_trace, sizeof(unsigned long long) * 8 * ctas) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 namespace {
 const char* kTrafficKernels[kNumKernels] = {"k_accept", "k_spawn"};
