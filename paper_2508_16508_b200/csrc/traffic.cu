@@ -50,10 +50,17 @@ constexpr int kCI = 4;  // columns per thread in k_accept: one int4 of occupants
 #define ABMX_TRF_NA_MAX 1024
 #endif
 constexpr int kAcceptMaxNT = ABMX_TRF_NA_MAX;  // k_accept CTA size for long roads
+#ifndef ABMX_TRF_POLL_NS
+#define ABMX_TRF_POLL_NS 0
+#endif
 constexpr unsigned kSlotMask = (1u << 28) - 1;
 constexpr unsigned long long kFlagAgg = 1ULL << 62;
 constexpr unsigned long long kFlagPre = 2ULL << 62;
-constexpr int kNumKernels = 2;  // k_accept (with the apply), k_spawn
+constexpr int kNumKernels = 2;
+// A tile's lookback word sits alone in a 128-byte line: packed, the ~90 words of C4's road were
+// 6 lines, and the first poll of every tile (32 lanes x 86 tiles at once) queued ~2.5 us at
+// their L2 slices (traced: one poll load, ~2.7 us walk).
+constexpr int kStatusStride = 16;  // k_accept (with the apply), k_spawn
 
 enum : int { kStay = -1, kExit = -2 };
 
@@ -74,7 +81,7 @@ struct TParams {
     long long* ids;
     long long* ages;
     int* occ;
-    unsigned long long* cstatus;  // [R][ctiles] lookback words
+    unsigned long long* cstatus;  // [R][ctiles][kStatusStride] lookback words, one per 128-byte line
     unsigned* ticket;             // [2]
     int spawn_pending;            // 1: k_accept's column-0 tile first runs the PREVIOUS step's
     long long spawn_t;            //    spawn (step spawn_t, metrics row spawn_row), which a
@@ -106,14 +113,14 @@ __device__ __forceinline__ int proposal(const TParams& P, int slot, int p, bool 
     const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
     return tl * P.Lp + cell + 1;
 }
-// the same with the lane and cell known (no division)
-__device__ __forceinline__ int proposal_lc(const TParams& P, int slot, int lane, int cell, bool green,
-                                          unsigned long long key) {
+// the TARGET LANE of car `slot` at (lane, cell), or kStay / kExit: the target cell is always
+// (lane', cell + 1), so k_accept keeps lanes and never divides by the lane stride
+__device__ __forceinline__ int proposal_lane(const TParams& P, int slot, int lane, int cell, bool green,
+                                            unsigned long long key) {
     if (cell == P.L - 1) return green ? kExit : kStay;
     const int n = 1 + (lane > 0) + (lane < 2);
     const int pick = static_cast<int>(uniform_span(key, static_cast<unsigned long long>(slot), static_cast<unsigned long long>(n)));
-    const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
-    return tl * P.Lp + cell + 1;
+    return pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
 }
 // a[k % 3][k / 3] for a runtime k < 12, by selects (a per-thread array indexed at run time would
 // live in local memory)
@@ -169,7 +176,8 @@ __device__ void spawn_road(const TParams& P, int r, long long t, unsigned row, u
 
 #ifdef ABMX_TRF_TRACE  // per-CTA %globaltimer stamps of k_accept (thread 0): start, occupants
                        // used, targets used, block scan, lookback, end
-__device__ unsigned long long g_trf_trace[4096][8];
+__device__ unsigned long long g_trf_trace[4096][10];
+__device__ unsigned g_trf_polls[4096][2];  // lane 0's poll loads and walk rounds
 __device__ unsigned long long g_trf_warp[32][4];  // the last tile: per warp, lane 0: occupants, targets, maps
 #define TRF_WSTAMP(k)                                                                   \
     if ((threadIdx.x & 31) == 0 && blockIdx.x == gridDim.x - 1) {                      \
@@ -234,12 +242,12 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     // thread holds in all three lanes, so the conflict winner (same lane > from the left > from
     // the right, traffic.cpp:95-124) is decided here without bid words; then the targets'
     // occupants, one batched round of independent loads
-    int X[3][kCI];
+    int X[3][kCI];  // target lane (the target cell is (X, c + 1)), kStay or kExit
 #pragma unroll
     for (int l = 0; l < 3; ++l)
 #pragma unroll
         for (int q = 0; q < kCI; ++q)
-            X[l][q] = o[l][q] >= 0 ? proposal_lc(P, o[l][q], l, c_lo + q, green, key) : kStay;
+            X[l][q] = o[l][q] >= 0 ? proposal_lane(P, o[l][q], l, c_lo + q, green, key) : kStay;
     TRF_STAMP(1);
     TRF_WSTAMP(0);
     int ox[3][kCI];  // occupant of the target if this car won it, else kStay - 1 (lost / no move)
@@ -249,13 +257,13 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         for (int l = 0; l < 3; ++l) {
             bool won = X[l][q] >= 0;
             if (won) {
-                const int tl = X[l][q] / P.Lp;
+                const int tl = X[l][q];
                 const int pr = l == tl ? 0 : (l == tl - 1 ? 1 : 2);
 #pragma unroll
                 for (int l2 = 0; l2 < 3; ++l2)
                     if (l2 != l && X[l2][q] == X[l][q] && (l2 == tl ? 0 : (l2 == tl - 1 ? 1 : 2)) < pr) won = false;
             }
-            ox[l][q] = won ? P.occ[cb + X[l][q]] : kStay - 1;
+            ox[l][q] = won ? P.occ[cb + X[l][q] * P.Lp + c_lo + q + 1] : kStay - 1;
         }
     // the halo: occupants of column c_lo - 1, read now, before any thread or tile of this step
     // writes occupancy (lane + 1's column c_lo + 3 of its int4; across warps and tiles a load)
@@ -272,7 +280,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     for (int q = 1; q < kCI; ++q)
 #pragma unroll
         for (int l = 0; l < 3; ++l)
-            if (ox[l][q - 1] != kStay - 1) into |= 1u << (3 * q + X[l][q - 1] / P.Lp);
+            if (ox[l][q - 1] != kStay - 1) into |= 1u << (3 * q + X[l][q - 1]);
     unsigned F[kCI];
     unsigned occm = 0;
     TRF_STAMP(2);
@@ -293,7 +301,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
                     if (X[l][q] == kExit)
                         m = 1;
                     else if (ox[l][q] != kStay - 1)
-                        m = ox[l][q] < 0 ? 1u : 2u + static_cast<unsigned>(X[l][q] / P.Lp);
+                        m = ox[l][q] < 0 ? 1u : 2u + static_cast<unsigned>(X[l][q]);
                 }
                 f |= m << (3 * l);
             }
@@ -330,22 +338,35 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     TRF_STAMP(3);
     if (warp == 0) {  // decoupled lookback, 32 predecessors per round
         const unsigned A = s_warp[NA / 32 - 1];  // tile aggregate
-        unsigned long long* st = P.cstatus + static_cast<size_t>(r) * P.ctiles;
+        unsigned long long* st = P.cstatus + static_cast<size_t>(r) * P.ctiles * kStatusStride;
         const unsigned long long tag = (P.epoch & 0x3FFFFFFFULL) << 32;
         unsigned vin = 0;
         if (tau > 0) {
-            if (lane == 0) st_word(&st[tau], kFlagAgg | tag | A);
+            if (lane == 0) st_word(&st[tau * kStatusStride], kFlagAgg | tag | A);
             unsigned accf = kIdentityFn;  // composition of the aggregates passed so far
+#ifdef ABMX_TRF_TRACE
+            unsigned n_polls = 0, n_rounds = 0;
+#endif
             for (int base = tau - 1;; base -= 32) {
+#ifdef ABMX_TRF_TRACE
+                ++n_rounds;
+#endif
                 const int j = base - lane;  // lane 0 = nearest predecessor
                 unsigned long long w = 0;
                 unsigned fl = j >= 0 ? 0u : 2u;  // beyond the road's first tile: never reached
-                do {  // all lanes stay in the loop until every predecessor has published
+                for (;;) {  // all lanes stay in the loop until every predecessor has published
                     if (fl == 0) {
-                        w = ld_word(&st[j]);
+#ifdef ABMX_TRF_TRACE
+                        ++n_polls;
+#endif
+                        w = ld_word(&st[j * kStatusStride]);
                         fl = ((w & (0x3FFFFFFFULL << 32)) == tag) ? static_cast<unsigned>(w >> 62) : 0u;
                     }
-                } while (__any_sync(0xffffffffu, fl == 0));
+                    if (!__any_sync(0xffffffffu, fl == 0)) break;
+#if ABMX_TRF_POLL_NS > 0
+                    __nanosleep(ABMX_TRF_POLL_NS);  // back off: every tile's warp polls the same few lines
+#endif
+                }
                 // every lane now holds an aggregate (1) or a prefix (2); the lanes BEFORE the
                 // first prefix contribute their aggregates, the first prefix ends the walk
                 const unsigned pre = __ballot_sync(0xffffffffu, fl == 2);
@@ -364,11 +385,19 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
                     break;
                 }
             }
+#ifdef ABMX_TRF_TRACE
+            if (lane == 0 && blockIdx.x < 4096) {
+                g_trf_polls[blockIdx.x][0] = n_polls;
+                g_trf_polls[blockIdx.x][1] = n_rounds;
+            }
+#endif
         }
+        TRF_STAMP(8);
         if (lane == 0) {
-            st_word(&st[tau], kFlagPre | tag | apply_fn(A, vin));
+            st_word(&st[tau * kStatusStride], kFlagPre | tag | apply_fn(A, vin));
             s_vin = vin;
         }
+        TRF_STAMP(9);
     }
     __syncthreads();  // every thread's occupancy loads are done: the writes below may start
     TRF_STAMP(4);
@@ -391,7 +420,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
 #pragma unroll 1
         for (int l = 0; l < 3; ++l) {
             const int ohl = l == 0 ? oh[0] : (l == 1 ? oh[1] : oh[2]);
-            const int x = ohl >= 0 ? proposal_lc(P, ohl, l, c_lo - 1, green, key) : kStay;
+            const int x = ohl >= 0 ? proposal_lane(P, ohl, l, c_lo - 1, green, key) : kStay;
             if (l == 0)
                 xh0 = x;
             else if (l == 1)
@@ -403,7 +432,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
 #pragma unroll
         for (int l = 0; l < 3; ++l) {
             if (xh[l] < 0) continue;
-            const int tl = xh[l] / P.Lp;
+            const int tl = xh[l];
             const int pr = l == tl ? 0 : (l == tl - 1 ? 1 : 2);
             bool won = true;
 #pragma unroll
@@ -419,9 +448,9 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
 #pragma unroll 1
     for (unsigned mm = accm; mm; mm &= mm - 1) {
         const int k = __ffs(static_cast<int>(mm)) - 1, q = k / 3, l = k - 3 * q;
-        const int i = pick12(o, k), x = pick12(X, k);
-        ABMX_ASSERT(i >= 0 && i < P.C && (x == kExit || (x >= 0 && x < 3 * P.Lp)));
-        if (x == kExit) {  // reset_slot (agent_set.cpp:45-58)
+        const int i = pick12(o, k), tl = pick12(X, k);
+        ABMX_ASSERT(i >= 0 && i < P.C && (tl == kExit || (tl >= 0 && tl < 3)));
+        if (tl == kExit) {  // reset_slot (agent_set.cpp:45-58)
             P.active[sb + i] = 0;
             P.ids[sb + i] = 0;
             P.ages[sb + i] = 0;
@@ -434,6 +463,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
                 ex.w = i;
             ++ex.x;
         } else {
+            const int x = tl * P.Lp + c_lo + q + 1;
             P.pos[sb + i] = x;
             P.occ[cb + x] = i;
         }
@@ -831,7 +861,7 @@ struct abmx_traffic {
         ALT(P.ids, ns * 8);
         ALT(P.ages, ns * 8);
         ALT(P.occ, nc * 4);
-        ALT(P.cstatus, static_cast<size_t>(R) * P.ctiles * 8);
+        ALT(P.cstatus, static_cast<size_t>(R) * P.ctiles * 8 * kStatusStride);
         ALT(P.ticket, 16);
         ALT(P.fbits, static_cast<size_t>(R) * P.Wb * 4);
         ALT(P.fsum, static_cast<size_t>(R) * P.Ws * 4);
@@ -854,7 +884,7 @@ struct abmx_traffic {
         }
         CKT(cudaMemcpy(phase, ph.data(), ph.size() * 8, cudaMemcpyHostToDevice));
         CKT(cudaMemcpy(sd, seeds, static_cast<size_t>(R) * 8, cudaMemcpyHostToDevice));
-        CKT(cudaMemset(P.cstatus, 0, static_cast<size_t>(R) * P.ctiles * 8));
+        CKT(cudaMemset(P.cstatus, 0, static_cast<size_t>(R) * P.ctiles * 8 * kStatusStride));
         CKT(cudaMemset(P.ticket, 0, 16));
         CKT(cudaMemset(P.cnt, 0, static_cast<size_t>(R) * 64));
         CKT(cudaMemset(d_metrics_step, 0, static_cast<size_t>(R) * 32));
@@ -1172,11 +1202,14 @@ struct abmx_traffic {
 };
 
 #ifdef ABMX_TRF_TRACE
+extern "C" int abmx_trf_polls(unsigned* out, int ctas) {
+    return cudaMemcpyFromSymbol(out, abmx_trf::g_trf_polls, sizeof(unsigned) * 2 * ctas) == cudaSuccess ? 0 : -1;
+}
 extern "C" int abmx_trf_warp_trace(unsigned long long* out) {
     return cudaMemcpyFromSymbol(out, abmx_trf::g_trf_warp, sizeof(unsigned long long) * 32 * 4) == cudaSuccess ? 0 : -1;
 }
 extern "C" int abmx_trf_trace(unsigned long long* out, int ctas) {
-    return cudaMemcpyFromSymbol(out, abmx_trf::g_trf_trace, sizeof(unsigned long long) * 8 * ctas) == cudaSuccess ? 0 : -1;
+    return cudaMemcpyFromSymbol(out, abmx_trf::g_trf_trace, sizeof(unsigned long long) * 10 * ctas) == cudaSuccess ? 0 : -1;
 }
 #endif
 

@@ -29,18 +29,21 @@ def trace(flushed):
         trace.t += 1
         m.collect_metrics()
     G = 86
-    buf = np.zeros((G, 8), np.uint64)
+    buf = np.zeros((G, 10), np.uint64)
     abmx.lib.abmx_trf_trace.restype = C.c_int
     assert abmx.lib.abmx_trf_trace(buf.ctypes.data_as(C.POINTER(C.c_uint64)), G) == 0
     tr = (buf.astype(np.int64) - int(buf[:, 0].min())) / 1e3
     print(f"k_accept<1024>, {G} tiles, last of 3 per-call steps, L2 {'flushed' if flushed else 'warm'} "
           "(us from the first CTA start)")
-    for k, lab in enumerate(["start", "occupants", "targets", "scan", "lookback", "end", "maps", "warp scan"]):
+    for k, lab in enumerate(["start", "occupants", "targets", "scan", "lookback", "end", "maps", "warp scan", "walk done", "prefix out"]):
         v = tr[:, k]
         print(f"  {lab:9s} p0 {v.min():6.2f}  p50 {np.median(v):6.2f}  p90 {np.percentile(v, 90):6.2f}  max {v.max():6.2f}")
     print("  lookback done by tile (0 = road end):", " ".join(f"{x:.1f}" for x in tr[::8, 4]))
     slow = int(np.argmax(tr[:, 5]))
     print(f"  slowest tile {slow}:", " ".join(f"{x:.2f}" for x in tr[slow]))
+    pl = np.zeros((G, 2), np.uint32)
+    assert abmx.lib.abmx_trf_polls(pl.ctypes.data_as(C.POINTER(C.c_uint32)), G) == 0
+    print("  lane-0 poll loads / walk rounds by tile (every 8th):", " ".join(f"{a}/{b}" for a, b in pl[::8]))
     wb = np.zeros((32, 4), np.uint64)
     assert abmx.lib.abmx_trf_warp_trace(wb.ctypes.data_as(C.POINTER(C.c_uint64))) == 0
     wt = (wb[:, :3].astype(np.int64) - int(buf[:, 0].min())) / 1e3
