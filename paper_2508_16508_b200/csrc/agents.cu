@@ -387,6 +387,9 @@ __device__ unsigned long long g_life_trace[4096][8];
 #define LIFE_STAMP(k)
 #endif
 
+#ifndef ABMX_BAR_NS
+#define ABMX_BAR_NS 100
+#endif
 constexpr int kCoopMaxTiles = 2048;  // slot + row tiles of one k_life_coop grid (shared prefix array)
 
 struct LifeWs {
@@ -400,6 +403,9 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned G) {
     if (threadIdx.x == 0) {
         red_release_add(ctr, 1u);
         while (ld_acquire_u32(ctr) < G) {
+#if ABMX_BAR_NS > 0
+            __nanosleep(ABMX_BAR_NS);  // back off: every CTA's thread 0 polls this one line
+#endif
         }
     }
     __syncthreads();
@@ -500,12 +506,16 @@ __global__ void __launch_bounds__(kT) k_life_coop(const uint8_t* __restrict__ ki
     // ---- resolve: exclusive prefixes over all tiles (slot tiles first: the lo field of a row
     // tile's prefix is F + its valid prefix; F + Q < 2^31 since the grid is co-resident)
     {
+        // the totals come in lane-contiguous (coalesced) loads, staged in s_pref: every CTA reads
+        // the same few lines, so each load instruction should touch as few of them as possible
         constexpr int kPer = (kCoopMaxTiles + kT - 1) / kT;
+        for (unsigned q = tid; q < G; q += kT) s_pref[q] = ws->tot[q];
+        __syncthreads();
         unsigned long long v[kPer], sum = 0;
 #pragma unroll
         for (int e = 0; e < kPer; ++e) {
             const unsigned q = static_cast<unsigned>(tid) * kPer + e;
-            v[e] = q < G ? ws->tot[q] : 0ULL;
+            v[e] = q < G ? s_pref[q] : 0ULL;
             sum += v[e];
         }
         unsigned long long all;

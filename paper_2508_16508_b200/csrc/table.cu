@@ -137,6 +137,10 @@ __device__ __forceinline__ unsigned long long gtime() {
 #define SCAN_STAMP(k)
 #endif
 
+#ifndef ABMX_SCAN_BAR_NS
+#define ABMX_SCAN_BAR_NS 0
+#endif
+
 // Workspace of one call (zeroed: the chunk totals and the three counters; the per-tile arrays
 // are fully written before they are read).
 struct ScanWs {
@@ -260,6 +264,9 @@ __global__ void __launch_bounds__(kPT, kCompact ? kCMinB : kPMinB) scan_pipe_ker
             // one counter of published chunks (release); only this thread polls it (acquire)
             red_release_add(&ws->published, 1u);
             while (ld_acquire_u32(&ws->published) < static_cast<unsigned>(G)) {
+#if ABMX_SCAN_BAR_NS > 0
+                __nanosleep(ABMX_SCAN_BAR_NS);  // back off: every CTA's thread 0 polls this one line
+#endif
             }
         }
         __syncthreads();  // thread 0's acquire + the barrier: every chunk word is visible
