@@ -440,7 +440,9 @@ def agents_section(args, rank):
         cycle(s, arr, k)
         ev[k][1].record()
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev) / K
+    import statistics
+    cyc = [a.elapsed_time(b) for a, b in ev]
+    ms, ms_mean = statistics.median(cyc), sum(cyc) / K
     w2, warr2, wkeep2 = make()
     for k in range(3):  # warm-up of the two-call path too (its own scratch sizes, first launches)
         cycle_two_calls(w2, warr2, K + k)
@@ -453,15 +455,18 @@ def agents_section(args, rank):
         cycle_two_calls(s2, arr2, k)
         ev2[k][1].record()
     torch.cuda.synchronize()
-    ms_two = sum(a.elapsed_time(b) for a, b in ev2) / K
+    cyc2 = [a.elapsed_time(b) for a, b in ev2]
+    ms_two, ms_two_mean = statistics.median(cyc2), sum(cyc2) / K
     same = all(np.array_equal(a, b) for a, b in zip(s.to_numpy().values(), s2.to_numpy().values()))
     out_d = {"workload": f"lifecycle cycles on a {cap}-slot set (e:i64, w:f64, f:u8; 70% live): "
                          f"remove_agents of {AGENT_CHURN} random slots + spawn_agents of {cap} rows with "
                          f"{AGENT_CHURN} valid, copy apply (fused: abmx_agents_lifecycle); {K} cycles, "
                          f"L2 flushed before each",
-             "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms,
+             "value": cap / (ms / 1e3), "unit": "slot-cycles/s", "ms_per_cycle": ms, "ms_per_cycle_mean": ms_mean,
+             "timing": "event-timed per cycle on the set's stream, median of the cycles (a cycle's events also "
+                       "see any host submission delay, ~14 us of API calls per cycle; the mean is beside it)",
              "launches_per_cycle": "1 memset + 1 cooperative kernel (abmx_agents_lifecycle, k_life_coop)",
-             "two_call_ms_per_cycle": ms_two,
+             "two_call_ms_per_cycle": ms_two, "two_call_ms_per_cycle_mean": ms_two_mean,
              "two_call_launches_per_cycle": "2 x (1 memset + 1 cooperative kernel): abmx_agents_remove and "
                                             "abmx_agents_spawn, each one k_life_coop",
              "fused_equals_two_calls": bool(same)}
