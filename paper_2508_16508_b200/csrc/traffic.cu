@@ -250,6 +250,15 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
             X[l][q] = o[l][q] >= 0 ? proposal_lane(P, o[l][q], l, c_lo + q, green, key) : kStay;
     TRF_STAMP(1);
     TRF_WSTAMP(0);
+    // occupants of column c_lo + 4 (every target of column c_lo + 3): the previous thread's first
+    // column (a shuffle; across warps and tiles a load), so no target occupant needs a dependent
+    // load: the targets of columns c_lo .. c_lo + 2 are this thread's own occupants
+    int nx[3];
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        nx[l] = __shfl_up_sync(0xffffffffu, o[l][0], 1);
+        if ((threadIdx.x & 31) == 0) nx[l] = c_lo >= 0 && c_lo + kCI < P.Lp ? P.occ[cb + l * P.Lp + c_lo + kCI] : -1;
+    }
     int ox[3][kCI];  // occupant of the target if this car won it, else kStay - 1 (lost / no move)
 #pragma unroll
     for (int q = 0; q < kCI; ++q)
@@ -263,7 +272,13 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
                 for (int l2 = 0; l2 < 3; ++l2)
                     if (l2 != l && X[l2][q] == X[l][q] && (l2 == tl ? 0 : (l2 == tl - 1 ? 1 : 2)) < pr) won = false;
             }
-            ox[l][q] = won ? P.occ[cb + X[l][q] * P.Lp + c_lo + q + 1] : kStay - 1;
+            if (won) {
+                const int tl = X[l][q];
+                ox[l][q] = q + 1 < kCI ? (tl == 0 ? o[0][q + 1 < kCI ? q + 1 : 0] : (tl == 1 ? o[1][q + 1 < kCI ? q + 1 : 0] : o[2][q + 1 < kCI ? q + 1 : 0]))
+                                       : (tl == 0 ? nx[0] : (tl == 1 ? nx[1] : nx[2]));
+            } else {
+                ox[l][q] = kStay - 1;
+            }
         }
     // the halo: occupants of column c_lo - 1, read now, before any thread or tile of this step
     // writes occupancy (lane + 1's column c_lo + 3 of its int4; across warps and tiles a load)
