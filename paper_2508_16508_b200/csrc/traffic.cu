@@ -104,17 +104,9 @@ __device__ __forceinline__ bool green_of(const TParams& P, int r) { return green
 __device__ __forceinline__ unsigned long long propose_key(const TParams& P, int r) {
     return split(split(P.seeds[r], 6), static_cast<unsigned long long>(P.t));  // TrafficPropose
 }
-// target cell index of car `slot` at cell index p, or kStay / kExit (traffic.cpp:57-79)
-__device__ __forceinline__ int proposal(const TParams& P, int slot, int p, bool green, unsigned long long key) {
-    const int lane = p / P.Lp, cell = p - lane * P.Lp;
-    if (cell == P.L - 1) return green ? kExit : kStay;
-    const int n = 1 + (lane > 0) + (lane < 2);
-    const int pick = static_cast<int>(uniform_span(key, static_cast<unsigned long long>(slot), static_cast<unsigned long long>(n)));
-    const int tl = pick == 0 ? lane : (pick == 1 ? (lane > 0 ? lane - 1 : lane + 1) : lane + 1);
-    return tl * P.Lp + cell + 1;
-}
-// the TARGET LANE of car `slot` at (lane, cell), or kStay / kExit: the target cell is always
-// (lane', cell + 1), so k_accept keeps lanes and never divides by the lane stride
+// the TARGET LANE of car `slot` at (lane, cell), or kStay / kExit (traffic.cpp:57-79): the
+// target cell is always (lane', cell + 1), so k_accept keeps lanes and never divides by the
+// lane stride
 __device__ __forceinline__ int proposal_lane(const TParams& P, int slot, int lane, int cell, bool green,
                                             unsigned long long key) {
     if (cell == P.L - 1) return green ? kExit : kStay;
@@ -129,10 +121,6 @@ __device__ __forceinline__ int pick12(const int (&a)[3][4], int k) {
 #pragma unroll
     for (int kk = 1; kk < 12; ++kk) v = k == kk ? a[kk % 3][kk / 3] : v;
     return v;
-}
-// tag of an accepted entry into a cell this epoch (never 0, the initial word)
-__device__ __forceinline__ unsigned inc_tag(unsigned long long epoch) {
-    return 0x80000000u | static_cast<unsigned>(epoch & 0x7FFFFFFFULL);
 }
 __device__ __forceinline__ unsigned long long bid_word(unsigned long long epoch, int prio, int slot) {
     return (epoch << 32) | (0xFFFFFFFFu - ((static_cast<unsigned>(prio) << 28) | static_cast<unsigned>(slot)));
