@@ -214,13 +214,27 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     const bool green = s_green != 0;
     const unsigned long long key = s_key;
     const size_t cb = static_cast<size_t>(r) * P.Cpad;
-    const int c_lo = hi - (static_cast<int>(threadIdx.x) + 1) * kCI;  // multiple of 4
-    // occupants of this thread's 4 columns x 3 lanes (column c_lo + q)
+    // columns per thread: kCI, except in a road-entry tile (the partial last one) whose span fits
+    // 2 or 1 column per thread. Cars enter at column 0, so early in a run every car of a long
+    // road sits in that tile's first few warps: thinner columns spread their proposals over
+    // 2-4x the threads (the traced critical path of C4). Columns c_lo + q, q >= cpt,
+    // belong to the previous thread: empty here, identity maps.
+    const int cpt = tau == P.ctiles - 1 && hi <= NA * 2 ? (hi <= NA ? 1 : 2) : kCI;
+    const int c_lo = hi - (static_cast<int>(threadIdx.x) + 1) * cpt;  // multiple of cpt
+    // occupants of this thread's columns x 3 lanes (column c_lo + q)
     int o[3][kCI];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
         int4 v4 = make_int4(-1, -1, -1, -1);
-        if (c_lo >= 0) v4 = *reinterpret_cast<const int4*>(&P.occ[cb + l * P.Lp + c_lo]);
+        if (c_lo >= 0) {
+            const int* p = &P.occ[cb + l * P.Lp + c_lo];
+            if (cpt == kCI) {
+                v4 = *reinterpret_cast<const int4*>(p);
+            } else {
+                v4.x = p[0];
+                if (cpt > 1) v4.y = p[1];
+            }
+        }
         o[l][0] = v4.x;
         o[l][1] = v4.y;
         o[l][2] = v4.z;
@@ -238,14 +252,14 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
             X[l][q] = o[l][q] >= 0 ? proposal_lane(P, o[l][q], l, c_lo + q, green, key) : kStay;
     TRF_STAMP(1);
     TRF_WSTAMP(0);
-    // occupants of column c_lo + 4 (every target of column c_lo + 3): the previous thread's first
-    // column (a shuffle; across warps and tiles a load), so no target occupant needs a dependent
-    // load: the targets of columns c_lo .. c_lo + 2 are this thread's own occupants
+    // occupants of column c_lo + cpt (every target of this thread's last column): the previous
+    // thread's first column (a shuffle; across warps and tiles a load), so no target occupant
+    // needs a dependent load: the other targets are this thread's own occupants
     int nx[3];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
         nx[l] = __shfl_up_sync(0xffffffffu, o[l][0], 1);
-        if ((threadIdx.x & 31) == 0) nx[l] = c_lo >= 0 && c_lo + kCI < P.Lp ? P.occ[cb + l * P.Lp + c_lo + kCI] : -1;
+        if ((threadIdx.x & 31) == 0) nx[l] = c_lo >= 0 && c_lo + cpt < P.Lp ? P.occ[cb + l * P.Lp + c_lo + cpt] : -1;
     }
     int ox[3][kCI];  // occupant of the target if this car won it, else kStay - 1 (lost / no move)
 #pragma unroll
@@ -262,7 +276,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
             }
             if (won) {
                 const int tl = X[l][q];
-                ox[l][q] = q + 1 < kCI ? (tl == 0 ? o[0][q + 1 < kCI ? q + 1 : 0] : (tl == 1 ? o[1][q + 1 < kCI ? q + 1 : 0] : o[2][q + 1 < kCI ? q + 1 : 0]))
+                ox[l][q] = q + 1 < cpt ? (tl == 0 ? o[0][q + 1 < kCI ? q + 1 : 0] : (tl == 1 ? o[1][q + 1 < kCI ? q + 1 : 0] : o[2][q + 1 < kCI ? q + 1 : 0]))
                                        : (tl == 0 ? nx[0] : (tl == 1 ? nx[1] : nx[2]));
             } else {
                 ox[l][q] = kStay - 1;
@@ -273,7 +287,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     int oh[3];
 #pragma unroll
     for (int l = 0; l < 3; ++l) {
-        oh[l] = __shfl_down_sync(0xffffffffu, o[l][kCI - 1], 1);
+        oh[l] = __shfl_down_sync(0xffffffffu, cpt == kCI ? o[l][kCI - 1] : (cpt == 2 ? o[l][1] : o[l][0]), 1);
         if ((threadIdx.x & 31) == 31) oh[l] = c_lo > 0 ? P.occ[cb + l * P.Lp + c_lo - 1] : -1;
     }
     // bit 3q + l of into (q >= 1; q = 0 after the scan, from the halo): a car of column
@@ -293,7 +307,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
     for (int j = 0; j < kCI; ++j) {  // j = 0 is the rightmost column of this thread
         const int q = kCI - 1 - j;
         unsigned f = kIdentityFn;
-        if (c_lo + q >= 0) {
+        if (c_lo + q >= 0 && q < cpt) {
             f = 0;
 #pragma unroll
             for (int l = 0; l < 3; ++l) {
@@ -473,7 +487,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         if (!((into >> k) & 1u)) P.occ[cb + l * P.Lp + c_lo + q] = -1;
     }
     // the exit column's thread publishes the step's exits (read by this step's spawn)
-    if (c_lo <= P.L - 1 && P.L - 1 < c_lo + kCI) P.exits[static_cast<size_t>(r) * 2 + (P.epoch & 1)] = ex;
+    if (c_lo <= P.L - 1 && P.L - 1 < c_lo + cpt) P.exits[static_cast<size_t>(r) * 2 + (P.epoch & 1)] = ex;
     TRF_STAMP(5);
 }
 
