@@ -326,6 +326,13 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
         F[j] = f;
         T = compose(f, T);
     }
+    // the proposals, packed for the apply (3 bits per (l, q): target lane + 2, kStay + 2, kExit
+    // + 2): the unpacked array would stay live across the scan and lookback (register pressure)
+    unsigned long long xp = 0;
+#pragma unroll
+    for (int q = 0; q < kCI; ++q)
+#pragma unroll
+        for (int l = 0; l < 3; ++l) xp |= static_cast<unsigned long long>(X[l][q] + 2) << (3 * (3 * q + l));
     TRF_STAMP(6);
     TRF_WSTAMP(2);
     // block scan over threads (thread 0 = rightmost): I_t = T_t ∘ I_{t-1}
@@ -465,7 +472,7 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
 #pragma unroll 1
     for (unsigned mm = accm; mm; mm &= mm - 1) {
         const int k = __ffs(static_cast<int>(mm)) - 1, q = k / 3, l = k - 3 * q;
-        const int i = pick12(o, k), tl = pick12(X, k);
+        const int i = pick12(o, k), tl = static_cast<int>((xp >> (3 * k)) & 7u) - 2;
         ABMX_ASSERT(i >= 0 && i < P.C && (tl == kExit || (tl >= 0 && tl < 3)));
         if (tl == kExit) {  // reset_slot (agent_set.cpp:45-58)
             P.active[sb + i] = 0;
