@@ -386,13 +386,18 @@ __global__ void __launch_bounds__(NA) k_accept(TParams P) {
                         w = ld_word(&st[j * kStatusStride]);
                         fl = ((w & (0x3FFFFFFFULL << 32)) == tag) ? static_cast<unsigned>(w >> 62) : 0u;
                     }
-                    if (!__any_sync(0xffffffffu, fl == 0)) break;
+                    // done once every lane up to the nearest published prefix has its word
+                    // (the lanes beyond it are not needed), or every lane has one
+                    const unsigned zero = __ballot_sync(0xffffffffu, fl == 0);
+                    const unsigned pre2 = __ballot_sync(0xffffffffu, fl == 2);
+                    if (!zero || (pre2 && !(zero & ((pre2 & (0u - pre2)) - 1u)))) break;
 #if ABMX_TRF_POLL_NS > 0
                     __nanosleep(ABMX_TRF_POLL_NS);  // back off: every tile's warp polls the same few lines
 #endif
                 }
-                // every lane now holds an aggregate (1) or a prefix (2); the lanes BEFORE the
-                // first prefix contribute their aggregates, the first prefix ends the walk
+                // every lane up to the first prefix holds an aggregate (1) or that prefix (2);
+                // the lanes BEFORE the first prefix contribute their aggregates, the first prefix
+                // ends the walk (lanes beyond it may still be unpublished: not read)
                 const unsigned pre = __ballot_sync(0xffffffffu, fl == 2);
                 const int first = pre ? __ffs(pre) - 1 : 32;
                 unsigned f = lane < first ? static_cast<unsigned>(w & 0x1FFu) : kIdentityFn;
