@@ -6,6 +6,8 @@
 //   memset+coop    both, as abmx_agents_lifecycle issues them
 //   coop_2bar      memset + cooperative kernel that only crosses two grid barriers
 //   plain_2bar     the same two barriers, plain launch (co-residency not guaranteed by the API)
+//   empty_smem33k  the empty kernel with 33 KB of static shared memory (a carveout change after the
+//                  flush kernel); smem33k_coop the same, memset + cooperative
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/launch_probe tools/launch_probe.cu
 #include <cuda_runtime.h>
 #include <algorithm>
@@ -13,6 +15,12 @@
 #include <vector>
 
 __global__ void k_empty() {}
+__global__ void k_empty_smem() {  // 33 KB of static shared memory, like k_life_coop
+    __shared__ unsigned long long buf[4100];
+    if (threadIdx.x == 1024) buf[threadIdx.x] = 1;  // never true: keeps the array
+    __syncthreads();
+    if (threadIdx.x == 1025) asm volatile("" ::"l"(buf[0]));
+}
 __global__ void k_flush(int* p, size_t n, int v) {
     for (size_t i = blockIdx.x * 256ull + threadIdx.x; i < n; i += 256ull * gridDim.x) p[i] = v;
 }
@@ -67,8 +75,9 @@ int main() {
         cfg.numAttrs = coop ? 1 : 0;
         cudaLaunchKernelEx(&cfg, k_2bar, ctr);
     };
-    const char* names[] = {"memset8", "empty", "empty_coop", "memset+coop", "coop_2bar", "plain_2bar"};
-    for (int t = 0; t < 6; ++t) {
+    const char* names[] = {"memset8", "empty", "empty_coop", "memset+coop", "coop_2bar", "plain_2bar", "empty_smem33k",
+                           "smem33k_coop"};
+    for (int t = 0; t < 8; ++t) {
         std::vector<float> v;
         for (int r = 0; r < 53; ++r) {
             k_flush<<<1184, 256, 0, st>>>(fl, fn, r);
@@ -80,6 +89,8 @@ int main() {
                 case 3: cudaMemsetAsync(ctr, 0, 8, st); launch(k_empty, true); break;
                 case 4: cudaMemsetAsync(ctr, 0, 8, st); launch2(true); break;
                 case 5: cudaMemsetAsync(ctr, 0, 8, st); launch2(false); break;
+                case 6: launch(k_empty_smem, false); break;
+                case 7: cudaMemsetAsync(ctr, 0, 8, st); launch(k_empty_smem, true); break;
             }
             cudaEventRecord(b, st);
             cudaEventSynchronize(b);
