@@ -283,7 +283,9 @@ int abmx_agents_lifecycle(const abmx_agent_set* s, const uint8_t* d_kill, int32_
                           int64_t* d_result, void* stream);
 /* set_agents_rm / set_agents_sci (kernels.cpp:116-153) with the copy apply: the k-th target
  * slot receives the k-th valid row, k < min(popcount(target), popcount(valid)). With a copy
- * apply RM and SCI coincide (kernels.hpp:96-99). d_result (nullable): {pairs, valid rows}. */
+ * apply RM and SCI coincide (kernels.hpp:96-99). d_result (nullable): {pairs, valid rows};
+ * d_slots / d_rows (nullable): pair k, k < pairs. One cooperative launch when the set's tiles
+ * fit on the GPU at once (lifecycle fields and counters untouched). */
 int abmx_agents_set_rm(const abmx_agent_set* s, const uint8_t* d_target, int32_t m,
                        const uint8_t* d_valid, const abmx_column* rows, int32_t* d_slots,
                        int32_t* d_rows, int64_t* d_result, void* stream);
