@@ -184,7 +184,12 @@ def test_long_road_vs_oracle(T, oracle, L, steps):
     assert_road(dev.road(), ref.export())
 
 
-@pytest.mark.parametrize("L,dens,seed", [(5000, 0.9, 1), (4097, 0.5, 2), (20000, 0.97, 3), (1, 1.0, 4)])
+@pytest.mark.parametrize("L,dens,seed", [(5000, 0.9, 1), (4097, 0.5, 2), (20000, 0.97, 3), (1, 1.0, 4),
+                                         # the road-entry tile's column spacing (k_accept): 1 column
+                                         # per thread (single tile / last tile span <= 1024 columns),
+                                         # 2 per thread (<= 2048), 4 (wider)
+                                         (30, 0.8, 5), (50, 0.8, 6), (4596, 0.85, 7), (5596, 0.85, 8),
+                                         (7096, 0.85, 9), (8193, 0.6, 10)])
 def test_dense_roads_vs_oracle(T, oracle, L, dens, seed):
     """Dense random roads: long blocking chains through the column scan and its tile lookback
     (4096 columns per tile)."""
